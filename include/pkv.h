@@ -1,0 +1,179 @@
+/*
+ * pkv.h -- C ABI of the B200-native ProphetKV selective-recompute prefill.
+ *
+ * The reference (`pikv`, /root/reference/pkg/src/pikv) is a pure-Python numpy
+ * package with no FFI of its own; this header is the boundary its Python API
+ * would bind (see INTEGRATION.md for the ctypes binding).  Every entry point
+ * names the reference function it replaces.  Conventions:
+ *
+ *   - plain C types only; all tensor pointers are caller-owned DEVICE memory
+ *     unless a field says "host"; no allocation inside (workspace is passed in,
+ *     sized by the *_workspace() queries);
+ *   - every call is stream-ordered on the given cudaStream_t (passed as void*),
+ *     never synchronises the host, and is reentrant across streams;
+ *   - return value is a status code (PKV_OK or one of the PKV_ERR_* below, which
+ *     map 1:1 onto pikv.errors classes); pkv_last_error() gives a thread-local
+ *     message.
+ *
+ * Device layouts (bf16 = IEEE bfloat16, little endian):
+ *   dkp  = 64 if head_dim <= 64 else 128 (head dims zero-padded)
+ *   Dp   = hidden_dim rounded up to 64,  Fp = ffn_dim rounded up to 128
+ *   NQKV = (n_heads + 2*n_kv_heads) * dkp
+ *   weights are transposed ("output-major", K contiguous):
+ *     wqkv [NQKV][Dp]  rows = q heads, k heads, v heads, each dkp rows
+ *     wo   [Dp][n_heads*dkp]
+ *     wgu  [2*Fp][Dp]  gate/up interleaved in blocks of 128 rows
+ *     wd   [Dp][Fp]
+ *     embed, lm_head [vocab][Dp];   norm gains fp32 [Dp]
+ *   chunk store (one buffer per chunk): bf16 [n_layers][t_c][n_kv_heads][dkp], keys UNROTATED
+ *   paged KV cache: bf16 K and V pools [n_layers][n_kv_heads][pool_tokens][dkp];
+ *     token t lives in slot page_table[t / 128] * 128 + t % 128
+ *   RoPE tables: float64 cos/sin [rope_len][head_dim/2], angle = pos * theta^(-2i/d)
+ */
+#ifndef PKV_H_
+#define PKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> pikv.errors (reference errors.py:4-41) */
+enum {
+  PKV_OK = 0,
+  PKV_ERR_SHAPE = 1,        /* ShapeError */
+  PKV_ERR_ARGUMENT = 2,     /* ArgumentError */
+  PKV_ERR_CONFIG = 3,       /* ConfigError */
+  PKV_ERR_INPUT = 4,        /* InputError */
+  PKV_ERR_STATE = 5,        /* StateError */
+  PKV_ERR_INCOMPATIBLE = 6, /* IncompatibleError */
+  PKV_ERR_NUMERICS = 7,     /* NumericsError */
+  PKV_ERR_CUDA = 100        /* EngineError (device failure) */
+};
+
+/* query-pass flags */
+enum {
+  PKV_QP_SCORES = 1,    /* capture per-layer context scores (score_prophet) */
+  PKV_QP_RENORM = 2,    /* renormalize_context_only=True */
+  PKV_QP_LOGITS = 4,    /* compute last-row logits (finalize_query) */
+  PKV_QP_APPEND_KV = 8, /* append query K/V to the cache pool at positions s.. */
+  PKV_QP_FROM_CHUNKS = 16 /* read context keys/values from the chunk store (naive cache) */
+};
+
+/* reference ModelConfig, model.py:24-63 */
+typedef struct pkv_config {
+  int32_t n_layers, n_heads, n_kv_heads, head_dim, hidden_dim, ffn_dim, vocab_size;
+  double rope_theta, norm_eps;
+} pkv_config;
+
+/* reference LayerWeights, model.py:66-76 (device layouts above) */
+typedef struct pkv_layer_weights {
+  const float* attn_norm;
+  const float* ffn_norm;
+  const void* wqkv;
+  const void* wo;
+  const void* wgu;
+  const void* wd;
+} pkv_layer_weights;
+
+/* reference ModelWeights, model.py:79-160 */
+typedef struct pkv_weights {
+  const void* embed;
+  const float* final_norm;
+  const void* lm_head;
+  const pkv_layer_weights* layers; /* host array [n_layers] */
+} pkv_weights;
+
+/* reference AssembledCache, chunkstore.py:65-96 (device state) */
+typedef struct pkv_cache {
+  void* k_pool;
+  void* v_pool;
+  int64_t pool_tokens;       /* slots per (layer, kv head); multiple of 128 */
+  const int32_t* page_table; /* [ceil(rope_len/128)] */
+  int32_t s;                 /* context length */
+  const int32_t* token_ids;  /* [s] */
+  const double* rope_cos;    /* [rope_len][head_dim/2] */
+  const double* rope_sin;
+  int32_t rope_len;          /* positions covered (>= s + query length) */
+  const uint8_t* recomputed; /* nullable [s]: 1 = entry repaired by Stage II (read from the pool
+                                even when a query pass reads the others from the chunk store) */
+} pkv_cache;
+
+/* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */
+typedef struct pkv_chunks {
+  const uint64_t* k_nr;      /* device [n_chunks] device pointers, bf16 [L][t_c][Hkv][dkp] */
+  const uint64_t* v;         /* device [n_chunks] */
+  const int32_t* chunk_len;  /* device [n_chunks] */
+  const int32_t* src_chunk;  /* device [s] chunk ordinal of each token */
+  const int32_t* src_local;  /* device [s] index inside its chunk */
+  int32_t n_chunks;
+} pkv_chunks;
+
+typedef struct pkv_model pkv_model; /* opaque: config + device weight views */
+
+/* padded layout: out[0..4] = dkp, Dp, Fp, NQKV, n_heads*dkp */
+int pkv_layout(const pkv_config* cfg, int32_t out[5]);
+
+/* validates the config like ModelConfig.__post_init__ (model.py:36-50) */
+int pkv_model_create(const pkv_config* cfg, const pkv_weights* w, pkv_model** out);
+void pkv_model_destroy(pkv_model* m);
+
+/* assemble(chunks, config) -- chunkstore.py:99-140 (+ rope_apply tensor.py:89-114):
+ * concatenates the chunk K/V into the paged cache, rotating keys at global
+ * positions 0..s-1 with the float64 tables. */
+int pkv_assemble(const pkv_config* cfg, const pkv_chunks* chunks, const pkv_cache* cache, void* stream);
+
+/* query_pass -- model.py:370-402; with PKV_QP_SCORES it is score_prophet
+ * (selection.py:64-86, per_layer [L][s] f32); with PKV_QP_LOGITS|PKV_QP_APPEND_KV
+ * it is finalize_query (recompute.py:105-125, last_logits [vocab] f32).
+ * query_ids: device int32 [m].  fresh_k/fresh_v (nullable): fp32 [L][m][Hkv][head_dim]. */
+size_t pkv_query_pass_workspace(const pkv_model* m, int32_t s, int32_t n_query, int32_t flags);
+int pkv_query_pass(const pkv_model* m, const pkv_cache* cache, const pkv_chunks* chunks, const int32_t* query_ids,
+                   int32_t n_query, int32_t flags, float* per_layer, float* fresh_k, float* fresh_v,
+                   float* last_logits, void* workspace, size_t workspace_bytes, void* stream);
+
+/* fuse_layers + select_top_p -- selection.py:52-61 with top_k_indices tensor.py:117-133.
+ * per_layer [L][s] f32 -> fused [s] f32 (nullable) and the k indices, ascending, in idx_out.
+ * status_out (device int32) receives PKV_OK or PKV_ERR_NUMERICS (non-finite scores). */
+size_t pkv_select_workspace(int32_t n_layers, int32_t s);
+int pkv_fuse_select(const float* per_layer, int32_t n_layers, int32_t s, int32_t k, float* fused, int32_t* idx_out,
+                    int32_t* status_out, void* workspace, size_t workspace_bytes, void* stream);
+/* top_k_indices -- tensor.py:117-133 on an arbitrary f32 vector */
+int pkv_topk(const float* scores, int32_t n, int32_t k, int32_t* idx_out, int32_t* status_out, void* stream);
+
+/* recompute_selected (fresh-peer mode) -- recompute.py:43-82.
+ * sel: device int32 [k], strictly ascending positions.  Per layer: fresh K/V of
+ * all selected tokens are written into the cache first (replace_entries,
+ * chunkstore.py:143-160), then the selected queries attend over the updated
+ * layer with mask pos_kv <= pos_sel.  tap_k/tap_v (nullable): fp32
+ * [L][k][Hkv][head_dim] copies of the recomputed K/V before bf16 storage. */
+size_t pkv_recompute_workspace(const pkv_model* m, int32_t k);
+int pkv_recompute(const pkv_model* m, const pkv_cache* cache, const int32_t* sel, int32_t k, float* tap_k,
+                  float* tap_v, void* workspace, size_t workspace_bytes, void* stream);
+
+/* replace_entries -- chunkstore.py:143-160 (standalone scatter of fp32 rows) */
+int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* cache, int32_t layer, const int32_t* idx, int32_t n,
+                        const float* new_k, const float* new_v, void* stream);
+
+/* f32 view of one cache layer as keys_rebased/values ([s][Hkv][head_dim]).
+ * chunks != NULL: derive from the chunk store (exact f32 rotation of the
+ * assembled keys); chunks == NULL: read the bf16 cache. */
+int pkv_cache_view(const pkv_config* cfg, const pkv_cache* cache, const pkv_chunks* chunks, int32_t layer, int32_t is_key,
+                   float* out, void* stream);
+
+/* unit-level entry points used by the kernel tests */
+int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K, float* C,
+                  int64_t ldc, int32_t bn, int32_t epilogue, void* stream);
+int pkv_attention_sparse(const pkv_model* m, const pkv_cache* cache, int32_t layer, const void* q, void* out,
+                         const int32_t* pos, int32_t n_q, void* stream);
+
+const char* pkv_last_error(void);
+uint64_t pkv_launch_count(void);
+int pkv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PKV_H_ */

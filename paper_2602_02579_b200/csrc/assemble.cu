@@ -1,0 +1,159 @@
+// K1: position-independent KV assembly (reference chunkstore.py:99-140 with
+// rope_apply tensor.py:89-114) and the K8 standalone scatter (replace_entries,
+// chunkstore.py:143-160).
+//
+// Chunk store layout (input): per chunk, bf16 [L][t_c][Hkv][dkp], keys unrotated.
+// Paged cache (output):       bf16 [L][Hkv][pool_tokens][dkp]; slot of token t is
+//                             page_table[t/128]*128 + t%128.
+// Keys are rotated with the float64 cos/sin table (identical bytes to the
+// oracle's rope_cos_sin), products and the difference rounded exactly like the
+// reference's float64 numpy expression, then rounded f64->f32->bf16: the stored
+// key is bf16(reference f32 key) bit for bit.
+#include "kernels.cuh"
+
+namespace pkv {
+
+
+__device__ __forceinline__ void rope_pair64(float e, float o, double c, double s, float& oe, float& oo) {
+  double de = (double)e, dd = (double)o;
+  oe = (float)__dsub_rn(__dmul_rn(de, c), __dmul_rn(dd, s));
+  oo = (float)__dadd_rn(__dmul_rn(de, s), __dmul_rn(dd, c));
+}
+
+// one thread = one (token, 16-byte column vector); loops over layers and heads
+__global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int L, int Hkv, int dkp, int head_dim,
+                                                       const double* __restrict__ rcos,
+                                                       const double* __restrict__ rsin, const int32_t* page_table,
+                                                       __nv_bfloat16* k_pool, __nv_bfloat16* v_pool,
+                                                       long pool_tokens) {
+  const int vecs = dkp / 8;
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)s * vecs) return;
+  const int t = (int)(gid / vecs);
+  const int c = (int)(gid - (long)t * vecs);
+  const int ch = cv.src_chunk[t];
+  const int loc = cv.src_local[t];
+  const int tc = cv.chunk_len[ch];
+  const __nv_bfloat16* kb = reinterpret_cast<const __nv_bfloat16*>(cv.k_nr[ch]);
+  const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(cv.v[ch]);
+  const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
+  const int half = head_dim >> 1;
+  // this thread's 4 pairs of cos/sin stay in registers for all L*Hkv rows
+  double cs[4], sn[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    int i = c * 4 + p;
+    cs[p] = i < half ? rcos[(long)t * half + i] : 1.0;
+    sn[p] = i < half ? rsin[(long)t * half + i] : 0.0;
+  }
+  for (int l = 0; l < L; ++l) {
+    const long src_row = ((long)l * tc + loc) * Hkv;
+    const long dst_layer = (long)l * Hkv * pool_tokens;
+    for (int h = 0; h < Hkv; ++h) {
+      const long so = (src_row + h) * dkp + c * 8;
+      uint4 kv = __ldg(reinterpret_cast<const uint4*>(kb + so));
+      uint4 vv = __ldg(reinterpret_cast<const uint4*>(vb + so));
+      uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w}, o[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        float e = bf16_lo(w[p]), od = bf16_hi(w[p]);
+        float re = e, ro = od;
+        if (2 * (c * 4 + p) < head_dim) rope_pair64(e, od, cs[p], sn[p], re, ro);
+        o[p] = pack_bf16(re, ro);
+      }
+      const long dofs = (dst_layer + (long)h * pool_tokens + slot) * dkp + c * 8;
+      *reinterpret_cast<uint4*>(k_pool + dofs) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(v_pool + dofs) = vv;
+    }
+  }
+}
+
+int assemble_launch(const ChunkView& cv, int s, int L, int Hkv, int dkp, int head_dim, const double* rcos,
+                    const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
+                    cudaStream_t stream) {
+  if (s <= 0) return PKV_OK;
+  const long threads = (long)s * (dkp / 8);
+  assemble_kernel<<<ceil_div(threads, 128), 128, 0, stream>>>(
+      cv, s, L, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__nv_bfloat16*>(k_pool),
+      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("assemble_kernel");
+  return PKV_OK;
+}
+
+// f32 view of one cache layer as the reference stores it ([s][Hkv][dk]).
+// Keys of entries not yet recomputed are re-derived exactly from the chunk store
+// (rotation in float64 -> f32, bit-identical to keys_rebased); recomputed entries
+// and values come from the fp32 taps when given, else from the bf16 cache.
+__global__ void cache_view_kernel(ChunkView cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
+                                  const double* rcos, const double* rsin, const int32_t* page_table,
+                                  const __nv_bfloat16* pool, long pool_tokens, int is_key, float* out) {
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)s * Hkv * head_dim;
+  if (gid >= total) return;
+  const int d = (int)(gid % head_dim);
+  const long th = gid / head_dim;
+  const int h = (int)(th % Hkv);
+  const int t = (int)(th / Hkv);
+  if (use_chunks) {
+    const int ch = cv.src_chunk[t], loc = cv.src_local[t], tc = cv.chunk_len[ch];
+    const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(is_key ? cv.k_nr[ch] : cv.v[ch]);
+    const long row = (((long)layer * tc + loc) * Hkv + h) * dkp;
+    if (!is_key) {
+      out[gid] = __bfloat162float(base[row + d]);
+      return;
+    }
+    const int i = d >> 1, half = head_dim >> 1;
+    float e = __bfloat162float(base[row + 2 * i]), o = __bfloat162float(base[row + 2 * i + 1]);
+    float re, ro;
+    rope_pair64(e, o, rcos[(long)t * half + i], rsin[(long)t * half + i], re, ro);
+    out[gid] = (d & 1) ? ro : re;
+  } else {
+    const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
+    out[gid] = __bfloat162float(pool[(((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d]);
+  }
+}
+
+int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
+                      const double* rcos, const double* rsin, const int32_t* page_table, const void* pool,
+                      long pool_tokens, int is_key, float* out, cudaStream_t stream) {
+  const long total = (long)s * Hkv * head_dim;
+  if (total <= 0) return PKV_OK;
+  cache_view_kernel<<<ceil_div(total, 256), 256, 0, stream>>>(cv, use_chunks, s, layer, Hkv, dkp, head_dim, rcos,
+                                                             rsin, page_table,
+                                                             reinterpret_cast<const __nv_bfloat16*>(pool),
+                                                             pool_tokens, is_key, out);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("cache_view_kernel");
+  return PKV_OK;
+}
+
+// scatter fp32 rows [n][Hkv][dk] into the bf16 cache at token indices idx
+__global__ void scatter_kernel(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim,
+                               const float* src, const int32_t* page_table, __nv_bfloat16* pool,
+                               long pool_tokens) {
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long total = (long)n * Hkv * dkp;
+  if (gid >= total) return;
+  const int d = (int)(gid % dkp);
+  const long rh = gid / dkp;
+  const int h = (int)(rh % Hkv);
+  const int r = (int)(rh / Hkv);
+  const int t = idx[r];
+  const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
+  const float v = d < head_dim ? src[((long)r * Hkv + h) * head_dim + d] : 0.f;
+  pool[(((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d] = __float2bfloat16_rn(v);
+}
+
+int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim, const float* src,
+                   const int32_t* page_table, void* pool, long pool_tokens, cudaStream_t stream) {
+  const long total = (long)n * Hkv * dkp;
+  if (total <= 0) return PKV_OK;
+  scatter_kernel<<<ceil_div(total, 256), 256, 0, stream>>>(idx, n, layer, Hkv, dkp, head_dim, src, page_table,
+                                                          reinterpret_cast<__nv_bfloat16*>(pool), pool_tokens);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("scatter_kernel");
+  return PKV_OK;
+}
+
+}  // namespace pkv

@@ -1,0 +1,478 @@
+// C-ABI entry points (include/pkv.h): validation, workspace carving and the
+// per-layer launch sequences of the three stages.  The host loop lives here (C++),
+// so Python makes one call per stage.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+struct pkv_model {
+  pkv_config cfg;
+  int dkp, Dp, Fp, NQKV, HQ;
+  pkv_weights w;
+  std::vector<pkv_layer_weights> layers;
+};
+
+namespace pkv {
+
+// ---- error state / bookkeeping
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int num_sms() {
+  static int n = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  });
+  return n;
+}
+
+// ---- workspace carving
+struct Carver {
+  uint8_t* base;
+  size_t off = 0, cap;
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+static int layout_of(const pkv_config* c, int out[5]) {
+  if (c->n_layers <= 0 || c->n_heads <= 0 || c->n_kv_heads <= 0 || c->head_dim <= 0 || c->ffn_dim <= 0 ||
+      c->vocab_size <= 0)
+    return set_error(PKV_ERR_CONFIG, "all model dimensions must be positive");
+  if (c->n_heads % c->n_kv_heads != 0) return set_error(PKV_ERR_CONFIG, "n_heads not divisible by n_kv_heads");
+  if (c->hidden_dim != c->n_heads * c->head_dim) return set_error(PKV_ERR_CONFIG, "hidden_dim != n_heads*head_dim");
+  if (c->head_dim % 2 != 0) return set_error(PKV_ERR_CONFIG, "head_dim must be even");
+  if (!(c->rope_theta > 0) || !(c->norm_eps > 0)) return set_error(PKV_ERR_CONFIG, "rope_theta/norm_eps must be > 0");
+  if (c->head_dim > 128) return set_error(PKV_ERR_CONFIG, "head_dim > 128 not supported by the sm_100a kernels");
+  if (c->n_heads / c->n_kv_heads > 128) return set_error(PKV_ERR_CONFIG, "GQA group larger than 128");
+  const int dkp = c->head_dim <= 64 ? 64 : 128;
+  out[0] = dkp;
+  out[1] = (c->hidden_dim + 63) / 64 * 64;
+  out[2] = (c->ffn_dim + 127) / 128 * 128;
+  out[3] = (c->n_heads + 2 * c->n_kv_heads) * dkp;
+  out[4] = c->n_heads * dkp;
+  return PKV_OK;
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// fp32-faithful projection of m (<= any) fp32 rows: out[m][N] (=|+=) x[m][K] . W[N][K]^T
+// via tcgen05 on the 3-way bf16 split of x, split-K partials and a reduce.
+struct ProjWs {
+  void* x3;        // bf16 [96][Kmax]
+  long ldx;
+  float* part;     // [8][Nmax][96]
+};
+static int choose_splits(int N, int K) {
+  const int m_tiles = ceil_div(N, 128), k_tiles = ceil_div(K, 64);
+  int sp = std::max(1, num_sms() / std::max(1, m_tiles));
+  sp = std::min(sp, 8);
+  sp = std::min(sp, std::max(1, k_tiles / 8));
+  return sp;
+}
+static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, int m, float* out, long ldo, int mode,
+                    const ProjWs& ws, cudaStream_t st) {
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    const int rows = std::min(32, m - r0);
+    int rc = split3_launch(x + (long)r0 * ldx_src, rows, K, ldx_src, ws.x3, ws.ldx, st);
+    if (rc) return rc;
+    GemmArgs g{};
+    g.M = N;
+    g.N = 96;
+    const int sp = choose_splits(N, K);
+    g.n_splits = sp;
+    g.k_tiles_per_split = ceil_div(ceil_div(K, 64), sp);
+    g.C = ws.part;
+    g.ldc = 96;
+    const int nsp = ceil_div(ceil_div(K, 64), g.k_tiles_per_split);
+    rc = gemm_tc_launch(EPI_F32, 96, W, K, ws.x3, ws.ldx, K, g, st);
+    if (rc) return rc;
+    rc = splitk_reduce_launch(ws.part, nsp, N, rows, out + (long)r0 * ldo, ldo, mode, st);
+    if (rc) return rc;
+  }
+  return PKV_OK;
+}
+
+}  // namespace pkv
+
+using namespace pkv;
+
+extern "C" {
+
+int pkv_version(void) { return 1; }
+const char* pkv_last_error(void) { return g_err; }
+uint64_t pkv_launch_count(void) { return g_launches.load(); }
+
+int pkv_layout(const pkv_config* cfg, int32_t out[5]) {
+  int o[5];
+  int rc = layout_of(cfg, o);
+  if (rc) return rc;
+  for (int i = 0; i < 5; ++i) out[i] = o[i];
+  return PKV_OK;
+}
+
+int pkv_model_create(const pkv_config* cfg, const pkv_weights* w, pkv_model** out) {
+  int o[5];
+  int rc = layout_of(cfg, o);
+  if (rc) return rc;
+  if (!w || !w->layers || !w->embed || !w->lm_head || !w->final_norm)
+    return set_error(PKV_ERR_ARGUMENT, "null weight pointer");
+  pkv_model* m = new pkv_model();
+  m->cfg = *cfg;
+  m->dkp = o[0];
+  m->Dp = o[1];
+  m->Fp = o[2];
+  m->NQKV = o[3];
+  m->HQ = o[4];
+  m->layers.assign(w->layers, w->layers + cfg->n_layers);
+  for (auto& l : m->layers)
+    if (!l.wqkv || !l.wo || !l.wgu || !l.wd || !l.attn_norm || !l.ffn_norm) {
+      delete m;
+      return set_error(PKV_ERR_ARGUMENT, "null layer weight pointer");
+    }
+  m->w = *w;
+  m->w.layers = m->layers.data();
+  *out = m;
+  return PKV_OK;
+}
+
+void pkv_model_destroy(pkv_model* m) { delete m; }
+
+int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c, void* stream) {
+  if (!cfg || !ch || !c) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  int lay[5];
+  int rc = layout_of(cfg, lay);
+  if (rc) return rc;
+  if (ch->n_chunks <= 0) return set_error(PKV_ERR_INPUT, "assemble needs at least one chunk");
+  if (c->pool_tokens % 128 != 0 || c->pool_tokens < c->s) return set_error(PKV_ERR_SHAPE, "pool too small");
+  if (c->rope_len < c->s) return set_error(PKV_ERR_SHAPE, "rope table shorter than the context");
+  ChunkView cv{ch->k_nr, ch->v, ch->src_chunk, ch->src_local, ch->chunk_len};
+  return assemble_launch(cv, c->s, cfg->n_layers, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos, c->rope_sin,
+                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, S(stream));
+}
+
+int pkv_cache_view(const pkv_config* cfg, const pkv_cache* c, const pkv_chunks* ch, int32_t layer, int32_t is_key,
+                   float* out, void* stream) {
+  int lay[5];
+  int rc = layout_of(cfg, lay);
+  if (rc) return rc;
+  if (layer < 0 || layer >= cfg->n_layers) return set_error(PKV_ERR_ARGUMENT, "layer out of range");
+  ChunkView cv{};
+  if (ch) cv = ChunkView{ch->k_nr, ch->v, ch->src_chunk, ch->src_local, ch->chunk_len};
+  const void* pool = is_key ? c->k_pool : c->v_pool;
+  return cache_view_launch(cv, ch != nullptr, c->s, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos,
+                           c->rope_sin, c->page_table, pool, c->pool_tokens, is_key, out, S(stream));
+}
+
+int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer, const int32_t* idx, int32_t n,
+                        const float* new_k, const float* new_v, void* stream) {
+  int lay[5];
+  int rc = layout_of(cfg, lay);
+  if (rc) return rc;
+  if (layer < 0 || layer >= cfg->n_layers) return set_error(PKV_ERR_ARGUMENT, "layer out of range");
+  rc = scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_k, c->page_table, c->k_pool,
+                      c->pool_tokens, S(stream));
+  if (rc) return rc;
+  return scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_v, c->page_table, c->v_pool,
+                        c->pool_tokens, S(stream));
+}
+
+// ------------------------------------------------------------------ query pass
+struct QpWs {
+  float *h, *x, *qkv, *q, *k, *v, *attn, *gu, *act, *S, *Opart, *Mpart, *Lpart, *Mfin, *Lfin, *rows, *xl;
+  double* denom;
+  ProjWs proj;
+  int n_splits, keys_per_split;
+};
+
+static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, size_t* total) {
+  const pkv_config& c = md->cfg;
+  const int H = c.n_heads, Hkv = c.n_kv_heads, G = H / Hkv, dkp = md->dkp;
+  const int R = m * G;
+  const int s_tot = s + m;
+  QpWs w{};
+  Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
+  const long kmax = std::max({(long)md->Dp, (long)md->HQ, (long)md->Fp});
+  const long nmax = std::max({(long)md->NQKV, (long)md->Dp, 2L * md->Fp});
+  w.h = cv.take<float>((size_t)m * md->Dp);
+  w.x = cv.take<float>((size_t)m * md->Dp);
+  w.qkv = cv.take<float>((size_t)m * md->NQKV);
+  w.q = cv.take<float>((size_t)m * H * dkp);
+  w.k = cv.take<float>((size_t)m * Hkv * dkp);
+  w.v = cv.take<float>((size_t)m * Hkv * dkp);
+  w.attn = cv.take<float>((size_t)m * H * dkp);
+  w.gu = cv.take<float>((size_t)m * 2 * md->Fp);
+  w.act = cv.take<float>((size_t)m * md->Fp);
+  w.proj.x3 = cv.take<__nv_bfloat16>((size_t)96 * kmax);
+  w.proj.ldx = kmax;
+  w.proj.part = cv.take<float>((size_t)8 * nmax * 96);
+  w.keys_per_split = 512;
+  w.n_splits = ceil_div(s_tot, w.keys_per_split);
+  const int row_blocks = ceil_div(R, 128);
+  (void)row_blocks;
+  if (flags & PKV_QP_SCORES) {
+    w.S = cv.take<float>((size_t)Hkv * R * s_tot);
+    w.rows = cv.take<float>((size_t)m * s);
+    w.denom = cv.take<double>((size_t)m);
+  }
+  w.Opart = cv.take<float>((size_t)w.n_splits * Hkv * R * dkp);
+  w.Mpart = cv.take<float>((size_t)w.n_splits * Hkv * R);
+  w.Lpart = cv.take<float>((size_t)w.n_splits * Hkv * R);
+  w.Mfin = cv.take<float>((size_t)Hkv * R);
+  w.Lfin = cv.take<float>((size_t)Hkv * R);
+  w.xl = cv.take<float>((size_t)md->Dp);
+  *total = cv.off + 256;
+  return w;
+}
+
+size_t pkv_query_pass_workspace(const pkv_model* m, int32_t s, int32_t n_query, int32_t flags) {
+  size_t total = 0;
+  carve_qp(m, s, n_query, flags, nullptr, &total);
+  return total;
+}
+
+int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch, const int32_t* query_ids,
+                   int32_t m, int32_t flags, float* per_layer, float* fresh_k, float* fresh_v, float* last_logits,
+                   void* workspace, size_t ws_bytes, void* stream) {
+  if (!md || !c || !query_ids) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (m <= 0) return set_error(PKV_ERR_INPUT, "token sequence must be non-empty");
+  const pkv_config& cf = md->cfg;
+  const int s = c->s;
+  if (c->rope_len < s + m) return set_error(PKV_ERR_SHAPE, "rope table shorter than context + query");
+  if ((flags & PKV_QP_FROM_CHUNKS) && !ch) return set_error(PKV_ERR_ARGUMENT, "chunk view required");
+  if ((flags & PKV_QP_APPEND_KV) && c->pool_tokens < s + m) return set_error(PKV_ERR_SHAPE, "pool too small to append");
+  size_t need = 0;
+  QpWs w = carve_qp(md, s, m, flags, workspace, &need);
+  if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = S(stream);
+  const int H = cf.n_heads, Hkv = cf.n_kv_heads, G = H / Hkv, dk = cf.head_dim, dkp = md->dkp;
+  const int Dp = md->Dp, Fp = md->Fp;
+  int rc;
+#define TRY(x)             \
+  do {                     \
+    if ((rc = (x)) != 0) return rc; \
+  } while (0)
+  TRY(embed_gather_launch(md->w.embed, Dp, query_ids, nullptr, m, cf.hidden_dim, w.h, Dp, st));
+  const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
+  for (int l = 0; l < cf.n_layers; ++l) {
+    const pkv_layer_weights& lw = md->layers[l];
+    TRY(rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
+    TRY(proj_f32(lw.wqkv, md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
+    __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
+    __nv_bfloat16* vp = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
+    const bool append = (flags & PKV_QP_APPEND_KV) != 0;
+    TRY(query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v, append ? kp : nullptr,
+                         append ? vp : nullptr, c->pool_tokens, c->page_table,
+                         fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
+                         fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, st));
+    S1Attn a{};
+    a.q = w.q;
+    a.m = m;
+    a.H = H;
+    a.Hkv = Hkv;
+    a.G = G;
+    a.dk = dk;
+    a.dkp = dkp;
+    a.s = s;
+    a.s_tot = s + m;
+    a.R = m * G;
+    a.keys_per_split = w.keys_per_split;
+    a.n_splits = w.n_splits;
+    a.scale = (float)(1.0 / std::sqrt((double)dk));
+    a.src_chunks = (flags & PKV_QP_FROM_CHUNKS) ? 1 : 0;
+    a.recomp = c->recomputed;
+    if (ch) {
+      a.ck = ch->k_nr;
+      a.cv = ch->v;
+      a.src_chunk = ch->src_chunk;
+      a.src_local = ch->src_local;
+      a.chunk_len = ch->chunk_len;
+    }
+    a.rcos = c->rope_cos;
+    a.rsin = c->rope_sin;
+    a.k_pool = kp;
+    a.v_pool = vp;
+    a.pool_tokens = c->pool_tokens;
+    a.page_table = c->page_table;
+    a.layer = l;
+    a.fk = w.k;
+    a.fv = w.v;
+    const bool scores = (flags & PKV_QP_SCORES) && per_layer;
+    a.S = scores ? w.S : nullptr;
+    a.Opart = w.Opart;
+    a.Mpart = w.Mpart;
+    a.Lpart = w.Lpart;
+    TRY(s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
+                            (flags & PKV_QP_RENORM) ? 1 : 0, st));
+    TRY(proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, 1, w.proj, st));
+    TRY(rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
+    TRY(proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
+    TRY(silu_act_launch(w.gu, m, cf.ffn_dim, Fp, w.act, st));
+    TRY(proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, 1, w.proj, st));
+  }
+  if ((flags & PKV_QP_LOGITS) && last_logits) {
+    TRY(rmsnorm_launch(w.h + (long)(m - 1) * Dp, 1, cf.hidden_dim, Dp, md->w.final_norm, cf.norm_eps, w.xl, nullptr, 0,
+                       nullptr, st));
+    TRY(gemv_launch(w.xl, md->w.lm_head, cf.vocab_size, Dp, Dp, last_logits, st));
+  }
+  return PKV_OK;
+}
+
+// ------------------------------------------------------------------- selection
+size_t pkv_select_workspace(int32_t n_layers, int32_t s) { return ((size_t)s * 4 + 255) & ~size_t(255); }
+
+int pkv_fuse_select(const float* per_layer, int32_t L, int32_t s, int32_t k, float* fused, int32_t* idx_out,
+                    int32_t* status_out, void* workspace, size_t ws_bytes, void* stream) {
+  if (k < 0 || k > s) return set_error(PKV_ERR_ARGUMENT, "k=%d outside [0, %d]", k, s);
+  float* f = fused;
+  if (!f) {
+    if (ws_bytes < (size_t)s * 4) return set_error(PKV_ERR_ARGUMENT, "workspace too small");
+    f = reinterpret_cast<float*>(workspace);
+  }
+  int rc = fuse_layers_launch(per_layer, L, s, f, S(stream));
+  if (rc) return rc;
+  return topk_launch(f, s, k, idx_out, status_out, S(stream));
+}
+
+int pkv_topk(const float* scores, int32_t n, int32_t k, int32_t* idx_out, int32_t* status_out, void* stream) {
+  if (k < 0 || k > n) return set_error(PKV_ERR_ARGUMENT, "k=%d outside [0, %d]", k, n);
+  return topk_launch(scores, n, k, idx_out, status_out, S(stream));
+}
+
+// ------------------------------------------------------------------- recompute
+struct RcWs {
+  float* h;
+  __nv_bfloat16 *xb, *qb, *ab, *act;
+};
+static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
+  Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
+  RcWs w{};
+  w.h = cv.take<float>((size_t)k * md->Dp);
+  w.xb = cv.take<__nv_bfloat16>((size_t)k * md->Dp);
+  w.qb = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
+  w.ab = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
+  w.act = cv.take<__nv_bfloat16>((size_t)k * md->Fp);
+  *total = cv.off + 256;
+  return w;
+}
+
+size_t pkv_recompute_workspace(const pkv_model* m, int32_t k) {
+  size_t t = 0;
+  carve_rc(m, k, nullptr, &t);
+  return t;
+}
+
+int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k, float* tap_v,
+                  void* workspace, size_t ws_bytes, void* stream) {
+  if (k == 0) return PKV_OK;
+  if (k < 0 || k > c->s) return set_error(PKV_ERR_ARGUMENT, "bad selection size %d", k);
+  size_t need = 0;
+  RcWs w = carve_rc(md, k, workspace, &need);
+  if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
+  cudaStream_t st = S(stream);
+  const pkv_config& cf = md->cfg;
+  const int H = cf.n_heads, Hkv = cf.n_kv_heads, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
+  const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
+  int rc;
+  TRY(embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
+  for (int l = 0; l < cf.n_layers; ++l) {
+    const pkv_layer_weights& lw = md->layers[l];
+    TRY(rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    GemmArgs g{};
+    g.M = k;
+    g.N = md->NQKV;
+    g.n_splits = 1;
+    g.C = w.qb;
+    g.ldc = md->HQ;
+    g.pos = sel;
+    g.rope_cos = c->rope_cos;
+    g.rope_sin = c->rope_sin;
+    g.head_dim = dk;
+    g.dkp = dkp;
+    g.n_heads = H;
+    g.n_kv_heads = Hkv;
+    g.k_pool = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
+    g.v_pool = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
+    g.pool_tokens = c->pool_tokens;
+    g.page_table = c->page_table;
+    g.tap_k = tap_k ? tap_k + (long)l * k * Hkv * dk : nullptr;
+    g.tap_v = tap_v ? tap_v + (long)l * k * Hkv * dk : nullptr;
+    // K/V of every selected token are in the cache before this layer's attention
+    TRY(gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    TRY(attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
+                       (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
+    GemmArgs go{};
+    go.M = k;
+    go.N = Dp;
+    go.n_splits = 1;
+    go.C = w.h;
+    go.ldc = Dp;
+    TRY(gemm_tc_launch(EPI_RESID, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
+    TRY(rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    GemmArgs gg{};
+    gg.M = k;
+    gg.N = 2 * Fp;
+    gg.n_splits = 1;
+    gg.C = w.act;
+    gg.ldc = Fp;
+    TRY(gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
+    GemmArgs gd{};
+    gd.M = k;
+    gd.N = Dp;
+    gd.n_splits = 1;
+    gd.C = w.h;
+    gd.ldc = Dp;
+    TRY(gemm_tc_launch(EPI_RESID, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
+  }
+  return PKV_OK;
+}
+
+// ------------------------------------------------------------------ unit entry
+int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K, float* C,
+                  int64_t ldc, int32_t bn, int32_t epi, void* stream) {
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.n_splits = 1;
+  g.C = C;
+  g.ldc = ldc;
+  if (epi != EPI_F32 && epi != EPI_RESID && epi != EPI_BF16) return set_error(PKV_ERR_ARGUMENT, "epilogue");
+  return gemm_tc_launch(epi, bn, A, lda, B, ldb, K, g, S(stream));
+}
+
+int pkv_attention_sparse(const pkv_model* md, const pkv_cache* c, int32_t layer, const void* q, void* out,
+                         const int32_t* pos, int32_t n_q, void* stream) {
+  const pkv_config& cf = md->cfg;
+  return attn_tc_launch(q, out, pos, n_q, cf.n_heads, cf.n_kv_heads, cf.head_dim, md->dkp, c->k_pool, c->v_pool,
+                        (long)cf.n_layers * cf.n_kv_heads * c->pool_tokens, c->pool_tokens, layer, c->page_table,
+                        S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Host side of the tcgen05 GEMM: TMA descriptor encoding (cached per buffer) and
+// launch dispatch over (BN, epilogue).
+#include <mutex>
+#include <unordered_map>
+
+#include "gemm_tc.cuh"
+
+namespace pkv {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// row-major bf16 matrix [rows][cols] with the given row stride; box = box_rows x box_cols,
+// 128-byte swizzle (box_cols must be 64). Out-of-range rows/cols read as zero.
+bool make_tmap_2d(CUtensorMap* map, const void* base, long rows, long cols, long row_stride_elems, int box_rows,
+                  int box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_stride_elems * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+namespace {
+struct MapKey {
+  const void* p;
+  long rows, cols, stride;
+  int box_rows;
+  bool operator==(const MapKey& o) const {
+    return p == o.p && rows == o.rows && cols == o.cols && stride == o.stride && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.p);
+    h ^= (size_t)k.rows * 0x9E3779B97F4A7C15ull;
+    h ^= (size_t)k.cols * 0xC2B2AE3D27D4EB4Full + (size_t)k.stride * 31 + (size_t)k.box_rows;
+    return h;
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+}  // namespace
+
+static bool cached_tmap(CUtensorMap* out, const void* base, long rows, long cols, long stride, int box_rows) {
+  MapKey key{base, rows, cols, stride, box_rows};
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto it = g_maps.find(key);
+  if (it != g_maps.end()) {
+    *out = it->second;
+    return true;
+  }
+  if (g_maps.size() > 4096) g_maps.clear();
+  if (!make_tmap_2d(out, base, rows, cols, stride, box_rows, 64)) return false;
+  g_maps.emplace(key, *out);
+  return true;
+}
+
+template <int BN, int EPI>
+static int launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t stream) {
+  using Cfg = GemmCfg<BN>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  });
+  if (attr_err != cudaSuccess) return set_error(PKV_ERR_CUDA, "gemm smem attr: %s", cudaGetErrorString(attr_err));
+  long tiles = (long)ceil_div(args.M, Cfg::BM) * ceil_div(args.N, BN) * args.n_splits;
+  int grid = (int)std::min<long>(tiles, num_sms());
+  if (grid <= 0) return PKV_OK;
+  gemm_tc_kernel<BN, EPI><<<grid, 192, Cfg::SMEM, stream>>>(ta, tb, args);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("gemm_tc_kernel");
+  return PKV_OK;
+}
+
+// A: [M][K] bf16 (row stride lda elements), B: [N][K] bf16 (row stride ldb).
+int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long ldb, int K, GemmArgs args,
+                   cudaStream_t stream) {
+  if (args.M <= 0 || args.N <= 0) return PKV_OK;
+  if (K <= 0) return set_error(PKV_ERR_SHAPE, "gemm: K must be positive");
+  if ((lda * 2) % 16 != 0 || (ldb * 2) % 16 != 0)
+    return set_error(PKV_ERR_SHAPE, "gemm: row strides must be multiples of 8 elements");
+  args.K = K;
+  int kt = ceil_div(K, 64);
+  if (args.n_splits <= 0) args.n_splits = 1;
+  if (args.k_tiles_per_split <= 0) args.k_tiles_per_split = ceil_div(kt, args.n_splits);
+  args.n_splits = ceil_div(kt, args.k_tiles_per_split);  // no empty splits
+  CUtensorMap ta, tb;
+  if (!cached_tmap(&ta, A, args.M, K, lda, 128)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode A failed");
+  if (!cached_tmap(&tb, B, args.N, K, ldb, bn)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode B failed");
+  switch (bn * 16 + epi) {
+    case 256 * 16 + EPI_F32: return launch_one<256, EPI_F32>(ta, tb, args, stream);
+    case 256 * 16 + EPI_BF16: return launch_one<256, EPI_BF16>(ta, tb, args, stream);
+    case 256 * 16 + EPI_RESID: return launch_one<256, EPI_RESID>(ta, tb, args, stream);
+    case 256 * 16 + EPI_SILU: return launch_one<256, EPI_SILU>(ta, tb, args, stream);
+    case 256 * 16 + EPI_QKV: return launch_one<256, EPI_QKV>(ta, tb, args, stream);
+    case 128 * 16 + EPI_F32: return launch_one<128, EPI_F32>(ta, tb, args, stream);
+    case 128 * 16 + EPI_RESID: return launch_one<128, EPI_RESID>(ta, tb, args, stream);
+    case 96 * 16 + EPI_F32: return launch_one<96, EPI_F32>(ta, tb, args, stream);
+    default: return set_error(PKV_ERR_ARGUMENT, "gemm: unsupported (BN=%d, epi=%d)", bn, epi);
+  }
+}
+
+}  // namespace pkv

@@ -1,0 +1,313 @@
+// Persistent, warp-specialised tcgen05 GEMM:  D[M,N] = A[M,K] . B[N,K]^T
+// (both operands K-major bf16, fp32 accumulation in TMEM) with fused epilogues.
+//
+//   warp 0      TMA producer (one elected lane) -> smem ring of STAGES (A,B) tiles
+//   warp 1      TMEM allocator + MMA issuer (one elected lane), 2 TMEM accumulators
+//   warps 2..5  epilogue: tcgen05.ld a row per thread, apply EPI, store to HBM
+//
+// Used by Stage II (recompute_selected, reference recompute.py:55-82: QKV / o /
+// gate-up / down projections) with A = activations of the k selected tokens and
+// B = transposed weights, and by the fp32-faithful narrow pass with A = weights
+// and B = a 3-way bf16 split of the fp32 activations (split-K partials).
+#pragma once
+#include "common.cuh"
+
+namespace pkv {
+
+enum GemmEpi : int {
+  EPI_F32 = 0,      // C (+ split * M * ldc) = acc               (fp32 partials / plain store)
+  EPI_BF16 = 1,     // C = bf16(acc)
+  EPI_RESID = 2,    // C += acc                                    (fp32 residual stream)
+  EPI_SILU = 3,     // C[:, n/2..] = bf16(silu(gate) * up), gate/up interleaved per 128 cols
+  EPI_QKV = 4,      // rope(q), rope(k) at token positions; q -> bf16 buffer; k, v -> paged cache
+};
+
+struct GemmArgs {
+  int M, N, K;
+  int k_tiles_per_split;  // in units of 64
+  int n_splits;
+  void* C;                // output (see GemmEpi)
+  long ldc;               // elements
+  // EPI_QKV -----------------------------------------------------------------
+  const int32_t* pos;         // [M] token positions (also cache slot via page table)
+  const double* rope_cos;     // [n_pos][dk/2]
+  const double* rope_sin;
+  int head_dim, dkp, n_heads, n_kv_heads;
+  __nv_bfloat16* k_pool;      // layer base: [Hkv][pool_tokens][dkp]
+  __nv_bfloat16* v_pool;
+  long pool_tokens;
+  const int32_t* page_table;
+  float* tap_k;               // optional fp32 [M][Hkv][dk]
+  float* tap_v;
+};
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 7);
+  static constexpr int ACC_STRIDE = BN <= 128 ? 128 : 256;
+  static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
+  using Cfg = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + Cfg::STAGES;
+  uint64_t* tfull_bar = empty_bar + Cfg::STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int tiles_m = (args.M + Cfg::BM - 1) / Cfg::BM;
+  const int tiles_n = (args.N + BN - 1) / BN;
+  const int total_tiles = tiles_m * tiles_n * args.n_splits;
+  const int k_tiles_total = (args.K + Cfg::BK - 1) / Cfg::BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& mb, int& nb, int& sp) {
+    mb = t % tiles_m;
+    int r = t / tiles_m;
+    nb = r % tiles_n;
+    sp = r / tiles_n;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int mb, nb, sp;
+        tile_coords(t, mb, nb, sp);
+        int k0 = sp * args.k_tiles_per_split;
+        int k1 = min(k0 + args.k_tiles_per_split, k_tiles_total);
+        for (int kt = k0; kt < k1; ++kt) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full_bar[stage], kt * Cfg::BK, mb * Cfg::BM);
+          tma_load_2d(sb, &tmB, &full_bar[stage], kt * Cfg::BK, nb * BN);
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = make_idesc_bf16(128, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      int mb, nb, sp;
+      tile_coords(t, mb, nb, sp);
+      int k0 = sp * args.k_tiles_per_split;
+      int k1 = min(k0 + args.k_tiles_per_split, k_tiles_total);
+      const int acc = local & 1;
+      const uint32_t use = (uint32_t)(local >> 1);
+      mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_STRIDE;
+      for (int kt = k0; kt < k1; ++kt) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_addr = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < Cfg::BK / 16; ++kk) {
+            uint64_t ad = sdesc_sw128(a_addr + kk * 32, 16, 1024);
+            uint64_t bd = sdesc_sw128(b_addr + kk * 32, 16, 1024);
+            umma_bf16(d_tmem, ad, bd, idesc, (kt > k0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = quarter * 32 + lane;
+    int local = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      int mb, nb, sp;
+      tile_coords(t, mb, nb, sp);
+      const int acc = local & 1;
+      const uint32_t use = (uint32_t)(local >> 1);
+      mbar_wait(&tfull_bar[acc], use & 1);
+      tc_fence_after();
+      const int row = mb * Cfg::BM + row_in_tile;
+      const bool row_ok = row < args.M;
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * Cfg::ACC_STRIDE;
+
+      if constexpr (EPI == EPI_SILU) {
+        // gate columns [0,BN/2), up columns [BN/2,BN) of this tile feed BN/2 outputs
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t g[32], u[32];
+          __syncwarp();
+          tmem_ld32(t_row + c * 32, g);
+          tmem_ld32(t_row + BN / 2 + c * 32, u);
+          tmem_ld_wait();
+          const int col = nb * (BN / 2) + c * 32;
+          if (row_ok && col < args.N / 2) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              float a0 = silu_f(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
+              float a1 = silu_f(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
+              packed[j] = pack_bf16(a0, a1);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          __syncwarp();
+          tmem_ld32(t_row + c * 32, r);
+          tmem_ld_wait();
+          const int col0 = nb * BN + c * 32;
+          if (!row_ok || col0 >= args.N) continue;
+          const bool full = col0 + 32 <= args.N;
+          if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
+            float* dst = reinterpret_cast<float*>(args.C) + (long)sp * args.M * args.ldc + (long)row * args.ldc + col0;
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                       __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                if constexpr (EPI == EPI_RESID) {
+                  float4 o = reinterpret_cast<float4*>(dst)[j];
+                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                }
+                reinterpret_cast<float4*>(dst)[j] = v;
+              }
+            } else {
+              for (int j = 0; j < 32 && col0 + j < args.N; ++j) {
+                float v = __uint_as_float(r[j]);
+                if constexpr (EPI == EPI_RESID) v += dst[j];
+                dst[j] = v;
+              }
+            }
+          } else if constexpr (EPI == EPI_BF16) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col0;
+            if (full) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                reinterpret_cast<uint4*>(dst)[j] =
+                    make_uint4(pack_bf16(__uint_as_float(r[8 * j]), __uint_as_float(r[8 * j + 1])),
+                               pack_bf16(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
+                               pack_bf16(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
+                               pack_bf16(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
+            } else {
+              for (int j = 0; j < 32 && col0 + j < args.N; ++j) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+            }
+          } else if constexpr (EPI == EPI_QKV) {
+            // a 32-column chunk never straddles a head (dkp is 64 or 128)
+            const int dkp = args.dkp;
+            const int head_all = col0 / dkp;  // 0..H+2Hkv-1
+            const int d0 = col0 - head_all * dkp;
+            const int H = args.n_heads, Hkv = args.n_kv_heads;
+            const int pos = args.pos[row];
+            const bool is_v = head_all >= H + Hkv;
+            float vals[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]);
+            if (!is_v) {
+              // interleaved-pair RoPE with float64 factors (reference tensor.py:104-113)
+              const int half = args.head_dim >> 1;
+              const double* cs = args.rope_cos + (long)pos * half;
+              const double* sn = args.rope_sin + (long)pos * half;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                int i = (d0 >> 1) + j;
+                if (2 * i < args.head_dim) {
+                  double c = cs[i], s = sn[i];
+                  double e = (double)vals[2 * j], o = (double)vals[2 * j + 1];
+                  vals[2 * j] = (float)__dsub_rn(__dmul_rn(e, c), __dmul_rn(o, s));
+                  vals[2 * j + 1] = (float)__dadd_rn(__dmul_rn(e, s), __dmul_rn(o, c));
+                }
+              }
+            }
+            uint32_t packed[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) packed[j] = pack_bf16(vals[2 * j], vals[2 * j + 1]);
+            __nv_bfloat16* dst;
+            if (head_all < H) {
+              dst = reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col0;
+            } else {
+              const int g = is_v ? head_all - H - Hkv : head_all - H;
+              const long slot = (long)args.page_table[pos >> 7] * 128 + (pos & 127);
+              __nv_bfloat16* pool = is_v ? args.v_pool : args.k_pool;
+              dst = pool + ((long)g * args.pool_tokens + slot) * dkp + d0;
+              float* tap = is_v ? args.tap_v : args.tap_k;
+              if (tap != nullptr) {
+                float* tp = tap + ((long)row * Hkv + g) * args.head_dim;
+                for (int j = 0; j < 32; ++j)
+                  if (d0 + j < args.head_dim) tp[d0 + j] = vals[j];
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              reinterpret_cast<uint4*>(dst)[j] =
+                  make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// host launcher (gemm_tc.cu)
+int gemm_tc_launch(int epi, int bn, const void* A, long lda_rows, const void* B, long ldb_rows, int K, GemmArgs args,
+                   cudaStream_t stream);
+bool make_tmap_2d(CUtensorMap* map, const void* base, long rows, long cols, long row_stride_elems, int box_rows,
+                  int box_cols);
+
+}  // namespace pkv

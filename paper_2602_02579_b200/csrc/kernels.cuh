@@ -1,0 +1,67 @@
+// Launcher declarations and the argument structs shared between translation units.
+#pragma once
+#include "common.cuh"
+
+namespace pkv {
+
+struct ChunkView {
+  const uint64_t* k_nr;
+  const uint64_t* v;
+  const int32_t* src_chunk;
+  const int32_t* src_local;
+  const int32_t* chunk_len;
+};
+int assemble_launch(const ChunkView& cv, int s, int L, int Hkv, int dkp, int head_dim, const double* rcos,
+                    const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
+                    cudaStream_t stream);
+int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
+                      const double* rcos, const double* rsin, const int32_t* page_table, const void* pool,
+                      long pool_tokens, int is_key, float* out, cudaStream_t stream);
+int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim, const float* src,
+                   const int32_t* page_table, void* pool, long pool_tokens, cudaStream_t stream);
+int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, cudaStream_t st);
+int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
+                   void* ybf, cudaStream_t st);
+int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, long ldy, int mode, cudaStream_t st);
+int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
+                     const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, cudaStream_t st);
+int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st);
+struct S1Attn {
+  const float* q;
+  int m, H, Hkv, G, dk, dkp, s, s_tot, R, keys_per_split, n_splits;
+  float scale;
+  int src_chunks;
+  const uint8_t* recomp;  // nullable [s]: repaired entries come from the pool
+  const uint64_t* ck;
+  const uint64_t* cv;
+  const int32_t* src_chunk;
+  const int32_t* src_local;
+  const int32_t* chunk_len;
+  const double* rcos;
+  const double* rsin;
+  const __nv_bfloat16* k_pool;
+  const __nv_bfloat16* v_pool;
+  long pool_tokens;
+  const int32_t* page_table;
+  int layer;
+  const float* fk;
+  const float* fv;
+  float* S;
+  float* Opart;
+  float* Mpart;
+  float* Lpart;
+};
+int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
+                        float* per_layer, int renorm, cudaStream_t st);
+int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st);
+int embed_gather_launch(const void* embed, long lde, const int32_t* ids, const int32_t* sel, int n, int D, float* out,
+                        long ldo, cudaStream_t st);
+int fuse_layers_launch(const float* per_layer, int L, int s, float* fused, cudaStream_t st);
+int topk_launch(const float* v, int n, int k, int32_t* out, int32_t* status, cudaStream_t st);
+int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H, int Hkv, int head_dim, int dkp,
+                   const void* k_pool, const void* v_pool, long pool_rows_total, long pool_tokens, int layer,
+                   const int32_t* page_table, cudaStream_t stream);
+
+
+}  // namespace pkv

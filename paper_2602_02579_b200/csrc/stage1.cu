@@ -1,0 +1,589 @@
+// Narrow query pass kernels (reference model.py:370-402 query_pass; scoring
+// selection.py:64-86; finalize recompute.py:105-125).  Everything here is
+// fp32-faithful: the m query rows stay fp32, projections run on tcgen05 with a
+// 3-way bf16 split of the activations (x = hi + mid + lo exactly), attention
+// scores / softmax / PV are fp32 SIMT, and the per-token score reductions run in
+// float64 like the reference.
+#include <mutex>
+#include "kernels.cuh"
+
+namespace pkv {
+
+// --------------------------------------------------------------- split / norm
+__device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  float r1 = x - __bfloat162float(hi);
+  mid = __float2bfloat16_rn(r1);
+  float r2 = r1 - __bfloat162float(mid);
+  lo = __float2bfloat16_rn(r2);
+}
+
+// x [m][ld] fp32 (first `cols` valid) -> X3 [96][ldx] bf16 rows i, 32+i, 64+i
+__global__ void split3_kernel(const float* x, int m, int cols, long ld, __nv_bfloat16* x3, long ldx) {
+  const int i = blockIdx.y;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ldx; c += gridDim.x * blockDim.x) {
+    float v = (i < m && c < cols) ? x[(long)i * ld + c] : 0.f;
+    __nv_bfloat16 a, b, d;
+    split3(v, a, b, d);
+    x3[(long)i * ldx + c] = a;
+    x3[(long)(32 + i) * ldx + c] = b;
+    x3[(long)(64 + i) * ldx + c] = d;
+  }
+}
+
+int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, cudaStream_t st) {
+  dim3 grid(ceil_div(ldx, 256) > 64 ? 64 : ceil_div(ldx, 256), 32);
+  split3_kernel<<<grid, 256, 0, st>>>(x, m, cols, ld, reinterpret_cast<__nv_bfloat16*>(x3), ldx);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("split3_kernel");
+  return PKV_OK;
+}
+
+// RMSNorm of each row in float64 (reference tensor.py:78-86), output fp32 and/or
+// the bf16 3-way split (rows >= m of X3 are zero-filled by this kernel).
+__global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const float* gain, double eps, float* y,
+                               __nv_bfloat16* x3, long ldx, __nv_bfloat16* ybf) {
+  const int i = blockIdx.x;
+  __shared__ double red[32];
+  double acc = 0.0;
+  if (i < m) {
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      double v = (double)h[(long)i * ld + c];
+      acc += v * v;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double inv = 1.0 / sqrt(red[0] / (double)D + eps);
+  const long width = x3 ? ldx : ld;
+  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+    float out = 0.f;
+    if (i < m && c < D) out = (float)((double)h[(long)i * ld + c] * inv * (double)gain[c]);
+    if (y && c < ld) y[(long)i * ld + c] = out;
+    if (ybf && c < ld) ybf[(long)i * ld + c] = __float2bfloat16_rn(out);
+    if (x3) {
+      __nv_bfloat16 a, b, d;
+      split3(out, a, b, d);
+      x3[(long)i * ldx + c] = a;
+      x3[(long)(32 + i) * ldx + c] = b;
+      x3[(long)(64 + i) * ldx + c] = d;
+    }
+  }
+}
+
+// rows = max(m, 32) blocks when x3 is given so that the padding rows get zeros
+int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
+                   void* ybf, cudaStream_t st) {
+  int rows = x3 ? 32 : m;
+  if (rows <= 0) return PKV_OK;
+  rmsnorm_kernel<<<rows, 256, 0, st>>>(h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
+                                       reinterpret_cast<__nv_bfloat16*>(ybf));
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("rmsnorm_kernel");
+  return PKV_OK;
+}
+
+// split-K partials P [splits][N][96] -> Y[i][n] (mode 0: store, 1: += residual)
+__global__ void splitk_reduce_kernel(const float* part, int splits, int N, int m, float* y, long ldy, int mode) {
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)N * m) return;
+  const int i = (int)(gid / N);
+  const int n = (int)(gid - (long)i * N);
+  float acc = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float* p = part + ((long)s * N + n) * 96;
+    acc += (p[i] + p[32 + i]) + p[64 + i];
+  }
+  float* dst = y + (long)i * ldy + n;
+  if (mode == 1) *dst = *dst + acc;
+  else *dst = acc;
+}
+
+int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, long ldy, int mode, cudaStream_t st) {
+  const long total = (long)N * m;
+  splitk_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(part, splits, N, m, y, ldy, mode);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("splitk_reduce_kernel");
+  return PKV_OK;
+}
+
+// ------------------------------------------------------------ q/k/v of queries
+// qkv fp32 [m][NQKV] (padded-head layout) -> rotated q [m][H][dkp], k [m][Hkv][dkp],
+// v [m][Hkv][dkp] at positions pos0 + i; optionally append k/v (bf16) to the cache
+// pool and emit the fp32 fresh K/V as the reference returns them ([m][Hkv][dk]).
+__global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0,
+                                 const double* rcos, const double* rsin, float* q, float* k, float* v,
+                                 __nv_bfloat16* k_pool, __nv_bfloat16* v_pool, long pool_tokens,
+                                 const int32_t* page_table, float* fresh_k, float* fresh_v) {
+  const int heads = H + 2 * Hkv;
+  const long total = (long)m * heads * (dkp / 2);
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= total) return;
+  const int pi = (int)(gid % (dkp / 2));
+  const long rh = gid / (dkp / 2);
+  const int hh = (int)(rh % heads);
+  const int i = (int)(rh / heads);
+  const int pos = pos0 + i;
+  const float* src = qkv + ((long)i * heads + hh) * dkp + 2 * pi;
+  float e = src[0], o = src[1];
+  const bool is_v = hh >= H + Hkv;
+  if (!is_v && 2 * pi < dk) {
+    const int half = dk >> 1;
+    double c = rcos[(long)pos * half + pi], s = rsin[(long)pos * half + pi];
+    double de = e, dd = o;
+    float re = (float)__dsub_rn(__dmul_rn(de, c), __dmul_rn(dd, s));
+    float ro = (float)__dadd_rn(__dmul_rn(de, s), __dmul_rn(dd, c));
+    e = re;
+    o = ro;
+  }
+  if (hh < H) {
+    float* d = q + ((long)i * H + hh) * dkp + 2 * pi;
+    d[0] = e;
+    d[1] = o;
+    return;
+  }
+  const int g = is_v ? hh - H - Hkv : hh - H;
+  float* d = (is_v ? v : k) + ((long)i * Hkv + g) * dkp + 2 * pi;
+  d[0] = e;
+  d[1] = o;
+  if (k_pool != nullptr) {
+    const long slot = (long)page_table[pos >> 7] * 128 + (pos & 127);
+    __nv_bfloat16* pd = (is_v ? v_pool : k_pool) + ((long)g * pool_tokens + slot) * dkp + 2 * pi;
+    *reinterpret_cast<uint32_t*>(pd) = pack_bf16(e, o);
+  }
+  float* fr = is_v ? fresh_v : fresh_k;
+  if (fr != nullptr && 2 * pi < dk) {
+    float* fd = fr + ((long)i * Hkv + g) * dk + 2 * pi;
+    fd[0] = e;
+    fd[1] = o;
+  }
+}
+
+int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
+                     const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, cudaStream_t st) {
+  const long total = (long)m * (H + 2 * Hkv) * (dkp / 2);
+  query_qkv_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+      qkv, m, H, Hkv, dk, dkp, pos0, rcos, rsin, q, k, v, reinterpret_cast<__nv_bfloat16*>(k_pool),
+      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("query_qkv_kernel");
+  return PKV_OK;
+}
+
+// gate/up interleaved per 256 columns -> act = f32(silu64(gate)) * up
+// (reference model.py:260-262 and 318-321)
+__global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* act) {
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)m * Fp) return;
+  const int i = (int)(gid / Fp), f = (int)(gid - (long)i * Fp);
+  float a = 0.f;
+  if (f < F) {
+    const int b = f >> 7, j = f & 127;
+    const float g = gu[(long)i * 2 * Fp + b * 256 + j];
+    const float u = gu[(long)i * 2 * Fp + b * 256 + 128 + j];
+    const double gd = (double)g;
+    a = (float)(gd / (1.0 + exp(-gd))) * u;
+  }
+  act[gid] = a;
+}
+
+int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st) {
+  const long total = (long)m * Fp;
+  silu_act_kernel<<<ceil_div(total, 256), 256, 0, st>>>(gu, m, F, Fp, act);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("silu_act_kernel");
+  return PKV_OK;
+}
+
+// ------------------------------------------------------------ attention pass 1
+// One CTA: KV head g, a contiguous key range, up to 128 rows r = j*m + i (head
+// g*G + j, query i).  Keys t < s come from the chunk store (unrotated, rotated
+// here in float64 -- exactly the reference's keys_rebased) or from the cache
+// pool; keys s..s+m-1 are the queries' own fresh K/V.  Scores (already scaled,
+// masked -> -inf) are written to S[g][r][t] for the scoring reduction; per-split
+// online-softmax partials (m, l, O) go to the combine kernel.
+
+template <int DKP>
+__global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
+  constexpr int LDQ = DKP + 4;
+  constexpr int NQ = DKP / 32;  // float4 groups of output dims per thread
+  extern __shared__ float sm[];
+  float* Qs = sm;                  // [128][LDQ]
+  float* Ks = Qs + 128 * LDQ;      // [32][LDQ]
+  float* Vs = Ks + 32 * LDQ;       // [32][LDQ]
+  float* Ps = Vs + 32 * LDQ;       // [128][33]
+  const int g = blockIdx.y;
+  const int split = blockIdx.x;
+  const int r0 = blockIdx.z * 128;
+  const int tid = threadIdx.x;
+  const int tx = tid & 7, ty = tid >> 3;
+
+  // Q rows of this block
+  for (int e = tid; e < 128 * (DKP / 4); e += 256) {
+    const int rr = e / (DKP / 4), c4 = e - rr * (DKP / 4);
+    const int r = r0 + rr;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < a.R) {
+      const int j = r / a.m, i = r - j * a.m;
+      v = *reinterpret_cast<const float4*>(a.q + ((long)i * a.H + g * a.G + j) * DKP + c4 * 4);
+    }
+    *reinterpret_cast<float4*>(Qs + rr * LDQ + c4 * 4) = v;
+  }
+
+  float mrow[4], lrow[4], o[4][NQ][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    mrow[x] = -INFINITY;
+    lrow[x] = 0.f;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[x][q][e] = 0.f;
+  }
+  int qi[4];  // query index of each of this thread's rows (for the causal part)
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int r = r0 + ty * 4 + x;
+    qi[x] = r < a.R ? r % a.m : -1;
+  }
+
+  const int k_begin = split * a.keys_per_split;
+  const int k_end = min(k_begin + a.keys_per_split, a.s_tot);
+  const int half = a.dk >> 1;
+
+  for (int t0 = k_begin; t0 < k_end; t0 += 32) {
+    __syncthreads();
+    // ---- K/V tile -> smem fp32
+    for (int e = tid; e < 32 * (DKP / 8); e += 256) {
+      const int kr = e / (DKP / 8), c8 = e - kr * (DKP / 8);
+      const int t = t0 + kr;
+      float kf[8], vf[8];
+      if (t < k_end && t < a.s) {
+        uint4 kraw, vraw;
+        const bool from_chunk = a.src_chunks && !(a.recomp != nullptr && a.recomp[t]);
+        if (from_chunk) {
+          const int ch = a.src_chunk[t], loc = a.src_local[t], tc = a.chunk_len[ch];
+          const long off = (((long)a.layer * tc + loc) * a.Hkv + g) * DKP + c8 * 8;
+          kraw = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.ck[ch]) + off);
+          vraw = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.cv[ch]) + off);
+        } else {
+          const long slot = (long)a.page_table[t >> 7] * 128 + (t & 127);
+          const long off = ((long)g * a.pool_tokens + slot) * DKP + c8 * 8;
+          kraw = *reinterpret_cast<const uint4*>(a.k_pool + off);
+          vraw = *reinterpret_cast<const uint4*>(a.v_pool + off);
+        }
+        const uint32_t kw[4] = {kraw.x, kraw.y, kraw.z, kraw.w};
+        const uint32_t vw[4] = {vraw.x, vraw.y, vraw.z, vraw.w};
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          float e0 = bf16_lo(kw[p]), e1 = bf16_hi(kw[p]);
+          const int pi = c8 * 4 + p;
+          if (from_chunk && pi < half) {
+            const double c = a.rcos[(long)t * half + pi], sn = a.rsin[(long)t * half + pi];
+            const double de = e0, dd = e1;
+            e0 = (float)__dsub_rn(__dmul_rn(de, c), __dmul_rn(dd, sn));
+            e1 = (float)__dadd_rn(__dmul_rn(de, sn), __dmul_rn(dd, c));
+          }
+          kf[2 * p] = e0;
+          kf[2 * p + 1] = e1;
+          vf[2 * p] = bf16_lo(vw[p]);
+          vf[2 * p + 1] = bf16_hi(vw[p]);
+        }
+      } else if (t < k_end) {
+        const int i = t - a.s;
+        const float* ks = a.fk + ((long)i * a.Hkv + g) * DKP + c8 * 8;
+        const float* vs = a.fv + ((long)i * a.Hkv + g) * DKP + c8 * 8;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+          kf[p] = ks[p];
+          vf[p] = vs[p];
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) kf[p] = vf[p] = 0.f;
+      }
+      float* kd = Ks + kr * LDQ + c8 * 8;
+      float* vd = Vs + kr * LDQ + c8 * 8;
+      *reinterpret_cast<float4*>(kd) = make_float4(kf[0], kf[1], kf[2], kf[3]);
+      *reinterpret_cast<float4*>(kd + 4) = make_float4(kf[4], kf[5], kf[6], kf[7]);
+      *reinterpret_cast<float4*>(vd) = make_float4(vf[0], vf[1], vf[2], vf[3]);
+      *reinterpret_cast<float4*>(vd + 4) = make_float4(vf[4], vf[5], vf[6], vf[7]);
+    }
+    __syncthreads();
+
+    // ---- scores: rows ty*4+x, keys b*8+tx
+    float acc[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[x][b] = 0.f;
+#pragma unroll 4
+    for (int d = 0; d < DKP; d += 4) {
+      float4 qv[4], kv[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) qv[x] = *reinterpret_cast<const float4*>(Qs + (ty * 4 + x) * LDQ + d);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) kv[b] = *reinterpret_cast<const float4*>(Ks + (b * 8 + tx) * LDQ + d);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          acc[x][b] = fmaf(qv[x].x, kv[b].x, acc[x][b]);
+          acc[x][b] = fmaf(qv[x].y, kv[b].y, acc[x][b]);
+          acc[x][b] = fmaf(qv[x].z, kv[b].z, acc[x][b]);
+          acc[x][b] = fmaf(qv[x].w, kv[b].w, acc[x][b]);
+        }
+    }
+    // ---- scale, mask, store S, online softmax
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int r = r0 + ty * 4 + x;
+      float tmax = -INFINITY;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int t = t0 + b * 8 + tx;
+        const bool vis = qi[x] >= 0 && t < k_end && (t < a.s || (t - a.s) <= qi[x]);
+        const float sv = vis ? acc[x][b] * a.scale : -INFINITY;
+        acc[x][b] = sv;
+        if (a.S != nullptr && r < a.R && t < k_end) a.S[((long)g * a.R + r) * a.s_tot + t] = sv;
+        tmax = fmaxf(tmax, sv);
+      }
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+      const float m_new = fmaxf(mrow[x], tmax);
+      const float corr = (mrow[x] == -INFINITY) ? 0.f : expf(mrow[x] - m_new);
+      float psum = 0.f;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float p = (acc[x][b] == -INFINITY) ? 0.f : expf(acc[x][b] - m_new);
+        psum += p;
+        Ps[(ty * 4 + x) * 33 + b * 8 + tx] = p;
+      }
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, off);
+      if (m_new != -INFINITY) {
+        lrow[x] = lrow[x] * corr + psum;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[x][q][e] *= corr;
+        mrow[x] = m_new;
+      }
+    }
+    __syncthreads();
+    // ---- O += P V : rows ty*4+x, dims tx*4 + 32q + e
+#pragma unroll 4
+    for (int c = 0; c < 32; ++c) {
+      float p[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) p[x] = Ps[(ty * 4 + x) * 33 + c];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 vv = *reinterpret_cast<const float4*>(Vs + c * LDQ + tx * 4 + 32 * q);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          o[x][q][0] = fmaf(p[x], vv.x, o[x][q][0]);
+          o[x][q][1] = fmaf(p[x], vv.y, o[x][q][1]);
+          o[x][q][2] = fmaf(p[x], vv.z, o[x][q][2]);
+          o[x][q][3] = fmaf(p[x], vv.w, o[x][q][3]);
+        }
+      }
+    }
+  }
+  // ---- partials
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int r = r0 + ty * 4 + x;
+    if (r >= a.R) continue;
+    const long base = ((long)split * a.Hkv + g) * a.R + r;
+    float* od = a.Opart + base * DKP;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      *reinterpret_cast<float4*>(od + tx * 4 + 32 * q) = make_float4(o[x][q][0], o[x][q][1], o[x][q][2], o[x][q][3]);
+    if (tx == 0) {
+      a.Mpart[base] = mrow[x];
+      a.Lpart[base] = lrow[x];
+    }
+  }
+}
+
+// combine split partials -> attention output [m][H][dkp] fp32 and the final
+// per-row (max, denominator) used by the scoring reduction
+__global__ void s1_attn_combine(const float* Opart, const float* Mpart, const float* Lpart, int splits, int Hkv,
+                                int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin) {
+  const int r = blockIdx.x, g = blockIdx.y;
+  float M = -INFINITY;
+  for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, Mpart[((long)sp * Hkv + g) * R + r]);
+  float L = 0.f;
+  for (int sp = 0; sp < splits; ++sp) {
+    const long b = ((long)sp * Hkv + g) * R + r;
+    if (Mpart[b] != -INFINITY) L += Lpart[b] * expf(Mpart[b] - M);
+  }
+  const int j = r / m, i = r - j * m;
+  for (int d = threadIdx.x; d < dkp; d += blockDim.x) {
+    float acc = 0.f;
+    for (int sp = 0; sp < splits; ++sp) {
+      const long b = ((long)sp * Hkv + g) * R + r;
+      if (Mpart[b] != -INFINITY) acc += Opart[b * dkp + d] * expf(Mpart[b] - M);
+    }
+    out[((long)i * H + g * G + j) * dkp + d] = acc / L;
+  }
+  if (threadIdx.x == 0 && Mfin != nullptr) {
+    Mfin[(long)g * R + r] = M;
+    Lfin[(long)g * R + r] = L;
+  }
+}
+
+// head-mean rows over the context (model.py:294, 303-307):
+//   rows[i][t] = f32( sum_h f64(p_{h,i,t}) / H ),  p = exp(S - M) / L
+__global__ void s1_rows_kernel(const float* S, const float* Mfin, const float* Lfin, int Hkv, int G, int R, int m,
+                               int s, int s_tot, float* rows) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (t >= s) return;
+  double acc = 0.0;
+  for (int g = 0; g < Hkv; ++g)
+    for (int j = 0; j < G; ++j) {
+      const int r = j * m + i;
+      const long rr = (long)g * R + r;
+      const float p = expf(S[rr * s_tot + t] - Mfin[rr]) / Lfin[rr];
+      acc += (double)p;
+    }
+  rows[(long)i * s + t] = (float)(acc / (double)(Hkv * G));
+}
+
+// optional context-only renormalisation denominators (selection.py:80-84)
+__global__ void s1_row_sums_kernel(const float* rows, int s, double* denom) {
+  const int i = blockIdx.x;
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < s; t += blockDim.x) acc += (double)rows[(long)i * s + t];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w];
+    denom[i] = v > 1e-30 ? v : 1e-30;
+  }
+}
+
+// per_layer[t] = f32( mean_i f64(rows[i][t]) )  (selection.py:79-86)
+__global__ void s1_query_mean_kernel(const float* rows, const double* denom, int m, int s, float* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= s) return;
+  double acc = 0.0;
+  for (int i = 0; i < m; ++i) {
+    double v = (double)rows[(long)i * s + t];
+    if (denom) v = v / denom[i];
+    acc += v;
+  }
+  out[t] = (float)(acc / (double)m);
+}
+
+int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
+                        float* per_layer, int renorm, cudaStream_t st) {
+  S1Attn a = a_in;
+  const int row_blocks = ceil_div(a.R, 128);
+  dim3 grid(a.n_splits, a.Hkv, row_blocks);
+  const int smem = (128 * (a.dkp + 4) + 2 * 32 * (a.dkp + 4) + 128 * 33) * 4;
+  if (a.dkp == 128) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(s1_attn_pass1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+    });
+    s1_attn_pass1<128><<<grid, 256, smem, st>>>(a);
+  } else if (a.dkp == 64) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(s1_attn_pass1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+    });
+    s1_attn_pass1<64><<<grid, 256, smem, st>>>(a);
+  } else {
+    return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", a.dkp);
+  }
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("s1_attn_pass1");
+  s1_attn_combine<<<dim3(a.R, a.Hkv), 128, 0, st>>>(a.Opart, a.Mpart, a.Lpart, a.n_splits, a.Hkv, a.R, a.m, a.G, a.H,
+                                                    a.dkp, attn_out, Mfin, Lfin);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("s1_attn_combine");
+  if (a.S != nullptr && per_layer != nullptr) {
+    s1_rows_kernel<<<dim3(ceil_div(a.s, 256), a.m), 256, 0, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s,
+                                                                   a.s_tot, rows);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("s1_rows_kernel");
+    if (renorm) {
+      s1_row_sums_kernel<<<a.m, 256, 0, st>>>(rows, a.s, denom);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_row_sums_kernel");
+    }
+    s1_query_mean_kernel<<<ceil_div(a.s, 256), 256, 0, st>>>(rows, renorm ? denom : nullptr, a.m, a.s, per_layer);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("s1_query_mean_kernel");
+  }
+  return PKV_OK;
+}
+
+// ------------------------------------------------------------------ lm_head
+// logits[n] = dot(x, W[n]) over D, fp32 accumulation (x = final-normed last row)
+__global__ void gemv_rows_kernel(const float* x, const __nv_bfloat16* W, int N, int D, long ldw, float* out) {
+  extern __shared__ float xs[];
+  for (int c = threadIdx.x; c < D; c += blockDim.x) xs[c] = x[c];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int n = blockIdx.x * wpb + warp; n < N; n += gridDim.x * wpb) {
+    const __nv_bfloat16* w = W + (long)n * ldw;
+    float acc = 0.f;
+    for (int c = lane * 8; c < D; c += 256) {
+      const uint4 u = *reinterpret_cast<const uint4*>(w + c);
+      const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        if (c + 2 * p < D) acc = fmaf(xs[c + 2 * p], bf16_lo(uw[p]), acc);
+        if (c + 2 * p + 1 < D) acc = fmaf(xs[c + 2 * p + 1], bf16_hi(uw[p]), acc);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[n] = acc;
+  }
+}
+
+int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st) {
+  const int blocks = std::min(ceil_div(N, 8), num_sms() * 8);
+  gemv_rows_kernel<<<blocks, 256, D * sizeof(float), st>>>(x, reinterpret_cast<const __nv_bfloat16*>(W), N, D, ldw,
+                                                           out);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("gemv_rows_kernel");
+  return PKV_OK;
+}
+
+// embedding rows (bf16 table) -> fp32 [n][ld]
+__global__ void embed_gather_kernel(const __nv_bfloat16* embed, long lde, const int32_t* ids, const int32_t* sel,
+                                    int n, int D, float* out, long ldo) {
+  const int r = blockIdx.x;
+  if (r >= n) return;
+  const int tok = sel ? ids[sel[r]] : ids[r];
+  for (int c = threadIdx.x; c < ldo; c += blockDim.x)
+    out[(long)r * ldo + c] = c < D ? __bfloat162float(embed[(long)tok * lde + c]) : 0.f;
+}
+
+int embed_gather_launch(const void* embed, long lde, const int32_t* ids, const int32_t* sel, int n, int D, float* out,
+                        long ldo, cudaStream_t st) {
+  if (n <= 0) return PKV_OK;
+  embed_gather_kernel<<<n, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(embed), lde, ids, sel, n, D, out, ldo);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("embed_gather_kernel");
+  return PKV_OK;
+}
+
+}  // namespace pkv

@@ -1,0 +1,400 @@
+"""Model types of the drop-in and their B200 device image.
+
+Host-side types keep the reference ``pikv.model`` surface (ModelConfig,
+LayerWeights, ModelWeights, random_weights, FlopTally, KVCache -- reference
+model.py:24-228) so caller code constructs them unchanged.  ``DeviceModel`` is the
+B200 image: bf16 weights transposed to output-major rows, head dims padded to the
+kernel tile (see include/pkv.h "Device layouts"), plus the C-ABI model handle.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConfigError, EngineError
+
+F32 = np.float32
+F64 = np.float64
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Shape contract; validation mirrors reference model.py:36-50."""
+
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    hidden_dim: int
+    ffn_dim: int
+    vocab_size: int
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+
+    def __post_init__(self) -> None:
+        dims = (self.n_layers, self.n_heads, self.n_kv_heads, self.head_dim, self.ffn_dim, self.vocab_size)
+        if min(dims) <= 0:
+            raise ConfigError("all model dimensions must be positive")
+        if self.n_heads % self.n_kv_heads:
+            raise ConfigError(f"n_heads={self.n_heads} not divisible by n_kv_heads={self.n_kv_heads}")
+        if self.hidden_dim != self.n_heads * self.head_dim:
+            raise ConfigError(f"hidden_dim={self.hidden_dim} != n_heads*head_dim={self.n_heads * self.head_dim}")
+        if self.head_dim % 2:
+            raise ConfigError(f"head_dim must be even for rotary pairs, got {self.head_dim}")
+        if self.rope_theta <= 0 or self.norm_eps <= 0:
+            raise ConfigError("rope_theta and norm_eps must be positive")
+
+    @property
+    def kv_dim(self) -> int:
+        return self.n_kv_heads * self.head_dim
+
+    def to_json_dict(self) -> dict:
+        return {k: getattr(self, k) for k in ("n_layers", "n_heads", "n_kv_heads", "head_dim", "hidden_dim",
+                                              "ffn_dim", "vocab_size", "rope_theta", "norm_eps")}
+
+    def c_struct(self) -> _lib.Config:
+        return _lib.Config(self.n_layers, self.n_heads, self.n_kv_heads, self.head_dim, self.hidden_dim,
+                           self.ffn_dim, self.vocab_size, float(self.rope_theta), float(self.norm_eps))
+
+    def layout(self) -> "Layout":
+        return Layout.of(self)
+
+
+@dataclass(frozen=True)
+class Layout:
+    """Padded device layout (pkv_layout): dkp, Dp, Fp, NQKV, HQ."""
+
+    dkp: int
+    Dp: int
+    Fp: int
+    NQKV: int
+    HQ: int
+
+    @staticmethod
+    def of(cfg: ModelConfig) -> "Layout":
+        if cfg.head_dim > 128:
+            raise ConfigError("head_dim > 128 is not supported by the sm_100a kernels")
+        dkp = 64 if cfg.head_dim <= 64 else 128
+        Dp = -(-cfg.hidden_dim // 64) * 64
+        Fp = -(-cfg.ffn_dim // 128) * 128
+        return Layout(dkp, Dp, Fp, (cfg.n_heads + 2 * cfg.n_kv_heads) * dkp, cfg.n_heads * dkp)
+
+
+@dataclass
+class LayerWeights:
+    attn_norm: np.ndarray   # [hidden]
+    wq: np.ndarray          # [hidden, n_heads*head_dim]
+    wk: np.ndarray          # [hidden, kv_dim]
+    wv: np.ndarray          # [hidden, kv_dim]
+    wo: np.ndarray          # [n_heads*head_dim, hidden]
+    ffn_norm: np.ndarray    # [hidden]
+    w_gate: np.ndarray      # [hidden, ffn]
+    w_up: np.ndarray        # [hidden, ffn]
+    w_down: np.ndarray      # [ffn, hidden]
+
+
+@dataclass
+class ModelWeights:
+    """Host weights, input-major like the reference (model.py:79-160)."""
+
+    embed: np.ndarray
+    layers: list
+    final_norm: np.ndarray
+    lm_head: np.ndarray
+    _fingerprint: str | None = field(default=None, repr=False, compare=False)
+    _device: dict = field(default_factory=dict, repr=False, compare=False)
+
+    def validate(self, config: ModelConfig) -> None:
+        h, kv, hd = config.hidden_dim, config.kv_dim, config.n_heads * config.head_dim
+        if self.embed.shape != (config.vocab_size, h):
+            raise ConfigError(f"embed shape {self.embed.shape} does not match config")
+        if len(self.layers) != config.n_layers:
+            raise ConfigError(f"{len(self.layers)} layer weight sets for {config.n_layers} layers")
+        want = {"attn_norm": (h,), "wq": (h, hd), "wk": (h, kv), "wv": (h, kv), "wo": (hd, h), "ffn_norm": (h,),
+                "w_gate": (h, config.ffn_dim), "w_up": (h, config.ffn_dim), "w_down": (config.ffn_dim, h)}
+        for i, lw in enumerate(self.layers):
+            for name, shape in want.items():
+                if getattr(lw, name).shape != shape:
+                    raise ConfigError(f"layers.{i}.{name} shape {getattr(lw, name).shape}, expected {shape}")
+        if self.final_norm.shape != (h,) or self.lm_head.shape != (h, config.vocab_size):
+            raise ConfigError("final_norm / lm_head shape mismatch")
+
+    def named_tensors(self) -> list:
+        out = [("embed.weight", self.embed)]
+        for i, lw in enumerate(self.layers):
+            p = f"layers.{i}"
+            out += [(f"{p}.attn_norm.gain", lw.attn_norm), (f"{p}.attn.wq", lw.wq), (f"{p}.attn.wk", lw.wk),
+                    (f"{p}.attn.wv", lw.wv), (f"{p}.attn.wo", lw.wo), (f"{p}.ffn_norm.gain", lw.ffn_norm),
+                    (f"{p}.ffn.w_gate", lw.w_gate), (f"{p}.ffn.w_up", lw.w_up), (f"{p}.ffn.w_down", lw.w_down)]
+        return out + [("final_norm.gain", self.final_norm), ("lm_head.weight", self.lm_head)]
+
+    def fingerprint(self, config: ModelConfig) -> str:
+        """blake2b-8 of config JSON + weight bytes (reference model.py:147-160)."""
+        if self._fingerprint is None:
+            h = hashlib.blake2b(digest_size=8)
+            h.update(json.dumps(config.to_json_dict(), sort_keys=True).encode())
+            for name, t in self.named_tensors():
+                h.update(name.encode())
+                h.update(np.ascontiguousarray(t, dtype=F32).tobytes())
+            self._fingerprint = h.hexdigest()
+        return self._fingerprint
+
+    def device(self, config: ModelConfig) -> "DeviceModel":
+        """The cached B200 image of these weights (uploaded once)."""
+        dm = self._device.get("dm")
+        if dm is None:
+            dm = DeviceModel.from_host(self, config)
+            self._device["dm"] = dm
+        return dm
+
+
+def random_weights(config: ModelConfig, seed: int) -> ModelWeights:
+    """Seeded host weights; same PCG64 stream and scaling as reference model.py:163-185."""
+    rng = np.random.default_rng(seed)
+
+    def mat(rows, cols):
+        return (rng.standard_normal((rows, cols)) / np.sqrt(rows)).astype(F32)
+
+    h, hd, kv, f = config.hidden_dim, config.n_heads * config.head_dim, config.kv_dim, config.ffn_dim
+    layers = []
+    for _ in range(config.n_layers):
+        wq, wk, wv, wo = mat(h, hd), mat(h, kv), mat(h, kv), mat(hd, h)
+        wg, wu, wd = mat(h, f), mat(h, f), mat(f, h)
+        layers.append(LayerWeights(np.ones(h, F32), wq, wk, wv, wo, np.ones(h, F32), wg, wu, wd))
+    embed = rng.standard_normal((config.vocab_size, h)).astype(F32)
+    return ModelWeights(embed=embed, layers=layers, final_norm=np.ones(h, F32), lm_head=mat(h, config.vocab_size))
+
+
+@dataclass
+class FlopCounter:
+    """Monotonic multiply-accumulate counter (reference tensor.py:37-46)."""
+
+    multiply_accumulate_count: int = 0
+
+    def add(self, n: int) -> None:
+        from .errors import ArgumentError
+        if n < 0:
+            raise ArgumentError(f"flop increment must be >= 0, got {n}")
+        self.multiply_accumulate_count += n
+
+
+@dataclass
+class FlopTally:
+    """MAC books (reference model.py:188-193), filled analytically by the device path."""
+
+    total: FlopCounter = field(default_factory=FlopCounter)
+    attn_scores: FlopCounter = field(default_factory=FlopCounter)
+
+
+def bill_query_pass(tally, config: ModelConfig, s: int, m: int, with_logits: bool = True) -> None:
+    """Books of one narrow pass of m tokens over s entries, as the reference's
+    matmul-level counting produces them."""
+    if tally is None:
+        return
+    H, dk, D, F, KV = config.n_heads, config.head_dim, config.hidden_dim, config.ffn_dim, config.kv_dim
+    t = s + m
+    per = m * D * (H * dk + 2 * KV) + 2 * H * m * dk * t + m * H * dk * D + 3 * m * D * F
+    tally.total.add(config.n_layers * per + (m * D * config.vocab_size if with_logits else 0))
+    tally.attn_scores.add(config.n_layers * H * m * dk * t)
+
+
+def bill_repair(tally, config: ModelConfig, s: int, k: int) -> None:
+    """Books of the Stage-II repair of k tokens (dense k x s attention billing)."""
+    if tally is None or k == 0:
+        return
+    H, dk, D, F, KV = config.n_heads, config.head_dim, config.hidden_dim, config.ffn_dim, config.kv_dim
+    per = k * D * (H * dk + 2 * KV) + 2 * H * k * dk * s + k * H * dk * D + 3 * k * D * F
+    tally.total.add(config.n_layers * per)
+    tally.attn_scores.add(config.n_layers * H * k * dk * s)
+
+
+class KVCache:
+    """Context + query K/V handed to decoding (reference model.py:208-228).
+
+    Device-backed: ``keys``/``values`` materialise per-layer f32 arrays lazily.
+    """
+
+    def __init__(self, keys, values, positions, last_logits=None):
+        self._keys = keys
+        self._values = values
+        self.positions = positions
+        self.last_logits = last_logits
+
+    @property
+    def keys(self):
+        return self._keys() if callable(self._keys) else self._keys
+
+    @property
+    def values(self):
+        return self._values() if callable(self._values) else self._values
+
+    @property
+    def length(self) -> int:
+        return int(self.positions.shape[0])
+
+
+# ---------------------------------------------------------------------------- device
+
+
+def _pad2(t, rows, cols):
+    import torch
+    out = torch.zeros((rows, cols), dtype=t.dtype, device=t.device)
+    out[: t.shape[0], : t.shape[1]] = t
+    return out
+
+
+class DeviceModel:
+    """bf16 device weights in the kernel layout + the C-ABI model handle."""
+
+    def __init__(self, config: ModelConfig, tensors: dict, fingerprint: str):
+        torch = _lib.require_cuda()
+        self.config = config
+        self.lay = Layout.of(config)
+        self.fingerprint = fingerprint
+        self.t = tensors  # keeps device memory alive
+        L = config.n_layers
+        self._layers = (_lib.LayerWeights * L)()
+        for i in range(L):
+            lt = tensors["layers"][i]
+            self._layers[i] = _lib.LayerWeights(lt["attn_norm"].data_ptr(), lt["ffn_norm"].data_ptr(),
+                                                lt["wqkv"].data_ptr(), lt["wo"].data_ptr(), lt["wgu"].data_ptr(),
+                                                lt["wd"].data_ptr())
+        self._w = _lib.Weights(tensors["embed"].data_ptr(), tensors["final_norm"].data_ptr(),
+                               tensors["lm_head"].data_ptr(), self._layers)
+        self._cfg = config.c_struct()
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().pkv_model_create(ctypes.byref(self._cfg), ctypes.byref(self._w), ctypes.byref(h)))
+        self.handle = h
+        self.device = tensors["embed"].device
+        del torch
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _lib.load().pkv_model_destroy(self.handle)
+        except Exception:
+            pass
+
+    @property
+    def cfg_ptr(self):
+        return ctypes.byref(self._cfg)
+
+    # -- construction ---------------------------------------------------------
+    @classmethod
+    def from_host(cls, weights: ModelWeights, config: ModelConfig, device=None) -> "DeviceModel":
+        """Upload reference-layout f32 weights, rounding to bf16 (RNE)."""
+        torch = _lib.require_cuda()
+        weights.validate(config)
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        lay = Layout.of(config)
+        H, Hkv, dk = config.n_heads, config.n_kv_heads, config.head_dim
+        bf = torch.bfloat16
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=F32)).to(dev)
+
+        def heads_rows(w, n_h):  # [D, n_h*dk] -> [n_h*dkp, Dp] (transposed, padded per head)
+            t = up(w).t().reshape(n_h, dk, -1)
+            out = torch.zeros((n_h, lay.dkp, lay.Dp), dtype=torch.float32, device=dev)
+            out[:, :dk, : config.hidden_dim] = t
+            return out.reshape(n_h * lay.dkp, lay.Dp)
+
+        def norm(g):
+            out = torch.zeros(lay.Dp, dtype=torch.float32, device=dev)
+            out[: config.hidden_dim] = up(g)
+            return out
+
+        layers = []
+        for lw in weights.layers:
+            wqkv = torch.cat([heads_rows(lw.wq, H), heads_rows(lw.wk, Hkv), heads_rows(lw.wv, Hkv)]).to(bf)
+            wo = up(lw.wo).t().reshape(config.hidden_dim, H, dk)
+            wo_p = torch.zeros((lay.Dp, H, lay.dkp), dtype=torch.float32, device=dev)
+            wo_p[: config.hidden_dim, :, :dk] = wo
+            g = _pad2(up(lw.w_gate).t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
+            u = _pad2(up(lw.w_up).t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
+            wgu = torch.stack([g, u], dim=1).reshape(2 * lay.Fp, lay.Dp).to(bf)
+            wd = _pad2(up(lw.w_down).t(), lay.Dp, lay.Fp).to(bf)
+            layers.append({"attn_norm": norm(lw.attn_norm), "ffn_norm": norm(lw.ffn_norm), "wqkv": wqkv.contiguous(),
+                           "wo": wo_p.reshape(lay.Dp, lay.HQ).to(bf).contiguous(), "wgu": wgu.contiguous(),
+                           "wd": wd.contiguous()})
+        tensors = {"layers": layers,
+                   "embed": _pad2(up(weights.embed), config.vocab_size, lay.Dp).to(bf).contiguous(),
+                   "lm_head": _pad2(up(weights.lm_head).t(), config.vocab_size, lay.Dp).to(bf).contiguous(),
+                   "final_norm": norm(weights.final_norm)}
+        return cls(config, tensors, weights.fingerprint(config))
+
+    @classmethod
+    def random(cls, config: ModelConfig, seed: int = 0, device=None) -> "DeviceModel":
+        """Random-init bf16 weights generated on the device (benchmarks; the layout
+        matches from_host, the values follow the reference's N(0,1)/sqrt(fan_in))."""
+        torch = _lib.require_cuda()
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        lay = Layout.of(config)
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        bf = torch.bfloat16
+        D, F, dk, H, Hkv = config.hidden_dim, config.ffn_dim, config.head_dim, config.n_heads, config.n_kv_heads
+
+        def rnd(rows, cols, fan_in, real_rows, real_cols):
+            t = torch.zeros((rows, cols), dtype=bf, device=dev)
+            t[:real_rows, :real_cols] = (torch.randn((real_rows, real_cols), generator=g, device=dev,
+                                                     dtype=torch.float32) / fan_in ** 0.5).to(bf)
+            return t
+
+        ones = torch.zeros(lay.Dp, dtype=torch.float32, device=dev)
+        ones[:D] = 1.0
+        layers = []
+        for _ in range(config.n_layers):
+            if dk == lay.dkp and D == lay.Dp:
+                wqkv = (torch.randn((lay.NQKV, D), generator=g, device=dev) / D ** 0.5).to(bf)
+            else:
+                wqkv = torch.zeros((H + 2 * Hkv, lay.dkp, lay.Dp), dtype=bf, device=dev)
+                wqkv[:, :dk, :D] = (torch.randn((H + 2 * Hkv, dk, D), generator=g, device=dev) / D ** 0.5).to(bf)
+                wqkv = wqkv.reshape(lay.NQKV, lay.Dp)
+            wo = rnd(lay.Dp, lay.HQ, H * dk, D, lay.HQ)
+            if dk != lay.dkp:
+                wo.view(lay.Dp, H, lay.dkp)[:, :, dk:] = 0
+            layers.append({"attn_norm": ones.clone(), "ffn_norm": ones.clone(), "wqkv": wqkv.contiguous(), "wo": wo,
+                           "wgu": rnd(2 * lay.Fp, lay.Dp, D, 2 * lay.Fp, D), "wd": rnd(lay.Dp, lay.Fp, F, D, F)})
+        embed = torch.zeros((config.vocab_size, lay.Dp), dtype=bf, device=dev)
+        embed[:, :D] = torch.randn((config.vocab_size, D), generator=g, device=dev).to(bf)
+        tensors = {"layers": layers, "embed": embed, "lm_head": rnd(config.vocab_size, lay.Dp, D, config.vocab_size, D),
+                   "final_norm": ones.clone()}
+        return cls(config, tensors, f"device-random-{seed}")
+
+    def weight_bytes(self, include_head: bool = True) -> int:
+        n = 0
+        for lt in self.t["layers"]:
+            n += sum(lt[k].numel() * lt[k].element_size() for k in ("wqkv", "wo", "wgu", "wd"))
+        if include_head:
+            n += self.t["lm_head"].numel() * 2
+        return n
+
+
+def resolve_device_model(weights, config: ModelConfig) -> DeviceModel:
+    """Accept either host ModelWeights (uploaded once, cached) or a DeviceModel."""
+    if isinstance(weights, DeviceModel):
+        return weights
+    if isinstance(weights, ModelWeights):
+        return weights.device(config)
+    # reference pikv.ModelWeights (duck-typed): same field names
+    if hasattr(weights, "layers") and hasattr(weights, "embed"):
+        cache = getattr(weights, "__b200_device__", None)
+        if cache is None:
+            mw = ModelWeights(embed=weights.embed, layers=[LayerWeights(**{k: getattr(lw, k) for k in (
+                "attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")})
+                for lw in weights.layers], final_norm=weights.final_norm, lm_head=weights.lm_head)
+            cache = DeviceModel.from_host(mw, config)
+            cache.fingerprint = weights.fingerprint(config) if hasattr(weights, "fingerprint") else cache.fingerprint
+            try:
+                weights.__b200_device__ = cache
+            except AttributeError:
+                pass
+        return cache
+    raise EngineError(f"unsupported weights object {type(weights)!r}")

@@ -1,0 +1,196 @@
+"""Stage II repair and query finalisation on the GPU.
+
+Drop-in for reference recompute.py (RecomputePlan 35-40, recompute_selected
+43-82, FinalizeResult 98-102, finalize_query 105-125, selection_digest 153-155,
+run_strategy 173-253).  Stage II runs through ``pkv_recompute``: per layer a
+tcgen05 QKV GEMM whose epilogue rotates q/k and scatters the fresh K/V into the
+paged cache, then the sparse-query tcgen05 attention over the updated layer,
+then o / gate-up(SiLU) / down GEMMs with fp32 residual epilogues.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .chunkstore import assemble, mark_finalized
+from .errors import ArgumentError, ConfigError, InputError, StateError
+from .model import FlopTally, KVCache, ModelConfig, bill_query_pass, bill_repair, resolve_device_model
+from .selection import (STRATEGIES, SelectionResult, ValueScores, check_tokens, run_query_pass, score_epic,
+                        score_prophet, score_random, select_top_p, workspace)
+
+
+@dataclass
+class RecomputePlan:
+    selection: SelectionResult
+    # the reference's stale-peer ablation (recompute.py:60-78) is not on the B200 path
+    stale_peers: bool = False
+
+
+def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
+                       tally: FlopTally | None = None):
+    """Repair the cache in place at the planned token set; returns the same object."""
+    torch = _lib.require_cuda()
+    if cache.finalized:
+        raise StateError("cannot repair a finalized cache")
+    if cache.recomputed.any():
+        raise StateError("cache was already repaired once")
+    if plan.stale_peers:
+        raise ConfigError("stale_peers ablation is not implemented on the B200 path")
+    sel = np.asarray(plan.selection.indices, dtype=np.int64)
+    if sel.size == 0:
+        return cache
+    if not np.all(np.diff(sel) > 0):
+        raise ArgumentError("selection indices must be strictly ascending")
+    if sel[0] < 0 or sel[-1] >= cache.context_length:
+        raise InputError("replacement index out of range")
+    dm = resolve_device_model(weights, config)
+    k = int(sel.size)
+    d_sel = plan.selection._dev_idx
+    if d_sel is None or int(d_sel.numel()) != k:
+        d_sel = torch.from_numpy(sel.astype(np.int32)).to(cache.device)
+    L, Hkv, dk = config.n_layers, config.n_kv_heads, config.head_dim
+    tap_k = tap_v = None
+    if cache.fp32_taps:
+        tap_k = torch.empty((L, k, Hkv, dk), dtype=torch.float32, device=cache.device)
+        tap_v = torch.empty_like(tap_k)
+    lib = _lib.load()
+    ws = workspace(lib.pkv_recompute_workspace(dm.handle, k), "rc")
+    _lib.check(lib.pkv_recompute(dm.handle, ctypes.byref(cache.c_cache), d_sel.data_ptr(), k,
+                                 tap_k.data_ptr() if tap_k is not None else None,
+                                 tap_v.data_ptr() if tap_v is not None else None, ws.data_ptr(), ws.numel(),
+                                 _lib.stream_ptr(torch)))
+    cache.recomputed[:, sel] = True
+    cache._d_recomp[d_sel.long()] = 1
+    if tap_k is not None:
+        for li in range(L):
+            cache.add_tap(li, sel, tap_k[li], tap_v[li])
+    if cache.access_log is not None:
+        for li in range(L):  # each layer writes its fresh K/V before its attention reads them
+            cache.access_log.append(("write", li))
+            cache.access_log.append(("read", li))
+    bill_repair(tally, config, cache.context_length, k)
+    return cache
+
+
+@dataclass
+class FinalizeResult:
+    cache: KVCache               # context + query, ready for decoding
+    first_logits: np.ndarray     # [vocab] at the last query position
+    rows: list | None
+
+
+def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_attn: bool = False,
+                   tally: FlopTally | None = None) -> FinalizeResult:
+    """Compute the query over the (repaired) cache and append its K/V entries.
+    One-shot per cache (reference recompute.py:105-125)."""
+    torch = _lib.require_cuda()
+    mark_finalized(cache)
+    dm = resolve_device_model(weights, config)
+    ids = check_tokens(query_tokens, config)
+    m = int(ids.shape[0])
+    if cache.access_log is not None:
+        cache.access_log.extend(("read", li) for li in range(config.n_layers))
+    L, Hkv, dk = config.n_layers, config.n_kv_heads, config.head_dim
+    fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
+    fv = torch.empty_like(fk)
+    logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
+    flags = _lib.PKV_QP_LOGITS | _lib.PKV_QP_APPEND_KV | _lib.PKV_QP_FROM_CHUNKS
+    run_query_pass(dm, cache, ids, flags, fresh_k=fk, fresh_v=fv, logits=logits)
+    cache.query_kv = (fk, fv)
+    bill_query_pass(tally, config, cache.context_length, m)
+    first = logits.cpu().numpy()
+    s = cache.context_length
+
+    def keys():
+        fkh = fk.cpu().numpy()
+        return [np.concatenate([cache.keys_rebased[li], fkh[li]], axis=0) for li in range(L)]
+
+    def values():
+        fvh = fv.cpu().numpy()
+        return [np.concatenate([cache.values[li], fvh[li]], axis=0) for li in range(L)]
+
+    kv = KVCache(keys=keys, values=values, positions=np.arange(s + m, dtype=np.int64), last_logits=first)
+    return FinalizeResult(cache=kv, first_logits=first, rows=None)
+
+
+def selection_digest(indices) -> str:
+    return hashlib.blake2b(np.asarray(sorted(indices), dtype=np.int64).tobytes(), digest_size=8).hexdigest()
+
+
+@dataclass
+class AnswerRecord:
+    task_id: str
+    strategy: str
+    p: float
+    answer_tokens: list
+    answer_text: str
+    exact_match: bool | None
+    semantic_loss: float
+    residual_loss: float
+    flops_stage1: int
+    flops_stage2: int
+    selected_indices: list
+    selection_digest: str
+
+    def to_json_line(self) -> str:
+        return json.dumps({"task_id": self.task_id, "strategy": self.strategy, "p": self.p,
+                           "answer_text": self.answer_text, "exact_match": self.exact_match,
+                           "semantic_loss": self.semantic_loss, "residual_loss": self.residual_loss,
+                           "flops_stage1": self.flops_stage1, "flops_stage2": self.flops_stage2,
+                           "selected_digest": self.selection_digest}, sort_keys=True)
+
+
+@dataclass
+class StrategyRun:
+    """The TTFT slice of one (strategy, budget) cell.  The reference's unbilled
+    measurement apparatus (full-prefill summaries, losses, greedy decoding --
+    recompute.py:194-206, 228-247) is outside the B200 hot path: those fields are
+    None and the losses NaN."""
+    record: AnswerRecord
+    selection: SelectionResult
+    scores: ValueScores
+    full_summary: object
+    naive_summary: object
+    repaired_summary: object
+    per_token_naive: object
+    generated: object
+    first_logits: np.ndarray
+
+
+def run_strategy(weights, config: ModelConfig, chunks, query_tokens, strategy: str, p: float, *, seed: int = 0,
+                 max_new_tokens: int = 16, stop_ids=(), gold_tokens=None, task_id: str = "",
+                 tokenizer=None) -> StrategyRun:
+    """assemble -> score -> select -> repair -> finalize (reference recompute.py:173-253)."""
+    if strategy not in STRATEGIES and strategy != "naive":
+        raise ArgumentError(f"unknown strategy {strategy!r}")
+    if strategy == "naive" and p != 0.0:
+        raise ConfigError("the naive baseline is only defined at p=0.0")
+    cache = assemble(chunks, config)
+    s = cache.context_length
+    query = list(query_tokens)
+    stage1 = FlopTally()
+    if strategy == "prophet":
+        scores = score_prophet(weights, config, cache, query, tally=stage1)
+    elif strategy == "epic":
+        scores = score_epic(cache, config.n_layers)
+    elif strategy == "random":
+        scores = score_random(s, seed, config.n_layers)
+    else:
+        scores = ValueScores.from_vector("naive", np.zeros(s, dtype=np.float32), config.n_layers)
+    sel = select_top_p(scores, p)
+    stage2 = FlopTally()
+    recompute_selected(weights, config, cache, RecomputePlan(sel), tally=stage2)
+    fin = finalize_query(weights, config, cache, query, tally=stage2)
+    record = AnswerRecord(task_id=task_id, strategy=strategy, p=p, answer_tokens=[], answer_text="",
+                          exact_match=None, semantic_loss=float("nan"), residual_loss=float("nan"),
+                          flops_stage1=stage1.total.multiply_accumulate_count,
+                          flops_stage2=stage2.total.multiply_accumulate_count, selected_indices=sel.indices,
+                          selection_digest=selection_digest(sel.indices))
+    return StrategyRun(record=record, selection=sel, scores=scores, full_summary=None, naive_summary=None,
+                       repaired_summary=None, per_token_naive=None, generated=None, first_logits=fin.first_logits)

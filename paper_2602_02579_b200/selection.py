@@ -1,0 +1,172 @@
+"""Stage I scoring, layer fusion and budgeted selection on the GPU.
+
+Drop-in for reference selection.py (ValueScores 25-42, SelectionResult 45-49,
+fuse_layers 52-54, select_top_p 57-61, score_prophet 64-86).  The static
+baselines (epic, random) are host one-liners kept for run_strategy
+compatibility; the probe baselines (cacheblend/kvshare) are out of scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ArgumentError, InputError, NumericsError, ShapeError
+from .model import F32, F64, FlopTally, ModelConfig, bill_query_pass, resolve_device_model
+from .tensor import device_topk, ratio_budget
+
+STRATEGIES = ("prophet", "epic", "random")
+
+
+def _host_layer_mean(per_layer: np.ndarray) -> np.ndarray:
+    return per_layer.astype(F64).mean(axis=0).astype(F32)
+
+
+@dataclass
+class ValueScores:
+    strategy: str
+    per_layer: np.ndarray   # [L, s]
+    fused: np.ndarray       # [s]
+    _dev_fused: object = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self) -> None:
+        if self.per_layer.ndim != 2:
+            raise ShapeError(f"per-layer scores must be [L, s], got {self.per_layer.shape}")
+        want = _host_layer_mean(self.per_layer)
+        if self.fused.shape != want.shape or not np.allclose(self.fused, want, atol=1e-6):
+            raise ArgumentError("fused scores must be the mean of the per-layer rows")
+
+    @classmethod
+    def from_vector(cls, strategy: str, vector, n_layers: int) -> "ValueScores":
+        v = np.asarray(vector, dtype=F32)
+        per_layer = np.repeat(v[None, :], n_layers, axis=0)
+        return cls(strategy=strategy, per_layer=per_layer, fused=_host_layer_mean(per_layer))
+
+
+@dataclass
+class SelectionResult:
+    indices: list   # ascending
+    p: float
+    k: int
+    _dev_idx: object = field(default=None, repr=False, compare=False)
+
+
+_WS: dict = {}
+
+
+def workspace(nbytes: int, tag: str = "ws"):
+    """Grow-only device scratch per (device, tag)."""
+    torch = _lib.require_cuda()
+    key = (torch.cuda.current_device(), tag)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
+        _WS[key] = buf
+    return buf
+
+
+def fuse_layers(per_layer) -> np.ndarray:
+    """Uniform mean over layers (reference selection.py:52-54), on the GPU."""
+    torch = _lib.require_cuda()
+    a = np.ascontiguousarray(per_layer, dtype=F32)
+    if a.ndim != 2:
+        raise ShapeError(f"per-layer scores must be [L, s], got {a.shape}")
+    d = torch.from_numpy(a).cuda()
+    fused = torch.empty(a.shape[1], dtype=torch.float32, device=d.device)
+    _fuse_device(d, fused)
+    return fused.cpu().numpy()
+
+
+def _fuse_device(per_layer_dev, fused_out, stream=None):
+    torch = _lib.require_cuda()
+    L, s = per_layer_dev.shape
+    idx = torch.empty(1, dtype=torch.int32, device=per_layer_dev.device)
+    st = torch.empty(1, dtype=torch.int32, device=per_layer_dev.device)
+    _lib.check(_lib.load().pkv_fuse_select(per_layer_dev.data_ptr(), int(L), int(s), 0, fused_out.data_ptr(),
+                                           idx.data_ptr(), st.data_ptr(), None, 0, _lib.stream_ptr(torch, stream)))
+
+
+def select_top_p(scores: ValueScores, p: float) -> SelectionResult:
+    """Top ceil(p*s) tokens of the fused vector; ties toward smaller index."""
+    torch = _lib.require_cuda()
+    s = scores.fused.shape[0]
+    k = ratio_budget(p, s)
+    fused = scores._dev_fused
+    if fused is None:
+        fused = torch.from_numpy(np.ascontiguousarray(scores.fused, dtype=F32)).cuda()
+    if k == 0:
+        return SelectionResult(indices=[], p=p, k=0, _dev_idx=torch.empty(0, dtype=torch.int32, device=fused.device))
+    idx, status = device_topk(fused, k)
+    st = int(status.item())
+    if st == 7:
+        raise NumericsError("non-finite values in top-k scores")
+    _lib.check(st)
+    return SelectionResult(indices=[int(i) for i in idx.cpu().tolist()], p=p, k=k, _dev_idx=idx)
+
+
+def check_tokens(tokens, config: ModelConfig) -> np.ndarray:
+    """Non-empty 1-D ids inside the vocab (reference model.py:231-237)."""
+    ids = np.asarray(tokens, dtype=np.int64)
+    if ids.ndim != 1 or ids.shape[0] == 0:
+        raise InputError(f"token sequence must be non-empty 1-D, got shape {ids.shape}")
+    if ids.min() < 0 or ids.max() >= config.vocab_size:
+        raise InputError("token id out of range for vocab")
+    return ids
+
+
+def run_query_pass(dm, cache, ids: np.ndarray, flags: int, per_layer=None, fresh_k=None, fresh_v=None, logits=None,
+                   stream=None):
+    """One device narrow pass (reference model.py:370-402) over the cache."""
+    torch = _lib.require_cuda()
+    m = int(ids.shape[0])
+    cache.ensure_query_room(m)
+    d_ids = torch.from_numpy(ids.astype(np.int32)).to(cache.device)
+    lib = _lib.load()
+    nbytes = lib.pkv_query_pass_workspace(dm.handle, cache.context_length, m, flags)
+    ws = workspace(nbytes, "qp")
+
+    def ptr(t):
+        return t.data_ptr() if t is not None else None
+
+    import ctypes
+    chunks = ctypes.byref(cache.c_chunks)
+    _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(cache.c_cache), chunks, d_ids.data_ptr(), m, flags,
+                                  ptr(per_layer), ptr(fresh_k), ptr(fresh_v), ptr(logits), ws.data_ptr(), ws.numel(),
+                                  _lib.stream_ptr(torch, stream)))
+
+
+def score_prophet(weights, config: ModelConfig, cache, query_tokens, tally: FlopTally | None = None,
+                  renormalize_context_only: bool = False) -> ValueScores:
+    """Query-to-context attention over the assembled (approximate) cache: one
+    fp32-faithful narrow pass on the GPU; per-layer head-mean, query-mean rows
+    over the context become the layer scores (reference selection.py:64-86)."""
+    torch = _lib.require_cuda()
+    dm = resolve_device_model(weights, config)
+    ids = check_tokens(query_tokens, config)
+    if cache.access_log is not None:
+        cache.access_log.extend(("read", li) for li in range(config.n_layers))
+    s = cache.context_length
+    per_layer = torch.empty((config.n_layers, s), dtype=torch.float32, device=cache.device)
+    flags = _lib.PKV_QP_SCORES | _lib.PKV_QP_FROM_CHUNKS
+    if renormalize_context_only:
+        flags |= _lib.PKV_QP_RENORM
+    run_query_pass(dm, cache, ids, flags, per_layer=per_layer)
+    fused = torch.empty(s, dtype=torch.float32, device=cache.device)
+    _fuse_device(per_layer, fused)
+    bill_query_pass(tally, config, s, int(ids.shape[0]))
+    pl = per_layer.cpu().numpy()
+    if not np.isfinite(pl).all():
+        raise NumericsError("non-finite values in attention scores")
+    return ValueScores(strategy="prophet", per_layer=pl, fused=fused.cpu().numpy(), _dev_fused=fused)
+
+
+def score_epic(cache, n_layers: int) -> ValueScores:
+    """Static positional prior: negated distance to the chunk start (reference selection.py:89-92)."""
+    return ValueScores.from_vector("epic", (-cache.source_local.astype(np.int64)).astype(F32), n_layers)
+
+
+def score_random(s_context: int, seed: int, n_layers: int) -> ValueScores:
+    """Uniform noise scores (reference selection.py:145-148)."""
+    return ValueScores.from_vector("random", np.random.default_rng(seed).random(s_context), n_layers)

@@ -1,0 +1,168 @@
+"""Kernel-level GPU tests: each sm_100a kernel against a plain fp32 torch
+reference (GEMM, attention) or the CPU oracle (assembly, top-k)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import pikv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(128, 256, 64, 256), (300, 512, 4096, 256), (7, 8, 8, 256),
+                                      (1000, 640, 448, 128), (6144, 96, 4096, 96), (129, 96, 70, 96)])
+def test_gemm_matches_fp32_reference(built, M, N, K, bn):
+    torch = _torch()
+    P = built
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn((M, K), generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn((N, K), generator=g, device="cuda").to(torch.bfloat16)
+    C = torch.full((M, N), float("nan"), device="cuda")
+    rc = P._lib.load().pkv_gemm_bf16(A.data_ptr(), K, B.data_ptr(), K, M, N, K, C.data_ptr(), N, bn, 0,
+                                     torch.cuda.current_stream().cuda_stream)
+    P._lib.check(rc)
+    torch.cuda.synchronize()
+    want = A.float() @ B.float().t()
+    err = (C - want).abs().max().item()
+    assert err <= 1e-3 * max(1.0, want.abs().max().item()), err
+
+
+def test_gemm_residual_epilogue(built):
+    torch = _torch()
+    P = built
+    M, N, K = 200, 512, 256
+    A = torch.randn((M, K), device="cuda").to(torch.bfloat16)
+    B = torch.randn((N, K), device="cuda").to(torch.bfloat16)
+    C0 = torch.randn((M, N), device="cuda")
+    C = C0.clone()
+    P._lib.check(P._lib.load().pkv_gemm_bf16(A.data_ptr(), K, B.data_ptr(), K, M, N, K, C.data_ptr(), N, 256, 2,
+                                             torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = C0 + A.float() @ B.float().t()
+    assert (C - want).abs().max().item() < 1e-3
+
+
+def _attn_setup(torch, P, H, Hkv, dk, s, n_q, perm_pages, seed):
+    cfg = P.ModelConfig(n_layers=2, n_heads=H, n_kv_heads=Hkv, head_dim=dk, hidden_dim=H * dk, ffn_dim=256,
+                        vocab_size=64)
+    dm = P.DeviceModel.random(cfg, seed=1)
+    lay = cfg.layout()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    pool_tokens = -(-s // 128) * 128
+    n_pages = pool_tokens // 128
+    L = cfg.n_layers
+    kp = torch.zeros((L, Hkv, pool_tokens, lay.dkp), dtype=torch.bfloat16, device="cuda")
+    vp = torch.zeros_like(kp)
+    kp[..., :dk] = torch.randn((L, Hkv, pool_tokens, dk), generator=g, device="cuda").to(torch.bfloat16)
+    vp[..., :dk] = torch.randn((L, Hkv, pool_tokens, dk), generator=g, device="cuda").to(torch.bfloat16)
+    pages = torch.randperm(n_pages, generator=g, device="cuda").int() if perm_pages else \
+        torch.arange(n_pages, dtype=torch.int32, device="cuda")
+    pos = torch.sort(torch.randperm(s, generator=g, device="cuda")[:n_q])[0].int()
+    q = torch.zeros((n_q, H, lay.dkp), dtype=torch.bfloat16, device="cuda")
+    q[..., :dk] = torch.randn((n_q, H, dk), generator=g, device="cuda").to(torch.bfloat16)
+    cache = P._lib.Cache(kp.data_ptr(), vp.data_ptr(), pool_tokens, pages.data_ptr(), s, 0, 0, 0, 0, 0)
+    return cfg, dm, lay, kp, vp, pages, pos, q, cache
+
+
+def _attn_reference(torch, layer, kp, vp, pages, pos, q, H, Hkv, dk, s):
+    # logical token t -> slot pages[t//128]*128 + t%128
+    t = torch.arange(s, device="cuda")
+    slot = pages.long()[t // 128] * 128 + t % 128
+    K = kp[layer][:, slot, :dk].float()   # [Hkv, s, dk]
+    V = vp[layer][:, slot, :dk].float()
+    G = H // Hkv
+    out = torch.empty((q.shape[0], H, dk), device="cuda")
+    mask = t[None, :] <= pos.long()[:, None]
+    for h in range(H):
+        sc = (q[:, h, :dk].float() @ K[h // G].t()) / dk ** 0.5
+        sc = sc.masked_fill(~mask, float("-inf"))
+        out[:, h] = torch.softmax(sc, dim=-1) @ V[h // G]
+    return out
+
+
+@pytest.mark.parametrize("H,Hkv,dk,s,n_q,perm", [(32, 8, 128, 4096, 819, False), (4, 2, 64, 2048, 410, True),
+                                                 (8, 8, 128, 1000, 100, True), (2, 1, 4, 300, 64, False)])
+def test_sparse_attention_matches_fp32_reference(built, H, Hkv, dk, s, n_q, perm):
+    torch = _torch()
+    P = built
+    cfg, dm, lay, kp, vp, pages, pos, q, cache = _attn_setup(torch, P, H, Hkv, dk, s, n_q, perm, seed=H + s)
+    out = torch.zeros((n_q, H, lay.dkp), dtype=torch.bfloat16, device="cuda")
+    layer = 1
+    P._lib.check(P._lib.load().pkv_attention_sparse(dm.handle, ctypes.byref(cache), layer, q.data_ptr(),
+                                                    out.data_ptr(), pos.data_ptr(), n_q,
+                                                    torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = _attn_reference(torch, layer, kp, vp, pages, pos, q, H, Hkv, dk, s)
+    got = out[..., :dk].float()
+    err = (got - want).abs().max().item()
+    cos = torch.nn.functional.cosine_similarity(got.flatten(), want.flatten(), dim=0).item()
+    assert err < 3e-2 and cos > 0.9999, (err, cos)
+
+
+def test_assembly_is_bf16_of_reference_keys(built):
+    torch = _torch()
+    P = built
+    cfg_o = O.Cfg(n_layers=3, n_heads=8, n_kv_heads=2, head_dim=128, hidden_dim=1024, ffn_dim=256,
+                  vocab_size=64, rope_theta=500000.0)
+    rng = np.random.default_rng(5)
+    lens = [300, 1, 517, 128]
+    chunks = []
+    for ci, t in enumerate(lens):
+        kn = [O.bf16_round(rng.standard_normal((t, 2, 128)).astype(np.float32) * 3) for _ in range(3)]
+        vv = [O.bf16_round(rng.standard_normal((t, 2, 128)).astype(np.float32)) for _ in range(3)]
+        chunks.append(O.Chunk(chunk_id=ci, fp="fp", token_ids=rng.integers(0, 64, t), k_nr=kn, v=vv))
+    ref = O.stitch(chunks, cfg_o)
+    cfg = P.ModelConfig(**cfg_o.json())
+    dch = [P.ChunkKV(c.chunk_id, "fp", c.token_ids, c.k_nr, c.v) for c in chunks]
+    cache = P.assemble(dch, cfg)
+    torch.cuda.synchronize()
+    s = cache.context_length
+    kp = cache.k_pool[:, :, :s, :128].permute(0, 2, 1, 3)  # [L, s, Hkv, dk]
+    vp = cache.v_pool[:, :, :s, :128].permute(0, 2, 1, 3)
+    for li in range(3):
+        want_k = torch.from_numpy(ref.keys[li]).cuda().to(torch.bfloat16)
+        want_v = torch.from_numpy(ref.values[li]).cuda().to(torch.bfloat16)
+        assert torch.equal(kp[li].view(torch.int16), want_k.view(torch.int16))
+        assert torch.equal(vp[li].view(torch.int16), want_v.view(torch.int16))
+        # the f32 view equals the reference's keys_rebased bit for bit
+        assert np.array_equal(cache.keys_rebased[li], ref.keys[li])
+        assert np.array_equal(cache.values[li], ref.values[li])
+
+
+@pytest.mark.parametrize("n,k,mode", [(32768, 6554, "rand"), (2048, 410, "ties"), (5, 0, "rand"), (5, 5, "rand"),
+                                      (3000, 1, "ties"), (100000, 26215, "rand"), (7, 3, "allequal"),
+                                      (1000, 500, "signed")])
+def test_topk_matches_reference_rule(built, n, k, mode):
+    P = built
+    rng = np.random.default_rng(n + k)
+    if mode == "rand":
+        v = rng.random(n).astype(np.float32)
+    elif mode == "ties":
+        v = rng.integers(0, 20, n).astype(np.float32) / 7
+    elif mode == "allequal":
+        v = np.full(n, 0.25, dtype=np.float32)
+    else:
+        v = (rng.standard_normal(n) * 3).astype(np.float32)
+        v[::17] = 0.0
+        v[::19] = -0.0
+    assert P.top_k_indices(v, k) == O.topk_ascending(v, k)
+
+
+def test_topk_rejects_non_finite(built):
+    P = built
+    with pytest.raises(P.NumericsError):
+        P.top_k_indices(np.array([np.nan, 1.0], dtype=np.float32), 1)
+
+
+def test_fuse_layers_bit_exact(built):
+    P = built
+    rng = np.random.default_rng(3)
+    per = rng.random((32, 4096)).astype(np.float32) * 1e-3
+    assert np.array_equal(P.fuse_layers(per), O.layer_mean(per))
