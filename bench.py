@@ -1,0 +1,353 @@
+"""ProphetKV selective-recompute prefill benchmark (BASELINE.json metric).
+
+Step = one full prefill of one RAG request: assemble 16 precomputed 2048-token
+chunks (Llama-3-8B shape, random init, synthetic inputs) into the paged cache,
+score the context with the 32-token query (fp32-faithful narrow pass), fuse +
+top-k at p = 0.2, Stage-II recompute of k = 6554 tokens, finalize -> first-token
+logits.  value = effective prefill tok/s = n_gpus * s / TTFT (weak scaling: one
+independent request per GPU, no data-path collective).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # BASELINE.json configs[2]: Llama-3-8B shape, 32k context of 16 chunks, 20% recompute
+    "llama3-8b-32k": dict(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, hidden_dim=4096, ffn_dim=14336,
+                          vocab_size=128256, rope_theta=500000.0, n_chunks=16, chunk_len=2048),
+    # configs[1]: Mistral-7B shape, 8k context of 8 chunks
+    "mistral-7b-8k": dict(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, hidden_dim=4096, ffn_dim=14336,
+                          vocab_size=32000, rope_theta=1000000.0, n_chunks=8, chunk_len=1024),
+}
+METRIC = "effective prefill tok/s @32k ctx, 20% recompute (TTFT = s / value)"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return float("nan")
+        sm = [num(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": num(rows[0][1]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(num(r[2]) for r in rows)}
+
+
+# --------------------------------------------------------------------- CPU baseline
+def cpu_sample(cfgd: dict, p: float, m: int = 32, n_rows: int = 256, seed: int = 0):
+    """Time the reference algorithm (oracle port of pikv) on a bounded sample of the
+    workload and extrapolate to the full request: one layer of the full-width model
+    at the full context s; Stage II on n_rows of the k selected rows (its cost is
+    linear in rows: dense k x s attention per the reference); x n_layers."""
+    from oracle import pikv_oracle as O
+    L = cfgd["n_layers"]
+    c1 = O.Cfg(1, cfgd["n_heads"], cfgd["n_kv_heads"], cfgd["head_dim"], cfgd["hidden_dim"], cfgd["ffn_dim"],
+               cfgd["vocab_size"], cfgd["rope_theta"])
+    rng = np.random.default_rng(seed)
+    D, F, V, KV = c1.hidden_dim, c1.ffn_dim, c1.vocab_size, c1.kv_dim
+    HQ = c1.n_heads * c1.head_dim
+
+    def mat(a, b):
+        return (rng.standard_normal((a, b), dtype=np.float32) / np.float32(math.sqrt(a)))
+
+    w = O.Weights(embed=rng.standard_normal((V, D), dtype=np.float32),
+                  layers=[O.Layer(np.ones(D, np.float32), mat(D, HQ), mat(D, KV), mat(D, KV), mat(HQ, D),
+                                  np.ones(D, np.float32), mat(D, F), mat(D, F), mat(F, D))],
+                  final_norm=np.ones(D, np.float32), lm_head=mat(D, V), _fp="cpu-sample")
+    chunks = []
+    for ci in range(cfgd["n_chunks"]):
+        t = cfgd["chunk_len"]
+        kn = [O.bf16_round(rng.standard_normal((t, c1.n_kv_heads, c1.head_dim), dtype=np.float32))]
+        vv = [O.bf16_round(rng.standard_normal((t, c1.n_kv_heads, c1.head_dim), dtype=np.float32))]
+        chunks.append(O.Chunk(ci, "cpu-sample", rng.integers(0, V, t), kn, vv))
+    query = rng.integers(0, V, m).tolist()
+    tm = {}
+    t0 = time.perf_counter()
+    cache = O.stitch(chunks, c1)
+    tm["assemble"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    per, fused = O.prophet_scores(w, c1, cache, query)
+    tm["score"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.logits_of(w, c1, np.zeros((m, D), np.float32) + 0.01, None)
+    tm["head"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sel, k = O.select(fused, p)
+    tm["select"] = time.perf_counter() - t0
+    sample = sel[:: max(1, len(sel) // n_rows)][:n_rows]
+    t0 = time.perf_counter()
+    O.repair(w, c1, cache, sample)
+    tm["repair_sample"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.finalize(w, c1, cache, query)
+    tm["finalize"] = time.perf_counter() - t0
+    body = tm["assemble"] + (tm["score"] - tm["head"]) + (tm["finalize"] - tm["head"])
+    ttft = L * body + 2 * tm["head"] + tm["select"] + L * tm["repair_sample"] * (k / len(sample))
+    return ttft, tm, k, len(sample), sum(tm.values())
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+# ----------------------------------------------------------------------------- main
+def run_reference(args, cfgd, rank, world):
+    if rank != 0:
+        return
+    s = cfgd["n_chunks"] * cfgd["chunk_len"]
+    times = []
+    for i in range(args.warmup + args.steps):
+        ttft, tm, k, n_s, wall = cpu_sample(cfgd, args.p, n_rows=args.ref_rows, seed=i)
+        if i >= args.warmup:
+            times.append(ttft)
+    ttft = float(np.mean(times))
+    value = s / ttft
+    cores = cpu_cores()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft * 1e3, "ttft_ms": ttft * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
+            "data": "synthetic", "config": {"workload": args.config, "s": s, "m": 32, "p": args.p, "k": k,
+                                            "l2": "inputs larger than L2 (CPU run)"},
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
+                             "sample": f"oracle port of pikv, 1 layer at full width and s={s}, Stage II on {n_s} "
+                                       f"of k={k} rows, extrapolated x{cfgd['n_layers']} layers and k/{n_s} rows; "
+                                       f"phase seconds {json.dumps({a: round(b, 3) for a, b in tm.items()})}"},
+            "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llama3-8b-32k", choices=list(CONFIGS))
+    ap.add_argument("--p", type=float, default=0.2)
+    ap.add_argument("--m", type=int, default=32)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=128)
+    args = ap.parse_args()
+    cfgd = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfgd, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2602_02579_b200 as P
+    from paper_2602_02579_b200 import _lib
+    from paper_2602_02579_b200.pipeline import PrefillPipeline, random_device_chunks
+
+    cfg = P.ModelConfig(**{k: cfgd[k] for k in ("n_layers", "n_heads", "n_kv_heads", "head_dim", "hidden_dim",
+                                                "ffn_dim", "vocab_size", "rope_theta")})
+    s = cfgd["n_chunks"] * cfgd["chunk_len"]
+    dm = P.DeviceModel.random(cfg, seed=0)
+    chunks = random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=1 + rank)
+    pipe = PrefillPipeline(dm, chunks, args.m, args.p)
+    rng = np.random.default_rng(7 + rank)
+    query = rng.integers(0, cfg.vocab_size, args.m)
+    pipe.set_query(query)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        pipe.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    _lib.timing(True)
+    _lib.timing_collect()
+    n0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        pipe.step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    n_launch = _lib.launch_count() - n0
+    phases = _lib.timing_collect()
+    _lib.timing(False)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    value = world * s / (ms / 1e3)
+
+    # ---- roofline of every kernel group; the dominant one is reported
+    hbm, tf_burst, tf_sust, peak_kind = _peaks()
+    idx = pipe.idx[: pipe.k].cpu().numpy().astype(np.int64)
+    k = pipe.k
+    L, H, Hkv, dk, D, F = cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden_dim, cfg.ffn_dim
+    lay = cfg.layout()
+    work = {  # per launch group: (bound, algorithmic units, unit)
+        "assemble": ("hbm", 4.0 * L * s * Hkv * lay.dkp * 2, "GB/s"),
+        "qp_proj": ("hbm", dm.weight_bytes(include_head=False) / (4 * L), "GB/s"),
+        "rc_qkv": ("tensor", 2.0 * k * D * (H + 2 * Hkv) * dk, "TFLOP/s"),
+        "rc_attn": ("tensor", 4.0 * H * dk * float(np.sum(idx + 1)), "TFLOP/s"),
+        "rc_o": ("tensor", 2.0 * k * H * dk * D, "TFLOP/s"),
+        "rc_gate_up": ("tensor", 2.0 * k * D * 2 * F, "TFLOP/s"),
+        "rc_down": ("tensor", 2.0 * k * F * D, "TFLOP/s"),
+        "lm_head": ("hbm", 2.0 * cfg.vocab_size * lay.Dp, "GB/s"),
+    }
+    rooflines = {}
+    for name, (bound, units, unit) in work.items():
+        tot_ms, cnt = phases[name]
+        if cnt == 0 or tot_ms <= 0:
+            continue
+        per_launch_s = tot_ms / cnt / 1e3
+        ach = units / per_launch_s / (1e9 if unit == "GB/s" else 1e12)
+        peak = hbm if bound == "hbm" else tf_sust
+        rooflines[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                           "ms_per_launch": per_launch_s * 1e3, "launches": cnt}
+    step_total = sum(v[0] for v in phases.values())
+    dominant = max((n for n in rooflines), key=lambda n: phases[n][0])
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get(dominant)
+    roof = dict(rooflines[dominant], kernel=dominant, traffic=traffic,
+                peak_kind=f"{peak_kind} ({'sustained bf16' if rooflines[dominant]['bound'] == 'tensor' else 'HBM copy'})")
+
+    line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 (Stage II) / fp32-faithful (narrow passes)",
+            "data": "synthetic (random-init weights, N(0,1) chunk K/V, uniform token ids)",
+            "config": {"workload": args.config, "model": "Llama-3-8B shape" if "llama" in args.config else
+                       "Mistral-7B shape", "s": s, "chunks": cfgd["n_chunks"], "m": args.m, "p": args.p, "k": k,
+                       "parallelism": f"request-dp{world}", "l2": "inputs larger than L2 (16 GB weights, 4.3 GB KV)"},
+            "gpu_launches": int(n_launch), "clocks": clk, "roofline": roof,
+            "phases_ms": {n: round(v[0] / args.steps, 3) for n, v in phases.items()},
+            "phase_share": {n: round(v[0] / step_total, 4) for n, v in phases.items() if step_total > 0},
+            "kernel_rooflines": rooflines}
+
+    # ---- e2e through the public API with host (pinned) inputs
+    if args.e2e_steps > 0:
+        host =[(c._k_dev.cpu().pin_memory(), c._v_dev.cpu().pin_memory(), c.token_ids) for c in chunks]
+        h2d = sum(a.numel() * 2 + b.numel() * 2 for a, b, _ in host)
+        torch.cuda.synchronize()
+        mw = dm
+
+        def e2e_step():
+            dch = [P.ChunkKV.from_device(i, "device-random", ids, a.to("cuda", non_blocking=True),
+                                         b.to("cuda", non_blocking=True), cfg.head_dim)
+                   for i, (a, b, ids) in enumerate(host)]
+            cache = P.assemble(dch, cfg, fp32_taps=False)
+            sc = P.score_prophet(mw, cfg, cache, query)
+            sel = P.select_top_p(sc, args.p)
+            P.recompute_selected(mw, cfg, cache, P.RecomputePlan(sel))
+            return P.finalize_query(mw, cfg, cache, query).first_logits
+
+        e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        d2h = L * s * 4 + s * 4 + k * 4 + cfg.vocab_size * 4
+        line["e2e"] = {"value": world * s / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
+                       "h2d_bytes_per_step": int(h2d + args.m * 8), "d2h_bytes_per_step": int(d2h),
+                       "path": "assemble -> score_prophet -> select_top_p -> recompute_selected -> finalize_query, "
+                               "chunk K/V copied from pinned host memory each step"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ttft, tm, kk, n_s, wall = cpu_sample(cfgd, args.p, n_rows=args.ref_rows)
+        line["cpu_baseline"] = {"value": s / ttft, "unit": "tok/s", "cores": cpu_cores(), "kind": "port",
+                                "ttft_ms": ttft * 1e3,
+                                "sample": f"oracle port of pikv: 1 layer, full width, s={s}, Stage II on {n_s}/{kk} "
+                                          f"rows; extrapolated x{L} layers (sample wall {wall:.1f}s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -169,6 +169,15 @@ int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_
 int pkv_attention_sparse(const pkv_model* m, const pkv_cache* cache, int32_t layer, const void* q, void* out,
                          const int32_t* pos, int32_t n_q, void* stream);
 
+/* phase timers: when enabled, every stage records CUDA events on its stream around
+ * each kernel group; collect() waits for them and returns per-category totals (ms)
+ * and launch-group counts.  Categories: 0 assemble, 1 narrow-pass projections,
+ * 2 narrow-pass attention+scores, 3 narrow-pass misc, 4 fuse+top-k, 5 Stage-II
+ * QKV GEMM (+RoPE+scatter), 6 Stage-II attention, 7 o GEMM, 8 gate/up GEMM,
+ * 9 down GEMM, 10 Stage-II misc (norms, gather), 11 lm_head. */
+int pkv_timing_enable(int32_t on);
+int pkv_timing_collect(double* ms, int32_t* counts, int32_t ncat);
+
 const char* pkv_last_error(void);
 uint64_t pkv_launch_count(void);
 int pkv_version(void);

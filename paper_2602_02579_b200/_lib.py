@@ -69,6 +69,8 @@ _SIGS = {
     "pkv_cache_view": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), ctypes.POINTER(Chunks), c_i32, c_i32, c_vp, c_vp]),
     "pkv_gemm_bf16": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "pkv_attention_sparse": (c_i32, [c_vp, ctypes.POINTER(Cache), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
+    "pkv_timing_enable": (c_i32, [c_i32]),
+    "pkv_timing_collect": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i32), c_i32]),
     "pkv_last_error": (ctypes.c_char_p, []),
     "pkv_launch_count": (ctypes.c_uint64, []),
     "pkv_version": (c_i32, []),
@@ -120,3 +122,19 @@ def stream_ptr(torch, stream=None) -> int:
 
 def launch_count() -> int:
     return int(load().pkv_launch_count())
+
+
+TIMER_NAMES = ("assemble", "qp_proj", "qp_attn", "qp_misc", "select", "rc_qkv", "rc_attn", "rc_o", "rc_gate_up",
+               "rc_down", "rc_misc", "lm_head")
+
+
+def timing(enable: bool) -> None:
+    load().pkv_timing_enable(1 if enable else 0)
+
+
+def timing_collect() -> dict:
+    n = len(TIMER_NAMES)
+    ms = (ctypes.c_double * n)()
+    cnt = (c_i32 * n)()
+    check(load().pkv_timing_collect(ms, cnt, n))
+    return {name: (ms[i], cnt[i]) for i, name in enumerate(TIMER_NAMES)}

@@ -345,7 +345,6 @@ def replace_entries(cache: AssembledCache, layer: int, indices, new_keys, new_va
     if cache.fp32_taps:
         cache.add_tap(layer, idx, tk, tv)
     cache.recomputed[layer, idx] = True
-    cache._d_recomp[d_idx.long()] = 1
 
 
 def mark_finalized(cache: AssembledCache) -> None:

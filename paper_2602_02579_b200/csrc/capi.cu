@@ -83,6 +83,59 @@ static int layout_of(const pkv_config* c, int out[5]) {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- native phase timers (pkv_timing_enable / pkv_timing_collect): CUDA events
+// recorded on the launching stream around each kernel group when enabled.
+enum TimerCat { T_ASSEMBLE = 0, T_QP_PROJ, T_QP_ATTN, T_QP_MISC, T_SELECT, T_RC_QKV, T_RC_ATTN, T_RC_O, T_RC_GU,
+                T_RC_DOWN, T_RC_MISC, T_LMHEAD, T_NCAT };
+struct TimerRec {
+  int cat;
+  cudaEvent_t a, b;
+};
+static std::mutex g_tm_mu;
+static std::vector<TimerRec> g_tm;
+static std::vector<cudaEvent_t> g_ev_pool;
+static std::atomic<int> g_timing{0};
+
+static cudaEvent_t ev_get() {
+  std::lock_guard<std::mutex> lk(g_tm_mu);
+  if (!g_ev_pool.empty()) {
+    cudaEvent_t e = g_ev_pool.back();
+    g_ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ScopedTimer {
+  int cat;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ScopedTimer(int c, cudaStream_t s) : cat(c), st(s) {
+    if (g_timing.load(std::memory_order_relaxed)) {
+      a = ev_get();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ScopedTimer() {
+    if (a) {
+      cudaEvent_t b = ev_get();
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_tm_mu);
+      g_tm.push_back({cat, a, b});
+    }
+  }
+};
+#define TTRY(cat, x)                     \
+  do {                                   \
+    ::pkv::ScopedTimer t__(cat, st);     \
+    if ((rc = (x)) != 0) return rc;      \
+  } while (0)
+
+int mark_launch(const int32_t* idx, int n, uint8_t* flags, cudaStream_t st);
+
+
 // fp32-faithful projection of m (<= any) fp32 rows: out[m][N] (=|+=) x[m][K] . W[N][K]^T
 // via tcgen05 on the 3-way bf16 split of x, split-K partials and a reduce.
 struct ProjWs {
@@ -127,6 +180,39 @@ using namespace pkv;
 extern "C" {
 
 int pkv_version(void) { return 1; }
+
+int pkv_timing_enable(int32_t on) {
+  g_timing.store(on ? 1 : 0);
+  return PKV_OK;
+}
+
+int pkv_timing_collect(double* ms, int32_t* counts, int32_t ncat) {
+  std::vector<TimerRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_tm_mu);
+    recs.swap(g_tm);
+  }
+  for (int i = 0; i < ncat; ++i) {
+    ms[i] = 0.0;
+    counts[i] = 0;
+  }
+  int rc = PKV_OK;
+  for (auto& r : recs) {
+    if (cudaEventSynchronize(r.b) != cudaSuccess) rc = set_error(PKV_ERR_CUDA, "timer event failed");
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    if (r.cat < ncat) {
+      ms[r.cat] += t;
+      counts[r.cat] += 1;
+    }
+  }
+  std::lock_guard<std::mutex> lk(g_tm_mu);
+  for (auto& r : recs) {
+    g_ev_pool.push_back(r.a);
+    g_ev_pool.push_back(r.b);
+  }
+  return rc;
+}
 const char* pkv_last_error(void) { return g_err; }
 uint64_t pkv_launch_count(void) { return g_launches.load(); }
 
@@ -174,8 +260,11 @@ int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c
   if (c->pool_tokens % 128 != 0 || c->pool_tokens < c->s) return set_error(PKV_ERR_SHAPE, "pool too small");
   if (c->rope_len < c->s) return set_error(PKV_ERR_SHAPE, "rope table shorter than the context");
   ChunkView cv{ch->k_nr, ch->v, ch->src_chunk, ch->src_local, ch->chunk_len};
+  cudaStream_t st = S(stream);
+  if (c->recomputed) cudaMemsetAsync(const_cast<uint8_t*>(c->recomputed), 0, (size_t)c->s, st);
+  ScopedTimer t__(T_ASSEMBLE, st);
   return assemble_launch(cv, c->s, cfg->n_layers, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos, c->rope_sin,
-                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, S(stream));
+                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, st);
 }
 
 int pkv_cache_view(const pkv_config* cfg, const pkv_cache* c, const pkv_chunks* ch, int32_t layer, int32_t is_key,
@@ -200,6 +289,7 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer
   rc = scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_k, c->page_table, c->k_pool,
                       c->pool_tokens, S(stream));
   if (rc) return rc;
+  if (c->recomputed && (rc = mark_launch(idx, n, const_cast<uint8_t*>(c->recomputed), S(stream))) != 0) return rc;
   return scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_v, c->page_table, c->v_pool,
                         c->pool_tokens, S(stream));
 }
@@ -279,16 +369,16 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
   do {                     \
     if ((rc = (x)) != 0) return rc; \
   } while (0)
-  TRY(embed_gather_launch(md->w.embed, Dp, query_ids, nullptr, m, cf.hidden_dim, w.h, Dp, st));
+  TTRY(T_QP_MISC, embed_gather_launch(md->w.embed, Dp, query_ids, nullptr, m, cf.hidden_dim, w.h, Dp, st));
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
   for (int l = 0; l < cf.n_layers; ++l) {
     const pkv_layer_weights& lw = md->layers[l];
-    TRY(rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
-    TRY(proj_f32(lw.wqkv, md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
+    TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
+    TTRY(T_QP_PROJ, proj_f32(lw.wqkv, md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
     __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
     __nv_bfloat16* vp = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
     const bool append = (flags & PKV_QP_APPEND_KV) != 0;
-    TRY(query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v, append ? kp : nullptr,
+    TTRY(T_QP_MISC, query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v, append ? kp : nullptr,
                          append ? vp : nullptr, c->pool_tokens, c->page_table,
                          fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
                          fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, st));
@@ -329,18 +419,18 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.Opart = w.Opart;
     a.Mpart = w.Mpart;
     a.Lpart = w.Lpart;
-    TRY(s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
+    TTRY(T_QP_ATTN, s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
                             (flags & PKV_QP_RENORM) ? 1 : 0, st));
-    TRY(proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, 1, w.proj, st));
-    TRY(rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
-    TRY(proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
-    TRY(silu_act_launch(w.gu, m, cf.ffn_dim, Fp, w.act, st));
-    TRY(proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, 1, w.proj, st));
+    TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, 1, w.proj, st));
+    TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
+    TTRY(T_QP_PROJ, proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
+    TTRY(T_QP_MISC, silu_act_launch(w.gu, m, cf.ffn_dim, Fp, w.act, st));
+    TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, 1, w.proj, st));
   }
   if ((flags & PKV_QP_LOGITS) && last_logits) {
-    TRY(rmsnorm_launch(w.h + (long)(m - 1) * Dp, 1, cf.hidden_dim, Dp, md->w.final_norm, cf.norm_eps, w.xl, nullptr, 0,
+    TTRY(T_LMHEAD, rmsnorm_launch(w.h + (long)(m - 1) * Dp, 1, cf.hidden_dim, Dp, md->w.final_norm, cf.norm_eps, w.xl, nullptr, 0,
                        nullptr, st));
-    TRY(gemv_launch(w.xl, md->w.lm_head, cf.vocab_size, Dp, Dp, last_logits, st));
+    TTRY(T_LMHEAD, gemv_launch(w.xl, md->w.lm_head, cf.vocab_size, Dp, Dp, last_logits, st));
   }
   return PKV_OK;
 }
@@ -356,9 +446,11 @@ int pkv_fuse_select(const float* per_layer, int32_t L, int32_t s, int32_t k, flo
     if (ws_bytes < (size_t)s * 4) return set_error(PKV_ERR_ARGUMENT, "workspace too small");
     f = reinterpret_cast<float*>(workspace);
   }
-  int rc = fuse_layers_launch(per_layer, L, s, f, S(stream));
+  cudaStream_t st = S(stream);
+  ScopedTimer t__(T_SELECT, st);
+  int rc = fuse_layers_launch(per_layer, L, s, f, st);
   if (rc) return rc;
-  return topk_launch(f, s, k, idx_out, status_out, S(stream));
+  return topk_launch(f, s, k, idx_out, status_out, st);
 }
 
 int pkv_topk(const float* scores, int32_t n, int32_t k, int32_t* idx_out, int32_t* status_out, void* stream) {
@@ -401,10 +493,11 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
   const int H = cf.n_heads, Hkv = cf.n_kv_heads, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
   int rc;
-  TRY(embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
+  if (c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
+  TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
   for (int l = 0; l < cf.n_layers; ++l) {
     const pkv_layer_weights& lw = md->layers[l];
-    TRY(rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
     g.M = k;
     g.N = md->NQKV;
@@ -425,8 +518,8 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     g.tap_k = tap_k ? tap_k + (long)l * k * Hkv * dk : nullptr;
     g.tap_v = tap_v ? tap_v + (long)l * k * Hkv * dk : nullptr;
     // K/V of every selected token are in the cache before this layer's attention
-    TRY(gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
-    TRY(attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
+    TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
                        (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
     GemmArgs go{};
     go.M = k;
@@ -434,22 +527,22 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     go.n_splits = 1;
     go.C = w.h;
     go.ldc = Dp;
-    TRY(gemm_tc_launch(EPI_RESID, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
-    TRY(rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    TTRY(T_RC_O, gemm_tc_launch(EPI_RESID, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
+    TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs gg{};
     gg.M = k;
     gg.N = 2 * Fp;
     gg.n_splits = 1;
     gg.C = w.act;
     gg.ldc = Fp;
-    TRY(gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
+    TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
     GemmArgs gd{};
     gd.M = k;
     gd.N = Dp;
     gd.n_splits = 1;
     gd.C = w.h;
     gd.ldc = Dp;
-    TRY(gemm_tc_launch(EPI_RESID, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
+    TTRY(T_RC_DOWN, gemm_tc_launch(EPI_RESID, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
   }
   return PKV_OK;
 }

@@ -108,6 +108,19 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float* v, int 
   if (tid == 0) *status = (s_base == k) ? PKV_OK : PKV_ERR_CUDA;
 }
 
+__global__ void mark_kernel(const int32_t* idx, int n, uint8_t* flags) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) flags[idx[i]] = 1;
+}
+
+int mark_launch(const int32_t* idx, int n, uint8_t* flags, cudaStream_t st) {
+  if (n <= 0) return PKV_OK;
+  mark_kernel<<<ceil_div(n, 256), 256, 0, st>>>(idx, n, flags);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("mark_kernel");
+  return PKV_OK;
+}
+
 int fuse_layers_launch(const float* per_layer, int L, int s, float* fused, cudaStream_t st) {
   if (s <= 0) return PKV_OK;
   fuse_layers_kernel<<<ceil_div(s, 256), 256, 0, st>>>(per_layer, L, s, fused);

@@ -1,0 +1,90 @@
+"""Sync-free device pipeline of one ProphetKV prefill (the bench's "step").
+
+assemble -> narrow pass with scores -> fuse + top-k -> Stage II -> finalize,
+as five stream-ordered C-ABI calls on preallocated buffers.  k = ceil(p*s) is
+computed on the host before launch (reference tensor.py:136-140), so nothing in
+the step waits for the device.  The public pikv-style functions run the same
+calls but materialise numpy results (selection list, scores, logits) between
+stages.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .chunkstore import AssembledCache, ChunkKV, ctypes_ref
+from .model import DeviceModel
+from .tensor import ratio_budget
+
+
+class PrefillPipeline:
+    def __init__(self, dm: DeviceModel, chunks: list, m: int, p: float):
+        torch = _lib.require_cuda()
+        self.dm = dm
+        cfg = dm.config
+        self.cfg = cfg
+        self.cache = AssembledCache(cfg, chunks, track_access=False, fp32_taps=False)
+        self.cache.ensure_query_room(m)
+        s = self.cache.context_length
+        self.s, self.m, self.p = s, m, p
+        self.k = ratio_budget(p, s)
+        dev = self.cache.device
+        lib = _lib.load()
+        self.flags_score = _lib.PKV_QP_SCORES | _lib.PKV_QP_FROM_CHUNKS
+        self.flags_final = _lib.PKV_QP_LOGITS | _lib.PKV_QP_APPEND_KV | _lib.PKV_QP_FROM_CHUNKS
+        qp_bytes = max(lib.pkv_query_pass_workspace(dm.handle, s, m, self.flags_score),
+                       lib.pkv_query_pass_workspace(dm.handle, s, m, self.flags_final))
+        self.ws_qp = torch.empty(qp_bytes, dtype=torch.uint8, device=dev)
+        self.ws_rc = torch.empty(max(lib.pkv_recompute_workspace(dm.handle, max(self.k, 1)), 256), dtype=torch.uint8,
+                                 device=dev)
+        self.per_layer = torch.empty((cfg.n_layers, s), dtype=torch.float32, device=dev)
+        self.fused = torch.empty(s, dtype=torch.float32, device=dev)
+        self.idx = torch.empty(max(self.k, 1), dtype=torch.int32, device=dev)
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
+        self.query = torch.zeros(m, dtype=torch.int32, device=dev)
+
+    def set_query(self, ids) -> None:
+        torch = _lib.require_cuda()
+        self.query.copy_(torch.as_tensor(np.asarray(ids, dtype=np.int32)), non_blocking=True)
+
+    def step(self, stream=None) -> None:
+        """One full prefill; results stay on the device (idx, logits, per_layer)."""
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        st = _lib.stream_ptr(torch, stream)
+        c = self.cache
+        cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
+        _lib.check(lib.pkv_assemble(ctypes_ref(c._cfg_c), ch, cc, st))
+        _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_score,
+                                      self.per_layer.data_ptr(), None, None, None, self.ws_qp.data_ptr(),
+                                      self.ws_qp.numel(), st))
+        _lib.check(lib.pkv_fuse_select(self.per_layer.data_ptr(), self.cfg.n_layers, self.s, self.k,
+                                       self.fused.data_ptr(), self.idx.data_ptr(), self.status.data_ptr(), None, 0, st))
+        _lib.check(lib.pkv_recompute(self.dm.handle, cc, self.idx.data_ptr(), self.k, None, None,
+                                     self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
+        _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_final, None,
+                                      None, None, self.logits.data_ptr(), self.ws_qp.data_ptr(), self.ws_qp.numel(),
+                                      st))
+
+
+def random_device_chunks(cfg, n_chunks: int, chunk_len: int, seed: int = 0, fingerprint: str = "device-random"):
+    """Synthetic chunk store: N(0,1) bf16 unrotated keys and values per chunk
+    (layout [L][t][Hkv][dkp]) and uniform token ids -- for benchmarks only."""
+    torch = _lib.require_cuda()
+    lay = cfg.layout()
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    rng = np.random.default_rng(seed)
+    out = []
+    for ci in range(n_chunks):
+        shape = (cfg.n_layers, chunk_len, cfg.n_kv_heads, lay.dkp)
+        k = torch.zeros(shape, dtype=torch.bfloat16, device="cuda")
+        v = torch.zeros(shape, dtype=torch.bfloat16, device="cuda")
+        k[..., :cfg.head_dim] = torch.randn(shape[:-1] + (cfg.head_dim,), generator=g, device="cuda")
+        v[..., :cfg.head_dim] = torch.randn(shape[:-1] + (cfg.head_dim,), generator=g, device="cuda")
+        ids = rng.integers(0, cfg.vocab_size, chunk_len)
+        out.append(ChunkKV.from_device(ci, fingerprint, ids, k, v, cfg.head_dim))
+    return out

@@ -66,7 +66,6 @@ def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
                                  tap_v.data_ptr() if tap_v is not None else None, ws.data_ptr(), ws.numel(),
                                  _lib.stream_ptr(torch)))
     cache.recomputed[:, sel] = True
-    cache._d_recomp[d_sel.long()] = 1
     if tap_k is not None:
         for li in range(L):
             cache.add_tap(li, sel, tap_k[li], tap_v[li])
