@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -299,7 +300,7 @@ struct QpWs {
   float *h, *x, *qkv, *q, *k, *v, *attn, *gu, *act, *S, *Opart, *Mpart, *Lpart, *Mfin, *Lfin, *rows, *xl;
   double* denom;
   ProjWs proj;
-  int n_splits, keys_per_split;
+  int n_splits, keys_per_split, tc_splits, tc_keys_per_split;
 };
 
 static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, size_t* total) {
@@ -325,6 +326,15 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.proj.part = cv.take<float>((size_t)8 * nmax * 96);
   w.keys_per_split = 512;
   w.n_splits = ceil_div(s_tot, w.keys_per_split);
+  {
+    // tensor-core split of the context keys: ~2 waves of (KV head x split) CTAs
+    static const bool simt_only = getenv("PKV_S1_SIMT") != nullptr;
+    const int row_blocks = ceil_div(R, 128);
+    const int target = std::max(1, 2 * num_sms() / std::max(1, Hkv * row_blocks));
+    w.tc_keys_per_split = std::max(64, ceil_div(ceil_div(s, target), 64) * 64);
+    w.tc_splits = (simt_only || s == 0) ? 0 : ceil_div(s, w.tc_keys_per_split);
+    if (w.tc_splits > 0) w.n_splits = w.tc_splits + 1;
+  }
   const int row_blocks = ceil_div(R, 128);
   (void)row_blocks;
   if (flags & PKV_QP_SCORES) {
@@ -394,7 +404,11 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.s_tot = s + m;
     a.R = m * G;
     a.keys_per_split = w.keys_per_split;
-    a.n_splits = w.n_splits;
+    a.n_splits = w.tc_splits > 0 ? 1 : w.n_splits;
+    a.key_base = 0;
+    a.split_base = 0;
+    a.tc_splits = w.tc_splits;
+    a.tc_keys_per_split = w.tc_keys_per_split;
     a.scale = (float)(1.0 / std::sqrt((double)dk));
     a.src_chunks = (flags & PKV_QP_FROM_CHUNKS) ? 1 : 0;
     a.recomp = c->recomputed;

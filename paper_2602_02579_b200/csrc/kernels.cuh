@@ -30,6 +30,8 @@ int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStrea
 struct S1Attn {
   const float* q;
   int m, H, Hkv, G, dk, dkp, s, s_tot, R, keys_per_split, n_splits;
+  int key_base, split_base;        // SIMT pass: first key / first partial index
+  int tc_splits, tc_keys_per_split;  // >0: context keys on tcgen05 (s1_attn_tc), fresh keys on SIMT
   float scale;
   int src_chunks;
   const uint8_t* recomp;  // nullable [s]: repaired entries come from the pool
@@ -52,6 +54,30 @@ struct S1Attn {
   float* Mpart;
   float* Lpart;
 };
+struct S1TcArgs {
+  const float* q;  // [m][H][DKP] rotated fp32
+  int m, H, Hkv, G, dk, R, s, s_tot, keys_per_split, n_splits;
+  float scale;
+  int src_chunks;
+  const uint8_t* recomp;
+  const uint64_t* ck;
+  const uint64_t* cv;
+  const int32_t* src_chunk;
+  const int32_t* src_local;
+  const int32_t* chunk_len;
+  const double* rcos;
+  const double* rsin;
+  const __nv_bfloat16* k_pool;  // layer base
+  const __nv_bfloat16* v_pool;
+  long pool_tokens;
+  const int32_t* page_table;
+  int layer;
+  float* S;  // [Hkv][R][s_tot] or null
+  float* Opart;
+  float* Mpart;
+  float* Lpart;
+};
+int s1_attn_tc_launch(const S1TcArgs& a, cudaStream_t st);
 int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
                         float* per_layer, int renorm, cudaStream_t st);
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st);

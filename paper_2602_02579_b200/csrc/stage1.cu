@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
     qi[x] = r < a.R ? r % a.m : -1;
   }
 
-  const int k_begin = split * a.keys_per_split;
+  const int k_begin = a.key_base + split * a.keys_per_split;
   const int k_end = min(k_begin + a.keys_per_split, a.s_tot);
   const int half = a.dk >> 1;
 
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
   for (int x = 0; x < 4; ++x) {
     const int r = r0 + ty * 4 + x;
     if (r >= a.R) continue;
-    const long base = ((long)split * a.Hkv + g) * a.R + r;
+    const long base = ((long)(a.split_base + split) * a.Hkv + g) * a.R + r;
     float* od = a.Opart + base * DKP;
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
@@ -493,6 +493,49 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
                         float* per_layer, int renorm, cudaStream_t st) {
   S1Attn a = a_in;
   const int row_blocks = ceil_div(a.R, 128);
+  int total_splits = a.n_splits;
+  if (a.tc_splits > 0) {
+    // context keys [0, s) on the tensor cores (3-way bf16 split, fp32-faithful)
+    S1TcArgs t{};
+    t.q = a.q;
+    t.m = a.m;
+    t.H = a.H;
+    t.Hkv = a.Hkv;
+    t.G = a.G;
+    t.dk = a.dk;
+    t.R = a.R;
+    t.s = a.s;
+    t.s_tot = a.s_tot;
+    t.keys_per_split = a.tc_keys_per_split;
+    t.n_splits = a.tc_splits;
+    t.scale = a.scale;
+    t.src_chunks = a.src_chunks;
+    t.recomp = a.recomp;
+    t.ck = a.ck;
+    t.cv = a.cv;
+    t.src_chunk = a.src_chunk;
+    t.src_local = a.src_local;
+    t.chunk_len = a.chunk_len;
+    t.rcos = a.rcos;
+    t.rsin = a.rsin;
+    t.k_pool = a.k_pool;
+    t.v_pool = a.v_pool;
+    t.pool_tokens = a.pool_tokens;
+    t.page_table = a.page_table;
+    t.layer = a.layer;
+    t.S = a.S;
+    t.Opart = a.Opart;
+    t.Mpart = a.Mpart;
+    t.Lpart = a.Lpart;
+    int rc = s1_attn_tc_launch(t, st);
+    if (rc) return rc;
+    // the m fresh query keys (fp32 K/V) on the SIMT path as one extra split
+    a.key_base = a.s;
+    a.keys_per_split = a.m;
+    a.n_splits = 1;
+    a.split_base = a.tc_splits;
+    total_splits = a.tc_splits + 1;
+  }
   dim3 grid(a.n_splits, a.Hkv, row_blocks);
   const int smem = (128 * (a.dkp + 4) + 2 * 32 * (a.dkp + 4) + 128 * 33) * 4;
   if (a.dkp == 128) {
@@ -512,7 +555,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   }
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_pass1");
-  s1_attn_combine<<<dim3(a.R, a.Hkv), 128, 0, st>>>(a.Opart, a.Mpart, a.Lpart, a.n_splits, a.Hkv, a.R, a.m, a.G, a.H,
+  s1_attn_combine<<<dim3(a.R, a.Hkv), 128, 0, st>>>(a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");

@@ -49,6 +49,21 @@ def _cos(a, b):
     return float(a @ b / (np.linalg.norm(a) * np.linalg.norm(b) + 1e-300))
 
 
+def _report(**kw):
+    """Append measured parity numbers (DESIGN.md quotes them) to a JSONL report."""
+    import json
+    import os
+    path = os.environ.get("PKV_PARITY_REPORT", "gpurun_out/parity_report.jsonl")
+    try:
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        kw["s1_path"] = "simt" if os.environ.get("PKV_S1_SIMT") else "tcgen05-split3"
+        with open(path, "a") as f:
+            f.write(json.dumps({k: (float(v) if isinstance(v, (np.floating, float)) else v) for k, v in kw.items()})
+                    + "\n")
+    except OSError:
+        pass
+
+
 def _selection_ok(sel_gpu, sel_ref, fused_ref, k):
     kth = np.sort(fused_ref)[::-1][k - 1] if k else 0.0
     band = np.abs(fused_ref - kth) <= REL_TOL * abs(kth)
@@ -91,8 +106,12 @@ def test_prophet_slice_matches_oracle(built, case):
     cache = P.assemble(dch, cfg, fp32_taps=True)
     scores = P.score_prophet(mw, cfg, cache, query)
     rel = np.abs(scores.per_layer - per_ref) / np.maximum(np.abs(per_ref), 1e-30)
-    assert rel.max() <= REL_TOL, f"per-layer score rel err {rel.max():.3e}"
+    frel = np.abs(scores.fused - fused_ref) / np.maximum(np.abs(fused_ref), 1e-30)
     sel = P.select_top_p(scores, p)
+    kth = np.sort(fused_ref)[::-1][k - 1] if k else 0.0
+    band = int(np.sum(np.abs(fused_ref - kth) <= REL_TOL * abs(kth)))
+    sym = len(set(sel.indices) ^ set(sel_ref))
+    assert rel.max() <= REL_TOL, f"per-layer score rel err {rel.max():.3e}"
     assert sel.k == k
     assert _selection_ok(sel.indices, sel_ref, fused_ref, k)
     # on identical fused input the device top-k is the reference rule, bit for bit
@@ -105,15 +124,21 @@ def test_prophet_slice_matches_oracle(built, case):
     O.repair(w, cfg_o, cache_o, sel.indices, capture=cap)
     lg_ref, _ = O.finalize(w, cfg_o, cache_o, query)
     ix = np.asarray(sel.indices)
+    kv_err, kv_cos = 0.0, 1.0
     for li in range(cfg_o.n_layers):
         gk = cache.keys_rebased[li][ix]
         gv = cache.values[li][ix]
+        kv_err = max(kv_err, np.abs(gk - cap["k"][li]).max(), np.abs(gv - cap["v"][li]).max())
+        kv_cos = min(kv_cos, _cos(gk, cap["k"][li]), _cos(gv, cap["v"][li]))
         assert np.abs(gk - cap["k"][li]).max() <= KV_ABS and _cos(gk, cap["k"][li]) >= COS_MIN, li
         assert np.abs(gv - cap["v"][li]).max() <= KV_ABS and _cos(gv, cap["v"][li]) >= COS_MIN, li
         # untouched entries keep the exact assembled keys
         rest = np.setdiff1d(np.arange(cache.context_length), ix)
         assert np.array_equal(cache.keys_rebased[li][rest], cache_o.keys[li][rest])
     err = np.abs(fin.first_logits - lg_ref).max()
+    _report(case=case, s=cache.context_length, k=k, per_layer_max_rel=rel.max(), fused_max_rel=frel.max(),
+            tie_band=band, sel_symdiff=sym, kv_max_abs=kv_err, kv_min_cos=kv_cos, logits_max_abs=err,
+            logits_cos=_cos(fin.first_logits, lg_ref))
     assert err <= KV_ABS and _cos(fin.first_logits, lg_ref) >= COS_MIN, err
     assert cache.recomputed[:, ix].all() and cache.recomputed.sum() == cfg_o.n_layers * len(ix)
 
