@@ -99,6 +99,8 @@ typedef struct pkv_cache {
   int32_t rope_len;          /* positions covered (>= s + query length) */
   const uint8_t* recomputed; /* nullable [s]: 1 = entry repaired by Stage II (read from the pool
                                 even when a query pass reads the others from the chunk store) */
+  void* k2_pool;             /* residual key planes, same layout as k_pool: the f32 key is exactly */
+  void* k3_pool;             /* k_pool + k2_pool + k3_pool (bf16 each); used by the narrow passes  */
 } pkv_cache;
 
 /* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */

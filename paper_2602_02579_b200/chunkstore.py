@@ -185,6 +185,10 @@ class AssembledCache:
         self._d_pages = torch.arange(n_pages, dtype=torch.int32, device=dev)
         self.k_pool = torch.zeros((L, Hkv, self.pool_tokens, dkp), dtype=torch.bfloat16, device=dev)
         self.v_pool = torch.zeros_like(self.k_pool)
+        # residual planes of every f32 key (k_pool + k2 + k3 == f32 key exactly), read by
+        # the fp32-faithful narrow passes on the tensor cores
+        self.k2_pool = torch.zeros_like(self.k_pool)
+        self.k3_pool = torch.zeros_like(self.k_pool)
         self.rope_len, self._rcos, self._rsin = rope_device_tables(config.rope_theta, config.head_dim,
                                                                    self.pool_tokens)
         if fp32_taps == "auto":
@@ -193,9 +197,7 @@ class AssembledCache:
         self._taps: dict = {}  # layer -> list of (idx np.int64, k f32 tensor, v f32 tensor)
         self._c_chunks = _lib.Chunks(self._d_kptr.data_ptr(), self._d_vptr.data_ptr(), self._d_len.data_ptr(),
                                      self._d_src_chunk.data_ptr(), self._d_src_local.data_ptr(), len(chunks))
-        self._c_cache = _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens,
-                                   self._d_pages.data_ptr(), s, self._d_tokens.data_ptr(), self._rcos.data_ptr(),
-                                   self._rsin.data_ptr(), self.rope_len, self._d_recomp.data_ptr())
+        self._c_cache = self._make_c_cache()
         self._cfg_c = config.c_struct()
         self.query_kv = None  # set by finalize_query: (fresh_k, fresh_v) f32 device [L][m][Hkv][dk]
 
@@ -259,7 +261,7 @@ class AssembledCache:
         torch = _lib.require_cuda()
         new_tokens = -(-need // PAGE) * PAGE
         L, Hkv, dkp = self.k_pool.shape[0], self.k_pool.shape[1], self.k_pool.shape[3]
-        for name in ("k_pool", "v_pool"):
+        for name in ("k_pool", "v_pool", "k2_pool", "k3_pool"):
             old = getattr(self, name)
             new = torch.zeros((L, Hkv, new_tokens, dkp), dtype=old.dtype, device=old.device)
             new[:, :, : self.pool_tokens] = old
@@ -268,10 +270,13 @@ class AssembledCache:
         self._d_pages = torch.arange(new_tokens // PAGE, dtype=torch.int32, device=self.device)
         self.rope_len, self._rcos, self._rsin = rope_device_tables(self.config.rope_theta, self.config.head_dim,
                                                                    new_tokens)
-        self._c_cache = _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens,
-                                   self._d_pages.data_ptr(), self.context_length, self._d_tokens.data_ptr(),
-                                   self._rcos.data_ptr(), self._rsin.data_ptr(), self.rope_len,
-                                   self._d_recomp.data_ptr())
+        self._c_cache = self._make_c_cache()
+
+    def _make_c_cache(self):
+        return _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self._d_pages.data_ptr(),
+                          self.context_length, self._d_tokens.data_ptr(), self._rcos.data_ptr(),
+                          self._rsin.data_ptr(), self.rope_len, self._d_recomp.data_ptr(), self.k2_pool.data_ptr(),
+                          self.k3_pool.data_ptr())
 
 
 def _as_chunk(c) -> ChunkKV:

@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
                                                        const double* __restrict__ rcos,
                                                        const double* __restrict__ rsin, const int32_t* page_table,
                                                        __nv_bfloat16* k_pool, __nv_bfloat16* v_pool,
-                                                       long pool_tokens) {
+                                                       long pool_tokens, __nv_bfloat16* k2_pool,
+                                                       __nv_bfloat16* k3_pool) {
   const int vecs = dkp / 8;
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)s * vecs) return;
@@ -53,29 +54,35 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
       const long so = (src_row + h) * dkp + c * 8;
       uint4 kv = __ldg(reinterpret_cast<const uint4*>(kb + so));
       uint4 vv = __ldg(reinterpret_cast<const uint4*>(vb + so));
-      uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w}, o[4];
+      uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w}, o[4], o2[4], o3[4];
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
         float e = bf16_lo(w[p]), od = bf16_hi(w[p]);
         float re = e, ro = od;
         if (2 * (c * 4 + p) < head_dim) rope_pair64(e, od, cs[p], sn[p], re, ro);
-        o[p] = pack_bf16(re, ro);
+        // plane 1 (the bf16 cache) is RNE(f32 key); planes 2/3 carry the rest exactly
+        split3_pack(re, ro, o[p], o2[p], o3[p]);
       }
       const long dofs = (dst_layer + (long)h * pool_tokens + slot) * dkp + c * 8;
       *reinterpret_cast<uint4*>(k_pool + dofs) = make_uint4(o[0], o[1], o[2], o[3]);
       *reinterpret_cast<uint4*>(v_pool + dofs) = vv;
+      if (k2_pool != nullptr) {
+        *reinterpret_cast<uint4*>(k2_pool + dofs) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+        *reinterpret_cast<uint4*>(k3_pool + dofs) = make_uint4(o3[0], o3[1], o3[2], o3[3]);
+      }
     }
   }
 }
 
 int assemble_launch(const ChunkView& cv, int s, int L, int Hkv, int dkp, int head_dim, const double* rcos,
                     const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
-                    cudaStream_t stream) {
+                    void* k2_pool, void* k3_pool, cudaStream_t stream) {
   if (s <= 0) return PKV_OK;
   const long threads = (long)s * (dkp / 8);
   assemble_kernel<<<ceil_div(threads, 128), 128, 0, stream>>>(
       cv, s, L, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__nv_bfloat16*>(k_pool),
-      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens);
+      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, reinterpret_cast<__nv_bfloat16*>(k2_pool),
+      reinterpret_cast<__nv_bfloat16*>(k3_pool));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("assemble_kernel");
   return PKV_OK;
@@ -131,26 +138,38 @@ int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int
 // scatter fp32 rows [n][Hkv][dk] into the bf16 cache at token indices idx
 __global__ void scatter_kernel(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim,
                                const float* src, const int32_t* page_table, __nv_bfloat16* pool,
-                               long pool_tokens) {
+                               long pool_tokens, __nv_bfloat16* pool2, __nv_bfloat16* pool3) {
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long total = (long)n * Hkv * dkp;
+  const long total = (long)n * Hkv * (dkp / 2);
   if (gid >= total) return;
-  const int d = (int)(gid % dkp);
-  const long rh = gid / dkp;
+  const int d = 2 * (int)(gid % (dkp / 2));
+  const long rh = gid / (dkp / 2);
   const int h = (int)(rh % Hkv);
   const int r = (int)(rh / Hkv);
   const int t = idx[r];
   const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
-  const float v = d < head_dim ? src[((long)r * Hkv + h) * head_dim + d] : 0.f;
-  pool[(((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d] = __float2bfloat16_rn(v);
+  const float* row = src + ((long)r * Hkv + h) * head_dim;
+  const float v0 = d < head_dim ? row[d] : 0.f, v1 = d + 1 < head_dim ? row[d + 1] : 0.f;
+  uint32_t p1, p2, p3;
+  split3_pack(v0, v1, p1, p2, p3);
+  const long o = (((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d;
+  *reinterpret_cast<uint32_t*>(pool + o) = p1;
+  if (pool2 != nullptr) {
+    *reinterpret_cast<uint32_t*>(pool2 + o) = p2;
+    *reinterpret_cast<uint32_t*>(pool3 + o) = p3;
+  }
 }
 
+// pool2/pool3 (nullable): residual planes of a key pool
 int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim, const float* src,
-                   const int32_t* page_table, void* pool, long pool_tokens, cudaStream_t stream) {
-  const long total = (long)n * Hkv * dkp;
+                   const int32_t* page_table, void* pool, long pool_tokens, void* pool2, void* pool3,
+                   cudaStream_t stream) {
+  const long total = (long)n * Hkv * (dkp / 2);
   if (total <= 0) return PKV_OK;
   scatter_kernel<<<ceil_div(total, 256), 256, 0, stream>>>(idx, n, layer, Hkv, dkp, head_dim, src, page_table,
-                                                          reinterpret_cast<__nv_bfloat16*>(pool), pool_tokens);
+                                                          reinterpret_cast<__nv_bfloat16*>(pool), pool_tokens,
+                                                          reinterpret_cast<__nv_bfloat16*>(pool2),
+                                                          reinterpret_cast<__nv_bfloat16*>(pool3));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("scatter_kernel");
   return PKV_OK;

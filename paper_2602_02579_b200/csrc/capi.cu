@@ -265,7 +265,7 @@ int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c
   if (c->recomputed) cudaMemsetAsync(const_cast<uint8_t*>(c->recomputed), 0, (size_t)c->s, st);
   ScopedTimer t__(T_ASSEMBLE, st);
   return assemble_launch(cv, c->s, cfg->n_layers, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos, c->rope_sin,
-                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, st);
+                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, c->k2_pool, c->k3_pool, st);
 }
 
 int pkv_cache_view(const pkv_config* cfg, const pkv_cache* c, const pkv_chunks* ch, int32_t layer, int32_t is_key,
@@ -288,11 +288,11 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer
   if (rc) return rc;
   if (layer < 0 || layer >= cfg->n_layers) return set_error(PKV_ERR_ARGUMENT, "layer out of range");
   rc = scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_k, c->page_table, c->k_pool,
-                      c->pool_tokens, S(stream));
+                      c->pool_tokens, c->k2_pool, c->k3_pool, S(stream));
   if (rc) return rc;
   if (c->recomputed && (rc = mark_launch(idx, n, const_cast<uint8_t*>(c->recomputed), S(stream))) != 0) return rc;
   return scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_v, c->page_table, c->v_pool,
-                        c->pool_tokens, S(stream));
+                        c->pool_tokens, nullptr, nullptr, S(stream));
 }
 
 // ------------------------------------------------------------------ query pass
@@ -333,7 +333,8 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
     const int target = std::max(1, 2 * num_sms() / std::max(1, Hkv * row_blocks));
     w.tc_keys_per_split = std::max(64, ceil_div(ceil_div(s, target), 64) * 64);
     w.tc_splits = (simt_only || s == 0) ? 0 : ceil_div(s, w.tc_keys_per_split);
-    if (w.tc_splits > 0) w.n_splits = w.tc_splits + 1;
+    // partial buffers sized for either path (the caller's cache decides which runs)
+    w.n_splits = std::max(w.n_splits, w.tc_splits + 1);
   }
   const int row_blocks = ceil_div(R, 128);
   (void)row_blocks;
@@ -388,10 +389,14 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
     __nv_bfloat16* vp = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
     const bool append = (flags & PKV_QP_APPEND_KV) != 0;
-    TTRY(T_QP_MISC, query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v, append ? kp : nullptr,
-                         append ? vp : nullptr, c->pool_tokens, c->page_table,
-                         fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
-                         fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, st));
+    const bool planes = c->k2_pool != nullptr && c->k3_pool != nullptr;
+    void* k2p = planes ? reinterpret_cast<__nv_bfloat16*>(c->k2_pool) + l * layer_pool : nullptr;
+    void* k3p = planes ? reinterpret_cast<__nv_bfloat16*>(c->k3_pool) + l * layer_pool : nullptr;
+    TTRY(T_QP_MISC, query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v,
+                                     append ? kp : nullptr, append ? vp : nullptr, c->pool_tokens, c->page_table,
+                                     fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
+                                     fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, append ? k2p : nullptr,
+                                     append ? k3p : nullptr, st));
     S1Attn a{};
     a.q = w.q;
     a.m = m;
@@ -403,12 +408,18 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.s = s;
     a.s_tot = s + m;
     a.R = m * G;
+    const int tc_splits = planes ? w.tc_splits : 0;  // the tensor-core path needs the key planes
     a.keys_per_split = w.keys_per_split;
-    a.n_splits = w.tc_splits > 0 ? 1 : w.n_splits;
+    a.n_splits = tc_splits > 0 ? 1 : ceil_div(s + m, w.keys_per_split);
     a.key_base = 0;
     a.split_base = 0;
-    a.tc_splits = w.tc_splits;
+    a.tc_splits = tc_splits;
     a.tc_keys_per_split = w.tc_keys_per_split;
+    a.k1_all = c->k_pool;
+    a.k2_all = c->k2_pool;
+    a.k3_all = c->k3_pool;
+    a.v_all = c->v_pool;
+    a.pool_rows_total = (long)cf.n_layers * Hkv * c->pool_tokens;
     a.scale = (float)(1.0 / std::sqrt((double)dk));
     a.src_chunks = (flags & PKV_QP_FROM_CHUNKS) ? 1 : 0;
     a.recomp = c->recomputed;
@@ -531,6 +542,10 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     g.page_table = c->page_table;
     g.tap_k = tap_k ? tap_k + (long)l * k * Hkv * dk : nullptr;
     g.tap_v = tap_v ? tap_v + (long)l * k * Hkv * dk : nullptr;
+    if (c->k2_pool != nullptr && c->k3_pool != nullptr) {
+      g.k2_pool = reinterpret_cast<__nv_bfloat16*>(c->k2_pool) + l * layer_pool;
+      g.k3_pool = reinterpret_cast<__nv_bfloat16*>(c->k3_pool) + l * layer_pool;
+    }
     // K/V of every selected token are in the cache before this layer's attention
     TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
     TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,

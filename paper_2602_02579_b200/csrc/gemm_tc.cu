@@ -61,7 +61,7 @@ std::mutex g_map_mu;
 std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 }  // namespace
 
-static bool cached_tmap(CUtensorMap* out, const void* base, long rows, long cols, long stride, int box_rows) {
+bool cached_tmap(CUtensorMap* out, const void* base, long rows, long cols, long stride, int box_rows) {
   MapKey key{base, rows, cols, stride, box_rows};
   std::lock_guard<std::mutex> lk(g_map_mu);
   auto it = g_maps.find(key);

@@ -39,6 +39,8 @@ struct GemmArgs {
   const int32_t* page_table;
   float* tap_k;               // optional fp32 [M][Hkv][dk]
   float* tap_v;
+  __nv_bfloat16* k2_pool;     // optional residual key planes (layer base), see s1_attn_tc.cu
+  __nv_bfloat16* k3_pool;
 };
 
 template <int BN>
@@ -266,9 +268,9 @@ __global__ void __launch_bounds__(192, 1)
                 }
               }
             }
-            uint32_t packed[16];
+            uint32_t packed[16], pk2[16], pk3[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) packed[j] = pack_bf16(vals[2 * j], vals[2 * j + 1]);
+            for (int j = 0; j < 16; ++j) split3_pack(vals[2 * j], vals[2 * j + 1], packed[j], pk2[j], pk3[j]);
             __nv_bfloat16* dst;
             if (head_all < H) {
               dst = reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col0;
@@ -276,7 +278,17 @@ __global__ void __launch_bounds__(192, 1)
               const int g = is_v ? head_all - H - Hkv : head_all - H;
               const long slot = (long)args.page_table[pos >> 7] * 128 + (pos & 127);
               __nv_bfloat16* pool = is_v ? args.v_pool : args.k_pool;
-              dst = pool + ((long)g * args.pool_tokens + slot) * dkp + d0;
+              const long po = ((long)g * args.pool_tokens + slot) * dkp + d0;
+              dst = pool + po;
+              if (!is_v && args.k2_pool != nullptr) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  reinterpret_cast<uint4*>(args.k2_pool + po)[j] =
+                      make_uint4(pk2[4 * j], pk2[4 * j + 1], pk2[4 * j + 2], pk2[4 * j + 3]);
+                  reinterpret_cast<uint4*>(args.k3_pool + po)[j] =
+                      make_uint4(pk3[4 * j], pk3[4 * j + 1], pk3[4 * j + 2], pk3[4 * j + 3]);
+                }
+              }
               float* tap = is_v ? args.tap_v : args.tap_k;
               if (tap != nullptr) {
                 float* tp = tap + ((long)row * Hkv + g) * args.head_dim;
@@ -309,5 +321,7 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda_rows, const void* B,
                    cudaStream_t stream);
 bool make_tmap_2d(CUtensorMap* map, const void* base, long rows, long cols, long row_stride_elems, int box_rows,
                   int box_cols);
+// encoded once per (buffer, shape), 128B swizzle, 64-column boxes
+bool cached_tmap(CUtensorMap* out, const void* base, long rows, long cols, long stride, int box_rows);
 
 }  // namespace pkv

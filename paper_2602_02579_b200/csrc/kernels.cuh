@@ -13,53 +13,34 @@ struct ChunkView {
 };
 int assemble_launch(const ChunkView& cv, int s, int L, int Hkv, int dkp, int head_dim, const double* rcos,
                     const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
-                    cudaStream_t stream);
+                    void* k2_pool, void* k3_pool, cudaStream_t stream);
 int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
                       const double* rcos, const double* rsin, const int32_t* page_table, const void* pool,
                       long pool_tokens, int is_key, float* out, cudaStream_t stream);
 int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim, const float* src,
-                   const int32_t* page_table, void* pool, long pool_tokens, cudaStream_t stream);
+                   const int32_t* page_table, void* pool, long pool_tokens, void* pool2, void* pool3,
+                   cudaStream_t stream);
+int mark_launch(const int32_t* idx, int n, uint8_t* flags, cudaStream_t st);
 int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, cudaStream_t st);
 int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
                    void* ybf, cudaStream_t st);
 int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, long ldy, int mode, cudaStream_t st);
 int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
-                     const int32_t* page_table, float* fresh_k, float* fresh_v, cudaStream_t st);
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, void* k3_pool,
+                     cudaStream_t st);
 int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st);
+
+// SIMT fp32 narrow-pass attention (all keys, or only the fresh query keys when
+// the context keys run on the tensor cores)
 struct S1Attn {
   const float* q;
   int m, H, Hkv, G, dk, dkp, s, s_tot, R, keys_per_split, n_splits;
-  int key_base, split_base;        // SIMT pass: first key / first partial index
-  int tc_splits, tc_keys_per_split;  // >0: context keys on tcgen05 (s1_attn_tc), fresh keys on SIMT
+  int key_base, split_base;          // first key / first partial index of this launch
+  int tc_splits, tc_keys_per_split;  // >0: context keys on tcgen05 (s1_attn_tc), fresh keys here
   float scale;
   int src_chunks;
   const uint8_t* recomp;  // nullable [s]: repaired entries come from the pool
-  const uint64_t* ck;
-  const uint64_t* cv;
-  const int32_t* src_chunk;
-  const int32_t* src_local;
-  const int32_t* chunk_len;
-  const double* rcos;
-  const double* rsin;
-  const __nv_bfloat16* k_pool;
-  const __nv_bfloat16* v_pool;
-  long pool_tokens;
-  const int32_t* page_table;
-  int layer;
-  const float* fk;
-  const float* fv;
-  float* S;
-  float* Opart;
-  float* Mpart;
-  float* Lpart;
-};
-struct S1TcArgs {
-  const float* q;  // [m][H][DKP] rotated fp32
-  int m, H, Hkv, G, dk, R, s, s_tot, keys_per_split, n_splits;
-  float scale;
-  int src_chunks;
-  const uint8_t* recomp;
   const uint64_t* ck;
   const uint64_t* cv;
   const int32_t* src_chunk;
@@ -72,12 +53,35 @@ struct S1TcArgs {
   long pool_tokens;
   const int32_t* page_table;
   int layer;
+  const float* fk;
+  const float* fv;
+  float* S;
+  float* Opart;
+  float* Mpart;
+  float* Lpart;
+  // whole-pool bases for the tensor-core path (TMA)
+  const void* k1_all;
+  const void* k2_all;
+  const void* k3_all;
+  const void* v_all;
+  long pool_rows_total;
+};
+
+// tensor-core narrow-pass attention over the context keys [0, s)
+struct S1TcArgs {
+  const float* q;  // [m][H][DKP] rotated fp32
+  int m, H, Hkv, G, dk, R, s, s_tot, keys_per_split, n_splits;
+  float scale;
+  long kv_row0;  // first pool row of this layer: layer * Hkv * pool_tokens
+  long pool_tokens;
+  const int32_t* page_table;
   float* S;  // [Hkv][R][s_tot] or null
   float* Opart;
   float* Mpart;
   float* Lpart;
 };
-int s1_attn_tc_launch(const S1TcArgs& a, cudaStream_t st);
+int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* k3, const void* v,
+                      long pool_rows_total, int dkp, cudaStream_t st);
 int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
                         float* per_layer, int renorm, cudaStream_t st);
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st);
@@ -88,6 +92,5 @@ int topk_launch(const float* v, int n, int k, int32_t* out, int32_t* status, cud
 int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H, int Hkv, int head_dim, int dkp,
                    const void* k_pool, const void* v_pool, long pool_rows_total, long pool_tokens, int layer,
                    const int32_t* page_table, cudaStream_t stream);
-
 
 }  // namespace pkv

@@ -1,62 +1,54 @@
 // fp32-faithful narrow-pass attention on tcgen05 (reference model.py:278-308 as
 // called by query_pass model.py:370-402, i.e. score_prophet and finalize_query).
 //
-// The reference computes q.k and p.v in float64 on f32 inputs.  Here every fp32
+// The reference computes q.k and p.v in float64 on f32 inputs.  Every fp32
 // operand x is split exactly into three bf16 planes x = xh + xm + xl (24 bits of
-// significand), so
+// significand), so on the bf16 tensor cores with fp32 accumulation in TMEM
 //     Q K^T  = Qh Kh + Qh Km + Qm Kh + Qh Kl + Qm Km + Ql Kh   (+ terms < 2^-24 rel.)
 //     P V    = Ph V + Pm V + Pl V                                (V is bf16-exact)
-// on the bf16 tensor cores with fp32 accumulation in TMEM.  Only the context keys
-// [0, s) run here; the m fresh query keys (fp32 V) are a separate SIMT split.
+// The key planes live in the cache: plane 1 is the bf16 K pool itself (RNE of the
+// f32 key), planes 2/3 are written next to it by assembly, Stage II and
+// replace_entries.  Only the context keys [0, s) run here; the m fresh query keys
+// (fp32 K/V) are one extra SIMT split.
 //
 // CTA = (KV head g, key split): 128 rows r = j*m + i (query head g*G+j, query i),
-// 64-key tiles, 2-stage smem ring.
-//   warps 0-3  producers: load K (chunk store: unrotated bf16 + float64 RoPE, or
-//              the repaired pool entry), split 3-way, write SW128 K-major planes
-//              and the V tile (MN-major for the PV MMA)
-//   warps 4-7  softmax: S row from TMEM, scale+mask, exact online softmax
-//              (expf), scores -> S workspace, P split -> TMEM (A operand of PV)
-//   warp 8     TMEM owner + MMA issuer
+// 64-key tiles (half a cache page), 2-stage TMA ring.
+//   warps 0-3  softmax: Q planes -> smem once; per tile S row from TMEM, scale +
+//              mask, exact online softmax (expf), scores -> S workspace, P split
+//              -> TMEM (A operand of the PV MMA), O rescale in TMEM on max growth
+//   warp 4     TMA producer: Kh, Km, Kl, V tiles
+//   warp 5     TMEM owner + MMA issuer (6 + 3 products per tile)
 #include <mutex>
 
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace pkv {
 
-
 template <int DKP>
 struct S1TcCfg {
   static constexpr int ATOMS = DKP / 64;
-  static constexpr int KT = 64;                       // keys per tile
-  static constexpr int QSPLIT = 128 * DKP * 2;        // one Q plane (128 rows)
-  static constexpr int PLANE = KT * DKP * 2;          // one K plane / the V tile
-  static constexpr int ATOM_Q = 128 * 128;            // bytes per 64-col atom of a Q plane
-  static constexpr int ATOM_K = KT * 128;             // bytes per 64-col atom of a K/V plane
-  static constexpr int STAGE = 4 * PLANE;             // Kh, Km, Kl, V
+  static constexpr int KT = 64;                 // keys per tile
+  static constexpr int QSPLIT = 128 * DKP * 2;  // one Q plane (128 rows)
+  static constexpr int PLANE = KT * DKP * 2;    // one K plane / the V tile
+  static constexpr int ATOM_Q = 128 * 128;      // bytes per 64-col atom of a Q plane
+  static constexpr int ATOM_K = KT * 128;       // bytes per 64-col atom of a K/V plane
+  static constexpr int STAGE = 4 * PLANE;       // Kh, Km, Kl, V
   static constexpr int STAGES = 2;
   static constexpr int SMEM = 3 * QSPLIT + STAGES * STAGE + 1024 + 256;
   // TMEM columns: S0 [0,64) S1 [64,128) O [128,128+DKP) P planes [256,352)
   static constexpr int T_S = 0, T_O = 128, T_P = 256;
 };
 
-__device__ __forceinline__ void split3_bf(float x, uint32_t& h, uint32_t& m, uint32_t& l) {
-  __nv_bfloat16 a = __float2bfloat16_rn(x);
-  float r1 = x - __bfloat162float(a);
-  __nv_bfloat16 b = __float2bfloat16_rn(r1);
-  float r2 = r1 - __bfloat162float(b);
-  __nv_bfloat16 c = __float2bfloat16_rn(r2);
-  h = *reinterpret_cast<uint16_t*>(&a);
-  m = *reinterpret_cast<uint16_t*>(&b);
-  l = *reinterpret_cast<uint16_t*>(&c);
-}
-
 template <int DKP>
-__global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
+__global__ void __launch_bounds__(192, 1)
+    s1_attn_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
+                      const __grid_constant__ CUtensorMap tK3, const __grid_constant__ CUtensorMap tV, S1TcArgs a) {
   using C = S1TcCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                     // 3 planes
-  uint8_t* sKV = smem + 3 * C::QSPLIT;    // STAGES x {Kh, Km, Kl, V}
+  uint8_t* sQ = smem;                   // 3 planes
+  uint8_t* sKV = smem + 3 * C::QSPLIT;  // STAGES x {Kh, Km, Kl, V}
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::STAGE);
   uint64_t* kv_full = bars;
   uint64_t* kv_empty = bars + C::STAGES;
@@ -77,7 +69,7 @@ __global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) {
-      mbar_init(&kv_full[i], 4);
+      mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -89,73 +81,37 @@ __global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
     mbar_init(q_full, 4);
     fence_barrier_init();
   }
-  if (warp == 8) tmem_alloc(tmem_slot, 512);
+  if (warp == 5) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
-    // ------------------------------------------------------------- producers
-    const int tid = threadIdx.x;  // 0..127
-    constexpr int VECS = DKP / 8;
-    const int half = a.dk >> 1;
-    for (int j = 0; j < n_tiles; ++j) {
-      const int st = j % C::STAGES;
-      mbar_wait(&kv_empty[st], ((uint32_t)(j / C::STAGES) & 1) ^ 1);
-      uint8_t* base = sKV + st * C::STAGE;
-      for (int e = tid; e < C::KT * VECS; e += 128) {
-        const int kr = e / VECS, c8 = e - kr * VECS;
-        const int t = k_begin + j * C::KT + kr;
-        uint32_t kh[4], km[4], kl[4];
-        uint4 vraw = make_uint4(0, 0, 0, 0);
-        if (t < k_end) {
-          const bool from_chunk = a.src_chunks && !(a.recomp != nullptr && a.recomp[t]);
-          uint4 kraw;
-          if (from_chunk) {
-            const int ch = a.src_chunk[t], loc = a.src_local[t], tc = a.chunk_len[ch];
-            const long off = (((long)a.layer * tc + loc) * a.Hkv + g) * DKP + c8 * 8;
-            kraw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.ck[ch]) + off));
-            vraw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.cv[ch]) + off));
-          } else {
-            const long slot = (long)a.page_table[t >> 7] * 128 + (t & 127);
-            const long off = ((long)g * a.pool_tokens + slot) * DKP + c8 * 8;
-            kraw = *reinterpret_cast<const uint4*>(a.k_pool + off);
-            vraw = *reinterpret_cast<const uint4*>(a.v_pool + off);
-          }
-          const uint32_t kw[4] = {kraw.x, kraw.y, kraw.z, kraw.w};
+  if (warp == 4) {
+    // ----------------------------------------------------------- TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tK1);
+      tma_prefetch(&tK2);
+      tma_prefetch(&tK3);
+      tma_prefetch(&tV);
+      const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % C::STAGES;
+        mbar_wait(&kv_empty[st], ((uint32_t)(j / C::STAGES) & 1) ^ 1);
+        const int t0 = k_begin + j * C::KT;  // 64-aligned: inside one 128-token page
+        const int row = (int)(head_row + (long)a.page_table[t0 >> 7] * 128 + (t0 & 127));
+        uint8_t* base = sKV + st * C::STAGE;
+        mbar_expect_tx(&kv_full[st], C::STAGE);
 #pragma unroll
-          for (int p = 0; p < 4; ++p) {
-            float e0 = bf16_lo(kw[p]), e1 = bf16_hi(kw[p]);
-            const int pi = c8 * 4 + p;
-            if (from_chunk && pi < half) {
-              const double cs = a.rcos[(long)t * half + pi], sn = a.rsin[(long)t * half + pi];
-              const double de = e0, dd = e1;
-              e0 = (float)__dsub_rn(__dmul_rn(de, cs), __dmul_rn(dd, sn));
-              e1 = (float)__dadd_rn(__dmul_rn(de, sn), __dmul_rn(dd, cs));
-            }
-            uint32_t h0, m0, l0, h1, m1, l1;
-            split3_bf(e0, h0, m0, l0);
-            split3_bf(e1, h1, m1, l1);
-            kh[p] = h0 | (h1 << 16);
-            km[p] = m0 | (m1 << 16);
-            kl[p] = l0 | (l1 << 16);
-          }
-        } else {
-#pragma unroll
-          for (int p = 0; p < 4; ++p) kh[p] = km[p] = kl[p] = 0u;
+        for (int at = 0; at < C::ATOMS; ++at) {
+          tma_load_2d(base + at * C::ATOM_K, &tK1, &kv_full[st], at * 64, row);
+          tma_load_2d(base + C::PLANE + at * C::ATOM_K, &tK2, &kv_full[st], at * 64, row);
+          tma_load_2d(base + 2 * C::PLANE + at * C::ATOM_K, &tK3, &kv_full[st], at * 64, row);
+          tma_load_2d(base + 3 * C::PLANE + at * C::ATOM_K, &tV, &kv_full[st], at * 64, row);
         }
-        const uint32_t off = (c8 >> 3) * C::ATOM_K + sw128_offset(kr, (c8 & 7) * 8);
-        *reinterpret_cast<uint4*>(base + off) = make_uint4(kh[0], kh[1], kh[2], kh[3]);
-        *reinterpret_cast<uint4*>(base + C::PLANE + off) = make_uint4(km[0], km[1], km[2], km[3]);
-        *reinterpret_cast<uint4*>(base + 2 * C::PLANE + off) = make_uint4(kl[0], kl[1], kl[2], kl[3]);
-        *reinterpret_cast<uint4*>(base + 3 * C::PLANE + off) = vraw;
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&kv_full[st]);
     }
-  } else if (warp == 8) {
+  } else if (warp == 5) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KT);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
@@ -209,27 +165,22 @@ __global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
     }
   } else {
     // ---------------------------------------------------------------- softmax
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;  // TMEM lane == tile row
+    const int r = warp * 32 + lane;  // TMEM lane == tile row (warps 0-3)
     const int row = r0 + r;
     const bool valid = row < a.R;
     const int jh = valid ? row / a.m : 0, qi = valid ? row - jh * a.m : 0;
-    const uint32_t lb = (uint32_t)(quarter * 32) << 16;
+    const uint32_t lb = (uint32_t)(warp * 32) << 16;
     {  // Q planes
-      const float* src = a.q + ((long)qi * a.H + g * a.G + jh) * DKP;
+      const float4* src = reinterpret_cast<const float4*>(a.q + ((long)qi * a.H + g * a.G + jh) * DKP);
 #pragma unroll 1
       for (int c8 = 0; c8 < DKP / 8; ++c8) {
+        float4 x0 = valid ? src[2 * c8] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 x1 = valid ? src[2 * c8 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t h[4], m[4], l[4];
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          float e0 = valid ? src[c8 * 8 + 2 * p] : 0.f, e1 = valid ? src[c8 * 8 + 2 * p + 1] : 0.f;
-          uint32_t h0, m0, l0, h1, m1, l1;
-          split3_bf(e0, h0, m0, l0);
-          split3_bf(e1, h1, m1, l1);
-          h[p] = h0 | (h1 << 16);
-          m[p] = m0 | (m1 << 16);
-          l[p] = l0 | (l1 << 16);
-        }
+        split3_pack(x0.x, x0.y, h[0], m[0], l[0]);
+        split3_pack(x0.z, x0.w, h[1], m[1], l[1]);
+        split3_pack(x1.x, x1.y, h[2], m[2], l[2]);
+        split3_pack(x1.z, x1.w, h[3], m[3], l[3]);
         const uint32_t off = (c8 >> 3) * C::ATOM_Q + sw128_offset(r, (c8 & 7) * 8);
         *reinterpret_cast<uint4*>(sQ + off) = make_uint4(h[0], h[1], h[2], h[3]);
         *reinterpret_cast<uint4*>(sQ + C::QSPLIT + off) = make_uint4(m[0], m[1], m[2], m[3]);
@@ -260,6 +211,7 @@ __global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
       float tmax = -INFINITY;
 #pragma unroll
       for (int i = 0; i < C::KT; ++i) {
+        // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298
         const float x = (key0 + i < k_end) ? sv[i] * a.scale : -INFINITY;
         sv[i] = x;
         tmax = fmaxf(tmax, x);
@@ -282,12 +234,7 @@ __global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
       for (int i = 0; i < C::KT / 2; ++i) {
         const float p0 = expf(sv[2 * i] - m_new), p1 = expf(sv[2 * i + 1] - m_new);
         psum += p0 + p1;
-        uint32_t h0, m0, l0, h1, m1, l1;
-        split3_bf(p0, h0, m0, l0);
-        split3_bf(p1, h1, m1, l1);
-        ph[i] = h0 | (h1 << 16);
-        pm[i] = m0 | (m1 << 16);
-        pl[i] = l0 | (l1 << 16);
+        split3_pack(p0, p1, ph[i], pm[i], pl[i]);
       }
       if (j >= 1) {
         mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
@@ -340,31 +287,35 @@ __global__ void __launch_bounds__(288, 1) s1_attn_tc_kernel(S1TcArgs a) {
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 5) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
 
-int s1_attn_tc_launch(const S1TcArgs& a, cudaStream_t st) {
-  dim3 grid(a.n_splits, a.Hkv, ceil_div(a.R, 128));
+int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* k3, const void* v,
+                      long pool_rows_total, int dkp, cudaStream_t st) {
   if (a.n_splits <= 0) return PKV_OK;
-  if (a.dk > 128) return set_error(PKV_ERR_CONFIG, "head_dim > 128");
-  // the kernel template follows the padded head dim of the cache layout
-  const int dkp = a.dk <= 64 ? 64 : 128;
+  if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
+  dim3 grid(a.n_splits, a.Hkv, ceil_div(a.R, 128));
+  CUtensorMap m1, m2, m3, mv;
+  if (!cached_tmap(&m1, k1, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&m2, k2, pool_rows_total, dkp, dkp, 64) ||
+      !cached_tmap(&m3, k3, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&mv, v, pool_rows_total, dkp, dkp, 64))
+    return set_error(PKV_ERR_CUDA, "narrow pass: TMA encode failed");
   if (dkp == 128) {
     static std::once_flag once;
     std::call_once(once, [] {
-      cudaFuncSetAttribute(s1_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           S1TcCfg<128>::SMEM);
+      cudaFuncSetAttribute(s1_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<128>::SMEM);
     });
-    s1_attn_tc_kernel<128><<<grid, 288, S1TcCfg<128>::SMEM, st>>>(a);
-  } else {
+    s1_attn_tc_kernel<128><<<grid, 192, S1TcCfg<128>::SMEM, st>>>(m1, m2, m3, mv, a);
+  } else if (dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<64>::SMEM);
     });
-    s1_attn_tc_kernel<64><<<grid, 288, S1TcCfg<64>::SMEM, st>>>(a);
+    s1_attn_tc_kernel<64><<<grid, 192, S1TcCfg<64>::SMEM, st>>>(m1, m2, m3, mv, a);
+  } else {
+    return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", dkp);
   }
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_tc_kernel");

@@ -121,7 +121,8 @@ int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, 
 __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0,
                                  const double* rcos, const double* rsin, float* q, float* k, float* v,
                                  __nv_bfloat16* k_pool, __nv_bfloat16* v_pool, long pool_tokens,
-                                 const int32_t* page_table, float* fresh_k, float* fresh_v) {
+                                 const int32_t* page_table, float* fresh_k, float* fresh_v,
+                                 __nv_bfloat16* k2_pool, __nv_bfloat16* k3_pool) {
   const int heads = H + 2 * Hkv;
   const long total = (long)m * heads * (dkp / 2);
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -155,8 +156,14 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
   d[1] = o;
   if (k_pool != nullptr) {
     const long slot = (long)page_table[pos >> 7] * 128 + (pos & 127);
-    __nv_bfloat16* pd = (is_v ? v_pool : k_pool) + ((long)g * pool_tokens + slot) * dkp + 2 * pi;
-    *reinterpret_cast<uint32_t*>(pd) = pack_bf16(e, o);
+    const long po = ((long)g * pool_tokens + slot) * dkp + 2 * pi;
+    uint32_t p1, p2, p3;
+    split3_pack(e, o, p1, p2, p3);
+    *reinterpret_cast<uint32_t*>((is_v ? v_pool : k_pool) + po) = p1;
+    if (!is_v && k2_pool != nullptr) {
+      *reinterpret_cast<uint32_t*>(k2_pool + po) = p2;
+      *reinterpret_cast<uint32_t*>(k3_pool + po) = p3;
+    }
   }
   float* fr = is_v ? fresh_v : fresh_k;
   if (fr != nullptr && 2 * pi < dk) {
@@ -168,11 +175,13 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
 
 int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
-                     const int32_t* page_table, float* fresh_k, float* fresh_v, cudaStream_t st) {
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, void* k3_pool,
+                     cudaStream_t st) {
   const long total = (long)m * (H + 2 * Hkv) * (dkp / 2);
   query_qkv_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
       qkv, m, H, Hkv, dk, dkp, pos0, rcos, rsin, q, k, v, reinterpret_cast<__nv_bfloat16*>(k_pool),
-      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v);
+      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v,
+      reinterpret_cast<__nv_bfloat16*>(k2_pool), reinterpret_cast<__nv_bfloat16*>(k3_pool));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("query_qkv_kernel");
   return PKV_OK;
@@ -419,20 +428,34 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
 // per-row (max, denominator) used by the scoring reduction
 __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const float* Lpart, int splits, int Hkv,
                                 int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin) {
+  extern __shared__ float wsp[];  // [splits] rescale weight of each split
+  __shared__ float sM, sL;
   const int r = blockIdx.x, g = blockIdx.y;
-  float M = -INFINITY;
-  for (int sp = 0; sp < splits; ++sp) M = fmaxf(M, Mpart[((long)sp * Hkv + g) * R + r]);
-  float L = 0.f;
-  for (int sp = 0; sp < splits; ++sp) {
-    const long b = ((long)sp * Hkv + g) * R + r;
-    if (Mpart[b] != -INFINITY) L += Lpart[b] * expf(Mpart[b] - M);
+  if (threadIdx.x < 32) {
+    float M = -INFINITY;
+    for (int sp = threadIdx.x; sp < splits; sp += 32) M = fmaxf(M, Mpart[((long)sp * Hkv + g) * R + r]);
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    for (int sp = threadIdx.x; sp < splits; sp += 32) {
+      const long b = ((long)sp * Hkv + g) * R + r;
+      const float w = Mpart[b] != -INFINITY ? expf(Mpart[b] - M) : 0.f;
+      wsp[sp] = w;
+      L += Lpart[b] * w;
+    }
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (threadIdx.x == 0) {
+      sM = M;
+      sL = L;
+    }
   }
+  __syncthreads();
+  const float M = sM, L = sL;
   const int j = r / m, i = r - j * m;
   for (int d = threadIdx.x; d < dkp; d += blockDim.x) {
     float acc = 0.f;
     for (int sp = 0; sp < splits; ++sp) {
-      const long b = ((long)sp * Hkv + g) * R + r;
-      if (Mpart[b] != -INFINITY) acc += Opart[b * dkp + d] * expf(Mpart[b] - M);
+      const float w = wsp[sp];
+      if (w != 0.f) acc += Opart[(((long)sp * Hkv + g) * R + r) * dkp + d] * w;
     }
     out[((long)i * H + g * G + j) * dkp + d] = acc / L;
   }
@@ -509,25 +532,14 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.keys_per_split = a.tc_keys_per_split;
     t.n_splits = a.tc_splits;
     t.scale = a.scale;
-    t.src_chunks = a.src_chunks;
-    t.recomp = a.recomp;
-    t.ck = a.ck;
-    t.cv = a.cv;
-    t.src_chunk = a.src_chunk;
-    t.src_local = a.src_local;
-    t.chunk_len = a.chunk_len;
-    t.rcos = a.rcos;
-    t.rsin = a.rsin;
-    t.k_pool = a.k_pool;
-    t.v_pool = a.v_pool;
+    t.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
     t.pool_tokens = a.pool_tokens;
     t.page_table = a.page_table;
-    t.layer = a.layer;
     t.S = a.S;
     t.Opart = a.Opart;
     t.Mpart = a.Mpart;
     t.Lpart = a.Lpart;
-    int rc = s1_attn_tc_launch(t, st);
+    int rc = s1_attn_tc_launch(t, a.k1_all, a.k2_all, a.k3_all, a.v_all, a.pool_rows_total, a.dkp, st);
     if (rc) return rc;
     // the m fresh query keys (fp32 K/V) on the SIMT path as one extra split
     a.key_base = a.s;
@@ -555,7 +567,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   }
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_pass1");
-  s1_attn_combine<<<dim3(a.R, a.Hkv), 128, 0, st>>>(a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
+  s1_attn_combine<<<dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st>>>(a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");

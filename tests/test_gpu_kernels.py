@@ -131,6 +131,11 @@ def test_assembly_is_bf16_of_reference_keys(built):
         want_v = torch.from_numpy(ref.values[li]).cuda().to(torch.bfloat16)
         assert torch.equal(kp[li].view(torch.int16), want_k.view(torch.int16))
         assert torch.equal(vp[li].view(torch.int16), want_v.view(torch.int16))
+        # the three key planes sum to the reference's f32 key exactly
+        k2 = cache.k2_pool[li, :, :s, :128].permute(1, 0, 2).float()
+        k3 = cache.k3_pool[li, :, :s, :128].permute(1, 0, 2).float()
+        planes = ((kp[li].float() + k2) + k3).cpu().numpy()
+        assert np.array_equal(planes, ref.keys[li])
         # the f32 view equals the reference's keys_rebased bit for bit
         assert np.array_equal(cache.keys_rebased[li], ref.keys[li])
         assert np.array_equal(cache.values[li], ref.values[li])
