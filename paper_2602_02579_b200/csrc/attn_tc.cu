@@ -6,11 +6,13 @@
 // are the G query heads sharing g (GQA packing), row r = j*T + i (head g*G+j,
 // token b*T+i).  KV tiles are 128-token pages of the paged cache, TMA-loaded.
 //
-//   warps 0-3  softmax: tcgen05.ld S row, mask (key pos <= query pos), online
-//              softmax in the log2 domain, P -> smem (bf16, SW128 K-major),
+//   warps 0-7  softmax: warp w owns TMEM lane quarter w%4 (32 rows) and key
+//              columns [64*(w/4), +64) of each tile; both warps of a quarter read
+//              the full S row for the max (no exchange), then exponentiate their
+//              half in the log2 domain, P -> smem (bf16, SW128 K-major atom w/4),
 //              conditional O rescale in TMEM (only when the max grows by > 2^8)
-//   warp 4     TMA producer: K and V pages, 2-stage ring
-//   warp 5     TMEM owner + MMA issuer: S = Q K^T (double-buffered in TMEM),
+//   warp 8     TMA producer: K and V pages, 2-stage ring
+//   warp 9     TMEM owner + MMA issuer: S = Q K^T (double-buffered in TMEM),
 //              O += P V (V as MN-major B operand)
 #include <mutex>
 #include "kernels.cuh"
@@ -37,10 +39,11 @@ struct AttnCfg {
   static constexpr int P_BYTES = 128 * 128 * 2;
   static constexpr int STAGES = 2;
   static constexpr int SMEM = Q_BYTES + STAGES * 2 * KV_BYTES + P_BYTES + 1024 + 256;
+  static constexpr int SOFTMAX_WARPS = 8;
 };
 
 template <int DKP>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
   using Cfg = AttnCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
@@ -74,14 +77,14 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
+      mbar_init(&s_free[i], Cfg::SOFTMAX_WARPS);
     }
-    mbar_init(p_full, 4);
+    mbar_init(p_full, Cfg::SOFTMAX_WARPS);
     mbar_init(pv_full, 1);
-    mbar_init(q_full, 4);
+    mbar_init(q_full, Cfg::SOFTMAX_WARPS);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tS = tmem;          // S buffers at cols 0 and 128
   const uint32_t tO = tmem + 256;    // O accumulator
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
       tma_prefetch(&tmK);
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 128);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
@@ -158,69 +161,81 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------------------------------------------------------- softmax
-    const int r = threadIdx.x;  // 0..127 == TMEM lane
+    const int quarter = warp & 3, hc = warp >> 2;
+    const int r = quarter * 32 + lane;  // 0..127 == TMEM lane
     const int hj = r / a.T;
     const int ti = r - hj * a.T;
     const int tok = tok0 + ti;
     const bool valid = hj < a.G && tok < a.n_q;
     const int head = g * a.G + hj;
     const int my_pos = valid ? a.pos[tok] : max_pos;
-    const uint32_t lane_base = (uint32_t)((warp * 32) << 16);
+    const uint32_t lane_base = (uint32_t)((quarter * 32) << 16);
+    const float sl2 = a.scale_log2;
 
-    // Q row -> smem, 128B-swizzled K-major atoms
-    {
+    // Q row -> smem (this warp: 64-column atom hc), 128B-swizzled K-major
+    if (hc < Cfg::ATOMS) {
       const uint4* src = valid ? reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) : nullptr;
 #pragma unroll
-      for (int c = 0; c < DKP / 8; ++c) {
+      for (int c = hc * 8; c < hc * 8 + 8; ++c) {
         uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
-        const int at = c >> 3, ch = (c & 7) ^ (r & 7);
-        *reinterpret_cast<uint4*>(sQ + at * 16384 + r * 128 + ch * 16) = v;
+        const int ch = (c & 7) ^ (r & 7);
+        *reinterpret_cast<uint4*>(sQ + hc * 16384 + r * 128 + ch * 16) = v;
       }
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_full);
 
-    float m_run = -INFINITY, l_run = 0.f;
+    float m_run = -INFINITY, l_run = 0.f;  // m in log2 units; l: this warp's half of the row sum
     for (int j = 0; j < n_kv_tiles; ++j) {
       mbar_wait(&s_full[j & 1], (uint32_t)(j >> 1) & 1);
       tc_fence_after();
-      float s[128];
+      const int key0 = j * 128;
+      const bool unmasked = key0 + 127 <= min_pos;
+      // the partner half only contributes to the max
+      float omax = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld32(tS + lane_base + (j & 1) * 128 + c * 32, u);
+        const int col = (hc ^ 1) * 64 + c * 32;
+        tmem_ld32(tS + lane_base + (j & 1) * 128 + col, u);
+        tmem_ld_wait();
+        if (unmasked) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) omax = fmaxf(omax, __uint_as_float(u[i]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (key0 + col + i <= my_pos) omax = fmaxf(omax, __uint_as_float(u[i]));
+        }
+      }
+      float s[64];
+      float lmax = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t u[32];
+        const int col = hc * 64 + c * 32;
+        tmem_ld32(tS + lane_base + (j & 1) * 128 + col, u);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]);
+        for (int i = 0; i < 32; ++i) {
+          const float x = (unmasked || key0 + col + i <= my_pos) ? __uint_as_float(u[i]) : -INFINITY;
+          s[c * 32 + i] = x;
+          lmax = fmaxf(lmax, x);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[j & 1]);
 
-      const int key0 = j * 128;
-      float tmax = -INFINITY;
-      if (key0 + 127 <= min_pos) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          s[i] *= a.scale_log2;
-          tmax = fmaxf(tmax, s[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          s[i] = (key0 + i <= my_pos) ? s[i] * a.scale_log2 : -INFINITY;
-          tmax = fmaxf(tmax, s[i]);
-        }
-      }
-      const float m_new = fmaxf(m_run, tmax);
+      const float m_new = fmaxf(m_run, fmaxf(lmax, omax) * sl2);
       const bool grow = (m_new - m_run) > 8.0f;  // also true on the first tile (m_run = -inf)
       const float m_use = grow ? m_new : m_run;
       float rsum = 0.f;
-      uint32_t pk[64];
+      uint32_t pk[32];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        float p0 = ex2(s[2 * i] - m_use), p1 = ex2(s[2 * i + 1] - m_use);
+      for (int i = 0; i < 32; ++i) {
+        const float p0 = ex2(fmaf(s[2 * i], sl2, -m_use)), p1 = ex2(fmaf(s[2 * i + 1], sl2, -m_use));
         rsum += p0 + p1;
         pk[i] = pack_bf16(p0, p1);
       }
@@ -233,7 +248,7 @@ __global__ void __launch_bounds__(192, 1)
       if (any_grow) {
         const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
 #pragma unroll 1
-        for (int c = 0; c < DKP / 32; ++c) {
+        for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
           uint32_t u[32];
           tmem_ld32(tO + lane_base + c * 32, u);
           tmem_ld_wait();
@@ -242,14 +257,14 @@ __global__ void __launch_bounds__(192, 1)
           tmem_st32(tO + lane_base + c * 32, u);
         }
         tmem_st_wait();
-        if (grow && j > 0) l_run *= alpha;
       }
+      if (grow && j > 0) l_run *= ex2(m_run - m_use);
       if (grow) m_run = m_use;
       l_run += rsum;
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int at = c >> 3, ch = (c & 7) ^ (r & 7);
-        *reinterpret_cast<uint4*>(sP + at * 16384 + r * 128 + ch * 16) =
+      for (int c = 0; c < 8; ++c) {
+        const int ch = c ^ (r & 7);
+        *reinterpret_cast<uint4*>(sP + hc * 16384 + r * 128 + ch * 16) =
             make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       fence_proxy_async_smem();
@@ -259,9 +274,13 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_wait(pv_full, (uint32_t)(n_kv_tiles - 1) & 1);
     tc_fence_after();
-    const float inv_l = 1.f / l_run;
+    // row sum = both halves; all MMAs are done, so the P buffer is free for the exchange
+    float* red = reinterpret_cast<float*>(sP);
+    red[hc * 128 + r] = l_run;
+    named_bar_sync(1 + quarter, 64);
+    const float inv_l = 1.f / (red[r] + red[128 + r]);
 #pragma unroll 1
-    for (int c = 0; c < DKP / 32; ++c) {
+    for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
       uint32_t u[32];
       tmem_ld32(tO + lane_base + c * 32, u);
       tmem_ld_wait();
@@ -278,7 +297,7 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -294,7 +313,7 @@ static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnA
     err = cudaFuncSetAttribute(attn_tc_kernel<DKP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn smem attr: %s", cudaGetErrorString(err));
-  attn_tc_kernel<DKP><<<a.n_tiles * a.Hkv, 192, Cfg::SMEM, stream>>>(tk, tv, a);
+  attn_tc_kernel<DKP><<<a.n_tiles * a.Hkv, 320, Cfg::SMEM, stream>>>(tk, tv, a);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_tc_kernel");
   return PKV_OK;
@@ -322,8 +341,8 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   a.pool_tokens = pool_tokens;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
   CUtensorMap tk, tv;
-  if (!make_tmap_2d(&tk, k_pool, pool_rows_total, dkp, dkp, 128, 64) ||
-      !make_tmap_2d(&tv, v_pool, pool_rows_total, dkp, dkp, 128, 64))
+  if (!cached_tmap(&tk, k_pool, pool_rows_total, dkp, dkp, 128) ||
+      !cached_tmap(&tv, v_pool, pool_rows_total, dkp, dkp, 128))
     return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
   if (dkp == 128) return launch_attn<128>(tk, tv, a, stream);
   if (dkp == 64) return launch_attn<64>(tk, tv, a, stream);

@@ -13,11 +13,14 @@
 //
 // CTA = (KV head g, key split): 128 rows r = j*m + i (query head g*G+j, query i),
 // 64-key tiles (half a cache page), 2-stage TMA ring.
-//   warps 0-3  softmax: Q planes -> smem once; per tile S row from TMEM, scale +
-//              mask, exact online softmax (expf), scores -> S workspace, P split
-//              -> TMEM (A operand of the PV MMA), O rescale in TMEM on max growth
-//   warp 4     TMA producer: Kh, Km, Kl, V tiles
-//   warp 5     TMEM owner + MMA issuer (6 + 3 products per tile)
+//   warps 0-7  softmax: warp w owns TMEM lane quarter w%4 (32 rows) and key
+//              columns [32*(w/4), +32) of each tile; the two warps of a quarter
+//              exchange their row maxima through smem.  Q planes -> smem once;
+//              per tile: S from TMEM, scale + mask, exact online softmax,
+//              scores -> S workspace, P split -> TMEM (A operand of PV),
+//              O rescale in TMEM when the row max grows
+//   warp 8     TMA producer: Kh, Km, Kl, V tiles
+//   warp 9     TMEM owner + MMA issuer (6 + 3 products per tile)
 #include <mutex>
 
 #include "gemm_tc.cuh"
@@ -38,10 +41,11 @@ struct S1TcCfg {
   static constexpr int SMEM = 3 * QSPLIT + STAGES * STAGE + 1024 + 256;
   // TMEM columns: S0 [0,64) S1 [64,128) O [128,128+DKP) P planes [256,352)
   static constexpr int T_S = 0, T_O = 128, T_P = 256;
+  static constexpr int SOFTMAX_WARPS = 8;
 };
 
 template <int DKP>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     s1_attn_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
                       const __grid_constant__ CUtensorMap tK3, const __grid_constant__ CUtensorMap tV, S1TcArgs a) {
   using C = S1TcCfg<DKP>;
@@ -74,20 +78,20 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
+      mbar_init(&s_free[i], C::SOFTMAX_WARPS);
     }
-    mbar_init(p_full, 4);
+    mbar_init(p_full, C::SOFTMAX_WARPS);
     mbar_init(pv_full, 1);
-    mbar_init(q_full, 4);
+    mbar_init(q_full, C::SOFTMAX_WARPS);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ----------------------------------------------------------- TMA producer
     if (elect_one()) {
       tma_prefetch(&tK1);
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KT);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
@@ -165,15 +169,17 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ---------------------------------------------------------------- softmax
-    const int r = warp * 32 + lane;  // TMEM lane == tile row (warps 0-3)
+    constexpr float LOG2E = 1.4426950408889634f;
+    const int quarter = warp & 3, hc = warp >> 2;
+    const int r = quarter * 32 + lane;  // TMEM lane == tile row
     const int row = r0 + r;
     const bool valid = row < a.R;
     const int jh = valid ? row / a.m : 0, qi = valid ? row - jh * a.m : 0;
-    const uint32_t lb = (uint32_t)(warp * 32) << 16;
-    {  // Q planes
+    const uint32_t lb = (uint32_t)(quarter * 32) << 16;
+    {  // Q planes: this warp fills dims [hc*DKP/2, (hc+1)*DKP/2) of its rows
       const float4* src = reinterpret_cast<const float4*>(a.q + ((long)qi * a.H + g * a.G + jh) * DKP);
 #pragma unroll 1
-      for (int c8 = 0; c8 < DKP / 8; ++c8) {
+      for (int c8 = hc * DKP / 16; c8 < (hc + 1) * DKP / 16; ++c8) {
         float4 x0 = valid ? src[2 * c8] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 x1 = valid ? src[2 * c8 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
         uint32_t h[4], m[4], l[4];
@@ -190,49 +196,53 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(q_full);
     }
-    float m_run = -INFINITY, l_run = 0.f;
+    constexpr int HC = C::KT / 2;  // columns per warp
+    float m_run = -INFINITY, l_run = 0.f;  // l_run: this warp's half of the row sum
     float* srow = (a.S != nullptr && valid) ? a.S + ((long)g * a.R + row) * a.s_tot : nullptr;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&s_full[j & 1], (uint32_t)(j >> 1) & 1);
       tc_fence_after();
-      float sv[C::KT];
-#pragma unroll
-      for (int c = 0; c < C::KT / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tmem + lb + C::T_S + (j & 1) * C::KT + c * 32, u);
+      // both warps of a quarter read the whole 64-key row (cheap TMEM reads) so each
+      // has the tile max without an exchange; each then handles its 32 columns
+      float sv[HC];
+      float tmax = -INFINITY;
+      const int key0 = k_begin + j * C::KT + hc * HC;
+      {
+        uint32_t u[32], w[32];
+        tmem_ld32(tmem + lb + C::T_S + (j & 1) * C::KT + hc * HC, u);
+        tmem_ld32(tmem + lb + C::T_S + (j & 1) * C::KT + (hc ^ 1) * HC, w);
         tmem_ld_wait();
+        const int okey0 = k_begin + j * C::KT + (hc ^ 1) * HC;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(u[i]);
+        for (int i = 0; i < HC; ++i) {
+          // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298
+          const float x = (key0 + i < k_end) ? __uint_as_float(u[i]) * a.scale : -INFINITY;
+          const float y = (okey0 + i < k_end) ? __uint_as_float(w[i]) * a.scale : -INFINITY;
+          sv[i] = x;
+          tmax = fmaxf(tmax, fmaxf(x, y));
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[j & 1]);
-      const int key0 = k_begin + j * C::KT;
-      float tmax = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < C::KT; ++i) {
-        // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298
-        const float x = (key0 + i < k_end) ? sv[i] * a.scale : -INFINITY;
-        sv[i] = x;
-        tmax = fmaxf(tmax, x);
-      }
       if (srow != nullptr) {
-        if (key0 + C::KT <= k_end) {
+        if (key0 + HC <= k_end) {
 #pragma unroll
-          for (int i = 0; i < C::KT; i += 4)
+          for (int i = 0; i < HC; i += 4)
             *reinterpret_cast<float4*>(srow + key0 + i) = make_float4(sv[i], sv[i + 1], sv[i + 2], sv[i + 3]);
         } else {
-          for (int i = 0; i < C::KT && key0 + i < k_end; ++i) srow[key0 + i] = sv[i];
+          for (int i = 0; i < HC && key0 + i < k_end; ++i) srow[key0 + i] = sv[i];
         }
       }
       const float m_new = fmaxf(m_run, tmax);
       const bool grow = m_new > m_run;
-      const float corr = (m_run == -INFINITY) ? 0.f : expf(m_run - m_new);
+      const float corr = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_new) * LOG2E);
+      const float mb = m_new * LOG2E;
       float psum = 0.f;
-      uint32_t ph[C::KT / 2], pm[C::KT / 2], pl[C::KT / 2];
+      uint32_t ph[HC / 2], pm[HC / 2], pl[HC / 2];
 #pragma unroll
-      for (int i = 0; i < C::KT / 2; ++i) {
-        const float p0 = expf(sv[2 * i] - m_new), p1 = expf(sv[2 * i + 1] - m_new);
+      for (int i = 0; i < HC / 2; ++i) {
+        const float p0 = ex2(fmaf(sv[2 * i], LOG2E, -mb)), p1 = ex2(fmaf(sv[2 * i + 1], LOG2E, -mb));
         psum += p0 + p1;
         split3_pack(p0, p1, ph[i], pm[i], pl[i]);
       }
@@ -242,7 +252,7 @@ __global__ void __launch_bounds__(192, 1)
         if (__any_sync(0xffffffffu, grow)) {
           const float f = grow ? corr : 1.f;
 #pragma unroll 1
-          for (int c = 0; c < DKP / 32; ++c) {
+          for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
             uint32_t u[32];
             tmem_ld32(tmem + lb + C::T_O + c * 32, u);
             tmem_ld_wait();
@@ -254,9 +264,9 @@ __global__ void __launch_bounds__(192, 1)
       }
       l_run = l_run * (grow ? corr : 1.f) + psum;
       m_run = m_new;
-      tmem_st32(tmem + lb + C::T_P, ph);
-      tmem_st32(tmem + lb + C::T_P + C::KT / 2, pm);
-      tmem_st32(tmem + lb + C::T_P + C::KT, pl);
+      tmem_st16(tmem + lb + C::T_P + hc * (HC / 2), ph);
+      tmem_st16(tmem + lb + C::T_P + C::KT / 2 + hc * (HC / 2), pm);
+      tmem_st16(tmem + lb + C::T_P + C::KT + hc * (HC / 2), pl);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     const long base = ((long)split * a.Hkv + g) * a.R + row;
 #pragma unroll 1
-    for (int c = 0; c < DKP / 32; ++c) {
+    for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
       uint32_t u[32];
       tmem_ld32(tmem + lb + C::T_O + c * 32, u);
       tmem_ld_wait();
@@ -280,14 +290,18 @@ __global__ void __launch_bounds__(192, 1)
                                                            __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
       }
     }
-    if (valid) {
+    // row sum = both halves (all MMAs and TMA loads are done: reuse the K/V ring)
+    float* red = reinterpret_cast<float*>(sKV);
+    red[hc * 128 + r] = l_run;
+    named_bar_sync(1 + quarter, 64);
+    if (valid && hc == 0) {
       a.Mpart[base] = n_tiles > 0 ? m_run : -INFINITY;
-      a.Lpart[base] = l_run;
+      a.Lpart[base] = l_run + red[128 + r];
     }
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -307,13 +321,13 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<128>::SMEM);
     });
-    s1_attn_tc_kernel<128><<<grid, 192, S1TcCfg<128>::SMEM, st>>>(m1, m2, m3, mv, a);
+    s1_attn_tc_kernel<128><<<grid, 320, S1TcCfg<128>::SMEM, st>>>(m1, m2, m3, mv, a);
   } else if (dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<64>::SMEM);
     });
-    s1_attn_tc_kernel<64><<<grid, 192, S1TcCfg<64>::SMEM, st>>>(m1, m2, m3, mv, a);
+    s1_attn_tc_kernel<64><<<grid, 320, S1TcCfg<64>::SMEM, st>>>(m1, m2, m3, mv, a);
   } else {
     return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", dkp);
   }

@@ -1,0 +1,33 @@
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list per kernel."""
+import collections
+import csv
+import io
+import json
+import sys
+
+
+def shares(path):
+    txt = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(txt) if l.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(txt[start:]))))
+    agg = collections.defaultdict(lambda: [0.0, 0])
+    for r in rows:
+        name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r["Metric Unit"]
+        ms = v / 1e6 if unit in ("nsecond", "ns") else (v / 1e3 if unit in ("usecond", "us") else v)
+        agg[name][0] += ms
+        agg[name][1] += 1
+    tot = sum(a[0] for a in agg.values())
+    out = sorted(((k, round(v[0], 3), v[1], round(v[0] / tot, 4)) for k, v in agg.items()), key=lambda x: -x[1])
+    return tot, out
+
+
+if __name__ == "__main__":
+    tot, out = shares(sys.argv[1])
+    print(f"total ms {tot:.2f}")
+    for o in out:
+        print(f"  {o[0]:28s} {o[1]:9.3f} ms  {o[2]:5d} launches  {100 * o[3]:5.1f}%")
+    if len(sys.argv) > 2:
+        json.dump({"total_ms": tot, "kernels": [dict(name=a, ms=b, launches=c, share=d) for a, b, c, d in out]},
+                  open(sys.argv[2], "w"), indent=1)
