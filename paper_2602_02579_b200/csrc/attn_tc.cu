@@ -2,18 +2,22 @@
 // -> model.py:_attend 278-308 with pos_q = positions of the selected tokens and
 // pos_kv = 0..s-1 over the repaired cache).
 //
-// One CTA = one KV head g and a block of T = 128/G selected tokens; its 128 MMA rows
-// are the G query heads sharing g (GQA packing), row r = j*T + i (head g*G+j,
-// token b*T+i).  KV tiles are 128-token pages of the paged cache, TMA-loaded.
+// GQA packing: a 128-row Q tile = the G query heads sharing KV head g for a block of
+// T = 128/G selected tokens, row r = j*T + i (head g*G+j, token b*T+i).
+// One CTA = KV head g and TWO consecutive token blocks (tiles A, B): every 128-token
+// K/V page is TMA-loaded once and used by both tiles, which halves L2->SM traffic
+// per FLOP (the per-SM L2 read budget, not the tensor pipe, bounded the one-tile
+// design).
 //
-//   warps 0-7  softmax: warp w owns TMEM lane quarter w%4 (32 rows) and key
-//              columns [64*(w/4), +64) of each tile; both warps of a quarter read
-//              the full S row for the max (no exchange), then exponentiate their
-//              half in the log2 domain, P -> smem (bf16, SW128 K-major atom w/4),
-//              conditional O rescale in TMEM (only when the max grows by > 2^8)
+//   warps 0-3  softmax of tile A, warps 4-7 softmax of tile B: one row per thread;
+//              pass 1 reads the S row from TMEM for the max, pass 2 re-reads it,
+//              exponentiates in the log2 domain and writes P (bf16) back into the
+//              first 64 TMEM columns of its own S buffer (the A operand of the PV
+//              MMA); O is rescaled in TMEM only when the max grows by > 2^8
 //   warp 8     TMA producer: K and V pages, 2-stage ring
-//   warp 9     TMEM owner + MMA issuer: S = Q K^T (double-buffered in TMEM),
-//              O += P V (V as MN-major B operand)
+//   warp 9     TMEM owner + MMA issuer, pipe order per page j:
+//              PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+// TMEM: S_A [0,128) S_B [128,256) O_A [256,256+DKP) O_B [384,384+DKP).
 #include <mutex>
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
@@ -25,7 +29,7 @@ struct AttnArgs {
   __nv_bfloat16* out;        // [n_q][H][DKP]
   const int32_t* pos;        // [n_q] ascending
   const int32_t* page_table; // logical page -> physical page
-  int n_q, H, Hkv, G, T, n_tiles;
+  int n_q, H, Hkv, G, T, n_tiles, n_pairs;
   long kv_row0;              // first pool row of this layer: layer * Hkv * pool_tokens
   long pool_tokens;
   float scale_log2;          // log2(e) / sqrt(head_dim)
@@ -34,12 +38,10 @@ struct AttnArgs {
 template <int DKP>
 struct AttnCfg {
   static constexpr int ATOMS = DKP / 64;
-  static constexpr int Q_BYTES = 128 * DKP * 2;
+  static constexpr int Q_BYTES = 128 * DKP * 2;   // one Q tile
   static constexpr int KV_BYTES = 128 * DKP * 2;  // one K or V page
-  static constexpr int P_BYTES = 128 * 128 * 2;
   static constexpr int STAGES = 2;
-  static constexpr int SMEM = Q_BYTES + STAGES * 2 * KV_BYTES + P_BYTES + 1024 + 256;
-  static constexpr int SOFTMAX_WARPS = 8;
+  static constexpr int SMEM = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
 };
 
 template <int DKP>
@@ -48,27 +50,23 @@ __global__ void __launch_bounds__(320, 1)
   using Cfg = AttnCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = sQ + Cfg::Q_BYTES;  // stage s: K at sKV + s*2*KV_BYTES, V right after
-  uint8_t* sP = sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
-  uint64_t* kv_full = bars;                    // [STAGES]
-  uint64_t* kv_empty = bars + Cfg::STAGES;     // [STAGES]
-  uint64_t* s_full = bars + 2 * Cfg::STAGES;   // [2]
-  uint64_t* s_free = s_full + 2;               // [2]
-  uint64_t* p_full = s_free + 2;
-  uint64_t* pv_full = p_full + 1;
-  uint64_t* q_full = pv_full + 1;
+  uint8_t* sQ = smem;                      // tile A at +0, tile B at +Q_BYTES
+  uint8_t* sKV = sQ + 2 * Cfg::Q_BYTES;    // stage s: K at sKV + s*2*KV_BYTES, V right after
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES);
+  uint64_t* kv_full = bars;                 // [STAGES]
+  uint64_t* kv_empty = bars + Cfg::STAGES;  // [STAGES]
+  uint64_t* s_full = bars + 2 * Cfg::STAGES;  // [2] per tile
+  uint64_t* p_full = s_full + 2;              // [2]
+  uint64_t* pv_full = p_full + 2;             // [2]
+  uint64_t* q_full = pv_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x % a.Hkv;
-  const int b = a.n_tiles - 1 - blockIdx.x / a.Hkv;  // heaviest token blocks first (LPT)
-  const int tok0 = b * a.T;
-  const int last_tok = min(tok0 + a.T, a.n_q) - 1;
-  const int max_pos = a.pos[last_tok];
-  const int min_pos = a.pos[tok0];
-  const int n_kv_tiles = max_pos / 128 + 1;
+  const int pair = a.n_pairs - 1 - blockIdx.x / a.Hkv;  // heaviest pairs first (LPT)
+  // last valid token of the pair decides how many KV pages the CTA walks
+  const int last_tok = min((2 * pair + 2) * a.T, a.n_q) - 1;
+  const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -77,11 +75,10 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], Cfg::SOFTMAX_WARPS);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_full[i], 1);
     }
-    mbar_init(p_full, Cfg::SOFTMAX_WARPS);
-    mbar_init(pv_full, 1);
-    mbar_init(q_full, Cfg::SOFTMAX_WARPS);
+    mbar_init(q_full, 8);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -89,8 +86,6 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem;          // S buffers at cols 0 and 128
-  const uint32_t tO = tmem + 256;    // O accumulator
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
@@ -120,169 +115,158 @@ __global__ void __launch_bounds__(320, 1)
     mbar_wait(q_full, 0);
     tc_fence_after();
     const uint32_t q_addr = smem_u32(sQ);
-    const uint32_t p_addr = smem_u32(sP);
-    for (int j = 0; j <= n_kv_tiles; ++j) {
-      if (j < n_kv_tiles) {
-        const int st = j % Cfg::STAGES;
-        mbar_wait(&kv_full[st], (uint32_t)(j / Cfg::STAGES) & 1);
-        if (j >= 2) mbar_wait(&s_free[j & 1], (uint32_t)((j - 2) >> 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t k_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES);
+    auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+      const int st = j % Cfg::STAGES;
+      const uint32_t k_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES);
+      if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < DKP / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-            umma_bf16(tS + (j & 1) * 128, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
-                      idesc_s, kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[j & 1]);
+        for (int kk = 0; kk < DKP / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                    sdesc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
-        __syncwarp();
+        umma_commit(&s_full[t]);
       }
-      if (j >= 1) {
-        const int jp = j - 1;
-        const int st = jp % Cfg::STAGES;
-        mbar_wait(p_full, (uint32_t)jp & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t v_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P from TMEM
+      const int st = j % Cfg::STAGES;
+      const uint32_t v_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+      if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t a_off = (kk >> 2) * 16384 + (kk & 3) * 32;  // P: K-major, 64-col atoms
-            const uint32_t b_off = kk * 16 * 128;                       // V: 16 kv rows per step
-            umma_bf16(tO, sdesc_sw128(p_addr + a_off, 16, 1024), sdesc_sw128(v_addr + b_off, 16384, 1024), idesc_o,
-                      (jp > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(pv_full);
-          umma_commit(&kv_empty[st]);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < 8; ++kk)
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                       sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&pv_full[t]);
       }
+      __syncwarp();
+    };
+    mbar_wait(&kv_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int j = 0; j < n_kv_tiles; ++j) {
+      const bool more = j + 1 < n_kv_tiles;
+      mbar_wait(&p_full[0], (uint32_t)j & 1);
+      tc_fence_after();
+      issue_pv(0, j);
+      if (more) {
+        mbar_wait(&kv_full[(j + 1) % Cfg::STAGES], (uint32_t)((j + 1) / Cfg::STAGES) & 1);
+        tc_fence_after();
+        issue_s(0, j + 1);  // in-order after PV_A(j): P_A's TMEM columns are free again
+      }
+      mbar_wait(&p_full[1], (uint32_t)j & 1);
+      tc_fence_after();
+      issue_pv(1, j);
+      if (elect_one()) umma_commit(&kv_empty[j % Cfg::STAGES]);
+      __syncwarp();
+      if (more) issue_s(1, j + 1);
     }
   } else {
     // ---------------------------------------------------------------- softmax
-    const int quarter = warp & 3, hc = warp >> 2;
+    const int t = warp >> 2;           // Q tile A (0) or B (1)
+    const int quarter = warp & 3;
     const int r = quarter * 32 + lane;  // 0..127 == TMEM lane
+    const int b = 2 * pair + t;
     const int hj = r / a.T;
     const int ti = r - hj * a.T;
-    const int tok = tok0 + ti;
-    const bool valid = hj < a.G && tok < a.n_q;
+    const int tok = b * a.T + ti;
+    const bool valid = hj < a.G && tok < a.n_q && b < a.n_tiles;
     const int head = g * a.G + hj;
-    const int my_pos = valid ? a.pos[tok] : max_pos;
-    const uint32_t lane_base = (uint32_t)((quarter * 32) << 16);
+    const int tile_last = min((b + 1) * a.T, a.n_q) - 1;
+    const int min_pos = b < a.n_tiles ? a.pos[b * a.T] : 0x7fffffff;
+    const int my_pos = valid ? a.pos[tok] : (b < a.n_tiles ? a.pos[tile_last] : 0x7fffffff);
+    const uint32_t lb = (uint32_t)((quarter * 32) << 16);
+    const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
     const float sl2 = a.scale_log2;
 
-    // Q row -> smem (this warp: 64-column atom hc), 128B-swizzled K-major
-    if (hc < Cfg::ATOMS) {
-      const uint4* src = valid ? reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) : nullptr;
+    {  // Q row -> smem, 128B-swizzled K-major atoms (all loads first, then stores)
+      uint4 v[DKP / 8];
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP);
 #pragma unroll
-      for (int c = hc * 8; c < hc * 8 + 8; ++c) {
-        uint4 v = valid ? src[c] : make_uint4(0, 0, 0, 0);
-        const int ch = (c & 7) ^ (r & 7);
-        *reinterpret_cast<uint4*>(sQ + hc * 16384 + r * 128 + ch * 16) = v;
+      for (int c = 0; c < DKP / 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < DKP / 8; ++c) {
+        const int at = c >> 3, ch = (c & 7) ^ (r & 7);
+        *reinterpret_cast<uint4*>(sQ + t * Cfg::Q_BYTES + at * 16384 + r * 128 + ch * 16) = v[c];
       }
       fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(q_full);
 
-    float m_run = -INFINITY, l_run = 0.f;  // m in log2 units; l: this warp's half of the row sum
+    float m_run = -INFINITY, l_run = 0.f;  // m in log2 units
     for (int j = 0; j < n_kv_tiles; ++j) {
-      mbar_wait(&s_full[j & 1], (uint32_t)(j >> 1) & 1);
+      mbar_wait(&s_full[t], (uint32_t)j & 1);  // also implies PV_t(j-1) is complete
       tc_fence_after();
       const int key0 = j * 128;
       const bool unmasked = key0 + 127 <= min_pos;
-      // the partner half only contributes to the max
-      float omax = -INFINITY;
+      // pass 1: row max
+      float tmax = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t u[32];
-        const int col = (hc ^ 1) * 64 + c * 32;
-        tmem_ld32(tS + lane_base + (j & 1) * 128 + col, u);
+        tmem_ld32(tS + lb + c * 32, u);
         tmem_ld_wait();
         if (unmasked) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) omax = fmaxf(omax, __uint_as_float(u[i]));
+          for (int i = 0; i < 32; ++i) tmax = fmaxf(tmax, __uint_as_float(u[i]));
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i)
-            if (key0 + col + i <= my_pos) omax = fmaxf(omax, __uint_as_float(u[i]));
+            if (key0 + c * 32 + i <= my_pos) tmax = fmaxf(tmax, __uint_as_float(u[i]));
         }
       }
-      float s[64];
-      float lmax = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t u[32];
-        const int col = hc * 64 + c * 32;
-        tmem_ld32(tS + lane_base + (j & 1) * 128 + col, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float x = (unmasked || key0 + col + i <= my_pos) ? __uint_as_float(u[i]) : -INFINITY;
-          s[c * 32 + i] = x;
-          lmax = fmaxf(lmax, x);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[j & 1]);
-
-      const float m_new = fmaxf(m_run, fmaxf(lmax, omax) * sl2);
+      const float m_new = fmaxf(m_run, tmax * sl2);
       const bool grow = (m_new - m_run) > 8.0f;  // also true on the first tile (m_run = -inf)
       const float m_use = grow ? m_new : m_run;
+      // pass 2: P = 2^(s*sl2 - m) -> bf16 into TMEM columns [0,64) of this S buffer
+      // (chunk c writes columns 16c..16c+15, all below the S columns it reads)
       float rsum = 0.f;
-      uint32_t pk[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float p0 = ex2(fmaf(s[2 * i], sl2, -m_use)), p1 = ex2(fmaf(s[2 * i + 1], sl2, -m_use));
-        rsum += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tS + lb + c * 32, u);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const bool v0 = unmasked || key0 + c * 32 + 2 * i <= my_pos;
+          const bool v1 = unmasked || key0 + c * 32 + 2 * i + 1 <= my_pos;
+          const float p0 = v0 ? ex2(fmaf(__uint_as_float(u[2 * i]), sl2, -m_use)) : 0.f;
+          const float p1 = v1 ? ex2(fmaf(__uint_as_float(u[2 * i + 1]), sl2, -m_use)) : 0.f;
+          rsum += p0 + p1;
+          pk[i] = pack_bf16(p0, p1);
+        }
+        tmem_st16(tS + lb + c * 16, pk);
       }
-      // previous PV must be done before P is overwritten and before O is rescaled
-      if (j >= 1) {
-        mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
-        tc_fence_after();
-      }
-      const bool any_grow = __any_sync(0xffffffffu, grow && j > 0) != 0;
-      if (any_grow) {
+      if (__any_sync(0xffffffffu, grow && j > 0)) {
         const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
 #pragma unroll 1
-        for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
+        for (int c = 0; c < DKP / 32; ++c) {
           uint32_t u[32];
-          tmem_ld32(tO + lane_base + c * 32, u);
+          tmem_ld32(tO + lb + c * 32, u);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-          tmem_st32(tO + lane_base + c * 32, u);
+          tmem_st32(tO + lb + c * 32, u);
         }
-        tmem_st_wait();
       }
       if (grow && j > 0) l_run *= ex2(m_run - m_use);
       if (grow) m_run = m_use;
       l_run += rsum;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int ch = c ^ (r & 7);
-        *reinterpret_cast<uint4*>(sP + hc * 16384 + r * 128 + ch * 16) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
-      fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
-    mbar_wait(pv_full, (uint32_t)(n_kv_tiles - 1) & 1);
+    mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
     tc_fence_after();
-    // row sum = both halves; all MMAs are done, so the P buffer is free for the exchange
-    float* red = reinterpret_cast<float*>(sP);
-    red[hc * 128 + r] = l_run;
-    named_bar_sync(1 + quarter, 64);
-    const float inv_l = 1.f / (red[r] + red[128 + r]);
+    const float inv_l = 1.f / l_run;
 #pragma unroll 1
-    for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
+    for (int c = 0; c < DKP / 32; ++c) {
       uint32_t u[32];
-      tmem_ld32(tO + lane_base + c * 32, u);
+      tmem_ld32(tO + lb + c * 32, u);
       tmem_ld_wait();
       if (valid) {
         uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + c * 32);
@@ -313,7 +297,7 @@ static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnA
     err = cudaFuncSetAttribute(attn_tc_kernel<DKP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn smem attr: %s", cudaGetErrorString(err));
-  attn_tc_kernel<DKP><<<a.n_tiles * a.Hkv, 320, Cfg::SMEM, stream>>>(tk, tv, a);
+  attn_tc_kernel<DKP><<<a.n_pairs * a.Hkv, 320, Cfg::SMEM, stream>>>(tk, tv, a);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_tc_kernel");
   return PKV_OK;
@@ -337,6 +321,7 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   a.G = G;
   a.T = 128 / G;
   a.n_tiles = ceil_div(n_q, a.T);
+  a.n_pairs = ceil_div(a.n_tiles, 2);
   a.kv_row0 = (long)layer * Hkv * pool_tokens;
   a.pool_tokens = pool_tokens;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));

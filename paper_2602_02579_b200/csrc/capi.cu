@@ -299,6 +299,7 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer
 struct QpWs {
   float *h, *x, *qkv, *q, *k, *v, *attn, *gu, *act, *S, *Opart, *Mpart, *Lpart, *Mfin, *Lfin, *rows, *xl;
   double* denom;
+  __nv_bfloat16* q3;
   ProjWs proj;
   int n_splits, keys_per_split, tc_splits, tc_keys_per_split;
 };
@@ -349,6 +350,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.Mfin = cv.take<float>((size_t)Hkv * R);
   w.Lfin = cv.take<float>((size_t)Hkv * R);
   w.xl = cv.take<float>((size_t)md->Dp);
+  w.q3 = cv.take<__nv_bfloat16>((size_t)Hkv * ceil_div(R, 128) * 3 * 128 * dkp);
   *total = cv.off + 256;
   return w;
 }
@@ -415,6 +417,7 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.split_base = 0;
     a.tc_splits = tc_splits;
     a.tc_keys_per_split = w.tc_keys_per_split;
+    a.q3 = w.q3;
     a.k1_all = c->k_pool;
     a.k2_all = c->k2_pool;
     a.k3_all = c->k3_pool;

@@ -59,7 +59,8 @@ struct S1Attn {
   float* Opart;
   float* Mpart;
   float* Lpart;
-  // whole-pool bases for the tensor-core path (TMA)
+  // whole-pool bases for the tensor-core path (TMA) and its Q-plane workspace
+  void* q3;
   const void* k1_all;
   const void* k2_all;
   const void* k3_all;
@@ -70,6 +71,7 @@ struct S1Attn {
 // tensor-core narrow-pass attention over the context keys [0, s)
 struct S1TcArgs {
   const float* q;  // [m][H][DKP] rotated fp32
+  void* q3;        // workspace: bf16 Q planes [Hkv][RB][3][128][DKP]
   int m, H, Hkv, G, dk, R, s, s_tot, keys_per_split, n_splits;
   float scale;
   long kv_row0;  // first pool row of this layer: layer * Hkv * pool_tokens

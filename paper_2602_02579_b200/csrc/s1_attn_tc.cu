@@ -44,10 +44,30 @@ struct S1TcCfg {
   static constexpr int SOFTMAX_WARPS = 8;
 };
 
+// Q planes for the TMA: q3[((g*RB + rb)*3 + plane)*128 + r][DKP] bf16, row r of row
+// block rb = query head g*G + j, query i with rb*128 + r = j*m + i (zero padded)
+__global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int RB, int dkp, __nv_bfloat16* q3) {
+  const int g = blockIdx.y, rr = blockIdx.x;  // rr = rb*128 + r
+  const int rb = rr >> 7, r = rr & 127;
+  const bool valid = rr < R;
+  const int jh = valid ? rr / m : 0, qi = valid ? rr - jh * m : 0;
+  const float* src = q + ((long)qi * H + g * G + jh) * dkp;
+  for (int d2 = threadIdx.x; d2 < dkp / 2; d2 += blockDim.x) {
+    float x0 = valid ? src[2 * d2] : 0.f, x1 = valid ? src[2 * d2 + 1] : 0.f;
+    uint32_t h, mi, l;
+    split3_pack(x0, x1, h, mi, l);
+    const long base = (((long)g * RB + rb) * 3) * 128 + r;
+    reinterpret_cast<uint32_t*>(q3 + base * dkp)[d2] = h;
+    reinterpret_cast<uint32_t*>(q3 + (base + 128) * dkp)[d2] = mi;
+    reinterpret_cast<uint32_t*>(q3 + (base + 256) * dkp)[d2] = l;
+  }
+}
+
 template <int DKP>
 __global__ void __launch_bounds__(320, 1)
     s1_attn_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
-                      const __grid_constant__ CUtensorMap tK3, const __grid_constant__ CUtensorMap tV, S1TcArgs a) {
+                      const __grid_constant__ CUtensorMap tK3, const __grid_constant__ CUtensorMap tV,
+                      const __grid_constant__ CUtensorMap tQ, S1TcArgs a) {
   using C = S1TcCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -82,7 +102,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_init(p_full, C::SOFTMAX_WARPS);
     mbar_init(pv_full, 1);
-    mbar_init(q_full, C::SOFTMAX_WARPS);
+    mbar_init(q_full, 1);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -98,6 +118,15 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch(&tK2);
       tma_prefetch(&tK3);
       tma_prefetch(&tV);
+      {  // the three Q planes of this (head, row block)
+        const int qrow = ((g * (int)gridDim.z + blockIdx.z) * 3) * 128;
+        mbar_expect_tx(q_full, 3 * C::QSPLIT);
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+#pragma unroll
+          for (int at = 0; at < C::ATOMS; ++at)
+            tma_load_2d(sQ + x * C::QSPLIT + at * C::ATOM_Q, &tQ, q_full, at * 64, qrow + x * 128);
+      }
       const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % C::STAGES;
@@ -174,28 +203,7 @@ __global__ void __launch_bounds__(320, 1)
     const int r = quarter * 32 + lane;  // TMEM lane == tile row
     const int row = r0 + r;
     const bool valid = row < a.R;
-    const int jh = valid ? row / a.m : 0, qi = valid ? row - jh * a.m : 0;
     const uint32_t lb = (uint32_t)(quarter * 32) << 16;
-    {  // Q planes: this warp fills dims [hc*DKP/2, (hc+1)*DKP/2) of its rows
-      const float4* src = reinterpret_cast<const float4*>(a.q + ((long)qi * a.H + g * a.G + jh) * DKP);
-#pragma unroll 1
-      for (int c8 = hc * DKP / 16; c8 < (hc + 1) * DKP / 16; ++c8) {
-        float4 x0 = valid ? src[2 * c8] : make_float4(0.f, 0.f, 0.f, 0.f);
-        float4 x1 = valid ? src[2 * c8 + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-        uint32_t h[4], m[4], l[4];
-        split3_pack(x0.x, x0.y, h[0], m[0], l[0]);
-        split3_pack(x0.z, x0.w, h[1], m[1], l[1]);
-        split3_pack(x1.x, x1.y, h[2], m[2], l[2]);
-        split3_pack(x1.z, x1.w, h[3], m[3], l[3]);
-        const uint32_t off = (c8 >> 3) * C::ATOM_Q + sw128_offset(r, (c8 & 7) * 8);
-        *reinterpret_cast<uint4*>(sQ + off) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4*>(sQ + C::QSPLIT + off) = make_uint4(m[0], m[1], m[2], m[3]);
-        *reinterpret_cast<uint4*>(sQ + 2 * C::QSPLIT + off) = make_uint4(l[0], l[1], l[2], l[3]);
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
-    }
     constexpr int HC = C::KT / 2;  // columns per warp
     float m_run = -INFINITY, l_run = 0.f;  // l_run: this warp's half of the row sum
     float* srow = (a.S != nullptr && valid) ? a.S + ((long)g * a.R + row) * a.s_tot : nullptr;
@@ -311,23 +319,29 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
                       long pool_rows_total, int dkp, cudaStream_t st) {
   if (a.n_splits <= 0) return PKV_OK;
   if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
-  dim3 grid(a.n_splits, a.Hkv, ceil_div(a.R, 128));
-  CUtensorMap m1, m2, m3, mv;
+  const int RB = ceil_div(a.R, 128);
+  dim3 grid(a.n_splits, a.Hkv, RB);
+  s1_qprep_kernel<<<dim3(RB * 128, a.Hkv), 64, 0, st>>>(a.q, a.m, a.H, a.G, a.R, RB, dkp,
+                                                       reinterpret_cast<__nv_bfloat16*>(a.q3));
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("s1_qprep_kernel");
+  CUtensorMap m1, m2, m3, mv, mq;
   if (!cached_tmap(&m1, k1, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&m2, k2, pool_rows_total, dkp, dkp, 64) ||
-      !cached_tmap(&m3, k3, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&mv, v, pool_rows_total, dkp, dkp, 64))
+      !cached_tmap(&m3, k3, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&mv, v, pool_rows_total, dkp, dkp, 64) ||
+      !cached_tmap(&mq, a.q3, (long)a.Hkv * RB * 3 * 128, dkp, dkp, 128))
     return set_error(PKV_ERR_CUDA, "narrow pass: TMA encode failed");
   if (dkp == 128) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<128>::SMEM);
     });
-    s1_attn_tc_kernel<128><<<grid, 320, S1TcCfg<128>::SMEM, st>>>(m1, m2, m3, mv, a);
+    s1_attn_tc_kernel<128><<<grid, 320, S1TcCfg<128>::SMEM, st>>>(m1, m2, m3, mv, mq, a);
   } else if (dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<64>::SMEM);
     });
-    s1_attn_tc_kernel<64><<<grid, 320, S1TcCfg<64>::SMEM, st>>>(m1, m2, m3, mv, a);
+    s1_attn_tc_kernel<64><<<grid, 320, S1TcCfg<64>::SMEM, st>>>(m1, m2, m3, mv, mq, a);
   } else {
     return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", dkp);
   }

@@ -532,6 +532,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.keys_per_split = a.tc_keys_per_split;
     t.n_splits = a.tc_splits;
     t.scale = a.scale;
+    t.q3 = a.q3;
     t.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
     t.pool_tokens = a.pool_tokens;
     t.page_table = a.page_table;
