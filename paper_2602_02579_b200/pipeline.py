@@ -51,6 +51,23 @@ class PrefillPipeline:
         torch = _lib.require_cuda()
         self.query.copy_(torch.as_tensor(np.asarray(ids, dtype=np.int32)), non_blocking=True)
 
+    def capture(self):
+        """Record one step into a CUDA graph (call after a warm-up step so every
+        kernel attribute is set); replay() then launches the ~1.5k kernels of a
+        prefill with one host call."""
+        torch = _lib.require_cuda()
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(self.graph, stream=side):
+                self.step()
+        torch.cuda.current_stream().wait_stream(side)
+        return self.graph
+
+    def replay(self) -> None:
+        self.graph.replay()
+
     def step(self, stream=None) -> None:
         """One full prefill; results stay on the device (idx, logits, per_layer)."""
         torch = _lib.require_cuda()
