@@ -9,13 +9,15 @@
 // per FLOP (the per-SM L2 read budget, not the tensor pipe, bounded the one-tile
 // design).
 //
-//   warps 0-3  softmax of tile A, warps 4-7 softmax of tile B: one row per thread;
-//              pass 1 reads the S row from TMEM for the max, pass 2 re-reads it,
-//              exponentiates in the log2 domain and writes P (bf16) back into the
-//              first 64 TMEM columns of its own S buffer (the A operand of the PV
-//              MMA); O is rescaled in TMEM only when the max grows by > 2^8
-//   warp 8     TMA producer: K and V pages, 2-stage ring
-//   warp 9     TMEM owner + MMA issuer, pipe order per page j:
+//   warps 0-7  softmax of tile A, warps 8-15 softmax of tile B; per tile, the two
+//              warps on a TMEM lane quarter split the 128 key columns: pass 1
+//              reads the whole S row for the max, pass 2 exponentiates the warp's
+//              64 keys in the log2 domain (1/4 of them with a degree-3 polynomial
+//              on the FMA pipe to offload MUFU) and writes P (bf16) back into the
+//              first 64 TMEM columns of its S buffer (A operand of the PV MMA);
+//              O is rescaled in TMEM only when the max grows by > 2^8
+//   warp 16    TMA producer: K and V pages, 2-stage ring
+//   warp 17    TMEM owner + MMA issuer, pipe order per page j:
 //              PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
 // TMEM: S_A [0,128) S_B [128,256) O_A [256,256+DKP) O_B [384,384+DKP).
 #include <mutex>
@@ -44,8 +46,18 @@ struct AttnCfg {
   static constexpr int SMEM = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
 };
 
+// 2^x on the FMA pipe: floor/fraction split, degree-3 polynomial for 2^f on [0,1)
+// (max relative error 8.6e-5; P is rounded to bf16 afterwards), exponent by integer add
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float xi = floorf(x);
+  const float f = x - xi;
+  const float p = fmaf(fmaf(fmaf(0.07706641f, f, 0.22764443f), f, 0.69511737f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((int)xi << 23));
+}
+
 template <int DKP>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(576, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
   using Cfg = AttnCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
@@ -75,19 +87,19 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 8);
       mbar_init(&pv_full[i], 1);
     }
-    mbar_init(q_full, 8);
+    mbar_init(q_full, 16);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == 17) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 16) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
       tma_prefetch(&tmK);
@@ -108,7 +120,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     // ------------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc_s = make_idesc_bf16(128, 128);
     constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
@@ -164,9 +176,12 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else {
     // ---------------------------------------------------------------- softmax
-    const int t = warp >> 2;           // Q tile A (0) or B (1)
+    // warp w: tile t = w/8, TMEM lane quarter w%4, key-column half h = (w/4)%2
+    const int t = warp >> 3;
     const int quarter = warp & 3;
+    const int h = (warp >> 2) & 1;
     const int r = quarter * 32 + lane;  // 0..127 == TMEM lane
+    const int bar_id = 1 + t * 4 + quarter;  // the two column halves of these 32 rows
     const int b = 2 * pair + t;
     const int hj = r / a.T;
     const int ti = r - hj * a.T;
@@ -180,28 +195,28 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
     const float sl2 = a.scale_log2;
 
-    {  // Q row -> smem, 128B-swizzled K-major atoms (all loads first, then stores)
-      uint4 v[DKP / 8];
-      const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP);
+    if (h < Cfg::ATOMS) {  // Q row, this warp's 64-column atom -> smem (128B-swizzled K-major)
+      uint4 v[8];
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) + h * 8;
 #pragma unroll
-      for (int c = 0; c < DKP / 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int c = 0; c < DKP / 8; ++c) {
-        const int at = c >> 3, ch = (c & 7) ^ (r & 7);
-        *reinterpret_cast<uint4*>(sQ + t * Cfg::Q_BYTES + at * 16384 + r * 128 + ch * 16) = v[c];
+      for (int c = 0; c < 8; ++c) {
+        const int ch = c ^ (r & 7);
+        *reinterpret_cast<uint4*>(sQ + t * Cfg::Q_BYTES + h * 16384 + r * 128 + ch * 16) = v[c];
       }
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_full);
 
-    float m_run = -INFINITY, l_run = 0.f;  // m in log2 units
+    float m_run = -INFINITY, l_run = 0.f;  // m in log2 units; l: this half's row sum
     for (int j = 0; j < n_kv_tiles; ++j) {
       mbar_wait(&s_full[t], (uint32_t)j & 1);  // also implies PV_t(j-1) is complete
       tc_fence_after();
       const int key0 = j * 128;
       const bool unmasked = key0 + 127 <= min_pos;
-      // pass 1: row max
+      // pass 1: max over the whole row (both halves read it; no exchange needed)
       float tmax = -INFINITY;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -220,30 +235,44 @@ __global__ void __launch_bounds__(320, 1)
       const float m_new = fmaxf(m_run, tmax * sl2);
       const bool grow = (m_new - m_run) > 8.0f;  // also true on the first tile (m_run = -inf)
       const float m_use = grow ? m_new : m_run;
-      // pass 2: P = 2^(s*sl2 - m) -> bf16 into TMEM columns [0,64) of this S buffer
-      // (chunk c writes columns 16c..16c+15, all below the S columns it reads)
+      // pass 2: this half's 64 keys -> P (bf16 pairs), a quarter of them on the FMA pipe
       float rsum = 0.f;
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t u[32];
-        tmem_ld32(tS + lb + c * 32, u);
+        const int col = h * 64 + c * 32;
+        tmem_ld32(tS + lb + col, u);
         tmem_ld_wait();
-        uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const bool v0 = unmasked || key0 + c * 32 + 2 * i <= my_pos;
-          const bool v1 = unmasked || key0 + c * 32 + 2 * i + 1 <= my_pos;
-          const float p0 = v0 ? ex2(fmaf(__uint_as_float(u[2 * i]), sl2, -m_use)) : 0.f;
-          const float p1 = v1 ? ex2(fmaf(__uint_as_float(u[2 * i + 1]), sl2, -m_use)) : 0.f;
+          const bool v0 = unmasked || key0 + col + 2 * i <= my_pos;
+          const bool v1 = unmasked || key0 + col + 2 * i + 1 <= my_pos;
+          const float x0 = fmaf(__uint_as_float(u[2 * i]), sl2, -m_use);
+          const float x1 = fmaf(__uint_as_float(u[2 * i + 1]), sl2, -m_use);
+          float p0, p1;
+          if ((i & 3) == 3) {
+            p0 = exp2_poly(x0);
+            p1 = exp2_poly(x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          p0 = v0 ? p0 : 0.f;
+          p1 = v1 ? p1 : 0.f;
           rsum += p0 + p1;
-          pk[i] = pack_bf16(p0, p1);
+          pk[c * 16 + i] = pack_bf16(p0, p1);
         }
-        tmem_st16(tS + lb + c * 16, pk);
       }
+      // P of keys [64h, 64h+64) goes to TMEM columns [32h, 32h+32) of this S buffer,
+      // which the other half may still be reading: wait for both halves first
+      named_bar_sync(bar_id, 64);
+      tmem_st16(tS + lb + h * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
+      tmem_st16(tS + lb + h * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
       if (__any_sync(0xffffffffu, grow && j > 0)) {
         const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
 #pragma unroll 1
-        for (int c = 0; c < DKP / 32; ++c) {
+        for (int c = h * DKP / 64; c < (h + 1) * DKP / 64; ++c) {
           uint32_t u[32];
           tmem_ld32(tO + lb + c * 32, u);
           tmem_ld_wait();
@@ -262,9 +291,13 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
     tc_fence_after();
-    const float inv_l = 1.f / l_run;
+    // row sum = both halves; every MMA has completed, so the Q tile is free scratch
+    float* red = reinterpret_cast<float*>(sQ + t * Cfg::Q_BYTES);
+    red[h * 128 + r] = l_run;
+    named_bar_sync(bar_id, 64);
+    const float inv_l = 1.f / (red[r] + red[128 + r]);
 #pragma unroll 1
-    for (int c = 0; c < DKP / 32; ++c) {
+    for (int c = h * DKP / 64; c < (h + 1) * DKP / 64; ++c) {
       uint32_t u[32];
       tmem_ld32(tO + lb + c * 32, u);
       tmem_ld_wait();
@@ -281,7 +314,7 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 17) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -297,7 +330,7 @@ static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnA
     err = cudaFuncSetAttribute(attn_tc_kernel<DKP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn smem attr: %s", cudaGetErrorString(err));
-  attn_tc_kernel<DKP><<<a.n_pairs * a.Hkv, 320, Cfg::SMEM, stream>>>(tk, tv, a);
+  attn_tc_kernel<DKP><<<a.n_pairs * a.Hkv, 576, Cfg::SMEM, stream>>>(tk, tv, a);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_tc_kernel");
   return PKV_OK;
