@@ -229,20 +229,19 @@ def main():
     for _ in range(args.warmup):
         pipe.step()
     torch.cuda.synchronize()
-    # eager step with the native timers: fills the event pool and counts our launches
+    # eager steps with the native timers (CUDA events on the launching stream around each
+    # kernel group): per-kernel device times for the roofline; counts our launches
     _lib.timing(True)
     n0 = _lib.launch_count()
-    pipe.step()
+    for _ in range(args.steps):
+        pipe.step()
     torch.cuda.synchronize()
-    launches_per_step = _lib.launch_count() - n0
-    eager_phases = _lib.timing_collect()
-    # graph with timer event nodes (one replay -> per-phase device times, no CPU gaps)
-    timed_graph = pipe.capture()
-    _lib.timing(False)
-    timed_graph.replay()
-    torch.cuda.synchronize()
+    launches_per_step = (_lib.launch_count() - n0) // args.steps
     phases = _lib.timing_collect()
-    # plain graph for the timed region
+    _lib.timing(False)
+    eager_phases = {n: (v[0] / args.steps, v[1]) for n, v in phases.items()}
+    phases = {n: (v[0] / args.steps, v[1] / args.steps) for n, v in phases.items()}
+    # CUDA graph of one step for the timed region
     pipe.capture()
     for _ in range(max(1, args.warmup)):
         pipe.replay()
