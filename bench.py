@@ -262,11 +262,12 @@ def main():
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     phases = {n: (v[0] * args.steps, v[1] * args.steps) for n, v in phases.items()}
+    # weak scaling: each rank serves its own request (paper_2602_02579_b200.dist), the
+    # job is as slow as its slowest rank
+    from paper_2602_02579_b200 import dist as pdist
+    ms = pdist.max_over_ranks(ms, device="cuda")
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
-        ms = float(t.item())
     value = world * s / (ms / 1e3)
 
     # ---- roofline of every kernel group; the dominant one is reported
