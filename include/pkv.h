@@ -101,6 +101,9 @@ typedef struct pkv_cache {
                                 even when a query pass reads the others from the chunk store) */
   void* k2_pool;             /* residual key planes, same layout as k_pool: the f32 key is exactly */
   void* k3_pool;             /* k_pool + k2_pool + k3_pool (bf16 each); used by the narrow passes  */
+  void* const* layer_ready;  /* nullable host array [n_layers] of cudaEvent_t: a query pass makes its
+                                stream wait on layer_ready[l] before reading layer l (pipelined
+                                host->device chunk transfer + per-layer assembly) */
 } pkv_cache;
 
 /* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */
@@ -126,6 +129,9 @@ void pkv_model_destroy(pkv_model* m);
  * concatenates the chunk K/V into the paged cache, rotating keys at global
  * positions 0..s-1 with the float64 tables. */
 int pkv_assemble(const pkv_config* cfg, const pkv_chunks* chunks, const pkv_cache* cache, void* stream);
+/* same for layers [layer_begin, layer_end) only (layer-pipelined assembly) */
+int pkv_assemble_layers(const pkv_config* cfg, const pkv_chunks* chunks, const pkv_cache* cache, int32_t layer_begin,
+                        int32_t layer_end, void* stream);
 
 /* query_pass -- model.py:370-402; with PKV_QP_SCORES it is score_prophet
  * (selection.py:64-86, per_layer [L][s] f32); with PKV_QP_LOGITS|PKV_QP_APPEND_KV

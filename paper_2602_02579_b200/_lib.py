@@ -45,7 +45,7 @@ class Weights(ctypes.Structure):
 class Cache(ctypes.Structure):
     _fields_ = [("k_pool", c_vp), ("v_pool", c_vp), ("pool_tokens", c_i64), ("page_table", c_vp), ("s", c_i32),
                 ("token_ids", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("rope_len", c_i32), ("recomputed", c_vp),
-                ("k2_pool", c_vp), ("k3_pool", c_vp)]
+                ("k2_pool", c_vp), ("k3_pool", c_vp), ("layer_ready", ctypes.POINTER(c_vp))]
 
 
 class Chunks(ctypes.Structure):
@@ -58,6 +58,8 @@ _SIGS = {
     "pkv_model_create": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Weights), ctypes.POINTER(c_vp)]),
     "pkv_model_destroy": (None, [c_vp]),
     "pkv_assemble": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Chunks), ctypes.POINTER(Cache), c_vp]),
+    "pkv_assemble_layers": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Chunks), ctypes.POINTER(Cache), c_i32,
+                                    c_i32, c_vp]),
     "pkv_query_pass_workspace": (c_sz, [c_vp, c_i32, c_i32, c_i32]),
     "pkv_query_pass": (c_i32, [c_vp, ctypes.POINTER(Cache), ctypes.POINTER(Chunks), c_vp, c_i32, c_i32, c_vp, c_vp,
                                c_vp, c_vp, c_vp, c_sz, c_vp]),

@@ -70,8 +70,20 @@ class ChunkKV:
         a = t.float().cpu().numpy()
         return [np.ascontiguousarray(a[l, :, :, :dk]) for l in range(a.shape[0])]
 
+    @property
+    def pending_h2d(self) -> bool:
+        """True while the device copy of a pinned-host chunk has not been scheduled."""
+        return getattr(self, "_pinned", None) is not None
+
     def device_buffers(self, config: ModelConfig):
-        """(K, V) bf16 device tensors [L][t][Hkv][dkp]; uploaded once from the host form."""
+        """(K, V) bf16 device tensors [L][t][Hkv][dkp]; uploaded once from the host form.
+        For pinned-host chunks the buffers are allocated here and filled layer by layer
+        by assemble() (pipelined with the first query pass)."""
+        if self._k_dev is None and self.pending_h2d:
+            torch = _lib.require_cuda()
+            kp, vp = self._pinned
+            self._k_dev = torch.empty(kp.shape, dtype=kp.dtype, device="cuda")
+            self._v_dev = torch.empty(vp.shape, dtype=vp.dtype, device="cuda")
         if self._k_dev is None:
             torch = _lib.require_cuda()
             lay = Layout.of(config)
@@ -96,6 +108,15 @@ class ChunkKV:
     @classmethod
     def from_device(cls, chunk_id, fingerprint, token_ids, k_dev, v_dev, head_dim):
         c = cls(chunk_id, fingerprint, token_ids, device_k=k_dev, device_v=v_dev)
+        c._dk = head_dim
+        return c
+
+    @classmethod
+    def from_pinned(cls, chunk_id, fingerprint, token_ids, k_host, v_host, head_dim):
+        """Chunk whose bf16 K/V ([L][t][Hkv][dkp]) live in pinned host memory (a host-tier
+        chunk store); assemble() streams them to HBM layer by layer."""
+        c = cls(chunk_id, fingerprint, token_ids)
+        c._pinned = (k_host, v_host)
         c._dk = head_dim
         return c
 
@@ -183,12 +204,19 @@ class AssembledCache:
         self.pool_tokens = -(-(s + QUERY_RESERVE) // PAGE) * PAGE
         n_pages = self.pool_tokens // PAGE
         self._d_pages = torch.arange(n_pages, dtype=torch.int32, device=dev)
-        self.k_pool = torch.zeros((L, Hkv, self.pool_tokens, dkp), dtype=torch.bfloat16, device=dev)
-        self.v_pool = torch.zeros_like(self.k_pool)
+        shape = (L, Hkv, self.pool_tokens, dkp)
+        self.k_pool = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+        self.v_pool = torch.empty_like(self.k_pool)
         # residual planes of every f32 key (k_pool + k2 + k3 == f32 key exactly), read by
         # the fp32-faithful narrow passes on the tensor cores
-        self.k2_pool = torch.zeros_like(self.k_pool)
-        self.k3_pool = torch.zeros_like(self.k_pool)
+        self.k2_pool = torch.empty_like(self.k_pool)
+        self.k3_pool = torch.empty_like(self.k_pool)
+        # slots [s, pool) are read by full-page tiles (masked, but P*V must stay finite):
+        # assembly writes [0, s), so only the tail needs zeros
+        for pool in (self.k_pool, self.v_pool, self.k2_pool, self.k3_pool):
+            pool[:, :, s:].zero_()
+        self.layer_events = None  # per-layer readiness when the chunk transfer is pipelined
+        self._copy_stream = None
         self.rope_len, self._rcos, self._rsin = rope_device_tables(config.rope_theta, config.head_dim,
                                                                    self.pool_tokens)
         if fp32_taps == "auto":
@@ -237,6 +265,7 @@ class AssembledCache:
 
     def _layer_f32(self, layer: int, is_key: bool) -> np.ndarray:
         torch = _lib.require_cuda()
+        self.wait_ready()
         s, Hkv, dk = self.context_length, self.config.n_kv_heads, self.config.head_dim
         out = torch.empty((s, Hkv, dk), dtype=torch.float32, device=self.device)
         # never-recomputed entries: exact f32 from the chunk store; others: the cache
@@ -259,6 +288,7 @@ class AssembledCache:
         if need <= self.pool_tokens:
             return
         torch = _lib.require_cuda()
+        self.wait_ready()
         new_tokens = -(-need // PAGE) * PAGE
         L, Hkv, dkp = self.k_pool.shape[0], self.k_pool.shape[1], self.k_pool.shape[3]
         for name in ("k_pool", "v_pool", "k2_pool", "k3_pool"):
@@ -273,10 +303,20 @@ class AssembledCache:
         self._c_cache = self._make_c_cache()
 
     def _make_c_cache(self):
+        ready = None
+        if self.layer_events is not None:
+            self._c_events = (_lib.c_vp * len(self.layer_events))(*[e.cuda_event for e in self.layer_events])
+            ready = self._c_events
         return _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self._d_pages.data_ptr(),
                           self.context_length, self._d_tokens.data_ptr(), self._rcos.data_ptr(),
                           self._rsin.data_ptr(), self.rope_len, self._d_recomp.data_ptr(), self.k2_pool.data_ptr(),
-                          self.k3_pool.data_ptr())
+                          self.k3_pool.data_ptr(), ready)
+
+    def wait_ready(self, stream=None) -> None:
+        """Make `stream` (default: current) wait for a pipelined chunk transfer to finish."""
+        if self._copy_stream is not None:
+            torch = _lib.require_cuda()
+            (stream or torch.cuda.current_stream()).wait_stream(self._copy_stream)
 
 
 def _as_chunk(c) -> ChunkKV:
@@ -315,9 +355,40 @@ def assemble(chunks, config: ModelConfig, track_access: bool = False, *, fp32_ta
         if k is not None and len(k) != config.n_layers:
             raise IncompatibleError("chunk layer count does not match model config")
     torch = _lib.require_cuda()
+    pending = [c for c in chunks if c.pending_h2d]
     cache = AssembledCache(config, chunks, track_access, fp32_taps)
-    _lib.check(_lib.load().pkv_assemble(ctypes_ref(cache._cfg_c), ctypes_ref(cache._c_chunks),
-                                        ctypes_ref(cache._c_cache), _lib.stream_ptr(torch, stream)))
+    lib = _lib.load()
+    if not pending:
+        _lib.check(lib.pkv_assemble(ctypes_ref(cache._cfg_c), ctypes_ref(cache._c_chunks),
+                                    ctypes_ref(cache._c_cache), _lib.stream_ptr(torch, stream)))
+        return cache
+    # host-tier chunks: stream them layer by layer on a copy stream and assemble each
+    # layer as soon as it lands; query passes / Stage II wait per layer on its event
+    main = stream or torch.cuda.current_stream()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(main)  # pools and buffers were allocated / zeroed on `main`
+    events = []
+    with torch.cuda.stream(cs):
+        for li in range(config.n_layers):
+            for c in pending:
+                kp, vp = c._pinned
+                c._k_dev[li].copy_(kp[li], non_blocking=True)
+                c._v_dev[li].copy_(vp[li], non_blocking=True)
+            _lib.check(lib.pkv_assemble_layers(ctypes_ref(cache._cfg_c), ctypes_ref(cache._c_chunks),
+                                               ctypes_ref(cache._c_cache), li, li + 1, cs.cuda_stream))
+            ev = torch.cuda.Event()
+            ev.record(cs)
+            events.append(ev)
+    cache._pinned_refs = [c._pinned for c in pending]  # host buffers stay alive until the DMA is done
+    for c in pending:
+        c._k_dev.record_stream(cs)
+        c._v_dev.record_stream(cs)
+        c._pinned = None
+    for t in (cache.k_pool, cache.v_pool, cache.k2_pool, cache.k3_pool, cache._d_recomp):
+        t.record_stream(cs)
+    cache.layer_events = events
+    cache._copy_stream = cs
+    cache._c_cache = cache._make_c_cache()
     return cache
 
 
@@ -337,6 +408,7 @@ def replace_entries(cache: AssembledCache, layer: int, indices, new_keys, new_va
         raise ShapeError(f"replacement shape {nk.shape}/{nv.shape}, expected {want}")
     if cache.access_log is not None:
         cache.access_log.append(("write", layer))
+    cache.wait_ready()
     if idx.size == 0:
         return
     torch = _lib.require_cuda()

@@ -21,7 +21,8 @@ __device__ __forceinline__ void rope_pair64(float e, float o, double c, double s
 }
 
 // one thread = one (token, 16-byte column vector); loops over layers and heads
-__global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int L, int Hkv, int dkp, int head_dim,
+__global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int l0, int l1, int Hkv, int dkp,
+                                                       int head_dim,
                                                        const double* __restrict__ rcos,
                                                        const double* __restrict__ rsin, const int32_t* page_table,
                                                        __nv_bfloat16* k_pool, __nv_bfloat16* v_pool,
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
     cs[p] = i < half ? rcos[(long)t * half + i] : 1.0;
     sn[p] = i < half ? rsin[(long)t * half + i] : 0.0;
   }
-  for (int l = 0; l < L; ++l) {
+  for (int l = l0; l < l1; ++l) {
     const long src_row = ((long)l * tc + loc) * Hkv;
     const long dst_layer = (long)l * Hkv * pool_tokens;
     for (int h = 0; h < Hkv; ++h) {
@@ -74,13 +75,13 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
   }
 }
 
-int assemble_launch(const ChunkView& cv, int s, int L, int Hkv, int dkp, int head_dim, const double* rcos,
+int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp, int head_dim, const double* rcos,
                     const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
                     void* k2_pool, void* k3_pool, cudaStream_t stream) {
   if (s <= 0) return PKV_OK;
   const long threads = (long)s * (dkp / 8);
   assemble_kernel<<<ceil_div(threads, 128), 128, 0, stream>>>(
-      cv, s, L, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__nv_bfloat16*>(k_pool),
+      cv, s, l0, l1, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__nv_bfloat16*>(k_pool),
       reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, reinterpret_cast<__nv_bfloat16*>(k2_pool),
       reinterpret_cast<__nv_bfloat16*>(k3_pool));
   PKV_LAUNCHED();

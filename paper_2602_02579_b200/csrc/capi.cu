@@ -252,7 +252,8 @@ int pkv_model_create(const pkv_config* cfg, const pkv_weights* w, pkv_model** ou
 
 void pkv_model_destroy(pkv_model* m) { delete m; }
 
-int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c, void* stream) {
+int pkv_assemble_layers(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c, int32_t l0, int32_t l1,
+                        void* stream) {
   if (!cfg || !ch || !c) return set_error(PKV_ERR_ARGUMENT, "null argument");
   int lay[5];
   int rc = layout_of(cfg, lay);
@@ -260,12 +261,18 @@ int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c
   if (ch->n_chunks <= 0) return set_error(PKV_ERR_INPUT, "assemble needs at least one chunk");
   if (c->pool_tokens % 128 != 0 || c->pool_tokens < c->s) return set_error(PKV_ERR_SHAPE, "pool too small");
   if (c->rope_len < c->s) return set_error(PKV_ERR_SHAPE, "rope table shorter than the context");
+  if (l0 < 0 || l1 > cfg->n_layers || l0 >= l1) return set_error(PKV_ERR_ARGUMENT, "bad layer range");
   ChunkView cv{ch->k_nr, ch->v, ch->src_chunk, ch->src_local, ch->chunk_len};
   cudaStream_t st = S(stream);
-  if (c->recomputed) cudaMemsetAsync(const_cast<uint8_t*>(c->recomputed), 0, (size_t)c->s, st);
+  if (c->recomputed && l0 == 0) cudaMemsetAsync(const_cast<uint8_t*>(c->recomputed), 0, (size_t)c->s, st);
   ScopedTimer t__(T_ASSEMBLE, st);
-  return assemble_launch(cv, c->s, cfg->n_layers, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos, c->rope_sin,
+  return assemble_launch(cv, c->s, l0, l1, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos, c->rope_sin,
                          c->page_table, c->k_pool, c->v_pool, c->pool_tokens, c->k2_pool, c->k3_pool, st);
+}
+
+int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c, void* stream) {
+  if (!cfg) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  return pkv_assemble_layers(cfg, ch, c, 0, cfg->n_layers, stream);
 }
 
 int pkv_cache_view(const pkv_config* cfg, const pkv_cache* c, const pkv_chunks* ch, int32_t layer, int32_t is_key,
@@ -444,6 +451,9 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.fv = w.v;
     const bool scores = (flags & PKV_QP_SCORES) && per_layer;
     a.S = scores ? w.S : nullptr;
+    // pipelined transfer: layer l of the cache may still be in flight
+    if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
+      cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
     a.Opart = w.Opart;
     a.Mpart = w.Mpart;
     a.Lpart = w.Lpart;
@@ -525,6 +535,9 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
   TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
   for (int l = 0; l < cf.n_layers; ++l) {
     const pkv_layer_weights& lw = md->layers[l];
+    // the scatter must land after this layer's (possibly pipelined) assembly
+    if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
+      cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
     TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
     g.M = k;

@@ -11,7 +11,7 @@ struct ChunkView {
   const int32_t* src_local;
   const int32_t* chunk_len;
 };
-int assemble_launch(const ChunkView& cv, int s, int L, int Hkv, int dkp, int head_dim, const double* rcos,
+int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp, int head_dim, const double* rcos,
                     const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
                     void* k2_pool, void* k3_pool, cudaStream_t stream);
 int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,

@@ -164,6 +164,34 @@ def test_full_budget_repair_reproduces_joint_forward(built):
     assert np.abs(fin.first_logits - full.logits[-1]).max() <= KV_ABS
 
 
+def test_pinned_host_chunks_pipeline_is_identical(built):
+    """Host-tier chunks (pinned bf16, streamed layer by layer and overlapped with the
+    scoring pass) give exactly the device-resident result."""
+    import torch
+    P = built
+    cfg_o, seed, units, query, p = _materialise("c1")
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg, mw, dch = _device_inputs(P, cfg_o, w, chunks)
+    runs = []
+    for pinned in (False, True):
+        if pinned:
+            src = [P.ChunkKV.from_pinned(c.chunk_id, c.config_fingerprint, c.token_ids,
+                                         c.device_buffers(cfg)[0].cpu().pin_memory(),
+                                         c.device_buffers(cfg)[1].cpu().pin_memory(), cfg.head_dim) for c in dch]
+        else:
+            src = dch
+        cache = P.assemble(src, cfg, fp32_taps=False)
+        sc = P.score_prophet(mw, cfg, cache, query)
+        sel = P.select_top_p(sc, p)
+        P.recompute_selected(mw, cfg, cache, P.RecomputePlan(sel))
+        fin = P.finalize_query(mw, cfg, cache, query)
+        torch.cuda.synchronize()
+        runs.append((sc.per_layer, sel.indices, fin.first_logits))
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert runs[0][1] == runs[1][1]
+    assert np.array_equal(runs[0][2], runs[1][2])
+
+
 def test_state_machine_and_errors(built):
     P = built
     cfg_o, seed, units, query, _ = CASES["tiny_ref"][0], 42, CASES["tiny_ref"][2], CASES["tiny_ref"][3], 0.3
