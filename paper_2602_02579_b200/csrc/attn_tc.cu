@@ -43,8 +43,28 @@ struct AttnCfg {
   static constexpr int Q_BYTES = 128 * DKP * 2;   // one Q tile
   static constexpr int KV_BYTES = 128 * DKP * 2;  // one K or V page
   static constexpr int STAGES = 2;
-  static constexpr int SMEM = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
+  static constexpr int SMEM = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256 + 4096;  // + max exchange
 };
+
+// packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a)
+__device__ __forceinline__ uint64_t f32x2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f32x2_unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 
 // 2^x on the FMA pipe: floor/fraction split, degree-3 polynomial for 2^f on [0,1)
 // (max relative error 8.6e-5; P is rounded to bf16 afterwards), exponent by integer add
@@ -211,45 +231,52 @@ __global__ void __launch_bounds__(576, 1)
     if (lane == 0) mbar_arrive(q_full);
 
     float m_run = -INFINITY, l_run = 0.f;  // m in log2 units; l: this half's row sum
+    float* red = reinterpret_cast<float*>(sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES + 256);  // [2][2 tiles][2][128]
     for (int j = 0; j < n_kv_tiles; ++j) {
       mbar_wait(&s_full[t], (uint32_t)j & 1);  // also implies PV_t(j-1) is complete
       tc_fence_after();
-      const int key0 = j * 128;
-      const bool unmasked = key0 + 127 <= min_pos;
-      // pass 1: max over the whole row (both halves read it; no exchange needed)
-      float tmax = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tS + lb + c * 32, u);
+      const int key0 = j * 128 + h * 64;
+      // pass 1: this half's 64 scores -> registers (masked -> -inf only on diagonal pages)
+      float sv[64];
+      {
+        uint32_t u[32], w[32];
+        tmem_ld32(tS + lb + h * 64, u);
+        tmem_ld32(tS + lb + h * 64 + 32, w);
         tmem_ld_wait();
-        if (unmasked) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) tmax = fmaxf(tmax, __uint_as_float(u[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (key0 + c * 32 + i <= my_pos) tmax = fmaxf(tmax, __uint_as_float(u[i]));
+        for (int i = 0; i < 32; ++i) {
+          sv[i] = __uint_as_float(u[i]);
+          sv[32 + i] = __uint_as_float(w[i]);
         }
       }
+      if (key0 + 63 > min_pos) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) sv[i] = (key0 + i <= my_pos) ? sv[i] : -INFINITY;
+      }
+      float hmax = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) hmax = fmaxf(hmax, fmaxf(sv[i], sv[i + 1]));
+      // exchange the half-row maxima with the partner warp (same rows, other 64 keys)
+      float* rb = red + ((j & 1) * 2 + t) * 256;
+      rb[h * 128 + r] = hmax;
+      named_bar_sync(bar_id, 64);  // both halves have their S in registers from here on
+      const float tmax = fmaxf(hmax, rb[(h ^ 1) * 128 + r]);
       const float m_new = fmaxf(m_run, tmax * sl2);
       const bool grow = (m_new - m_run) > 8.0f;  // also true on the first tile (m_run = -inf)
       const float m_use = grow ? m_new : m_run;
-      // pass 2: this half's 64 keys -> P (bf16 pairs), a quarter of them on the FMA pipe
-      float rsum = 0.f;
-      uint32_t pk[32];
+      // pass 2: P = 2^(s*sl2 - m) with packed f32x2 FMA/ADD; 1/4 of the exponentials on
+      // the FMA pipe.  P of keys [64h, 64h+64) -> TMEM columns [32h, 32h+32) of the S
+      // buffer (safe: the partner's S is in its registers since the barrier)
+      const uint64_t sl2x2 = f32x2(sl2, sl2), negm = f32x2(-m_use, -m_use);
+      uint64_t rsum2 = f32x2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t u[32];
-        const int col = h * 64 + c * 32;
-        tmem_ld32(tS + lb + col, u);
-        tmem_ld_wait();
+        uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const bool v0 = unmasked || key0 + col + 2 * i <= my_pos;
-          const bool v1 = unmasked || key0 + col + 2 * i + 1 <= my_pos;
-          const float x0 = fmaf(__uint_as_float(u[2 * i]), sl2, -m_use);
-          const float x1 = fmaf(__uint_as_float(u[2 * i + 1]), sl2, -m_use);
+          const uint64_t x = ffma2(f32x2(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]), sl2x2, negm);
+          float x0, x1;
+          f32x2_unpack(x, x0, x1);
           float p0, p1;
           if ((i & 3) == 3) {
             p0 = exp2_poly(x0);
@@ -258,17 +285,14 @@ __global__ void __launch_bounds__(576, 1)
             p0 = ex2(x0);
             p1 = ex2(x1);
           }
-          p0 = v0 ? p0 : 0.f;
-          p1 = v1 ? p1 : 0.f;
-          rsum += p0 + p1;
-          pk[c * 16 + i] = pack_bf16(p0, p1);
+          rsum2 = fadd2(rsum2, f32x2(p0, p1));
+          pk[i] = pack_bf16(p0, p1);
         }
+        tmem_st16(tS + lb + h * 32 + c * 16, pk);
       }
-      // P of keys [64h, 64h+64) goes to TMEM columns [32h, 32h+32) of this S buffer,
-      // which the other half may still be reading: wait for both halves first
-      named_bar_sync(bar_id, 64);
-      tmem_st16(tS + lb + h * 32, *reinterpret_cast<uint32_t(*)[16]>(pk));
-      tmem_st16(tS + lb + h * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(pk + 16));
+      float rs0, rs1;
+      f32x2_unpack(rsum2, rs0, rs1);
+      const float rsum = rs0 + rs1;
       if (__any_sync(0xffffffffu, grow && j > 0)) {
         const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
 #pragma unroll 1
@@ -292,10 +316,10 @@ __global__ void __launch_bounds__(576, 1)
     mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
     tc_fence_after();
     // row sum = both halves; every MMA has completed, so the Q tile is free scratch
-    float* red = reinterpret_cast<float*>(sQ + t * Cfg::Q_BYTES);
-    red[h * 128 + r] = l_run;
+    float* lred = reinterpret_cast<float*>(sQ + t * Cfg::Q_BYTES);
+    lred[h * 128 + r] = l_run;
     named_bar_sync(bar_id, 64);
-    const float inv_l = 1.f / (red[r] + red[128 + r]);
+    const float inv_l = 1.f / (lred[r] + lred[128 + r]);
 #pragma unroll 1
     for (int c = h * DKP / 64; c < (h + 1) * DKP / 64; ++c) {
       uint32_t u[32];
