@@ -143,6 +143,7 @@ struct ProjWs {
   void* x3;        // bf16 [96][Kmax]
   long ldx;
   float* part;     // [8][Nmax][96]
+  int* cnt;        // [Nmax/128] split-K arrival counters (EPI_PROJ)
 };
 static int choose_splits(int N, int K) {
   const int m_tiles = ceil_div(N, 128), k_tiles = ceil_div(K, 64);
@@ -172,6 +173,25 @@ static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, i
     if (rc) return rc;
   }
   return PKV_OK;
+}
+
+// m <= 32: the producer already wrote x's 3 bf16 planes into ws.x3; one GEMM launch sums
+// the planes and the split-K partials (deterministically) and stores / accumulates out.
+static int proj_fused(const void* W, int N, int K, int m, float* out, long ldo, int resid, const ProjWs& ws,
+                      cudaStream_t st) {
+  GemmArgs g{};
+  g.M = N;
+  g.N = 96;
+  const int sp = choose_splits(N, K);
+  g.n_splits = sp;
+  g.k_tiles_per_split = ceil_div(ceil_div(K, 64), sp);
+  g.out = out;
+  g.ldo = ldo;
+  g.mrows = m;
+  g.resid = resid;
+  g.part = ws.part;
+  g.cnt = ws.cnt;
+  return gemm_tc_launch(EPI_PROJ, 96, W, K, ws.x3, ws.ldx, K, g, st);
 }
 
 }  // namespace pkv
@@ -332,6 +352,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.proj.x3 = cv.take<__nv_bfloat16>((size_t)96 * kmax);
   w.proj.ldx = kmax;
   w.proj.part = cv.take<float>((size_t)8 * nmax * 96);
+  w.proj.cnt = cv.take<int>((size_t)ceil_div(nmax, 128));
   w.keys_per_split = 512;
   w.n_splits = ceil_div(s_tot, w.keys_per_split);
   {
@@ -391,10 +412,18 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
   } while (0)
   TTRY(T_QP_MISC, embed_gather_launch(md->w.embed, Dp, query_ids, nullptr, m, cf.hidden_dim, w.h, Dp, st));
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
+  // m <= 32: producers write the bf16 planes of the next GEMM input directly and the
+  // projection epilogue reduces planes + split-K partials itself (one launch each)
+  const bool fused = m <= 32;
+  if (fused) cudaMemsetAsync(w.proj.cnt, 0, sizeof(int) * ceil_div(std::max({(long)md->NQKV, (long)Dp, 2L * Fp}), 128), st);
+  void* x3 = fused ? w.proj.x3 : nullptr;
+  const long ldx = w.proj.ldx;
   for (int l = 0; l < cf.n_layers; ++l) {
     const pkv_layer_weights& lw = md->layers[l];
-    TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
-    TTRY(T_QP_PROJ, proj_f32(lw.wqkv, md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
+    TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, fused ? nullptr : w.x, x3,
+                                   ldx, nullptr, st));
+    if (fused) TTRY(T_QP_PROJ, proj_fused(lw.wqkv, md->NQKV, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
+    else TTRY(T_QP_PROJ, proj_f32(lw.wqkv, md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
     __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
     __nv_bfloat16* vp = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
     const bool append = (flags & PKV_QP_APPEND_KV) != 0;
@@ -457,13 +486,23 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.Opart = w.Opart;
     a.Mpart = w.Mpart;
     a.Lpart = w.Lpart;
+    a.x3_out = x3;
+    a.x3_ld = ldx;
     TTRY(T_QP_ATTN, s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
                             (flags & PKV_QP_RENORM) ? 1 : 0, st));
-    TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, 1, w.proj, st));
-    TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
-    TTRY(T_QP_PROJ, proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
-    TTRY(T_QP_MISC, silu_act_launch(w.gu, m, cf.ffn_dim, Fp, w.act, st));
-    TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, 1, w.proj, st));
+    if (fused) {
+      TTRY(T_QP_PROJ, proj_fused(lw.wo, Dp, md->HQ, m, w.h, Dp, 1, w.proj, st));
+      TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, x3, ldx, nullptr, st));
+      TTRY(T_QP_PROJ, proj_fused(lw.wgu, 2 * Fp, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
+      TTRY(T_QP_MISC, silu_act_launch(w.gu, m, cf.ffn_dim, Fp, nullptr, st, x3, ldx));
+      TTRY(T_QP_PROJ, proj_fused(lw.wd, Dp, Fp, m, w.h, Dp, 1, w.proj, st));
+    } else {
+      TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, 1, w.proj, st));
+      TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
+      TTRY(T_QP_MISC, silu_act_launch(w.gu, m, cf.ffn_dim, Fp, w.act, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, 1, w.proj, st));
+    }
   }
   if ((flags & PKV_QP_LOGITS) && last_logits) {
     TTRY(T_LMHEAD, rmsnorm_launch(w.h + (long)(m - 1) * Dp, 1, cf.hidden_dim, Dp, md->w.final_norm, cf.norm_eps, w.xl, nullptr, 0,

@@ -117,6 +117,7 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
     case 128 * 16 + EPI_F32: return launch_one<128, EPI_F32>(ta, tb, args, stream);
     case 128 * 16 + EPI_RESID: return launch_one<128, EPI_RESID>(ta, tb, args, stream);
     case 96 * 16 + EPI_F32: return launch_one<96, EPI_F32>(ta, tb, args, stream);
+    case 96 * 16 + EPI_PROJ: return launch_one<96, EPI_PROJ>(ta, tb, args, stream);
     default: return set_error(PKV_ERR_ARGUMENT, "gemm: unsupported (BN=%d, epi=%d)", bn, epi);
   }
 }

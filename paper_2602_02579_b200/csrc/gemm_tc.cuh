@@ -20,6 +20,9 @@ enum GemmEpi : int {
   EPI_RESID = 2,    // C += acc                                    (fp32 residual stream)
   EPI_SILU = 3,     // C[:, n/2..] = bf16(silu(gate) * up), gate/up interleaved per 128 cols
   EPI_QKV = 4,      // rope(q), rope(k) at token positions; q -> bf16 buffer; k, v -> paged cache
+  EPI_PROJ = 5,     // narrow pass (BN = 96): y[i][n] = acc[n][i] + acc[n][32+i] + acc[n][64+i] (the 3
+                    // bf16 planes of 32 fp32 rows), stored / added to out[i][n]; split-K partials are
+                    // reduced in split order by the last-arriving CTA of each M tile (deterministic)
 };
 
 struct GemmArgs {
@@ -41,6 +44,13 @@ struct GemmArgs {
   float* tap_v;
   __nv_bfloat16* k2_pool;     // optional residual key planes (layer base), see s1_attn_tc.cu
   __nv_bfloat16* k3_pool;
+  // EPI_PROJ ---------------------------------------------------------------
+  float* out;                 // [mrows][ldo]
+  long ldo;
+  int mrows;                  // valid query rows (<= 32)
+  int resid;                  // 1: out += y
+  float* part;                // split-K partials [n_splits][tiles_m*128][32]
+  int* cnt;                   // [tiles_m] arrival counters (zero; reset by the reducing CTA)
 };
 
 template <int BN>
@@ -174,7 +184,57 @@ __global__ void __launch_bounds__(192, 1)
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * Cfg::ACC_STRIDE;
 
-      if constexpr (EPI == EPI_SILU) {
+      if constexpr (EPI == EPI_PROJ) {
+        // one thread = one output feature n; the 96 accumulator columns are the hi/mid/lo
+        // planes of the 32 query rows
+        __shared__ int s_last;
+        uint32_t a0[32], a1[32], a2[32];
+        __syncwarp();
+        tmem_ld32(t_row, a0);
+        tmem_ld32(t_row + 32, a1);
+        tmem_ld32(t_row + 64, a2);
+        tmem_ld_wait();
+        float y[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          y[i] = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
+        const int n = row;  // GEMM row == output feature
+        bool write = args.n_splits == 1;
+        if (!write) {
+          float* mine = args.part + ((long)(sp * tiles_m + mb) * 128 + row_in_tile) * 32;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(mine + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+          __threadfence();
+          named_bar_sync(1, 128);
+          if (threadIdx.x == 64) s_last = (atomicAdd(&args.cnt[mb], 1) == args.n_splits - 1) ? 1 : 0;
+          named_bar_sync(1, 128);
+          if (s_last) {
+            __threadfence();
+            // fixed split order -> bit-identical regardless of which CTA arrives last
+#pragma unroll 1
+            for (int s2 = 0; s2 < args.n_splits; ++s2) {
+              const float* p = args.part + ((long)(s2 * tiles_m + mb) * 128 + row_in_tile) * 32;
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(p + i));
+                if (s2 == 0) {
+                  y[i] = v.x; y[i + 1] = v.y; y[i + 2] = v.z; y[i + 3] = v.w;
+                } else {
+                  y[i] += v.x; y[i + 1] += v.y; y[i + 2] += v.z; y[i + 3] += v.w;
+                }
+              }
+            }
+            if (threadIdx.x == 64) args.cnt[mb] = 0;
+            write = true;
+          }
+        }
+        if (write && n < args.M) {
+          for (int i = 0; i < args.mrows; ++i) {
+            float* dst = args.out + (long)i * args.ldo + n;
+            *dst = args.resid ? *dst + y[i] : y[i];
+          }
+        }
+      } else if constexpr (EPI == EPI_SILU) {
         // gate columns [0,BN/2), up columns [BN/2,BN) of this tile feed BN/2 outputs
 #pragma unroll 1
         for (int c = 0; c < BN / 64; ++c) {

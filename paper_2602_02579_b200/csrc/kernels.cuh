@@ -29,7 +29,8 @@ int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, i
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
                      const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, void* k3_pool,
                      cudaStream_t st);
-int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st);
+int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st, void* x3 = nullptr,
+                    long ldx = 0);
 
 // SIMT fp32 narrow-pass attention (all keys, or only the fresh query keys when
 // the context keys run on the tensor cores)
@@ -61,6 +62,8 @@ struct S1Attn {
   float* Lpart;
   // whole-pool bases for the tensor-core path (TMA) and its Q-plane workspace
   void* q3;
+  void* x3_out;  // nullable: also write the output as 3 bf16 planes (next projection's B operand)
+  long x3_ld;
   const void* k1_all;
   const void* k2_all;
   const void* k3_all;

@@ -189,7 +189,9 @@ int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, i
 
 // gate/up interleaved per 256 columns -> act = f32(silu64(gate)) * up
 // (reference model.py:260-262 and 318-321)
-__global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* act) {
+// act (nullable) fp32 [m][Fp]; x3 (nullable): the 3 bf16 planes of act for the next
+// projection, rows i / 32+i / 64+i (valid rows only)
+__global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* act, __nv_bfloat16* x3, long ldx) {
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)m * Fp) return;
   const int i = (int)(gid / Fp), f = (int)(gid - (long)i * Fp);
@@ -201,12 +203,20 @@ __global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* ac
     const double gd = (double)g;
     a = (float)(gd / (1.0 + exp(-gd))) * u;
   }
-  act[gid] = a;
+  if (act) act[gid] = a;
+  if (x3) {
+    __nv_bfloat16 p, q, r;
+    split3(a, p, q, r);
+    x3[(long)i * ldx + f] = p;
+    x3[(long)(32 + i) * ldx + f] = q;
+    x3[(long)(64 + i) * ldx + f] = r;
+  }
 }
 
-int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st) {
+int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st, void* x3, long ldx) {
   const long total = (long)m * Fp;
-  silu_act_kernel<<<ceil_div(total, 256), 256, 0, st>>>(gu, m, F, Fp, act);
+  silu_act_kernel<<<ceil_div(total, 256), 256, 0, st>>>(gu, m, F, Fp, act, reinterpret_cast<__nv_bfloat16*>(x3),
+                                                        ldx);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("silu_act_kernel");
   return PKV_OK;
@@ -427,7 +437,8 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
 // combine split partials -> attention output [m][H][dkp] fp32 and the final
 // per-row (max, denominator) used by the scoring reduction
 __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const float* Lpart, int splits, int Hkv,
-                                int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin) {
+                                int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin,
+                                __nv_bfloat16* x3, long ldx) {
   extern __shared__ float wsp[];  // [splits] rescale weight of each split
   __shared__ float sM, sL;
   const int r = blockIdx.x, g = blockIdx.y;
@@ -457,7 +468,16 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
       const float w = wsp[sp];
       if (w != 0.f) acc += Opart[(((long)sp * Hkv + g) * R + r) * dkp + d] * w;
     }
-    out[((long)i * H + g * G + j) * dkp + d] = acc / L;
+    const float o = acc / L;
+    const long col = (long)(g * G + j) * dkp + d;
+    out[(long)i * H * dkp + col] = o;
+    if (x3 != nullptr) {  // the o-projection's B operand (3 bf16 planes, rows i/32+i/64+i)
+      __nv_bfloat16 p, q, rr;
+      split3(o, p, q, rr);
+      x3[(long)i * ldx + col] = p;
+      x3[(long)(32 + i) * ldx + col] = q;
+      x3[(long)(64 + i) * ldx + col] = rr;
+    }
   }
   if (threadIdx.x == 0 && Mfin != nullptr) {
     Mfin[(long)g * R + r] = M;
@@ -569,7 +589,8 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_pass1");
   s1_attn_combine<<<dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st>>>(a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
-                                                    a.dkp, attn_out, Mfin, Lfin);
+                                                    a.dkp, attn_out, Mfin, Lfin,
+                                                    reinterpret_cast<__nv_bfloat16*>(a.x3_out), a.x3_ld);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   if (a.S != nullptr && per_layer != nullptr) {
