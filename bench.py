@@ -191,6 +191,7 @@ def main():
     ap.add_argument("--p", type=float, default=0.2)
     ap.add_argument("--m", type=int, default=32)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--full-steps", type=int, default=1, help="full-prefill comparator runs (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=128)
     args = ap.parse_args()
@@ -318,6 +319,25 @@ def main():
             "phases_ms": {n: round(v[0] / args.steps, 3) for n, v in phases.items()},
             "phase_share": {n: round(v[0] / step_total, 4) for n, v in phases.items() if step_total > 0},
             "kernel_rooflines": rooflines}
+
+    # ---- the north star's comparator: full GPU prefill of the same request, same kernels
+    if args.full_steps > 0:
+        pipe.full_prefill_step()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.full_steps):
+            pipe.full_prefill_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        full_ms = f0.elapsed_time(f1) / args.full_steps
+        H, dk = cfg.n_heads, cfg.head_dim
+        full_tf = 2.0 * s * dm.weight_bytes(include_head=False) / 2 + 4.0 * L * H * dk * s * (s + 1) / 2
+        line["full_prefill"] = {"ttft_ms": full_ms, "tok_per_s": s / (full_ms / 1e3),
+                                "ttft_ratio_full_over_prophet": full_ms / ms,
+                                "tflops": full_tf / (full_ms / 1e3) / 1e12,
+                                "what": "Stage II with all s context tokens selected (no chunk reuse) + finalize, "
+                                        "eager launches"}
 
     # ---- e2e through the public API with host (pinned) inputs
     if args.e2e_steps > 0:

@@ -51,6 +51,26 @@ class PrefillPipeline:
         torch = _lib.require_cuda()
         self.query.copy_(torch.as_tensor(np.asarray(ids, dtype=np.int32)), non_blocking=True)
 
+    def full_prefill_step(self, stream=None) -> None:
+        """The comparator of the north star's TTFT ratio: a full GPU prefill of the same
+        request (reference model.py:332-359 over context + query) with the same kernels --
+        Stage II with every context token selected (every cache entry recomputed, no chunk
+        reuse), then the query pass for the first-token logits."""
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        if not hasattr(self, "_all_idx"):
+            self._all_idx = torch.arange(self.s, dtype=torch.int32, device=self.cache.device)
+            self._ws_full = torch.empty(lib.pkv_recompute_workspace(self.dm.handle, self.s), dtype=torch.uint8,
+                                        device=self.cache.device)
+        st = _lib.stream_ptr(torch, stream)
+        c = self.cache
+        cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
+        _lib.check(lib.pkv_recompute(self.dm.handle, cc, self._all_idx.data_ptr(), self.s, None, None,
+                                     self._ws_full.data_ptr(), self._ws_full.numel(), st))
+        _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_final, None,
+                                      None, None, self.logits.data_ptr(), self.ws_qp.data_ptr(), self.ws_qp.numel(),
+                                      st))
+
     def capture(self):
         """Record one step into a CUDA graph (call after a warm-up step so every
         kernel attribute is set); replay() then launches the ~1.5k kernels of a
