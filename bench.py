@@ -4,10 +4,17 @@ Step = one full prefill of one RAG request: assemble 16 precomputed 2048-token
 chunks (Llama-3-8B shape, random init, synthetic inputs) into the paged cache,
 score the context with the 32-token query (fp32-faithful narrow pass), fuse +
 top-k at p = 0.2, Stage-II recompute of k = 6554 tokens, finalize -> first-token
-logits.  value = effective prefill tok/s = n_gpus * s / TTFT (weak scaling: one
-independent request per GPU, no data-path collective).
+logits.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (one process per GPU under torchrun), --mode:
+  heads     (default for N > 1; BASELINE configs[2]) one 32k request head-sharded over
+            the N GPUs (tensor parallel, paper_2602_02579_b200.tp): per-layer NCCL sums of
+            the per-token score partials before the global top-k and of the o/down
+            projection outputs; value = s / TTFT (strong scaling)
+  requests  (configs[4]-style) one independent request per GPU, no data-path
+            collective; value = N * s / TTFT (weak scaling)
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode heads|requests]
 """
 
 from __future__ import annotations
@@ -194,6 +201,7 @@ def main():
     ap.add_argument("--full-steps", type=int, default=1, help="full-prefill comparator runs (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=128)
+    ap.add_argument("--mode", default="auto", choices=["auto", "heads", "requests"])
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -219,10 +227,27 @@ def main():
     cfg = P.ModelConfig(**{k: cfgd[k] for k in ("n_layers", "n_heads", "n_kv_heads", "head_dim", "hidden_dim",
                                                 "ffn_dim", "vocab_size", "rope_theta")})
     s = cfgd["n_chunks"] * cfgd["chunk_len"]
-    dm = P.DeviceModel.random(cfg, seed=0)
-    chunks = random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=1 + rank)
+    mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
+    heads = mode == "heads" and world > 1
+    if heads:
+        # one request, KV heads (and ffn blocks) sharded over the ranks; every rank builds
+        # the same seeded model / chunk store and keeps its slice
+        from paper_2602_02579_b200 import tp
+        comm = tp.nccl_comm()
+        full = P.DeviceModel.random(cfg, seed=0)
+        dm = full.shard(rank, world, comm.handle)
+        del full
+        full_chunks = random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=1)
+        chunks = tp.shard_chunks(full_chunks, rank, world)
+        del full_chunks
+        torch.cuda.empty_cache()
+        qseed = 7
+    else:
+        dm = P.DeviceModel.random(cfg, seed=0)
+        chunks = random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=1 + rank)
+        qseed = 7 + rank
     pipe = PrefillPipeline(dm, chunks, args.m, args.p)
-    rng = np.random.default_rng(7 + rank)
+    rng = np.random.default_rng(qseed)
     query = rng.integers(0, cfg.vocab_size, args.m)
     pipe.set_query(query)
     stream = torch.cuda.current_stream()
@@ -242,10 +267,21 @@ def main():
     _lib.timing(False)
     eager_phases = {n: (v[0] / args.steps, v[1]) for n, v in phases.items()}
     phases = {n: (v[0] / args.steps, v[1] / args.steps) for n, v in phases.items()}
-    # CUDA graph of one step for the timed region
-    pipe.capture()
-    for _ in range(max(1, args.warmup)):
-        pipe.replay()
+    # CUDA graph of one step for the timed region (eager launches if capture fails,
+    # e.g. a collective back end that cannot be captured)
+    launch_mode = "CUDA graph of one prefill step, replayed K times"
+    try:
+        pipe.capture()
+        for _ in range(max(1, args.warmup)):
+            pipe.replay()
+    except Exception as e:  # noqa: BLE001
+        launch_mode = f"eager launches (graph capture failed: {type(e).__name__})"
+        pipe.replay = pipe.step
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for _ in range(max(1, args.warmup)):
+            pipe.step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -263,19 +299,22 @@ def main():
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     phases = {n: (v[0] * args.steps, v[1] * args.steps) for n, v in phases.items()}
-    # weak scaling: each rank serves its own request (paper_2602_02579_b200.dist), the
-    # job is as slow as its slowest rank
+    # the job is as slow as its slowest rank; requests mode: each rank serves its own
+    # request (weak scaling); heads mode: all ranks serve one request (strong scaling)
     from paper_2602_02579_b200 import dist as pdist
     ms = pdist.max_over_ranks(ms, device="cuda")
     if world > 1:
         dist.barrier()
-    value = world * s / (ms / 1e3)
+    value = (1 if heads else world) * s / (ms / 1e3)
 
     # ---- roofline of every kernel group; the dominant one is reported
     hbm, tf_burst, tf_sust, peak_kind = _peaks()
     idx = pipe.idx[: pipe.k].cpu().numpy().astype(np.int64)
     k = pipe.k
-    L, H, Hkv, dk, D, F = cfg.n_layers, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.hidden_dim, cfg.ffn_dim
+    # per-rank work: this rank's heads / ffn slice when head-sharded
+    lcfg = dm.cache_config
+    L, H, Hkv, dk, D = cfg.n_layers, lcfg.n_heads, lcfg.n_kv_heads, cfg.head_dim, cfg.hidden_dim
+    F = cfg.ffn_dim // dm.tp_world
     lay = cfg.layout()
     work = {  # per launch group: (bound, algorithmic units, unit)
         "assemble": ("hbm", 4.0 * L * s * Hkv * lay.dkp * 2, "GB/s"),
@@ -307,13 +346,15 @@ def main():
                 peak_kind=f"{peak_kind} ({'sustained bf16' if rooflines[dominant]['bound'] == 'tensor' else 'HBM copy'})")
 
     line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True,
+            "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16 (Stage II) / fp32-faithful (narrow passes)",
             "data": "synthetic (random-init weights, N(0,1) chunk K/V, uniform token ids)",
             "config": {"workload": args.config, "model": "Llama-3-8B shape" if "llama" in args.config else
                        "Mistral-7B shape", "s": s, "chunks": cfgd["n_chunks"], "m": args.m, "p": args.p, "k": k,
-                       "parallelism": f"request-dp{world}", "l2": "inputs larger than L2 (16 GB weights, 4.3 GB KV)"},
-            "gpu_launches": int(n_launch), "launch_mode": "CUDA graph of one prefill step, replayed K times",
+                       "parallelism": f"tp{world} (KV-head sharded, NCCL)" if heads else f"request-dp{world}",
+                       "l2": "inputs larger than L2 (16 GB weights, 4.3 GB KV)"},
+            "gpu_launches": int(n_launch), "launch_mode": launch_mode,
             "clocks": clk, "roofline": roof,
             "eager_phases_ms": {n: round(v[0], 3) for n, v in eager_phases.items()},
             "phases_ms": {n: round(v[0] / args.steps, 3) for n, v in phases.items()},
@@ -351,7 +392,7 @@ def main():
             # layer, overlapped with the scoring pass
             dch = [P.ChunkKV.from_pinned(i, "device-random", ids, a, b, cfg.head_dim)
                    for i, (a, b, ids) in enumerate(host)]
-            cache = P.assemble(dch, cfg, fp32_taps=False)
+            cache = P.assemble(dch, dm.cache_config, fp32_taps=False)
             sc = P.score_prophet(mw, cfg, cache, query)
             sel = P.select_top_p(sc, args.p)
             P.recompute_selected(mw, cfg, cache, P.RecomputePlan(sel))
@@ -369,7 +410,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         d2h = L * s * 4 + s * 4 + k * 4 + cfg.vocab_size * 4
-        line["e2e"] = {"value": world * s / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
+        line["e2e"] = {"value": (1 if heads else world) * s / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
                        "h2d_bytes_per_step": int(h2d + args.m * 8), "d2h_bytes_per_step": int(d2h),
                        "path": "assemble -> score_prophet -> select_top_p -> recompute_selected -> finalize_query, "
                                "chunk K/V copied from pinned host memory each step (layer-pipelined with "

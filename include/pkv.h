@@ -171,6 +171,41 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* cache, int32_t l
 int pkv_cache_view(const pkv_config* cfg, const pkv_cache* cache, const pkv_chunks* chunks, int32_t layer, int32_t is_key,
                    float* out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Head-sharded (tensor-parallel) prefill -- SURVEY §8(e), config C3 on 2/4/8 GPUs.
+ * No reference counterpart: the reference is single-process numpy.
+ * Rank r of W owns KV heads [r*Hkv/W, (r+1)*Hkv/W) with their query heads, and
+ * ffn blocks [r*Fp/W, (r+1)*Fp/W) (Fp/128 must be divisible by W):
+ *   wqkv_r = rows of its q, k and v heads; wo_r = its head columns of wo;
+ *   wgu_r  = its 2*Fp/W rows (gate/up 128-row blocks); wd_r = its Fp/W columns.
+ * embed, lm_head and the norm gains are replicated.  The cache and the chunk
+ * store of a rank hold its KV heads only (n_kv_heads = Hkv/W in their config).
+ * Exchange points (in-place sums): the per-(query, token) head-score partials
+ * of every layer before the f32 head mean (so all ranks select the same
+ * tokens), and the o / down projection outputs of every layer (narrow passes:
+ * [m][Dp] fp32; Stage II: [k][Dp] fp32).                                    */
+typedef struct pkv_comm pkv_comm;
+enum { PKV_DT_F32 = 0, PKV_DT_F64 = 1, PKV_DT_BF16 = 2 };
+#define PKV_MAX_LOCAL_RANKS 8
+
+/* NCCL back end (libnccl.so.2 is dlopen'ed; path may be NULL = default search) */
+int pkv_nccl_load(const char* path);
+int pkv_comm_unique_id(uint8_t id_out[128]);
+int pkv_comm_create_nccl(const uint8_t id[128], int32_t rank, int32_t world, pkv_comm** out);
+/* in-process back end: `world` rank handles (out[world]) sharing one device,
+ * each driven by its own host thread and stream (single-GPU tests of the
+ * sharded path); sums are bit-identical on every rank */
+int pkv_comm_create_local(int32_t world, pkv_comm** out);
+int pkv_comm_allreduce(pkv_comm* c, void* buf, size_t count, int32_t dtype, void* stream);
+int pkv_comm_rank(const pkv_comm* c);
+int pkv_comm_world(const pkv_comm* c);
+void pkv_comm_destroy(pkv_comm* c);
+
+/* cfg is the FULL model config; w holds rank tp_rank's weight shard (layouts
+ * above with the local head / ffn counts).  comm may be NULL iff tp_world == 1. */
+int pkv_model_create_sharded(const pkv_config* cfg, const pkv_weights* w, int32_t tp_rank, int32_t tp_world,
+                             pkv_comm* comm, pkv_model** out);
+
 /* unit-level entry points used by the kernel tests */
 int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K, float* C,
                   int64_t ldc, int32_t bn, int32_t epilogue, void* stream);

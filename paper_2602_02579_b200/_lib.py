@@ -25,6 +25,7 @@ PKV_QP_RENORM = 2
 PKV_QP_LOGITS = 4
 PKV_QP_APPEND_KV = 8
 PKV_QP_FROM_CHUNKS = 16
+PKV_DT_F32, PKV_DT_F64, PKV_DT_BF16 = 0, 1, 2
 
 
 class Config(ctypes.Structure):
@@ -74,6 +75,16 @@ _SIGS = {
     "pkv_attention_sparse": (c_i32, [c_vp, ctypes.POINTER(Cache), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "pkv_timing_enable": (c_i32, [c_i32]),
     "pkv_timing_collect": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i32), c_i32]),
+    "pkv_nccl_load": (c_i32, [ctypes.c_char_p]),
+    "pkv_comm_unique_id": (c_i32, [ctypes.c_char_p]),
+    "pkv_comm_create_nccl": (c_i32, [ctypes.c_char_p, c_i32, c_i32, ctypes.POINTER(c_vp)]),
+    "pkv_comm_create_local": (c_i32, [c_i32, ctypes.POINTER(c_vp)]),
+    "pkv_comm_allreduce": (c_i32, [c_vp, c_vp, c_sz, c_i32, c_vp]),
+    "pkv_comm_rank": (c_i32, [c_vp]),
+    "pkv_comm_world": (c_i32, [c_vp]),
+    "pkv_comm_destroy": (None, [c_vp]),
+    "pkv_model_create_sharded": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Weights), c_i32, c_i32, c_vp,
+                                         ctypes.POINTER(c_vp)]),
     "pkv_last_error": (ctypes.c_char_p, []),
     "pkv_launch_count": (ctypes.c_uint64, []),
     "pkv_version": (c_i32, []),
@@ -128,7 +139,7 @@ def launch_count() -> int:
 
 
 TIMER_NAMES = ("assemble", "qp_proj", "qp_attn", "qp_misc", "select", "rc_qkv", "rc_attn", "rc_o", "rc_gate_up",
-               "rc_down", "rc_misc", "lm_head")
+               "rc_down", "rc_misc", "lm_head", "comm")
 
 
 def timing(enable: bool) -> None:

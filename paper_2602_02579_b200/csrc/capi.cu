@@ -11,13 +11,18 @@
 #include <mutex>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 struct pkv_model {
-  pkv_config cfg;
+  pkv_config cfg;       // the full model
   int dkp, Dp, Fp, NQKV, HQ;
+  int H, Hkv, F;        // this rank's query heads, KV heads and ffn width (== cfg when unsharded);
+                        // Fp, NQKV and HQ above are the local padded sizes
+  int tp_rank = 0, tp_world = 1;
+  pkv_comm* comm = nullptr;
   pkv_weights w;
   std::vector<pkv_layer_weights> layers;
 };
@@ -87,7 +92,7 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 // ---- native phase timers (pkv_timing_enable / pkv_timing_collect): CUDA events
 // recorded on the launching stream around each kernel group when enabled.
 enum TimerCat { T_ASSEMBLE = 0, T_QP_PROJ, T_QP_ATTN, T_QP_MISC, T_SELECT, T_RC_QKV, T_RC_ATTN, T_RC_O, T_RC_GU,
-                T_RC_DOWN, T_RC_MISC, T_LMHEAD, T_NCAT };
+                T_RC_DOWN, T_RC_MISC, T_LMHEAD, T_COMM, T_NCAT };
 struct TimerRec {
   int cat;
   cudaEvent_t a, b;
@@ -245,19 +250,35 @@ int pkv_layout(const pkv_config* cfg, int32_t out[5]) {
   return PKV_OK;
 }
 
-int pkv_model_create(const pkv_config* cfg, const pkv_weights* w, pkv_model** out) {
+int pkv_model_create_sharded(const pkv_config* cfg, const pkv_weights* w, int32_t tp_rank, int32_t tp_world,
+                             pkv_comm* comm, pkv_model** out) {
+  if (!cfg || !out) return set_error(PKV_ERR_ARGUMENT, "null argument");
   int o[5];
   int rc = layout_of(cfg, o);
   if (rc) return rc;
   if (!w || !w->layers || !w->embed || !w->lm_head || !w->final_norm)
     return set_error(PKV_ERR_ARGUMENT, "null weight pointer");
+  if (tp_world < 1 || tp_rank < 0 || tp_rank >= tp_world) return set_error(PKV_ERR_ARGUMENT, "bad tp rank");
+  if (tp_world > 1) {
+    if (!comm) return set_error(PKV_ERR_ARGUMENT, "sharded model needs a communicator");
+    if (comm_world(comm) != tp_world || comm_rank(comm) != tp_rank)
+      return set_error(PKV_ERR_ARGUMENT, "communicator rank/size do not match the shard");
+    if (cfg->n_kv_heads % tp_world != 0) return set_error(PKV_ERR_CONFIG, "n_kv_heads not divisible by tp size");
+    if ((o[2] / 128) % tp_world != 0) return set_error(PKV_ERR_CONFIG, "ffn blocks not divisible by tp size");
+  }
   pkv_model* m = new pkv_model();
   m->cfg = *cfg;
   m->dkp = o[0];
   m->Dp = o[1];
-  m->Fp = o[2];
-  m->NQKV = o[3];
-  m->HQ = o[4];
+  m->H = cfg->n_heads / tp_world;
+  m->Hkv = cfg->n_kv_heads / tp_world;
+  m->Fp = o[2] / tp_world;
+  m->F = tp_world == 1 ? cfg->ffn_dim : m->Fp;  // shards carry zero-padded columns, silu(0)*0 = 0
+  m->NQKV = (m->H + 2 * m->Hkv) * m->dkp;
+  m->HQ = m->H * m->dkp;
+  m->tp_rank = tp_rank;
+  m->tp_world = tp_world;
+  m->comm = tp_world > 1 ? comm : nullptr;
   m->layers.assign(w->layers, w->layers + cfg->n_layers);
   for (auto& l : m->layers)
     if (!l.wqkv || !l.wo || !l.wgu || !l.wd || !l.attn_norm || !l.ffn_norm) {
@@ -268,6 +289,10 @@ int pkv_model_create(const pkv_config* cfg, const pkv_weights* w, pkv_model** ou
   m->w.layers = m->layers.data();
   *out = m;
   return PKV_OK;
+}
+
+int pkv_model_create(const pkv_config* cfg, const pkv_weights* w, pkv_model** out) {
+  return pkv_model_create_sharded(cfg, w, 0, 1, nullptr, out);
 }
 
 void pkv_model_destroy(pkv_model* m) { delete m; }
@@ -326,14 +351,14 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer
 struct QpWs {
   float *h, *x, *qkv, *q, *k, *v, *attn, *gu, *act, *S, *Opart, *Mpart, *Lpart, *Mfin, *Lfin, *rows, *xl;
   double* denom;
+  double* rows64;  // tensor-parallel: per-(query, token) head-sum partials, all-reduced
   __nv_bfloat16* q3;
   ProjWs proj;
   int n_splits, keys_per_split, tc_splits, tc_keys_per_split;
 };
 
 static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, size_t* total) {
-  const pkv_config& c = md->cfg;
-  const int H = c.n_heads, Hkv = c.n_kv_heads, G = H / Hkv, dkp = md->dkp;
+  const int H = md->H, Hkv = md->Hkv, G = H / Hkv, dkp = md->dkp;
   const int R = m * G;
   const int s_tot = s + m;
   QpWs w{};
@@ -371,6 +396,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
     w.S = cv.take<float>((size_t)Hkv * R * s_tot);
     w.rows = cv.take<float>((size_t)m * s);
     w.denom = cv.take<double>((size_t)m);
+    if (md->tp_world > 1) w.rows64 = cv.take<double>((size_t)m * s);
   }
   w.Opart = cv.take<float>((size_t)w.n_splits * Hkv * R * dkp);
   w.Mpart = cv.take<float>((size_t)w.n_splits * Hkv * R);
@@ -403,8 +429,13 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
   QpWs w = carve_qp(md, s, m, flags, workspace, &need);
   if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
   cudaStream_t st = S(stream);
-  const int H = cf.n_heads, Hkv = cf.n_kv_heads, G = H / Hkv, dk = cf.head_dim, dkp = md->dkp;
+  const int H = md->H, Hkv = md->Hkv, G = H / Hkv, dk = cf.head_dim, dkp = md->dkp;
   const int Dp = md->Dp, Fp = md->Fp;
+  // row-parallel o / down projections: rank 0 adds its partial into the replicated
+  // residual stream, the other ranks overwrite it with theirs, and the in-place sum
+  // over ranks yields h + sum of partials everywhere
+  const int resid = md->tp_rank == 0 ? 1 : 0;
+  pkv_comm* comm = md->comm;
   int rc;
 #define TRY(x)             \
   do {                     \
@@ -489,19 +520,23 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.x3_out = x3;
     a.x3_ld = ldx;
     TTRY(T_QP_ATTN, s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
-                            (flags & PKV_QP_RENORM) ? 1 : 0, st));
+                            (flags & PKV_QP_RENORM) ? 1 : 0, cf.n_heads, w.rows64, comm, st));
     if (fused) {
-      TTRY(T_QP_PROJ, proj_fused(lw.wo, Dp, md->HQ, m, w.h, Dp, 1, w.proj, st));
+      TTRY(T_QP_PROJ, proj_fused(lw.wo, Dp, md->HQ, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
       TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, x3, ldx, nullptr, st));
       TTRY(T_QP_PROJ, proj_fused(lw.wgu, 2 * Fp, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
-      TTRY(T_QP_MISC, silu_act_launch(w.gu, m, cf.ffn_dim, Fp, nullptr, st, x3, ldx));
-      TTRY(T_QP_PROJ, proj_fused(lw.wd, Dp, Fp, m, w.h, Dp, 1, w.proj, st));
+      TTRY(T_QP_MISC, silu_act_launch(w.gu, m, md->F, Fp, nullptr, st, x3, ldx));
+      TTRY(T_QP_PROJ, proj_fused(lw.wd, Dp, Fp, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
     } else {
-      TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, 1, w.proj, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
       TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
       TTRY(T_QP_PROJ, proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
-      TTRY(T_QP_MISC, silu_act_launch(w.gu, m, cf.ffn_dim, Fp, w.act, st));
-      TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, 1, w.proj, st));
+      TTRY(T_QP_MISC, silu_act_launch(w.gu, m, md->F, Fp, w.act, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
     }
   }
   if ((flags & PKV_QP_LOGITS) && last_logits) {
@@ -567,7 +602,11 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
   if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
   cudaStream_t st = S(stream);
   const pkv_config& cf = md->cfg;
-  const int H = cf.n_heads, Hkv = cf.n_kv_heads, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
+  const int H = md->H, Hkv = md->Hkv, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
+  // row-parallel o / down GEMMs under tensor parallelism: rank 0 accumulates into the
+  // residual stream, the others store their partial there; the sum restores h + sum
+  const int epi_resid = md->tp_rank == 0 ? EPI_RESID : EPI_F32;
+  pkv_comm* comm = md->comm;
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
   int rc;
   if (c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
@@ -611,7 +650,8 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     go.n_splits = 1;
     go.C = w.h;
     go.ldc = Dp;
-    TTRY(T_RC_O, gemm_tc_launch(EPI_RESID, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
+    TTRY(T_RC_O, gemm_tc_launch(epi_resid, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
+    TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
     TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs gg{};
     gg.M = k;
@@ -626,7 +666,8 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     gd.n_splits = 1;
     gd.C = w.h;
     gd.ldc = Dp;
-    TTRY(T_RC_DOWN, gemm_tc_launch(EPI_RESID, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
+    TTRY(T_RC_DOWN, gemm_tc_launch(epi_resid, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
+    TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
   }
   return PKV_OK;
 }
@@ -647,8 +688,8 @@ int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_
 int pkv_attention_sparse(const pkv_model* md, const pkv_cache* c, int32_t layer, const void* q, void* out,
                          const int32_t* pos, int32_t n_q, void* stream) {
   const pkv_config& cf = md->cfg;
-  return attn_tc_launch(q, out, pos, n_q, cf.n_heads, cf.n_kv_heads, cf.head_dim, md->dkp, c->k_pool, c->v_pool,
-                        (long)cf.n_layers * cf.n_kv_heads * c->pool_tokens, c->pool_tokens, layer, c->page_table,
+  return attn_tc_launch(q, out, pos, n_q, md->H, md->Hkv, cf.head_dim, md->dkp, c->k_pool, c->v_pool,
+                        (long)cf.n_layers * md->Hkv * c->pool_tokens, c->pool_tokens, layer, c->page_table,
                         S(stream));
 }
 

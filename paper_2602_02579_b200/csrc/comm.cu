@@ -1,0 +1,259 @@
+// Tensor-parallel collectives for the head-sharded prefill (SURVEY §8e, config C3 on
+// 2/4/8 GPUs).  The reference has no distribution at all (pure numpy);
+// these are the exchange points the head split introduces:
+//   - per-layer sum of the per-(query row, token) head-score partials before the
+//     f32 rounding of the head mean (model.py:294, 303-307) -> identical per-layer
+//     scores, fused scores and top-k selection on every rank;
+//   - the row-parallel o / down projections of the narrow passes and of Stage II
+//     (sum of per-rank partial outputs into the replicated fp32 residual stream).
+//
+// Two back ends behind one handle:
+//   NCCL  -- one communicator per process (one process per GPU, NVLink/NVSwitch).
+//            libnccl is dlopen'ed (torch ships 2.28.x), so libpkv.so has no link-time
+//            NCCL dependency and still loads on CPU-only hosts.
+//   local -- W ranks as W host threads of one process on ONE device: a host barrier
+//            plus a device sum kernel over the peers' buffers.  It gives the sharded
+//            math a real multi-rank execution on a single GPU (tests); the summation
+//            order is fixed (rank 0..W-1), so every rank gets bit-identical sums.
+#include <dlfcn.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "comm.cuh"
+
+struct pkv_comm {
+  int rank = 0, world = 1;
+  int kind = 0;  // 0 = NCCL, 1 = local
+  void* nccl = nullptr;
+  std::shared_ptr<pkv::LocalGroup> grp;
+};
+
+namespace pkv {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclId {
+  char internal[128];
+};
+struct NcclApi {
+  void* so = nullptr;
+  int (*get_id)(NcclId*) = nullptr;
+  int (*init_rank)(void**, int, NcclId, int) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*destroy)(void*) = nullptr;
+  const char* (*err_str)(int) = nullptr;
+};
+static NcclApi g_nccl;
+static std::mutex g_nccl_mu;
+
+static int nccl_load(const char* path) {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.so) return PKV_OK;
+  const char* cands[] = {path, getenv("PKV_NCCL_LIB"), "libnccl.so.2", "libnccl.so"};
+  void* so = nullptr;
+  for (const char* c : cands)
+    if (c && *c && (so = dlopen(c, RTLD_NOW | RTLD_GLOBAL)) != nullptr) break;
+  if (!so) return set_error(PKV_ERR_CUDA, "libnccl not found (pass its path to pkv_nccl_load)");
+  NcclApi a;
+  a.so = so;
+  a.get_id = reinterpret_cast<int (*)(NcclId*)>(dlsym(so, "ncclGetUniqueId"));
+  a.init_rank = reinterpret_cast<int (*)(void**, int, NcclId, int)>(dlsym(so, "ncclCommInitRank"));
+  a.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+      dlsym(so, "ncclAllReduce"));
+  a.destroy = reinterpret_cast<int (*)(void*)>(dlsym(so, "ncclCommDestroy"));
+  a.err_str = reinterpret_cast<const char* (*)(int)>(dlsym(so, "ncclGetErrorString"));
+  if (!a.get_id || !a.init_rank || !a.all_reduce || !a.destroy || !a.err_str)
+    return set_error(PKV_ERR_CUDA, "libnccl is missing an entry point");
+  g_nccl = a;
+  return PKV_OK;
+}
+
+static int nccl_dtype(int dt) { return dt == PKV_DT_F64 ? 8 : dt == PKV_DT_BF16 ? 9 : 7; }
+
+// ------------------------------------------------------------------ local group
+struct LocalGroup {
+  int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  bool broken = false;
+  std::vector<void*> bufs;
+  std::vector<cudaEvent_t> ready, done;
+  std::vector<void*> tmp;
+  std::vector<size_t> tmp_bytes;
+  int refs = 0;
+
+  explicit LocalGroup(int w) : world(w), bufs(w), ready(w), done(w), tmp(w, nullptr), tmp_bytes(w, 0), refs(w) {
+    for (int i = 0; i < w; ++i) {
+      cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+    }
+  }
+  ~LocalGroup() {
+    for (int i = 0; i < world; ++i) {
+      cudaEventDestroy(ready[i]);
+      cudaEventDestroy(done[i]);
+      if (tmp[i]) cudaFree(tmp[i]);
+    }
+  }
+  // host barrier of the W rank threads; a rank that never arrives (it failed
+  // before this collective) breaks the group instead of hanging the others
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
+    const long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+};
+
+struct SumPtrs {
+  const void* p[PKV_MAX_LOCAL_RANKS];
+};
+
+template <class T>
+__global__ void local_sum_kernel(SumPtrs src, int world, size_t n, T* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    T acc = reinterpret_cast<const T*>(src.p[0])[i];
+    for (int r = 1; r < world; ++r) acc += reinterpret_cast<const T*>(src.p[r])[i];
+    out[i] = acc;
+  }
+}
+__global__ void local_sum_bf16_kernel(SumPtrs src, int world, size_t n, __nv_bfloat16* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float acc = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src.p[0])[i]);
+    for (int r = 1; r < world; ++r) acc += __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src.p[r])[i]);
+    out[i] = __float2bfloat16_rn(acc);
+  }
+}
+
+static size_t dt_size(int dt) { return dt == PKV_DT_F64 ? 8 : dt == PKV_DT_BF16 ? 2 : 4; }
+
+static int local_allreduce(pkv_comm* c, void* buf, size_t count, int dt, cudaStream_t st) {
+  LocalGroup& g = *c->grp;
+  const int r = c->rank;
+  const size_t bytes = count * dt_size(dt);
+  if (g.tmp_bytes[r] < bytes) {  // grown once per group (outside any timed region)
+    if (g.tmp[r]) cudaFree(g.tmp[r]);
+    if (cudaMalloc(&g.tmp[r], bytes) != cudaSuccess) return set_error(PKV_ERR_CUDA, "local comm: out of memory");
+    g.tmp_bytes[r] = bytes;
+  }
+  g.bufs[r] = buf;
+  cudaEventRecord(g.ready[r], st);
+  if (!g.barrier()) return set_error(PKV_ERR_CUDA, "local comm: a rank did not reach the collective");
+  SumPtrs sp{};
+  for (int j = 0; j < g.world; ++j) {
+    cudaStreamWaitEvent(st, g.ready[j], 0);
+    sp.p[j] = g.bufs[j];
+  }
+  const int grid = std::max(1, std::min(4 * num_sms(), ceil_div((long)count, 256)));
+  if (dt == PKV_DT_F64)
+    local_sum_kernel<double><<<grid, 256, 0, st>>>(sp, g.world, count, reinterpret_cast<double*>(g.tmp[r]));
+  else if (dt == PKV_DT_BF16)
+    local_sum_bf16_kernel<<<grid, 256, 0, st>>>(sp, g.world, count, reinterpret_cast<__nv_bfloat16*>(g.tmp[r]));
+  else
+    local_sum_kernel<float><<<grid, 256, 0, st>>>(sp, g.world, count, reinterpret_cast<float*>(g.tmp[r]));
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("local_sum_kernel");
+  cudaEventRecord(g.done[r], st);
+  if (!g.barrier()) return set_error(PKV_ERR_CUDA, "local comm: a rank did not reach the collective");
+  for (int j = 0; j < g.world; ++j) cudaStreamWaitEvent(st, g.done[j], 0);  // peers finished reading buf
+  cudaMemcpyAsync(buf, g.tmp[r], bytes, cudaMemcpyDeviceToDevice, st);
+  return PKV_OK;
+}
+
+int comm_allreduce(pkv_comm* c, void* buf, size_t count, int dt, cudaStream_t st) {
+  if (c == nullptr || c->world <= 1 || count == 0) return PKV_OK;
+  if (c->kind == 1) return local_allreduce(c, buf, count, dt, st);
+  const int r = g_nccl.all_reduce(buf, buf, count, nccl_dtype(dt), /*ncclSum*/ 0, c->nccl, st);
+  if (r != 0) return set_error(PKV_ERR_CUDA, "ncclAllReduce: %s", g_nccl.err_str(r));
+  return PKV_OK;
+}
+
+int comm_rank(const pkv_comm* c) { return c ? c->rank : 0; }
+int comm_world(const pkv_comm* c) { return c ? c->world : 1; }
+
+}  // namespace pkv
+
+using namespace pkv;
+
+extern "C" {
+
+int pkv_nccl_load(const char* path) { return nccl_load(path); }
+
+int pkv_comm_unique_id(uint8_t out[128]) {
+  if (!out) return set_error(PKV_ERR_ARGUMENT, "null id buffer");
+  int rc = nccl_load(nullptr);
+  if (rc) return rc;
+  NcclId id;
+  const int r = g_nccl.get_id(&id);
+  if (r != 0) return set_error(PKV_ERR_CUDA, "ncclGetUniqueId: %s", g_nccl.err_str(r));
+  memcpy(out, id.internal, 128);
+  return PKV_OK;
+}
+
+int pkv_comm_create_nccl(const uint8_t id[128], int32_t rank, int32_t world, pkv_comm** out) {
+  if (!id || !out) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return set_error(PKV_ERR_ARGUMENT, "bad rank %d of %d", rank, world);
+  int rc = nccl_load(nullptr);
+  if (rc) return rc;
+  NcclId nid;
+  memcpy(nid.internal, id, 128);
+  void* comm = nullptr;
+  const int r = g_nccl.init_rank(&comm, world, nid, rank);
+  if (r != 0) return set_error(PKV_ERR_CUDA, "ncclCommInitRank: %s", g_nccl.err_str(r));
+  pkv_comm* c = new pkv_comm();
+  c->rank = rank;
+  c->world = world;
+  c->kind = 0;
+  c->nccl = comm;
+  *out = c;
+  return PKV_OK;
+}
+
+int pkv_comm_create_local(int32_t world, pkv_comm** out) {
+  if (!out) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (world < 1 || world > PKV_MAX_LOCAL_RANKS) return set_error(PKV_ERR_ARGUMENT, "local group size %d", world);
+  auto grp = std::make_shared<LocalGroup>(world);
+  for (int r = 0; r < world; ++r) {
+    pkv_comm* c = new pkv_comm();
+    c->rank = r;
+    c->world = world;
+    c->kind = 1;
+    c->grp = grp;
+    out[r] = c;
+  }
+  return PKV_OK;
+}
+
+int pkv_comm_allreduce(pkv_comm* c, void* buf, size_t count, int32_t dtype, void* stream) {
+  if (!c || !buf) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (dtype != PKV_DT_F32 && dtype != PKV_DT_F64 && dtype != PKV_DT_BF16)
+    return set_error(PKV_ERR_ARGUMENT, "dtype %d", dtype);
+  return comm_allreduce(c, buf, count, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int pkv_comm_rank(const pkv_comm* c) { return comm_rank(c); }
+int pkv_comm_world(const pkv_comm* c) { return comm_world(c); }
+
+void pkv_comm_destroy(pkv_comm* c) {
+  if (!c) return;
+  if (c->kind == 0 && c->nccl && g_nccl.destroy) g_nccl.destroy(c->nccl);
+  delete c;
+}
+
+}  // extern "C"

@@ -6,6 +6,7 @@
 // float64 like the reference.
 #include <mutex>
 #include "kernels.cuh"
+#include "comm.cuh"
 
 namespace pkv {
 
@@ -503,6 +504,26 @@ __global__ void s1_rows_kernel(const float* S, const float* Mfin, const float* L
   rows[(long)i * s + t] = (float)(acc / (double)(Hkv * G));
 }
 
+// tensor-parallel variant: this rank's head sum in f64 (rows64[i][t]); after the
+// in-place sum over ranks, s1_rows_finish rounds the mean over all H heads to f32
+__global__ void s1_rows_partial_kernel(const float* S, const float* Mfin, const float* Lfin, int Hkv, int G, int R,
+                                       int m, int s, int s_tot, double* rows64) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (t >= s) return;
+  double acc = 0.0;
+  for (int g = 0; g < Hkv; ++g)
+    for (int j = 0; j < G; ++j) {
+      const long rr = (long)g * R + j * m + i;
+      acc += (double)(expf(S[rr * s_tot + t] - Mfin[rr]) / Lfin[rr]);
+    }
+  rows64[(long)i * s + t] = acc;
+}
+__global__ void s1_rows_finish_kernel(const double* rows64, long n, int H_total, float* rows) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) rows[i] = (float)(rows64[i] / (double)H_total);
+}
+
 // optional context-only renormalisation denominators (selection.py:80-84)
 __global__ void s1_row_sums_kernel(const float* rows, int s, double* denom) {
   const int i = blockIdx.x;
@@ -533,7 +554,7 @@ __global__ void s1_query_mean_kernel(const float* rows, const double* denom, int
 }
 
 int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
-                        float* per_layer, int renorm, cudaStream_t st) {
+                        float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st) {
   S1Attn a = a_in;
   const int row_blocks = ceil_div(a.R, 128);
   int total_splits = a.n_splits;
@@ -594,10 +615,24 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   if (a.S != nullptr && per_layer != nullptr) {
-    s1_rows_kernel<<<dim3(ceil_div(a.s, 256), a.m), 256, 0, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s,
-                                                                   a.s_tot, rows);
-    PKV_LAUNCHED();
-    PKV_CHECK_LAUNCH("s1_rows_kernel");
+    if (comm_world(comm) > 1) {
+      // per-token score exchange before the global top-k: sum the ranks' head partials
+      s1_rows_partial_kernel<<<dim3(ceil_div(a.s, 256), a.m), 256, 0, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m,
+                                                                           a.s, a.s_tot, rows64);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_rows_partial_kernel");
+      int rc = comm_allreduce(comm, rows64, (size_t)a.m * a.s, PKV_DT_F64, st);
+      if (rc) return rc;
+      const long n = (long)a.m * a.s;
+      s1_rows_finish_kernel<<<ceil_div(n, 256), 256, 0, st>>>(rows64, n, H_total, rows);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_rows_finish_kernel");
+    } else {
+      s1_rows_kernel<<<dim3(ceil_div(a.s, 256), a.m), 256, 0, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s,
+                                                                     a.s_tot, rows);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_rows_kernel");
+    }
     if (renorm) {
       s1_row_sums_kernel<<<a.m, 256, 0, st>>>(rows, a.s, denom);
       PKV_LAUNCHED();

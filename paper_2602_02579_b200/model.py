@@ -252,10 +252,14 @@ def _pad2(t, rows, cols):
 class DeviceModel:
     """bf16 device weights in the kernel layout + the C-ABI model handle."""
 
-    def __init__(self, config: ModelConfig, tensors: dict, fingerprint: str):
+    def __init__(self, config: ModelConfig, tensors: dict, fingerprint: str, tp_rank: int = 0, tp_world: int = 1,
+                 comm=None):
         torch = _lib.require_cuda()
         self.config = config
         self.lay = Layout.of(config)
+        self.tp_rank, self.tp_world, self.comm = tp_rank, tp_world, comm
+        # config of this rank's cache / chunk store (its KV heads only when head-sharded)
+        self.cache_config = config if tp_world == 1 else shard_config(config, tp_world)
         self.fingerprint = fingerprint
         self.t = tensors  # keeps device memory alive
         L = config.n_layers
@@ -269,7 +273,8 @@ class DeviceModel:
                                tensors["lm_head"].data_ptr(), self._layers)
         self._cfg = config.c_struct()
         h = ctypes.c_void_p()
-        _lib.check(_lib.load().pkv_model_create(ctypes.byref(self._cfg), ctypes.byref(self._w), ctypes.byref(h)))
+        _lib.check(_lib.load().pkv_model_create_sharded(ctypes.byref(self._cfg), ctypes.byref(self._w), tp_rank,
+                                                        tp_world, comm, ctypes.byref(h)))
         self.handle = h
         self.device = tensors["embed"].device
         del torch
@@ -368,6 +373,30 @@ class DeviceModel:
                    "final_norm": ones.clone()}
         return cls(config, tensors, f"device-random-{seed}")
 
+    def shard(self, rank: int, world: int, comm) -> "DeviceModel":
+        """Rank `rank`'s tensor-parallel slice of this model (include/pkv.h, "Head-sharded
+        prefill"): its q/k/v head rows, wo head columns, gate/up 128-row blocks and wd
+        columns; embed / lm_head / norm gains are shared (same device tensors)."""
+        torch = _lib.require_cuda()
+        cfg, lay = self.config, self.lay
+        H, Hkv, dkp = cfg.n_heads, cfg.n_kv_heads, lay.dkp
+        check_shardable(cfg, world)
+        hl, kl, fl = H // world, Hkv // world, lay.Fp // world
+        layers = []
+        for lt in self.t["layers"]:
+            wqkv = lt["wqkv"]
+            q = wqkv[rank * hl * dkp:(rank + 1) * hl * dkp]
+            k = wqkv[(H + rank * kl) * dkp:(H + (rank + 1) * kl) * dkp]
+            v = wqkv[(H + Hkv + rank * kl) * dkp:(H + Hkv + (rank + 1) * kl) * dkp]
+            layers.append({"attn_norm": lt["attn_norm"], "ffn_norm": lt["ffn_norm"],
+                           "wqkv": torch.cat([q, k, v]).contiguous(),
+                           "wo": lt["wo"][:, rank * hl * dkp:(rank + 1) * hl * dkp].contiguous(),
+                           "wgu": lt["wgu"][2 * rank * fl:2 * (rank + 1) * fl].contiguous(),
+                           "wd": lt["wd"][:, rank * fl:(rank + 1) * fl].contiguous()})
+        tensors = {"layers": layers, "embed": self.t["embed"], "lm_head": self.t["lm_head"],
+                   "final_norm": self.t["final_norm"]}
+        return DeviceModel(cfg, tensors, self.fingerprint, rank, world, comm)
+
     def weight_bytes(self, include_head: bool = True) -> int:
         n = 0
         for lt in self.t["layers"]:
@@ -375,6 +404,21 @@ class DeviceModel:
         if include_head:
             n += self.t["lm_head"].numel() * 2
         return n
+
+
+def check_shardable(cfg: ModelConfig, world: int) -> None:
+    lay = Layout.of(cfg)
+    if world < 1 or cfg.n_kv_heads % world or (lay.Fp // 128) % world:
+        raise ConfigError(f"cannot head-shard {cfg.n_kv_heads} KV heads / {lay.Fp // 128} ffn blocks over {world} ranks")
+
+
+def shard_config(cfg: ModelConfig, world: int) -> ModelConfig:
+    """Config of one rank's cache and chunk store under head sharding: its H/W query
+    heads and Hkv/W KV heads (hidden/ffn sizes are those of the local view)."""
+    check_shardable(cfg, world)
+    hl = cfg.n_heads // world
+    return ModelConfig(cfg.n_layers, hl, cfg.n_kv_heads // world, cfg.head_dim, hl * cfg.head_dim,
+                       Layout.of(cfg).Fp // world, cfg.vocab_size, cfg.rope_theta, cfg.norm_eps)
 
 
 def resolve_device_model(weights, config: ModelConfig) -> DeviceModel:

@@ -26,7 +26,7 @@ class PrefillPipeline:
         self.dm = dm
         cfg = dm.config
         self.cfg = cfg
-        self.cache = AssembledCache(cfg, chunks, track_access=False, fp32_taps=False)
+        self.cache = AssembledCache(dm.cache_config, chunks, track_access=False, fp32_taps=False)
         self.cache.ensure_query_room(m)
         s = self.cache.context_length
         self.s, self.m, self.p = s, m, p

@@ -54,7 +54,8 @@ def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
     d_sel = plan.selection._dev_idx
     if d_sel is None or int(d_sel.numel()) != k:
         d_sel = torch.from_numpy(sel.astype(np.int32)).to(cache.device)
-    L, Hkv, dk = config.n_layers, config.n_kv_heads, config.head_dim
+    # the cache holds this rank's KV heads (all of them unless the model is head-sharded)
+    L, Hkv, dk = config.n_layers, cache.config.n_kv_heads, config.head_dim
     tap_k = tap_v = None
     if cache.fp32_taps:
         tap_k = torch.empty((L, k, Hkv, dk), dtype=torch.float32, device=cache.device)
@@ -95,7 +96,7 @@ def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_at
     m = int(ids.shape[0])
     if cache.access_log is not None:
         cache.access_log.extend(("read", li) for li in range(config.n_layers))
-    L, Hkv, dk = config.n_layers, config.n_kv_heads, config.head_dim
+    L, Hkv, dk = config.n_layers, cache.config.n_kv_heads, config.head_dim
     fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
     fv = torch.empty_like(fk)
     logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
