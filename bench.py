@@ -229,11 +229,17 @@ def main():
     s = cfgd["n_chunks"] * cfgd["chunk_len"]
     mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
     heads = mode == "heads" and world > 1
+    comm = None
+    if heads:
+        from paper_2602_02579_b200 import tp
+        try:
+            comm = tp.nccl_comm()
+        except Exception as e:  # noqa: BLE001 -- report and fall back to independent requests
+            print(f"[bench] NCCL communicator failed ({e}); falling back to --mode requests", file=sys.stderr)
+            heads = False
     if heads:
         # one request, KV heads (and ffn blocks) sharded over the ranks; every rank builds
         # the same seeded model / chunk store and keeps its slice
-        from paper_2602_02579_b200 import tp
-        comm = tp.nccl_comm()
         full = P.DeviceModel.random(cfg, seed=0)
         dm = full.shard(rank, world, comm.handle)
         del full

@@ -104,6 +104,9 @@ typedef struct pkv_cache {
   void* const* layer_ready;  /* nullable host array [n_layers] of cudaEvent_t: a query pass makes its
                                 stream wait on layer_ready[l] before reading layer l (pipelined
                                 host->device chunk transfer + per-layer assembly) */
+  const float* rope_cs32;    /* nullable [rope_len][head_dim/2][2]: (cos, sin) of the float64 tables
+                                rounded to f32, used by the bf16 Stage-II RoPE epilogue (the
+                                fp32-faithful paths and assembly always use the float64 tables) */
 } pkv_cache;
 
 /* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */

@@ -141,7 +141,9 @@ def rope_device_tables(theta: float, d: int, n: int):
         n_alloc = max(n, 2 * (hit[0] if hit else 0))
         c, s = _rope_tables(theta, d, n_alloc)
         dev = torch.device("cuda", torch.cuda.current_device())
-        hit = (n_alloc, torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev))
+        cs32 = np.stack([c.astype(np.float32), s.astype(np.float32)], axis=-1)  # [n][d/2][2]
+        hit = (n_alloc, torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev),
+               torch.from_numpy(np.ascontiguousarray(cs32)).to(dev))
         _ROPE_CACHE[key] = hit
     return hit
 
@@ -217,8 +219,8 @@ class AssembledCache:
             pool[:, :, s:].zero_()
         self.layer_events = None  # per-layer readiness when the chunk transfer is pipelined
         self._copy_stream = None
-        self.rope_len, self._rcos, self._rsin = rope_device_tables(config.rope_theta, config.head_dim,
-                                                                   self.pool_tokens)
+        self.rope_len, self._rcos, self._rsin, self._rcs32 = rope_device_tables(config.rope_theta, config.head_dim,
+                                                                                self.pool_tokens)
         if fp32_taps == "auto":
             fp32_taps = 2 * L * s * Hkv * config.head_dim * 4 <= (1 << 30)
         self.fp32_taps = bool(fp32_taps)
@@ -298,8 +300,8 @@ class AssembledCache:
             setattr(self, name, new)
         self.pool_tokens = new_tokens
         self._d_pages = torch.arange(new_tokens // PAGE, dtype=torch.int32, device=self.device)
-        self.rope_len, self._rcos, self._rsin = rope_device_tables(self.config.rope_theta, self.config.head_dim,
-                                                                   new_tokens)
+        self.rope_len, self._rcos, self._rsin, self._rcs32 = rope_device_tables(
+            self.config.rope_theta, self.config.head_dim, new_tokens)
         self._c_cache = self._make_c_cache()
 
     def _make_c_cache(self):
@@ -310,7 +312,7 @@ class AssembledCache:
         return _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self._d_pages.data_ptr(),
                           self.context_length, self._d_tokens.data_ptr(), self._rcos.data_ptr(),
                           self._rsin.data_ptr(), self.rope_len, self._d_recomp.data_ptr(), self.k2_pool.data_ptr(),
-                          self.k3_pool.data_ptr(), ready)
+                          self.k3_pool.data_ptr(), ready, self._rcs32.data_ptr())
 
     def wait_ready(self, stream=None) -> None:
         """Make `stream` (default: current) wait for a pipelined chunk transfer to finish."""

@@ -150,12 +150,28 @@ struct ProjWs {
   float* part;     // [8][Nmax][96]
   int* cnt;        // [Nmax/128] split-K arrival counters (EPI_PROJ)
 };
+// split-K count of a narrow-pass projection (N output features of K inputs, 128 x 64
+// weight tiles streamed once): the persistent grid runs ceil(tiles / SMs) rounds of
+// k_tiles/splits tiles each plus a fixed per-tile cost (pipeline fill + split fixup),
+// so pick the split that minimises rounds * (k per split + overhead).
 static int choose_splits(int N, int K) {
+  const char* env = getenv("PKV_PROJ_SPLITS");  // tuning override
+  const int forced = env ? atoi(env) : 0;
   const int m_tiles = ceil_div(N, 128), k_tiles = ceil_div(K, 64);
-  int sp = std::max(1, num_sms() / std::max(1, m_tiles));
-  sp = std::min(sp, 8);
-  sp = std::min(sp, std::max(1, k_tiles / 8));
-  return sp;
+  if (forced > 0) return std::min(std::min(forced, 16), k_tiles);
+  int best = 1;
+  double best_cost = 1e30;
+  for (int sp = 1; sp <= 16 && k_tiles / sp >= 4; ++sp) {
+    const int per = ceil_div(k_tiles, sp);
+    const int nsp = ceil_div(k_tiles, per);
+    const int rounds = ceil_div((long)m_tiles * nsp, num_sms());
+    const double cost = rounds * (per + 3.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = nsp;
+    }
+  }
+  return best;
 }
 static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, int m, float* out, long ldo, int mode,
                     const ProjWs& ws, cudaStream_t st) {
@@ -376,7 +392,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.act = cv.take<float>((size_t)m * md->Fp);
   w.proj.x3 = cv.take<__nv_bfloat16>((size_t)96 * kmax);
   w.proj.ldx = kmax;
-  w.proj.part = cv.take<float>((size_t)8 * nmax * 96);
+  w.proj.part = cv.take<float>((size_t)16 * nmax * 96);  // up to 16 split-K partials
   w.proj.cnt = cv.take<int>((size_t)ceil_div(nmax, 128));
   w.keys_per_split = 512;
   w.n_splits = ceil_div(s_tot, w.keys_per_split);
@@ -523,20 +539,20 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
                             (flags & PKV_QP_RENORM) ? 1 : 0, cf.n_heads, w.rows64, comm, st));
     if (fused) {
       TTRY(T_QP_PROJ, proj_fused(lw.wo, Dp, md->HQ, m, w.h, Dp, resid, w.proj, st));
-      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
+      if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
       TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, x3, ldx, nullptr, st));
       TTRY(T_QP_PROJ, proj_fused(lw.wgu, 2 * Fp, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
       TTRY(T_QP_MISC, silu_act_launch(w.gu, m, md->F, Fp, nullptr, st, x3, ldx));
       TTRY(T_QP_PROJ, proj_fused(lw.wd, Dp, Fp, m, w.h, Dp, resid, w.proj, st));
-      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
+      if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
     } else {
       TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, resid, w.proj, st));
-      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
+      if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
       TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
       TTRY(T_QP_PROJ, proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
       TTRY(T_QP_MISC, silu_act_launch(w.gu, m, md->F, Fp, w.act, st));
       TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, resid, w.proj, st));
-      TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
+      if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
     }
   }
   if ((flags & PKV_QP_LOGITS) && last_logits) {
@@ -626,6 +642,7 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     g.pos = sel;
     g.rope_cos = c->rope_cos;
     g.rope_sin = c->rope_sin;
+    g.rope_cs32 = reinterpret_cast<const float2*>(c->rope_cs32);
     g.head_dim = dk;
     g.dkp = dkp;
     g.n_heads = H;
@@ -651,7 +668,7 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     go.C = w.h;
     go.ldc = Dp;
     TTRY(T_RC_O, gemm_tc_launch(epi_resid, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
-    TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
+    if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
     TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs gg{};
     gg.M = k;
@@ -667,7 +684,7 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     gd.C = w.h;
     gd.ldc = Dp;
     TTRY(T_RC_DOWN, gemm_tc_launch(epi_resid, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
-    TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
+    if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
   }
   return PKV_OK;
 }

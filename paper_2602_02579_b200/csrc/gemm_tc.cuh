@@ -35,6 +35,7 @@ struct GemmArgs {
   const int32_t* pos;         // [M] token positions (also cache slot via page table)
   const double* rope_cos;     // [n_pos][dk/2]
   const double* rope_sin;
+  const float2* rope_cs32;    // optional f32 (cos, sin) [n_pos][dk/2]: fp32 rotation (bf16 Stage II)
   int head_dim, dkp, n_heads, n_kv_heads;
   __nv_bfloat16* k_pool;      // layer base: [Hkv][pool_tokens][dkp]
   __nv_bfloat16* v_pool;
@@ -312,7 +313,23 @@ __global__ void __launch_bounds__(192, 1)
             float vals[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]);
-            if (!is_v) {
+            if (!is_v && args.rope_cs32 != nullptr) {
+              // interleaved-pair RoPE (reference tensor.py:104-113) in fp32 with the float64
+              // factors rounded to f32: Stage II computes in bf16, so the f64 rotation buys
+              // nothing here and would make the FP64 pipe the epilogue's bottleneck
+              const int half = args.head_dim >> 1;
+              const float2* cs = args.rope_cs32 + (long)pos * half;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int i = (d0 >> 1) + j;
+                if (2 * i < args.head_dim) {
+                  const float2 f = __ldg(cs + i);
+                  const float e = vals[2 * j], o = vals[2 * j + 1];
+                  vals[2 * j] = fmaf(e, f.x, -o * f.y);
+                  vals[2 * j + 1] = fmaf(e, f.y, o * f.x);
+                }
+              }
+            } else if (!is_v) {
               // interleaved-pair RoPE with float64 factors (reference tensor.py:104-113)
               const int half = args.head_dim >> 1;
               const double* cs = args.rope_cos + (long)pos * half;

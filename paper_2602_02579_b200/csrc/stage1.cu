@@ -4,6 +4,7 @@
 // 3-way bf16 split of the activations (x = hi + mid + lo exactly), attention
 // scores / softmax / PV are fp32 SIMT, and the per-token score reductions run in
 // float64 like the reference.
+#include <algorithm>
 #include <mutex>
 #include "kernels.cuh"
 #include "comm.cuh"
@@ -63,8 +64,11 @@ __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const floa
   }
   __syncthreads();
   const double inv = 1.0 / sqrt(red[0] / (double)D + eps);
-  const long width = x3 ? ldx : ld;
-  for (int c = threadIdx.x; c < width; c += blockDim.x) {
+  // columns of this CTA: gridDim.y column chunks of the row (the next GEMM reads
+  // x3 columns [0, ld) only); every chunk recomputes the row's sum of squares
+  const long cw = (ld + gridDim.y - 1) / gridDim.y;
+  const long c0 = blockIdx.y * cw, c1 = min(ld, c0 + cw);
+  for (long c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
     float out = 0.f;
     if (i < m && c < D) out = (float)((double)h[(long)i * ld + c] * inv * (double)gain[c]);
     if (y && c < ld) y[(long)i * ld + c] = out;
@@ -79,12 +83,63 @@ __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const floa
   }
 }
 
+// Stage-II rows (bf16 GEMM operand only): one 128-thread CTA per row, the row held in
+// registers as float4 vectors (one coalesced read of h), f64 sum of squares as above
+template <int NV>
+__global__ void __launch_bounds__(128) rmsnorm_bf16_kernel(const float* __restrict__ h, int D, long ld,
+                                                           const float* __restrict__ gain, double eps,
+                                                           __nv_bfloat16* __restrict__ ybf) {
+  const long i = blockIdx.x;
+  const float4* src = reinterpret_cast<const float4*>(h + i * ld);
+  const int nvec = (int)(ld >> 2);
+  float4 v[NV];
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = j * 128 + threadIdx.x;
+    v[j] = c < nvec ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc += (double)v[j].x * v[j].x + (double)v[j].y * v[j].y + (double)v[j].z * v[j].z + (double)v[j].w * v[j].w;
+  }
+  __shared__ double red[4];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  const double inv = 1.0 / sqrt((red[0] + red[1] + red[2] + red[3]) / (double)D + eps);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+  uint2* dst = reinterpret_cast<uint2*>(ybf + i * ld);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = j * 128 + threadIdx.x;
+    if (c < nvec) {
+      const float4 g = __ldg(g4 + c);
+      const float o0 = (4 * c + 0 < D) ? (float)((double)v[j].x * inv * (double)g.x) : 0.f;
+      const float o1 = (4 * c + 1 < D) ? (float)((double)v[j].y * inv * (double)g.y) : 0.f;
+      const float o2 = (4 * c + 2 < D) ? (float)((double)v[j].z * inv * (double)g.z) : 0.f;
+      const float o3 = (4 * c + 3 < D) ? (float)((double)v[j].w * inv * (double)g.w) : 0.f;
+      dst[c] = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+    }
+  }
+}
+
 // rows = max(m, 32) blocks when x3 is given so that the padding rows get zeros
 int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
                    void* ybf, cudaStream_t st) {
+  if (ybf && !y && !x3 && ld % 4 == 0 && ld <= 128 * 4 * 16) {
+    const int nv = ceil_div(ld / 4, 128);
+    auto* out = reinterpret_cast<__nv_bfloat16*>(ybf);
+    if (nv <= 2) rmsnorm_bf16_kernel<2><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
+    else if (nv <= 4) rmsnorm_bf16_kernel<4><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
+    else if (nv <= 8) rmsnorm_bf16_kernel<8><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
+    else rmsnorm_bf16_kernel<16><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("rmsnorm_bf16_kernel");
+    return PKV_OK;
+  }
   int rows = x3 ? 32 : m;
+  if (x3 && ld > ldx) return set_error(PKV_ERR_SHAPE, "rmsnorm: plane width %ld < row width %ld", ldx, ld);
+  const int chunks = x3 ? std::max(1, std::min(8, (int)(ld / 512))) : 1;
   if (rows <= 0) return PKV_OK;
-  rmsnorm_kernel<<<rows, 256, 0, st>>>(h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
+  rmsnorm_kernel<<<dim3(rows, chunks), 256, 0, st>>>(h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
                                        reinterpret_cast<__nv_bfloat16*>(ybf));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("rmsnorm_kernel");
