@@ -66,17 +66,21 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return d;
 }
 
-// 2^x on the FMA pipe: floor/fraction split, degree-3 polynomial for 2^f on [0,1)
-// (max relative error 8.6e-5; P is rounded to bf16 afterwards), exponent by integer add
+// 2^x without the XU pipe (MUFU.EX2, FRND and F2I all issue there; with every
+// exponential on MUFU the XU pipe, not the tensor pipe, bounds this kernel):
+// round-to-nearest via the 1.5*2^23 magic add (FADD), degree-3 minimax polynomial
+// for 2^f on [-0.5, 0.5] (max relative error 7.5e-5; P is rounded to bf16 afterwards),
+// exponent added as an integer taken from the magic sum's low mantissa bits.
 __device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float xi = floorf(x);
-  const float f = x - xi;
-  const float p = fmaf(fmaf(fmaf(0.07706641f, f, 0.22764443f), f, 0.69511737f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((int)xi << 23));
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517606f, f, 0.24261151f), f, 0.69326018f), f, 0.99992803f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-template <int DKP>
+// POLY of every 8 exponentials go to the FMA-pipe polynomial, the rest to MUFU.EX2
+template <int DKP, int POLY>
 __global__ void __launch_bounds__(576, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
   using Cfg = AttnCfg<DKP>;
@@ -253,9 +257,13 @@ __global__ void __launch_bounds__(576, 1)
 #pragma unroll
         for (int i = 0; i < 64; ++i) sv[i] = (key0 + i <= my_pos) ? sv[i] : -INFINITY;
       }
-      float hmax = -INFINITY;
+      // 4 independent max chains (a single 32-deep dependent chain is pure latency)
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int i = 0; i < 64; i += 2) hmax = fmaxf(hmax, fmaxf(sv[i], sv[i + 1]));
+      for (int i = 0; i < 64; i += 8)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(sv[i + 2 * q], sv[i + 2 * q + 1]));
+      const float hmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
       // exchange the half-row maxima with the partner warp (same rows, other 64 keys)
       float* rb = red + ((j & 1) * 2 + t) * 256;
       rb[h * 128 + r] = hmax;
@@ -268,7 +276,7 @@ __global__ void __launch_bounds__(576, 1)
       // the FMA pipe.  P of keys [64h, 64h+64) -> TMEM columns [32h, 32h+32) of the S
       // buffer (safe: the partner's S is in its registers since the barrier)
       const uint64_t sl2x2 = f32x2(sl2, sl2), negm = f32x2(-m_use, -m_use);
-      uint64_t rsum2 = f32x2(0.f, 0.f);
+      uint64_t rsum2 = f32x2(0.f, 0.f), rsum2b = f32x2(0.f, 0.f);  // two sum chains
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t pk[16];
@@ -278,20 +286,22 @@ __global__ void __launch_bounds__(576, 1)
           float x0, x1;
           f32x2_unpack(x, x0, x1);
           float p0, p1;
-          if ((i & 3) == 3) {
+          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+          if ((kPolyMask >> (i & 7)) & 1u) {
             p0 = exp2_poly(x0);
             p1 = exp2_poly(x1);
           } else {
             p0 = ex2(x0);
             p1 = ex2(x1);
           }
-          rsum2 = fadd2(rsum2, f32x2(p0, p1));
+          if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
+          else rsum2 = fadd2(rsum2, f32x2(p0, p1));
           pk[i] = pack_bf16(p0, p1);
         }
         tmem_st16(tS + lb + h * 32 + c * 16, pk);
       }
       float rs0, rs1;
-      f32x2_unpack(rsum2, rs0, rs1);
+      f32x2_unpack(fadd2(rsum2, rsum2b), rs0, rs1);
       const float rsum = rs0 + rs1;
       if (__any_sync(0xffffffffu, grow && j > 0)) {
         const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
@@ -345,16 +355,16 @@ __global__ void __launch_bounds__(576, 1)
 }
 
 // ------------------------------------------------------------------ host side
-template <int DKP>
+template <int DKP, int POLY>
 static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
   using Cfg = AttnCfg<DKP>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(attn_tc_kernel<DKP>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    err = cudaFuncSetAttribute(attn_tc_kernel<DKP, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn smem attr: %s", cudaGetErrorString(err));
-  attn_tc_kernel<DKP><<<a.n_pairs * a.Hkv, 576, Cfg::SMEM, stream>>>(tk, tv, a);
+  attn_tc_kernel<DKP, POLY><<<a.n_pairs * a.Hkv, 576, Cfg::SMEM, stream>>>(tk, tv, a);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_tc_kernel");
   return PKV_OK;
@@ -386,8 +396,13 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   if (!cached_tmap(&tk, k_pool, pool_rows_total, dkp, dkp, 128) ||
       !cached_tmap(&tv, v_pool, pool_rows_total, dkp, dkp, 128))
     return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
-  if (dkp == 128) return launch_attn<128>(tk, tv, a, stream);
-  if (dkp == 64) return launch_attn<64>(tk, tv, a, stream);
+  const char* env = getenv("PKV_ATTN_POLY");  // tuning override: exponentials on the FMA pipe per 8
+  const int poly = env ? atoi(env) : 1;
+  if (dkp == 128) {
+    if (poly == 1) return launch_attn<128, 1>(tk, tv, a, stream);
+    return launch_attn<128, 2>(tk, tv, a, stream);
+  }
+  if (dkp == 64) return launch_attn<64, 2>(tk, tv, a, stream);
   return set_error(PKV_ERR_CONFIG, "attention: padded head dim %d unsupported", dkp);
 }
 
