@@ -286,23 +286,26 @@ int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStrea
 // masked -> -inf) are written to S[g][r][t] for the scoring reduction; per-split
 // online-softmax partials (m, l, O) go to the combine kernel.
 
-template <int DKP>
+// RPT rows per thread: a CTA covers ROWS = 32*RPT rows (RPT = 1 for the short fresh-key
+// split next to the tensor-core path -> 4x more CTAs; 4 for long SIMT key ranges)
+template <int DKP, int RPT>
 __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
   constexpr int LDQ = DKP + 4;
   constexpr int NQ = DKP / 32;  // float4 groups of output dims per thread
+  constexpr int ROWS = 32 * RPT;
   extern __shared__ float sm[];
-  float* Qs = sm;                  // [128][LDQ]
-  float* Ks = Qs + 128 * LDQ;      // [32][LDQ]
+  float* Qs = sm;                  // [ROWS][LDQ]
+  float* Ks = Qs + ROWS * LDQ;     // [32][LDQ]
   float* Vs = Ks + 32 * LDQ;       // [32][LDQ]
-  float* Ps = Vs + 32 * LDQ;       // [128][33]
+  float* Ps = Vs + 32 * LDQ;       // [ROWS][33]
   const int g = blockIdx.y;
   const int split = blockIdx.x;
-  const int r0 = blockIdx.z * 128;
+  const int r0 = blockIdx.z * ROWS;
   const int tid = threadIdx.x;
   const int tx = tid & 7, ty = tid >> 3;
 
   // Q rows of this block
-  for (int e = tid; e < 128 * (DKP / 4); e += 256) {
+  for (int e = tid; e < ROWS * (DKP / 4); e += 256) {
     const int rr = e / (DKP / 4), c4 = e - rr * (DKP / 4);
     const int r = r0 + rr;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -313,9 +316,9 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
     *reinterpret_cast<float4*>(Qs + rr * LDQ + c4 * 4) = v;
   }
 
-  float mrow[4], lrow[4], o[4][NQ][4];
+  float mrow[RPT], lrow[RPT], o[RPT][NQ][4];
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
+  for (int x = 0; x < RPT; ++x) {
     mrow[x] = -INFINITY;
     lrow[x] = 0.f;
 #pragma unroll
@@ -323,10 +326,10 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) o[x][q][e] = 0.f;
   }
-  int qi[4];  // query index of each of this thread's rows (for the causal part)
+  int qi[RPT];  // query index of each of this thread's rows (for the causal part)
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int r = r0 + ty * 4 + x;
+  for (int x = 0; x < RPT; ++x) {
+    const int r = r0 + ty * RPT + x;
     qi[x] = r < a.R ? r % a.m : -1;
   }
 
@@ -395,20 +398,20 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
     __syncthreads();
 
     // ---- scores: rows ty*4+x, keys b*8+tx
-    float acc[4][4];
+    float acc[RPT][4];
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
+    for (int x = 0; x < RPT; ++x)
 #pragma unroll
       for (int b = 0; b < 4; ++b) acc[x][b] = 0.f;
 #pragma unroll 4
     for (int d = 0; d < DKP; d += 4) {
-      float4 qv[4], kv[4];
+      float4 qv[RPT], kv[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) qv[x] = *reinterpret_cast<const float4*>(Qs + (ty * 4 + x) * LDQ + d);
+      for (int x = 0; x < RPT; ++x) qv[x] = *reinterpret_cast<const float4*>(Qs + (ty * RPT + x) * LDQ + d);
 #pragma unroll
       for (int b = 0; b < 4; ++b) kv[b] = *reinterpret_cast<const float4*>(Ks + (b * 8 + tx) * LDQ + d);
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int x = 0; x < RPT; ++x)
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           acc[x][b] = fmaf(qv[x].x, kv[b].x, acc[x][b]);
@@ -419,8 +422,8 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
     }
     // ---- scale, mask, store S, online softmax
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int r = r0 + ty * 4 + x;
+    for (int x = 0; x < RPT; ++x) {
+      const int r = r0 + ty * RPT + x;
       float tmax = -INFINITY;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
       for (int b = 0; b < 4; ++b) {
         const float p = (acc[x][b] == -INFINITY) ? 0.f : expf(acc[x][b] - m_new);
         psum += p;
-        Ps[(ty * 4 + x) * 33 + b * 8 + tx] = p;
+        Ps[(ty * RPT + x) * 33 + b * 8 + tx] = p;
       }
 #pragma unroll
       for (int off = 1; off < 8; off <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, off);
@@ -457,14 +460,14 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
     // ---- O += P V : rows ty*4+x, dims tx*4 + 32q + e
 #pragma unroll 4
     for (int c = 0; c < 32; ++c) {
-      float p[4];
+      float p[RPT];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) p[x] = Ps[(ty * 4 + x) * 33 + c];
+      for (int x = 0; x < RPT; ++x) p[x] = Ps[(ty * RPT + x) * 33 + c];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         const float4 vv = *reinterpret_cast<const float4*>(Vs + c * LDQ + tx * 4 + 32 * q);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
+        for (int x = 0; x < RPT; ++x) {
           o[x][q][0] = fmaf(p[x], vv.x, o[x][q][0]);
           o[x][q][1] = fmaf(p[x], vv.y, o[x][q][1]);
           o[x][q][2] = fmaf(p[x], vv.z, o[x][q][2]);
@@ -475,8 +478,8 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
   }
   // ---- partials
 #pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int r = r0 + ty * 4 + x;
+  for (int x = 0; x < RPT; ++x) {
+    const int r = r0 + ty * RPT + x;
     if (r >= a.R) continue;
     const long base = ((long)(a.split_base + split) * a.Hkv + g) * a.R + r;
     float* od = a.Opart + base * DKP;
@@ -520,9 +523,13 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
   const int j = r / m, i = r - j * m;
   for (int d = threadIdx.x; d < dkp; d += blockDim.x) {
     float acc = 0.f;
+    const float* op = Opart + ((long)g * R + r) * dkp + d;
+    const long sstride = (long)Hkv * R * dkp;
+#pragma unroll 8
     for (int sp = 0; sp < splits; ++sp) {
-      const float w = wsp[sp];
-      if (w != 0.f) acc += Opart[(((long)sp * Hkv + g) * R + r) * dkp + d] * w;
+      const float w = wsp[sp];  // 0 for empty splits, whose partials may be garbage
+      const float v = __ldg(op + sp * sstride);
+      acc = w != 0.f ? fmaf(v, w, acc) : acc;
     }
     const float o = acc / L;
     const long col = (long)(g * G + j) * dkp + d;
@@ -543,36 +550,46 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
 
 // head-mean rows over the context (model.py:294, 303-307):
 //   rows[i][t] = f32( sum_h f64(p_{h,i,t}) / H ),  p = exp(S - M) / L
-__global__ void s1_rows_kernel(const float* S, const float* Mfin, const float* Lfin, int Hkv, int G, int R, int m,
-                               int s, int s_tot, float* rows) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+// p is evaluated as 2^(S*log2e - M*log2e) * (1/L) (rel. error ~3e-7, far inside the
+// 1e-4 score tolerance); four consecutive tokens per thread (float4 rows of S), one
+// independent f64 sum chain per token.  PARTIAL (tensor parallel): this rank's head
+// sum in f64 into rows64, the mean over all H heads is taken after the rank sum.
+template <bool PARTIAL>
+__global__ void __launch_bounds__(256) s1_rows_kernel(const float* __restrict__ S, const float* __restrict__ Mfin,
+                                                      const float* __restrict__ Lfin, int Hkv, int G, int R, int m,
+                                                      int s, int s_tot, int H_total, float* rows, double* rows64) {
+  extern __shared__ float sh[];  // [Hkv*G][2]: M*log2e, 1/L of this query's rows
+  constexpr float LOG2E = 1.4426950408889634f;
   const int i = blockIdx.y;
-  if (t >= s) return;
-  double acc = 0.0;
-  for (int g = 0; g < Hkv; ++g)
-    for (int j = 0; j < G; ++j) {
-      const int r = j * m + i;
-      const long rr = (long)g * R + r;
-      const float p = expf(S[rr * s_tot + t] - Mfin[rr]) / Lfin[rr];
-      acc += (double)p;
+  const int nr = Hkv * G;
+  for (int q = threadIdx.x; q < nr; q += blockDim.x) {
+    const long rr = (long)(q / G) * R + (q % G) * m + i;
+    sh[2 * q] = Mfin[rr] * LOG2E;
+    sh[2 * q + 1] = 1.f / Lfin[rr];
+  }
+  __syncthreads();
+  const int t0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (t0 >= s) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const bool vec = (s_tot % 4 == 0) && (t0 + 4 <= s);
+  for (int q = 0; q < nr; ++q) {
+    const long rr = (long)(q / G) * R + (q % G) * m + i;
+    const float* row = S + rr * s_tot + t0;
+    const float ml2 = sh[2 * q], il = sh[2 * q + 1];
+    if (vec) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(row));
+      acc[0] += (double)(ex2(fmaf(v.x, LOG2E, -ml2)) * il);
+      acc[1] += (double)(ex2(fmaf(v.y, LOG2E, -ml2)) * il);
+      acc[2] += (double)(ex2(fmaf(v.z, LOG2E, -ml2)) * il);
+      acc[3] += (double)(ex2(fmaf(v.w, LOG2E, -ml2)) * il);
+    } else {
+      for (int c = 0; c < 4 && t0 + c < s; ++c) acc[c] += (double)(ex2(fmaf(row[c], LOG2E, -ml2)) * il);
     }
-  rows[(long)i * s + t] = (float)(acc / (double)(Hkv * G));
-}
-
-// tensor-parallel variant: this rank's head sum in f64 (rows64[i][t]); after the
-// in-place sum over ranks, s1_rows_finish rounds the mean over all H heads to f32
-__global__ void s1_rows_partial_kernel(const float* S, const float* Mfin, const float* Lfin, int Hkv, int G, int R,
-                                       int m, int s, int s_tot, double* rows64) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int i = blockIdx.y;
-  if (t >= s) return;
-  double acc = 0.0;
-  for (int g = 0; g < Hkv; ++g)
-    for (int j = 0; j < G; ++j) {
-      const long rr = (long)g * R + j * m + i;
-      acc += (double)(expf(S[rr * s_tot + t] - Mfin[rr]) / Lfin[rr]);
-    }
-  rows64[(long)i * s + t] = acc;
+  }
+  for (int c = 0; c < 4 && t0 + c < s; ++c) {
+    if (PARTIAL) rows64[(long)i * s + t0 + c] = acc[c];
+    else rows[(long)i * s + t0 + c] = (float)(acc[c] / (double)H_total);
+  }
 }
 __global__ void s1_rows_finish_kernel(const double* rows64, long n, int H_total, float* rows) {
   const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -645,20 +662,27 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     a.split_base = a.tc_splits;
     total_splits = a.tc_splits + 1;
   }
-  dim3 grid(a.n_splits, a.Hkv, row_blocks);
-  const int smem = (128 * (a.dkp + 4) + 2 * 32 * (a.dkp + 4) + 128 * 33) * 4;
+  // short fresh-key split: 32-row CTAs (4x the parallelism); long SIMT ranges: 128 rows
+  const bool small = a.tc_splits > 0;
+  const int rows_per_cta = small ? 32 : 128;
+  dim3 grid(a.n_splits, a.Hkv, ceil_div(a.R, rows_per_cta));
+  const int smem = (rows_per_cta * (a.dkp + 4) + 2 * 32 * (a.dkp + 4) + rows_per_cta * 33) * 4;
   if (a.dkp == 128) {
     static std::once_flag once;
     std::call_once(once, [] {
-      cudaFuncSetAttribute(s1_attn_pass1<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+      cudaFuncSetAttribute(s1_attn_pass1<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+      cudaFuncSetAttribute(s1_attn_pass1<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
     });
-    s1_attn_pass1<128><<<grid, 256, smem, st>>>(a);
+    if (small) s1_attn_pass1<128, 1><<<grid, 256, smem, st>>>(a);
+    else s1_attn_pass1<128, 4><<<grid, 256, smem, st>>>(a);
   } else if (a.dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
-      cudaFuncSetAttribute(s1_attn_pass1<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+      cudaFuncSetAttribute(s1_attn_pass1<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+      cudaFuncSetAttribute(s1_attn_pass1<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
     });
-    s1_attn_pass1<64><<<grid, 256, smem, st>>>(a);
+    if (small) s1_attn_pass1<64, 1><<<grid, 256, smem, st>>>(a);
+    else s1_attn_pass1<64, 4><<<grid, 256, smem, st>>>(a);
   } else {
     return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", a.dkp);
   }
@@ -670,12 +694,14 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   if (a.S != nullptr && per_layer != nullptr) {
+    const dim3 rgrid(ceil_div(a.s, 1024), a.m);
+    const size_t rsmem = (size_t)a.Hkv * a.G * 2 * sizeof(float);
     if (comm_world(comm) > 1) {
       // per-token score exchange before the global top-k: sum the ranks' head partials
-      s1_rows_partial_kernel<<<dim3(ceil_div(a.s, 256), a.m), 256, 0, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m,
-                                                                           a.s, a.s_tot, rows64);
+      s1_rows_kernel<true><<<rgrid, 256, rsmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, a.s_tot, H_total,
+                                                      nullptr, rows64);
       PKV_LAUNCHED();
-      PKV_CHECK_LAUNCH("s1_rows_partial_kernel");
+      PKV_CHECK_LAUNCH("s1_rows_kernel");
       int rc = comm_allreduce(comm, rows64, (size_t)a.m * a.s, PKV_DT_F64, st);
       if (rc) return rc;
       const long n = (long)a.m * a.s;
@@ -683,8 +709,8 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_rows_finish_kernel");
     } else {
-      s1_rows_kernel<<<dim3(ceil_div(a.s, 256), a.m), 256, 0, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s,
-                                                                     a.s_tot, rows);
+      s1_rows_kernel<false><<<rgrid, 256, rsmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, a.s_tot,
+                                                       H_total, rows, nullptr);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_rows_kernel");
     }
