@@ -80,7 +80,7 @@ struct S1TcArgs {
   long kv_row0;  // first pool row of this layer: layer * Hkv * pool_tokens
   long pool_tokens;
   const int32_t* page_table;
-  float* S;  // [Hkv][R][s_tot] or null
+  float* S;  // key-major scores [Hkv][s][R] (context keys only) or null
   float* Opart;
   float* Mpart;
   float* Lpart;

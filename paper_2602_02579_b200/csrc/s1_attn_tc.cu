@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lb = (uint32_t)(quarter * 32) << 16;
     constexpr int HC = C::KT / 2;  // columns per warp
     float m_run = -INFINITY, l_run = 0.f;  // l_run: this warp's half of the row sum
-    float* srow = (a.S != nullptr && valid) ? a.S + ((long)g * a.R + row) * a.s_tot : nullptr;
+    // scores, key-major S[g][t][r] (t < s): one warp store = 32 consecutive rows = 128 B
+    float* scol = (a.S != nullptr && valid) ? a.S + (long)g * a.s * a.R + row : nullptr;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&s_full[j & 1], (uint32_t)(j >> 1) & 1);
       tc_fence_after();
@@ -233,13 +234,12 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[j & 1]);
-      if (srow != nullptr) {
+      if (scol != nullptr) {
         if (key0 + HC <= k_end) {
 #pragma unroll
-          for (int i = 0; i < HC; i += 4)
-            *reinterpret_cast<float4*>(srow + key0 + i) = make_float4(sv[i], sv[i + 1], sv[i + 2], sv[i + 3]);
+          for (int i = 0; i < HC; ++i) scol[(long)(key0 + i) * a.R] = sv[i];
         } else {
-          for (int i = 0; i < HC && key0 + i < k_end; ++i) srow[key0 + i] = sv[i];
+          for (int i = 0; i < HC && key0 + i < k_end; ++i) scol[(long)(key0 + i) * a.R] = sv[i];
         }
       }
       const float m_new = fmaxf(m_run, tmax);

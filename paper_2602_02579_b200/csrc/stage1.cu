@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
         const bool vis = qi[x] >= 0 && t < k_end && (t < a.s || (t - a.s) <= qi[x]);
         const float sv = vis ? acc[x][b] * a.scale : -INFINITY;
         acc[x][b] = sv;
-        if (a.S != nullptr && r < a.R && t < k_end) a.S[((long)g * a.R + r) * a.s_tot + t] = sv;
+        if (a.S != nullptr && r < a.R && t < k_end && t < a.s) a.S[((long)g * a.s + t) * a.R + r] = sv;
         tmax = fmaxf(tmax, sv);
       }
 #pragma unroll
@@ -548,52 +548,86 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
   }
 }
 
-// head-mean rows over the context (model.py:294, 303-307):
-//   rows[i][t] = f32( sum_h f64(p_{h,i,t}) / H ),  p = exp(S - M) / L
-// p is evaluated as 2^(S*log2e - M*log2e) * (1/L) (rel. error ~3e-7, far inside the
-// 1e-4 score tolerance); four consecutive tokens per thread (float4 rows of S), one
-// independent f64 sum chain per token.  PARTIAL (tensor parallel): this rank's head
-// sum in f64 into rows64, the mean over all H heads is taken after the rank sum.
-template <bool PARTIAL>
-__global__ void __launch_bounds__(256) s1_rows_kernel(const float* __restrict__ S, const float* __restrict__ Mfin,
-                                                      const float* __restrict__ Lfin, int Hkv, int G, int R, int m,
-                                                      int s, int s_tot, int H_total, float* rows, double* rows64) {
-  extern __shared__ float sh[];  // [Hkv*G][2]: M*log2e, 1/L of this query's rows
+// Scores of one layer from the key-major S [Hkv][s][R] (model.py:294, 303-307 and
+// selection.py:79-86):
+//   rows[i][t]      = f32( sum_h f64(p_{h,i,t}) / H ),  p = exp(S - M) / L
+//   per_layer[t]    = f32( mean_i f64(rows[i][t]) )
+// One warp per context token, lane = query i (S loads of 32 consecutive rows).  p is
+// evaluated as 2^(S*log2e - M*log2e) * (1/L) (rel. error ~3e-7, far inside the 1e-4
+// score tolerance); the query mean is a fixed-order f64 warp reduction.
+//   MODE 0: per_layer directly;  MODE 1: rows [m][s] f32 (renormalised scoring);
+//   MODE 2: this rank's head sums rows64 [s][m] f64 (tensor parallel; summed over ranks,
+//           then s1_scores_finish applies the mean over all H heads).
+enum { SC_MEAN = 0, SC_ROWS = 1, SC_PARTIAL = 2 };
+
+__device__ __forceinline__ double warp_sum_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict__ S, const float* __restrict__ Mfin,
+                                                        const float* __restrict__ Lfin, int Hkv, int G, int R, int m,
+                                                        int s, int H_total, float* out, double* out64) {
+  extern __shared__ float2 shn[];  // [Hkv*R]: (M*log2e, 1/L) per row g*R + r
   constexpr float LOG2E = 1.4426950408889634f;
-  const int i = blockIdx.y;
-  const int nr = Hkv * G;
-  for (int q = threadIdx.x; q < nr; q += blockDim.x) {
-    const long rr = (long)(q / G) * R + (q % G) * m + i;
-    sh[2 * q] = Mfin[rr] * LOG2E;
-    sh[2 * q + 1] = 1.f / Lfin[rr];
-  }
+  for (int q = threadIdx.x; q < Hkv * R; q += blockDim.x) shn[q] = make_float2(Mfin[q] * LOG2E, 1.f / Lfin[q]);
   __syncthreads();
-  const int t0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (t0 >= s) return;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const bool vec = (s_tot % 4 == 0) && (t0 + 4 <= s);
-  for (int q = 0; q < nr; ++q) {
-    const long rr = (long)(q / G) * R + (q % G) * m + i;
-    const float* row = S + rr * s_tot + t0;
-    const float ml2 = sh[2 * q], il = sh[2 * q + 1];
-    if (vec) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(row));
-      acc[0] += (double)(ex2(fmaf(v.x, LOG2E, -ml2)) * il);
-      acc[1] += (double)(ex2(fmaf(v.y, LOG2E, -ml2)) * il);
-      acc[2] += (double)(ex2(fmaf(v.z, LOG2E, -ml2)) * il);
-      acc[3] += (double)(ex2(fmaf(v.w, LOG2E, -ml2)) * il);
-    } else {
-      for (int c = 0; c < 4 && t0 + c < s; ++c) acc[c] += (double)(ex2(fmaf(row[c], LOG2E, -ml2)) * il);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < s; t += gridDim.x * wpb) {
+    double tok = 0.0;
+    for (int i0 = 0; i0 < m; i0 += 32) {
+      const int i = i0 + lane;
+      double acc = 0.0;
+      if (i < m) {
+        for (int g = 0; g < Hkv; ++g) {
+          const float* col = S + ((long)g * s + t) * R;
+#pragma unroll 4
+          for (int j = 0; j < G; ++j) {
+            const int r = j * m + i;
+            const float2 n = shn[g * R + r];
+            acc += (double)(ex2(fmaf(__ldg(col + r), LOG2E, -n.x)) * n.y);
+          }
+        }
+      }
+      if (MODE == SC_PARTIAL) {
+        if (i < m) out64[(long)t * m + i] = acc;
+      } else {
+        const float rv = (float)(acc / (double)H_total);
+        if (MODE == SC_ROWS) {
+          if (i < m) out[(long)i * s + t] = rv;
+        } else if (i < m) {
+          tok += (double)rv;
+        }
+      }
+    }
+    if (MODE == SC_MEAN) {
+      tok = warp_sum_f64(tok);
+      if (lane == 0) out[t] = (float)(tok / (double)m);
     }
   }
-  for (int c = 0; c < 4 && t0 + c < s; ++c) {
-    if (PARTIAL) rows64[(long)i * s + t0 + c] = acc[c];
-    else rows[(long)i * s + t0 + c] = (float)(acc[c] / (double)H_total);
-  }
 }
-__global__ void s1_rows_finish_kernel(const double* rows64, long n, int H_total, float* rows) {
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) rows[i] = (float)(rows64[i] / (double)H_total);
+
+// after the rank sum: rows64 [s][m] -> MODE 0 per_layer / MODE 1 rows [m][s]
+template <int MODE>
+__global__ void __launch_bounds__(256) s1_scores_finish(const double* __restrict__ rows64, int m, int s, int H_total,
+                                                        float* out) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < s; t += gridDim.x * wpb) {
+    double tok = 0.0;
+    for (int i = lane; i < m; i += 32) {
+      const float rv = (float)(rows64[(long)t * m + i] / (double)H_total);
+      if (MODE == SC_ROWS) out[(long)i * s + t] = rv;
+      else tok += (double)rv;
+    }
+    if (MODE == SC_MEAN) {
+      tok = warp_sum_f64(tok);
+      if (lane == 0) out[t] = (float)(tok / (double)m);
+    }
+  }
 }
 
 // optional context-only renormalisation denominators (selection.py:80-84)
@@ -694,34 +728,46 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   if (a.S != nullptr && per_layer != nullptr) {
-    const dim3 rgrid(ceil_div(a.s, 1024), a.m);
-    const size_t rsmem = (size_t)a.Hkv * a.G * 2 * sizeof(float);
+    const int sgrid = std::min(ceil_div(a.s, 8), 8 * num_sms());
+    const size_t ssmem = (size_t)a.Hkv * a.R * sizeof(float2);
+    if (ssmem > 48 * 1024) {
+      static std::once_flag once;
+      std::call_once(once, [] {
+        for (auto f : {s1_scores_kernel<SC_MEAN>, s1_scores_kernel<SC_ROWS>, s1_scores_kernel<SC_PARTIAL>})
+          cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      });
+    }
+    float* target = renorm ? rows : per_layer;
     if (comm_world(comm) > 1) {
       // per-token score exchange before the global top-k: sum the ranks' head partials
-      s1_rows_kernel<true><<<rgrid, 256, rsmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, a.s_tot, H_total,
-                                                      nullptr, rows64);
+      s1_scores_kernel<SC_PARTIAL><<<sgrid, 256, ssmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+                                                              nullptr, rows64);
       PKV_LAUNCHED();
-      PKV_CHECK_LAUNCH("s1_rows_kernel");
+      PKV_CHECK_LAUNCH("s1_scores_kernel");
       int rc = comm_allreduce(comm, rows64, (size_t)a.m * a.s, PKV_DT_F64, st);
       if (rc) return rc;
-      const long n = (long)a.m * a.s;
-      s1_rows_finish_kernel<<<ceil_div(n, 256), 256, 0, st>>>(rows64, n, H_total, rows);
+      if (renorm) s1_scores_finish<SC_ROWS><<<sgrid, 256, 0, st>>>(rows64, a.m, a.s, H_total, target);
+      else s1_scores_finish<SC_MEAN><<<sgrid, 256, 0, st>>>(rows64, a.m, a.s, H_total, target);
       PKV_LAUNCHED();
-      PKV_CHECK_LAUNCH("s1_rows_finish_kernel");
+      PKV_CHECK_LAUNCH("s1_scores_finish");
     } else {
-      s1_rows_kernel<false><<<rgrid, 256, rsmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, a.s_tot,
-                                                       H_total, rows, nullptr);
+      if (renorm)
+        s1_scores_kernel<SC_ROWS><<<sgrid, 256, ssmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+                                                             target, nullptr);
+      else
+        s1_scores_kernel<SC_MEAN><<<sgrid, 256, ssmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+                                                             target, nullptr);
       PKV_LAUNCHED();
-      PKV_CHECK_LAUNCH("s1_rows_kernel");
+      PKV_CHECK_LAUNCH("s1_scores_kernel");
     }
     if (renorm) {
       s1_row_sums_kernel<<<a.m, 256, 0, st>>>(rows, a.s, denom);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_row_sums_kernel");
+      s1_query_mean_kernel<<<ceil_div(a.s, 256), 256, 0, st>>>(rows, denom, a.m, a.s, per_layer);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_query_mean_kernel");
     }
-    s1_query_mean_kernel<<<ceil_div(a.s, 256), 256, 0, st>>>(rows, renorm ? denom : nullptr, a.m, a.s, per_layer);
-    PKV_LAUNCHED();
-    PKV_CHECK_LAUNCH("s1_query_mean_kernel");
   }
   return PKV_OK;
 }
