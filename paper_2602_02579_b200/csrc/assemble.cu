@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
                                                        __nv_bfloat16* k_pool, __nv_bfloat16* v_pool,
                                                        long pool_tokens, __nv_bfloat16* k2_pool,
                                                        __nv_bfloat16* k3_pool) {
+  pdl_entry();
   const int vecs = dkp / 8;
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)s * vecs) return;
@@ -80,7 +81,7 @@ int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp
                     void* k2_pool, void* k3_pool, cudaStream_t stream) {
   if (s <= 0) return PKV_OK;
   const long threads = (long)s * (dkp / 8);
-  assemble_kernel<<<ceil_div(threads, 128), 128, 0, stream>>>(
+  launch_k(assemble_kernel, ceil_div(threads, 128), 128, 0, stream, 
       cv, s, l0, l1, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__nv_bfloat16*>(k_pool),
       reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, reinterpret_cast<__nv_bfloat16*>(k2_pool),
       reinterpret_cast<__nv_bfloat16*>(k3_pool));
@@ -96,6 +97,7 @@ int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp
 __global__ void cache_view_kernel(ChunkView cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
                                   const double* rcos, const double* rsin, const int32_t* page_table,
                                   const __nv_bfloat16* pool, long pool_tokens, int is_key, float* out) {
+  pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long total = (long)s * Hkv * head_dim;
   if (gid >= total) return;
@@ -127,7 +129,7 @@ int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int
                       long pool_tokens, int is_key, float* out, cudaStream_t stream) {
   const long total = (long)s * Hkv * head_dim;
   if (total <= 0) return PKV_OK;
-  cache_view_kernel<<<ceil_div(total, 256), 256, 0, stream>>>(cv, use_chunks, s, layer, Hkv, dkp, head_dim, rcos,
+  launch_k(cache_view_kernel, ceil_div(total, 256), 256, 0, stream, cv, use_chunks, s, layer, Hkv, dkp, head_dim, rcos,
                                                              rsin, page_table,
                                                              reinterpret_cast<const __nv_bfloat16*>(pool),
                                                              pool_tokens, is_key, out);
@@ -140,6 +142,7 @@ int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int
 __global__ void scatter_kernel(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim,
                                const float* src, const int32_t* page_table, __nv_bfloat16* pool,
                                long pool_tokens, __nv_bfloat16* pool2, __nv_bfloat16* pool3) {
+  pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long total = (long)n * Hkv * (dkp / 2);
   if (gid >= total) return;
@@ -167,7 +170,7 @@ int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int h
                    cudaStream_t stream) {
   const long total = (long)n * Hkv * (dkp / 2);
   if (total <= 0) return PKV_OK;
-  scatter_kernel<<<ceil_div(total, 256), 256, 0, stream>>>(idx, n, layer, Hkv, dkp, head_dim, src, page_table,
+  launch_k(scatter_kernel, ceil_div(total, 256), 256, 0, stream, idx, n, layer, Hkv, dkp, head_dim, src, page_table,
                                                           reinterpret_cast<__nv_bfloat16*>(pool), pool_tokens,
                                                           reinterpret_cast<__nv_bfloat16*>(pool2),
                                                           reinterpret_cast<__nv_bfloat16*>(pool3));

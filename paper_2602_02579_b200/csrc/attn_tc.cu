@@ -100,9 +100,6 @@ __global__ void __launch_bounds__(576, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x % a.Hkv;
   const int pair = a.n_pairs - 1 - blockIdx.x / a.Hkv;  // heaviest pairs first (LPT)
-  // last valid token of the pair decides how many KV pages the CTA walks
-  const int last_tok = min((2 * pair + 2) * a.T, a.n_q) - 1;
-  const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -122,6 +119,11 @@ __global__ void __launch_bounds__(576, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: q / the scattered K/V come from the previous kernel
+  griddep_launch();
+  // last valid token of the pair decides how many KV pages the CTA walks
+  const int last_tok = min((2 * pair + 2) * a.T, a.n_q) - 1;
+  const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
 
   if (warp == 16) {
     // ------------------------------------------------------------ TMA producer
@@ -364,7 +366,7 @@ static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnA
     err = cudaFuncSetAttribute(attn_tc_kernel<DKP, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn smem attr: %s", cudaGetErrorString(err));
-  attn_tc_kernel<DKP, POLY><<<a.n_pairs * a.Hkv, 576, Cfg::SMEM, stream>>>(tk, tv, a);
+  launch_k(attn_tc_kernel<DKP, POLY>, a.n_pairs * a.Hkv, 576, Cfg::SMEM, stream, tk, tv, a);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_tc_kernel");
   return PKV_OK;

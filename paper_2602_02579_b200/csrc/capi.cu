@@ -43,6 +43,16 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+// PDL is off by default: measured neutral without an early trigger and ~3% slower with
+// one (dependents parked on busy SMs); PKV_PDL=1 enables it
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PKV_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 int num_sms() {
   static int n = 0;
   static std::once_flag once;

@@ -26,7 +26,41 @@ int set_error(int code, const char* fmt, ...);
 inline int ceil_div(long a, long b) { return (int)((a + b - 1) / b); }
 int num_sms();
 
+// ---- programmatic dependent launch (PDL).  Every kernel of the stage loops is launched
+// with programmatic stream serialization: it may be scheduled while the previous kernel
+// drains, runs its prologue (barrier init, TMEM alloc, tensor-map prefetch), then calls
+// griddep_wait() -- by every thread, before its first global access -- which returns once
+// the previous grid has completed and its writes are visible.  griddep_launch() lets the
+// next kernel be scheduled as soon as every CTA of this one has started.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ------------------------------------------------------------- device side
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() {
+#ifdef PKV_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// simple kernels: wait for the previous grid, then allow the next one to be scheduled
+__device__ __forceinline__ void pdl_entry() {
+  griddep_wait();
+  griddep_launch();
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -87,7 +87,7 @@ static int launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmAr
   long tiles = (long)ceil_div(args.M, Cfg::BM) * ceil_div(args.N, BN) * args.n_splits;
   int grid = (int)std::min<long>(tiles, num_sms());
   if (grid <= 0) return PKV_OK;
-  gemm_tc_kernel<BN, EPI><<<grid, 192, Cfg::SMEM, stream>>>(ta, tb, args);
+  launch_k(gemm_tc_kernel<BN, EPI>, grid, 192, Cfg::SMEM, stream, ta, tb, args);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("gemm_tc_kernel");
   return PKV_OK;

@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: the prologue above overlapped the previous kernel; from here on we read its outputs
+  griddep_wait();
+  griddep_launch();
 
   auto tile_coords = [&](int t, int& mb, int& nb, int& sp) {
     mb = t % tiles_m;

@@ -47,6 +47,7 @@ struct S1TcCfg {
 // Q planes for the TMA: q3[((g*RB + rb)*3 + plane)*128 + r][DKP] bf16, row r of row
 // block rb = query head g*G + j, query i with rb*128 + r = j*m + i (zero padded)
 __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int RB, int dkp, __nv_bfloat16* q3) {
+  pdl_entry();
   const int g = blockIdx.y, rr = blockIdx.x;  // rr = rb*128 + r
   const int rb = rr >> 7, r = rr & 127;
   const bool valid = rr < R;
@@ -110,6 +111,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: the Q planes come from the previous kernel
+  griddep_launch();
 
   if (warp == 8) {
     // ----------------------------------------------------------- TMA producer
@@ -321,7 +324,7 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
   if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
   const int RB = ceil_div(a.R, 128);
   dim3 grid(a.n_splits, a.Hkv, RB);
-  s1_qprep_kernel<<<dim3(RB * 128, a.Hkv), 64, 0, st>>>(a.q, a.m, a.H, a.G, a.R, RB, dkp,
+  launch_k(s1_qprep_kernel, dim3(RB * 128, a.Hkv), 64, 0, st, a.q, a.m, a.H, a.G, a.R, RB, dkp,
                                                        reinterpret_cast<__nv_bfloat16*>(a.q3));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_qprep_kernel");
@@ -335,13 +338,13 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<128>::SMEM);
     });
-    s1_attn_tc_kernel<128><<<grid, 320, S1TcCfg<128>::SMEM, st>>>(m1, m2, m3, mv, mq, a);
+    launch_k(s1_attn_tc_kernel<128>, grid, 320, S1TcCfg<128>::SMEM, st, m1, m2, m3, mv, mq, a);
   } else if (dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<64>::SMEM);
     });
-    s1_attn_tc_kernel<64><<<grid, 320, S1TcCfg<64>::SMEM, st>>>(m1, m2, m3, mv, mq, a);
+    launch_k(s1_attn_tc_kernel<64>, grid, 320, S1TcCfg<64>::SMEM, st, m1, m2, m3, mv, mq, a);
   } else {
     return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", dkp);
   }

@@ -13,6 +13,7 @@
 namespace pkv {
 
 __global__ void fuse_layers_kernel(const float* per_layer, int L, int s, float* fused) {
+  pdl_entry();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= s) return;
   double acc = 0.0;
@@ -32,6 +33,7 @@ constexpr int TOPK_THREADS = 1024;
 
 __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float* v, int n, int k, int32_t* out,
                                                             int32_t* status) {
+  pdl_entry();
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix;
   __shared__ int s_remaining;
@@ -109,13 +111,14 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(const float* v, int 
 }
 
 __global__ void mark_kernel(const int32_t* idx, int n, uint8_t* flags) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) flags[idx[i]] = 1;
 }
 
 int mark_launch(const int32_t* idx, int n, uint8_t* flags, cudaStream_t st) {
   if (n <= 0) return PKV_OK;
-  mark_kernel<<<ceil_div(n, 256), 256, 0, st>>>(idx, n, flags);
+  launch_k(mark_kernel, ceil_div(n, 256), 256, 0, st, idx, n, flags);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("mark_kernel");
   return PKV_OK;
@@ -123,14 +126,14 @@ int mark_launch(const int32_t* idx, int n, uint8_t* flags, cudaStream_t st) {
 
 int fuse_layers_launch(const float* per_layer, int L, int s, float* fused, cudaStream_t st) {
   if (s <= 0) return PKV_OK;
-  fuse_layers_kernel<<<ceil_div(s, 256), 256, 0, st>>>(per_layer, L, s, fused);
+  launch_k(fuse_layers_kernel, ceil_div(s, 256), 256, 0, st, per_layer, L, s, fused);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("fuse_layers_kernel");
   return PKV_OK;
 }
 
 int topk_launch(const float* v, int n, int k, int32_t* out, int32_t* status, cudaStream_t st) {
-  topk_kernel<<<1, TOPK_THREADS, 0, st>>>(v, n, k, out, status);
+  launch_k(topk_kernel, 1, TOPK_THREADS, 0, st, v, n, k, out, status);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("topk_kernel");
   return PKV_OK;

@@ -22,6 +22,7 @@ __device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16
 
 // x [m][ld] fp32 (first `cols` valid) -> X3 [96][ldx] bf16 rows i, 32+i, 64+i
 __global__ void split3_kernel(const float* x, int m, int cols, long ld, __nv_bfloat16* x3, long ldx) {
+  pdl_entry();
   const int i = blockIdx.y;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ldx; c += gridDim.x * blockDim.x) {
     float v = (i < m && c < cols) ? x[(long)i * ld + c] : 0.f;
@@ -35,7 +36,7 @@ __global__ void split3_kernel(const float* x, int m, int cols, long ld, __nv_bfl
 
 int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, cudaStream_t st) {
   dim3 grid(ceil_div(ldx, 256) > 64 ? 64 : ceil_div(ldx, 256), 32);
-  split3_kernel<<<grid, 256, 0, st>>>(x, m, cols, ld, reinterpret_cast<__nv_bfloat16*>(x3), ldx);
+  launch_k(split3_kernel, grid, 256, 0, st, x, m, cols, ld, reinterpret_cast<__nv_bfloat16*>(x3), ldx);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("split3_kernel");
   return PKV_OK;
@@ -45,6 +46,7 @@ int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, 
 // the bf16 3-way split (rows >= m of X3 are zero-filled by this kernel).
 __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const float* gain, double eps, float* y,
                                __nv_bfloat16* x3, long ldx, __nv_bfloat16* ybf) {
+  pdl_entry();
   const int i = blockIdx.x;
   __shared__ double red[32];
   double acc = 0.0;
@@ -89,6 +91,7 @@ template <int NV>
 __global__ void __launch_bounds__(128) rmsnorm_bf16_kernel(const float* __restrict__ h, int D, long ld,
                                                            const float* __restrict__ gain, double eps,
                                                            __nv_bfloat16* __restrict__ ybf) {
+  pdl_entry();
   const long i = blockIdx.x;
   const float4* src = reinterpret_cast<const float4*>(h + i * ld);
   const int nvec = (int)(ld >> 2);
@@ -127,10 +130,10 @@ int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, dou
   if (ybf && !y && !x3 && ld % 4 == 0 && ld <= 128 * 4 * 16) {
     const int nv = ceil_div(ld / 4, 128);
     auto* out = reinterpret_cast<__nv_bfloat16*>(ybf);
-    if (nv <= 2) rmsnorm_bf16_kernel<2><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
-    else if (nv <= 4) rmsnorm_bf16_kernel<4><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
-    else if (nv <= 8) rmsnorm_bf16_kernel<8><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
-    else rmsnorm_bf16_kernel<16><<<m, 128, 0, st>>>(h, D, ld, gain, eps, out);
+    if (nv <= 2) launch_k(rmsnorm_bf16_kernel<2>, m, 128, 0, st, h, D, ld, gain, eps, out);
+    else if (nv <= 4) launch_k(rmsnorm_bf16_kernel<4>, m, 128, 0, st, h, D, ld, gain, eps, out);
+    else if (nv <= 8) launch_k(rmsnorm_bf16_kernel<8>, m, 128, 0, st, h, D, ld, gain, eps, out);
+    else launch_k(rmsnorm_bf16_kernel<16>, m, 128, 0, st, h, D, ld, gain, eps, out);
     PKV_LAUNCHED();
     PKV_CHECK_LAUNCH("rmsnorm_bf16_kernel");
     return PKV_OK;
@@ -139,7 +142,7 @@ int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, dou
   if (x3 && ld > ldx) return set_error(PKV_ERR_SHAPE, "rmsnorm: plane width %ld < row width %ld", ldx, ld);
   const int chunks = x3 ? std::max(1, std::min(8, (int)(ld / 512))) : 1;
   if (rows <= 0) return PKV_OK;
-  rmsnorm_kernel<<<dim3(rows, chunks), 256, 0, st>>>(h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
+  launch_k(rmsnorm_kernel, dim3(rows, chunks), 256, 0, st, h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
                                        reinterpret_cast<__nv_bfloat16*>(ybf));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("rmsnorm_kernel");
@@ -148,6 +151,7 @@ int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, dou
 
 // split-K partials P [splits][N][96] -> Y[i][n] (mode 0: store, 1: += residual)
 __global__ void splitk_reduce_kernel(const float* part, int splits, int N, int m, float* y, long ldy, int mode) {
+  pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)N * m) return;
   const int i = (int)(gid / N);
@@ -164,7 +168,7 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int N, int m
 
 int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, long ldy, int mode, cudaStream_t st) {
   const long total = (long)N * m;
-  splitk_reduce_kernel<<<ceil_div(total, 256), 256, 0, st>>>(part, splits, N, m, y, ldy, mode);
+  launch_k(splitk_reduce_kernel, ceil_div(total, 256), 256, 0, st, part, splits, N, m, y, ldy, mode);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("splitk_reduce_kernel");
   return PKV_OK;
@@ -179,6 +183,7 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
                                  __nv_bfloat16* k_pool, __nv_bfloat16* v_pool, long pool_tokens,
                                  const int32_t* page_table, float* fresh_k, float* fresh_v,
                                  __nv_bfloat16* k2_pool, __nv_bfloat16* k3_pool) {
+  pdl_entry();
   const int heads = H + 2 * Hkv;
   const long total = (long)m * heads * (dkp / 2);
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -234,7 +239,7 @@ int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, i
                      const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, void* k3_pool,
                      cudaStream_t st) {
   const long total = (long)m * (H + 2 * Hkv) * (dkp / 2);
-  query_qkv_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+  launch_k(query_qkv_kernel, ceil_div(total, 256), 256, 0, st, 
       qkv, m, H, Hkv, dk, dkp, pos0, rcos, rsin, q, k, v, reinterpret_cast<__nv_bfloat16*>(k_pool),
       reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v,
       reinterpret_cast<__nv_bfloat16*>(k2_pool), reinterpret_cast<__nv_bfloat16*>(k3_pool));
@@ -248,6 +253,7 @@ int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, i
 // act (nullable) fp32 [m][Fp]; x3 (nullable): the 3 bf16 planes of act for the next
 // projection, rows i / 32+i / 64+i (valid rows only)
 __global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* act, __nv_bfloat16* x3, long ldx) {
+  pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)m * Fp) return;
   const int i = (int)(gid / Fp), f = (int)(gid - (long)i * Fp);
@@ -271,7 +277,7 @@ __global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* ac
 
 int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st, void* x3, long ldx) {
   const long total = (long)m * Fp;
-  silu_act_kernel<<<ceil_div(total, 256), 256, 0, st>>>(gu, m, F, Fp, act, reinterpret_cast<__nv_bfloat16*>(x3),
+  launch_k(silu_act_kernel, ceil_div(total, 256), 256, 0, st, gu, m, F, Fp, act, reinterpret_cast<__nv_bfloat16*>(x3),
                                                         ldx);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("silu_act_kernel");
@@ -290,6 +296,7 @@ int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStrea
 // split next to the tensor-core path -> 4x more CTAs; 4 for long SIMT key ranges)
 template <int DKP, int RPT>
 __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
+  pdl_entry();
   constexpr int LDQ = DKP + 4;
   constexpr int NQ = DKP / 32;  // float4 groups of output dims per thread
   constexpr int ROWS = 32 * RPT;
@@ -498,6 +505,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
 __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const float* Lpart, int splits, int Hkv,
                                 int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin,
                                 __nv_bfloat16* x3, long ldx) {
+  pdl_entry();
   extern __shared__ float wsp[];  // [splits] rescale weight of each split
   __shared__ float sM, sL;
   const int r = blockIdx.x, g = blockIdx.y;
@@ -570,6 +578,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict__ S, const float* __restrict__ Mfin,
                                                         const float* __restrict__ Lfin, int Hkv, int G, int R, int m,
                                                         int s, int H_total, float* out, double* out64) {
+  pdl_entry();
   extern __shared__ float2 shn[];  // [Hkv*R]: (M*log2e, 1/L) per row g*R + r
   constexpr float LOG2E = 1.4426950408889634f;
   for (int q = threadIdx.x; q < Hkv * R; q += blockDim.x) shn[q] = make_float2(Mfin[q] * LOG2E, 1.f / Lfin[q]);
@@ -614,6 +623,7 @@ __global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict_
 template <int MODE>
 __global__ void __launch_bounds__(256) s1_scores_finish(const double* __restrict__ rows64, int m, int s, int H_total,
                                                         float* out) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int t = blockIdx.x * wpb + (threadIdx.x >> 5); t < s; t += gridDim.x * wpb) {
@@ -632,6 +642,7 @@ __global__ void __launch_bounds__(256) s1_scores_finish(const double* __restrict
 
 // optional context-only renormalisation denominators (selection.py:80-84)
 __global__ void s1_row_sums_kernel(const float* rows, int s, double* denom) {
+  pdl_entry();
   const int i = blockIdx.x;
   __shared__ double red[32];
   double acc = 0.0;
@@ -648,6 +659,7 @@ __global__ void s1_row_sums_kernel(const float* rows, int s, double* denom) {
 
 // per_layer[t] = f32( mean_i f64(rows[i][t]) )  (selection.py:79-86)
 __global__ void s1_query_mean_kernel(const float* rows, const double* denom, int m, int s, float* out) {
+  pdl_entry();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= s) return;
   double acc = 0.0;
@@ -707,22 +719,22 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
       cudaFuncSetAttribute(s1_attn_pass1<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
       cudaFuncSetAttribute(s1_attn_pass1<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
     });
-    if (small) s1_attn_pass1<128, 1><<<grid, 256, smem, st>>>(a);
-    else s1_attn_pass1<128, 4><<<grid, 256, smem, st>>>(a);
+    if (small) launch_k(s1_attn_pass1<128, 1>, grid, 256, smem, st, a);
+    else launch_k(s1_attn_pass1<128, 4>, grid, 256, smem, st, a);
   } else if (a.dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_pass1<64, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
       cudaFuncSetAttribute(s1_attn_pass1<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
     });
-    if (small) s1_attn_pass1<64, 1><<<grid, 256, smem, st>>>(a);
-    else s1_attn_pass1<64, 4><<<grid, 256, smem, st>>>(a);
+    if (small) launch_k(s1_attn_pass1<64, 1>, grid, 256, smem, st, a);
+    else launch_k(s1_attn_pass1<64, 4>, grid, 256, smem, st, a);
   } else {
     return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", a.dkp);
   }
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_pass1");
-  s1_attn_combine<<<dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st>>>(a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
+  launch_k(s1_attn_combine, dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st, a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin,
                                                     reinterpret_cast<__nv_bfloat16*>(a.x3_out), a.x3_ld);
   PKV_LAUNCHED();
@@ -740,31 +752,31 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     float* target = renorm ? rows : per_layer;
     if (comm_world(comm) > 1) {
       // per-token score exchange before the global top-k: sum the ranks' head partials
-      s1_scores_kernel<SC_PARTIAL><<<sgrid, 256, ssmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+      launch_k(s1_scores_kernel<SC_PARTIAL>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
                                                               nullptr, rows64);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_scores_kernel");
       int rc = comm_allreduce(comm, rows64, (size_t)a.m * a.s, PKV_DT_F64, st);
       if (rc) return rc;
-      if (renorm) s1_scores_finish<SC_ROWS><<<sgrid, 256, 0, st>>>(rows64, a.m, a.s, H_total, target);
-      else s1_scores_finish<SC_MEAN><<<sgrid, 256, 0, st>>>(rows64, a.m, a.s, H_total, target);
+      if (renorm) launch_k(s1_scores_finish<SC_ROWS>, sgrid, 256, 0, st, rows64, a.m, a.s, H_total, target);
+      else launch_k(s1_scores_finish<SC_MEAN>, sgrid, 256, 0, st, rows64, a.m, a.s, H_total, target);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_scores_finish");
     } else {
       if (renorm)
-        s1_scores_kernel<SC_ROWS><<<sgrid, 256, ssmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+        launch_k(s1_scores_kernel<SC_ROWS>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
                                                              target, nullptr);
       else
-        s1_scores_kernel<SC_MEAN><<<sgrid, 256, ssmem, st>>>(a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+        launch_k(s1_scores_kernel<SC_MEAN>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
                                                              target, nullptr);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_scores_kernel");
     }
     if (renorm) {
-      s1_row_sums_kernel<<<a.m, 256, 0, st>>>(rows, a.s, denom);
+      launch_k(s1_row_sums_kernel, a.m, 256, 0, st, rows, a.s, denom);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_row_sums_kernel");
-      s1_query_mean_kernel<<<ceil_div(a.s, 256), 256, 0, st>>>(rows, denom, a.m, a.s, per_layer);
+      launch_k(s1_query_mean_kernel, ceil_div(a.s, 256), 256, 0, st, rows, denom, a.m, a.s, per_layer);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_query_mean_kernel");
     }
@@ -775,6 +787,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
 // ------------------------------------------------------------------ lm_head
 // logits[n] = dot(x, W[n]) over D, fp32 accumulation (x = final-normed last row)
 __global__ void gemv_rows_kernel(const float* x, const __nv_bfloat16* W, int N, int D, long ldw, float* out) {
+  pdl_entry();
   extern __shared__ float xs[];
   for (int c = threadIdx.x; c < D; c += blockDim.x) xs[c] = x[c];
   __syncthreads();
@@ -799,7 +812,7 @@ __global__ void gemv_rows_kernel(const float* x, const __nv_bfloat16* W, int N, 
 
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st) {
   const int blocks = std::min(ceil_div(N, 8), num_sms() * 8);
-  gemv_rows_kernel<<<blocks, 256, D * sizeof(float), st>>>(x, reinterpret_cast<const __nv_bfloat16*>(W), N, D, ldw,
+  launch_k(gemv_rows_kernel, blocks, 256, D * sizeof(float), st, x, reinterpret_cast<const __nv_bfloat16*>(W), N, D, ldw,
                                                            out);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("gemv_rows_kernel");
@@ -809,6 +822,7 @@ int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* ou
 // embedding rows (bf16 table) -> fp32 [n][ld]
 __global__ void embed_gather_kernel(const __nv_bfloat16* embed, long lde, const int32_t* ids, const int32_t* sel,
                                     int n, int D, float* out, long ldo) {
+  pdl_entry();
   const int r = blockIdx.x;
   if (r >= n) return;
   const int tok = sel ? ids[sel[r]] : ids[r];
@@ -819,7 +833,7 @@ __global__ void embed_gather_kernel(const __nv_bfloat16* embed, long lde, const 
 int embed_gather_launch(const void* embed, long lde, const int32_t* ids, const int32_t* sel, int n, int D, float* out,
                         long ldo, cudaStream_t st) {
   if (n <= 0) return PKV_OK;
-  embed_gather_kernel<<<n, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(embed), lde, ids, sel, n, D, out, ldo);
+  launch_k(embed_gather_kernel, n, 256, 0, st, reinterpret_cast<const __nv_bfloat16*>(embed), lde, ids, sel, n, D, out, ldo);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("embed_gather_kernel");
   return PKV_OK;

@@ -11,6 +11,7 @@ stages.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -46,6 +47,16 @@ class PrefillPipeline:
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
         self.logits = torch.empty(cfg.vocab_size, dtype=torch.float32, device=dev)
         self.query = torch.zeros(m, dtype=torch.int32, device=dev)
+        # layer-pipelined assembly: layer l is assembled on a side stream and the scoring
+        # pass (and Stage II's scatter) wait on layer_ready[l] (include/pkv.h), so the
+        # HBM-bound assembly of layers l+1.. overlaps the narrow pass over layer l
+        self.side = torch.cuda.Stream(device=dev)
+        # per-layer assembly on the side stream overlapping the scoring pass: measured
+        # neutral for device-resident chunks (both phases compete for HBM), so opt-in
+        self.pipelined_assembly = os.environ.get("PKV_ASM_PIPE", "0") == "1"
+        self.layer_events = [torch.cuda.Event() for _ in range(cfg.n_layers)]
+        self.cache.layer_events = self.layer_events
+        self.cache._c_cache = self.cache._make_c_cache()
 
     def set_query(self, ids) -> None:
         torch = _lib.require_cuda()
@@ -95,7 +106,16 @@ class PrefillPipeline:
         st = _lib.stream_ptr(torch, stream)
         c = self.cache
         cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
-        _lib.check(lib.pkv_assemble(ctypes_ref(c._cfg_c), ch, cc, st))
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self.side.wait_stream(main)
+        if self.pipelined_assembly:
+            for li in range(self.cfg.n_layers):
+                _lib.check(lib.pkv_assemble_layers(ctypes_ref(c._cfg_c), ch, cc, li, li + 1, self.side.cuda_stream))
+                self.layer_events[li].record(self.side)
+        else:
+            _lib.check(lib.pkv_assemble(ctypes_ref(c._cfg_c), ch, cc, self.side.cuda_stream))
+            for ev in self.layer_events:
+                ev.record(self.side)
         _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_score,
                                       self.per_layer.data_ptr(), None, None, None, self.ws_qp.data_ptr(),
                                       self.ws_qp.numel(), st))
@@ -106,6 +126,7 @@ class PrefillPipeline:
         _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_final, None,
                                       None, None, self.logits.data_ptr(), self.ws_qp.data_ptr(), self.ws_qp.numel(),
                                       st))
+        main.wait_stream(self.side)  # rejoin (required for graph capture)
 
 
 def random_device_chunks(cfg, n_chunks: int, chunk_len: int, seed: int = 0, fingerprint: str = "device-random"):
