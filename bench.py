@@ -41,8 +41,13 @@ CONFIGS = {
     # configs[1]: Mistral-7B shape, 8k context of 8 chunks
     "mistral-7b-8k": dict(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, hidden_dim=4096, ffn_dim=14336,
                           vocab_size=32000, rope_theta=1000000.0, n_chunks=8, chunk_len=1024),
+    # configs[4]: Llama-3-8B shape, 128k context of 64 chunks, one request per GPU (--mode requests)
+    "llama3-8b-128k": dict(n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, hidden_dim=4096, ffn_dim=14336,
+                           vocab_size=128256, rope_theta=500000.0, n_chunks=64, chunk_len=2048),
 }
-METRIC = "effective prefill tok/s @32k ctx, 20% recompute (TTFT = s / value)"
+def metric_name(cfgd: dict, p: float) -> str:
+    s = cfgd["n_chunks"] * cfgd["chunk_len"]
+    return f"effective prefill tok/s @{s // 1024}k ctx, {p * 100:g}% recompute (TTFT = s / value)"
 
 
 def _peaks():
@@ -175,7 +180,7 @@ def run_reference(args, cfgd, rank, world):
     ttft = float(np.mean(times))
     value = s / ttft
     cores = cpu_cores()
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world,
+    line = {"impl": "reference", "metric": metric_name(cfgd, args.p), "value": value, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft * 1e3, "ttft_ms": ttft * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
             "data": "synthetic", "config": {"workload": args.config, "s": s, "m": 32, "p": args.p, "k": k,
@@ -202,6 +207,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=128)
     ap.add_argument("--mode", default="auto", choices=["auto", "heads", "requests"])
+    ap.add_argument("--p-sweep", default="0.05,0.1,0.2,0.4", help="recompute ratios of the sweep ('' = skip)")
+    ap.add_argument("--sweep-steps", type=int, default=3)
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -346,12 +353,12 @@ def main():
     dominant = max((n for n in rooflines), key=lambda n: phases[n][0])
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get(dominant)
+    if tfile.exists():  # ncu --set full capture of this workload's dominant kernel (per launch)
+        traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dominant) if not heads else None
     roof = dict(rooflines[dominant], kernel=dominant, traffic=traffic,
                 peak_kind=f"{peak_kind} ({'sustained bf16' if rooflines[dominant]['bound'] == 'tensor' else 'HBM copy'})")
 
-    line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+    line = {"metric": metric_name(cfgd, args.p), "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16 (Stage II) / fp32-faithful (narrow passes)",
@@ -379,12 +386,42 @@ def main():
         torch.cuda.synchronize()
         full_ms = f0.elapsed_time(f1) / args.full_steps
         H, dk = cfg.n_heads, cfg.head_dim
-        full_tf = 2.0 * s * dm.weight_bytes(include_head=False) / 2 + 4.0 * L * H * dk * s * (s + 1) / 2
+        full_tf = 2.0 * s * dm.weight_bytes(include_head=False) * dm.tp_world / 2 + 4.0 * L * H * dk * s * (s + 1) / 2
         line["full_prefill"] = {"ttft_ms": full_ms, "tok_per_s": s / (full_ms / 1e3),
                                 "ttft_ratio_full_over_prophet": full_ms / ms,
                                 "tflops": full_tf / (full_ms / 1e3) / 1e12,
                                 "what": "Stage II with all s context tokens selected (no chunk reuse) + finalize, "
                                         "eager launches"}
+
+    # ---- BASELINE configs[3]: recompute-ratio sweep at the same context (graph-replayed)
+    if args.p_sweep:
+        sweep = {}
+        for pp in [float(x) for x in args.p_sweep.split(",") if x.strip()]:
+            if abs(pp - args.p) < 1e-12:
+                sweep[f"{pp:g}"] = {"k": k, "ttft_ms": ms, "tok_per_s": s / (ms / 1e3)}
+            else:
+                sp_pipe = PrefillPipeline(dm, chunks, args.m, pp)
+                sp_pipe.set_query(query)
+                sp_pipe.step()
+                sp_pipe.capture()
+                sp_pipe.replay()
+                torch.cuda.synchronize()
+                if world > 1:
+                    dist.barrier()
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                for _ in range(args.sweep_steps):
+                    sp_pipe.replay()
+                g1.record(stream)
+                torch.cuda.synchronize()
+                t_ms = pdist.max_over_ranks(g0.elapsed_time(g1) / args.sweep_steps, device="cuda")
+                sweep[f"{pp:g}"] = {"k": sp_pipe.k, "ttft_ms": t_ms, "tok_per_s": s / (t_ms / 1e3)}
+                del sp_pipe
+                torch.cuda.empty_cache()
+            if "full_prefill" in line:
+                sweep[f"{pp:g}"]["ttft_ratio_full_over_prophet"] = line["full_prefill"]["ttft_ms"] / \
+                    sweep[f"{pp:g}"]["ttft_ms"]
+        line["p_sweep"] = sweep
 
     # ---- e2e through the public API with host (pinned) inputs
     if args.e2e_steps > 0:

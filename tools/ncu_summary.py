@@ -52,7 +52,17 @@ if __name__ == "__main__":
         res[phase] = summarize(rep)
     os.makedirs(dst, exist_ok=True)
     json.dump(res, open(os.path.join(dst, "ncu_summary.json"), "w"), indent=1)
-    json.dump({k: v["traffic_bytes"] for k, v in res.items()}, open("profiles/ncu_traffic.json", "w"), indent=1)
+    # per-launch DRAM traffic of the captured kernels (tools/profile_step.py runs the
+    # llama3-8b-32k workload), merged into the file bench.py reads
+    tpath = "profiles/ncu_traffic.json"
+    try:
+        allt = json.load(open(tpath))
+    except (OSError, ValueError):
+        allt = {}
+    if not all(isinstance(v, dict) for v in allt.values()):
+        allt = {}
+    allt.setdefault("llama3-8b-32k", {}).update({k: v["traffic_bytes"] for k, v in res.items()})
+    json.dump(allt, open(tpath, "w"), indent=1)
     for k, v in res.items():
         print(f"{k:12s} {v['duration'] * 1e6:9.1f} us  traffic {v['traffic_bytes'] / 1e6:9.1f} MB  "
               f"dram {v.get('dram_pct_of_peak', 0):5.1f}%  tensor {v.get('tensor_pipe_pct', 0):5.1f}%  grid {v.get('grid')}")
