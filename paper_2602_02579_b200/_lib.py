@@ -73,6 +73,7 @@ _SIGS = {
     "pkv_replace_entries": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pkv_cache_view": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), ctypes.POINTER(Chunks), c_i32, c_i32, c_vp, c_vp]),
     "pkv_gemm_bf16": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),
+    "pkv_proj_narrow": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "pkv_attention_sparse": (c_i32, [c_vp, ctypes.POINTER(Cache), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
     "pkv_timing_enable": (c_i32, [c_i32]),
     "pkv_timing_collect": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i32), c_i32]),

@@ -167,11 +167,11 @@ struct ProjWs {
 static int choose_splits(int N, int K) {
   const char* env = getenv("PKV_PROJ_SPLITS");  // tuning override
   const int forced = env ? atoi(env) : 0;
-  const int m_tiles = ceil_div(N, 128), k_tiles = ceil_div(K, 64);
+  const int m_tiles = ceil_div(N, 128 * gemm_mt(96, EPI_PROJ)), k_tiles = ceil_div(K, gemm_bk(96));
   if (forced > 0) return std::min(std::min(forced, 16), k_tiles);
   int best = 1;
   double best_cost = 1e30;
-  for (int sp = 1; sp <= 16 && k_tiles / sp >= 4; ++sp) {
+  for (int sp = 1; sp <= 16 && k_tiles / sp >= 2; ++sp) {
     const int per = ceil_div(k_tiles, sp);
     const int nsp = ceil_div(k_tiles, per);
     const int rounds = ceil_div((long)m_tiles * nsp, num_sms());
@@ -194,12 +194,12 @@ static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, i
     g.N = 96;
     const int sp = choose_splits(N, K);
     g.n_splits = sp;
-    g.k_tiles_per_split = ceil_div(ceil_div(K, 64), sp);
+    g.k_tiles_per_split = 0;  // gemm_tc_launch splits the k range evenly
     g.C = ws.part;
     g.ldc = 96;
-    const int nsp = ceil_div(ceil_div(K, 64), g.k_tiles_per_split);
     rc = gemm_tc_launch(EPI_F32, 96, W, K, ws.x3, ws.ldx, K, g, st);
     if (rc) return rc;
+    const int ktt = ceil_div(K, gemm_bk(96)), nsp = ceil_div(ktt, ceil_div(ktt, sp));  // as gemm_tc_launch
     rc = splitk_reduce_launch(ws.part, nsp, N, rows, out + (long)r0 * ldo, ldo, mode, st);
     if (rc) return rc;
   }
@@ -215,7 +215,7 @@ static int proj_fused(const void* W, int N, int K, int m, float* out, long ldo, 
   g.N = 96;
   const int sp = choose_splits(N, K);
   g.n_splits = sp;
-  g.k_tiles_per_split = ceil_div(ceil_div(K, 64), sp);
+  g.k_tiles_per_split = 0;  // gemm_tc_launch splits the k range evenly
   g.out = out;
   g.ldo = ldo;
   g.mrows = m;
@@ -710,6 +710,25 @@ int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_
   g.ldc = ldc;
   if (epi != EPI_F32 && epi != EPI_RESID && epi != EPI_BF16) return set_error(PKV_ERR_ARGUMENT, "epilogue");
   return gemm_tc_launch(epi, bn, A, lda, B, ldb, K, g, S(stream));
+}
+
+int pkv_proj_narrow(const void* W, int32_t N, int32_t K, const void* x3, int64_t ldx, int32_t m, float* out,
+                    int64_t ldo, int32_t resid, float* part, int32_t* cnt, int32_t n_splits, void* stream) {
+  if (m <= 0 || m > 32) return set_error(PKV_ERR_ARGUMENT, "narrow projection takes 1..32 rows");
+  if (K % 64 != 0 || ldx < K) return set_error(PKV_ERR_SHAPE, "narrow projection: K must be a multiple of 64");
+  GemmArgs g{};
+  g.M = N;
+  g.N = 96;
+  const int sp = n_splits > 0 ? std::min(n_splits, 16) : choose_splits(N, K);
+  g.n_splits = sp;
+  g.k_tiles_per_split = 0;  // gemm_tc_launch splits the k range evenly
+  g.out = out;
+  g.ldo = ldo;
+  g.mrows = m;
+  g.resid = resid;
+  g.part = part;
+  g.cnt = cnt;
+  return gemm_tc_launch(EPI_PROJ, 96, W, K, x3, ldx, K, g, S(stream));
 }
 
 int pkv_attention_sparse(const pkv_model* md, const pkv_cache* c, int32_t layer, const void* q, void* out,

@@ -77,14 +77,14 @@ bool cached_tmap(CUtensorMap* out, const void* base, long rows, long cols, long 
 
 template <int BN, int EPI>
 static int launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
     attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (attr_err != cudaSuccess) return set_error(PKV_ERR_CUDA, "gemm smem attr: %s", cudaGetErrorString(attr_err));
-  long tiles = (long)ceil_div(args.M, Cfg::BM) * ceil_div(args.N, BN) * args.n_splits;
+  long tiles = (long)ceil_div(args.M, Cfg::BMT) * ceil_div(args.N, BN) * args.n_splits;
   int grid = (int)std::min<long>(tiles, num_sms());
   if (grid <= 0) return PKV_OK;
   launch_k(gemm_tc_kernel<BN, EPI>, grid, 192, Cfg::SMEM, stream, ta, tb, args);
@@ -101,7 +101,7 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   if ((lda * 2) % 16 != 0 || (ldb * 2) % 16 != 0)
     return set_error(PKV_ERR_SHAPE, "gemm: row strides must be multiples of 8 elements");
   args.K = K;
-  int kt = ceil_div(K, 64);
+  int kt = ceil_div(K, gemm_bk(bn));
   if (args.n_splits <= 0) args.n_splits = 1;
   if (args.k_tiles_per_split <= 0) args.k_tiles_per_split = ceil_div(kt, args.n_splits);
   args.n_splits = ceil_div(kt, args.k_tiles_per_split);  // no empty splits

@@ -54,24 +54,46 @@ struct GemmArgs {
   int* cnt;                   // [tiles_m] arrival counters (zero; reset by the reducing CTA)
 };
 
-template <int BN>
+// BK = k extent of one pipeline stage (SW128 atoms of 64 bf16); MT = 128-row sub-tiles of
+// A per CTA tile sharing each B tile (EPI_PROJ only).  Measured on the narrow-pass
+// projections (tools/bench_proj.py, graph-captured): BK = 128 and MT = 2 were both slower
+// or neutral (per-SM smem fill, not the barrier round trip or the B traffic, bounds them),
+// so both stay at 1 atom / 1 sub-tile; the knobs are kept for re-tuning.
+constexpr int gemm_bk(int bn) { return 64; }
+constexpr int gemm_mt(int bn, int epi) { return 1; }
+template <int BN, int EPI>
 struct GemmCfg {
-  static constexpr int BM = 128, BK = 64;
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int BM = 128, BK = gemm_bk(BN), MT = gemm_mt(BN, EPI), BMT = BM * MT;
+  static constexpr int ATOMS = BK / 64;
+  static constexpr int A_ATOM = BM * 128, B_ATOM = BN * 128;  // bytes of one 64-column atom
+  static constexpr int A_SUB = BM * BK * 2;                    // one 128-row sub-tile
+  static constexpr int A_BYTES = MT * A_SUB;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : 7);
-  static constexpr int ACC_STRIDE = BN <= 128 ? 128 : 256;
+  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : (MT == 2 ? 5 : 7));
+  static_assert(MT == 1 || EPI == EPI_PROJ, "sub-tiled A only for the narrow projection epilogue");
+  static constexpr int ACC_STRIDE = MT * (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
 
+// Narrow-pass projections (EPI_PROJ): every M tile streams its own weights but all of
+// them read the SAME activation tile at a given k, so in lock-step the whole grid hits
+// the few L2 slices holding that tile.  Each M tile therefore walks its k range from a
+// different starting point (fixed per tile: deterministic fp32 order).
+template <int EPI>
+__device__ __forceinline__ int k_rotation_t(int mb, int nk) {
+  if constexpr (EPI == EPI_PROJ) return nk > 0 ? (mb * 5) % nk : 0;
+  return 0;
+}
+#define k_rotation(mb, nk) k_rotation_t<EPI>(mb, nk)
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -83,7 +105,8 @@ __global__ void __launch_bounds__(192, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  const int tiles_m = (args.M + Cfg::BM - 1) / Cfg::BM;
+  const int tiles_m = (args.M + Cfg::BMT - 1) / Cfg::BMT;
+  const int subtiles_m = (args.M + Cfg::BM - 1) / Cfg::BM;  // EPI_PROJ partial / counter index space
   const int tiles_n = (args.N + BN - 1) / BN;
   const int total_tiles = tiles_m * tiles_n * args.n_splits;
   const int k_tiles_total = (args.K + Cfg::BK - 1) / Cfg::BK;
@@ -126,13 +149,21 @@ __global__ void __launch_bounds__(192, 1)
         tile_coords(t, mb, nb, sp);
         int k0 = sp * args.k_tiles_per_split;
         int k1 = min(k0 + args.k_tiles_per_split, k_tiles_total);
-        for (int kt = k0; kt < k1; ++kt) {
+        const int nk = k1 - k0, rot = k_rotation(mb, nk);
+        for (int i = 0; i < nk; ++i) {
+          const int kt = k0 + (i + rot) % nk;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
           mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full_bar[stage], kt * Cfg::BK, mb * Cfg::BM);
-          tma_load_2d(sb, &tmB, &full_bar[stage], kt * Cfg::BK, nb * BN);
+#pragma unroll
+          for (int at = 0; at < Cfg::ATOMS; ++at) {
+#pragma unroll
+            for (int j = 0; j < Cfg::MT; ++j)
+              tma_load_2d(sa + j * Cfg::A_SUB + at * Cfg::A_ATOM, &tmA, &full_bar[stage], kt * Cfg::BK + at * 64,
+                          mb * Cfg::BMT + j * Cfg::BM);
+            tma_load_2d(sb + at * Cfg::B_ATOM, &tmB, &full_bar[stage], kt * Cfg::BK + at * 64, nb * BN);
+          }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -152,7 +183,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_STRIDE;
-      for (int kt = k0; kt < k1; ++kt) {
+      const int nk = k1 - k0;
+      for (int i = 0; i < nk; ++i) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -160,9 +192,12 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t b_addr = a_addr + Cfg::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < Cfg::BK / 16; ++kk) {
-            uint64_t ad = sdesc_sw128(a_addr + kk * 32, 16, 1024);
-            uint64_t bd = sdesc_sw128(b_addr + kk * 32, 16, 1024);
-            umma_bf16(d_tmem, ad, bd, idesc, (kt > k0 || kk > 0) ? 1u : 0u);
+            uint64_t bd = sdesc_sw128(b_addr + (kk >> 2) * Cfg::B_ATOM + (kk & 3) * 32, 16, 1024);
+#pragma unroll
+            for (int j = 0; j < Cfg::MT; ++j) {
+              uint64_t ad = sdesc_sw128(a_addr + j * Cfg::A_SUB + (kk >> 2) * Cfg::A_ATOM + (kk & 3) * 32, 16, 1024);
+              umma_bf16(d_tmem + j * (Cfg::ACC_STRIDE / Cfg::MT), ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty_bar[stage]);
         }
@@ -189,35 +224,39 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * Cfg::ACC_STRIDE;
 
       if constexpr (EPI == EPI_PROJ) {
+       __shared__ int s_last;
+#pragma unroll 1
+       for (int j = 0; j < Cfg::MT; ++j) {
         // one thread = one output feature n; the 96 accumulator columns are the hi/mid/lo
         // planes of the 32 query rows
-        __shared__ int s_last;
+        const int msub = mb * Cfg::MT + j;  // 128-row sub-tile
         uint32_t a0[32], a1[32], a2[32];
         __syncwarp();
-        tmem_ld32(t_row, a0);
-        tmem_ld32(t_row + 32, a1);
-        tmem_ld32(t_row + 64, a2);
+        const uint32_t t_sub = t_row + j * (Cfg::ACC_STRIDE / Cfg::MT);
+        tmem_ld32(t_sub, a0);
+        tmem_ld32(t_sub + 32, a1);
+        tmem_ld32(t_sub + 64, a2);
         tmem_ld_wait();
         float y[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           y[i] = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
-        const int n = row;  // GEMM row == output feature
+        const int n = msub * Cfg::BM + row_in_tile;  // GEMM row == output feature
         bool write = args.n_splits == 1;
         if (!write) {
-          float* mine = args.part + ((long)(sp * tiles_m + mb) * 128 + row_in_tile) * 32;
+          float* mine = args.part + ((long)(sp * subtiles_m + msub) * 128 + row_in_tile) * 32;
 #pragma unroll
           for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(mine + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
           __threadfence();
           named_bar_sync(1, 128);
-          if (threadIdx.x == 64) s_last = (atomicAdd(&args.cnt[mb], 1) == args.n_splits - 1) ? 1 : 0;
+          if (threadIdx.x == 64) s_last = (atomicAdd(&args.cnt[msub], 1) == args.n_splits - 1) ? 1 : 0;
           named_bar_sync(1, 128);
           if (s_last) {
             __threadfence();
             // fixed split order -> bit-identical regardless of which CTA arrives last
 #pragma unroll 1
             for (int s2 = 0; s2 < args.n_splits; ++s2) {
-              const float* p = args.part + ((long)(s2 * tiles_m + mb) * 128 + row_in_tile) * 32;
+              const float* p = args.part + ((long)(s2 * subtiles_m + msub) * 128 + row_in_tile) * 32;
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
                 const float4 v = __ldcg(reinterpret_cast<const float4*>(p + i));
@@ -228,16 +267,20 @@ __global__ void __launch_bounds__(192, 1)
                 }
               }
             }
-            if (threadIdx.x == 64) args.cnt[mb] = 0;
+            if (threadIdx.x == 64) args.cnt[msub] = 0;
             write = true;
           }
         }
         if (write && n < args.M) {
-          for (int i = 0; i < args.mrows; ++i) {
-            float* dst = args.out + (long)i * args.ldo + n;
-            *dst = args.resid ? *dst + y[i] : y[i];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {  // constant indices keep y in registers
+            if (i < args.mrows) {
+              float* dst = args.out + (long)i * args.ldo + n;
+              *dst = args.resid ? *dst + y[i] : y[i];
+            }
           }
         }
+       }
       } else if constexpr (EPI == EPI_SILU) {
         // gate columns [0,BN/2), up columns [BN/2,BN) of this tile feed BN/2 outputs
 #pragma unroll 1
