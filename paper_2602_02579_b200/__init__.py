@@ -7,6 +7,7 @@ exchange.  Everything runs on hand-written sm_100a kernels behind the C ABI in
 ``include/pkv.h``; there is no CPU fallback.
 """
 
+from .chunkfile import load_chunk, load_chunk_pinned, store_chunk
 from .chunkstore import AssembledCache, ChunkKV, assemble, chunk_content_id, mark_finalized, replace_entries
 from .errors import (ArgumentError, ConfigError, EngineError, FormatError, IncompatibleError, InputError,
                      NumericsError, ShapeError, StateError, TruncatedError)

@@ -786,32 +786,55 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
 
 // ------------------------------------------------------------------ lm_head
 // logits[n] = dot(x, W[n]) over D, fp32 accumulation (x = final-normed last row)
-__global__ void gemv_rows_kernel(const float* x, const __nv_bfloat16* W, int N, int D, long ldw, float* out) {
+// 4 output rows per warp pass (16-byte loads of 4 rows in flight per lane, independent
+// accumulators); x (fp32, final-normed) staged in shared memory
+__global__ void __launch_bounds__(256) gemv_rows_kernel(const float* x, const __nv_bfloat16* __restrict__ W, int N,
+                                                        int D, long ldw, float* out) {
   pdl_entry();
   extern __shared__ float xs[];
   for (int c = threadIdx.x; c < D; c += blockDim.x) xs[c] = x[c];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
-  for (int n = blockIdx.x * wpb + warp; n < N; n += gridDim.x * wpb) {
-    const __nv_bfloat16* w = W + (long)n * ldw;
-    float acc = 0.f;
-    for (int c = lane * 8; c < D; c += 256) {
-      const uint4 u = *reinterpret_cast<const uint4*>(w + c);
-      const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+  const bool vec = (D % 8 == 0) && (ldw % 8 == 0);
+  for (int n0 = (blockIdx.x * wpb + warp) * 4; n0 < N; n0 += gridDim.x * wpb * 4) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    if (vec) {
+#pragma unroll 2
+      for (int c = lane * 8; c < D; c += 256) {
+        uint4 u[4];
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        if (c + 2 * p < D) acc = fmaf(xs[c + 2 * p], bf16_lo(uw[p]), acc);
-        if (c + 2 * p + 1 < D) acc = fmaf(xs[c + 2 * p + 1], bf16_hi(uw[p]), acc);
+        for (int r = 0; r < 4; ++r)
+          u[r] = n0 + r < N ? __ldg(reinterpret_cast<const uint4*>(W + (long)(n0 + r) * ldw + c)) : make_uint4(0, 0, 0, 0);
+        const float4 xa = *reinterpret_cast<const float4*>(xs + c);
+        const float4 xb = *reinterpret_cast<const float4*>(xs + c + 4);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          acc[r] = fmaf(xa.x, bf16_lo(u[r].x), acc[r]);
+          acc[r] = fmaf(xa.y, bf16_hi(u[r].x), acc[r]);
+          acc[r] = fmaf(xa.z, bf16_lo(u[r].y), acc[r]);
+          acc[r] = fmaf(xa.w, bf16_hi(u[r].y), acc[r]);
+          acc[r] = fmaf(xb.x, bf16_lo(u[r].z), acc[r]);
+          acc[r] = fmaf(xb.y, bf16_hi(u[r].z), acc[r]);
+          acc[r] = fmaf(xb.z, bf16_lo(u[r].w), acc[r]);
+          acc[r] = fmaf(xb.w, bf16_hi(u[r].w), acc[r]);
+        }
       }
+    } else {
+      for (int r = 0; r < 4 && n0 + r < N; ++r)
+        for (int c = lane; c < D; c += 32) acc[r] = fmaf(xs[c], __bfloat162float(W[(long)(n0 + r) * ldw + c]), acc[r]);
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out[n] = acc;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      float v = acc[r];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && n0 + r < N) out[n0 + r] = v;
+    }
   }
 }
 
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st) {
-  const int blocks = std::min(ceil_div(N, 8), num_sms() * 8);
+  const int blocks = std::min(ceil_div(N, 32), num_sms() * 8);
   launch_k(gemv_rows_kernel, blocks, 256, D * sizeof(float), st, x, reinterpret_cast<const __nv_bfloat16*>(W), N, D, ldw,
                                                            out);
   PKV_LAUNCHED();

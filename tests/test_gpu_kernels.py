@@ -171,3 +171,30 @@ def test_fuse_layers_bit_exact(built):
     rng = np.random.default_rng(3)
     per = rng.random((32, 4096)).astype(np.float32) * 1e-3
     assert np.array_equal(P.fuse_layers(per), O.layer_mean(per))
+
+
+@pytest.mark.parametrize("N,K,m,splits,resid", [(4096, 4096, 32, 0, 0), (384, 1024, 7, 3, 1), (6144, 4096, 32, 1, 0)])
+def test_narrow_projection_is_fp32_faithful(built, N, K, m, splits, resid):
+    """EPI_PROJ: out (+)= x . W^T for <= 32 fp32 rows given as 3 exact bf16 planes."""
+    torch = _torch()
+    P = built
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    W = torch.randn((N, K), generator=g, device="cuda").to(torch.bfloat16)
+    x = torch.randn((m, K), generator=g, device="cuda")
+    hi = x.to(torch.bfloat16)
+    mid = (x - hi.float()).to(torch.bfloat16)
+    lo = (x - hi.float() - mid.float()).to(torch.bfloat16)
+    x3 = torch.zeros((96, K), dtype=torch.bfloat16, device="cuda")
+    x3[:m], x3[32:32 + m], x3[64:64 + m] = hi, mid, lo
+    out = torch.randn((m, N), generator=g, device="cuda")
+    base = out.clone()
+    part = torch.empty(16 * ((N + 127) // 128) * 128 * 32, device="cuda")
+    cnt = torch.zeros((N + 127) // 128, dtype=torch.int32, device="cuda")
+    P._lib.check(P._lib.load().pkv_proj_narrow(W.data_ptr(), N, K, x3.data_ptr(), K, m, out.data_ptr(), N, resid,
+                                                part.data_ptr(), cnt.data_ptr(), splits,
+                                                torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    want = x.double() @ W.double().t() + (base.double() if resid else 0)
+    err = ((out.double() - want).abs().max() / want.abs().max()).item()
+    assert err < 1e-5, err
+    assert int(cnt.sum().item()) == 0  # split counters are reset for the next launch
