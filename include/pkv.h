@@ -164,6 +164,15 @@ size_t pkv_recompute_workspace(const pkv_model* m, int32_t k);
 int pkv_recompute(const pkv_model* m, const pkv_cache* cache, const int32_t* sel, int32_t k, float* tap_k,
                   float* tap_v, void* workspace, size_t workspace_bytes, void* stream);
 
+/* full_prefill -- model.py:332-359 (and precompute_chunk, chunkstore.py:52-62) on the
+ * device: the Stage-II layer loop over every position 0..s-1 of `cache` (its token_ids
+ * are the sequence; K/V land in its pool, RoPE'd at 0..s-1).  Optional captures:
+ * k_nr_out / v_out bf16 [L][s][Hkv][dkp] (the chunk-store layout; keys BEFORE RoPE),
+ * logits_out f32 [s][vocab] (final norm + lm_head on the bf16 tensor cores). */
+size_t pkv_full_prefill_workspace(const pkv_model* m, int32_t n);
+int pkv_full_prefill(const pkv_model* m, const pkv_cache* cache, void* k_nr_out, void* v_out, float* logits_out,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
 /* replace_entries -- chunkstore.py:143-160 (standalone scatter of fp32 rows) */
 int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* cache, int32_t layer, const int32_t* idx, int32_t n,
                         const float* new_k, const float* new_v, void* stream);

@@ -70,6 +70,8 @@ _SIGS = {
     "pkv_topk": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "pkv_recompute_workspace": (c_sz, [c_vp, c_i32]),
     "pkv_recompute": (c_i32, [c_vp, ctypes.POINTER(Cache), c_vp, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "pkv_full_prefill_workspace": (c_sz, [c_vp, c_i32]),
+    "pkv_full_prefill": (c_i32, [c_vp, ctypes.POINTER(Cache), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pkv_replace_entries": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pkv_cache_view": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), ctypes.POINTER(Chunks), c_i32, c_i32, c_vp, c_vp]),
     "pkv_gemm_bf16": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),

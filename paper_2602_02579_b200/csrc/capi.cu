@@ -619,14 +619,10 @@ size_t pkv_recompute_workspace(const pkv_model* m, int32_t k) {
   return t;
 }
 
-int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k, float* tap_v,
-                  void* workspace, size_t ws_bytes, void* stream) {
-  if (k == 0) return PKV_OK;
-  if (k < 0 || k > c->s) return set_error(PKV_ERR_ARGUMENT, "bad selection size %d", k);
-  size_t need = 0;
-  RcWs w = carve_rc(md, k, workspace, &need);
-  if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
-  cudaStream_t st = S(stream);
+// the Stage-II layer loop over the k rows `sel` (recompute_selected, and with sel = all
+// positions full_prefill / precompute_chunk); leaves the final residual stream in w.h
+static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k,
+                          float* tap_v, void* knr_out, void* v_out, const RcWs& w, cudaStream_t st) {
   const pkv_config& cf = md->cfg;
   const int H = md->H, Hkv = md->Hkv, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
   // row-parallel o / down GEMMs under tensor parallelism: rank 0 accumulates into the
@@ -663,6 +659,8 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     g.page_table = c->page_table;
     g.tap_k = tap_k ? tap_k + (long)l * k * Hkv * dk : nullptr;
     g.tap_v = tap_v ? tap_v + (long)l * k * Hkv * dk : nullptr;
+    g.knr_out = knr_out ? reinterpret_cast<__nv_bfloat16*>(knr_out) + (long)l * k * Hkv * dkp : nullptr;
+    g.vcap_out = v_out ? reinterpret_cast<__nv_bfloat16*>(v_out) + (long)l * k * Hkv * dkp : nullptr;
     if (c->k2_pool != nullptr && c->k3_pool != nullptr) {
       g.k2_pool = reinterpret_cast<__nv_bfloat16*>(c->k2_pool) + l * layer_pool;
       g.k3_pool = reinterpret_cast<__nv_bfloat16*>(c->k3_pool) + l * layer_pool;
@@ -695,6 +693,76 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
     gd.ldc = Dp;
     TTRY(T_RC_DOWN, gemm_tc_launch(epi_resid, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
     if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
+  }
+  return PKV_OK;
+}
+
+int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k, float* tap_v,
+                  void* workspace, size_t ws_bytes, void* stream) {
+  if (k == 0) return PKV_OK;
+  if (k < 0 || k > c->s) return set_error(PKV_ERR_ARGUMENT, "bad selection size %d", k);
+  size_t need = 0;
+  RcWs w = carve_rc(md, k, workspace, &need);
+  if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
+  return recompute_core(md, c, sel, k, tap_k, tap_v, nullptr, nullptr, w, S(stream));
+}
+
+// ------------------------------------------------------------------ full prefill
+__global__ void iota_kernel(int32_t* v, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+static size_t full_ws(const pkv_model* md, int n, RcWs* w, int32_t** sel, __nv_bfloat16** xl, void* base) {
+  size_t rc_bytes = 0;
+  carve_rc(md, n, nullptr, &rc_bytes);
+  Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
+  uint8_t* rc_base = cv.take<uint8_t>(rc_bytes);
+  *sel = cv.take<int32_t>((size_t)n);
+  *xl = cv.take<__nv_bfloat16>((size_t)n * md->Dp);
+  if (base) {
+    size_t t = 0;
+    *w = carve_rc(md, n, rc_base, &t);
+  }
+  return cv.off + 256;
+}
+
+size_t pkv_full_prefill_workspace(const pkv_model* m, int32_t n) {
+  RcWs w{};
+  int32_t* sel;
+  __nv_bfloat16* xl;
+  return full_ws(m, n, &w, &sel, &xl, nullptr);
+}
+
+int pkv_full_prefill(const pkv_model* md, const pkv_cache* c, void* k_nr_out, void* v_out, float* logits_out,
+                     void* workspace, size_t ws_bytes, void* stream) {
+  if (!md || !c) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  const int n = c->s;
+  if (n <= 0) return set_error(PKV_ERR_INPUT, "token sequence must be non-empty");
+  if (c->rope_len < n || c->pool_tokens < n) return set_error(PKV_ERR_SHAPE, "cache too small for the sequence");
+  RcWs w{};
+  int32_t* sel;
+  __nv_bfloat16* xl;
+  if (ws_bytes < full_ws(md, n, &w, &sel, &xl, nullptr))
+    return set_error(PKV_ERR_ARGUMENT, "workspace too small");
+  full_ws(md, n, &w, &sel, &xl, workspace);
+  cudaStream_t st = S(stream);
+  iota_kernel<<<ceil_div(n, 256), 256, 0, st>>>(sel, n);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("iota_kernel");
+  int rc = recompute_core(md, c, sel, n, nullptr, nullptr, k_nr_out, v_out, w, st);
+  if (rc) return rc;
+  if (logits_out) {  // _head_logits (model.py:326-329) for every row: final norm, then lm_head
+    const pkv_config& cf = md->cfg;
+    TTRY(T_LMHEAD, rmsnorm_launch(w.h, n, cf.hidden_dim, md->Dp, md->w.final_norm, cf.norm_eps, nullptr, nullptr, 0,
+                                  xl, st));
+    GemmArgs g{};
+    g.M = n;
+    g.N = cf.vocab_size;
+    g.n_splits = 1;
+    g.C = logits_out;
+    g.ldc = cf.vocab_size;
+    TTRY(T_LMHEAD, gemm_tc_launch(EPI_F32, 256, xl, md->Dp, md->w.lm_head, md->Dp, md->Dp, g, st));
   }
   return PKV_OK;
 }

@@ -45,6 +45,8 @@ struct GemmArgs {
   float* tap_v;
   __nv_bfloat16* k2_pool;     // optional residual key planes (layer base), see s1_attn_tc.cu
   __nv_bfloat16* k3_pool;
+  __nv_bfloat16* knr_out;     // optional bf16 [M][Hkv][dkp]: keys BEFORE RoPE (chunk-store layout)
+  __nv_bfloat16* vcap_out;    // optional bf16 [M][Hkv][dkp]: values (chunk-store layout)
   // EPI_PROJ ---------------------------------------------------------------
   float* out;                 // [mrows][ldo]
   long ldo;
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld_wait();
           const int col0 = nb * BN + c * 32;
           if (!row_ok || col0 >= args.N) continue;
-          const bool full = col0 + 32 <= args.N;
+          const bool full = col0 + 32 <= args.N && (args.ldc & 7) == 0;  // vector stores need aligned rows
           if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
             float* dst = reinterpret_cast<float*>(args.C) + (long)sp * args.M * args.ldc + (long)row * args.ldc + col0;
             if (full) {
@@ -359,6 +361,18 @@ __global__ void __launch_bounds__(192, 1)
             float vals[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]);
+            if (head_all >= H) {  // precompute_chunk captures: unrotated keys / values
+              __nv_bfloat16* cap = is_v ? args.vcap_out : args.knr_out;
+              if (cap != nullptr) {
+                const int gk = is_v ? head_all - H - Hkv : head_all - H;
+                uint4* cd = reinterpret_cast<uint4*>(cap + ((long)row * Hkv + gk) * dkp + d0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  cd[j] = make_uint4(pack_bf16(vals[8 * j], vals[8 * j + 1]), pack_bf16(vals[8 * j + 2], vals[8 * j + 3]),
+                                     pack_bf16(vals[8 * j + 4], vals[8 * j + 5]),
+                                     pack_bf16(vals[8 * j + 6], vals[8 * j + 7]));
+              }
+            }
             if (!is_v && args.rope_cs32 != nullptr) {
               // interleaved-pair RoPE (reference tensor.py:104-113) in fp32 with the float64
               // factors rounded to f32: Stage II computes in bf16, so the f64 rotation buys
