@@ -209,6 +209,7 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "heads", "requests"])
     ap.add_argument("--p-sweep", default="0.05,0.1,0.2,0.4", help="recompute ratios of the sweep ('' = skip)")
     ap.add_argument("--sweep-steps", type=int, default=3)
+    ap.add_argument("--chunks", default="precompute", choices=["precompute", "random"])
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -235,6 +236,18 @@ def main():
                                                 "ffn_dim", "vocab_size", "rope_theta")})
     s = cfgd["n_chunks"] * cfgd["chunk_len"]
     mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
+
+    def make_chunks(model, seed):
+        """The request's chunk store: each chunk precomputed on the GPU from uniform random
+        tokens (prefill.precompute_chunk path, realistic K/V), or N(0,1) K/V (--chunks random)."""
+        if args.chunks == "random":
+            return random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=seed)
+        from paper_2602_02579_b200.prefill import precompute_chunks_device
+        crng = np.random.default_rng(seed)
+        toks = [crng.integers(0, cfg.vocab_size, cfgd["chunk_len"]) for _ in range(cfgd["n_chunks"])]
+        out = precompute_chunks_device(model, cfg, toks)
+        torch.cuda.synchronize()
+        return out
     heads = mode == "heads" and world > 1
     comm = None
     if heads:
@@ -248,16 +261,16 @@ def main():
         # one request, KV heads (and ffn blocks) sharded over the ranks; every rank builds
         # the same seeded model / chunk store and keeps its slice
         full = P.DeviceModel.random(cfg, seed=0)
+        full_chunks = make_chunks(full, 1)
         dm = full.shard(rank, world, comm.handle)
         del full
-        full_chunks = random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=1)
         chunks = tp.shard_chunks(full_chunks, rank, world)
         del full_chunks
         torch.cuda.empty_cache()
         qseed = 7
     else:
         dm = P.DeviceModel.random(cfg, seed=0)
-        chunks = random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=1 + rank)
+        chunks = make_chunks(dm, 1 + rank)
         qseed = 7 + rank
     pipe = PrefillPipeline(dm, chunks, args.m, args.p)
     rng = np.random.default_rng(qseed)
@@ -344,6 +357,8 @@ def main():
         tot_ms, cnt = phases[name]
         if cnt == 0 or tot_ms <= 0:
             continue
+        if name == "lm_head":  # one GEMV per step, timed together with its final norm (2 timer scopes)
+            cnt = args.steps
         per_launch_s = tot_ms / cnt / 1e3
         ach = units / per_launch_s / (1e9 if unit == "GB/s" else 1e12)
         peak = hbm if bound == "hbm" else tf_sust
@@ -362,7 +377,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16 (Stage II) / fp32-faithful (narrow passes)",
-            "data": "synthetic (random-init weights, N(0,1) chunk K/V, uniform token ids)",
+            "data": ("synthetic: random-init weights, uniform random token ids; chunk K/V " +
+                     ("precomputed on the GPU (precompute_chunk)" if args.chunks == "precompute" else "N(0,1)")),
             "config": {"workload": args.config, "model": "Llama-3-8B shape" if "llama" in args.config else
                        "Mistral-7B shape", "s": s, "chunks": cfgd["n_chunks"], "m": args.m, "p": args.p, "k": k,
                        "parallelism": f"tp{world} (KV-head sharded, NCCL)" if heads else f"request-dp{world}",
