@@ -39,8 +39,10 @@ struct S1TcCfg {
   static constexpr int STAGE = 4 * PLANE;       // Kh, Km, Kl, V
   static constexpr int STAGES = 2;
   static constexpr int SMEM = 3 * QSPLIT + STAGES * STAGE + 1024 + 256;
-  // TMEM columns: S0 [0,64) S1 [64,128) O [128,128+DKP) P planes [256,352)
-  static constexpr int T_S = 0, T_O = 128, T_P = 256;
+  // TMEM columns: S0 [0,64) S1 [64,128) O [128,128+DKP) P planes, double-buffered:
+  // tile j's P at [256 + 96*(j&1), +96) so the softmax of tile j+1 can write its P while
+  // PV(j) still reads the other buffer
+  static constexpr int T_S = 0, T_O = 128, T_P = 256, P_BUF = 96;
   static constexpr int SOFTMAX_WARPS = 8;
 };
 
@@ -79,8 +81,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* kv_empty = bars + C::STAGES;
   uint64_t* s_full = bars + 2 * C::STAGES;
   uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;
-  uint64_t* pv_full = p_full + 1;
+  uint64_t* p_full = s_free + 2;  // [2] per P buffer
+  uint64_t* pv_full = p_full + 2;
   uint64_t* q_full = pv_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
@@ -101,7 +103,8 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], C::SOFTMAX_WARPS);
     }
-    mbar_init(p_full, C::SOFTMAX_WARPS);
+    mbar_init(&p_full[0], C::SOFTMAX_WARPS);
+    mbar_init(&p_full[1], C::SOFTMAX_WARPS);
     mbar_init(pv_full, 1);
     mbar_init(q_full, 1);
     fence_barrier_init();
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(320, 1)
       if (j >= 1) {
         const int jp = j - 1;
         const int st = jp % C::STAGES;
-        mbar_wait(p_full, (uint32_t)jp & 1);
+        mbar_wait(&p_full[jp & 1], (uint32_t)(jp >> 1) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t v_addr = smem_u32(sKV + st * C::STAGE + 3 * C::PLANE);
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int x = 0; x < 3; ++x)
 #pragma unroll
             for (int kk = 0; kk < C::KT / 16; ++kk, ++n)
-              umma_bf16_ts(tmem + C::T_O, tmem + C::T_P + x * (C::KT / 2) + kk * 8,
+              umma_bf16_ts(tmem + C::T_O, tmem + C::T_P + (jp & 1) * C::P_BUF + x * (C::KT / 2) + kk * 8,
                            sdesc_sw128(v_addr + kk * 16 * 128, C::ATOM_K, 1024), idesc_o,
                            (jp > 0 || n > 0) ? 1u : 0u);
           umma_commit(pv_full);
@@ -257,10 +260,12 @@ __global__ void __launch_bounds__(320, 1)
         psum += p0 + p1;
         split3_pack(p0, p1, ph[i], pm[i], pl[i]);
       }
-      if (j >= 1) {
+      // P(j) goes to buffer j&1, whose previous reader PV(j-2) is complete (S(j) was issued
+      // after it); only an O rescale must wait for PV(j-1)
+      if (j >= 1 && __any_sync(0xffffffffu, grow)) {
         mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, grow)) {
+        {
           const float f = grow ? corr : 1.f;
 #pragma unroll 1
           for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
@@ -275,14 +280,18 @@ __global__ void __launch_bounds__(320, 1)
       }
       l_run = l_run * (grow ? corr : 1.f) + psum;
       m_run = m_new;
-      tmem_st16(tmem + lb + C::T_P + hc * (HC / 2), ph);
-      tmem_st16(tmem + lb + C::T_P + C::KT / 2 + hc * (HC / 2), pm);
-      tmem_st16(tmem + lb + C::T_P + C::KT + hc * (HC / 2), pl);
+      const uint32_t tP = tmem + lb + C::T_P + (j & 1) * C::P_BUF;
+      tmem_st16(tP + hc * (HC / 2), ph);
+      tmem_st16(tP + C::KT / 2 + hc * (HC / 2), pm);
+      tmem_st16(tP + C::KT + hc * (HC / 2), pl);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
+    // the last two PVs may both be pending (S(j) only implies PV(j-2)): wait in order so
+    // the parity check cannot alias
+    if (n_tiles > 1) mbar_wait(pv_full, (uint32_t)(n_tiles - 2) & 1);
     if (n_tiles > 0) {
       mbar_wait(pv_full, (uint32_t)(n_tiles - 1) & 1);
       tc_fence_after();
