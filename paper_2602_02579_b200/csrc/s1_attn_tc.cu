@@ -37,12 +37,14 @@ struct S1TcCfg {
   static constexpr int ATOM_Q = 128 * 128;      // bytes per 64-col atom of a Q plane
   static constexpr int ATOM_K = KT * 128;       // bytes per 64-col atom of a K/V plane
   static constexpr int STAGE = 4 * PLANE;       // Kh, Km, Kl, V
-  static constexpr int STAGES = 2;
-  static constexpr int SMEM = 3 * QSPLIT + STAGES * STAGE + 1024 + 256;
-  // TMEM columns: S0 [0,64) S1 [64,128) O [128,128+DKP) P planes, double-buffered:
-  // tile j's P at [256 + 96*(j&1), +96) so the softmax of tile j+1 can write its P while
-  // PV(j) still reads the other buffer
-  static constexpr int T_S = 0, T_O = 128, T_P = 256, P_BUF = 96;
+  // The Q planes live in TMEM (A operand of the S MMAs), which frees shared memory for
+  // a third K/V stage: with two, the softmax waited for S ~45 % of the time behind the
+  // TMA (ncu, profiles/r01), the memory pipeline being too shallow.
+  static constexpr int STAGES = 3;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  // TMEM columns: Q planes [0,192) (plane x at 64x, DKP/2 columns each), S [192,256),
+  // O [256,256+DKP), P planes [384,480)
+  static constexpr int T_Q = 0, Q_PLANE = 64, T_S = 192, T_O = 256, T_P = 384;
   static constexpr int SOFTMAX_WARPS = 8;
 };
 
@@ -74,15 +76,14 @@ __global__ void __launch_bounds__(320, 1)
   using C = S1TcCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                   // 3 planes
-  uint8_t* sKV = smem + 3 * C::QSPLIT;  // STAGES x {Kh, Km, Kl, V}
+  uint8_t* sKV = smem;  // STAGES x {Kh, Km, Kl, V}
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::STAGE);
   uint64_t* kv_full = bars;
   uint64_t* kv_empty = bars + C::STAGES;
   uint64_t* s_full = bars + 2 * C::STAGES;
-  uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;  // [2] per P buffer
-  uint64_t* pv_full = p_full + 2;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* p_full = s_free + 1;
+  uint64_t* pv_full = p_full + 1;
   uint64_t* q_full = pv_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
@@ -99,14 +100,11 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], C::SOFTMAX_WARPS);
-    }
-    mbar_init(&p_full[0], C::SOFTMAX_WARPS);
-    mbar_init(&p_full[1], C::SOFTMAX_WARPS);
+    mbar_init(s_full, 1);
+    mbar_init(s_free, C::SOFTMAX_WARPS);
+    mbar_init(p_full, C::SOFTMAX_WARPS);
     mbar_init(pv_full, 1);
-    mbar_init(q_full, 1);
+    mbar_init(q_full, C::SOFTMAX_WARPS);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc(tmem_slot, 512);
@@ -124,15 +122,6 @@ __global__ void __launch_bounds__(320, 1)
       tma_prefetch(&tK2);
       tma_prefetch(&tK3);
       tma_prefetch(&tV);
-      {  // the three Q planes of this (head, row block)
-        const int qrow = ((g * (int)gridDim.z + blockIdx.z) * 3) * 128;
-        mbar_expect_tx(q_full, 3 * C::QSPLIT);
-#pragma unroll
-        for (int x = 0; x < 3; ++x)
-#pragma unroll
-          for (int at = 0; at < C::ATOMS; ++at)
-            tma_load_2d(sQ + x * C::QSPLIT + at * C::ATOM_Q, &tQ, q_full, at * 64, qrow + x * 128);
-      }
       const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
       for (int j = 0; j < n_tiles; ++j) {
         const int st = j % C::STAGES;
@@ -158,12 +147,11 @@ __global__ void __launch_bounds__(320, 1)
     constexpr int PB[6] = {0, 1, 0, 2, 1, 0};  // K plane of each product
     mbar_wait(q_full, 0);
     tc_fence_after();
-    const uint32_t q_addr = smem_u32(sQ);
     for (int j = 0; j <= n_tiles; ++j) {
       if (j < n_tiles) {
         const int st = j % C::STAGES;
         mbar_wait(&kv_full[st], (uint32_t)(j / C::STAGES) & 1);
-        if (j >= 2) mbar_wait(&s_free[j & 1], (uint32_t)((j - 2) >> 1) & 1);
+        if (j >= 1) mbar_wait(s_free, (uint32_t)(j - 1) & 1);  // S(j-1) is in the softmax's registers
         tc_fence_after();
         if (elect_one()) {
           const uint32_t k_addr = smem_u32(sKV + st * C::STAGE);
@@ -172,19 +160,18 @@ __global__ void __launch_bounds__(320, 1)
           for (int pr = 0; pr < 6; ++pr)
 #pragma unroll
             for (int kk = 0; kk < DKP / 16; ++kk, ++n) {
-              const uint32_t qo = PA[pr] * C::QSPLIT + (kk >> 2) * C::ATOM_Q + (kk & 3) * 32;
               const uint32_t ko = PB[pr] * C::PLANE + (kk >> 2) * C::ATOM_K + (kk & 3) * 32;
-              umma_bf16(tmem + C::T_S + (j & 1) * C::KT, sdesc_sw128(q_addr + qo, 16, 1024),
-                        sdesc_sw128(k_addr + ko, 16, 1024), idesc_s, n > 0 ? 1u : 0u);
+              umma_bf16_ts(tmem + C::T_S, tmem + C::T_Q + PA[pr] * C::Q_PLANE + kk * 8,
+                           sdesc_sw128(k_addr + ko, 16, 1024), idesc_s, n > 0 ? 1u : 0u);
             }
-          umma_commit(&s_full[j & 1]);
+          umma_commit(s_full);
         }
         __syncwarp();
       }
       if (j >= 1) {
         const int jp = j - 1;
         const int st = jp % C::STAGES;
-        mbar_wait(&p_full[jp & 1], (uint32_t)(jp >> 1) & 1);
+        mbar_wait(p_full, (uint32_t)jp & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t v_addr = smem_u32(sKV + st * C::STAGE + 3 * C::PLANE);
@@ -193,7 +180,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int x = 0; x < 3; ++x)
 #pragma unroll
             for (int kk = 0; kk < C::KT / 16; ++kk, ++n)
-              umma_bf16_ts(tmem + C::T_O, tmem + C::T_P + (jp & 1) * C::P_BUF + x * (C::KT / 2) + kk * 8,
+              umma_bf16_ts(tmem + C::T_O, tmem + C::T_P + x * (C::KT / 2) + kk * 8,
                            sdesc_sw128(v_addr + kk * 16 * 128, C::ATOM_K, 1024), idesc_o,
                            (jp > 0 || n > 0) ? 1u : 0u);
           umma_commit(pv_full);
@@ -211,11 +198,32 @@ __global__ void __launch_bounds__(320, 1)
     const bool valid = row < a.R;
     const uint32_t lb = (uint32_t)(quarter * 32) << 16;
     constexpr int HC = C::KT / 2;  // columns per warp
+    {  // this warp's half of the row's Q planes -> TMEM (lane = row): A operand of S = Q K^T
+      const __nv_bfloat16* q3 = reinterpret_cast<const __nv_bfloat16*>(a.q3);
+      if (hc * 32 < DKP / 2) {
+#pragma unroll 1
+        for (int x = 0; x < 3; ++x) {
+          const uint4* src = reinterpret_cast<const uint4*>(
+              q3 + ((((long)g * gridDim.z + blockIdx.z) * 3 + x) * 128 + r) * DKP + hc * 64);
+          uint32_t u[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = src[c];
+            u[4 * c] = v.x; u[4 * c + 1] = v.y; u[4 * c + 2] = v.z; u[4 * c + 3] = v.w;
+          }
+          tmem_st32(tmem + lb + C::T_Q + x * C::Q_PLANE + hc * 32, u);
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+    }
     float m_run = -INFINITY, l_run = 0.f;  // l_run: this warp's half of the row sum
     // scores, key-major S[g][t][r] (t < s): one warp store = 32 consecutive rows = 128 B
     float* scol = (a.S != nullptr && valid) ? a.S + (long)g * a.s * a.R + row : nullptr;
     for (int j = 0; j < n_tiles; ++j) {
-      mbar_wait(&s_full[j & 1], (uint32_t)(j >> 1) & 1);
+      mbar_wait(s_full, (uint32_t)j & 1);
       tc_fence_after();
       // both warps of a quarter read the whole 64-key row (cheap TMEM reads) so each
       // has the tile max without an exchange; each then handles its 32 columns
@@ -224,8 +232,8 @@ __global__ void __launch_bounds__(320, 1)
       const int key0 = k_begin + j * C::KT + hc * HC;
       {
         uint32_t u[32], w[32];
-        tmem_ld32(tmem + lb + C::T_S + (j & 1) * C::KT + hc * HC, u);
-        tmem_ld32(tmem + lb + C::T_S + (j & 1) * C::KT + (hc ^ 1) * HC, w);
+        tmem_ld32(tmem + lb + C::T_S + hc * HC, u);
+        tmem_ld32(tmem + lb + C::T_S + (hc ^ 1) * HC, w);
         tmem_ld_wait();
         const int okey0 = k_begin + j * C::KT + (hc ^ 1) * HC;
 #pragma unroll
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[j & 1]);
+      if (lane == 0) mbar_arrive(s_free);
       if (scol != nullptr) {
         if (key0 + HC <= k_end) {
 #pragma unroll
@@ -260,12 +268,10 @@ __global__ void __launch_bounds__(320, 1)
         psum += p0 + p1;
         split3_pack(p0, p1, ph[i], pm[i], pl[i]);
       }
-      // P(j) goes to buffer j&1, whose previous reader PV(j-2) is complete (S(j) was issued
-      // after it); only an O rescale must wait for PV(j-1)
-      if (j >= 1 && __any_sync(0xffffffffu, grow)) {
+      if (j >= 1) {  // PV(j-1) has read P and accumulated O
         mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
         tc_fence_after();
-        {
+        if (__any_sync(0xffffffffu, grow)) {
           const float f = grow ? corr : 1.f;
 #pragma unroll 1
           for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
@@ -280,18 +286,15 @@ __global__ void __launch_bounds__(320, 1)
       }
       l_run = l_run * (grow ? corr : 1.f) + psum;
       m_run = m_new;
-      const uint32_t tP = tmem + lb + C::T_P + (j & 1) * C::P_BUF;
+      const uint32_t tP = tmem + lb + C::T_P;
       tmem_st16(tP + hc * (HC / 2), ph);
       tmem_st16(tP + C::KT / 2 + hc * (HC / 2), pm);
       tmem_st16(tP + C::KT + hc * (HC / 2), pl);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) mbar_arrive(p_full);
     }
-    // the last two PVs may both be pending (S(j) only implies PV(j-2)): wait in order so
-    // the parity check cannot alias
-    if (n_tiles > 1) mbar_wait(pv_full, (uint32_t)(n_tiles - 2) & 1);
     if (n_tiles > 0) {
       mbar_wait(pv_full, (uint32_t)(n_tiles - 1) & 1);
       tc_fence_after();
