@@ -407,10 +407,12 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.keys_per_split = 512;
   w.n_splits = ceil_div(s_tot, w.keys_per_split);
   {
-    // tensor-core split of the context keys: ~2 waves of (KV head x split) CTAs
+    // tensor-core split of the context keys: one wave of (KV head x split) CTAs (measured
+    // best of 1..4 waves; PKV_S1_WAVES overrides)
     static const bool simt_only = getenv("PKV_S1_SIMT") != nullptr;
     const int row_blocks = ceil_div(R, 128);
-    const int target = std::max(1, 2 * num_sms() / std::max(1, Hkv * row_blocks));
+    static const int waves = getenv("PKV_S1_WAVES") ? std::max(1, atoi(getenv("PKV_S1_WAVES"))) : 1;
+    const int target = std::max(1, waves * num_sms() / std::max(1, Hkv * row_blocks));
     w.tc_keys_per_split = std::max(64, ceil_div(ceil_div(s, target), 64) * 64);
     w.tc_splits = (simt_only || s == 0) ? 0 : ceil_div(s, w.tc_keys_per_split);
     // partial buffers sized for either path (the caller's cache decides which runs)
