@@ -13,6 +13,8 @@ def shares(path):
     agg = collections.defaultdict(lambda: [0.0, 0])
     for r in rows:
         name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+        if not name.startswith("pkv::"):  # torch kernels of the model / input construction
+            continue
         v = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
         ms = v / 1e6 if unit in ("nsecond", "ns") else (v / 1e3 if unit in ("usecond", "us") else v)
