@@ -75,19 +75,40 @@ bool cached_tmap(CUtensorMap* out, const void* base, long rows, long cols, long 
   return true;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG = 1>
 static int launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, EPI>;
+  using Cfg = GemmCfg<BN, EPI, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (attr_err != cudaSuccess) return set_error(PKV_ERR_CUDA, "gemm smem attr: %s", cudaGetErrorString(attr_err));
   long tiles = (long)ceil_div(args.M, Cfg::BMT) * ceil_div(args.N, BN) * args.n_splits;
+  if (tiles <= 0) return PKV_OK;
+  if constexpr (CG == 2) {  // persistent CTA pairs, one cluster of 2 per TPC
+    const int pairs = (int)std::min<long>(tiles, num_sms() / 2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, EPI, CG>, ta, tb, args);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("gemm_tc_kernel (CTA pairs)");
+    return PKV_OK;
+  }
   int grid = (int)std::min<long>(tiles, num_sms());
-  if (grid <= 0) return PKV_OK;
-  launch_k(gemm_tc_kernel<BN, EPI>, grid, 192, Cfg::SMEM, stream, ta, tb, args);
+  launch_k(gemm_tc_kernel<BN, EPI, CG>, grid, 192, Cfg::SMEM, stream, ta, tb, args);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("gemm_tc_kernel");
   return PKV_OK;
@@ -106,8 +127,21 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   if (args.k_tiles_per_split <= 0) args.k_tiles_per_split = ceil_div(kt, args.n_splits);
   args.n_splits = ceil_div(kt, args.k_tiles_per_split);  // no empty splits
   CUtensorMap ta, tb;
+  // Stage-II GEMMs (BN = 256) on CTA pairs unless PKV_GEMM_CG=1
+  static const int cg_env = getenv("PKV_GEMM_CG") ? atoi(getenv("PKV_GEMM_CG")) : 2;
+  const int cg = (bn == 256 && cg_env == 2) ? 2 : 1;
   if (!cached_tmap(&ta, A, args.M, K, lda, 128)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode A failed");
-  if (!cached_tmap(&tb, B, args.N, K, ldb, bn)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode B failed");
+  if (!cached_tmap(&tb, B, args.N, K, ldb, bn / cg)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode B failed");
+  if (cg == 2) {
+    switch (epi) {
+      case EPI_F32: return launch_one<256, EPI_F32, 2>(ta, tb, args, stream);
+      case EPI_BF16: return launch_one<256, EPI_BF16, 2>(ta, tb, args, stream);
+      case EPI_RESID: return launch_one<256, EPI_RESID, 2>(ta, tb, args, stream);
+      case EPI_SILU: return launch_one<256, EPI_SILU, 2>(ta, tb, args, stream);
+      case EPI_QKV: return launch_one<256, EPI_QKV, 2>(ta, tb, args, stream);
+      default: return set_error(PKV_ERR_ARGUMENT, "gemm: unsupported pair epilogue %d", epi);
+    }
+  }
   switch (bn * 16 + epi) {
     case 256 * 16 + EPI_F32: return launch_one<256, EPI_F32>(ta, tb, args, stream);
     case 256 * 16 + EPI_BF16: return launch_one<256, EPI_BF16>(ta, tb, args, stream);

@@ -63,16 +63,23 @@ struct GemmArgs {
 // so both stay at 1 atom / 1 sub-tile; the knobs are kept for re-tuning.
 constexpr int gemm_bk(int bn) { return 64; }
 constexpr int gemm_mt(int bn, int epi) { return 1; }
-template <int BN, int EPI>
+// CG = 2: CTA pair (cluster of 2, cta_group::2).  One MMA tile is 256 x BN: each CTA
+// loads its 128 rows of A and HALF of B (BN/2 rows), the leader issues M = 256 MMAs that
+// read both CTAs' shared memory, and each CTA's TMEM receives its 128 rows x BN.  Per SM
+// this halves the B fill per MMA flop (the Stage-II GEMMs move 48 -> 32 KB per 64-deep
+// k step), the canonical Blackwell GEMM shape.
+template <int BN, int EPI, int CG = 1>
 struct GemmCfg {
-  static constexpr int BM = 128, BK = gemm_bk(BN), MT = gemm_mt(BN, EPI), BMT = BM * MT;
+  static constexpr int BM = 128, BK = gemm_bk(BN), MT = gemm_mt(BN, EPI), BMT = BM * MT * CG;
+  static constexpr int BN_CTA = BN / CG;                            // B rows held by one CTA
   static constexpr int ATOMS = BK / 64;
-  static constexpr int A_ATOM = BM * 128, B_ATOM = BN * 128;  // bytes of one 64-column atom
-  static constexpr int A_SUB = BM * BK * 2;                    // one 128-row sub-tile
+  static constexpr int A_ATOM = BM * 128, B_ATOM = BN_CTA * 128;  // bytes of one 64-column atom
+  static constexpr int A_SUB = BM * BK * 2;                        // one 128-row sub-tile
   static constexpr int A_BYTES = MT * A_SUB;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN >= 256) ? 4 : (BN >= 128 ? 6 : (MT == 2 ? 5 : 7));
+  static constexpr int STAGES = CG == 2 ? 6 : (BN >= 256) ? 4 : (BN >= 128 ? 6 : (MT == 2 ? 5 : 7));
+  static_assert(CG == 1 || (MT == 1 && EPI != EPI_PROJ), "CTA pairs only for the Stage-II epilogues");
   static_assert(MT == 1 || EPI == EPI_PROJ, "sub-tiled A only for the narrow projection epilogue");
   static constexpr int ACC_STRIDE = MT * (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
@@ -92,10 +99,13 @@ __device__ __forceinline__ int k_rotation_t(int mb, int nk) {
 }
 #define k_rotation(mb, nk) k_rotation_t<EPI>(mb, nk)
 
-template <int BN, int EPI>
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-  using Cfg = GemmCfg<BN, EPI>;
+  using Cfg = GemmCfg<BN, EPI, CG>;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA of the pair (0 = leader)
+  const int cta_id = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_ctas = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -122,11 +132,16 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty_bar[b], 4 * CG);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if constexpr (CG == 2) {
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrive / TMA
+    if (warp == 1) tmem_alloc_cg2(tmem_slot, Cfg::TMEM_COLS);
+  } else {
+    if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,7 +161,7 @@ __global__ void __launch_bounds__(192, 1)
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int t = cta_id; t < total_tiles; t += n_ctas) {
         int mb, nb, sp;
         tile_coords(t, mb, nb, sp);
         int k0 = sp * args.k_tiles_per_split;
@@ -157,25 +172,37 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
-          mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          if constexpr (CG == 2) {
+            // both CTAs' bytes land on the leader's full barrier (only the leader's MMA waits)
+            if (rank == 0) mbar_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
 #pragma unroll
-          for (int at = 0; at < Cfg::ATOMS; ++at) {
+            for (int at = 0; at < Cfg::ATOMS; ++at) {
+              tma_load_2d_cg2(sa + at * Cfg::A_ATOM, &tmA, &full_bar[stage], kt * Cfg::BK + at * 64,
+                              mb * Cfg::BMT + (int)rank * Cfg::BM);
+              tma_load_2d_cg2(sb + at * Cfg::B_ATOM, &tmB, &full_bar[stage], kt * Cfg::BK + at * 64,
+                              nb * BN + (int)rank * Cfg::BN_CTA);
+            }
+          } else {
+            mbar_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
 #pragma unroll
-            for (int j = 0; j < Cfg::MT; ++j)
-              tma_load_2d(sa + j * Cfg::A_SUB + at * Cfg::A_ATOM, &tmA, &full_bar[stage], kt * Cfg::BK + at * 64,
-                          mb * Cfg::BMT + j * Cfg::BM);
-            tma_load_2d(sb + at * Cfg::B_ATOM, &tmB, &full_bar[stage], kt * Cfg::BK + at * 64, nb * BN);
+            for (int at = 0; at < Cfg::ATOMS; ++at) {
+#pragma unroll
+              for (int j = 0; j < Cfg::MT; ++j)
+                tma_load_2d(sa + j * Cfg::A_SUB + at * Cfg::A_ATOM, &tmA, &full_bar[stage], kt * Cfg::BK + at * 64,
+                            mb * Cfg::BMT + j * Cfg::BM);
+              tma_load_2d(sb + at * Cfg::B_ATOM, &tmB, &full_bar[stage], kt * Cfg::BK + at * 64, nb * BN);
+            }
           }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc_bf16(128, BN);
+  } else if (warp == 1 && (CG == 1 || rank == 0)) {  // the pair's MMAs are issued by the leader
+    constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+    for (int t = cta_id; t < total_tiles; t += n_ctas, ++local) {
       int mb, nb, sp;
       tile_coords(t, mb, nb, sp);
       int k0 = sp * args.k_tiles_per_split;
@@ -198,30 +225,37 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int j = 0; j < Cfg::MT; ++j) {
               uint64_t ad = sdesc_sw128(a_addr + j * Cfg::A_SUB + (kk >> 2) * Cfg::A_ATOM + (kk & 3) * 32, 16, 1024);
-              umma_bf16(d_tmem + j * (Cfg::ACC_STRIDE / Cfg::MT), ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+              if constexpr (CG == 2)
+                umma_bf16_cg2(d_tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+              else
+                umma_bf16(d_tmem + j * (Cfg::ACC_STRIDE / Cfg::MT), ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty_bar[stage]);
+          if constexpr (CG == 2) umma_commit_cg2(&empty_bar[stage]);  // frees the stage in both CTAs
+          else umma_commit(&empty_bar[stage]);
         }
         __syncwarp();
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
-      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      if (elect_one()) {
+        if constexpr (CG == 2) umma_commit_cg2(&tfull_bar[acc]);
+        else umma_commit(&tfull_bar[acc]);
+      }
       __syncwarp();
     }
-  } else {
+  } else if (warp >= 2) {
     // ---------------------------------------------------------------- epilogue
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = quarter * 32 + lane;
     int local = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+    for (int t = cta_id; t < total_tiles; t += n_ctas, ++local) {
       int mb, nb, sp;
       tile_coords(t, mb, nb, sp);
       const int acc = local & 1;
       const uint32_t use = (uint32_t)(local >> 1);
       mbar_wait(&tfull_bar[acc], use & 1);
       tc_fence_after();
-      const int row = mb * Cfg::BM + row_in_tile;
+      const int row = mb * Cfg::BMT + (int)rank * Cfg::BM + row_in_tile;
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * Cfg::ACC_STRIDE;
 
@@ -442,14 +476,19 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);  // the leader's MMA waits
+        else mbar_arrive(&tempty_bar[acc]);
+      }
     }
   }
 
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // no TMEM use or remote arrive left in either CTA
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
