@@ -79,7 +79,18 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-// POLY of every 8 exponentials go to the FMA-pipe polynomial, the rest to MUFU.EX2
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ void unpack_f16x2(uint32_t v, float& lo, float& hi) {
+  asm("{\n\t.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tcvt.f32.f16 %0, l;\n\tcvt.f32.f16 %1, h;\n\t}"
+      : "=f"(lo), "=f"(hi) : "r"(v));
+}
+
+// POLY of every 8 exponentials go to the FMA-pipe polynomial, the rest to MUFU.EX2;
+// POLY < 0: packed half-precision MUFU.EX2 (two exponentials per op)
 template <int DKP, int POLY>
 __global__ void __launch_bounds__(576, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
@@ -289,7 +300,15 @@ __global__ void __launch_bounds__(576, 1)
           f32x2_unpack(x, x0, x1);
           float p0, p1;
           constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
-          if ((kPolyMask >> (i & 7)) & 1u) {
+          if constexpr (POLY < 0) {
+            // two exponentials per MUFU op (ex2.approx.f16x2): the argument is rounded to
+            // f16 (|x| < 1: 2^-11 relative; larger |x| only for P < 2^-4) and P is rounded
+            // to bf16 for the MMA anyway
+            const uint32_t hx = pack_f16x2(x0, x1);
+            uint32_t hp;
+            asm("ex2.approx.f16x2 %0, %1;" : "=r"(hp) : "r"(hx));
+            unpack_f16x2(hp, p0, p1);
+          } else if ((kPolyMask >> (i & 7)) & 1u) {
             p0 = exp2_poly(x0);
             p1 = exp2_poly(x1);
           } else {
@@ -402,6 +421,7 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   const int poly = env ? atoi(env) : 1;
   if (dkp == 128) {
     if (poly == 1) return launch_attn<128, 1>(tk, tv, a, stream);
+    if (poly < 0) return launch_attn<128, -1>(tk, tv, a, stream);
     return launch_attn<128, 2>(tk, tv, a, stream);
   }
   if (dkp == 64) return launch_attn<64, 2>(tk, tv, a, stream);

@@ -79,13 +79,20 @@ CASES = {
     "c1": (O.Cfg(2, 4, 2, 64, 256, 1024, 1024), 0, "8x256", 32, 0.2),
     # Llama-3-8B layer width, 2 layers, 8 x 256 context
     "llama_width": (O.Cfg(2, 32, 8, 128, 4096, 14336, 2048, rope_theta=500000.0), 0, "8x256", 32, 0.2),
+    # BASELINE configs[3]: the recompute-ratio sweep end points (C1 shape)
+    "c1_p05": (O.Cfg(2, 4, 2, 64, 256, 1024, 1024), 0, "8x256", 32, 0.05),
+    "c1_p40": (O.Cfg(2, 4, 2, 64, 256, 1024, 1024), 0, "8x256", 32, 0.4),
+    # configs[1] geometry: Mistral-7B layer width, theta 1e6, ragged chunks
+    "mistral_width": (O.Cfg(2, 32, 8, 128, 4096, 14336, 2048, rope_theta=1000000.0), 3, "ragged", 24, 0.1),
 }
 
 
 def _materialise(case):
     cfg_o, seed, units, query, p = CASES[case]
     rng = np.random.default_rng(1000 + seed)
-    if isinstance(units, str):
+    if units == "ragged":  # uneven chunk lengths (not multiples of the 64/128-token tiles)
+        units = [rng.integers(0, cfg_o.vocab_size, t).tolist() for t in (300, 77, 513, 129, 255)]
+    elif isinstance(units, str):
         n, t = map(int, units.split("x"))
         units = [rng.integers(0, cfg_o.vocab_size, t).tolist() for _ in range(n)]
     if isinstance(query, int):
