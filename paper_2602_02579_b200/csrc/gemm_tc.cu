@@ -129,7 +129,8 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   CUtensorMap ta, tb;
   // Stage-II GEMMs (BN = 256) on CTA pairs unless PKV_GEMM_CG=1
   static const int cg_env = getenv("PKV_GEMM_CG") ? atoi(getenv("PKV_GEMM_CG")) : 2;
-  const int cg = (bn == 256 && cg_env == 2) ? 2 : 1;
+  static const int proj_cg_env = getenv("PKV_PROJ_CG") ? atoi(getenv("PKV_PROJ_CG")) : 1;
+  const int cg = ((bn == 256 && cg_env == 2) || (bn == 96 && epi == EPI_PROJ && proj_cg_env == 2)) ? 2 : 1;
   if (!cached_tmap(&ta, A, args.M, K, lda, 128)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode A failed");
   if (!cached_tmap(&tb, B, args.N, K, ldb, bn / cg)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode B failed");
   if (cg == 2) {
@@ -139,6 +140,7 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
       case EPI_RESID: return launch_one<256, EPI_RESID, 2>(ta, tb, args, stream);
       case EPI_SILU: return launch_one<256, EPI_SILU, 2>(ta, tb, args, stream);
       case EPI_QKV: return launch_one<256, EPI_QKV, 2>(ta, tb, args, stream);
+      case EPI_PROJ: return launch_one<96, EPI_PROJ, 2>(ta, tb, args, stream);
       default: return set_error(PKV_ERR_ARGUMENT, "gemm: unsupported pair epilogue %d", epi);
     }
   }

@@ -79,7 +79,7 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN_CTA * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = CG == 2 ? 6 : (BN >= 256) ? 4 : (BN >= 128 ? 6 : (MT == 2 ? 5 : 7));
-  static_assert(CG == 1 || (MT == 1 && EPI != EPI_PROJ), "CTA pairs only for the Stage-II epilogues");
+  static_assert(CG == 1 || MT == 1, "CTA pairs with one A sub-tile per CTA");
   static_assert(MT == 1 || EPI == EPI_PROJ, "sub-tiled A only for the narrow projection epilogue");
   static constexpr int ACC_STRIDE = MT * (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(192, 1)
        for (int j = 0; j < Cfg::MT; ++j) {
         // one thread = one output feature n; the 96 accumulator columns are the hi/mid/lo
         // planes of the 32 query rows
-        const int msub = mb * Cfg::MT + j;  // 128-row sub-tile
+        const int msub = (mb * CG + (int)rank) * Cfg::MT + j;  // 128-row sub-tile
         uint32_t a0[32], a1[32], a2[32];
         __syncwarp();
         const uint32_t t_sub = t_row + j * (Cfg::ACC_STRIDE / Cfg::MT);
