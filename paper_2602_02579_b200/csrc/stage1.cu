@@ -591,13 +591,35 @@ __global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict_
       const int i = i0 + lane;
       double acc = 0.0;
       if (i < m) {
-        for (int g = 0; g < Hkv; ++g) {
-          const float* col = S + ((long)g * s + t) * R;
+        if (G == 4 && (Hkv & 1) == 0) {
+          // common GQA case: 8 independent loads in flight per step, two f64 chains
+          double acc2 = 0.0;
+          for (int g = 0; g < Hkv; g += 2) {
+            const float* c0 = S + ((long)g * s + t) * R + i;
+            const float* c1 = c0 + (long)s * R;
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              v[j] = __ldg(c0 + j * m);
+              v[4 + j] = __ldg(c1 + j * m);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 n0 = shn[g * R + j * m + i], n1 = shn[(g + 1) * R + j * m + i];
+              acc += (double)(ex2(fmaf(v[j], LOG2E, -n0.x)) * n0.y);
+              acc2 += (double)(ex2(fmaf(v[4 + j], LOG2E, -n1.x)) * n1.y);
+            }
+          }
+          acc += acc2;
+        } else {
+          for (int g = 0; g < Hkv; ++g) {
+            const float* col = S + ((long)g * s + t) * R;
 #pragma unroll 4
-          for (int j = 0; j < G; ++j) {
-            const int r = j * m + i;
-            const float2 n = shn[g * R + r];
-            acc += (double)(ex2(fmaf(__ldg(col + r), LOG2E, -n.x)) * n.y);
+            for (int j = 0; j < G; ++j) {
+              const int r = j * m + i;
+              const float2 n = shn[g * R + r];
+              acc += (double)(ex2(fmaf(__ldg(col + r), LOG2E, -n.x)) * n.y);
+            }
           }
         }
       }
