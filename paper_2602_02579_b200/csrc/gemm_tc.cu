@@ -114,6 +114,38 @@ static int launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmAr
   return PKV_OK;
 }
 
+// narrow projection with split-K over a cluster of n_splits CTAs (DSMEM reduction)
+static int launch_proj_cluster(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args,
+                               cudaStream_t stream) {
+  using Cfg = GemmCfg<96, EPI_PROJ, 1>;
+  auto kern = gemm_tc_kernel<96, EPI_PROJ, 1, 1>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  });
+  if (attr_err != cudaSuccess) return set_error(PKV_ERR_CUDA, "gemm smem attr: %s", cudaGetErrorString(attr_err));
+  const int tiles_m = ceil_div(args.M, Cfg::BMT);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(tiles_m * args.n_splits);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = args.n_splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, ta, tb, args);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("gemm_tc_kernel (cluster split-K)");
+  return PKV_OK;
+}
+
 // A: [M][K] bf16 (row stride lda elements), B: [N][K] bf16 (row stride ldb).
 int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long ldb, int K, GemmArgs args,
                    cudaStream_t stream) {
@@ -133,6 +165,12 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   const int cg = ((bn == 256 && cg_env == 2) || (bn == 96 && epi == EPI_PROJ && proj_cg_env == 2)) ? 2 : 1;
   if (!cached_tmap(&ta, A, args.M, K, lda, 128)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode A failed");
   if (!cached_tmap(&tb, B, args.N, K, ldb, bn / cg)) return set_error(PKV_ERR_CUDA, "gemm: TMA encode B failed");
+  // cluster split-K for the narrow projection: correct, but clusters of 2..8 CTAs with
+  // ~200 KB of shared memory each co-schedule poorly (GPC packing) -- measured +4 ms per
+  // prefill, so opt-in (PKV_PROJ_CLUSTER=1)
+  static const bool proj_cluster = getenv("PKV_PROJ_CLUSTER") && getenv("PKV_PROJ_CLUSTER")[0] == '1';
+  if (cg == 1 && bn == 96 && epi == EPI_PROJ && proj_cluster && args.n_splits >= 2 && args.n_splits <= 8)
+    return launch_proj_cluster(ta, tb, args, stream);
   if (cg == 2) {
     switch (epi) {
       case EPI_F32: return launch_one<256, EPI_F32, 2>(ta, tb, args, stream);

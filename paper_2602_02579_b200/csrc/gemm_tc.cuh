@@ -99,13 +99,22 @@ __device__ __forceinline__ int k_rotation_t(int mb, int nk) {
 }
 #define k_rotation(mb, nk) k_rotation_t<EPI>(mb, nk)
 
-template <int BN, int EPI, int CG>
+// CK = 1 (EPI_PROJ only): split-K across a thread-block cluster of n_splits CTAs (one
+// m-tile per cluster, rank = split); the partial results are summed through distributed
+// shared memory by rank 0 in split order -- no global partials, fences or atomics.
+template <int BN, int EPI, int CG, int CK = 0>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
   using Cfg = GemmCfg<BN, EPI, CG>;
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // CTA of the pair (0 = leader)
-  const int cta_id = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int n_ctas = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  static_assert(CK == 0 || (EPI == EPI_PROJ && CG == 1), "cluster split-K is for the narrow projection");
+  const uint32_t rank = (CG == 2 || CK) ? cluster_ctarank() : 0;  // CTA of the pair / k split
+  int cta_id = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  int n_ctas = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  if constexpr (CK) {  // exactly one tile per CTA: (m-tile = cluster, split = rank)
+    const int tiles_m_ = (args.M + Cfg::BMT - 1) / Cfg::BMT;
+    cta_id = (int)(blockIdx.x / args.n_splits) + tiles_m_ * (int)rank;
+    n_ctas = 1 << 30;
+  }
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -279,7 +288,12 @@ __global__ void __launch_bounds__(192, 1)
           y[i] = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
         const int n = msub * Cfg::BM + row_in_tile;  // GEMM row == output feature
         bool write = args.n_splits == 1;
-        if (!write) {
+        if constexpr (CK) {  // partial -> own smem (the pipeline ring is drained); reduced below
+          float* xb = reinterpret_cast<float*>(smem) + row_in_tile * 33;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) xb[i] = y[i];
+          write = false;
+        } else if (!write) {
           float* mine = args.part + ((long)(sp * subtiles_m + msub) * 128 + row_in_tile) * 32;
 #pragma unroll
           for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(mine + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
@@ -484,6 +498,38 @@ __global__ void __launch_bounds__(192, 1)
   }
 
   __syncthreads();
+  if constexpr (CK) {
+    cluster_sync();  // every split's partial is in its shared memory
+    if (rank == 0 && warp >= 2) {
+      const int row_in_tile = (warp & 3) * 32 + (threadIdx.x & 31);
+      const int n = (cta_id % ((args.M + Cfg::BMT - 1) / Cfg::BMT)) * Cfg::BM + row_in_tile;
+      float y[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) y[i] = 0.f;
+      const uint32_t local = smem_u32(reinterpret_cast<float*>(smem) + row_in_tile * 33);
+#pragma unroll 1
+      for (int s2 = 0; s2 < args.n_splits; ++s2) {  // fixed split order: deterministic
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(s2));
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float v;
+          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote + 4 * i));
+          y[i] += v;
+        }
+      }
+      if (n < args.M) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i < args.mrows) {
+            float* dst = args.out + (long)i * args.ldo + n;
+            *dst = args.resid ? *dst + y[i] : y[i];
+          }
+        }
+      }
+    }
+    cluster_sync();  // peers keep their shared memory until rank 0 has read it
+  }
   if constexpr (CG == 2) cluster_sync();  // no TMEM use or remote arrive left in either CTA
   if (warp == 1) {
     tc_fence_after();
