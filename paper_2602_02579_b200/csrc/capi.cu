@@ -623,8 +623,13 @@ size_t pkv_recompute_workspace(const pkv_model* m, int32_t k) {
 
 // the Stage-II layer loop over the k rows `sel` (recompute_selected, and with sel = all
 // positions full_prefill / precompute_chunk); leaves the final residual stream in w.h
+// need_final_h = false: the last layer stops after its QKV projection + scatter.  Its
+// attention / o / MLP only update the residual stream, which recompute_selected drops
+// after the loop (reference recompute.py:57-82 returns the cache; the K/V writes are the
+// only observable result), so that work is dead.  full_prefill keeps it for the logits.
 static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k,
-                          float* tap_v, void* knr_out, void* v_out, const RcWs& w, cudaStream_t st) {
+                          float* tap_v, void* knr_out, void* v_out, const RcWs& w, cudaStream_t st,
+                          bool need_final_h) {
   const pkv_config& cf = md->cfg;
   const int H = md->H, Hkv = md->Hkv, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
   // row-parallel o / down GEMMs under tensor parallelism: rank 0 accumulates into the
@@ -669,6 +674,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     }
     // K/V of every selected token are in the cache before this layer's attention
     TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    if (l == cf.n_layers - 1 && !need_final_h) break;
     TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
                        (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
     GemmArgs go{};
@@ -706,7 +712,7 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
   size_t need = 0;
   RcWs w = carve_rc(md, k, workspace, &need);
   if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
-  return recompute_core(md, c, sel, k, tap_k, tap_v, nullptr, nullptr, w, S(stream));
+  return recompute_core(md, c, sel, k, tap_k, tap_v, nullptr, nullptr, w, S(stream), /*need_final_h=*/false);
 }
 
 // ------------------------------------------------------------------ full prefill
@@ -752,7 +758,7 @@ int pkv_full_prefill(const pkv_model* md, const pkv_cache* c, void* k_nr_out, vo
   iota_kernel<<<ceil_div(n, 256), 256, 0, st>>>(sel, n);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("iota_kernel");
-  int rc = recompute_core(md, c, sel, n, nullptr, nullptr, k_nr_out, v_out, w, st);
+  int rc = recompute_core(md, c, sel, n, nullptr, nullptr, k_nr_out, v_out, w, st, logits_out != nullptr);
   if (rc) return rc;
   if (logits_out) {  // _head_logits (model.py:326-329) for every row: final norm, then lm_head
     const pkv_config& cf = md->cfg;
