@@ -549,6 +549,9 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.x3_ld = ldx;
     TTRY(T_QP_ATTN, s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
                             (flags & PKV_QP_RENORM) ? 1 : 0, cf.n_heads, w.rows64, comm, st));
+    // without logits (score_prophet) the last layer's o-projection and MLP only feed a
+    // residual stream nobody reads: the per-layer scores are complete here
+    if (l == cf.n_layers - 1 && !(flags & PKV_QP_LOGITS)) break;
     if (fused) {
       TTRY(T_QP_PROJ, proj_fused(lw.wo, Dp, md->HQ, m, w.h, Dp, resid, w.proj, st));
       if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
