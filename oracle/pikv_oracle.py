@@ -545,6 +545,22 @@ def finalize(w, cfg, cache, query, want_rows=False, macs=None, score_macs=None):
     return res.last_logits, res
 
 
+def decode(w, cfg, kv_layers, kv_pos, tokens):
+    """Teacher-forced decode steps (model.py:405-441): each token attends to the KV state
+    plus its own fresh K/V, which is then appended.  Returns per-step logits."""
+    ks = [np.array(k) for k, _ in kv_layers]
+    vs = [np.array(v) for _, v in kv_layers]
+    pos = np.array(kv_pos, dtype=np.int64)
+    out = []
+    for t in tokens:
+        res = narrow_pass(w, cfg, list(zip(ks, vs)), pos, [int(t)])
+        out.append(res.last_logits)
+        ks = [np.concatenate([k, fk], axis=0) for k, fk in zip(ks, res.fresh_k)]
+        vs = [np.concatenate([v, fv], axis=0) for v, fv in zip(vs, res.fresh_v)]
+        pos = np.concatenate([pos, [pos.shape[0]]])
+    return out
+
+
 # --------------------------------------------------------------------------
 # MAC books (reference FlopTally semantics, model.py:188-193; formulas in
 # SURVEY.md Appendix B, verified against the reference tallies)

@@ -13,6 +13,7 @@ from .errors import (ArgumentError, ConfigError, EngineError, FormatError, Incom
                      NumericsError, ShapeError, StateError, TruncatedError)
 from .model import (DeviceModel, FlopCounter, FlopTally, KVCache, LayerWeights, ModelConfig, ModelWeights,
                     random_weights)
+from .decode import GenerationResult, decode_step, greedy_generate
 from .prefill import PrefillTrace, full_prefill, precompute_chunk
 from .recompute import (AnswerRecord, FinalizeResult, RecomputePlan, StrategyRun, finalize_query,
                         recompute_selected, run_strategy, selection_digest)

@@ -238,6 +238,13 @@ class KVCache:
     def length(self) -> int:
         return int(self.positions.shape[0])
 
+    @classmethod
+    def from_prefill(cls, trace) -> "KVCache":
+        """Reference KVCache.from_prefill (model.py:221-228): host copies of a prefill."""
+        return cls(keys=[np.array(k, copy=True) for k in trace.keys],
+                   values=[np.array(v, copy=True) for v in trace.values],
+                   positions=np.array(trace.positions, copy=True), last_logits=np.array(trace.logits[-1], copy=True))
+
 
 # ---------------------------------------------------------------------------- device
 

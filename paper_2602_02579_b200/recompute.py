@@ -116,6 +116,8 @@ def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_at
         return [np.concatenate([cache.values[li], fvh[li]], axis=0) for li in range(L)]
 
     kv = KVCache(keys=keys, values=values, positions=np.arange(s + m, dtype=np.int64), last_logits=first)
+    from .decode import DevicePools
+    kv._device_pools = DevicePools.from_assembled(cache, s + m)  # decoding continues on the device
     return FinalizeResult(cache=kv, first_logits=first, rows=None)
 
 
@@ -148,10 +150,10 @@ class AnswerRecord:
 
 @dataclass
 class StrategyRun:
-    """The TTFT slice of one (strategy, budget) cell.  The reference's unbilled
-    measurement apparatus (full-prefill summaries, losses, greedy decoding --
-    recompute.py:194-206, 228-247) is outside the B200 hot path: those fields are
-    None and the losses NaN."""
+    """One (strategy, budget) cell: the TTFT slice plus greedy decoding on the device.
+    The reference's unbilled measurement apparatus (full-prefill attention summaries and
+    losses, recompute.py:194-206, 228-247) is outside the B200 hot path: those fields
+    are None and the losses NaN."""
     record: AnswerRecord
     selection: SelectionResult
     scores: ValueScores
@@ -187,10 +189,15 @@ def run_strategy(weights, config: ModelConfig, chunks, query_tokens, strategy: s
     stage2 = FlopTally()
     recompute_selected(weights, config, cache, RecomputePlan(sel), tally=stage2)
     fin = finalize_query(weights, config, cache, query, tally=stage2)
-    record = AnswerRecord(task_id=task_id, strategy=strategy, p=p, answer_tokens=[], answer_text="",
-                          exact_match=None, semantic_loss=float("nan"), residual_loss=float("nan"),
+    from .decode import greedy_generate
+    gen = greedy_generate(weights, config, fin.cache, max_new_tokens, stop_ids=stop_ids)
+    gold = list(gold_tokens) if gold_tokens is not None else None
+    record = AnswerRecord(task_id=task_id, strategy=strategy, p=p, answer_tokens=gen.tokens,
+                          answer_text=tokenizer.decode(gen.tokens) if tokenizer is not None else "",
+                          exact_match=(gen.tokens == gold) if gold is not None else None,
+                          semantic_loss=float("nan"), residual_loss=float("nan"),
                           flops_stage1=stage1.total.multiply_accumulate_count,
                           flops_stage2=stage2.total.multiply_accumulate_count, selected_indices=sel.indices,
                           selection_digest=selection_digest(sel.indices))
     return StrategyRun(record=record, selection=sel, scores=scores, full_summary=None, naive_summary=None,
-                       repaired_summary=None, per_token_naive=None, generated=None, first_logits=fin.first_logits)
+                       repaired_summary=None, per_token_naive=None, generated=gen, first_logits=fin.first_logits)
