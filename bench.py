@@ -419,7 +419,11 @@ def main():
                 sp_pipe = PrefillPipeline(dm, chunks, args.m, pp)
                 sp_pipe.set_query(query)
                 sp_pipe.step()
-                sp_pipe.capture()
+                try:
+                    sp_pipe.capture()
+                except Exception:  # noqa: BLE001 -- eager launches if the step cannot be captured
+                    torch.cuda.synchronize()
+                    sp_pipe.replay = sp_pipe.step
                 sp_pipe.replay()
                 torch.cuda.synchronize()
                 if world > 1:
