@@ -21,6 +21,7 @@
 //              PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
 // TMEM: S_A [0,128) S_B [128,256) O_A [256,256+DKP) O_B [384,384+DKP).
 #include <mutex>
+#include <type_traits>
 #include "kernels.cuh"
 #include "gemm_tc.cuh"
 
@@ -375,6 +376,283 @@ __global__ void __launch_bounds__(576, 1)
   }
 }
 
+
+// Three key-column slices per TMEM lane quarter (48 + 48 + 32 keys of each 128-key page):
+// 24 softmax warps + TMA + MMA = 832 threads.  The page loop of a tile is a chain
+// softmax(j) -> PV(j), S(j+1) -> softmax(j+1); spreading the softmax of a page over three
+// warps per 32 rows (instead of two) shortens that chain.  Each slice writes its P into
+// its OWN S columns (cols [48c, 48c + W/2)), so the PV MMA reads P at slice offsets.
+// DKP = 128 only (O columns split 48/48/32 the same way).
+template <int POLY>
+__global__ void __launch_bounds__(832, 1)
+    attn_tc3_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
+  constexpr int DKP = 128;
+  using Cfg = AttnCfg<DKP>;
+  constexpr int TMA_WARP = 24, MMA_WARP = 25;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + 2 * Cfg::Q_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + Cfg::STAGES;
+  uint64_t* s_full = bars + 2 * Cfg::STAGES;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_full = p_full + 2;
+  uint64_t* q_full = pv_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x % a.Hkv;
+  const int pair = a.n_pairs - 1 - blockIdx.x / a.Hkv;  // heaviest pairs first (LPT)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 12);
+      mbar_init(&pv_full[i], 1);
+    }
+    mbar_init(q_full, 24);
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
+  const int last_tok = min((2 * pair + 2) * a.T, a.n_q) - 1;
+  const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
+
+  if (warp == TMA_WARP) {
+    if (elect_one()) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
+      for (int j = 0; j < n_kv_tiles; ++j) {
+        const int st = j % Cfg::STAGES;
+        mbar_wait(&kv_empty[st], ((uint32_t)(j / Cfg::STAGES) & 1) ^ 1);
+        uint8_t* sk = sKV + st * 2 * Cfg::KV_BYTES;
+        uint8_t* sv = sk + Cfg::KV_BYTES;
+        const int row = (int)(head_row + (long)a.page_table[j] * 128);
+        mbar_expect_tx(&kv_full[st], 2 * Cfg::KV_BYTES);
+#pragma unroll
+        for (int at = 0; at < Cfg::ATOMS; ++at) {
+          tma_load_2d(sk + at * 16384, &tmK, &kv_full[st], at * 64, row);
+          tma_load_2d(sv + at * 16384, &tmV, &kv_full[st], at * 64, row);
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(128, 128);
+    constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint32_t q_addr = smem_u32(sQ);
+    auto issue_s = [&](int t, int j) {
+      const uint32_t k_addr = smem_u32(sKV + (j % Cfg::STAGES) * 2 * Cfg::KV_BYTES);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < DKP / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                    sdesc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {  // P of keys 16kk.. sits in its slice's S columns
+      const uint32_t v_addr = smem_u32(sKV + (j % Cfg::STAGES) * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t pcol = kk < 3 ? kk * 8 : (kk < 6 ? 48 + (kk - 3) * 8 : 96 + (kk - 6) * 8);
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + pcol,
+                       sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&pv_full[t]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(&kv_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int j = 0; j < n_kv_tiles; ++j) {
+      const bool more = j + 1 < n_kv_tiles;
+      mbar_wait(&p_full[0], (uint32_t)j & 1);
+      tc_fence_after();
+      issue_pv(0, j);
+      if (more) {
+        mbar_wait(&kv_full[(j + 1) % Cfg::STAGES], (uint32_t)((j + 1) / Cfg::STAGES) & 1);
+        tc_fence_after();
+        issue_s(0, j + 1);
+      }
+      mbar_wait(&p_full[1], (uint32_t)j & 1);
+      tc_fence_after();
+      issue_pv(1, j);
+      if (elect_one()) umma_commit(&kv_empty[j % Cfg::STAGES]);
+      __syncwarp();
+      if (more) issue_s(1, j + 1);
+    }
+  } else {
+    const int t = warp / 12;
+    const int idx = warp - t * 12;
+    const int quarter = idx & 3;  // == warp % 4 (TMEM lane quarter rule)
+    const int c3 = idx >> 2;      // key-column slice 0..2
+    const int col0 = c3 * 48;
+    const int r = quarter * 32 + lane;
+    const int bar_id = 1 + t * 4 + quarter;  // the three slices of these 32 rows
+    const int b = 2 * pair + t;
+    const int hj = r / a.T;
+    const int ti = r - hj * a.T;
+    const int tok = b * a.T + ti;
+    const bool valid = hj < a.G && tok < a.n_q && b < a.n_tiles;
+    const int head = g * a.G + hj;
+    const int tile_last = min((b + 1) * a.T, a.n_q) - 1;
+    const int min_pos = b < a.n_tiles ? a.pos[b * a.T] : 0x7fffffff;
+    const int my_pos = valid ? a.pos[tok] : (b < a.n_tiles ? a.pos[tile_last] : 0x7fffffff);
+    const uint32_t lb = (uint32_t)((quarter * 32) << 16);
+    const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
+    const float sl2 = a.scale_log2;
+
+    if (c3 < Cfg::ATOMS) {  // Q row atom c3 -> smem (128B-swizzled K-major)
+      uint4 v[8];
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) + c3 * 8;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int ch = c ^ (r & 7);
+        *reinterpret_cast<uint4*>(sQ + t * Cfg::Q_BYTES + c3 * 16384 + r * 128 + ch * 16) = v[c];
+      }
+      fence_proxy_async_smem();
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_full);
+
+    float m_run = -INFINITY, l_run = 0.f;
+    float* red = reinterpret_cast<float*>(sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES + 256);  // [2][2 tiles][3][128]
+
+    auto page = [&](int j, auto WC) {
+      constexpr int W = decltype(WC)::value;  // keys of this slice
+      const int key0 = j * 128 + col0;
+      float sv[W];
+      {
+        uint32_t u[W];
+#pragma unroll
+        for (int c = 0; c < W / 16; ++c) tmem_ld16(tS + lb + col0 + c * 16, u + c * 16);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < W; ++i) sv[i] = __uint_as_float(u[i]);
+      }
+      if (key0 + W - 1 > min_pos) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) sv[i] = (key0 + i <= my_pos) ? sv[i] : -INFINITY;
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < W; i += 8)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(sv[i + 2 * q], sv[i + 2 * q + 1]));
+      const float hmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      float* rb = red + ((j & 1) * 2 + t) * 384;
+      rb[c3 * 128 + r] = hmax;
+      named_bar_sync(bar_id, 96);
+      const float tmax = fmaxf(fmaxf(rb[r], rb[128 + r]), rb[256 + r]);
+      const float m_new = fmaxf(m_run, tmax * sl2);
+      const bool grow = (m_new - m_run) > 8.0f;
+      const float m_use = grow ? m_new : m_run;
+      const uint64_t sl2x2 = f32x2(sl2, sl2), negm = f32x2(-m_use, -m_use);
+      uint64_t rsum2 = f32x2(0.f, 0.f), rsum2b = f32x2(0.f, 0.f);
+      uint32_t pk[W / 2];
+#pragma unroll
+      for (int i = 0; i < W / 2; ++i) {
+        const uint64_t x = ffma2(f32x2(sv[2 * i], sv[2 * i + 1]), sl2x2, negm);
+        float x0, x1;
+        f32x2_unpack(x, x0, x1);
+        float p0, p1;
+        constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+        if ((kPolyMask >> (i & 7)) & 1u) {
+          p0 = exp2_poly(x0);
+          p1 = exp2_poly(x1);
+        } else {
+          p0 = ex2(x0);
+          p1 = ex2(x1);
+        }
+        if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
+        else rsum2 = fadd2(rsum2, f32x2(p0, p1));
+        pk[i] = pack_bf16(p0, p1);
+      }
+      // P of this slice -> its own S columns [col0, col0 + W/2) (no other slice reads them)
+      tmem_st16p(tS + lb + col0, pk);
+      if constexpr (W / 2 > 16) tmem_st8(tS + lb + col0 + 16, pk + 16);
+      float rs0, rs1;
+      f32x2_unpack(fadd2(rsum2, rsum2b), rs0, rs1);
+      if (__any_sync(0xffffffffu, grow && j > 0)) {
+        const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < W / 16; ++c) {
+          uint32_t u[16];
+          tmem_ld16(tO + lb + col0 + c * 16, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st16p(tO + lb + col0 + c * 16, u);
+        }
+      }
+      if (grow && j > 0) l_run *= ex2(m_run - m_use);
+      if (grow) m_run = m_use;
+      l_run += rs0 + rs1;
+    };
+
+    for (int j = 0; j < n_kv_tiles; ++j) {
+      mbar_wait(&s_full[t], (uint32_t)j & 1);
+      tc_fence_after();
+      if (c3 < 2) page(j, std::integral_constant<int, 48>{});
+      else page(j, std::integral_constant<int, 32>{});
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
+    tc_fence_after();
+    float* lred = reinterpret_cast<float*>(sQ + t * Cfg::Q_BYTES);
+    lred[c3 * 128 + r] = l_run;
+    named_bar_sync(bar_id, 96);
+    const float inv_l = 1.f / ((lred[r] + lred[128 + r]) + lred[256 + r]);
+    const int W = c3 < 2 ? 48 : 32;
+#pragma unroll 1
+    for (int c = 0; c < W / 16; ++c) {
+      uint32_t u[16];
+      tmem_ld16(tO + lb + col0 + c * 16, u);
+      tmem_ld_wait();
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + col0 + c * 16);
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          dst[i] = make_uint4(pack_bf16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
+                              pack_bf16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
+                              pack_bf16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
+                              pack_bf16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 template <int DKP, int POLY>
 static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
@@ -419,6 +697,21 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
     return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
   const char* env = getenv("PKV_ATTN_POLY");  // tuning override: exponentials on the FMA pipe per 8
   const int poly = env ? atoi(env) : 1;
+  static const int split = getenv("PKV_ATTN_SPLIT") ? atoi(getenv("PKV_ATTN_SPLIT")) : 2;
+  if (dkp == 128 && split == 3) {
+    using Cfg = AttnCfg<128>;
+    constexpr int smem3 = Cfg::SMEM + 2048;  // 3-slice max exchange
+    static std::once_flag once3;
+    static cudaError_t err3 = cudaSuccess;
+    std::call_once(once3, [] {
+      err3 = cudaFuncSetAttribute(attn_tc3_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    });
+    if (err3 != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn3 smem attr: %s", cudaGetErrorString(err3));
+    launch_k(attn_tc3_kernel<1>, a.n_pairs * a.Hkv, 832, smem3, stream, tk, tv, a);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("attn_tc3_kernel");
+    return PKV_OK;
+  }
   if (dkp == 128) {
     if (poly == 1) return launch_attn<128, 1>(tk, tv, a, stream);
     if (poly < 0) return launch_attn<128, -1>(tk, tv, a, stream);
