@@ -85,3 +85,28 @@ def test_top_k_and_budget_match(pikv):
         assert top_k_indices(v, k) == O.topk_ascending(v, k)
         p = float(rng.random())
         assert ratio_budget(p, n) == O.budget(p, n)
+
+
+@pytest.mark.parametrize("ci", range(len(CFGS)))
+def test_decode_and_full_prefill_bit_identical(pikv, ci):
+    """The oracle's teacher-forced decode (used by tests/test_gpu_decode.py) and prefill
+    reproduce the reference's decode_step / full_prefill bit for bit."""
+    cfg_r = pikv.ModelConfig(**CFGS[ci])
+    cfg_o = O.Cfg(**cfg_r.to_json_dict())
+    wr, wo = pikv.random_weights(cfg_r, 5 + ci), O.init_weights(cfg_o, 5 + ci)
+    rng = np.random.default_rng(ci)
+    toks = rng.integers(0, cfg_r.vocab_size, 9).tolist()
+    tr = pikv.full_prefill(wr, cfg_r, toks)
+    to = O.prefill(wo, cfg_o, toks)
+    assert np.array_equal(tr.logits, to.logits)
+    for li in range(cfg_r.n_layers):
+        assert np.array_equal(tr.keys[li], to.keys[li]) and np.array_equal(tr.values[li], to.values[li])
+    cache = pikv.KVCache.from_prefill(tr)
+    steps = [3, 1, 4]
+    ref = []
+    for i, t in enumerate(steps):
+        lg, cache = pikv.decode_step(wr, cfg_r, cache, t, len(toks) + i)
+        ref.append(lg)
+    got = O.decode(wo, cfg_o, list(zip(to.keys, to.values)), np.arange(len(toks)), steps)
+    for a, b in zip(ref, got):
+        assert np.array_equal(a, b)
