@@ -85,6 +85,55 @@ __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const floa
   }
 }
 
+// narrow-pass rows -> the 3 bf16 planes of the next projection's B operand only: one
+// 256-thread CTA per plane row (32 rows; rows >= m zero-filled), the row in registers as
+// float4 vectors, one f64 block reduction, 8-byte plane stores
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_x3_kernel(const float* __restrict__ h, int m, int D, long ld,
+                                                         const float* __restrict__ gain, double eps,
+                                                         __nv_bfloat16* __restrict__ x3, long ldx) {
+  pdl_entry();
+  const int i = blockIdx.x;
+  const int nvec = (int)(ld >> 2);
+  float4 v[NV];
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = j * 256 + threadIdx.x;
+    v[j] = (i < m && c < nvec) ? __ldg(reinterpret_cast<const float4*>(h + (long)i * ld) + c)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc += (double)v[j].x * v[j].x + (double)v[j].y * v[j].y + (double)v[j].z * v[j].z + (double)v[j].w * v[j].w;
+  }
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double tot = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const double inv = 1.0 / sqrt(tot / (double)D + eps);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c = j * 256 + threadIdx.x;
+    if (c >= nvec) continue;
+    const float4 g = __ldg(g4 + c);
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    if (i < m) {
+      o[0] = (4 * c + 0 < D) ? (float)((double)v[j].x * inv * (double)g.x) : 0.f;
+      o[1] = (4 * c + 1 < D) ? (float)((double)v[j].y * inv * (double)g.y) : 0.f;
+      o[2] = (4 * c + 2 < D) ? (float)((double)v[j].z * inv * (double)g.z) : 0.f;
+      o[3] = (4 * c + 3 < D) ? (float)((double)v[j].w * inv * (double)g.w) : 0.f;
+    }
+    uint32_t h0, m0, l0, h1, m1, l1;
+    split3_pack(o[0], o[1], h0, m0, l0);
+    split3_pack(o[2], o[3], h1, m1, l1);
+    *reinterpret_cast<uint2*>(x3 + (long)i * ldx + 4 * c) = make_uint2(h0, h1);
+    *reinterpret_cast<uint2*>(x3 + (long)(32 + i) * ldx + 4 * c) = make_uint2(m0, m1);
+    *reinterpret_cast<uint2*>(x3 + (long)(64 + i) * ldx + 4 * c) = make_uint2(l0, l1);
+  }
+}
+
 // Stage-II rows (bf16 GEMM operand only): one 128-thread CTA per row, the row held in
 // registers as float4 vectors (one coalesced read of h), f64 sum of squares as above
 template <int NV>
@@ -140,6 +189,17 @@ int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, dou
   }
   int rows = x3 ? 32 : m;
   if (x3 && ld > ldx) return set_error(PKV_ERR_SHAPE, "rmsnorm: plane width %ld < row width %ld", ldx, ld);
+  if (x3 && !y && !ybf && m <= 32 && ld % 4 == 0 && ldx % 4 == 0 && ld <= 256 * 4 * 8) {
+    const int nv = ceil_div(ld / 4, 256);
+    auto* o = reinterpret_cast<__nv_bfloat16*>(x3);
+    if (nv <= 1) launch_k(rmsnorm_x3_kernel<1>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
+    else if (nv <= 2) launch_k(rmsnorm_x3_kernel<2>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
+    else if (nv <= 4) launch_k(rmsnorm_x3_kernel<4>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
+    else launch_k(rmsnorm_x3_kernel<8>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("rmsnorm_x3_kernel");
+    return PKV_OK;
+  }
   const int chunks = x3 ? std::max(1, std::min(8, (int)(ld / 512))) : 1;
   if (rows <= 0) return PKV_OK;
   launch_k(rmsnorm_kernel, dim3(rows, chunks), 256, 0, st, h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
@@ -556,6 +616,98 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
   }
 }
 
+// Combine fused with the m fresh query keys (keys s..s+m-1, fp32 K/V, causal within the
+// query) when the context keys ran on the tensor cores: each CTA (row r, KV head g) scores
+// its row against the fresh keys itself (a 32 x dk dot product set) instead of a separate
+// SIMT split kernel, then merges them with the split partials exactly like a split.
+__global__ void s1_attn_combine_fresh(const float* Opart, const float* Mpart, const float* Lpart, int splits,
+                                      int Hkv, int R, int m, int G, int H, int dkp, const float* __restrict__ q,
+                                      const float* __restrict__ fk, const float* __restrict__ fv, float scale,
+                                      float* out, float* Mfin, float* Lfin, __nv_bfloat16* x3, long ldx) {
+  pdl_entry();
+  extern __shared__ float shc[];  // wsp[splits] | sS[m] (scores, then probabilities) | sV[m][dkp]
+  float* wsp = shc;
+  float* sS = shc + splits;
+  float* sV = sS + m;
+  __shared__ float sM, sL, sWf;
+  const int r = blockIdx.x, g = blockIdx.y;
+  const int j = r / m, i = r - j * m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* qr = q + ((long)i * H + g * G + j) * dkp;
+  for (int e = threadIdx.x; e < m * dkp; e += blockDim.x) {  // the fresh values of head g -> smem
+    const int kk = e / dkp, d = e - kk * dkp;
+    sV[e] = fv[((long)kk * Hkv + g) * dkp + d];
+  }
+  for (int kk = warp; kk < m; kk += (int)(blockDim.x >> 5)) {  // S = f32(q.k) * scale, causal
+    const float* kr = fk + ((long)kk * Hkv + g) * dkp;
+    float part = 0.f;
+    for (int d = lane; d < dkp; d += 32) part = fmaf(qr[d], kr[d], part);
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) sS[kk] = kk <= i ? part * scale : -INFINITY;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float mf = -INFINITY;
+    for (int kk = lane; kk < m; kk += 32) mf = fmaxf(mf, sS[kk]);
+    for (int o = 16; o > 0; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+    float M = mf;  // finite: key 0 of the query is always visible
+    for (int sp = lane; sp < splits; sp += 32) M = fmaxf(M, Mpart[((long)sp * Hkv + g) * R + r]);
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f, lf = 0.f;
+    for (int sp = lane; sp < splits; sp += 32) {
+      const long b = ((long)sp * Hkv + g) * R + r;
+      const float w = Mpart[b] != -INFINITY ? expf(Mpart[b] - M) : 0.f;
+      wsp[sp] = w;
+      L += Lpart[b] * w;
+    }
+    for (int kk = lane; kk < m; kk += 32) {
+      const float p = sS[kk] == -INFINITY ? 0.f : expf(sS[kk] - mf);
+      sS[kk] = p;
+      lf += p;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      L += __shfl_xor_sync(0xffffffffu, L, o);
+      lf += __shfl_xor_sync(0xffffffffu, lf, o);
+    }
+    if (lane == 0) {
+      const float wf = expf(mf - M);
+      sM = M;
+      sL = L + lf * wf;
+      sWf = wf;
+    }
+  }
+  __syncthreads();
+  const float M = sM, L = sL, wf = sWf;
+  for (int d = threadIdx.x; d < dkp; d += blockDim.x) {
+    float acc = 0.f;
+    const float* op = Opart + ((long)g * R + r) * dkp + d;
+    const long sstride = (long)Hkv * R * dkp;
+#pragma unroll 8
+    for (int sp = 0; sp < splits; ++sp) {
+      const float w = wsp[sp];
+      const float v = __ldg(op + sp * sstride);
+      acc = w != 0.f ? fmaf(v, w, acc) : acc;
+    }
+    float of = 0.f;  // fresh keys' P.V, as its own split
+    for (int kk = 0; kk <= i && kk < m; ++kk) of = fmaf(sS[kk], sV[kk * dkp + d], of);
+    acc = fmaf(of, wf, acc);
+    const float o = acc / L;
+    const long col = (long)(g * G + j) * dkp + d;
+    out[(long)i * H * dkp + col] = o;
+    if (x3 != nullptr) {
+      __nv_bfloat16 p, qq, rr;
+      split3(o, p, qq, rr);
+      x3[(long)i * ldx + col] = p;
+      x3[(long)(32 + i) * ldx + col] = qq;
+      x3[(long)(64 + i) * ldx + col] = rr;
+    }
+  }
+  if (threadIdx.x == 0 && Mfin != nullptr) {
+    Mfin[(long)g * R + r] = M;
+    Lfin[(long)g * R + r] = L;
+  }
+}
+
 // Scores of one layer from the key-major S [Hkv][s][R] (model.py:294, 303-307 and
 // selection.py:79-86):
 //   rows[i][t]      = f32( sum_h f64(p_{h,i,t}) / H ),  p = exp(S - M) / L
@@ -698,6 +850,8 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   S1Attn a = a_in;
   const int row_blocks = ceil_div(a.R, 128);
   int total_splits = a.n_splits;
+  const size_t fresh_smem = (a.tc_splits + a.m + (size_t)a.m * a.dkp) * sizeof(float);
+  bool combined = false;
   if (a.tc_splits > 0) {
     // context keys [0, s) on the tensor cores (3-way bf16 split, fp32-faithful)
     S1TcArgs t{};
@@ -723,13 +877,31 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.Lpart = a.Lpart;
     int rc = s1_attn_tc_launch(t, a.k1_all, a.k2_all, a.k3_all, a.v_all, a.pool_rows_total, a.dkp, st);
     if (rc) return rc;
-    // the m fresh query keys (fp32 K/V) on the SIMT path as one extra split
-    a.key_base = a.s;
-    a.keys_per_split = a.m;
-    a.n_splits = 1;
-    a.split_base = a.tc_splits;
-    total_splits = a.tc_splits + 1;
+    // fused fresh keys + combine: measured neutral (each CTA re-reads the head's fresh V),
+    // so opt-in (PKV_FRESH_FUSED=1)
+    static const bool fused_fresh = getenv("PKV_FRESH_FUSED") && getenv("PKV_FRESH_FUSED")[0] == '1';
+    if (fused_fresh && fresh_smem <= 160 * 1024) {
+      // the m fresh query keys are merged inside the combine (one kernel instead of a
+      // SIMT split + combine)
+      static std::once_flag once_fresh;
+      std::call_once(once_fresh, [] {
+        cudaFuncSetAttribute(s1_attn_combine_fresh, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      });
+      launch_k(s1_attn_combine_fresh, dim3(a.R, a.Hkv), 128, fresh_smem, st, a.Opart, a.Mpart, a.Lpart,
+               a.tc_splits, a.Hkv, a.R, a.m, a.G, a.H, a.dkp, a.q, a.fk, a.fv, a.scale, attn_out, Mfin, Lfin,
+               reinterpret_cast<__nv_bfloat16*>(a.x3_out), a.x3_ld);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_attn_combine_fresh");
+      combined = true;
+    } else {  // long queries: the fresh keys as one extra SIMT split
+      a.key_base = a.s;
+      a.keys_per_split = a.m;
+      a.n_splits = 1;
+      a.split_base = a.tc_splits;
+      total_splits = a.tc_splits + 1;
+    }
   }
+  if (!combined) {
   // short fresh-key split: 32-row CTAs (4x the parallelism); long SIMT ranges: 128 rows
   const bool small = a.tc_splits > 0;
   const int rows_per_cta = small ? 32 : 128;
@@ -761,6 +933,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
                                                     reinterpret_cast<__nv_bfloat16*>(a.x3_out), a.x3_ld);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
+  }
   if (a.S != nullptr && per_layer != nullptr) {
     const int sgrid = std::min(ceil_div(a.s, 8), 8 * num_sms());
     const size_t ssmem = (size_t)a.Hkv * a.R * sizeof(float2);
