@@ -364,27 +364,36 @@ def assemble(chunks, config: ModelConfig, track_access: bool = False, *, fp32_ta
         _lib.check(lib.pkv_assemble(ctypes_ref(cache._cfg_c), ctypes_ref(cache._c_chunks),
                                     ctypes_ref(cache._c_cache), _lib.stream_ptr(torch, stream)))
         return cache
-    # host-tier chunks: stream them layer by layer on a copy stream and assemble each
-    # layer as soon as it lands; query passes / Stage II wait per layer on its event
+    # host-tier chunks: stream them layer by layer -- keys and values on two copy streams
+    # (two DMA engines, never stalled behind a kernel) -- and assemble each layer on a
+    # third stream as soon as both halves land; query passes / Stage II wait per layer
     main = stream or torch.cuda.current_stream()
-    cs = torch.cuda.Stream()
-    cs.wait_stream(main)  # pools and buffers were allocated / zeroed on `main`
+    cs, ck, cv = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    for st_ in (cs, ck, cv):
+        st_.wait_stream(main)  # pools and buffers were allocated / zeroed on `main`
     events = []
-    with torch.cuda.stream(cs):
-        for li in range(config.n_layers):
+    for li in range(config.n_layers):
+        ek, evv = torch.cuda.Event(), torch.cuda.Event()
+        with torch.cuda.stream(ck):
             for c in pending:
-                kp, vp = c._pinned
-                c._k_dev[li].copy_(kp[li], non_blocking=True)
-                c._v_dev[li].copy_(vp[li], non_blocking=True)
-            _lib.check(lib.pkv_assemble_layers(ctypes_ref(cache._cfg_c), ctypes_ref(cache._c_chunks),
-                                               ctypes_ref(cache._c_cache), li, li + 1, cs.cuda_stream))
-            ev = torch.cuda.Event()
-            ev.record(cs)
-            events.append(ev)
+                c._k_dev[li].copy_(c._pinned[0][li], non_blocking=True)
+            ek.record(ck)
+        with torch.cuda.stream(cv):
+            for c in pending:
+                c._v_dev[li].copy_(c._pinned[1][li], non_blocking=True)
+            evv.record(cv)
+        cs.wait_event(ek)
+        cs.wait_event(evv)
+        _lib.check(lib.pkv_assemble_layers(ctypes_ref(cache._cfg_c), ctypes_ref(cache._c_chunks),
+                                           ctypes_ref(cache._c_cache), li, li + 1, cs.cuda_stream))
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        events.append(ev)
     cache._pinned_refs = [c._pinned for c in pending]  # host buffers stay alive until the DMA is done
     for c in pending:
-        c._k_dev.record_stream(cs)
-        c._v_dev.record_stream(cs)
+        for st_ in (cs, ck, cv):
+            c._k_dev.record_stream(st_)
+            c._v_dev.record_stream(st_)
         c._pinned = None
     for t in (cache.k_pool, cache.v_pool, cache.k2_pool, cache.k3_pool, cache._d_recomp):
         t.record_stream(cs)
