@@ -224,7 +224,8 @@ int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_
 /* fp32-faithful narrow projection (the query passes' x.W of model.py:265-275 / 311-323):
  * out[i][n] (+)= sum_k x[i][k] W[n][k] for m <= 32 fp32 rows given as 3 bf16 planes
  * x3 [96][ldx] (rows i, 32+i, 64+i); W [N][K] bf16; part >= 16*ceil(N/128)*128*32 floats,
- * cnt >= ceil(N/128) zeroed ints; n_splits <= 0: the split-K heuristic. */
+ * cnt >= ceil(N/128) zeroed ints; n_splits > 0: split-K, 0: stream-K (default grid),
+ * < 0: stream-K on a grid of -n_splits CTAs. */
 int pkv_proj_narrow(const void* W, int32_t N, int32_t K, const void* x3, int64_t ldx, int32_t m, float* out,
                     int64_t ldo, int32_t resid, float* part, int32_t* cnt, int32_t n_splits, void* stream);
 int pkv_attention_sparse(const pkv_model* m, const pkv_cache* cache, int32_t layer, const void* q, void* out,

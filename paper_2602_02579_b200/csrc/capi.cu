@@ -213,8 +213,10 @@ static int proj_fused(const void* W, int N, int K, int m, float* out, long ldo, 
   GemmArgs g{};
   g.M = N;
   g.N = 96;
-  const int sp = choose_splits(N, K);
-  g.n_splits = sp;
+  // stream-K (balanced k ranges over the whole grid) unless a split count is forced
+  static const bool forced = getenv("PKV_PROJ_SPLITS") != nullptr;
+  g.stream_k = forced ? 0 : 1;
+  g.n_splits = forced ? choose_splits(N, K) : 1;
   g.k_tiles_per_split = 0;  // gemm_tc_launch splits the k range evenly
   g.out = out;
   g.ldo = ldo;
@@ -798,8 +800,10 @@ int pkv_proj_narrow(const void* W, int32_t N, int32_t K, const void* x3, int64_t
   GemmArgs g{};
   g.M = N;
   g.N = 96;
-  const int sp = n_splits > 0 ? std::min(n_splits, 16) : choose_splits(N, K);
-  g.n_splits = sp;
+  // n_splits > 0: split-K with that many splits; 0: stream-K on the default grid;
+  // < 0: stream-K on a grid of -n_splits CTAs (tuning)
+  g.stream_k = n_splits > 0 ? 0 : (n_splits < 0 ? -n_splits : 1);
+  g.n_splits = n_splits > 0 ? std::min(n_splits, 16) : 1;
   g.k_tiles_per_split = 0;  // gemm_tc_launch splits the k range evenly
   g.out = out;
   g.ldo = ldo;

@@ -194,6 +194,11 @@ __device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
       : "memory");
 }
 // arrive on the same-offset mbarrier of CTA `rank` of the cluster
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"

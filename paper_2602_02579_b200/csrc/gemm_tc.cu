@@ -108,6 +108,7 @@ static int launch_one(const CUtensorMap& ta, const CUtensorMap& tb, const GemmAr
     return PKV_OK;
   }
   int grid = (int)std::min<long>(tiles, num_sms());
+  if (EPI == EPI_PROJ && CG == 1 && args.stream_k) grid = args.stream_k;  // stream-K grid (see gemm_tc_launch)
   launch_k(gemm_tc_kernel<BN, EPI, CG>, grid, 192, Cfg::SMEM, stream, ta, tb, args);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("gemm_tc_kernel");
@@ -146,6 +147,21 @@ static int launch_proj_cluster(const CUtensorMap& ta, const CUtensorMap& tb, con
   return PKV_OK;
 }
 
+// Debug: PKV_GEMM_TRACE=1 makes the narrow projection stamp %globaltimer per CTA
+// (kernel entry, prologue done, accumulator ready, partial stored, counter acquired,
+// reduced, written) into a static buffer read back by pkv_debug_gemm_trace.
+static unsigned long long* g_trace = nullptr;
+static constexpr int kTraceCtas = 1024;
+static unsigned long long* gemm_trace_buffer() {
+  static const bool on = getenv("PKV_GEMM_TRACE") && getenv("PKV_GEMM_TRACE")[0] == '1';
+  if (!on) return nullptr;
+  if (g_trace == nullptr) {
+    if (cudaMalloc(&g_trace, kTraceCtas * 8 * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    cudaMemset(g_trace, 0, kTraceCtas * 8 * sizeof(unsigned long long));
+  }
+  return g_trace;
+}
+
 // A: [M][K] bf16 (row stride lda elements), B: [N][K] bf16 (row stride ldb).
 int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long ldb, int K, GemmArgs args,
                    cudaStream_t stream) {
@@ -158,6 +174,21 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   if (args.n_splits <= 0) args.n_splits = 1;
   if (args.k_tiles_per_split <= 0) args.k_tiles_per_split = ceil_div(kt, args.n_splits);
   args.n_splits = ceil_div(kt, args.k_tiles_per_split);  // no empty splits
+  if (epi == EPI_PROJ) args.trace = gemm_trace_buffer();
+  if (epi == EPI_PROJ && args.stream_k) {
+    // stream-K grid G (stream_k > 1: requested G): every CTA gets >= 1 unit and an m-tile is cut into <= 16 pieces
+    // (the partial buffer holds 16 per tile).  PKV_PROJ_SK_GRID overrides (tuning).
+    const long units = (long)ceil_div(args.M, 128) * kt;
+    static const int g_env = getenv("PKV_PROJ_SK_GRID") ? atoi(getenv("PKV_PROJ_SK_GRID")) : 0;
+    // 128 CTAs measured best on B200 for all four Llama-8B shapes (tools/bench_proj.py:
+    // 101 us per layer vs 107 on all 148 SMs and 127 for the old split-K cost model)
+    long g = args.stream_k > 1 ? args.stream_k : (g_env > 0 ? g_env : std::min(128, num_sms()));
+    g = std::min(g, units);
+    g = std::min(g, 15L * ceil_div(args.M, 128));
+    args.stream_k = (int)std::max(1L, g);
+    args.n_splits = 1;
+    args.k_tiles_per_split = kt;
+  }
   CUtensorMap ta, tb;
   // Stage-II GEMMs (BN = 256) on CTA pairs unless PKV_GEMM_CG=1
   static const int cg_env = getenv("PKV_GEMM_CG") ? atoi(getenv("PKV_GEMM_CG")) : 2;
@@ -197,3 +228,12 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
 }
 
 }  // namespace pkv
+
+extern "C" int pkv_debug_gemm_trace(unsigned long long* host, int n_ctas) {
+  if (pkv::g_trace == nullptr) return -1;
+  const int n = n_ctas < pkv::kTraceCtas ? n_ctas : pkv::kTraceCtas;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, pkv::g_trace, (size_t)n * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  cudaMemset(pkv::g_trace, 0, pkv::kTraceCtas * 8 * sizeof(unsigned long long));
+  return 0;
+}

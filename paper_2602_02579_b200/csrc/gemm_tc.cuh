@@ -54,7 +54,17 @@ struct GemmArgs {
   int resid;                  // 1: out += y
   float* part;                // split-K partials [n_splits][tiles_m*128][32]
   int* cnt;                   // [tiles_m] arrival counters (zero; reset by the reducing CTA)
+  unsigned long long* trace;  // debug (PKV_GEMM_TRACE=1): per-CTA globaltimer stamps [grid][8]
+  int stream_k;               // EPI_PROJ: 1 = stream-K (CTA c owns k units [c*U/G, (c+1)*U/G))
 };
+
+__device__ __forceinline__ void gemm_stamp(const GemmArgs& a, int i) {
+  if (a.trace != nullptr) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 8 + i] = t;
+  }
+}
 
 // BK = k extent of one pipeline stage (SW128 atoms of 64 bf16); MT = 128-row sub-tiles of
 // A per CTA tile sharing each B tile (EPI_PROJ only).  Measured on the narrow-pass
@@ -115,6 +125,7 @@ __global__ void __launch_bounds__(192, 1)
     cta_id = (int)(blockIdx.x / args.n_splits) + tiles_m_ * (int)rank;
     n_ctas = 1 << 30;
   }
+  if (threadIdx.x == 64) gemm_stamp(args, 0);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
@@ -158,6 +169,7 @@ __global__ void __launch_bounds__(192, 1)
   // PDL: the prologue above overlapped the previous kernel; from here on we read its outputs
   griddep_wait();
   griddep_launch();
+  if (threadIdx.x == 64) gemm_stamp(args, 1);
 
   auto tile_coords = [&](int t, int& mb, int& nb, int& sp) {
     mb = t % tiles_m;
@@ -166,16 +178,58 @@ __global__ void __launch_bounds__(192, 1)
     sp = r / tiles_n;
   };
 
+  // Work items.  Tile mode: tile t = (m, n, split) strided over the grid.  Stream-K
+  // (narrow projection): the U = tiles_m * k_tiles units (m-tile, 64-deep k step) are cut
+  // into G equal contiguous ranges, one per CTA; a range covers the tail of one m-tile,
+  // whole tiles and the head of another.  Piece idx of an m-tile is its idx-th owner, so
+  // the split points -- and the fixed-order sum of the pieces -- depend only on (U, G).
+  struct Work { int mb, nb, k0, k1, idx, nseg; };
+  const bool sk = (EPI == EPI_PROJ && CG == 1 && CK == 0) && args.stream_k;
+  const long U = (long)tiles_m * k_tiles_total;
+  auto sk_start = [&](int c) -> long { return (long)c * U / n_ctas; };
+  auto sk_owner = [&](long u) -> int {
+    int c = (int)((u * n_ctas) / U);
+    if (c >= n_ctas) c = n_ctas - 1;
+    while (c + 1 < n_ctas && sk_start(c + 1) <= u) ++c;
+    while (c > 0 && sk_start(c) > u) --c;
+    return c;
+  };
+  auto first_pos = [&]() -> long { return sk ? sk_start(cta_id) : (long)cta_id; };
+  auto next_work = [&](long& pos, Work& w) -> bool {
+    if (sk) {
+      const long u1 = sk_start(cta_id + 1);
+      if (pos >= u1) return false;
+      w.mb = (int)(pos / k_tiles_total);
+      w.nb = 0;
+      w.k0 = (int)(pos - (long)w.mb * k_tiles_total);
+      w.k1 = (int)min((long)k_tiles_total, (long)w.k0 + (u1 - pos));
+      const long tb = (long)w.mb * k_tiles_total;
+      const int o0 = sk_owner(tb);
+      w.idx = cta_id - o0;
+      w.nseg = sk_owner(tb + k_tiles_total - 1) - o0 + 1;
+      pos += w.k1 - w.k0;
+      return true;
+    }
+    if (pos >= total_tiles) return false;
+    int sp;
+    tile_coords((int)pos, w.mb, w.nb, sp);
+    w.k0 = sp * args.k_tiles_per_split;
+    w.k1 = min(w.k0 + args.k_tiles_per_split, k_tiles_total);
+    w.idx = sp;
+    w.nseg = args.n_splits;
+    pos += n_ctas;
+    return true;
+  };
+
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cta_id; t < total_tiles; t += n_ctas) {
-        int mb, nb, sp;
-        tile_coords(t, mb, nb, sp);
-        int k0 = sp * args.k_tiles_per_split;
-        int k1 = min(k0 + args.k_tiles_per_split, k_tiles_total);
-        const int nk = k1 - k0, rot = k_rotation(mb, nk);
+      long pos = first_pos();
+      Work w;
+      while (next_work(pos, w)) {
+        const int mb = w.mb, nb = w.nb, k0 = w.k0;
+        const int nk = w.k1 - k0, rot = k_rotation(mb, nk);
         for (int i = 0; i < nk; ++i) {
           const int kt = k0 + (i + rot) % nk;
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -211,11 +265,10 @@ __global__ void __launch_bounds__(192, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int t = cta_id; t < total_tiles; t += n_ctas, ++local) {
-      int mb, nb, sp;
-      tile_coords(t, mb, nb, sp);
-      int k0 = sp * args.k_tiles_per_split;
-      int k1 = min(k0 + args.k_tiles_per_split, k_tiles_total);
+    long pos = first_pos();
+    Work w;
+    for (; next_work(pos, w); ++local) {
+      const int k0 = w.k0, k1 = w.k1;
       const int acc = local & 1;
       const uint32_t use = (uint32_t)(local >> 1);
       mbar_wait(&tempty_bar[acc], (use & 1) ^ 1);
@@ -257,11 +310,24 @@ __global__ void __launch_bounds__(192, 1)
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = quarter * 32 + lane;
     int local = 0;
-    for (int t = cta_id; t < total_tiles; t += n_ctas, ++local) {
-      int mb, nb, sp;
-      tile_coords(t, mb, nb, sp);
+    long pos = first_pos();
+    Work w;
+    for (; next_work(pos, w); ++local) {
+      const int mb = w.mb, nb = w.nb;
       const int acc = local & 1;
       const uint32_t use = (uint32_t)(local >> 1);
+      // EPI_PROJ residual (out += y): a whole-tile item fetches out[.][n] while its MMAs
+      // run; a split tile's reducer fetches it with the pieces (one round trip either way)
+      [[maybe_unused]] float rres[32];
+      [[maybe_unused]] bool have_r = false;
+      if constexpr (EPI == EPI_PROJ && CG == 1 && Cfg::MT == 1) {
+        const int n = mb * Cfg::BM + (warp & 3) * 32 + lane;
+        if (args.resid && w.nseg == 1 && n < args.M) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rres[i] = i < args.mrows ? __ldcg(args.out + (long)i * args.ldo + n) : 0.f;
+          have_r = true;
+        }
+      }
       mbar_wait(&tfull_bar[acc], use & 1);
       tc_fence_after();
       const int row = mb * Cfg::BMT + (int)rank * Cfg::BM + row_in_tile;
@@ -270,6 +336,7 @@ __global__ void __launch_bounds__(192, 1)
 
       if constexpr (EPI == EPI_PROJ) {
        __shared__ int s_last;
+       if (threadIdx.x == 64) gemm_stamp(args, 2);
 #pragma unroll 1
        for (int j = 0; j < Cfg::MT; ++j) {
         // one thread = one output feature n; the 96 accumulator columns are the hi/mid/lo
@@ -282,54 +349,79 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(t_sub + 32, a1);
         tmem_ld32(t_sub + 64, a2);
         tmem_ld_wait();
+        if (CG == 1 && j == Cfg::MT - 1) {  // accumulator drained: the next item's MMAs may start
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        }
         float y[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           y[i] = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
         const int n = msub * Cfg::BM + row_in_tile;  // GEMM row == output feature
-        bool write = args.n_splits == 1;
+        bool write = w.nseg == 1;
         if constexpr (CK) {  // partial -> own smem (the pipeline ring is drained); reduced below
           float* xb = reinterpret_cast<float*>(smem) + row_in_tile * 33;
 #pragma unroll
           for (int i = 0; i < 32; ++i) xb[i] = y[i];
           write = false;
         } else if (!write) {
-          float* mine = args.part + ((long)(sp * subtiles_m + msub) * 128 + row_in_tile) * 32;
+          // partial piece, row-major [32 query rows][128 features]: coalesced stores/loads
+          float* mine = args.part + (long)(w.idx * subtiles_m + msub) * 4096 + row_in_tile;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(mine + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
-          __threadfence();
+          for (int i = 0; i < 32; ++i) __stcg(mine + i * 128, y[i]);
+          // release/acquire hand-off: the barrier orders the 128 threads' partial stores
+          // before thread 64's acq_rel atomic (cumulative), and the last CTA's reads after
+          // its acquire.  (__threadfence() here was a MEMBAR.SC.GPU + L1 invalidate per
+          // thread, several microseconds per launch.)
           named_bar_sync(1, 128);
-          if (threadIdx.x == 64) s_last = (atomicAdd(&args.cnt[msub], 1) == args.n_splits - 1) ? 1 : 0;
+          if (threadIdx.x == 64) gemm_stamp(args, 3);
+          if (threadIdx.x == 64) s_last = (atom_add_acq_rel_gpu(&args.cnt[msub], 1) == w.nseg - 1) ? 1 : 0;
           named_bar_sync(1, 128);
+          if (threadIdx.x == 64) gemm_stamp(args, 4);
           if (s_last) {
-            __threadfence();
-            // fixed split order -> bit-identical regardless of which CTA arrives last
-#pragma unroll 1
-            for (int s2 = 0; s2 < args.n_splits; ++s2) {
-              const float* p = args.part + ((long)(s2 * subtiles_m + msub) * 128 + row_in_tile) * 32;
+            // fixed piece order -> bit-identical regardless of which CTA arrives last;
+            // four pieces' loads in flight per round trip
+            if (CG == 1 && Cfg::MT == 1 && args.resid && n < args.M) {
 #pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                const float4 v = __ldcg(reinterpret_cast<const float4*>(p + i));
-                if (s2 == 0) {
-                  y[i] = v.x; y[i + 1] = v.y; y[i + 2] = v.z; y[i + 3] = v.w;
-                } else {
-                  y[i] += v.x; y[i + 1] += v.y; y[i + 2] += v.z; y[i + 3] += v.w;
+              for (int i = 0; i < 32; ++i) rres[i] = i < args.mrows ? __ldcg(args.out + (long)i * args.ldo + n) : 0.f;
+              have_r = true;
+            }
+#pragma unroll 1
+            for (int s0 = 0; s0 < w.nseg; s0 += 4) {
+              float v[4][32];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (s0 + q < w.nseg) {
+                  const float* p = args.part + (long)((s0 + q) * subtiles_m + msub) * 4096 + row_in_tile;
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) v[q][i] = __ldcg(p + i * 128);
+                }
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (s0 + q < w.nseg) {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) y[i] = (s0 + q == 0) ? v[q][i] : y[i] + v[q][i];
                 }
               }
             }
             if (threadIdx.x == 64) args.cnt[msub] = 0;
             write = true;
+            if (threadIdx.x == 64) gemm_stamp(args, 5);
           }
         }
         if (write && n < args.M) {
+          if (args.resid && !have_r) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) rres[i] = i < args.mrows ? __ldcg(args.out + (long)i * args.ldo + n) : 0.f;
+          }
 #pragma unroll
           for (int i = 0; i < 32; ++i) {  // constant indices keep y in registers
-            if (i < args.mrows) {
-              float* dst = args.out + (long)i * args.ldo + n;
-              *dst = args.resid ? *dst + y[i] : y[i];
-            }
+            if (i < args.mrows) args.out[(long)i * args.ldo + n] = args.resid ? rres[i] + y[i] : y[i];
           }
         }
+        if (threadIdx.x == 64) gemm_stamp(args, 6);
        }
       } else if constexpr (EPI == EPI_SILU) {
         // gate columns [0,BN/2), up columns [BN/2,BN) of this tile feed BN/2 outputs
@@ -366,7 +458,7 @@ __global__ void __launch_bounds__(192, 1)
           if (!row_ok || col0 >= args.N) continue;
           const bool full = col0 + 32 <= args.N && (args.ldc & 7) == 0;  // vector stores need aligned rows
           if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
-            float* dst = reinterpret_cast<float*>(args.C) + (long)sp * args.M * args.ldc + (long)row * args.ldc + col0;
+            float* dst = reinterpret_cast<float*>(args.C) + (long)w.idx * args.M * args.ldc + (long)row * args.ldc + col0;
             if (full) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
@@ -488,11 +580,13 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);  // the leader's MMA waits
-        else mbar_arrive(&tempty_bar[acc]);
+      if constexpr (EPI != EPI_PROJ || CG == 2) {  // (EPI_PROJ, CG = 1 released it above)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(&tempty_bar[acc], 0);  // the leader's MMA waits
+          else mbar_arrive(&tempty_bar[acc]);
+        }
       }
     }
   }
