@@ -607,6 +607,9 @@ int pkv_topk(const float* scores, int32_t n, int32_t k, int32_t* idx_out, int32_
 struct RcWs {
   float* h;
   __nv_bfloat16 *xb, *qb, *ab, *act;
+  float* sk_part;  // stream-K tail pieces of the Stage-II GEMMs (shared: they run in order)
+  int* sk_cnt;
+  size_t sk_cnt_n;
 };
 static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
@@ -616,6 +619,13 @@ static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   w.qb = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
   w.ab = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
   w.act = cv.take<__nv_bfloat16>((size_t)k * md->Fp);
+  const size_t skf = std::max(std::max(gemm_sk_ws_floats(k, md->NQKV, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->HQ)),
+                              std::max(gemm_sk_ws_floats(k, 2 * md->Fp, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->Fp)));
+  if (skf > 0) {
+    w.sk_cnt_n = (size_t)2 * (num_sms() / 2);
+    w.sk_cnt = cv.take<int>(w.sk_cnt_n);
+    w.sk_part = cv.take<float>(skf);
+  }
   *total = cv.off + 256;
   return w;
 }
@@ -643,6 +653,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
   pkv_comm* comm = md->comm;
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
   int rc;
+  if (w.sk_cnt) cudaMemsetAsync(w.sk_cnt, 0, w.sk_cnt_n * sizeof(int), st);
   if (c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
   TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
   for (int l = 0; l < cf.n_layers; ++l) {
@@ -652,6 +663,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
     TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
+    g.sk_part = w.sk_part;
+    g.sk_cnt = w.sk_cnt;
     g.M = k;
     g.N = md->NQKV;
     g.n_splits = 1;
@@ -683,6 +696,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
                        (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
     GemmArgs go{};
+    go.sk_part = w.sk_part;
+    go.sk_cnt = w.sk_cnt;
     go.M = k;
     go.N = Dp;
     go.n_splits = 1;
@@ -692,6 +707,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
     TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs gg{};
+    gg.sk_part = w.sk_part;
+    gg.sk_cnt = w.sk_cnt;
     gg.M = k;
     gg.N = 2 * Fp;
     gg.n_splits = 1;
@@ -699,6 +716,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     gg.ldc = Fp;
     TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
     GemmArgs gd{};
+    gd.sk_part = w.sk_part;
+    gd.sk_cnt = w.sk_cnt;
     gd.M = k;
     gd.N = Dp;
     gd.n_splits = 1;
@@ -790,6 +809,27 @@ int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_
   g.C = C;
   g.ldc = ldc;
   if (epi != EPI_F32 && epi != EPI_RESID && epi != EPI_BF16) return set_error(PKV_ERR_ARGUMENT, "epilogue");
+  // the stream-K tail needs piece storage: a per-device scratch grown on demand (unit
+  // tests / microbenchmarks only; the prefill path carves it from its workspace)
+  static float* sk_part[64] = {};
+  static int* sk_cnt[64] = {};
+  static size_t sk_cap[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const size_t need = gemm_sk_ws_floats(M, N, K);
+  if (need > 0 && dev < 64) {
+    if (need > sk_cap[dev]) {
+      if (sk_part[dev]) cudaFree(sk_part[dev]);
+      if (!sk_cnt[dev]) {
+        if (cudaMalloc(&sk_cnt[dev], 1024 * sizeof(int)) != cudaSuccess) return set_error(PKV_ERR_CUDA, "sk alloc");
+        cudaMemset(sk_cnt[dev], 0, 1024 * sizeof(int));
+      }
+      if (cudaMalloc(&sk_part[dev], need * sizeof(float)) != cudaSuccess) return set_error(PKV_ERR_CUDA, "sk alloc");
+      sk_cap[dev] = need;
+    }
+    g.sk_part = sk_part[dev];
+    g.sk_cnt = sk_cnt[dev];
+  }
   return gemm_tc_launch(epi, bn, A, lda, B, ldb, K, g, S(stream));
 }
 

@@ -162,6 +162,46 @@ static unsigned long long* gemm_trace_buffer() {
   return g_trace;
 }
 
+int gemm_sk_plan(int M, int N, int K, int* rem_out, int* maxp_out) {
+  // opt-in (PKV_GEMM_SK=1): correct and deterministic, but measured 2-4 % slower on the
+  // qkv / o shapes and neutral on gate_up / down (tools/bench_stage2_gemm.py): under the
+  // power cap a partial last wave runs at higher clocks, so the tail costs less than its
+  // tile count suggests, and the pieces lose the cross-pair B-tile sharing in L2
+  static const bool off = !(getenv("PKV_GEMM_SK") && getenv("PKV_GEMM_SK")[0] == '1');
+  *rem_out = 0;
+  *maxp_out = 0;
+  if (off || M <= 0 || N <= 0) return 0;
+  const int P = num_sms() / 2;
+  const long tiles = (long)ceil_div(M, 256) * ceil_div(N, 256);
+  const int kt = ceil_div(K, 64);
+  if (P <= 0 || tiles < P || kt < 8) return 0;
+  const int rem = (int)(tiles % P);
+  if (rem == 0) return 0;
+  const long U = (long)rem * kt;
+  // <= 4 tail tiles' worth of pairs per tile keeps pieces >= kt/4 deep
+  const int skp = (int)std::min<long>(P, std::min<long>(4L * rem, U));
+  auto start = [&](int c) { return (long)c * U / skp; };
+  auto owner = [&](long u) {
+    int c = (int)((u * skp) / U);
+    if (c >= skp) c = skp - 1;
+    while (c + 1 < skp && start(c + 1) <= u) ++c;
+    while (c > 0 && start(c) > u) --c;
+    return c;
+  };
+  int maxp = 0;
+  for (int sl = 0; sl < rem; ++sl) maxp = std::max(maxp, owner((long)sl * kt + kt - 1) - owner((long)sl * kt) + 1);
+  if (maxp > SK_MAXP) return 0;
+  *rem_out = rem;
+  *maxp_out = maxp;
+  return skp;
+}
+
+size_t gemm_sk_ws_floats(int M, int N, int K) {
+  int rem, maxp;
+  if (!gemm_sk_plan(M, N, K, &rem, &maxp)) return 0;
+  return (size_t)rem * maxp * 2 * 256 * 128;
+}
+
 // A: [M][K] bf16 (row stride lda elements), B: [N][K] bf16 (row stride ldb).
 int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long ldb, int K, GemmArgs args,
                    cudaStream_t stream) {
@@ -202,6 +242,12 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   static const bool proj_cluster = getenv("PKV_PROJ_CLUSTER") && getenv("PKV_PROJ_CLUSTER")[0] == '1';
   if (cg == 1 && bn == 96 && epi == EPI_PROJ && proj_cluster && args.n_splits >= 2 && args.n_splits <= 8)
     return launch_proj_cluster(ta, tb, args, stream);
+  args.sk_pairs = 0;
+  if (cg == 2 && epi != EPI_PROJ && bn == 256 && args.n_splits == 1 && args.sk_part && args.sk_cnt) {
+    int rem, maxp;
+    args.sk_pairs = gemm_sk_plan(args.M, args.N, K, &rem, &maxp);
+    args.sk_maxp = maxp;
+  }
   if (cg == 2) {
     switch (epi) {
       case EPI_F32: return launch_one<256, EPI_F32, 2>(ta, tb, args, stream);

@@ -56,7 +56,14 @@ struct GemmArgs {
   int* cnt;                   // [tiles_m] arrival counters (zero; reset by the reducing CTA)
   unsigned long long* trace;  // debug (PKV_GEMM_TRACE=1): per-CTA globaltimer stamps [grid][8]
   int stream_k;               // EPI_PROJ: 1 = stream-K (CTA c owns k units [c*U/G, (c+1)*U/G))
+  // Stage-II stream-K tail (CTA pairs): the T % P tiles of the last, partial wave are cut
+  // into k pieces over the first sk_pairs pairs, before the T - T % P whole tiles
+  int sk_pairs;               // 0 = off
+  float* sk_part;             // [rem tiles][SK_MAXP][CG][BN cols][128 rows] fp32 pieces
+  int* sk_cnt;                // [rem tiles][CG] arrival counters (zeroed; reset by the reducer)
+  int sk_maxp;                // piece stride per tail tile (<= SK_MAXP)
 };
+constexpr int SK_MAXP = 8;    // pieces per tail tile (host plan guarantees)
 
 __device__ __forceinline__ void gemm_stamp(const GemmArgs& a, int i) {
   if (a.trace != nullptr) {
@@ -183,7 +190,7 @@ __global__ void __launch_bounds__(192, 1)
   // into G equal contiguous ranges, one per CTA; a range covers the tail of one m-tile,
   // whole tiles and the head of another.  Piece idx of an m-tile is its idx-th owner, so
   // the split points -- and the fixed-order sum of the pieces -- depend only on (U, G).
-  struct Work { int mb, nb, k0, k1, idx, nseg; };
+  struct Work { int mb, nb, k0, k1, idx, nseg, slot; };
   const bool sk = (EPI == EPI_PROJ && CG == 1 && CK == 0) && args.stream_k;
   const long U = (long)tiles_m * k_tiles_total;
   auto sk_start = [&](int c) -> long { return (long)c * U / n_ctas; };
@@ -194,8 +201,45 @@ __global__ void __launch_bounds__(192, 1)
     while (c > 0 && sk_start(c) > u) --c;
     return c;
   };
-  auto first_pos = [&]() -> long { return sk ? sk_start(cta_id) : (long)cta_id; };
+  // Stage-II tail: phase 0 walks this pair's share of the rem tail tiles' k units
+  // (tiles T-rem..T-1), phase 1 the whole tiles 0..T-rem-1 strided over the pairs.
+  const int skp = (CG == 2 && EPI != EPI_PROJ) ? args.sk_pairs : 0;
+  const int sk_rem = skp ? (tiles_m * tiles_n) % n_ctas : 0;
+  const long Usk = (long)sk_rem * k_tiles_total;
+  auto t_start = [&](int c) -> long { return skp ? (long)c * Usk / skp : 0; };
+  auto t_owner = [&](long u) -> int {
+    int c = (int)((u * skp) / Usk);
+    if (c >= skp) c = skp - 1;
+    while (c + 1 < skp && t_start(c + 1) <= u) ++c;
+    while (c > 0 && t_start(c) > u) --c;
+    return c;
+  };
+  int phase0 = (skp && cta_id < skp) ? 1 : 0;
+  auto first_pos = [&]() -> long {
+    phase0 = (skp && cta_id < skp) ? 1 : 0;
+    return sk ? sk_start(cta_id) : (phase0 ? t_start(cta_id) : (long)cta_id);
+  };
   auto next_work = [&](long& pos, Work& w) -> bool {
+    w.slot = -1;
+    if (phase0) {
+      const long u1 = t_start(cta_id + 1);
+      if (pos < u1) {
+        const int sl = (int)(pos / k_tiles_total);
+        int sp_;
+        tile_coords(tiles_m * tiles_n - sk_rem + sl, w.mb, w.nb, sp_);
+        w.k0 = (int)(pos - (long)sl * k_tiles_total);
+        w.k1 = (int)min((long)k_tiles_total, (long)w.k0 + (u1 - pos));
+        const long tb = (long)sl * k_tiles_total;
+        const int o0 = t_owner(tb);
+        w.idx = cta_id - o0;
+        w.nseg = t_owner(tb + k_tiles_total - 1) - o0 + 1;
+        w.slot = sl;
+        pos += w.k1 - w.k0;
+        return true;
+      }
+      phase0 = 0;
+      pos = cta_id;
+    }
     if (sk) {
       const long u1 = sk_start(cta_id + 1);
       if (pos >= u1) return false;
@@ -210,7 +254,7 @@ __global__ void __launch_bounds__(192, 1)
       pos += w.k1 - w.k0;
       return true;
     }
-    if (pos >= total_tiles) return false;
+    if (pos >= total_tiles - sk_rem) return false;
     int sp;
     tile_coords((int)pos, w.mb, w.nb, sp);
     w.k0 = sp * args.k_tiles_per_split;
@@ -333,6 +377,56 @@ __global__ void __launch_bounds__(192, 1)
       const int row = mb * Cfg::BMT + (int)rank * Cfg::BM + row_in_tile;
       const bool row_ok = row < args.M;
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * Cfg::ACC_STRIDE;
+      bool do_epi = true;
+      if constexpr (CG == 2 && EPI != EPI_PROJ) {
+        if (w.slot >= 0 && w.nseg > 1) {
+          // tail piece: store the raw fp32 accumulator (coalesced: [col][row]); the last
+          // piece to arrive sums all pieces in piece order (deterministic) back into its
+          // TMEM accumulator and runs the normal epilogue on it
+          __shared__ int s_last2;
+          const long pstride = (long)CG * BN * 128;
+          const float* pbase = args.sk_part + (long)w.slot * args.sk_maxp * pstride + (long)rank * BN * 128 + row_in_tile;
+          float* mine = const_cast<float*>(pbase) + w.idx * pstride;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t a[32];
+            __syncwarp();
+            tmem_ld32(t_row + c * 32, a);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) __stcg(mine + (long)(c * 32 + i) * 128, __uint_as_float(a[i]));
+          }
+          named_bar_sync(1, 128);
+          if (threadIdx.x == 64)
+            s_last2 = atom_add_acq_rel_gpu(&args.sk_cnt[w.slot * CG + (int)rank], 1) == w.nseg - 1 ? 1 : 0;
+          named_bar_sync(1, 128);
+          if (!s_last2) {
+            do_epi = false;
+          } else {
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+              float sum[32];
+#pragma unroll 2
+              for (int j = 0; j < w.nseg; ++j) {
+                const float* pj = pbase + j * pstride + (long)c * 32 * 128;
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __ldcg(pj + (long)i * 128);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) sum[i] = j == 0 ? v[i] : sum[i] + v[i];
+              }
+              uint32_t r[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(sum[i]);
+              __syncwarp();
+              tmem_st32(t_row + c * 32, r);
+            }
+            tmem_st_wait();
+            if (threadIdx.x == 64) args.sk_cnt[w.slot * CG + (int)rank] = 0;
+          }
+        }
+      }
+      if (do_epi) {
 
       if constexpr (EPI == EPI_PROJ) {
        __shared__ int s_last;
@@ -458,7 +552,7 @@ __global__ void __launch_bounds__(192, 1)
           if (!row_ok || col0 >= args.N) continue;
           const bool full = col0 + 32 <= args.N && (args.ldc & 7) == 0;  // vector stores need aligned rows
           if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
-            float* dst = reinterpret_cast<float*>(args.C) + (long)w.idx * args.M * args.ldc + (long)row * args.ldc + col0;
+            float* dst = reinterpret_cast<float*>(args.C) + (long)(w.slot >= 0 ? 0 : w.idx) * args.M * args.ldc + (long)row * args.ldc + col0;
             if (full) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
@@ -580,6 +674,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      }  // do_epi
       if constexpr (EPI != EPI_PROJ || CG == 2) {  // (EPI_PROJ, CG = 1 released it above)
         tc_fence_before();
         __syncwarp();
@@ -633,6 +728,11 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 // host launcher (gemm_tc.cu)
+// Stage-II stream-K tail plan for an M x N x K GEMM on CTA pairs (256 x 256 tiles):
+// pairs sharing the tail (0 = off), tail tiles and the most pieces any tail tile gets.
+int gemm_sk_plan(int M, int N, int K, int* rem_out, int* maxp_out);
+// workspace for the tail pieces + counters of such a GEMM (0 when the plan is off)
+size_t gemm_sk_ws_floats(int M, int N, int K);
 int gemm_tc_launch(int epi, int bn, const void* A, long lda_rows, const void* B, long ldb_rows, int K, GemmArgs args,
                    cudaStream_t stream);
 bool make_tmap_2d(CUtensorMap* map, const void* base, long rows, long cols, long row_stride_elems, int box_rows,

@@ -198,3 +198,42 @@ def test_narrow_projection_is_fp32_faithful(built, N, K, m, splits, resid):
     err = ((out.double() - want).abs().max() / want.abs().max()).item()
     assert err < 1e-5, err
     assert int(cnt.sum().item()) == 0  # split counters are reset for the next launch
+
+
+_SK_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2602_02579_b200 as P
+lib = P._lib.load()
+M, N, K = 6554, 6144, 1024   # 26 x 24 = 624 tiles: a 32-tile tail on 74 CTA pairs
+g = torch.Generator(device="cuda").manual_seed(5)
+A = torch.randn((M, K), generator=g, device="cuda").to(torch.bfloat16)
+B = torch.randn((N, K), generator=g, device="cuda").to(torch.bfloat16)
+outs = []
+for _ in range(2):
+    C = torch.full((M, N), float("nan"), device="cuda")
+    P._lib.check(lib.pkv_gemm_bf16(A.data_ptr(), K, B.data_ptr(), K, M, N, K, C.data_ptr(), N, 256, 0,
+                                   torch.cuda.current_stream().cuda_stream))
+    outs.append(C)
+torch.cuda.synchronize()
+want = A.float() @ B.float().t()
+err = (outs[0] - want).abs().max().item()
+assert err <= 1e-3 * want.abs().max().item(), err
+assert torch.equal(outs[0], outs[1]), "stream-K tail is not deterministic"
+print("ok", err)
+"""
+
+
+def test_gemm_stream_k_tail_opt_in(built, tmp_path):
+    """PKV_GEMM_SK=1 (read once per process, hence the subprocess): the last wave's
+    tiles split into k pieces over all CTA pairs, summed in piece order."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "sk.py"
+    script.write_text(_SK_SCRIPT)
+    env = dict(os.environ, PKV_GEMM_SK="1")
+    r = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
