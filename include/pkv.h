@@ -107,6 +107,10 @@ typedef struct pkv_cache {
   const float* rope_cs32;    /* nullable [rope_len][head_dim/2][2]: (cos, sin) of the float64 tables
                                 rounded to f32, used by the bf16 Stage-II RoPE epilogue (the
                                 fp32-faithful paths and assembly always use the float64 tables) */
+  void* const* layer_done;   /* nullable host array [n_layers] of cudaEvent_t: pkv_recompute records
+                                layer_done[l] once layer l's K/V are final (after its QKV scatter),
+                                so the final query pass can follow Stage II layer by layer on
+                                another stream (pass it these events as layer_ready) */
 } pkv_cache;
 
 /* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */

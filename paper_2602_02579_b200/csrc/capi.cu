@@ -692,6 +692,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     }
     // K/V of every selected token are in the cache before this layer's attention
     TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    if (c->layer_done != nullptr && c->layer_done[l] != nullptr)
+      cudaEventRecord(reinterpret_cast<cudaEvent_t>(c->layer_done[l]), st);
     if (l == cf.n_layers - 1 && !need_final_h) break;
     TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
                        (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));

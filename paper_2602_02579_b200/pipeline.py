@@ -21,6 +21,16 @@ from .model import DeviceModel
 from .tensor import ratio_budget
 
 
+def _created_events(n: int) -> list:
+    """torch creates the cudaEvent_t behind torch.cuda.Event on its first record(); the
+    C side gets the raw handles (include/pkv.h layer_ready / layer_done), so record once."""
+    torch = _lib.require_cuda()
+    evs = [torch.cuda.Event() for _ in range(n)]
+    for e in evs:
+        e.record()
+    return evs
+
+
 class PrefillPipeline:
     def __init__(self, dm: DeviceModel, chunks: list, m: int, p: float):
         torch = _lib.require_cuda()
@@ -54,9 +64,23 @@ class PrefillPipeline:
         # per-layer assembly on the side stream overlapping the scoring pass: measured
         # neutral for device-resident chunks (both phases compete for HBM), so opt-in
         self.pipelined_assembly = os.environ.get("PKV_ASM_PIPE", "0") == "1"
-        self.layer_events = [torch.cuda.Event() for _ in range(cfg.n_layers)]
+        self.layer_events = _created_events(cfg.n_layers)
         self.cache.layer_events = self.layer_events
         self.cache._c_cache = self.cache._make_c_cache()
+        # final pass following Stage II layer by layer: pkv_recompute records done[l] once
+        # layer l's K/V are final and the final query pass (on its own stream) waits on
+        # done[l] before its layer-l attention, so its narrow kernels fill the gaps of
+        # Stage II instead of running after it (PKV_FINAL_OVERLAP=0: serial)
+        # (unsharded models only: two streams issuing collectives on one communicator
+        # could be ordered differently on different ranks)
+        self.final_overlap = os.environ.get("PKV_FINAL_OVERLAP", "1") == "1" and getattr(dm, "tp_world", 1) == 1
+        self.fin = torch.cuda.Stream(device=dev)
+        self.done_events = _created_events(cfg.n_layers)
+        self._c_done = (_lib.c_vp * cfg.n_layers)(*[e.cuda_event for e in self.done_events])
+        self._c_rc = _lib.Cache.from_buffer_copy(self.cache._c_cache)
+        self._c_rc.layer_done = self._c_done
+        self._c_fin = _lib.Cache.from_buffer_copy(self.cache._c_cache)
+        self._c_fin.layer_ready = self._c_done
 
     def set_query(self, ids) -> None:
         torch = _lib.require_cuda()
@@ -119,13 +143,25 @@ class PrefillPipeline:
         _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_score,
                                       self.per_layer.data_ptr(), None, None, None, self.ws_qp.data_ptr(),
                                       self.ws_qp.numel(), st))
+        if self.final_overlap:
+            # after the scoring pass (it shares ws_qp); layer l waits on done[l]
+            self.fin.wait_stream(main)
         _lib.check(lib.pkv_fuse_select(self.per_layer.data_ptr(), self.cfg.n_layers, self.s, self.k,
                                        self.fused.data_ptr(), self.idx.data_ptr(), self.status.data_ptr(), None, 0, st))
-        _lib.check(lib.pkv_recompute(self.dm.handle, cc, self.idx.data_ptr(), self.k, None, None,
-                                     self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
-        _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_final, None,
-                                      None, None, self.logits.data_ptr(), self.ws_qp.data_ptr(), self.ws_qp.numel(),
-                                      st))
+        if self.final_overlap:
+            self._c_rc.layer_ready = c.c_cache.layer_ready
+            _lib.check(lib.pkv_recompute(self.dm.handle, ctypes_ref(self._c_rc), self.idx.data_ptr(), self.k, None,
+                                         None, self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
+            _lib.check(lib.pkv_query_pass(self.dm.handle, ctypes_ref(self._c_fin), ch, self.query.data_ptr(), self.m,
+                                          self.flags_final, None, None, None, self.logits.data_ptr(),
+                                          self.ws_qp.data_ptr(), self.ws_qp.numel(), self.fin.cuda_stream))
+            main.wait_stream(self.fin)
+        else:
+            _lib.check(lib.pkv_recompute(self.dm.handle, cc, self.idx.data_ptr(), self.k, None, None,
+                                         self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
+            _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_final,
+                                          None, None, None, self.logits.data_ptr(), self.ws_qp.data_ptr(),
+                                          self.ws_qp.numel(), st))
         main.wait_stream(self.side)  # rejoin (required for graph capture)
 
 

@@ -62,7 +62,22 @@ def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
         tap_v = torch.empty_like(tap_k)
     lib = _lib.load()
     ws = workspace(lib.pkv_recompute_workspace(dm.handle, k), "rc")
-    _lib.check(lib.pkv_recompute(dm.handle, ctypes.byref(cache.c_cache), d_sel.data_ptr(), k,
+    c_rc = cache.c_cache
+    if _final_overlap(dm):
+        # finalize_query may follow Stage II layer by layer on its own stream: done[l] is
+        # recorded once layer l's K/V are final (include/pkv.h layer_done)
+        pre = torch.cuda.Event()
+        pre.record()
+        done = [torch.cuda.Event() for _ in range(L)]
+        for e in done:
+            e.record()  # creates the cudaEvent_t (torch creates it lazily)
+        arr = (_lib.c_vp * L)(*[e.cuda_event for e in done])
+        c_rc = _lib.Cache.from_buffer_copy(cache.c_cache)
+        c_rc.layer_done = arr
+        c_fin = _lib.Cache.from_buffer_copy(cache.c_cache)
+        c_fin.layer_ready = arr
+        cache._final_follow = (pre, done, arr, c_fin)
+    _lib.check(lib.pkv_recompute(dm.handle, ctypes.byref(c_rc), d_sel.data_ptr(), k,
                                  tap_k.data_ptr() if tap_k is not None else None,
                                  tap_v.data_ptr() if tap_v is not None else None, ws.data_ptr(), ws.numel(),
                                  _lib.stream_ptr(torch)))
@@ -85,6 +100,13 @@ class FinalizeResult:
     rows: list | None
 
 
+def _final_overlap(dm) -> bool:
+    """finalize_query follows Stage II layer by layer on a side stream (unsharded models:
+    collectives of two streams on one communicator could interleave differently per rank)."""
+    import os
+    return os.environ.get("PKV_FINAL_OVERLAP", "1") == "1" and getattr(dm, "tp_world", 1) == 1
+
+
 def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_attn: bool = False,
                    tally: FlopTally | None = None) -> FinalizeResult:
     """Compute the query over the (repaired) cache and append its K/V entries.
@@ -97,11 +119,29 @@ def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_at
     if cache.access_log is not None:
         cache.access_log.extend(("read", li) for li in range(config.n_layers))
     L, Hkv, dk = config.n_layers, cache.config.n_kv_heads, config.head_dim
-    fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
-    fv = torch.empty_like(fk)
-    logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
     flags = _lib.PKV_QP_LOGITS | _lib.PKV_QP_APPEND_KV | _lib.PKV_QP_FROM_CHUNKS
-    run_query_pass(dm, cache, ids, flags, fresh_k=fk, fresh_v=fv, logits=logits)
+    follow = getattr(cache, "_final_follow", None)
+    cache._final_follow = None
+    if follow is not None and cache.pool_tokens >= cache.context_length + m:
+        # after the scoring pass (pre), layer l after Stage II's layer l (done[l]): the
+        # narrow kernels of this pass run in the gaps of Stage II's big kernels
+        pre, done, arr, c_fin = follow
+        main = torch.cuda.current_stream()
+        side = torch.cuda.Stream(device=cache.device)
+        side.wait_event(pre)
+        with torch.cuda.stream(side):
+            fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
+            fv = torch.empty_like(fk)
+            logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
+            run_query_pass(dm, cache, ids, flags, fresh_k=fk, fresh_v=fv, logits=logits, stream=side, c_cache=c_fin)
+        main.wait_stream(side)
+        for t in (fk, fv, logits):
+            t.record_stream(main)
+    else:
+        fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
+        fv = torch.empty_like(fk)
+        logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
+        run_query_pass(dm, cache, ids, flags, fresh_k=fk, fresh_v=fv, logits=logits)
     cache.query_kv = (fk, fv)
     bill_query_pass(tally, config, cache.context_length, m)
     first = logits.cpu().numpy()

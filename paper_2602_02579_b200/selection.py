@@ -117,11 +117,14 @@ def check_tokens(tokens, config: ModelConfig) -> np.ndarray:
 
 
 def run_query_pass(dm, cache, ids: np.ndarray, flags: int, per_layer=None, fresh_k=None, fresh_v=None, logits=None,
-                   stream=None):
-    """One device narrow pass (reference model.py:370-402) over the cache."""
+                   stream=None, c_cache=None):
+    """One device narrow pass (reference model.py:370-402) over the cache (c_cache: a
+    copy of cache.c_cache with other layer_ready events)."""
     torch = _lib.require_cuda()
     m = int(ids.shape[0])
-    cache.ensure_query_room(m)
+    if c_cache is None:
+        cache.ensure_query_room(m)
+        c_cache = cache.c_cache
     d_ids = torch.from_numpy(ids.astype(np.int32)).to(cache.device)
     lib = _lib.load()
     nbytes = lib.pkv_query_pass_workspace(dm.handle, cache.context_length, m, flags)
@@ -132,7 +135,7 @@ def run_query_pass(dm, cache, ids: np.ndarray, flags: int, per_layer=None, fresh
 
     import ctypes
     chunks = ctypes.byref(cache.c_chunks)
-    _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(cache.c_cache), chunks, d_ids.data_ptr(), m, flags,
+    _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(c_cache), chunks, d_ids.data_ptr(), m, flags,
                                   ptr(per_layer), ptr(fresh_k), ptr(fresh_v), ptr(logits), ws.data_ptr(), ws.numel(),
                                   _lib.stream_ptr(torch, stream)))
 

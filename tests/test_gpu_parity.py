@@ -199,6 +199,45 @@ def test_pinned_host_chunks_pipeline_is_identical(built):
     assert np.array_equal(runs[0][2], runs[1][2])
 
 
+def test_final_pass_following_stage2_is_identical(built, monkeypatch):
+    """finalize_query on its own stream, each layer released by Stage II's per-layer
+    done event (PKV_FINAL_OVERLAP, default on), equals the serial order bit for bit --
+    through the public API and through the graph-captured PrefillPipeline."""
+    import torch
+
+    from paper_2602_02579_b200.pipeline import PrefillPipeline
+    P = built
+    cfg_o, seed, units, query, p = _materialise("llama_width")
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg, mw, dch = _device_inputs(P, cfg_o, w, chunks)
+    runs = []
+    for ov in ("0", "1"):
+        monkeypatch.setenv("PKV_FINAL_OVERLAP", ov)
+        cache = P.assemble(dch, cfg, fp32_taps=False)
+        sc = P.score_prophet(mw, cfg, cache, query)
+        sel = P.select_top_p(sc, p)
+        P.recompute_selected(mw, cfg, cache, P.RecomputePlan(sel))
+        fin = P.finalize_query(mw, cfg, cache, query)
+        torch.cuda.synchronize()
+        runs.append((sel.indices, fin.first_logits, cache.k_pool.clone()))
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
+    assert torch.equal(runs[0][2], runs[1][2])
+
+    dm = P.DeviceModel.from_host(mw, cfg)
+    outs = []
+    for ov in (False, True):
+        pipe = PrefillPipeline(dm, dch, len(query), p)
+        pipe.final_overlap = ov
+        pipe.set_query(query)
+        pipe.step()
+        pipe.capture()
+        pipe.replay()
+        torch.cuda.synchronize()
+        outs.append((pipe.idx.clone(), pipe.logits.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
 def test_state_machine_and_errors(built):
     P = built
     cfg_o, seed, units, query, _ = CASES["tiny_ref"][0], 42, CASES["tiny_ref"][2], CASES["tiny_ref"][3], 0.3
