@@ -118,6 +118,10 @@ class PrefillPipeline:
             with torch.cuda.graph(self.graph, stream=side):
                 self.step()
         torch.cuda.current_stream().wait_stream(side)
+        # the events' last record was a capture node: waiting on them from eager work
+        # (full_prefill_step, an eager step()) is an error until they are recorded again
+        for e in self.layer_events + self.done_events:
+            e.record()
         return self.graph
 
     def replay(self) -> None:
