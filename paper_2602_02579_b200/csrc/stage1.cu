@@ -981,8 +981,10 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
 
 // ------------------------------------------------------------------ lm_head
 // logits[n] = dot(x, W[n]) over D, fp32 accumulation (x = final-normed last row)
-// 4 output rows per warp pass (16-byte loads of 4 rows in flight per lane, independent
-// accumulators); x (fp32, final-normed) staged in shared memory
+// R output rows per warp pass (16-byte loads of R rows, UNR k-steps in flight per lane,
+// independent accumulators); x (fp32, final-normed) staged in shared memory.  R = 2: with
+// 4 rows per pass the 128k-row vocabulary split into 3.4 passes per warp (85 % balance)
+template <int R, int UNR>
 __global__ void __launch_bounds__(256) gemv_rows_kernel(const float* x, const __nv_bfloat16* __restrict__ W, int N,
                                                         int D, long ldw, float* out) {
   pdl_entry();
@@ -992,19 +994,21 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const float* x, const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const bool vec = (D % 8 == 0) && (ldw % 8 == 0);
-  for (int n0 = (blockIdx.x * wpb + warp) * 4; n0 < N; n0 += gridDim.x * wpb * 4) {
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    if (vec) {
-#pragma unroll 2
-      for (int c = lane * 8; c < D; c += 256) {
-        uint4 u[4];
+  for (int n0 = (blockIdx.x * wpb + warp) * R; n0 < N; n0 += gridDim.x * wpb * R) {
+    float acc[R];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    if (vec) {
+#pragma unroll UNR
+      for (int c = lane * 8; c < D; c += 256) {
+        uint4 u[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
           u[r] = n0 + r < N ? __ldg(reinterpret_cast<const uint4*>(W + (long)(n0 + r) * ldw + c)) : make_uint4(0, 0, 0, 0);
         const float4 xa = *reinterpret_cast<const float4*>(xs + c);
         const float4 xb = *reinterpret_cast<const float4*>(xs + c + 4);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < R; ++r) {
           acc[r] = fmaf(xa.x, bf16_lo(u[r].x), acc[r]);
           acc[r] = fmaf(xa.y, bf16_hi(u[r].x), acc[r]);
           acc[r] = fmaf(xa.z, bf16_lo(u[r].y), acc[r]);
@@ -1016,11 +1020,11 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const float* x, const __
         }
       }
     } else {
-      for (int r = 0; r < 4 && n0 + r < N; ++r)
+      for (int r = 0; r < R && n0 + r < N; ++r)
         for (int c = lane; c < D; c += 32) acc[r] = fmaf(xs[c], __bfloat162float(W[(long)(n0 + r) * ldw + c]), acc[r]);
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < R; ++r) {
       float v = acc[r];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0 && n0 + r < N) out[n0 + r] = v;
@@ -1028,10 +1032,68 @@ __global__ void __launch_bounds__(256) gemv_rows_kernel(const float* x, const __
   }
 }
 
+// one row per warp pass with the whole row's NV 16-byte loads per lane issued up front
+// (D = 256 * NV): fine-grained rows balance the 128k-row vocabulary over the warps (14 vs
+// 13.5 passes) while each lane keeps NV * 16 B in flight.  Same per-lane summation order
+// as gemv_rows_kernel (column blocks lane*8 + 256*i in increasing i), so bit-identical.
+template <int NV>
+__global__ void __launch_bounds__(256) gemv_row1_kernel(const float* x, const __nv_bfloat16* __restrict__ W, int N,
+                                                        long ldw, float* out) {
+  pdl_entry();
+  __shared__ __align__(16) float xs[NV * 256];
+  for (int c = threadIdx.x; c < NV * 256; c += blockDim.x) xs[c] = x[c];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int n = blockIdx.x * (blockDim.x >> 5) + warp; n < N; n += nw) {
+    const uint4* row = reinterpret_cast<const uint4*>(W + (long)n * ldw) + lane;
+    uint4 u[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) u[i] = __ldg(row + i * 32);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float* xp = xs + i * 256 + lane * 8;
+      const float4 xa = *reinterpret_cast<const float4*>(xp);
+      const float4 xb = *reinterpret_cast<const float4*>(xp + 4);
+      acc = fmaf(xa.x, bf16_lo(u[i].x), acc);
+      acc = fmaf(xa.y, bf16_hi(u[i].x), acc);
+      acc = fmaf(xa.z, bf16_lo(u[i].y), acc);
+      acc = fmaf(xa.w, bf16_hi(u[i].y), acc);
+      acc = fmaf(xb.x, bf16_lo(u[i].z), acc);
+      acc = fmaf(xb.y, bf16_hi(u[i].z), acc);
+      acc = fmaf(xb.z, bf16_lo(u[i].w), acc);
+      acc = fmaf(xb.w, bf16_hi(u[i].w), acc);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[n] = acc;
+  }
+}
+
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st) {
-  const int blocks = std::min(ceil_div(N, 32), num_sms() * 8);
-  launch_k(gemv_rows_kernel, blocks, 256, D * sizeof(float), st, x, reinterpret_cast<const __nv_bfloat16*>(W), N, D, ldw,
-                                                           out);
+  if (D % 256 == 0 && ldw % 8 == 0 && !getenv("PKV_GEMV_ROWS")) {
+    const int blocks = std::min(ceil_div(N, 8), num_sms() * 8);
+    auto* w = reinterpret_cast<const __nv_bfloat16*>(W);
+    switch (D / 256) {
+      case 1: launch_k(gemv_row1_kernel<1>, blocks, 256, 0, st, x, w, N, ldw, out); break;
+      case 2: launch_k(gemv_row1_kernel<2>, blocks, 256, 0, st, x, w, N, ldw, out); break;
+      case 4: launch_k(gemv_row1_kernel<4>, blocks, 256, 0, st, x, w, N, ldw, out); break;
+      case 8: launch_k(gemv_row1_kernel<8>, blocks, 256, 0, st, x, w, N, ldw, out); break;
+      case 16: launch_k(gemv_row1_kernel<16>, blocks, 256, 0, st, x, w, N, ldw, out); break;
+      default: goto rows_kernel;
+    }
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("gemv_row1_kernel");
+    return PKV_OK;
+  }
+rows_kernel:
+  static const int rows = getenv("PKV_GEMV_ROWS") ? atoi(getenv("PKV_GEMV_ROWS")) : 4;
+  const int per_block = 8 * rows;
+  const int blocks = std::min(ceil_div(N, per_block), num_sms() * 8);
+  auto* w = reinterpret_cast<const __nv_bfloat16*>(W);
+  if (rows == 4) launch_k(gemv_rows_kernel<4, 2>, blocks, 256, D * sizeof(float), st, x, w, N, D, ldw, out);
+  else if (rows == 1) launch_k(gemv_rows_kernel<1, 8>, blocks, 256, D * sizeof(float), st, x, w, N, D, ldw, out);
+  else launch_k(gemv_rows_kernel<2, 4>, blocks, 256, D * sizeof(float), st, x, w, N, D, ldw, out);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("gemv_rows_kernel");
   return PKV_OK;
