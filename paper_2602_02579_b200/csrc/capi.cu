@@ -610,6 +610,7 @@ struct RcWs {
   float* sk_part;  // stream-K tail pieces of the Stage-II GEMMs (shared: they run in order)
   int* sk_cnt;
   size_t sk_cnt_n;
+  float* ssq;      // deferred RMSNorm: [k][ceil(Dp/256)] per-tile sums of h^2
 };
 static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
@@ -619,6 +620,7 @@ static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   w.qb = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
   w.ab = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
   w.act = cv.take<__nv_bfloat16>((size_t)k * md->Fp);
+  w.ssq = cv.take<float>((size_t)k * ceil_div(md->Dp, 256));
   const size_t skf = std::max(std::max(gemm_sk_ws_floats(k, md->NQKV, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->HQ)),
                               std::max(gemm_sk_ws_floats(k, 2 * md->Fp, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->Fp)));
   if (skf > 0) {
@@ -653,6 +655,28 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
   pkv_comm* comm = md->comm;
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
   int rc;
+  // deferred RMSNorm (opt-in PKV_NORM_DEFER=1): the o / down GEMM epilogues (or,
+  // head-sharded, a small pass after the all-reduce) write bf16(h * g) and per-tile sums of
+  // h^2; the QKV / gate-up epilogues scale by 1/rms, so only layer 0's attention norm runs
+  // as its own kernel.  Measured +1 ms per prefill (fp32 sums; +15 ms with f64 sums): the
+  // extra epilogue stores compete with the mainloop's TMA fill, which costs more than the
+  // 2 ms of standalone norm passes it removes.
+  const bool defer = getenv("PKV_NORM_DEFER") && getenv("PKV_NORM_DEFER")[0] == '1';
+  const int ntile = ceil_div(Dp, 256);
+  auto consume = [&](GemmArgs& a) {
+    a.ssq_in = w.ssq;
+    a.ssq_n = ntile;
+    a.ssq_ld = ntile;
+    a.norm_D = cf.hidden_dim;
+    a.norm_eps = (float)cf.norm_eps;
+  };
+  auto produce = [&](GemmArgs& a, const float* gain) {
+    a.ng = gain;
+    a.xg = w.xb;
+    a.ldxg = Dp;
+    a.ssq = w.ssq;
+    a.ssq_ld = ntile;
+  };
   if (w.sk_cnt) cudaMemsetAsync(w.sk_cnt, 0, w.sk_cnt_n * sizeof(int), st);
   if (c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
   TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
@@ -661,8 +685,10 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     // the scatter must land after this layer's (possibly pipelined) assembly
     if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
-    TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    if (l == 0 || !defer)
+      TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
+    if (defer && l > 0) consume(g);
     g.sk_part = w.sk_part;
     g.sk_cnt = w.sk_cnt;
     g.M = k;
@@ -705,9 +731,13 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     go.n_splits = 1;
     go.C = w.h;
     go.ldc = Dp;
+    if (defer && !comm) produce(go, lw.ffn_norm);
     TTRY(T_RC_O, gemm_tc_launch(epi_resid, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
     if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
-    TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    if (!defer)
+      TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+    else if (comm)
+      TTRY(T_RC_MISC, norm_defer_launch(w.h, k, Dp, Dp, lw.ffn_norm, w.xb, Dp, w.ssq, ntile, st));
     GemmArgs gg{};
     gg.sk_part = w.sk_part;
     gg.sk_cnt = w.sk_cnt;
@@ -716,6 +746,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     gg.n_splits = 1;
     gg.C = w.act;
     gg.ldc = Fp;
+    if (defer) consume(gg);
     TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
     GemmArgs gd{};
     gd.sk_part = w.sk_part;
@@ -725,8 +756,12 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     gd.n_splits = 1;
     gd.C = w.h;
     gd.ldc = Dp;
+    const float* next_norm = l + 1 < cf.n_layers ? md->layers[l + 1].attn_norm : nullptr;
+    if (defer && !comm && next_norm) produce(gd, next_norm);
     TTRY(T_RC_DOWN, gemm_tc_launch(epi_resid, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
     if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
+    if (defer && comm && next_norm)
+      TTRY(T_RC_MISC, norm_defer_launch(w.h, k, Dp, Dp, next_norm, w.xb, Dp, w.ssq, ntile, st));
   }
   return PKV_OK;
 }

@@ -62,6 +62,20 @@ struct GemmArgs {
   float* sk_part;             // [rem tiles][SK_MAXP][CG][BN cols][128 rows] fp32 pieces
   int* sk_cnt;                // [rem tiles][CG] arrival counters (zeroed; reset by the reducer)
   int sk_maxp;                // piece stride per tail tile (<= SK_MAXP)
+  // deferred RMSNorm (Stage II).  rmsnorm(h) . W = ((h * g) . W) / rms(h) row by row, so
+  // an EPI_RESID producer writes xg = bf16(h_new * ng) and the fp32 sums of h_new^2 of each
+  // (row, BN-column tile) -- sequentially over the tile's columns -- and the next GEMM
+  // (EPI_QKV / EPI_SILU) scales its accumulator rows by 1 / sqrt(sum / norm_D + eps).
+  // Replaces a standalone norm pass over h (read 4 B + write 2 B per element) per norm.
+  const float* ng;            // producer: gain of the next norm [N] (nullptr: off)
+  __nv_bfloat16* xg;          // producer: [M][ldxg] bf16(h_new * ng)
+  long ldxg;
+  float* ssq;                 // producer: [M][ssq_ld] per-tile sums of h_new^2 (fp32, in column order)
+  int ssq_ld;
+  const float* ssq_in;        // consumer: [M][ssq_ld] (nullptr: input already normalised)
+  int ssq_n;                  // consumer: tiles to sum (in order)
+  int norm_D;                 // consumer: mean divisor (the unpadded hidden size)
+  float norm_eps;
 };
 constexpr int SK_MAXP = 8;    // pieces per tail tile (host plan guarantees)
 
@@ -427,6 +441,23 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       if (do_epi) {
+      [[maybe_unused]] float rnorm = 1.f;
+      if constexpr (EPI == EPI_QKV || EPI == EPI_SILU) {
+        if (args.ssq_in != nullptr && row_ok) {
+          // the tile sums in order; loads issued 8 at a time (one round trip for D <= 2048)
+          const float* sp = args.ssq_in + (long)row * args.ssq_ld;
+          float sq = 0.f;
+          for (int t0 = 0; t0 < args.ssq_n; t0 += 8) {
+            float part[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) part[q] = t0 + q < args.ssq_n ? sp[t0 + q] : 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (t0 + q < args.ssq_n) sq += part[q];
+          }
+          rnorm = 1.f / sqrtf(sq / (float)args.norm_D + args.norm_eps);
+        }
+      }
 
       if constexpr (EPI == EPI_PROJ) {
        __shared__ int s_last;
@@ -531,8 +562,8 @@ __global__ void __launch_bounds__(192, 1)
             uint32_t packed[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              float a0 = silu_f(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
-              float a1 = silu_f(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
+              float a0 = silu_f(__uint_as_float(g[2 * j]) * rnorm) * (__uint_as_float(u[2 * j]) * rnorm);
+              float a1 = silu_f(__uint_as_float(g[2 * j + 1]) * rnorm) * (__uint_as_float(u[2 * j + 1]) * rnorm);
               packed[j] = pack_bf16(a0, a1);
             }
             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col);
@@ -542,6 +573,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       } else {
+        [[maybe_unused]] float ssacc = 0.f;  // deferred norm: sum of h_new^2 over this tile
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
           uint32_t r[32];
@@ -554,20 +586,54 @@ __global__ void __launch_bounds__(192, 1)
           if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
             float* dst = reinterpret_cast<float*>(args.C) + (long)(w.slot >= 0 ? 0 : w.idx) * args.M * args.ldc + (long)row * args.ldc + col0;
             if (full) {
+              // all residual loads first: a store through another pointer (xg) between
+              // them would otherwise serialise every load behind the previous store
+              [[maybe_unused]] float4 o[8];
+              if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) o[j] = reinterpret_cast<const float4*>(dst)[j];
+              }
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
                 if constexpr (EPI == EPI_RESID) {
-                  float4 o = reinterpret_cast<float4*>(dst)[j];
-                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                  v.x += o[j].x; v.y += o[j].y; v.z += o[j].z; v.w += o[j].w;
+                  r[4 * j] = __float_as_uint(v.x);
+                  r[4 * j + 1] = __float_as_uint(v.y);
+                  r[4 * j + 2] = __float_as_uint(v.z);
+                  r[4 * j + 3] = __float_as_uint(v.w);
                 }
                 reinterpret_cast<float4*>(dst)[j] = v;
+              }
+              if constexpr (EPI == EPI_RESID) {
+                if (args.xg != nullptr) {
+                  float4 gg[8];
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) gg[j] = __ldg(reinterpret_cast<const float4*>(args.ng + col0) + j);
+                  uint2* xd = reinterpret_cast<uint2*>(args.xg + (long)row * args.ldxg + col0);
+#pragma unroll
+                  for (int j = 0; j < 8; ++j) {
+                    const float a = __uint_as_float(r[4 * j]), b = __uint_as_float(r[4 * j + 1]);
+                    const float c2 = __uint_as_float(r[4 * j + 2]), d = __uint_as_float(r[4 * j + 3]);
+                    ssacc = fmaf(a, a, ssacc);
+                    ssacc = fmaf(b, b, ssacc);
+                    ssacc = fmaf(c2, c2, ssacc);
+                    ssacc = fmaf(d, d, ssacc);
+                    xd[j] = make_uint2(pack_bf16(a * gg[j].x, b * gg[j].y), pack_bf16(c2 * gg[j].z, d * gg[j].w));
+                  }
+                }
               }
             } else {
               for (int j = 0; j < 32 && col0 + j < args.N; ++j) {
                 float v = __uint_as_float(r[j]);
-                if constexpr (EPI == EPI_RESID) v += dst[j];
+                if constexpr (EPI == EPI_RESID) {
+                  v += dst[j];
+                  if (args.xg != nullptr) {
+                    ssacc = fmaf(v, v, ssacc);
+                    args.xg[(long)row * args.ldxg + col0 + j] = __float2bfloat16_rn(v * args.ng[col0 + j]);
+                  }
+                }
                 dst[j] = v;
               }
             }
@@ -594,7 +660,7 @@ __global__ void __launch_bounds__(192, 1)
             const bool is_v = head_all >= H + Hkv;
             float vals[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]) * rnorm;
             if (head_all >= H) {  // precompute_chunk captures: unrotated keys / values
               __nv_bfloat16* cap = is_v ? args.vcap_out : args.knr_out;
               if (cap != nullptr) {
@@ -672,6 +738,9 @@ __global__ void __launch_bounds__(192, 1)
               reinterpret_cast<uint4*>(dst)[j] =
                   make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
           }
+        }
+        if constexpr (EPI == EPI_RESID) {
+          if (args.xg != nullptr && row_ok && nb * BN < args.N) args.ssq[(long)row * args.ssq_ld + nb] = ssacc;
         }
       }
       }  // do_epi

@@ -1099,6 +1099,37 @@ rows_kernel:
   return PKV_OK;
 }
 
+// Deferred RMSNorm after the tensor-parallel all-reduce of h: the xg = bf16(h * g) and
+// per-256-column-tile fp32 sums of h^2 that the EPI_RESID epilogue writes on one GPU, in the
+// same (increasing column) order, so head-sharded and unsharded Stage II normalise alike.
+__global__ void norm_defer_kernel(const float* __restrict__ h, long ld, int N, const float* __restrict__ g,
+                                  __nv_bfloat16* __restrict__ xg, long ldxg, float* __restrict__ ssq, int ssq_ld) {
+  pdl_entry();
+  const long row = blockIdx.x;
+  const int c0 = threadIdx.x * 256;
+  if (c0 >= N) return;
+  const float* hr = h + row * ld;
+  float acc = 0.f;
+  const int c1 = min(c0 + 256, N);
+  for (int c = c0; c < c1; ++c) {
+    const float v = hr[c];
+    acc = fmaf(v, v, acc);
+    xg[row * ldxg + c] = __float2bfloat16_rn(v * g[c]);
+  }
+  ssq[row * ssq_ld + threadIdx.x] = acc;
+}
+
+int norm_defer_launch(const float* h, int m, long ld, int N, const float* g, void* xg, long ldxg, float* ssq,
+                      int ssq_ld, cudaStream_t st) {
+  if (m <= 0) return PKV_OK;
+  const int threads = ceil_div(N, 256);
+  if (threads > 1024) return set_error(PKV_ERR_SHAPE, "norm_defer: row too wide");
+  launch_k(norm_defer_kernel, m, threads, 0, st, h, ld, N, g, reinterpret_cast<__nv_bfloat16*>(xg), ldxg, ssq, ssq_ld);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("norm_defer_kernel");
+  return PKV_OK;
+}
+
 // embedding rows (bf16 table) -> fp32 [n][ld]
 __global__ void embed_gather_kernel(const __nv_bfloat16* embed, long lde, const int32_t* ids, const int32_t* sel,
                                     int n, int D, float* out, long ldo) {

@@ -173,7 +173,9 @@ def test_fuse_layers_bit_exact(built):
     assert np.array_equal(P.fuse_layers(per), O.layer_mean(per))
 
 
-@pytest.mark.parametrize("N,K,m,splits,resid", [(4096, 4096, 32, 0, 0), (384, 1024, 7, 3, 1), (6144, 4096, 32, 1, 0)])
+@pytest.mark.parametrize("N,K,m,splits,resid", [(4096, 4096, 32, 0, 0), (384, 1024, 7, 3, 1), (6144, 4096, 32, 1, 0),
+                                                  # stream-K: one m-tile cut into 15 pieces; wd shape on 96 CTAs
+                                                  (128, 4096, 5, 0, 1), (4096, 14336, 32, -96, 1)])
 def test_narrow_projection_is_fp32_faithful(built, N, K, m, splits, resid):
     """EPI_PROJ: out (+)= x . W^T for <= 32 fp32 rows given as 3 exact bf16 planes."""
     torch = _torch()

@@ -238,6 +238,32 @@ def test_final_pass_following_stage2_is_identical(built, monkeypatch):
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
 
 
+def test_deferred_norm_matches_standalone_norm(built, monkeypatch):
+    """PKV_NORM_DEFER=1 (RMSNorm folded into the Stage-II GEMM epilogues) gives the same
+    repaired cache and first-token logits within the bf16 Stage-II tolerance."""
+    import torch
+    P = built
+    cfg_o, seed, units, query, p = _materialise("llama_width")
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg, mw, dch = _device_inputs(P, cfg_o, w, chunks)
+    runs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PKV_NORM_DEFER", mode)
+        cache = P.assemble(dch, cfg, fp32_taps=False)
+        sc = P.score_prophet(mw, cfg, cache, query)
+        sel = P.select_top_p(sc, p)
+        P.recompute_selected(mw, cfg, cache, P.RecomputePlan(sel))
+        fin = P.finalize_query(mw, cfg, cache, query)
+        torch.cuda.synchronize()
+        runs.append((sel.indices, fin.first_logits, cache.k_pool.float(), cache.v_pool.float()))
+    assert runs[0][0] == runs[1][0]
+    for a, b in ((runs[0][2], runs[1][2]), (runs[0][3], runs[1][3])):
+        # two bf16 Stage-II rounding paths, each within KV_ABS of the fp32 reference
+        assert float((a - b).abs().max()) <= 2 * KV_ABS
+        assert float(torch.nn.functional.cosine_similarity(a.flatten(), b.flatten(), dim=0)) >= 0.9999
+    assert np.abs(runs[0][1] - runs[1][1]).max() <= KV_ABS and _cos(runs[0][1], runs[1][1]) >= COS_MIN
+
+
 def test_state_machine_and_errors(built):
     P = built
     cfg_o, seed, units, query, _ = CASES["tiny_ref"][0], 42, CASES["tiny_ref"][2], CASES["tiny_ref"][3], 0.3

@@ -26,7 +26,9 @@ for _ in range(2):
 torch.cuda.synchronize()
 lib = _lib.load()
 c = pipe.cache
-cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
+_cc = _lib.Cache.from_buffer_copy(c.c_cache)
+_cc.layer_ready = None  # no cross-capture event waits (each phase is its own graph)
+cc, ch = ctypes_ref(_cc), ctypes_ref(c.c_chunks)
 
 
 def score(st):
