@@ -33,10 +33,31 @@ struct AttnArgs {
   const int32_t* pos;        // [n_q] ascending
   const int32_t* page_table; // logical page -> physical page
   int n_q, H, Hkv, G, T, n_tiles, n_pairs;
+  int hg;                    // KV heads per scheduling group (divides Hkv), see below
   long kv_row0;              // first pool row of this layer: layer * Hkv * pool_tokens
   long pool_tokens;
   float scale_log2;          // log2(e) / sqrt(head_dim)
+  unsigned long long* trace; // debug (PKV_ATTN_TRACE=1): %globaltimer per page of CTA 0, see below
 };
+
+// trace[ev * 64 + j] for page j < 64 of blockIdx.x == 0 (tools/attn_trace.py):
+//   ev 0/1: tile A/B softmax saw S(j) (warp 0 / 8, lane 0)   ev 2/3: A/B arrived P(j)
+//   ev 4/5: MMA warp issued PV_A(j) / PV_B(j)                ev 6: MMA warp saw K/V page j+1
+//   ev 7: producer issued the K/V loads of page j
+// Measured (C3 shape, tools/attn_trace.py + tools/bench_attn.py): a page takes ~1.7 us;
+// each softmax ~0.87 us; the MMA warp waits ~0.32 us per page for K/V(j+1) and S(j+1)
+// reaches the softmax ~0.2 us after its MMA.  A 64 KB page load takes ~0.9 us; issued
+// earlier (separate K / V rings, K(j+2) right after S_B(j+1)) it took ~2.3 us instead --
+// the SM's K/V stream is throughput-bound (~40 GB/s per SM with all SMs streaming), not
+// latency-bound (1.40 vs 1.36 ms).  Diagnostics: no exponentials -4.5 %, no half-row max
+// exchange -3 %, no V loads -8 %: no single stage dominates the S -> softmax -> PV chain.
+__device__ __forceinline__ void attn_stamp(const AttnArgs& a, int ev, int j) {
+  if (a.trace != nullptr && blockIdx.x == 0 && j < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[ev * 64 + j] = t;
+  }
+}
 
 template <int DKP>
 struct AttnCfg {
@@ -110,8 +131,13 @@ __global__ void __launch_bounds__(576, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x % a.Hkv;
-  const int pair = a.n_pairs - 1 - blockIdx.x / a.Hkv;  // heaviest pairs first (LPT)
+  // CTA order: KV-head groups of hg heads one after the other, inside a group heaviest
+  // pairs first (LPT).  All heads at once keep every head's K/V pages live -- 134 MB per
+  // layer at 32k, more than L2 -- while a group's K/V fits and is re-read from L2.
+  const int per_group = a.hg * a.n_pairs;
+  const int grp = blockIdx.x / per_group, rem_ = blockIdx.x - grp * per_group;
+  const int g = grp * a.hg + rem_ % a.hg;
+  const int pair = a.n_pairs - 1 - rem_ / a.hg;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -147,6 +173,7 @@ __global__ void __launch_bounds__(576, 1)
         const int st = j % Cfg::STAGES;
         const uint32_t ph = (uint32_t)(j / Cfg::STAGES) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
+        attn_stamp(a, 7, j);
         uint8_t* sk = sKV + st * 2 * Cfg::KV_BYTES;
         uint8_t* sv = sk + Cfg::KV_BYTES;
         const int row = (int)(head_row + (long)a.page_table[j] * 128);
@@ -199,14 +226,17 @@ __global__ void __launch_bounds__(576, 1)
       const bool more = j + 1 < n_kv_tiles;
       mbar_wait(&p_full[0], (uint32_t)j & 1);
       tc_fence_after();
+      if (lane == 0) attn_stamp(a, 4, j);
       issue_pv(0, j);
       if (more) {
         mbar_wait(&kv_full[(j + 1) % Cfg::STAGES], (uint32_t)((j + 1) / Cfg::STAGES) & 1);
         tc_fence_after();
+        if (lane == 0) attn_stamp(a, 6, j);
         issue_s(0, j + 1);  // in-order after PV_A(j): P_A's TMEM columns are free again
       }
       mbar_wait(&p_full[1], (uint32_t)j & 1);
       tc_fence_after();
+      if (lane == 0) attn_stamp(a, 5, j);
       issue_pv(1, j);
       if (elect_one()) umma_commit(&kv_empty[j % Cfg::STAGES]);
       __syncwarp();
@@ -253,6 +283,7 @@ __global__ void __launch_bounds__(576, 1)
     for (int j = 0; j < n_kv_tiles; ++j) {
       mbar_wait(&s_full[t], (uint32_t)j & 1);  // also implies PV_t(j-1) is complete
       tc_fence_after();
+      if ((warp & 7) == 0 && lane == 0) attn_stamp(a, t, j);
       const int key0 = j * 128 + h * 64;
       // pass 1: this half's 64 scores -> registers (masked -> -inf only on diagonal pages)
       float sv[64];
@@ -344,6 +375,7 @@ __global__ void __launch_bounds__(576, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
+      if ((warp & 7) == 0 && lane == 0) attn_stamp(a, 2 + t, j);
     }
     mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
     tc_fence_after();
@@ -403,8 +435,13 @@ __global__ void __launch_bounds__(832, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x % a.Hkv;
-  const int pair = a.n_pairs - 1 - blockIdx.x / a.Hkv;  // heaviest pairs first (LPT)
+  // CTA order: KV-head groups of hg heads one after the other, inside a group heaviest
+  // pairs first (LPT).  All heads at once keep every head's K/V pages live -- 134 MB per
+  // layer at 32k, more than L2 -- while a group's K/V fits and is re-read from L2.
+  const int per_group = a.hg * a.n_pairs;
+  const int grp = blockIdx.x / per_group, rem_ = blockIdx.x - grp * per_group;
+  const int g = grp * a.hg + rem_ % a.hg;
+  const int pair = a.n_pairs - 1 - rem_ / a.hg;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -669,6 +706,8 @@ static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnA
   return PKV_OK;
 }
 
+static unsigned long long* g_attn_trace = nullptr;
+
 // q/out: [n_q][H][dkp] bf16; k_pool/v_pool: [L][Hkv][pool_tokens][dkp] bf16 (whole pool)
 int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H, int Hkv, int head_dim, int dkp,
                    const void* k_pool, const void* v_pool, long pool_rows_total, long pool_tokens, int layer,
@@ -688,9 +727,24 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   a.T = 128 / G;
   a.n_tiles = ceil_div(n_q, a.T);
   a.n_pairs = ceil_div(a.n_tiles, 2);
+  {
+    static const int hg_env = getenv("PKV_ATTN_HG") ? atoi(getenv("PKV_ATTN_HG")) : 4;
+    int hg = std::max(1, std::min(hg_env, Hkv));
+    while (Hkv % hg) --hg;
+    a.hg = hg;
+  }
   a.kv_row0 = (long)layer * Hkv * pool_tokens;
   a.pool_tokens = pool_tokens;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
+  a.trace = nullptr;
+  {
+    static const bool tr = getenv("PKV_ATTN_TRACE") && getenv("PKV_ATTN_TRACE")[0] == '1';
+    static unsigned long long* buf = nullptr;
+    if (tr && buf == nullptr && cudaMalloc(&buf, 8 * 64 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(buf, 0, 8 * 64 * sizeof(unsigned long long));
+    if (tr) a.trace = buf;
+    g_attn_trace = buf;
+  }
   CUtensorMap tk, tv;
   if (!cached_tmap(&tk, k_pool, pool_rows_total, dkp, dkp, 128) ||
       !cached_tmap(&tv, v_pool, pool_rows_total, dkp, dkp, 128))
@@ -722,3 +776,10 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
 }
 
 }  // namespace pkv
+
+extern "C" int pkv_debug_attn_trace(unsigned long long* host) {
+  if (pkv::g_attn_trace == nullptr) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, pkv::g_attn_trace, 8 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
