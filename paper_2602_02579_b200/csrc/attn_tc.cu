@@ -113,18 +113,30 @@ __device__ __forceinline__ void unpack_f16x2(uint32_t v, float& lo, float& hi) {
 
 // POLY of every 8 exponentials go to the FMA-pipe polynomial, the rest to MUFU.EX2;
 // POLY < 0: packed half-precision MUFU.EX2 (two exponentials per op)
-template <int DKP, int POLY>
+// PAIR = 1: CTA pairs (cluster of 2, tcgen05 cta_group::2).  The pair's CTAs take two
+// adjacent query-pair blocks of the same KV head; every MMA is M = 256 (both CTAs' tiles)
+// and its B operand is split along N across the pair -- each CTA loads 64 of a page's
+// 128 keys of K and 64 of the 128 dims of V -- so per SM the K/V stream halves (it bounds
+// the page loop: ~40 GB/s per SM with every SM streaming) and the ring gets 4 stages.
+// tmK is then a 64-row-box map.  Only the leader's MMA warp issues.  Opt-in
+// (PKV_ATTN_PAIR=1): correct, and the K/V wait disappears, but every PV now waits for the
+// other CTA's softmax through a remote mbarrier arrive (~0.35 us on the critical chain),
+// so a page takes ~2.08 instead of ~1.70 us (1.59 vs 1.40 ms for the C3 layer).
+template <int DKP, int POLY, int PAIR = 0>
 __global__ void __launch_bounds__(576, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
   using Cfg = AttnCfg<DKP>;
+  static_assert(!PAIR || DKP == 128, "CTA-pair attention for head dim 128");
+  constexpr int NST = PAIR ? 2 * Cfg::STAGES : Cfg::STAGES;    // K/V ring stages
+  constexpr int KVB = PAIR ? Cfg::KV_BYTES / 2 : Cfg::KV_BYTES;  // this CTA's K (or V) bytes per page
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                      // tile A at +0, tile B at +Q_BYTES
   uint8_t* sKV = sQ + 2 * Cfg::Q_BYTES;    // stage s: K at sKV + s*2*KV_BYTES, V right after
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES);
-  uint64_t* kv_full = bars;                 // [STAGES]
-  uint64_t* kv_empty = bars + Cfg::STAGES;  // [STAGES]
-  uint64_t* s_full = bars + 2 * Cfg::STAGES;  // [2] per tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NST * 2 * KVB);
+  uint64_t* kv_full = bars;                 // [NST]
+  uint64_t* kv_empty = bars + NST;          // [NST]
+  uint64_t* s_full = bars + 2 * NST;          // [2] per tile
   uint64_t* p_full = s_full + 2;              // [2]
   uint64_t* pv_full = p_full + 2;             // [2]
   uint64_t* q_full = pv_full + 2;
@@ -134,25 +146,35 @@ __global__ void __launch_bounds__(576, 1)
   // CTA order: KV-head groups of hg heads one after the other, inside a group heaviest
   // pairs first (LPT).  All heads at once keep every head's K/V pages live -- 134 MB per
   // layer at 32k, more than L2 -- while a group's K/V fits and is re-read from L2.
-  const int per_group = a.hg * a.n_pairs;
-  const int grp = blockIdx.x / per_group, rem_ = blockIdx.x - grp * per_group;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_units = PAIR ? (a.n_pairs + 1) >> 1 : a.n_pairs;  // query-pair blocks (pairs of them)
+  const int per_group = a.hg * n_units;
+  const int grp = cid / per_group, rem_ = cid - grp * per_group;
   const int g = grp * a.hg + rem_ % a.hg;
-  const int pair = a.n_pairs - 1 - rem_ / a.hg;
+  const int unit = rem_ / a.hg;  // 0 = heaviest
+  const int pair = PAIR ? a.n_pairs - 1 - (2 * unit + (int)rank) : a.n_pairs - 1 - unit;  // < 0: no rows
+  const int lead_pair = PAIR ? a.n_pairs - 1 - 2 * unit : pair;  // sets the pages both CTAs walk
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < Cfg::STAGES; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 8);
+      mbar_init(&p_full[i], 8 * (PAIR + 1));
       mbar_init(&pv_full[i], 1);
     }
-    mbar_init(q_full, 16);
+    mbar_init(q_full, 16 * (PAIR + 1));
     fence_barrier_init();
   }
-  if (warp == 17) tmem_alloc(tmem_slot, 512);
+  if constexpr (PAIR) {
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrive / TMA
+    if (warp == 17) tmem_alloc_cg2(tmem_slot, 512);
+  } else {
+    if (warp == 17) tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -160,7 +182,7 @@ __global__ void __launch_bounds__(576, 1)
   griddep_wait();  // PDL: q / the scattered K/V come from the previous kernel
   griddep_launch();
   // last valid token of the pair decides how many KV pages the CTA walks
-  const int last_tok = min((2 * pair + 2) * a.T, a.n_q) - 1;
+  const int last_tok = min((2 * lead_pair + 2) * a.T, a.n_q) - 1;
   const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
 
   if (warp == 16) {
@@ -170,51 +192,75 @@ __global__ void __launch_bounds__(576, 1)
       tma_prefetch(&tmV);
       const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
       for (int j = 0; j < n_kv_tiles; ++j) {
-        const int st = j % Cfg::STAGES;
-        const uint32_t ph = (uint32_t)(j / Cfg::STAGES) & 1;
+        const int st = j % NST;
+        const uint32_t ph = (uint32_t)(j / NST) & 1;
         mbar_wait(&kv_empty[st], ph ^ 1);
         attn_stamp(a, 7, j);
-        uint8_t* sk = sKV + st * 2 * Cfg::KV_BYTES;
-        uint8_t* sv = sk + Cfg::KV_BYTES;
+        uint8_t* sk = sKV + st * 2 * KVB;
+        uint8_t* sv = sk + KVB;
         const int row = (int)(head_row + (long)a.page_table[j] * 128);
-        mbar_expect_tx(&kv_full[st], 2 * Cfg::KV_BYTES);
+        if constexpr (PAIR) {
+          // keys [64 rank, +64) of K (2 atoms of 64 rows), dims [64 rank, +64) of V; all
+          // four halves land on the leader's barrier (only its MMA waits)
+          if (rank == 0) mbar_expect_tx(&kv_full[st], 4 * KVB);
+          tma_load_2d_cg2(sk, &tmK, &kv_full[st], 0, row + (int)rank * 64);
+          tma_load_2d_cg2(sk + 8192, &tmK, &kv_full[st], 64, row + (int)rank * 64);
+          tma_load_2d_cg2(sv, &tmV, &kv_full[st], (int)rank * 64, row);
+        } else {
+          mbar_expect_tx(&kv_full[st], 2 * Cfg::KV_BYTES);
 #pragma unroll
-        for (int at = 0; at < Cfg::ATOMS; ++at) {
-          tma_load_2d(sk + at * 16384, &tmK, &kv_full[st], at * 64, row);
-          tma_load_2d(sv + at * 16384, &tmV, &kv_full[st], at * 64, row);
+          for (int at = 0; at < Cfg::ATOMS; ++at) {
+            tma_load_2d(sk + at * 16384, &tmK, &kv_full[st], at * 64, row);
+            tma_load_2d(sv + at * 16384, &tmV, &kv_full[st], at * 64, row);
+          }
         }
       }
     }
   } else if (warp == 17) {
+   if (!PAIR || rank == 0) {
     // ------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc_s = make_idesc_bf16(128, 128);
-    constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
+    constexpr uint32_t idesc_s = make_idesc_bf16(128 * (PAIR + 1), 128);
+    constexpr uint32_t idesc_o = make_idesc_bf16(128 * (PAIR + 1), DKP, /*b_mn_major=*/true);
     mbar_wait(q_full, 0);
     tc_fence_after();
     const uint32_t q_addr = smem_u32(sQ);
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (PAIR) umma_commit_cg2(bar);  // arrives in both CTAs
+      else umma_commit(bar);
+    };
     auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-      const int st = j % Cfg::STAGES;
-      const uint32_t k_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES);
+      const int st = j % NST;
+      const uint32_t k_addr = smem_u32(sKV + st * 2 * KVB);
       if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < DKP / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_bf16(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
-                    sdesc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          const uint32_t koff = (kk >> 2) * (PAIR ? 8192 : 16384) + (kk & 3) * 32;
+          if constexpr (PAIR)
+            umma_bf16_cg2(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                          sdesc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+          else
+            umma_bf16(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                      sdesc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[t]);
+        commit(&s_full[t]);
       }
       __syncwarp();
     };
     auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P from TMEM
-      const int st = j % Cfg::STAGES;
-      const uint32_t v_addr = smem_u32(sKV + st * 2 * Cfg::KV_BYTES + Cfg::KV_BYTES);
+      const int st = j % NST;
+      const uint32_t v_addr = smem_u32(sKV + st * 2 * KVB + KVB);
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                       sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(&pv_full[t]);
+        for (int kk = 0; kk < 8; ++kk) {
+          if constexpr (PAIR)
+            umma_bf16_ts_cg2(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                             sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          else
+            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                         sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        commit(&pv_full[t]);
       }
       __syncwarp();
     };
@@ -229,7 +275,7 @@ __global__ void __launch_bounds__(576, 1)
       if (lane == 0) attn_stamp(a, 4, j);
       issue_pv(0, j);
       if (more) {
-        mbar_wait(&kv_full[(j + 1) % Cfg::STAGES], (uint32_t)((j + 1) / Cfg::STAGES) & 1);
+        mbar_wait(&kv_full[(j + 1) % NST], (uint32_t)((j + 1) / NST) & 1);
         tc_fence_after();
         if (lane == 0) attn_stamp(a, 6, j);
         issue_s(0, j + 1);  // in-order after PV_A(j): P_A's TMEM columns are free again
@@ -238,10 +284,11 @@ __global__ void __launch_bounds__(576, 1)
       tc_fence_after();
       if (lane == 0) attn_stamp(a, 5, j);
       issue_pv(1, j);
-      if (elect_one()) umma_commit(&kv_empty[j % Cfg::STAGES]);
+      if (elect_one()) commit(&kv_empty[j % NST]);
       __syncwarp();
       if (more) issue_s(1, j + 1);
     }
+   }
   } else {
     // ---------------------------------------------------------------- softmax
     // warp w: tile t = w/8, TMEM lane quarter w%4, key-column half h = (w/4)%2
@@ -251,14 +298,15 @@ __global__ void __launch_bounds__(576, 1)
     const int r = quarter * 32 + lane;  // 0..127 == TMEM lane
     const int bar_id = 1 + t * 4 + quarter;  // the two column halves of these 32 rows
     const int b = 2 * pair + t;
+    const bool has_tile = pair >= 0 && b < a.n_tiles;  // (a pair CTA may have no rows)
     const int hj = r / a.T;
     const int ti = r - hj * a.T;
     const int tok = b * a.T + ti;
-    const bool valid = hj < a.G && tok < a.n_q && b < a.n_tiles;
+    const bool valid = has_tile && hj < a.G && tok < a.n_q;
     const int head = g * a.G + hj;
     const int tile_last = min((b + 1) * a.T, a.n_q) - 1;
-    const int min_pos = b < a.n_tiles ? a.pos[b * a.T] : 0x7fffffff;
-    const int my_pos = valid ? a.pos[tok] : (b < a.n_tiles ? a.pos[tile_last] : 0x7fffffff);
+    const int min_pos = has_tile ? a.pos[b * a.T] : 0x7fffffff;
+    const int my_pos = valid ? a.pos[tok] : (has_tile ? a.pos[tile_last] : 0x7fffffff);
     const uint32_t lb = (uint32_t)((quarter * 32) << 16);
     const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
     const float sl2 = a.scale_log2;
@@ -276,7 +324,10 @@ __global__ void __launch_bounds__(576, 1)
       fence_proxy_async_smem();
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(q_full);
+    if (lane == 0) {
+      if (PAIR && rank != 0) mbar_arrive_cluster(q_full, 0);  // the leader's MMA waits
+      else mbar_arrive(q_full);
+    }
 
     float m_run = -INFINITY, l_run = 0.f;  // m in log2 units; l: this half's row sum
     float* red = reinterpret_cast<float*>(sKV + Cfg::STAGES * 2 * Cfg::KV_BYTES + 256);  // [2][2 tiles][2][128]
@@ -374,7 +425,10 @@ __global__ void __launch_bounds__(576, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (lane == 0) {
+        if (PAIR && rank != 0) mbar_arrive_cluster(&p_full[t], 0);  // remote: the leader's MMA waits
+        else mbar_arrive(&p_full[t]);
+      }
       if ((warp & 7) == 0 && lane == 0) attn_stamp(a, 2 + t, j);
     }
     mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
@@ -402,9 +456,11 @@ __global__ void __launch_bounds__(576, 1)
     tc_fence_before();
   }
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // no TMEM use or remote arrive left in either CTA
   if (warp == 17) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if constexpr (PAIR) tmem_dealloc_cg2(tmem, 512);
+    else tmem_dealloc(tmem, 512);
   }
 }
 
@@ -706,6 +762,35 @@ static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnA
   return PKV_OK;
 }
 
+// CTA-pair launch: clusters of 2, grid = 2 * Hkv * ceil(n_pairs / 2)
+template <int POLY>
+static int launch_attn_pair(const CUtensorMap& tk64, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
+  using Cfg = AttnCfg<128>;
+  auto kern = attn_tc_kernel<128, POLY, 1>;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [&] { err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM); });
+  if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn pair smem attr: %s", cudaGetErrorString(err));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * a.Hkv * ((a.n_pairs + 1) / 2));
+  cfg.blockDim = dim3(576);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, kern, tk64, tv, a);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("attn_tc_kernel (CTA pairs)");
+  return PKV_OK;
+}
+
 static unsigned long long* g_attn_trace = nullptr;
 
 // q/out: [n_q][H][dkp] bf16; k_pool/v_pool: [L][Hkv][pool_tokens][dkp] bf16 (whole pool)
@@ -765,6 +850,13 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
     PKV_LAUNCHED();
     PKV_CHECK_LAUNCH("attn_tc3_kernel");
     return PKV_OK;
+  }
+  static const bool pair_env = getenv("PKV_ATTN_PAIR") && getenv("PKV_ATTN_PAIR")[0] == '1';
+  if (dkp == 128 && pair_env && poly == 1) {
+    CUtensorMap tk64;
+    if (!cached_tmap(&tk64, k_pool, pool_rows_total, dkp, dkp, 64))
+      return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
+    return launch_attn_pair<1>(tk64, tv, a, stream);
   }
   if (dkp == 128) {
     if (poly == 1) return launch_attn<128, 1>(tk, tv, a, stream);
