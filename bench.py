@@ -282,7 +282,11 @@ def main():
         pipe.step()
     torch.cuda.synchronize()
     # eager steps with the native timers (CUDA events on the launching stream around each
-    # kernel group): per-kernel device times for the roofline; counts our launches
+    # kernel group): per-kernel device times for the roofline; counts our launches.  The
+    # final pass runs serially here: overlapped with Stage II (the timed graph) its timer
+    # scopes would include the per-layer waits and the time shared with Stage II kernels.
+    overlap = pipe.final_overlap
+    pipe.final_overlap = False
     _lib.timing(True)
     n0 = _lib.launch_count()
     for _ in range(args.steps):
@@ -291,6 +295,7 @@ def main():
     launches_per_step = (_lib.launch_count() - n0) // args.steps
     phases = _lib.timing_collect()
     _lib.timing(False)
+    pipe.final_overlap = overlap
     eager_phases = {n: (v[0] / args.steps, v[1]) for n, v in phases.items()}
     phases = {n: (v[0] / args.steps, v[1] / args.steps) for n, v in phases.items()}
     # CUDA graph of one step for the timed region (eager launches if capture fails,
