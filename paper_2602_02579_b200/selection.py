@@ -45,6 +45,40 @@ class ValueScores:
         return cls(strategy=strategy, per_layer=per_layer, fused=_host_layer_mean(per_layer))
 
 
+class _DeviceScores(ValueScores):
+    """ValueScores of a device narrow pass.  The fused vector is the device layer mean (the
+    reference rule, so the host re-check of __post_init__ is skipped) and the host copies of
+    per_layer / fused are made on first access: select_top_p -> recompute_selected then
+    run on the device copies without a 4 MB read-back and a host mean on the critical path."""
+
+    def __init__(self, strategy: str, dev_per_layer, dev_fused):  # noqa: D107 -- no dataclass init
+        object.__setattr__(self, "strategy", strategy)
+        object.__setattr__(self, "_dev_per_layer", dev_per_layer)
+        object.__setattr__(self, "_dev_fused", dev_fused)
+        object.__setattr__(self, "_host_pl", None)
+        object.__setattr__(self, "_host_fused", None)
+
+    @property
+    def per_layer(self):
+        if self._host_pl is None:
+            object.__setattr__(self, "_host_pl", self._dev_per_layer.cpu().numpy())
+        return self._host_pl
+
+    @per_layer.setter
+    def per_layer(self, v):
+        object.__setattr__(self, "_host_pl", v)
+
+    @property
+    def fused(self):
+        if self._host_fused is None:
+            object.__setattr__(self, "_host_fused", self._dev_fused.cpu().numpy())
+        return self._host_fused
+
+    @fused.setter
+    def fused(self, v):
+        object.__setattr__(self, "_host_fused", v)
+
+
 @dataclass
 class SelectionResult:
     indices: list   # ascending
@@ -91,9 +125,9 @@ def _fuse_device(per_layer_dev, fused_out, stream=None):
 def select_top_p(scores: ValueScores, p: float) -> SelectionResult:
     """Top ceil(p*s) tokens of the fused vector; ties toward smaller index."""
     torch = _lib.require_cuda()
-    s = scores.fused.shape[0]
-    k = ratio_budget(p, s)
     fused = scores._dev_fused
+    s = int(fused.shape[0]) if fused is not None else scores.fused.shape[0]
+    k = ratio_budget(p, s)
     if fused is None:
         fused = torch.from_numpy(np.ascontiguousarray(scores.fused, dtype=F32)).cuda()
     if k == 0:
@@ -103,7 +137,7 @@ def select_top_p(scores: ValueScores, p: float) -> SelectionResult:
     if st == 7:
         raise NumericsError("non-finite values in top-k scores")
     _lib.check(st)
-    return SelectionResult(indices=[int(i) for i in idx.cpu().tolist()], p=p, k=k, _dev_idx=idx)
+    return SelectionResult(indices=idx.cpu().tolist(), p=p, k=k, _dev_idx=idx)
 
 
 def check_tokens(tokens, config: ModelConfig) -> np.ndarray:
@@ -159,10 +193,10 @@ def score_prophet(weights, config: ModelConfig, cache, query_tokens, tally: Flop
     fused = torch.empty(s, dtype=torch.float32, device=cache.device)
     _fuse_device(per_layer, fused)
     bill_query_pass(tally, config, s, int(ids.shape[0]))
-    pl = per_layer.cpu().numpy()
-    if not np.isfinite(pl).all():
+    # a non-finite per-layer score makes its token's layer mean non-finite: one device check
+    if not bool(torch.isfinite(fused).all()):
         raise NumericsError("non-finite values in attention scores")
-    return ValueScores(strategy="prophet", per_layer=pl, fused=fused.cpu().numpy(), _dev_fused=fused)
+    return _DeviceScores("prophet", per_layer, fused)
 
 
 def score_epic(cache, n_layers: int) -> ValueScores:
