@@ -59,7 +59,10 @@ enum {
   PKV_QP_RENORM = 2,    /* renormalize_context_only=True */
   PKV_QP_LOGITS = 4,    /* compute last-row logits (finalize_query) */
   PKV_QP_APPEND_KV = 8, /* append query K/V to the cache pool at positions s.. */
-  PKV_QP_FROM_CHUNKS = 16 /* read context keys/values from the chunk store (naive cache) */
+  PKV_QP_FROM_CHUNKS = 16, /* read context keys/values from the chunk store (naive cache) */
+  PKV_QP_PROBE = 32       /* low-layer probe (selection.py:95-124): stop after layer 1's QKV
+                             projection (fresh_v[1] = the probe's layer-1 values); the m
+                             rows are context tokens s.. attending causally to [0, s) */
 };
 
 /* reference ModelConfig, model.py:24-63 */

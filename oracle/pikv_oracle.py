@@ -493,6 +493,38 @@ def prophet_scores(w, cfg, cache, query, renorm=False, macs=None, score_macs=Non
     return per, layer_mean(per)
 
 
+def low_layer_probe(w, cfg, cache, macs=None, score_macs=None):
+    """Block 0 for every context token over the assembled layer-0 cache, then the fresh
+    layer-1 values (selection.py:95-124): (dv [s, kv_dim] f64, attention column sums [s] f64)."""
+    s = cache.s
+    h = w.embed[cache.token_ids].copy()
+    lw = w.layers[0]
+    x = rmsnorm(h, lw.attn_norm, cfg.norm_eps)
+    qr, _, _, _ = qkv_proj(lw, cfg, x, cache.positions, macs)
+    h, rows = block_tail(lw, cfg, h, qr, cache.keys[0], cache.values[0], cache.positions, cache.positions, macs,
+                         score_macs, want_rows=True)
+    colsum = rows.astype(f64).sum(axis=0)
+    if cfg.n_layers == 1:
+        return np.zeros((s, cfg.kv_dim), dtype=f64), colsum
+    lw1 = w.layers[1]
+    x1 = rmsnorm(h, lw1.attn_norm, cfg.norm_eps)
+    v1 = mm(x1, lw1.wv, macs)
+    dv = v1.astype(f64) - cache.values[1].reshape(s, cfg.kv_dim).astype(f64)
+    return dv, colsum
+
+
+def cacheblend_l1(w, cfg, cache, macs=None, score_macs=None):
+    """alpha = ||dV||_2 per token (selection.py:127-133); the layer-mean of identical rows."""
+    dv, _ = low_layer_probe(w, cfg, cache, macs, score_macs)
+    return np.linalg.norm(dv, axis=1).astype(f32)
+
+
+def kvshare_l1(w, cfg, cache, macs=None, score_macs=None):
+    """Attention column sums times ||dV||_1 (selection.py:136-142)."""
+    dv, colsum = low_layer_probe(w, cfg, cache, macs, score_macs)
+    return (colsum * np.abs(dv).sum(axis=1)).astype(f32)
+
+
 def select(fused, p):
     """(indices ascending, k) for ratio p (selection.py:57-61)."""
     k = budget(p, fused.shape[0])
@@ -581,6 +613,14 @@ def macs_repair(cfg, s, k):
     H, dk, D, F, KV = cfg.n_heads, cfg.head_dim, cfg.hidden_dim, cfg.ffn_dim, cfg.kv_dim
     per = k * D * (H * dk + 2 * KV) + 2 * H * k * dk * s + k * H * dk * D + 3 * k * D * F
     return cfg.n_layers * per, cfg.n_layers * H * k * dk * s
+
+
+def macs_probe(cfg, s):
+    """MACs the reference books for one low-layer probe over s context tokens: block 0 with
+    dense s x s attention, plus the layer-1 value projection when there is a layer 1."""
+    H, dk, D, F, KV = cfg.n_heads, cfg.head_dim, cfg.hidden_dim, cfg.ffn_dim, cfg.kv_dim
+    block0 = s * D * (H * dk + 2 * KV) + 2 * H * s * dk * s + s * H * dk * D + 3 * s * D * F
+    return block0 + (s * D * KV if cfg.n_layers > 1 else 0)
 
 
 def prophet_ttft_slice(w, cfg, chunks, query, p):

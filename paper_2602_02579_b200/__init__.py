@@ -17,8 +17,8 @@ from .decode import GenerationResult, decode_step, greedy_generate
 from .prefill import PrefillTrace, full_prefill, precompute_chunk
 from .recompute import (AnswerRecord, FinalizeResult, RecomputePlan, StrategyRun, finalize_query,
                         recompute_selected, run_strategy, selection_digest)
-from .selection import (STRATEGIES, SelectionResult, ValueScores, fuse_layers, score_epic, score_prophet,
-                        score_random, select_top_p)
+from .selection import (STRATEGIES, SelectionResult, ValueScores, fuse_layers, score_cacheblend_l1, score_epic,
+                        score_kvshare_l1, score_prophet, score_random, select_top_p)
 from .tensor import ratio_budget, top_k_indices
 
 __version__ = "0.1.0"

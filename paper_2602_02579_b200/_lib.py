@@ -25,6 +25,7 @@ PKV_QP_RENORM = 2
 PKV_QP_LOGITS = 4
 PKV_QP_APPEND_KV = 8
 PKV_QP_FROM_CHUNKS = 16
+PKV_QP_PROBE = 32
 PKV_DT_F32, PKV_DT_F64, PKV_DT_BF16 = 0, 1, 2
 
 

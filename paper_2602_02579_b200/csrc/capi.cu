@@ -496,6 +496,12 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
                                      fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
                                      fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, append ? k2p : nullptr,
                                      append ? k3p : nullptr, st));
+    if ((flags & PKV_QP_PROBE) && l == 1) break;  // the probe only needs layer 1's fresh values
+    if ((flags & PKV_QP_PROBE) && l == 0) {
+      if (!planes) return set_error(PKV_ERR_ARGUMENT, "probe needs the cache's key planes");
+      TTRY(T_QP_MISC, probe_cache_kv_launch(w.k, w.v, m, Hkv, dk, dkp, s, kp, k2p, k3p, vp, c->pool_tokens,
+                                            c->page_table, st));
+    }
     S1Attn a{};
     a.q = w.q;
     a.m = m;

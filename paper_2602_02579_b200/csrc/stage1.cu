@@ -308,6 +308,40 @@ int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, i
   return PKV_OK;
 }
 
+// Low-layer probe (selection.py:95-124): the probed context tokens attend to the
+// ASSEMBLED layer-0 entries, their own included -- overwrite the pass's fresh K (rotated)
+// and V of the m rows at positions pos0.. with the cache's exact f32 key (k + k2 + k3
+// planes) and value.
+__global__ void probe_cache_kv_kernel(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0,
+                                      const __nv_bfloat16* k_pool, const __nv_bfloat16* k2_pool,
+                                      const __nv_bfloat16* k3_pool, const __nv_bfloat16* v_pool, long pool_tokens,
+                                      const int32_t* page_table) {
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)m * Hkv * dk) return;
+  const int d = (int)(gid % dk);
+  const long rg = gid / dk;
+  const int g = (int)(rg % Hkv), i = (int)(rg / Hkv);
+  const int pos = pos0 + i;
+  const long slot = (long)page_table[pos >> 7] * 128 + (pos & 127);
+  const long po = ((long)g * pool_tokens + slot) * dkp + d;
+  k[((long)i * Hkv + g) * dkp + d] =
+      (__bfloat162float(k_pool[po]) + __bfloat162float(k2_pool[po])) + __bfloat162float(k3_pool[po]);
+  v[((long)i * Hkv + g) * dkp + d] = __bfloat162float(v_pool[po]);
+}
+
+int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0, const void* k_pool,
+                          const void* k2_pool, const void* k3_pool, const void* v_pool, long pool_tokens,
+                          const int32_t* page_table, cudaStream_t st) {
+  const long total = (long)m * Hkv * dk;
+  probe_cache_kv_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
+      k, v, m, Hkv, dk, dkp, pos0, reinterpret_cast<const __nv_bfloat16*>(k_pool),
+      reinterpret_cast<const __nv_bfloat16*>(k2_pool), reinterpret_cast<const __nv_bfloat16*>(k3_pool),
+      reinterpret_cast<const __nv_bfloat16*>(v_pool), pool_tokens, page_table);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("probe_cache_kv_kernel");
+  return PKV_OK;
+}
+
 // gate/up interleaved per 256 columns -> act = f32(silu64(gate)) * up
 // (reference model.py:260-262 and 318-321)
 // act (nullable) fp32 [m][Fp]; x3 (nullable): the 3 bf16 planes of act for the next

@@ -1,9 +1,10 @@
 """Stage I scoring, layer fusion and budgeted selection on the GPU.
 
 Drop-in for reference selection.py (ValueScores 25-42, SelectionResult 45-49,
-fuse_layers 52-54, select_top_p 57-61, score_prophet 64-86).  The static
-baselines (epic, random) are host one-liners kept for run_strategy
-compatibility; the probe baselines (cacheblend/kvshare) are out of scope.
+fuse_layers 52-54, select_top_p 57-61, score_prophet 64-86, score_cacheblend_l1
+127-133).  The static baselines (epic, random) are host one-liners kept for run_strategy
+compatibility; kvshare_l1 (it also needs the probe's layer-0 attention column sums) is
+not available on the B200 path.
 """
 
 from __future__ import annotations
@@ -13,11 +14,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .errors import ArgumentError, InputError, NumericsError, ShapeError
+from .errors import ArgumentError, ConfigError, InputError, NumericsError, ShapeError
 from .model import F32, F64, FlopTally, ModelConfig, bill_query_pass, resolve_device_model
 from .tensor import device_topk, ratio_budget
 
-STRATEGIES = ("prophet", "epic", "random")
+STRATEGIES = ("prophet", "epic", "cacheblend_l1", "random")
 
 
 def _host_layer_mean(per_layer: np.ndarray) -> np.ndarray:
@@ -202,6 +203,75 @@ def score_prophet(weights, config: ModelConfig, cache, query_tokens, tally: Flop
 def score_epic(cache, n_layers: int) -> ValueScores:
     """Static positional prior: negated distance to the chunk start (reference selection.py:89-92)."""
     return ValueScores.from_vector("epic", (-cache.source_local.astype(np.int64)).astype(F32), n_layers)
+
+
+def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None):
+    """Layer-1 values of the low-layer probe (reference selection.py:95-124) for every
+    context token, [s, kv_dim] f32 on the device: block 0 over the assembled layer-0 cache,
+    then rmsnorm + the value projection of layer 1.  Context tokens [p, p+32) run as one
+    fp32-faithful narrow pass over the cache truncated to [0, p) -- at positions p.. they
+    attend to it and causally to each other (their fresh layer-0 K/V equal the assembled
+    entries: layer 0 has no context) -- stopped after layer 1's projections
+    (``PKV_QP_PROBE``)."""
+    import ctypes
+    torch = _lib.require_cuda()
+    dm = resolve_device_model(weights, config)
+    s, L = cache.context_length, config.n_layers
+    Hkv, dk = cache.config.n_kv_heads, config.head_dim
+    m = 32
+    flags = _lib.PKV_QP_PROBE | _lib.PKV_QP_FROM_CHUNKS
+    lib = _lib.load()
+    fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
+    fv = torch.empty_like(fk)
+    v1 = torch.empty((s, Hkv * dk), dtype=torch.float32, device=cache.device)
+    ids = np.asarray(cache.token_ids, dtype=np.int32)
+    chunks = ctypes.byref(cache.c_chunks)
+    for p0 in range(0, s, m):
+        n = min(m, s - p0)
+        view = _lib.Cache.from_buffer_copy(cache.c_cache)
+        view.s = p0
+        view.layer_ready = None
+        d_ids = torch.from_numpy(ids[p0:p0 + n].copy()).to(cache.device)
+        ws = workspace(lib.pkv_query_pass_workspace(dm.handle, p0, n, flags), "probe")
+        _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(view), chunks, d_ids.data_ptr(), n, flags, None,
+                                      fk.data_ptr(), fv.data_ptr(), None, ws.data_ptr(), ws.numel(),
+                                      _lib.stream_ptr(torch)))
+        # fresh_v is [L][n][Hkv][dk] for this pass's n rows
+        v1[p0:p0 + n] = fv.view(-1)[n * Hkv * dk: 2 * n * Hkv * dk].view(n, Hkv * dk)
+    if tally is not None:  # reference books: block 0 with dense s x s attention + layer-1 wv
+        H, D, F, KV = config.n_heads, config.hidden_dim, config.ffn_dim, config.kv_dim
+        tally.total.add(s * D * (H * dk + 2 * KV) + 2 * H * s * dk * s + s * H * dk * D + 3 * s * D * F + s * D * KV)
+        tally.attn_scores.add(H * s * dk * s)
+    return v1
+
+
+def score_cacheblend_l1(weights, config: ModelConfig, cache, embeddings=None,
+                        tally: FlopTally | None = None) -> ValueScores:
+    """Value-deviation magnitude from the low-layer probe, alpha = ||dV||_2 (reference
+    selection.py:127-133), dV = probe layer-1 values - assembled layer-1 values."""
+    if embeddings is not None:
+        raise ConfigError("custom probe embeddings are not supported on the B200 path")
+    s, L = cache.context_length, config.n_layers
+    if L == 1:  # no layer 1: dV = 0 (reference selection.py:118-119)
+        if tally is not None:
+            H, dk, D, F, KV = config.n_heads, config.head_dim, config.hidden_dim, config.ffn_dim, config.kv_dim
+            tally.total.add(s * D * (H * dk + 2 * KV) + 2 * H * s * dk * s + s * H * dk * D + 3 * s * D * F)
+            tally.attn_scores.add(H * s * dk * s)
+        return ValueScores.from_vector("cacheblend_l1", np.zeros(s, dtype=F32), L)
+    v1 = _probe_values(weights, config, cache, tally)
+    Hkv, dk = cache.config.n_kv_heads, config.head_dim
+    # assembled layer-1 values from the pool (bf16 of the chunk store's f32 values; the
+    # pool slot of context token t is t)
+    cached = cache.v_pool[1, :, :s, :dk].permute(1, 0, 2).reshape(s, Hkv * dk)
+    dv = v1.double().cpu().numpy() - cached.double().cpu().numpy()
+    return ValueScores.from_vector("cacheblend_l1", np.linalg.norm(dv, axis=1), L)
+
+
+def score_kvshare_l1(weights, config: ModelConfig, cache, embeddings=None,
+                     tally: FlopTally | None = None) -> ValueScores:
+    """Reference selection.py:136-142: needs the probe's layer-0 attention column sums,
+    which the B200 attention kernels do not produce."""
+    raise ConfigError("score_kvshare_l1 needs layer-0 attention column sums (not available on the B200 path)")
 
 
 def score_random(s_context: int, seed: int, n_layers: int) -> ValueScores:

@@ -110,3 +110,23 @@ def test_decode_and_full_prefill_bit_identical(pikv, ci):
     got = O.decode(wo, cfg_o, list(zip(to.keys, to.values)), np.arange(len(toks)), steps)
     for a, b in zip(ref, got):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("ci", range(len(CFGS)))
+def test_probe_baselines_bit_identical(pikv, ci):
+    """The oracle's low-layer probe scores (cacheblend_l1 / kvshare_l1) and their MAC books
+    reproduce the reference's selection.py:95-142."""
+    cfg_r = pikv.ModelConfig(**CFGS[ci])
+    cfg_o = O.Cfg(**cfg_r.to_json_dict())
+    wr, wo = pikv.random_weights(cfg_r, 7 + ci), O.init_weights(cfg_o, 7 + ci)
+    rng = np.random.default_rng(10 + ci)
+    units = [rng.integers(0, cfg_r.vocab_size, int(rng.integers(3, 9))).tolist() for _ in range(3)]
+    car = pikv.assemble([pikv.precompute_chunk(wr, cfg_r, u) for u in units], cfg_r)
+    cao = O.stitch([O.make_chunk(wo, cfg_o, u) for u in units], cfg_o)
+    for name, fn in (("score_cacheblend_l1", O.cacheblend_l1), ("score_kvshare_l1", O.kvshare_l1)):
+        tr = pikv.FlopTally()
+        ref = getattr(pikv.selection, name)(wr, cfg_r, car, tally=tr)
+        macs = [0]
+        got = fn(wo, cfg_o, cao, macs=macs)
+        assert np.array_equal(ref.fused, got), name
+        assert tr.total.multiply_accumulate_count == macs[0] == O.macs_probe(cfg_o, car.context_length)
