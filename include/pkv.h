@@ -62,7 +62,11 @@ enum {
   PKV_QP_FROM_CHUNKS = 16, /* read context keys/values from the chunk store (naive cache) */
   PKV_QP_PROBE = 32       /* low-layer probe (selection.py:95-124): stop after layer 1's QKV
                              projection (fresh_v[1] = the probe's layer-1 values); the m
-                             rows are context tokens s.. attending causally to [0, s) */
+                             rows are context tokens s.. attending causally to [0, s) and
+                             to their own assembled layer-0 entries.  With PKV_QP_SCORES,
+                             per_layer[0..s) = layer 0's head/query-mean scores of the rows
+                             and per_layer[s..s+m) = sum over rows q >= i of row q's
+                             head-mean probability on block key i (kvshare column sums) */
 };
 
 /* reference ModelConfig, model.py:24-63 */

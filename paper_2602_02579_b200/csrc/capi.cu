@@ -557,6 +557,8 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.x3_ld = ldx;
     TTRY(T_QP_ATTN, s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
                             (flags & PKV_QP_RENORM) ? 1 : 0, cf.n_heads, w.rows64, comm, st));
+    if ((flags & PKV_QP_PROBE) && scores && l == 0)  // block keys' column sums after the context's
+      TTRY(T_QP_MISC, probe_diag_colsum_launch(w.q, w.k, w.Mfin, w.Lfin, m, H, Hkv, dk, dkp, a.scale, per_layer + s, st));
     // without logits (score_prophet) the last layer's o-projection and MLP only feed a
     // residual stream nobody reads: the per-layer scores are complete here
     if (l == cf.n_layers - 1 && !(flags & PKV_QP_LOGITS)) break;

@@ -92,6 +92,8 @@ int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lf
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st);
 int norm_defer_launch(const float* h, int m, long ld, int N, const float* g, void* xg, long ldxg, float* ssq,
                       int ssq_ld, cudaStream_t st);
+int probe_diag_colsum_launch(const float* q, const float* k, const float* Mfin, const float* Lfin, int m, int H,
+                             int Hkv, int dk, int dkp, float scale, float* out, cudaStream_t st);
 int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0, const void* k_pool,
                           const void* k2_pool, const void* k3_pool, const void* v_pool, long pool_tokens,
                           const int32_t* page_table, cudaStream_t st);

@@ -329,6 +329,43 @@ __global__ void probe_cache_kv_kernel(float* k, float* v, int m, int Hkv, int dk
   v[((long)i * Hkv + g) * dkp + d] = __bfloat162float(v_pool[po]);
 }
 
+// Low-layer probe, kvshare (selection.py:136-142): the block's own keys' share of the
+// layer-0 attention column sums, out[t] = sum_{q >= t} rows[q][t] over the block's queries
+// (rows = f32 head mean of the probabilities, reference model.py:296-305).  Scores are
+// recomputed exactly as s1_attn_pass1 forms the fresh-key scores (sequential f32 FMAs over
+// the padded head dim, then * scale) and normalised with the pass's final row max / sum.
+__global__ void probe_diag_colsum_kernel(const float* q, const float* k, const float* Mfin, const float* Lfin,
+                                         int m, int H, int Hkv, int dk, int dkp, float scale, float* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  constexpr float LOG2E = 1.4426950408889634f;
+  const int G = H / Hkv, R = m * G;
+  double col = 0.0;
+  for (int qi = t; qi < m; ++qi) {
+    double acc = 0.0;
+    for (int h = 0; h < H; ++h) {
+      const int g = h / G, j = h - g * G;
+      const float* qp = q + ((long)qi * H + h) * dkp;
+      const float* kp = k + ((long)t * Hkv + g) * dkp;
+      float sc = 0.f;
+      for (int d = 0; d < dkp; ++d) sc = fmaf(qp[d], kp[d], sc);
+      const float sv = sc * scale;
+      const int r = g * R + j * m + qi;
+      acc += (double)(ex2(fmaf(sv, LOG2E, -Mfin[r] * LOG2E)) * (1.f / Lfin[r]));
+    }
+    col += (double)(float)(acc / (double)H);
+  }
+  out[t] = (float)col;
+}
+
+int probe_diag_colsum_launch(const float* q, const float* k, const float* Mfin, const float* Lfin, int m, int H,
+                             int Hkv, int dk, int dkp, float scale, float* out, cudaStream_t st) {
+  probe_diag_colsum_kernel<<<ceil_div(m, 32), 32, 0, st>>>(q, k, Mfin, Lfin, m, H, Hkv, dk, dkp, scale, out);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("probe_diag_colsum_kernel");
+  return PKV_OK;
+}
+
 int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0, const void* k_pool,
                           const void* k2_pool, const void* k3_pool, const void* v_pool, long pool_tokens,
                           const int32_t* page_table, cudaStream_t st) {
@@ -968,7 +1005,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   }
-  if (a.S != nullptr && per_layer != nullptr) {
+  if (a.S != nullptr && per_layer != nullptr && a.s > 0) {  // (s = 0: no context keys to score)
     const int sgrid = std::min(ceil_div(a.s, 8), 8 * num_sms());
     const size_t ssmem = (size_t)a.Hkv * a.R * sizeof(float2);
     if (ssmem > 48 * 1024) {

@@ -22,7 +22,8 @@ from .chunkstore import assemble, mark_finalized
 from .errors import ArgumentError, ConfigError, InputError, StateError
 from .model import FlopTally, KVCache, ModelConfig, bill_query_pass, bill_repair, resolve_device_model
 from .selection import (STRATEGIES, SelectionResult, ValueScores, check_tokens, run_query_pass,
-                        score_cacheblend_l1, score_epic, score_prophet, score_random, select_top_p, workspace)
+                        score_cacheblend_l1, score_epic, score_kvshare_l1, score_prophet, score_random, select_top_p,
+                        workspace)
 
 
 @dataclass
@@ -223,6 +224,8 @@ def run_strategy(weights, config: ModelConfig, chunks, query_tokens, strategy: s
         scores = score_epic(cache, config.n_layers)
     elif strategy == "cacheblend_l1":
         scores = score_cacheblend_l1(weights, config, cache, tally=stage1)
+    elif strategy == "kvshare_l1":
+        scores = score_kvshare_l1(weights, config, cache, tally=stage1)
     elif strategy == "random":
         scores = score_random(s, seed, config.n_layers)
     else:

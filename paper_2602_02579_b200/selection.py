@@ -3,8 +3,8 @@
 Drop-in for reference selection.py (ValueScores 25-42, SelectionResult 45-49,
 fuse_layers 52-54, select_top_p 57-61, score_prophet 64-86, score_cacheblend_l1
 127-133).  The static baselines (epic, random) are host one-liners kept for run_strategy
-compatibility; kvshare_l1 (it also needs the probe's layer-0 attention column sums) is
-not available on the B200 path.
+compatibility; score_cacheblend_l1 / score_kvshare_l1 (136-142) run the low-layer probe
+as fp32-faithful narrow passes.
 """
 
 from __future__ import annotations
@@ -18,7 +18,7 @@ from .errors import ArgumentError, ConfigError, InputError, NumericsError, Shape
 from .model import F32, F64, FlopTally, ModelConfig, bill_query_pass, resolve_device_model
 from .tensor import device_topk, ratio_budget
 
-STRATEGIES = ("prophet", "epic", "cacheblend_l1", "random")
+STRATEGIES = ("prophet", "epic", "cacheblend_l1", "kvshare_l1", "random")
 
 
 def _host_layer_mean(per_layer: np.ndarray) -> np.ndarray:
@@ -38,6 +38,9 @@ class ValueScores:
         want = _host_layer_mean(self.per_layer)
         if self.fused.shape != want.shape or not np.allclose(self.fused, want, atol=1e-6):
             raise ArgumentError("fused scores must be the mean of the per-layer rows")
+
+    def _renamed(self, strategy: str) -> "ValueScores":
+        return ValueScores(strategy=strategy, per_layer=self.per_layer, fused=self.fused)
 
     @classmethod
     def from_vector(cls, strategy: str, vector, n_layers: int) -> "ValueScores":
@@ -205,7 +208,7 @@ def score_epic(cache, n_layers: int) -> ValueScores:
     return ValueScores.from_vector("epic", (-cache.source_local.astype(np.int64)).astype(F32), n_layers)
 
 
-def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None):
+def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None, want_colsum: bool = False):
     """Layer-1 values of the low-layer probe (reference selection.py:95-124) for every
     context token, [s, kv_dim] f32 on the device: block 0 over the assembled layer-0 cache,
     then rmsnorm + the value projection of layer 1.  Context tokens [p, p+32) run as one
@@ -219,8 +222,12 @@ def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None):
     s, L = cache.context_length, config.n_layers
     Hkv, dk = cache.config.n_kv_heads, config.head_dim
     m = 32
-    flags = _lib.PKV_QP_PROBE | _lib.PKV_QP_FROM_CHUNKS
+    flags = _lib.PKV_QP_PROBE | _lib.PKV_QP_FROM_CHUNKS | (_lib.PKV_QP_SCORES if want_colsum else 0)
     lib = _lib.load()
+    # kvshare: column sums of layer 0's head-mean attention over every context query;
+    # block [p, p+n) contributes n * (its mean row over keys < p) plus its own diagonal
+    colsum = np.zeros(s, dtype=F64) if want_colsum else None
+    pl = torch.empty(s + m, dtype=torch.float32, device=cache.device) if want_colsum else None
     fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
     fv = torch.empty_like(fk)
     v1 = torch.empty((s, Hkv * dk), dtype=torch.float32, device=cache.device)
@@ -233,16 +240,20 @@ def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None):
         view.layer_ready = None
         d_ids = torch.from_numpy(ids[p0:p0 + n].copy()).to(cache.device)
         ws = workspace(lib.pkv_query_pass_workspace(dm.handle, p0, n, flags), "probe")
-        _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(view), chunks, d_ids.data_ptr(), n, flags, None,
-                                      fk.data_ptr(), fv.data_ptr(), None, ws.data_ptr(), ws.numel(),
-                                      _lib.stream_ptr(torch)))
+        _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(view), chunks, d_ids.data_ptr(), n, flags,
+                                      pl.data_ptr() if pl is not None else None, fk.data_ptr(), fv.data_ptr(), None,
+                                      ws.data_ptr(), ws.numel(), _lib.stream_ptr(torch)))
+        if colsum is not None:
+            part = pl[: p0 + n].double().cpu().numpy()
+            colsum[:p0] += part[:p0] * n
+            colsum[p0:p0 + n] += part[p0:p0 + n]
         # fresh_v is [L][n][Hkv][dk] for this pass's n rows
         v1[p0:p0 + n] = fv.view(-1)[n * Hkv * dk: 2 * n * Hkv * dk].view(n, Hkv * dk)
     if tally is not None:  # reference books: block 0 with dense s x s attention + layer-1 wv
         H, D, F, KV = config.n_heads, config.hidden_dim, config.ffn_dim, config.kv_dim
         tally.total.add(s * D * (H * dk + 2 * KV) + 2 * H * s * dk * s + s * H * dk * D + 3 * s * D * F + s * D * KV)
         tally.attn_scores.add(H * s * dk * s)
-    return v1
+    return (v1, colsum) if want_colsum else v1
 
 
 def score_cacheblend_l1(weights, config: ModelConfig, cache, embeddings=None,
@@ -269,9 +280,18 @@ def score_cacheblend_l1(weights, config: ModelConfig, cache, embeddings=None,
 
 def score_kvshare_l1(weights, config: ModelConfig, cache, embeddings=None,
                      tally: FlopTally | None = None) -> ValueScores:
-    """Reference selection.py:136-142: needs the probe's layer-0 attention column sums,
-    which the B200 attention kernels do not produce."""
-    raise ConfigError("score_kvshare_l1 needs layer-0 attention column sums (not available on the B200 path)")
+    """Layer-0 attention column sums times ||dV||_1 from the same low-layer probe (reference
+    selection.py:136-142)."""
+    if embeddings is not None:
+        raise ConfigError("custom probe embeddings are not supported on the B200 path")
+    s, L = cache.context_length, config.n_layers
+    if L == 1:  # dV = 0, so colsum * ||dV||_1 = 0 (reference selection.py:118-119)
+        return score_cacheblend_l1(weights, config, cache, None, tally)._renamed("kvshare_l1")
+    v1, colsum = _probe_values(weights, config, cache, tally, want_colsum=True)
+    Hkv, dk = cache.config.n_kv_heads, config.head_dim
+    cached = cache.v_pool[1, :, :s, :dk].permute(1, 0, 2).reshape(s, Hkv * dk)
+    dv = v1.double().cpu().numpy() - cached.double().cpu().numpy()
+    return ValueScores.from_vector("kvshare_l1", colsum * np.abs(dv).sum(axis=1), L)
 
 
 def score_random(s_context: int, seed: int, n_layers: int) -> ValueScores:

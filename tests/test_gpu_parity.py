@@ -309,6 +309,27 @@ def test_flop_books_follow_reference_formulas(built):
 
 
 @pytest.mark.parametrize("case", ["tiny_ref", "c1", "llama_width"])
+def test_kvshare_probe_matches_oracle(built, case):
+    """score_kvshare_l1 (reference selection.py:136-142): layer-0 column sums x ||dV||_1."""
+    P = built
+    cfg_o, seed, units, query, p = _materialise(case)
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg, mw, dch = _device_inputs(P, cfg_o, w, chunks)
+    cache = P.assemble(dch, cfg, fp32_taps=False)
+    tally = P.FlopTally()
+    got = P.score_kvshare_l1(mw, cfg, cache, tally=tally).fused
+    ref = O.kvshare_l1(w, cfg_o, O.stitch(chunks, cfg_o))
+    assert tally.total.multiply_accumulate_count == O.macs_probe(cfg_o, cache.context_length)
+    err = float(np.abs(got - ref).max()) / max(float(np.abs(ref).max()), 1e-30)
+    assert err <= 1e-4, err
+    sel_ref, k = O.select(ref, p)
+    sel = P.select_top_p(P.ValueScores.from_vector("kvshare_l1", got, cfg.n_layers), p)
+    assert _selection_ok(sel.indices, sel_ref, ref, k)
+    _report(case=f"{case}_kvshare", s=cache.context_length, k=k, probe_max_rel=err,
+            sel_symdiff=len(set(sel.indices) ^ set(sel_ref)))
+
+
+@pytest.mark.parametrize("case", ["tiny_ref", "c1", "llama_width"])
 def test_cacheblend_probe_matches_oracle(built, case):
     """score_cacheblend_l1 (reference selection.py:127-133): the fp32-faithful probe passes
     reproduce the oracle's ||dV||_2 and its MAC books, and select the same tokens."""
