@@ -218,13 +218,14 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   if (epi == EPI_PROJ && args.stream_k) {
     // stream-K grid G (stream_k > 1: requested G): every CTA gets >= 1 unit and an m-tile is cut into <= 16 pieces
     // (the partial buffer holds 16 per tile).  PKV_PROJ_SK_GRID overrides (tuning).
-    const long units = (long)ceil_div(args.M, 128) * kt;
+    const long tm = ceil_div(args.M, 128 * gemm_mt(96, EPI_PROJ));  // m-tiles of the kernel
+    const long units = tm * kt;
     static const int g_env = getenv("PKV_PROJ_SK_GRID") ? atoi(getenv("PKV_PROJ_SK_GRID")) : 0;
     // 128 CTAs measured best on B200 for all four Llama-8B shapes (tools/bench_proj.py:
     // 101 us per layer vs 107 on all 148 SMs and 127 for the old split-K cost model)
     long g = args.stream_k > 1 ? args.stream_k : (g_env > 0 ? g_env : std::min(128, num_sms()));
     g = std::min(g, units);
-    g = std::min(g, 15L * ceil_div(args.M, 128));
+    g = std::min(g, 15L * tm);
     args.stream_k = (int)std::max(1L, g);
     args.n_splits = 1;
     args.k_tiles_per_split = kt;

@@ -92,8 +92,15 @@ __device__ __forceinline__ void gemm_stamp(const GemmArgs& a, int i) {
 // projections (tools/bench_proj.py, graph-captured): BK = 128 and MT = 2 were both slower
 // or neutral (per-SM smem fill, not the barrier round trip or the B traffic, bounds them),
 // so both stay at 1 atom / 1 sub-tile; the knobs are kept for re-tuning.
+// PKV_PROJ_MT (compile time): weight sub-tiles per narrow-projection CTA.  2 (44 KB stages,
+// 27 % less activation fill per weight byte) measured 1.5-2x slower with stream-K
+// (tools/bench_proj.py: wgu 62 vs 46 us, wd 41 vs 27 us): 5 stages of 44 KB keep fewer
+// weight bytes in flight per SM than 7 of 28 KB.
+#ifndef PKV_PROJ_MT
+#define PKV_PROJ_MT 1
+#endif
 constexpr int gemm_bk(int bn) { return 64; }
-constexpr int gemm_mt(int bn, int epi) { return 1; }
+constexpr int gemm_mt(int bn, int epi) { return (bn == 96 && epi == 5 /*EPI_PROJ*/) ? PKV_PROJ_MT : 1; }
 // CG = 2: CTA pair (cluster of 2, cta_group::2).  One MMA tile is 256 x BN: each CTA
 // loads its 128 rows of A and HALF of B (BN/2 rows), the leader issues M = 256 MMAs that
 // read both CTAs' shared memory, and each CTA's TMEM receives its 128 rows x BN.  Per SM
@@ -101,7 +108,7 @@ constexpr int gemm_mt(int bn, int epi) { return 1; }
 // k step), the canonical Blackwell GEMM shape.
 template <int BN, int EPI, int CG = 1>
 struct GemmCfg {
-  static constexpr int BM = 128, BK = gemm_bk(BN), MT = gemm_mt(BN, EPI), BMT = BM * MT * CG;
+  static constexpr int BM = 128, BK = gemm_bk(BN), MT = CG == 2 ? 1 : gemm_mt(BN, EPI), BMT = BM * MT * CG;
   static constexpr int BN_CTA = BN / CG;                            // B rows held by one CTA
   static constexpr int ATOMS = BK / 64;
   static constexpr int A_ATOM = BM * 128, B_ATOM = BN_CTA * 128;  // bytes of one 64-column atom
