@@ -94,8 +94,8 @@ __device__ __forceinline__ void gemm_stamp(const GemmArgs& a, int i) {
 // so both stay at 1 atom / 1 sub-tile; the knobs are kept for re-tuning.
 // PKV_PROJ_MT (compile time): weight sub-tiles per narrow-projection CTA.  2 (44 KB stages,
 // 27 % less activation fill per weight byte) measured 1.5-2x slower with stream-K
-// (tools/bench_proj.py: wgu 62 vs 46 us, wd 41 vs 27 us): 5 stages of 44 KB keep fewer
-// weight bytes in flight per SM than 7 of 28 KB.
+// (tools/bench_proj.py: wgu 62 vs 46 us, wd 41 vs 27 us), so the stage count and not the
+// activation share of the fill sets the per-CTA stream rate.
 #ifndef PKV_PROJ_MT
 #define PKV_PROJ_MT 1
 #endif
