@@ -84,6 +84,11 @@ CASES = {
     "c1_p40": (O.Cfg(2, 4, 2, 64, 256, 1024, 1024), 0, "8x256", 32, 0.4),
     # configs[1] geometry: Mistral-7B layer width, theta 1e6, ragged chunks
     "mistral_width": (O.Cfg(2, 32, 8, 128, 4096, 14336, 2048, rope_theta=1000000.0), 3, "ragged", 24, 0.1),
+    # edge cases: one chunk with a one-token query; a query longer than the 32-row narrow
+    # tile (unfused projection path); four layers with odd chunk lengths
+    "c1_single_m1": (O.Cfg(2, 4, 2, 64, 256, 1024, 1024), 5, "1x200", 1, 0.5),
+    "c1_m40": (O.Cfg(2, 4, 2, 64, 256, 1024, 1024), 6, "4x128", 40, 0.2),
+    "tiny_deep": (O.Cfg(4, 4, 2, 16, 64, 128, 256), 7, "5x37", 7, 0.25),
 }
 
 
