@@ -408,6 +408,9 @@ def replace_entries(cache: AssembledCache, layer: int, indices, new_keys, new_va
     chunkstore.py:143-160), scattering into the bf16 pool on the GPU."""
     if not 0 <= layer < cache.n_layers:
         raise ArgumentError(f"layer {layer} out of range for {cache.n_layers} layers")
+    # a later finalize_query must see this write: no overlap with the preceding repair
+    # (recompute.finalize_query only follows Stage II's per-layer events)
+    cache._final_follow = None
     idx = np.asarray(indices, dtype=np.int64)
     if idx.ndim != 1:
         raise ShapeError("indices must be 1-D")
