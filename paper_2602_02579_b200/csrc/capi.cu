@@ -724,8 +724,18 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
       g.k2_pool = reinterpret_cast<__nv_bfloat16*>(c->k2_pool) + l * layer_pool;
       g.k3_pool = reinterpret_cast<__nv_bfloat16*>(c->k3_pool) + l * layer_pool;
     }
-    // K/V of every selected token are in the cache before this layer's attention
-    TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    // K/V of every selected token are in the cache before this layer's attention.  The last
+    // layer of a repair only scatters K/V (its attention / o / MLP are dead, below): skip
+    // the query rows of wqkv.
+    if (l == cf.n_layers - 1 && !need_final_h) {
+      g.N = 2 * Hkv * dkp;
+      g.head0 = H;
+      TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp,
+                                    reinterpret_cast<const __nv_bfloat16*>(lw.wqkv) + (long)H * dkp * Dp, Dp, Dp, g,
+                                    st));
+    } else {
+      TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    }
     if (c->layer_done != nullptr && c->layer_done[l] != nullptr)
       cudaEventRecord(reinterpret_cast<cudaEvent_t>(c->layer_done[l]), st);
     if (l == cf.n_layers - 1 && !need_final_h) break;

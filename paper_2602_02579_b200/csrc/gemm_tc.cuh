@@ -47,6 +47,7 @@ struct GemmArgs {
   __nv_bfloat16* k3_pool;
   __nv_bfloat16* knr_out;     // optional bf16 [M][Hkv][dkp]: keys BEFORE RoPE (chunk-store layout)
   __nv_bfloat16* vcap_out;    // optional bf16 [M][Hkv][dkp]: values (chunk-store layout)
+  int head0;                  // first head of the GEMM's N range (H: K and V rows only)
   // EPI_PROJ ---------------------------------------------------------------
   float* out;                 // [mrows][ldo]
   long ldo;
@@ -660,8 +661,8 @@ __global__ void __launch_bounds__(192, 1)
           } else if constexpr (EPI == EPI_QKV) {
             // a 32-column chunk never straddles a head (dkp is 64 or 128)
             const int dkp = args.dkp;
-            const int head_all = col0 / dkp;  // 0..H+2Hkv-1
-            const int d0 = col0 - head_all * dkp;
+            const int d0 = col0 % dkp;
+            const int head_all = col0 / dkp + args.head0;  // 0..H+2Hkv-1
             const int H = args.n_heads, Hkv = args.n_kv_heads;
             const int pos = args.pos[row];
             const bool is_v = head_all >= H + Hkv;
