@@ -15,18 +15,20 @@
  *     map 1:1 onto pikv.errors classes); pkv_last_error() gives a thread-local
  *     message.
  *
- * Device layouts (bf16 = IEEE bfloat16, little endian):
+ * Device layouts (bf16 = IEEE bfloat16, fp16 = IEEE binary16, little endian):
  *   dkp  = 64 if head_dim <= 64 else 128 (head dims zero-padded)
  *   Dp   = hidden_dim rounded up to 64,  Fp = ffn_dim rounded up to 128
  *   NQKV = (n_heads + 2*n_kv_heads) * dkp
- *   weights are transposed ("output-major", K contiguous):
+ *   projection weights are fp16, transposed ("output-major", K contiguous) and
+ *   pre-scaled by a power of two per matrix (stored = w * 2^e, wscale = 2^-e):
  *     wqkv [NQKV][Dp]  rows = q heads, k heads, v heads, each dkp rows
  *     wo   [Dp][n_heads*dkp]
  *     wgu  [2*Fp][Dp]  gate/up interleaved in blocks of 128 rows
  *     wd   [Dp][Fp]
- *     embed, lm_head [vocab][Dp];   norm gains fp32 [Dp]
+ *     embed, lm_head: bf16 [vocab][Dp];   norm gains fp32 [Dp]
  *   chunk store (one buffer per chunk): bf16 [n_layers][t_c][n_kv_heads][dkp], keys UNROTATED
- *   paged KV cache: bf16 K and V pools [n_layers][n_kv_heads][pool_tokens][dkp];
+ *   paged KV cache: fp16 K and V pools [n_layers][n_kv_heads][pool_tokens][dkp], plus the
+ *     fp16 key residual plane k2_pool = fp16(f32 key - K) (same layout);
  *     token t lives in slot page_table[t / 128] * 128 + t % 128
  *   RoPE tables: float64 cos/sin [rope_len][head_dim/2], angle = pos * theta^(-2i/d)
  */
@@ -83,6 +85,7 @@ typedef struct pkv_layer_weights {
   const void* wo;
   const void* wgu;
   const void* wd;
+  float wscale[4];  /* 2^-e of wqkv, wo, wgu, wd (see "Device layouts") */
 } pkv_layer_weights;
 
 /* reference ModelWeights, model.py:79-160 */
@@ -106,13 +109,13 @@ typedef struct pkv_cache {
   int32_t rope_len;          /* positions covered (>= s + query length) */
   const uint8_t* recomputed; /* nullable [s]: 1 = entry repaired by Stage II (read from the pool
                                 even when a query pass reads the others from the chunk store) */
-  void* k2_pool;             /* residual key planes, same layout as k_pool: the f32 key is exactly */
-  void* k3_pool;             /* k_pool + k2_pool + k3_pool (bf16 each); used by the narrow passes  */
+  void* k2_pool;             /* residual key plane, same layout as k_pool: the f32 key is k_pool +
+                                k2_pool to 2^-22 (fp16 each); used by the fp32-faithful narrow passes */
   void* const* layer_ready;  /* nullable host array [n_layers] of cudaEvent_t: a query pass makes its
                                 stream wait on layer_ready[l] before reading layer l (pipelined
                                 host->device chunk transfer + per-layer assembly) */
   const float* rope_cs32;    /* nullable [rope_len][head_dim/2][2]: (cos, sin) of the float64 tables
-                                rounded to f32, used by the bf16 Stage-II RoPE epilogue (the
+                                rounded to f32, used by the fp16 Stage-II RoPE epilogue (the
                                 fp32-faithful paths and assembly always use the float64 tables) */
   void* const* layer_done;   /* nullable host array [n_layers] of cudaEvent_t: pkv_recompute records
                                 layer_done[l] once layer l's K/V are final (after its QKV scatter),
@@ -170,7 +173,7 @@ int pkv_topk(const float* scores, int32_t n, int32_t k, int32_t* idx_out, int32_
  * all selected tokens are written into the cache first (replace_entries,
  * chunkstore.py:143-160), then the selected queries attend over the updated
  * layer with mask pos_kv <= pos_sel.  tap_k/tap_v (nullable): fp32
- * [L][k][Hkv][head_dim] copies of the recomputed K/V before bf16 storage. */
+ * [L][k][Hkv][head_dim] copies of the recomputed K/V before fp16 storage. */
 size_t pkv_recompute_workspace(const pkv_model* m, int32_t k);
 int pkv_recompute(const pkv_model* m, const pkv_cache* cache, const int32_t* sel, int32_t k, float* tap_k,
                   float* tap_v, void* workspace, size_t workspace_bytes, void* stream);
@@ -179,7 +182,7 @@ int pkv_recompute(const pkv_model* m, const pkv_cache* cache, const int32_t* sel
  * device: the Stage-II layer loop over every position 0..s-1 of `cache` (its token_ids
  * are the sequence; K/V land in its pool, RoPE'd at 0..s-1).  Optional captures:
  * k_nr_out / v_out bf16 [L][s][Hkv][dkp] (the chunk-store layout; keys BEFORE RoPE),
- * logits_out f32 [s][vocab] (final norm + lm_head on the bf16 tensor cores). */
+ * logits_out f32 [s][vocab] (final norm + lm_head on the bf16 tensor cores; bf16 lm_head). */
 size_t pkv_full_prefill_workspace(const pkv_model* m, int32_t n);
 int pkv_full_prefill(const pkv_model* m, const pkv_cache* cache, void* k_nr_out, void* v_out, float* logits_out,
                      void* workspace, size_t workspace_bytes, void* stream);
@@ -190,7 +193,7 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* cache, int32_t l
 
 /* f32 view of one cache layer as keys_rebased/values ([s][Hkv][head_dim]).
  * chunks != NULL: derive from the chunk store (exact f32 rotation of the
- * assembled keys); chunks == NULL: read the bf16 cache. */
+ * assembled keys); chunks == NULL: read the fp16 cache (keys: k_pool + k2_pool). */
 int pkv_cache_view(const pkv_config* cfg, const pkv_cache* cache, const pkv_chunks* chunks, int32_t layer, int32_t is_key,
                    float* out, void* stream);
 
@@ -229,12 +232,14 @@ void pkv_comm_destroy(pkv_comm* c);
 int pkv_model_create_sharded(const pkv_config* cfg, const pkv_weights* w, int32_t tp_rank, int32_t tp_world,
                              pkv_comm* comm, pkv_model** out);
 
-/* unit-level entry points used by the kernel tests */
+/* unit-level entry points used by the kernel tests; pkv_gemm_bf16 takes fp16 A and B when
+ * epilogue has bit 0x100 set */
 int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_t M, int32_t N, int32_t K, float* C,
                   int64_t ldc, int32_t bn, int32_t epilogue, void* stream);
 /* fp32-faithful narrow projection (the query passes' x.W of model.py:265-275 / 311-323):
- * out[i][n] (+)= sum_k x[i][k] W[n][k] for m <= 32 fp32 rows given as 3 bf16 planes
- * x3 [96][ldx] (rows i, 32+i, 64+i); W [N][K] bf16; part >= 16*ceil(N/128)*128*32 floats,
+ * out[i][n] (+)= sum_k x[i][k] W[n][k] for m <= 32 fp32 rows given as 3 scaled fp16 planes
+ * x3 [96][ldx] (rows i, 32+i, 64+i: x = hi + 2^-11 mid + 2^-22 lo); W [N][K] fp16;
+ * part >= 16*ceil(N/128)*128*32 floats,
  * cnt >= ceil(N/128) zeroed ints; n_splits > 0: split-K, 0: stream-K (default grid),
  * < 0: stream-K on a grid of -n_splits CTAs. */
 int pkv_proj_narrow(const void* W, int32_t N, int32_t K, const void* x3, int64_t ldx, int32_t m, float* out,

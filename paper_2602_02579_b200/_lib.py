@@ -37,7 +37,7 @@ class Config(ctypes.Structure):
 
 class LayerWeights(ctypes.Structure):
     _fields_ = [("attn_norm", c_vp), ("ffn_norm", c_vp), ("wqkv", c_vp), ("wo", c_vp), ("wgu", c_vp),
-                ("wd", c_vp)]
+                ("wd", c_vp), ("wscale", ctypes.c_float * 4)]
 
 
 class Weights(ctypes.Structure):
@@ -47,7 +47,7 @@ class Weights(ctypes.Structure):
 class Cache(ctypes.Structure):
     _fields_ = [("k_pool", c_vp), ("v_pool", c_vp), ("pool_tokens", c_i64), ("page_table", c_vp), ("s", c_i32),
                 ("token_ids", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("rope_len", c_i32), ("recomputed", c_vp),
-                ("k2_pool", c_vp), ("k3_pool", c_vp), ("layer_ready", ctypes.POINTER(c_vp)),
+                ("k2_pool", c_vp), ("layer_ready", ctypes.POINTER(c_vp)),
                 ("rope_cs32", c_vp), ("layer_done", ctypes.POINTER(c_vp))]
 
 

@@ -2,7 +2,8 @@
 
 Drop-in for reference chunkstore.py (ChunkKV 37-49, AssembledCache 65-96,
 assemble 99-140, replace_entries 143-160, mark_finalized 232-236).  The cache
-lives in HBM as one paged bf16 pool per (K, V); the reference's per-layer f32
+lives in HBM as one paged fp16 pool per (K, V) plus the keys' fp16 residual plane;
+the reference's per-layer f32
 arrays (``keys_rebased``/``values``) are exposed as lazily materialised views:
 keys of entries that were never recomputed are re-derived bit-exactly from the
 chunk store, recomputed entries come from the fp32 taps of Stage II.
@@ -207,15 +208,14 @@ class AssembledCache:
         n_pages = self.pool_tokens // PAGE
         self._d_pages = torch.arange(n_pages, dtype=torch.int32, device=dev)
         shape = (L, Hkv, self.pool_tokens, dkp)
-        self.k_pool = torch.empty(shape, dtype=torch.bfloat16, device=dev)
+        self.k_pool = torch.empty(shape, dtype=torch.float16, device=dev)
         self.v_pool = torch.empty_like(self.k_pool)
-        # residual planes of every f32 key (k_pool + k2 + k3 == f32 key exactly), read by
-        # the fp32-faithful narrow passes on the tensor cores
+        # residual plane of every f32 key (k_pool + k2 == f32 key to 2^-22), read by the
+        # fp32-faithful narrow passes on the tensor cores
         self.k2_pool = torch.empty_like(self.k_pool)
-        self.k3_pool = torch.empty_like(self.k_pool)
         # slots [s, pool) are read by full-page tiles (masked, but P*V must stay finite):
         # assembly writes [0, s), so only the tail needs zeros
-        for pool in (self.k_pool, self.v_pool, self.k2_pool, self.k3_pool):
+        for pool in (self.k_pool, self.v_pool, self.k2_pool):
             pool[:, :, s:].zero_()
         self.layer_events = None  # per-layer readiness when the chunk transfer is pipelined
         self._copy_stream = None
@@ -293,7 +293,8 @@ class AssembledCache:
         self.wait_ready()
         new_tokens = -(-need // PAGE) * PAGE
         L, Hkv, dkp = self.k_pool.shape[0], self.k_pool.shape[1], self.k_pool.shape[3]
-        for name in ("k_pool", "v_pool", "k2_pool", "k3_pool"):
+        self._final_follow = None  # the overlapped final pass would read the freed pools
+        for name in ("k_pool", "v_pool", "k2_pool"):
             old = getattr(self, name)
             new = torch.zeros((L, Hkv, new_tokens, dkp), dtype=old.dtype, device=old.device)
             new[:, :, : self.pool_tokens] = old
@@ -312,7 +313,7 @@ class AssembledCache:
         return _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self._d_pages.data_ptr(),
                           self.context_length, self._d_tokens.data_ptr(), self._rcos.data_ptr(),
                           self._rsin.data_ptr(), self.rope_len, self._d_recomp.data_ptr(), self.k2_pool.data_ptr(),
-                          self.k3_pool.data_ptr(), ready, self._rcs32.data_ptr())
+                          ready, self._rcs32.data_ptr())
 
     def wait_ready(self, stream=None) -> None:
         """Make `stream` (default: current) wait for a pipelined chunk transfer to finish."""
@@ -395,7 +396,7 @@ def assemble(chunks, config: ModelConfig, track_access: bool = False, *, fp32_ta
             c._k_dev.record_stream(st_)
             c._v_dev.record_stream(st_)
         c._pinned = None
-    for t in (cache.k_pool, cache.v_pool, cache.k2_pool, cache.k3_pool, cache._d_recomp):
+    for t in (cache.k_pool, cache.v_pool, cache.k2_pool, cache._d_recomp):
         t.record_stream(cs)
     cache.layer_events = events
     cache._copy_stream = cs
@@ -405,7 +406,7 @@ def assemble(chunks, config: ModelConfig, track_access: bool = False, *, fp32_ta
 
 def replace_entries(cache: AssembledCache, layer: int, indices, new_keys, new_values) -> None:
     """Overwrite cache entries at one layer and mark them recomputed (reference
-    chunkstore.py:143-160), scattering into the bf16 pool on the GPU."""
+    chunkstore.py:143-160), scattering into the fp16 pool on the GPU."""
     if not 0 <= layer < cache.n_layers:
         raise ArgumentError(f"layer {layer} out of range for {cache.n_layers} layers")
     # a later finalize_query must see this write: no overlap with the preceding repair

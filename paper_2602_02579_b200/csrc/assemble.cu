@@ -3,12 +3,14 @@
 // chunkstore.py:143-160).
 //
 // Chunk store layout (input): per chunk, bf16 [L][t_c][Hkv][dkp], keys unrotated.
-// Paged cache (output):       bf16 [L][Hkv][pool_tokens][dkp]; slot of token t is
+// Paged cache (output):       fp16 [L][Hkv][pool_tokens][dkp]; slot of token t is
 //                             page_table[t/128]*128 + t%128.
 // Keys are rotated with the float64 cos/sin table (identical bytes to the
 // oracle's rope_cos_sin), products and the difference rounded exactly like the
-// reference's float64 numpy expression, then rounded f64->f32->bf16: the stored
-// key is bf16(reference f32 key) bit for bit.
+// reference's float64 numpy expression, then rounded f64->f32->fp16: the stored
+// key is fp16(reference f32 key) bit for bit, and the residual plane k2 holds
+// fp16(f32 key - key) for the fp32-faithful narrow passes.  Values are copied
+// (bf16 -> fp16 is exact for |v| >= 2^-14 and within 2^-25 below).
 #include "kernels.cuh"
 
 namespace pkv {
@@ -25,9 +27,8 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
                                                        int head_dim,
                                                        const double* __restrict__ rcos,
                                                        const double* __restrict__ rsin, const int32_t* page_table,
-                                                       __nv_bfloat16* k_pool, __nv_bfloat16* v_pool,
-                                                       long pool_tokens, __nv_bfloat16* k2_pool,
-                                                       __nv_bfloat16* k3_pool) {
+                                                       __half* k_pool, __half* v_pool,
+                                                       long pool_tokens, __half* k2_pool) {
   pdl_entry();
   const int vecs = dkp / 8;
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -56,35 +57,32 @@ __global__ void __launch_bounds__(128) assemble_kernel(ChunkView cv, int s, int 
       const long so = (src_row + h) * dkp + c * 8;
       uint4 kv = __ldg(reinterpret_cast<const uint4*>(kb + so));
       uint4 vv = __ldg(reinterpret_cast<const uint4*>(vb + so));
-      uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w}, o[4], o2[4], o3[4];
+      uint32_t w[4] = {kv.x, kv.y, kv.z, kv.w}, vw[4] = {vv.x, vv.y, vv.z, vv.w}, o[4], o2[4], ov[4];
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
         float e = bf16_lo(w[p]), od = bf16_hi(w[p]);
         float re = e, ro = od;
         if (2 * (c * 4 + p) < head_dim) rope_pair64(e, od, cs[p], sn[p], re, ro);
-        // plane 1 (the bf16 cache) is RNE(f32 key); planes 2/3 carry the rest exactly
-        split3_pack(re, ro, o[p], o2[p], o3[p]);
+        // the fp16 cache key is RNE(f32 key); the residual plane carries the rest
+        split2h_pack(re, ro, o[p], o2[p]);
+        ov[p] = pack_f16(bf16_lo(vw[p]), bf16_hi(vw[p]));
       }
       const long dofs = (dst_layer + (long)h * pool_tokens + slot) * dkp + c * 8;
       *reinterpret_cast<uint4*>(k_pool + dofs) = make_uint4(o[0], o[1], o[2], o[3]);
-      *reinterpret_cast<uint4*>(v_pool + dofs) = vv;
-      if (k2_pool != nullptr) {
-        *reinterpret_cast<uint4*>(k2_pool + dofs) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
-        *reinterpret_cast<uint4*>(k3_pool + dofs) = make_uint4(o3[0], o3[1], o3[2], o3[3]);
-      }
+      *reinterpret_cast<uint4*>(v_pool + dofs) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+      if (k2_pool != nullptr) *reinterpret_cast<uint4*>(k2_pool + dofs) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
     }
   }
 }
 
 int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp, int head_dim, const double* rcos,
                     const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
-                    void* k2_pool, void* k3_pool, cudaStream_t stream) {
+                    void* k2_pool, cudaStream_t stream) {
   if (s <= 0) return PKV_OK;
   const long threads = (long)s * (dkp / 8);
   launch_k(assemble_kernel, ceil_div(threads, 128), 128, 0, stream, 
-      cv, s, l0, l1, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__nv_bfloat16*>(k_pool),
-      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, reinterpret_cast<__nv_bfloat16*>(k2_pool),
-      reinterpret_cast<__nv_bfloat16*>(k3_pool));
+      cv, s, l0, l1, Hkv, dkp, head_dim, rcos, rsin, page_table, reinterpret_cast<__half*>(k_pool),
+      reinterpret_cast<__half*>(v_pool), pool_tokens, reinterpret_cast<__half*>(k2_pool));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("assemble_kernel");
   return PKV_OK;
@@ -93,10 +91,11 @@ int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp
 // f32 view of one cache layer as the reference stores it ([s][Hkv][dk]).
 // Keys of entries not yet recomputed are re-derived exactly from the chunk store
 // (rotation in float64 -> f32, bit-identical to keys_rebased); recomputed entries
-// and values come from the fp32 taps when given, else from the bf16 cache.
+// and values come from the fp32 taps when given, else from the fp16 cache (keys: the
+// fp16 key plus its residual plane).
 __global__ void cache_view_kernel(ChunkView cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
                                   const double* rcos, const double* rsin, const int32_t* page_table,
-                                  const __nv_bfloat16* pool, long pool_tokens, int is_key, float* out) {
+                                  const __half* pool, const __half* pool2, long pool_tokens, int is_key, float* out) {
   pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long total = (long)s * Hkv * head_dim;
@@ -120,28 +119,30 @@ __global__ void cache_view_kernel(ChunkView cv, int use_chunks, int s, int layer
     out[gid] = (d & 1) ? ro : re;
   } else {
     const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
-    out[gid] = __bfloat162float(pool[(((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d]);
+    const long o = (((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d;
+    out[gid] = __half2float(pool[o]) + (pool2 != nullptr ? __half2float(pool2[o]) : 0.f);
   }
 }
 
 int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
                       const double* rcos, const double* rsin, const int32_t* page_table, const void* pool,
-                      long pool_tokens, int is_key, float* out, cudaStream_t stream) {
+                      const void* pool2, long pool_tokens, int is_key, float* out, cudaStream_t stream) {
   const long total = (long)s * Hkv * head_dim;
   if (total <= 0) return PKV_OK;
   launch_k(cache_view_kernel, ceil_div(total, 256), 256, 0, stream, cv, use_chunks, s, layer, Hkv, dkp, head_dim, rcos,
                                                              rsin, page_table,
-                                                             reinterpret_cast<const __nv_bfloat16*>(pool),
-                                                             pool_tokens, is_key, out);
+                                                             reinterpret_cast<const __half*>(pool),
+                                                             reinterpret_cast<const __half*>(pool2), pool_tokens,
+                                                             is_key, out);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("cache_view_kernel");
   return PKV_OK;
 }
 
-// scatter fp32 rows [n][Hkv][dk] into the bf16 cache at token indices idx
+// scatter fp32 rows [n][Hkv][dk] into the fp16 cache at token indices idx
 __global__ void scatter_kernel(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim,
-                               const float* src, const int32_t* page_table, __nv_bfloat16* pool,
-                               long pool_tokens, __nv_bfloat16* pool2, __nv_bfloat16* pool3) {
+                               const float* src, const int32_t* page_table, __half* pool,
+                               long pool_tokens, __half* pool2) {
   pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   const long total = (long)n * Hkv * (dkp / 2);
@@ -154,26 +155,21 @@ __global__ void scatter_kernel(const int32_t* idx, int n, int layer, int Hkv, in
   const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
   const float* row = src + ((long)r * Hkv + h) * head_dim;
   const float v0 = d < head_dim ? row[d] : 0.f, v1 = d + 1 < head_dim ? row[d + 1] : 0.f;
-  uint32_t p1, p2, p3;
-  split3_pack(v0, v1, p1, p2, p3);
+  uint32_t p1, p2;
+  split2h_pack(v0, v1, p1, p2);
   const long o = (((long)layer * Hkv + h) * pool_tokens + slot) * dkp + d;
   *reinterpret_cast<uint32_t*>(pool + o) = p1;
-  if (pool2 != nullptr) {
-    *reinterpret_cast<uint32_t*>(pool2 + o) = p2;
-    *reinterpret_cast<uint32_t*>(pool3 + o) = p3;
-  }
+  if (pool2 != nullptr) *reinterpret_cast<uint32_t*>(pool2 + o) = p2;
 }
 
-// pool2/pool3 (nullable): residual planes of a key pool
+// pool2 (nullable): residual plane of a key pool
 int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim, const float* src,
-                   const int32_t* page_table, void* pool, long pool_tokens, void* pool2, void* pool3,
-                   cudaStream_t stream) {
+                   const int32_t* page_table, void* pool, long pool_tokens, void* pool2, cudaStream_t stream) {
   const long total = (long)n * Hkv * (dkp / 2);
   if (total <= 0) return PKV_OK;
   launch_k(scatter_kernel, ceil_div(total, 256), 256, 0, stream, idx, n, layer, Hkv, dkp, head_dim, src, page_table,
-                                                          reinterpret_cast<__nv_bfloat16*>(pool), pool_tokens,
-                                                          reinterpret_cast<__nv_bfloat16*>(pool2),
-                                                          reinterpret_cast<__nv_bfloat16*>(pool3));
+                                                          reinterpret_cast<__half*>(pool), pool_tokens,
+                                                          reinterpret_cast<__half*>(pool2));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("scatter_kernel");
   return PKV_OK;

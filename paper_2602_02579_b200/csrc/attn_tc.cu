@@ -1,6 +1,6 @@
 // Sparse-query causal attention on tcgen05 (Stage II, reference recompute.py:80-81
 // -> model.py:_attend 278-308 with pos_q = positions of the selected tokens and
-// pos_kv = 0..s-1 over the repaired cache).
+// pos_kv = 0..s-1 over the repaired cache).  Q, K, V and P are fp16 (fp32 accumulation).
 //
 // GQA packing: a 128-row Q tile = the G query heads sharing KV head g for a block of
 // T = 128/G selected tokens, row r = j*T + i (head g*G+j, token b*T+i).
@@ -12,8 +12,8 @@
 //   warps 0-7  softmax of tile A, warps 8-15 softmax of tile B; per tile, the two
 //              warps on a TMEM lane quarter split the 128 key columns: pass 1
 //              reads the whole S row for the max, pass 2 exponentiates the warp's
-//              64 keys in the log2 domain (1/4 of them with a degree-3 polynomial
-//              on the FMA pipe to offload MUFU) and writes P (bf16) back into the
+//              64 keys in the log2 domain (1/8 of them with a degree-3 polynomial
+//              on the FMA pipe to offload MUFU) and writes P (fp16) back into the
 //              first 64 TMEM columns of its S buffer (A operand of the PV MMA);
 //              O is rescaled in TMEM only when the max grows by > 2^8
 //   warp 16    TMA producer: K and V pages, 2-stage ring
@@ -28,8 +28,8 @@
 namespace pkv {
 
 struct AttnArgs {
-  const __nv_bfloat16* q;    // [n_q][H][DKP]
-  __nv_bfloat16* out;        // [n_q][H][DKP]
+  const __half* q;           // [n_q][H][DKP] fp16
+  __half* out;               // [n_q][H][DKP] fp16
   const int32_t* pos;        // [n_q] ascending
   const int32_t* page_table; // logical page -> physical page
   int n_q, H, Hkv, G, T, n_tiles, n_pairs;
@@ -91,7 +91,7 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
 // 2^x without the XU pipe (MUFU.EX2, FRND and F2I all issue there; with every
 // exponential on MUFU the XU pipe, not the tensor pipe, bounds this kernel):
 // round-to-nearest via the 1.5*2^23 magic add (FADD), degree-3 minimax polynomial
-// for 2^f on [-0.5, 0.5] (max relative error 7.5e-5; P is rounded to bf16 afterwards),
+// for 2^f on [-0.5, 0.5] (max relative error 7.5e-5; P is rounded to fp16, 2^-11, afterwards),
 // exponent added as an integer taken from the magic sum's low mantissa bits.
 __device__ __forceinline__ float exp2_poly(float x) {
   x = fmaxf(x, -125.f);
@@ -219,8 +219,8 @@ __global__ void __launch_bounds__(576, 1)
   } else if (warp == 17) {
    if (!PAIR || rank == 0) {
     // ------------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc_s = make_idesc_bf16(128 * (PAIR + 1), 128);
-    constexpr uint32_t idesc_o = make_idesc_bf16(128 * (PAIR + 1), DKP, /*b_mn_major=*/true);
+    constexpr uint32_t idesc_s = make_idesc_f16(128 * (PAIR + 1), 128);
+    constexpr uint32_t idesc_o = make_idesc_f16(128 * (PAIR + 1), DKP, /*b_mn_major=*/true);
     mbar_wait(q_full, 0);
     tc_fence_after();
     const uint32_t q_addr = smem_u32(sQ);
@@ -237,10 +237,10 @@ __global__ void __launch_bounds__(576, 1)
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
           const uint32_t koff = (kk >> 2) * (PAIR ? 8192 : 16384) + (kk & 3) * 32;
           if constexpr (PAIR)
-            umma_bf16_cg2(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+            umma_ss_cg2(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
                           sdesc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
           else
-            umma_bf16(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+            umma_ss(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
                       sdesc_sw128(k_addr + koff, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
         commit(&s_full[t]);
@@ -254,10 +254,10 @@ __global__ void __launch_bounds__(576, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if constexpr (PAIR)
-            umma_bf16_ts_cg2(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+            umma_ts_cg2(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
                              sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           else
-            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+            umma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
                          sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         commit(&pv_full[t]);
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(576, 1)
           if constexpr (POLY < 0) {
             // two exponentials per MUFU op (ex2.approx.f16x2): the argument is rounded to
             // f16 (|x| < 1: 2^-11 relative; larger |x| only for P < 2^-4) and P is rounded
-            // to bf16 for the MMA anyway
+            // to fp16 for the MMA anyway
             const uint32_t hx = pack_f16x2(x0, x1);
             uint32_t hp;
             asm("ex2.approx.f16x2 %0, %1;" : "=r"(hp) : "r"(hx));
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(576, 1)
           }
           if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
           else rsum2 = fadd2(rsum2, f32x2(p0, p1));
-          pk[i] = pack_bf16(p0, p1);
+          pk[i] = pack_f16(p0, p1);
         }
         tmem_st16(tS + lb + h * 32 + c * 16, pk);
       }
@@ -447,10 +447,10 @@ __global__ void __launch_bounds__(576, 1)
         uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + c * 32);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-          dst[i] = make_uint4(pack_bf16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
-                              pack_bf16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
-                              pack_bf16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
-                              pack_bf16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
+          dst[i] = make_uint4(pack_f16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
       }
     }
     tc_fence_before();
@@ -542,8 +542,8 @@ __global__ void __launch_bounds__(832, 1)
       }
     }
   } else if (warp == MMA_WARP) {
-    constexpr uint32_t idesc_s = make_idesc_bf16(128, 128);
-    constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
+    constexpr uint32_t idesc_s = make_idesc_f16(128, 128);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, DKP, /*b_mn_major=*/true);
     mbar_wait(q_full, 0);
     tc_fence_after();
     const uint32_t q_addr = smem_u32(sQ);
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(832, 1)
 #pragma unroll
         for (int kk = 0; kk < DKP / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_bf16(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+          umma_ss(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
                     sdesc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[t]);
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(832, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t pcol = kk < 3 ? kk * 8 : (kk < 6 ? 48 + (kk - 3) * 8 : 96 + (kk - 6) * 8);
-          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + pcol,
+          umma_ts(tmem + 256 + t * 128, tmem + t * 128 + pcol,
                        sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&pv_full[t]);
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(832, 1)
         }
         if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
         else rsum2 = fadd2(rsum2, f32x2(p0, p1));
-        pk[i] = pack_bf16(p0, p1);
+        pk[i] = pack_f16(p0, p1);
       }
       // P of this slice -> its own S columns [col0, col0 + W/2) (no other slice reads them)
       tmem_st16p(tS + lb + col0, pk);
@@ -731,10 +731,10 @@ __global__ void __launch_bounds__(832, 1)
         uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + col0 + c * 16);
 #pragma unroll
         for (int i = 0; i < 2; ++i)
-          dst[i] = make_uint4(pack_bf16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
-                              pack_bf16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
-                              pack_bf16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
-                              pack_bf16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
+          dst[i] = make_uint4(pack_f16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
       }
     }
     tc_fence_before();
@@ -793,7 +793,7 @@ static int launch_attn_pair(const CUtensorMap& tk64, const CUtensorMap& tv, cons
 
 static unsigned long long* g_attn_trace = nullptr;
 
-// q/out: [n_q][H][dkp] bf16; k_pool/v_pool: [L][Hkv][pool_tokens][dkp] bf16 (whole pool)
+// q/out: [n_q][H][dkp] fp16; k_pool/v_pool: [L][Hkv][pool_tokens][dkp] fp16 (whole pool)
 int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H, int Hkv, int head_dim, int dkp,
                    const void* k_pool, const void* v_pool, long pool_rows_total, long pool_tokens, int layer,
                    const int32_t* page_table, cudaStream_t stream) {
@@ -801,8 +801,8 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   const int G = H / Hkv;
   if (G > 128) return set_error(PKV_ERR_CONFIG, "attention: group size %d > 128", G);
   AttnArgs a;
-  a.q = reinterpret_cast<const __nv_bfloat16*>(q);
-  a.out = reinterpret_cast<__nv_bfloat16*>(out);
+  a.q = reinterpret_cast<const __half*>(q);
+  a.out = reinterpret_cast<__half*>(out);
   a.pos = pos;
   a.page_table = page_table;
   a.n_q = n_q;

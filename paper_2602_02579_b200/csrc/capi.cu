@@ -183,8 +183,8 @@ static int choose_splits(int N, int K) {
   }
   return best;
 }
-static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, int m, float* out, long ldo, int mode,
-                    const ProjWs& ws, cudaStream_t st) {
+static int proj_f32(const void* W, float wsc, int N, int K, const float* x, long ldx_src, int m, float* out, long ldo,
+                    int mode, const ProjWs& ws, cudaStream_t st) {
   for (int r0 = 0; r0 < m; r0 += 32) {
     const int rows = std::min(32, m - r0);
     int rc = split3_launch(x + (long)r0 * ldx_src, rows, K, ldx_src, ws.x3, ws.ldx, st);
@@ -197,6 +197,8 @@ static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, i
     g.k_tiles_per_split = 0;  // gemm_tc_launch splits the k range evenly
     g.C = ws.part;
     g.ldc = 96;
+    g.f16 = 1;
+    g.acc_scale = wsc;
     rc = gemm_tc_launch(EPI_F32, 96, W, K, ws.x3, ws.ldx, K, g, st);
     if (rc) return rc;
     const int ktt = ceil_div(K, gemm_bk(96)), nsp = ceil_div(ktt, ceil_div(ktt, sp));  // as gemm_tc_launch
@@ -208,9 +210,11 @@ static int proj_f32(const void* W, int N, int K, const float* x, long ldx_src, i
 
 // m <= 32: the producer already wrote x's 3 bf16 planes into ws.x3; one GEMM launch sums
 // the planes and the split-K partials (deterministically) and stores / accumulates out.
-static int proj_fused(const void* W, int N, int K, int m, float* out, long ldo, int resid, const ProjWs& ws,
+static int proj_fused(const void* W, float wsc, int N, int K, int m, float* out, long ldo, int resid, const ProjWs& ws,
                       cudaStream_t st) {
   GemmArgs g{};
+  g.f16 = 1;
+  g.acc_scale = wsc;
   g.M = N;
   g.N = 96;
   // stream-K (balanced k ranges over the whole grid) unless a split count is forced
@@ -340,7 +344,7 @@ int pkv_assemble_layers(const pkv_config* cfg, const pkv_chunks* ch, const pkv_c
   if (c->recomputed && l0 == 0) cudaMemsetAsync(const_cast<uint8_t*>(c->recomputed), 0, (size_t)c->s, st);
   ScopedTimer t__(T_ASSEMBLE, st);
   return assemble_launch(cv, c->s, l0, l1, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos, c->rope_sin,
-                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, c->k2_pool, c->k3_pool, st);
+                         c->page_table, c->k_pool, c->v_pool, c->pool_tokens, c->k2_pool, st);
 }
 
 int pkv_assemble(const pkv_config* cfg, const pkv_chunks* ch, const pkv_cache* c, void* stream) {
@@ -358,7 +362,8 @@ int pkv_cache_view(const pkv_config* cfg, const pkv_cache* c, const pkv_chunks* 
   if (ch) cv = ChunkView{ch->k_nr, ch->v, ch->src_chunk, ch->src_local, ch->chunk_len};
   const void* pool = is_key ? c->k_pool : c->v_pool;
   return cache_view_launch(cv, ch != nullptr, c->s, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, c->rope_cos,
-                           c->rope_sin, c->page_table, pool, c->pool_tokens, is_key, out, S(stream));
+                           c->rope_sin, c->page_table, pool, is_key ? c->k2_pool : nullptr, c->pool_tokens, is_key,
+                           out, S(stream));
 }
 
 int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer, const int32_t* idx, int32_t n,
@@ -368,11 +373,11 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer
   if (rc) return rc;
   if (layer < 0 || layer >= cfg->n_layers) return set_error(PKV_ERR_ARGUMENT, "layer out of range");
   rc = scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_k, c->page_table, c->k_pool,
-                      c->pool_tokens, c->k2_pool, c->k3_pool, S(stream));
+                      c->pool_tokens, c->k2_pool, S(stream));
   if (rc) return rc;
   if (c->recomputed && (rc = mark_launch(idx, n, const_cast<uint8_t*>(c->recomputed), S(stream))) != 0) return rc;
   return scatter_launch(idx, n, layer, cfg->n_kv_heads, lay[0], cfg->head_dim, new_v, c->page_table, c->v_pool,
-                        c->pool_tokens, nullptr, nullptr, S(stream));
+                        c->pool_tokens, nullptr, S(stream));
 }
 
 // ------------------------------------------------------------------ query pass
@@ -380,7 +385,7 @@ struct QpWs {
   float *h, *x, *qkv, *q, *k, *v, *attn, *gu, *act, *S, *Opart, *Mpart, *Lpart, *Mfin, *Lfin, *rows, *xl;
   double* denom;
   double* rows64;  // tensor-parallel: per-(query, token) head-sum partials, all-reduced
-  __nv_bfloat16* q3;
+  __half* q3;
   ProjWs proj;
   int n_splits, keys_per_split, tc_splits, tc_keys_per_split;
 };
@@ -402,7 +407,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.attn = cv.take<float>((size_t)m * H * dkp);
   w.gu = cv.take<float>((size_t)m * 2 * md->Fp);
   w.act = cv.take<float>((size_t)m * md->Fp);
-  w.proj.x3 = cv.take<__nv_bfloat16>((size_t)96 * kmax);
+  w.proj.x3 = cv.take<__half>((size_t)96 * kmax);
   w.proj.ldx = kmax;
   w.proj.part = cv.take<float>((size_t)16 * nmax * 96);  // up to 16 split-K partials
   w.proj.cnt = cv.take<int>((size_t)ceil_div(nmax, 128));
@@ -434,7 +439,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   w.Mfin = cv.take<float>((size_t)Hkv * R);
   w.Lfin = cv.take<float>((size_t)Hkv * R);
   w.xl = cv.take<float>((size_t)md->Dp);
-  w.q3 = cv.take<__nv_bfloat16>((size_t)Hkv * ceil_div(R, 128) * 3 * 128 * dkp);
+  w.q3 = cv.take<__half>((size_t)Hkv * ceil_div(R, 128) * 3 * 128 * dkp);
   *total = cv.off + 256;
   return w;
 }
@@ -483,24 +488,23 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     const pkv_layer_weights& lw = md->layers[l];
     TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, fused ? nullptr : w.x, x3,
                                    ldx, nullptr, st));
-    if (fused) TTRY(T_QP_PROJ, proj_fused(lw.wqkv, md->NQKV, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
-    else TTRY(T_QP_PROJ, proj_f32(lw.wqkv, md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
-    __nv_bfloat16* kp = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
-    __nv_bfloat16* vp = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
+    if (fused) TTRY(T_QP_PROJ, proj_fused(lw.wqkv, lw.wscale[0], md->NQKV, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
+    else TTRY(T_QP_PROJ, proj_f32(lw.wqkv, lw.wscale[0], md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
+    __half* kp = reinterpret_cast<__half*>(c->k_pool) + l * layer_pool;
+    __half* vp = reinterpret_cast<__half*>(c->v_pool) + l * layer_pool;
     const bool append = (flags & PKV_QP_APPEND_KV) != 0;
-    const bool planes = c->k2_pool != nullptr && c->k3_pool != nullptr;
-    void* k2p = planes ? reinterpret_cast<__nv_bfloat16*>(c->k2_pool) + l * layer_pool : nullptr;
-    void* k3p = planes ? reinterpret_cast<__nv_bfloat16*>(c->k3_pool) + l * layer_pool : nullptr;
+    const bool planes = c->k2_pool != nullptr;
+    __half* k2p = planes ? reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool : nullptr;
     TTRY(T_QP_MISC, query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v,
                                      append ? kp : nullptr, append ? vp : nullptr, c->pool_tokens, c->page_table,
                                      fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
                                      fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, append ? k2p : nullptr,
-                                     append ? k3p : nullptr, st));
+                                     st));
     if ((flags & PKV_QP_PROBE) && l == 1) break;  // the probe only needs layer 1's fresh values
     if ((flags & PKV_QP_PROBE) && l == 0) {
-      if (!planes) return set_error(PKV_ERR_ARGUMENT, "probe needs the cache's key planes");
-      TTRY(T_QP_MISC, probe_cache_kv_launch(w.k, w.v, m, Hkv, dk, dkp, s, kp, k2p, k3p, vp, c->pool_tokens,
-                                            c->page_table, st));
+      if (!planes) return set_error(PKV_ERR_ARGUMENT, "probe needs the cache's key plane");
+      TTRY(T_QP_MISC, probe_cache_kv_launch(w.k, w.v, m, Hkv, dk, dkp, s, kp, k2p, vp, c->pool_tokens, c->page_table,
+                                            st));
     }
     S1Attn a{};
     a.q = w.q;
@@ -513,7 +517,7 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.s = s;
     a.s_tot = s + m;
     a.R = m * G;
-    const int tc_splits = planes ? w.tc_splits : 0;  // the tensor-core path needs the key planes
+    const int tc_splits = planes ? w.tc_splits : 0;  // the tensor-core path needs the key plane
     a.keys_per_split = w.keys_per_split;
     a.n_splits = tc_splits > 0 ? 1 : ceil_div(s + m, w.keys_per_split);
     a.key_base = 0;
@@ -523,7 +527,6 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.q3 = w.q3;
     a.k1_all = c->k_pool;
     a.k2_all = c->k2_pool;
-    a.k3_all = c->k3_pool;
     a.v_all = c->v_pool;
     a.pool_rows_total = (long)cf.n_layers * Hkv * c->pool_tokens;
     a.scale = (float)(1.0 / std::sqrt((double)dk));
@@ -540,6 +543,7 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.rsin = c->rope_sin;
     a.k_pool = kp;
     a.v_pool = vp;
+    a.k2_pool = k2p;
     a.pool_tokens = c->pool_tokens;
     a.page_table = c->page_table;
     a.layer = l;
@@ -563,20 +567,20 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     // residual stream nobody reads: the per-layer scores are complete here
     if (l == cf.n_layers - 1 && !(flags & PKV_QP_LOGITS)) break;
     if (fused) {
-      TTRY(T_QP_PROJ, proj_fused(lw.wo, Dp, md->HQ, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_QP_PROJ, proj_fused(lw.wo, lw.wscale[1], Dp, md->HQ, m, w.h, Dp, resid, w.proj, st));
       if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
       TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, x3, ldx, nullptr, st));
-      TTRY(T_QP_PROJ, proj_fused(lw.wgu, 2 * Fp, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
+      TTRY(T_QP_PROJ, proj_fused(lw.wgu, lw.wscale[2], 2 * Fp, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
       TTRY(T_QP_MISC, silu_act_launch(w.gu, m, md->F, Fp, nullptr, st, x3, ldx));
-      TTRY(T_QP_PROJ, proj_fused(lw.wd, Dp, Fp, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_QP_PROJ, proj_fused(lw.wd, lw.wscale[3], Dp, Fp, m, w.h, Dp, resid, w.proj, st));
       if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
     } else {
-      TTRY(T_QP_PROJ, proj_f32(lw.wo, Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wo, lw.wscale[1], Dp, md->HQ, w.attn, md->HQ, m, w.h, Dp, resid, w.proj, st));
       if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
       TTRY(T_QP_MISC, rmsnorm_launch(w.h, m, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, w.x, nullptr, 0, nullptr, st));
-      TTRY(T_QP_PROJ, proj_f32(lw.wgu, 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wgu, lw.wscale[2], 2 * Fp, Dp, w.x, Dp, m, w.gu, 2 * Fp, 0, w.proj, st));
       TTRY(T_QP_MISC, silu_act_launch(w.gu, m, md->F, Fp, w.act, st));
-      TTRY(T_QP_PROJ, proj_f32(lw.wd, Dp, Fp, w.act, Fp, m, w.h, Dp, resid, w.proj, st));
+      TTRY(T_QP_PROJ, proj_f32(lw.wd, lw.wscale[3], Dp, Fp, w.act, Fp, m, w.h, Dp, resid, w.proj, st));
       if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)m * Dp, PKV_DT_F32, st));
     }
   }
@@ -614,7 +618,7 @@ int pkv_topk(const float* scores, int32_t n, int32_t k, int32_t* idx_out, int32_
 // ------------------------------------------------------------------- recompute
 struct RcWs {
   float* h;
-  __nv_bfloat16 *xb, *qb, *ab, *act;
+  __half *xb, *qb, *ab, *act;  // fp16 GEMM / attention operands
   float* sk_part;  // stream-K tail pieces of the Stage-II GEMMs (shared: they run in order)
   int* sk_cnt;
   size_t sk_cnt_n;
@@ -624,10 +628,10 @@ static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
   RcWs w{};
   w.h = cv.take<float>((size_t)k * md->Dp);
-  w.xb = cv.take<__nv_bfloat16>((size_t)k * md->Dp);
-  w.qb = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
-  w.ab = cv.take<__nv_bfloat16>((size_t)k * md->HQ);
-  w.act = cv.take<__nv_bfloat16>((size_t)k * md->Fp);
+  w.xb = cv.take<__half>((size_t)k * md->Dp);
+  w.qb = cv.take<__half>((size_t)k * md->HQ);
+  w.ab = cv.take<__half>((size_t)k * md->HQ);
+  w.act = cv.take<__half>((size_t)k * md->Fp);
   w.ssq = cv.take<float>((size_t)k * ceil_div(md->Dp, 256));
   const size_t skf = std::max(std::max(gemm_sk_ws_floats(k, md->NQKV, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->HQ)),
                               std::max(gemm_sk_ws_floats(k, 2 * md->Fp, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->Fp)));
@@ -697,6 +701,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
       TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
     if (defer && l > 0) consume(g);
+    g.f16 = 1;
+    g.acc_scale = lw.wscale[0];
     g.sk_part = w.sk_part;
     g.sk_cnt = w.sk_cnt;
     g.M = k;
@@ -712,18 +718,15 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     g.dkp = dkp;
     g.n_heads = H;
     g.n_kv_heads = Hkv;
-    g.k_pool = reinterpret_cast<__nv_bfloat16*>(c->k_pool) + l * layer_pool;
-    g.v_pool = reinterpret_cast<__nv_bfloat16*>(c->v_pool) + l * layer_pool;
+    g.k_pool = reinterpret_cast<__half*>(c->k_pool) + l * layer_pool;
+    g.v_pool = reinterpret_cast<__half*>(c->v_pool) + l * layer_pool;
     g.pool_tokens = c->pool_tokens;
     g.page_table = c->page_table;
     g.tap_k = tap_k ? tap_k + (long)l * k * Hkv * dk : nullptr;
     g.tap_v = tap_v ? tap_v + (long)l * k * Hkv * dk : nullptr;
     g.knr_out = knr_out ? reinterpret_cast<__nv_bfloat16*>(knr_out) + (long)l * k * Hkv * dkp : nullptr;
     g.vcap_out = v_out ? reinterpret_cast<__nv_bfloat16*>(v_out) + (long)l * k * Hkv * dkp : nullptr;
-    if (c->k2_pool != nullptr && c->k3_pool != nullptr) {
-      g.k2_pool = reinterpret_cast<__nv_bfloat16*>(c->k2_pool) + l * layer_pool;
-      g.k3_pool = reinterpret_cast<__nv_bfloat16*>(c->k3_pool) + l * layer_pool;
-    }
+    if (c->k2_pool != nullptr) g.k2_pool = reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool;
     // K/V of every selected token are in the cache before this layer's attention.  The last
     // layer of a repair only scatters K/V (its attention / o / MLP are dead, below): skip
     // the query rows of wqkv.
@@ -731,7 +734,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
       g.N = 2 * Hkv * dkp;
       g.head0 = H;
       TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp,
-                                    reinterpret_cast<const __nv_bfloat16*>(lw.wqkv) + (long)H * dkp * Dp, Dp, Dp, g,
+                                    reinterpret_cast<const __half*>(lw.wqkv) + (long)H * dkp * Dp, Dp, Dp, g,
                                     st));
     } else {
       TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
@@ -742,6 +745,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
                        (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
     GemmArgs go{};
+    go.f16 = 1;
+    go.acc_scale = lw.wscale[1];
     go.sk_part = w.sk_part;
     go.sk_cnt = w.sk_cnt;
     go.M = k;
@@ -757,6 +762,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     else if (comm)
       TTRY(T_RC_MISC, norm_defer_launch(w.h, k, Dp, Dp, lw.ffn_norm, w.xb, Dp, w.ssq, ntile, st));
     GemmArgs gg{};
+    gg.f16 = 1;
+    gg.acc_scale = lw.wscale[2];
     gg.sk_part = w.sk_part;
     gg.sk_cnt = w.sk_cnt;
     gg.M = k;
@@ -767,6 +774,8 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     if (defer) consume(gg);
     TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
     GemmArgs gd{};
+    gd.f16 = 1;
+    gd.acc_scale = lw.wscale[3];
     gd.sk_part = w.sk_part;
     gd.sk_cnt = w.sk_cnt;
     gd.M = k;
@@ -801,6 +810,7 @@ __global__ void iota_kernel(int32_t* v, int n) {
 }
 
 static size_t full_ws(const pkv_model* md, int n, RcWs* w, int32_t** sel, __nv_bfloat16** xl, void* base) {
+  // xl: the final-normed rows in bf16, the A operand of the bf16 lm_head GEMM
   size_t rc_bytes = 0;
   carve_rc(md, n, nullptr, &rc_bytes);
   Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
@@ -842,7 +852,7 @@ int pkv_full_prefill(const pkv_model* md, const pkv_cache* c, void* k_nr_out, vo
   if (logits_out) {  // _head_logits (model.py:326-329) for every row: final norm, then lm_head
     const pkv_config& cf = md->cfg;
     TTRY(T_LMHEAD, rmsnorm_launch(w.h, n, cf.hidden_dim, md->Dp, md->w.final_norm, cf.norm_eps, nullptr, nullptr, 0,
-                                  xl, st));
+                                  xl, st, /*y16_bf16=*/1));
     GemmArgs g{};
     g.M = n;
     g.N = cf.vocab_size;
@@ -863,6 +873,8 @@ int pkv_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int32_
   g.n_splits = 1;
   g.C = C;
   g.ldc = ldc;
+  g.f16 = (epi & 0x100) ? 1 : 0;  // 0x100: fp16 operands
+  epi &= 0xff;
   if (epi != EPI_F32 && epi != EPI_RESID && epi != EPI_BF16) return set_error(PKV_ERR_ARGUMENT, "epilogue");
   // the stream-K tail needs piece storage: a per-device scratch grown on demand (unit
   // tests / microbenchmarks only; the prefill path carves it from its workspace)
@@ -906,6 +918,7 @@ int pkv_proj_narrow(const void* W, int32_t N, int32_t K, const void* x3, int64_t
   g.resid = resid;
   g.part = part;
   g.cnt = cnt;
+  g.f16 = 1;
   return gemm_tc_launch(EPI_PROJ, 96, W, K, x3, ldx, K, g, S(stream));
 }
 

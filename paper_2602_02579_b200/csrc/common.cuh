@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "../../include/pkv.h"
@@ -136,8 +137,8 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (bf16 inputs, fp32 accumulate)
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::f16 (fp16 or bf16 inputs per idesc, fp32 accumulate)
+__device__ __forceinline__ void umma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -177,7 +178,7 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
       : "memory");
 }
-__device__ __forceinline__ void umma_bf16_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void umma_ss_cg2(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                               uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -208,14 +209,22 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank
       : "memory");
 }
 
-// instruction descriptor: bf16 x bf16 -> f32, A and B K-major unless b_mn_major
-__host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool b_mn_major = false) {
+// instruction descriptor, kind::f16 with fp32 accumulation: A and B both bf16 (f16 = false)
+// or both fp16 (the hardware rejects mixed A/B formats: illegal instruction on sm_100a,
+// tools/probe_mixed_mma.py); A and B K-major unless b_mn_major
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool f16, bool b_mn_major = false) {
   return (1u << 4)                      // D format f32
-         | (1u << 7)                    // A bf16
-         | (1u << 10)                   // B bf16
+         | ((f16 ? 0u : 1u) << 7)       // A: 0 = f16, 1 = bf16
+         | ((f16 ? 0u : 1u) << 10)      // B
          | ((b_mn_major ? 1u : 0u) << 16)  // B major
          | ((uint32_t)(N >> 3) << 17)   // N / 8
          | ((uint32_t)(M >> 4) << 24);  // M / 16
+}
+__host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool b_mn_major = false) {
+  return make_idesc(M, N, false, b_mn_major);
+}
+__host__ __device__ constexpr uint32_t make_idesc_f16(int M, int N, bool b_mn_major = false) {
+  return make_idesc(M, N, true, b_mn_major);
 }
 
 // shared-memory matrix descriptor, 128-byte swizzle (sm100 version field = 1).
@@ -299,7 +308,7 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 // D[tmem] (+)= A[tmem] * B[smem]^T  (A operand from tensor memory: lane = row,
 // 32-bit column c holds K elements 2c (low half) and 2c+1 (high half))
-__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                              uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -309,7 +318,7 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 }
 
 // CTA-pair variant: A (M = 256) from both CTAs' TMEM, B split along N across the pair
-__device__ __forceinline__ void umma_bf16_ts_cg2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void umma_ts_cg2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                                  uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -323,19 +332,65 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-// exact 3-way split of two fp32 values into bf16 planes: x = hi + mid + lo
-// (8 + 8 + 8 significant bits cover the 24-bit fp32 significand)
-__device__ __forceinline__ void split3_pack(float x0, float x1, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-  const float r0 = x0 - __low2float(h), r1 = x1 - __high2float(h);
-  __nv_bfloat162 m = __floats2bfloat162_rn(r0, r1);
-  __nv_bfloat162 l = __floats2bfloat162_rn(r0 - __low2float(m), r1 - __high2float(m));
+__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+
+// fp16 helpers ----------------------------------------------------------------
+// The Stage-II datapath, the paged cache and the projection weights are fp16: 11
+// significant bits instead of bf16's 8 keep the recomputed K/V within the north star's
+// 2e-2 at 32 layers (tools/precision_emulation.py: bf16 drifts to 0.04, fp16 stays
+// at 0.005), at the same tensor-core rate.
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {  // a -> low half
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float f16_lo(uint32_t u) { return __half2float(__ushort_as_half((unsigned short)(u & 0xFFFFu))); }
+__device__ __forceinline__ float f16_hi(uint32_t u) { return __half2float(__ushort_as_half((unsigned short)(u >> 16))); }
+__device__ __forceinline__ float f16_val(__half h) { return __half2float(h); }
+
+// fp16 value + fp16 residual of two fp32 values (the cache key k_pool and its plane
+// k2_pool): k = hi + lo to 2^-22 relative (2^-25 absolute where the residual is
+// subnormal, |k| < 2^-3) -- the narrow passes' keys, f32-faithful for the scores
+__device__ __forceinline__ void split2h_pack(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<uint32_t*>(&h);
+  lo = *reinterpret_cast<uint32_t*>(&l);
+}
+// three unscaled fp16 planes x = hi + mid + lo (operands that share one fp32 accumulator:
+// the narrow-pass attention's Q and P); exact to 2^-25 absolute, 2^-33 relative
+__device__ __forceinline__ void split3h_pack(float x0, float x1, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
+  __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const float r0 = x0 - hf.x, r1 = x1 - hf.y;
+  __half2 m = __floats2half2_rn(r0, r1);
+  const float2 mf = __half22float2(m);
+  __half2 l = __floats2half2_rn(r0 - mf.x, r1 - mf.y);
   hi = *reinterpret_cast<uint32_t*>(&h);
   mid = *reinterpret_cast<uint32_t*>(&m);
   lo = *reinterpret_cast<uint32_t*>(&l);
 }
-__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+// Scaled three-plane split of the narrow projections' activations (GEMM B operand, one
+// accumulator column block per plane): x = hi + 2^-11 mid + 2^-22 lo, each plane
+// rescaled into the fp16 normal range, so every fp32 x with |x| in [2^-14, 65504] is
+// represented exactly (33 >= 24 significant bits) and smaller ones to ~2^-35 absolute.
+// EPI_PROJ recombines y = (a_hi + 2^-11 a_mid) + 2^-22 a_lo.
+constexpr float X3_MID = 2048.f, X3_LO = 4194304.f;
+__device__ __forceinline__ void split3s(float x, __half& hi, __half& mid, __half& lo) {
+  hi = __float2half_rn(x);
+  const float r1 = (x - __half2float(hi)) * X3_MID;
+  mid = __float2half_rn(r1);
+  lo = __float2half_rn((r1 - __half2float(mid)) * X3_MID);
+}
+__device__ __forceinline__ void split3s_pack(float x0, float x1, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
+  __half h0, h1, m0, m1, l0, l1;
+  split3s(x0, h0, m0, l0);
+  split3s(x1, h1, m1, l1);
+  hi = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+  mid = (uint32_t)__half_as_ushort(m0) | ((uint32_t)__half_as_ushort(m1) << 16);
+  lo = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+}
 
 // byte offset of element (row, col) inside a K-major, 128B-swizzled bf16 tile whose
 // rows are 64 elements wide (one swizzle atom column). 16-byte chunk c of row r is

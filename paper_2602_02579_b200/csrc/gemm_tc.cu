@@ -24,7 +24,7 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// row-major bf16 matrix [rows][cols] with the given row stride; box = box_rows x box_cols,
+// row-major 16-bit (bf16 or fp16: TMA moves bytes) matrix [rows][cols] with the given row stride; box = box_rows x box_cols,
 // 128-byte swizzle (box_cols must be 64). Out-of-range rows/cols read as zero.
 bool make_tmap_2d(CUtensorMap* map, const void* base, long rows, long cols, long row_stride_elems, int box_rows,
                   int box_cols) {
@@ -202,7 +202,7 @@ size_t gemm_sk_ws_floats(int M, int N, int K) {
   return (size_t)rem * maxp * 2 * 256 * 128;
 }
 
-// A: [M][K] bf16 (row stride lda elements), B: [N][K] bf16 (row stride ldb).
+// A: [M][K], B: [N][K], both bf16 or both fp16 (args.f16), row strides lda / ldb elements.
 int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long ldb, int K, GemmArgs args,
                    cudaStream_t stream) {
   if (args.M <= 0 || args.N <= 0) return PKV_OK;
@@ -210,6 +210,7 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   if ((lda * 2) % 16 != 0 || (ldb * 2) % 16 != 0)
     return set_error(PKV_ERR_SHAPE, "gemm: row strides must be multiples of 8 elements");
   args.K = K;
+  if (args.acc_scale == 0.f) args.acc_scale = 1.f;  // value-initialised GemmArgs: unscaled
   int kt = ceil_div(K, gemm_bk(bn));
   if (args.n_splits <= 0) args.n_splits = 1;
   if (args.k_tiles_per_split <= 0) args.k_tiles_per_split = ceil_div(kt, args.n_splits);

@@ -1,5 +1,7 @@
 // Persistent, warp-specialised tcgen05 GEMM:  D[M,N] = A[M,K] . B[N,K]^T
-// (both operands K-major bf16, fp32 accumulation in TMEM) with fused epilogues.
+// (both operands K-major, both fp16 or both bf16, fp32 accumulation in TMEM) with
+// fused epilogues.  fp16 weights are stored pre-scaled by a power of two (see
+// DeviceModel); every epilogue multiplies the accumulator by acc_scale first.
 //
 //   warp 0      TMA producer (one elected lane) -> smem ring of STAGES (A,B) tiles
 //   warp 1      TMEM allocator + MMA issuer (one elected lane), 2 TMEM accumulators
@@ -8,7 +10,7 @@
 // Used by Stage II (recompute_selected, reference recompute.py:55-82: QKV / o /
 // gate-up / down projections) with A = activations of the k selected tokens and
 // B = transposed weights, and by the fp32-faithful narrow pass with A = weights
-// and B = a 3-way bf16 split of the fp32 activations (split-K partials).
+// and B = a scaled 3-way fp16 split of the fp32 activations (split3s, common.cuh).
 #pragma once
 #include "common.cuh"
 
@@ -18,11 +20,11 @@ enum GemmEpi : int {
   EPI_F32 = 0,      // C (+ split * M * ldc) = acc               (fp32 partials / plain store)
   EPI_BF16 = 1,     // C = bf16(acc)
   EPI_RESID = 2,    // C += acc                                    (fp32 residual stream)
-  EPI_SILU = 3,     // C[:, n/2..] = bf16(silu(gate) * up), gate/up interleaved per 128 cols
-  EPI_QKV = 4,      // rope(q), rope(k) at token positions; q -> bf16 buffer; k, v -> paged cache
-  EPI_PROJ = 5,     // narrow pass (BN = 96): y[i][n] = acc[n][i] + acc[n][32+i] + acc[n][64+i] (the 3
-                    // bf16 planes of 32 fp32 rows), stored / added to out[i][n]; split-K partials are
-                    // reduced in split order by the last-arriving CTA of each M tile (deterministic)
+  EPI_SILU = 3,     // C[:, n/2..] = fp16(silu(gate) * up), gate/up interleaved per 128 cols
+  EPI_QKV = 4,      // rope(q), rope(k) at token positions; q -> fp16 buffer; k, v -> paged fp16 cache
+  EPI_PROJ = 5,     // narrow pass (BN = 96): y[i][n] = (acc[n][i] + 2^-11 acc[n][32+i]) + 2^-22 acc[n][64+i]
+                    // (the 3 scaled fp16 planes of 32 fp32 rows), stored / added to out[i][n]; split-K
+                    // partials are reduced in split order by the last-arriving CTA of each M tile
 };
 
 struct GemmArgs {
@@ -35,16 +37,15 @@ struct GemmArgs {
   const int32_t* pos;         // [M] token positions (also cache slot via page table)
   const double* rope_cos;     // [n_pos][dk/2]
   const double* rope_sin;
-  const float2* rope_cs32;    // optional f32 (cos, sin) [n_pos][dk/2]: fp32 rotation (bf16 Stage II)
+  const float2* rope_cs32;    // optional f32 (cos, sin) [n_pos][dk/2]: fp32 rotation (fp16 Stage II)
   int head_dim, dkp, n_heads, n_kv_heads;
-  __nv_bfloat16* k_pool;      // layer base: [Hkv][pool_tokens][dkp]
-  __nv_bfloat16* v_pool;
+  __half* k_pool;             // layer base: [Hkv][pool_tokens][dkp] fp16
+  __half* v_pool;
   long pool_tokens;
   const int32_t* page_table;
   float* tap_k;               // optional fp32 [M][Hkv][dk]
   float* tap_v;
-  __nv_bfloat16* k2_pool;     // optional residual key planes (layer base), see s1_attn_tc.cu
-  __nv_bfloat16* k3_pool;
+  __half* k2_pool;            // optional residual key plane fp16(k - k_pool) (layer base), see s1_attn_tc.cu
   __nv_bfloat16* knr_out;     // optional bf16 [M][Hkv][dkp]: keys BEFORE RoPE (chunk-store layout)
   __nv_bfloat16* vcap_out;    // optional bf16 [M][Hkv][dkp]: values (chunk-store layout)
   int head0;                  // first head of the GEMM's N range (H: K and V rows only)
@@ -64,12 +65,12 @@ struct GemmArgs {
   int* sk_cnt;                // [rem tiles][CG] arrival counters (zeroed; reset by the reducer)
   int sk_maxp;                // piece stride per tail tile (<= SK_MAXP)
   // deferred RMSNorm (Stage II).  rmsnorm(h) . W = ((h * g) . W) / rms(h) row by row, so
-  // an EPI_RESID producer writes xg = bf16(h_new * ng) and the fp32 sums of h_new^2 of each
+  // an EPI_RESID producer writes xg = fp16(h_new * ng) and the fp32 sums of h_new^2 of each
   // (row, BN-column tile) -- sequentially over the tile's columns -- and the next GEMM
   // (EPI_QKV / EPI_SILU) scales its accumulator rows by 1 / sqrt(sum / norm_D + eps).
   // Replaces a standalone norm pass over h (read 4 B + write 2 B per element) per norm.
   const float* ng;            // producer: gain of the next norm [N] (nullptr: off)
-  __nv_bfloat16* xg;          // producer: [M][ldxg] bf16(h_new * ng)
+  __half* xg;                 // producer: [M][ldxg] fp16(h_new * ng)
   long ldxg;
   float* ssq;                 // producer: [M][ssq_ld] per-tile sums of h_new^2 (fp32, in column order)
   int ssq_ld;
@@ -77,6 +78,8 @@ struct GemmArgs {
   int ssq_n;                  // consumer: tiles to sum (in order)
   int norm_D;                 // consumer: mean divisor (the unpadded hidden size)
   float norm_eps;
+  int f16;                    // operands fp16 (Stage II, narrow projections) instead of bf16
+  float acc_scale;            // accumulator multiplier (2^-e of the pre-scaled fp16 weights)
 };
 constexpr int SK_MAXP = 8;    // pieces per tail tile (host plan guarantees)
 
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1 && (CG == 1 || rank == 0)) {  // the pair's MMAs are issued by the leader
-    constexpr uint32_t idesc = make_idesc_bf16(128 * CG, BN);
+    const uint32_t idesc = make_idesc(128 * CG, BN, args.f16 != 0);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
@@ -354,9 +357,9 @@ __global__ void __launch_bounds__(192, 1)
             for (int j = 0; j < Cfg::MT; ++j) {
               uint64_t ad = sdesc_sw128(a_addr + j * Cfg::A_SUB + (kk >> 2) * Cfg::A_ATOM + (kk & 3) * 32, 16, 1024);
               if constexpr (CG == 2)
-                umma_bf16_cg2(d_tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                umma_ss_cg2(d_tmem, ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
               else
-                umma_bf16(d_tmem + j * (Cfg::ACC_STRIDE / Cfg::MT), ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
+                umma_ss(d_tmem + j * (Cfg::ACC_STRIDE / Cfg::MT), ad, bd, idesc, (i > 0 || kk > 0) ? 1u : 0u);
             }
           }
           if constexpr (CG == 2) umma_commit_cg2(&empty_bar[stage]);  // frees the stage in both CTAs
@@ -375,6 +378,7 @@ __global__ void __launch_bounds__(192, 1)
     // ---------------------------------------------------------------- epilogue
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = quarter * 32 + lane;
+    const float asc = args.acc_scale;
     int local = 0;
     long pos = first_pos();
     Work w;
@@ -490,7 +494,8 @@ __global__ void __launch_bounds__(192, 1)
         float y[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          y[i] = (__uint_as_float(a0[i]) + __uint_as_float(a1[i])) + __uint_as_float(a2[i]);
+          y[i] = fmaf(__uint_as_float(a2[i]), 1.f / X3_LO, fmaf(__uint_as_float(a1[i]), 1.f / X3_MID,
+                                                                __uint_as_float(a0[i]))) * asc;
         const int n = msub * Cfg::BM + row_in_tile;  // GEMM row == output feature
         bool write = w.nseg == 1;
         if constexpr (CK) {  // partial -> own smem (the pipeline ring is drained); reduced below
@@ -568,13 +573,14 @@ __global__ void __launch_bounds__(192, 1)
           const int col = nb * (BN / 2) + c * 32;
           if (row_ok && col < args.N / 2) {
             uint32_t packed[16];
+            const float sc = rnorm * asc;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              float a0 = silu_f(__uint_as_float(g[2 * j]) * rnorm) * (__uint_as_float(u[2 * j]) * rnorm);
-              float a1 = silu_f(__uint_as_float(g[2 * j + 1]) * rnorm) * (__uint_as_float(u[2 * j + 1]) * rnorm);
-              packed[j] = pack_bf16(a0, a1);
+              float a0 = silu_f(__uint_as_float(g[2 * j]) * sc) * (__uint_as_float(u[2 * j]) * sc);
+              float a1 = silu_f(__uint_as_float(g[2 * j + 1]) * sc) * (__uint_as_float(u[2 * j + 1]) * sc);
+              packed[j] = pack_f16(a0, a1);
             }
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col);
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(args.C) + (long)row * args.ldc + col);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
@@ -603,8 +609,8 @@ __global__ void __launch_bounds__(192, 1)
               }
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                       __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+                float4 v = make_float4(__uint_as_float(r[4 * j]) * asc, __uint_as_float(r[4 * j + 1]) * asc,
+                                       __uint_as_float(r[4 * j + 2]) * asc, __uint_as_float(r[4 * j + 3]) * asc);
                 if constexpr (EPI == EPI_RESID) {
                   v.x += o[j].x; v.y += o[j].y; v.z += o[j].z; v.w += o[j].w;
                   r[4 * j] = __float_as_uint(v.x);
@@ -628,18 +634,18 @@ __global__ void __launch_bounds__(192, 1)
                     ssacc = fmaf(b, b, ssacc);
                     ssacc = fmaf(c2, c2, ssacc);
                     ssacc = fmaf(d, d, ssacc);
-                    xd[j] = make_uint2(pack_bf16(a * gg[j].x, b * gg[j].y), pack_bf16(c2 * gg[j].z, d * gg[j].w));
+                    xd[j] = make_uint2(pack_f16(a * gg[j].x, b * gg[j].y), pack_f16(c2 * gg[j].z, d * gg[j].w));
                   }
                 }
               }
             } else {
               for (int j = 0; j < 32 && col0 + j < args.N; ++j) {
-                float v = __uint_as_float(r[j]);
+                float v = __uint_as_float(r[j]) * asc;
                 if constexpr (EPI == EPI_RESID) {
                   v += dst[j];
                   if (args.xg != nullptr) {
                     ssacc = fmaf(v, v, ssacc);
-                    args.xg[(long)row * args.ldxg + col0 + j] = __float2bfloat16_rn(v * args.ng[col0 + j]);
+                    args.xg[(long)row * args.ldxg + col0 + j] = __float2half_rn(v * args.ng[col0 + j]);
                   }
                 }
                 dst[j] = v;
@@ -651,12 +657,12 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 reinterpret_cast<uint4*>(dst)[j] =
-                    make_uint4(pack_bf16(__uint_as_float(r[8 * j]), __uint_as_float(r[8 * j + 1])),
-                               pack_bf16(__uint_as_float(r[8 * j + 2]), __uint_as_float(r[8 * j + 3])),
-                               pack_bf16(__uint_as_float(r[8 * j + 4]), __uint_as_float(r[8 * j + 5])),
-                               pack_bf16(__uint_as_float(r[8 * j + 6]), __uint_as_float(r[8 * j + 7])));
+                    make_uint4(pack_bf16(__uint_as_float(r[8 * j]) * asc, __uint_as_float(r[8 * j + 1]) * asc),
+                               pack_bf16(__uint_as_float(r[8 * j + 2]) * asc, __uint_as_float(r[8 * j + 3]) * asc),
+                               pack_bf16(__uint_as_float(r[8 * j + 4]) * asc, __uint_as_float(r[8 * j + 5]) * asc),
+                               pack_bf16(__uint_as_float(r[8 * j + 6]) * asc, __uint_as_float(r[8 * j + 7]) * asc));
             } else {
-              for (int j = 0; j < 32 && col0 + j < args.N; ++j) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]));
+              for (int j = 0; j < 32 && col0 + j < args.N; ++j) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * asc);
             }
           } else if constexpr (EPI == EPI_QKV) {
             // a 32-column chunk never straddles a head (dkp is 64 or 128)
@@ -667,8 +673,9 @@ __global__ void __launch_bounds__(192, 1)
             const int pos = args.pos[row];
             const bool is_v = head_all >= H + Hkv;
             float vals[32];
+            const float sc = rnorm * asc;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]) * rnorm;
+            for (int j = 0; j < 32; ++j) vals[j] = __uint_as_float(r[j]) * sc;
             if (head_all >= H) {  // precompute_chunk captures: unrotated keys / values
               __nv_bfloat16* cap = is_v ? args.vcap_out : args.knr_out;
               if (cap != nullptr) {
@@ -683,7 +690,7 @@ __global__ void __launch_bounds__(192, 1)
             }
             if (!is_v && args.rope_cs32 != nullptr) {
               // interleaved-pair RoPE (reference tensor.py:104-113) in fp32 with the float64
-              // factors rounded to f32: Stage II computes in bf16, so the f64 rotation buys
+              // factors rounded to f32: Stage II stores fp16, so the f64 rotation buys
               // nothing here and would make the FP64 pipe the epilogue's bottleneck
               const int half = args.head_dim >> 1;
               const float2* cs = args.rope_cs32 + (long)pos * half;
@@ -713,26 +720,24 @@ __global__ void __launch_bounds__(192, 1)
                 }
               }
             }
-            uint32_t packed[16], pk2[16], pk3[16];
+            // q -> fp16 operand buffer; k -> fp16 pool + fp16 residual plane; v -> fp16 pool
+            uint32_t packed[16], pk2[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) split3_pack(vals[2 * j], vals[2 * j + 1], packed[j], pk2[j], pk3[j]);
-            __nv_bfloat16* dst;
+            for (int j = 0; j < 16; ++j) split2h_pack(vals[2 * j], vals[2 * j + 1], packed[j], pk2[j]);
+            __half* dst;
             if (head_all < H) {
-              dst = reinterpret_cast<__nv_bfloat16*>(args.C) + (long)row * args.ldc + col0;
+              dst = reinterpret_cast<__half*>(args.C) + (long)row * args.ldc + col0;
             } else {
               const int g = is_v ? head_all - H - Hkv : head_all - H;
               const long slot = (long)args.page_table[pos >> 7] * 128 + (pos & 127);
-              __nv_bfloat16* pool = is_v ? args.v_pool : args.k_pool;
+              __half* pool = is_v ? args.v_pool : args.k_pool;
               const long po = ((long)g * args.pool_tokens + slot) * dkp + d0;
               dst = pool + po;
               if (!is_v && args.k2_pool != nullptr) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 4; ++j)
                   reinterpret_cast<uint4*>(args.k2_pool + po)[j] =
                       make_uint4(pk2[4 * j], pk2[4 * j + 1], pk2[4 * j + 2], pk2[4 * j + 3]);
-                  reinterpret_cast<uint4*>(args.k3_pool + po)[j] =
-                      make_uint4(pk3[4 * j], pk3[4 * j + 1], pk3[4 * j + 2], pk3[4 * j + 3]);
-                }
               }
               float* tap = is_v ? args.tap_v : args.tap_k;
               if (tap != nullptr) {

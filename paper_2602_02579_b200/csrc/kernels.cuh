@@ -13,22 +13,22 @@ struct ChunkView {
 };
 int assemble_launch(const ChunkView& cv, int s, int l0, int l1, int Hkv, int dkp, int head_dim, const double* rcos,
                     const double* rsin, const int32_t* page_table, void* k_pool, void* v_pool, long pool_tokens,
-                    void* k2_pool, void* k3_pool, cudaStream_t stream);
+                    void* k2_pool, cudaStream_t stream);
 int cache_view_launch(const ChunkView& cv, int use_chunks, int s, int layer, int Hkv, int dkp, int head_dim,
                       const double* rcos, const double* rsin, const int32_t* page_table, const void* pool,
-                      long pool_tokens, int is_key, float* out, cudaStream_t stream);
+                      const void* pool2, long pool_tokens, int is_key, float* out, cudaStream_t stream);
 int scatter_launch(const int32_t* idx, int n, int layer, int Hkv, int dkp, int head_dim, const float* src,
-                   const int32_t* page_table, void* pool, long pool_tokens, void* pool2, void* pool3,
-                   cudaStream_t stream);
+                   const int32_t* page_table, void* pool, long pool_tokens, void* pool2, cudaStream_t stream);
 int mark_launch(const int32_t* idx, int n, uint8_t* flags, cudaStream_t st);
 int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, cudaStream_t st);
+// ybf (nullable): the normalised rows as a 16-bit GEMM operand, fp16 (Stage II) or bf16 (y16_bf16 = 1: the
+// full-prefill lm_head GEMM, whose weights stay bf16)
 int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
-                   void* ybf, cudaStream_t st);
+                   void* ybf, cudaStream_t st, int y16_bf16 = 0);
 int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, long ldy, int mode, cudaStream_t st);
 int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
-                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, void* k3_pool,
-                     cudaStream_t st);
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, cudaStream_t st);
 int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st, void* x3 = nullptr,
                     long ldx = 0);
 
@@ -49,8 +49,9 @@ struct S1Attn {
   const int32_t* chunk_len;
   const double* rcos;
   const double* rsin;
-  const __nv_bfloat16* k_pool;  // layer base
-  const __nv_bfloat16* v_pool;
+  const __half* k_pool;  // layer base (fp16)
+  const __half* v_pool;
+  const __half* k2_pool;  // layer base, nullable: residual key plane
   long pool_tokens;
   const int32_t* page_table;
   int layer;
@@ -62,11 +63,10 @@ struct S1Attn {
   float* Lpart;
   // whole-pool bases for the tensor-core path (TMA) and its Q-plane workspace
   void* q3;
-  void* x3_out;  // nullable: also write the output as 3 bf16 planes (next projection's B operand)
+  void* x3_out;  // nullable: also write the output as 3 scaled fp16 planes (next projection's B operand)
   long x3_ld;
   const void* k1_all;
   const void* k2_all;
-  const void* k3_all;
   const void* v_all;
   long pool_rows_total;
 };
@@ -74,7 +74,7 @@ struct S1Attn {
 // tensor-core narrow-pass attention over the context keys [0, s)
 struct S1TcArgs {
   const float* q;  // [m][H][DKP] rotated fp32
-  void* q3;        // workspace: bf16 Q planes [Hkv][RB][3][128][DKP]
+  void* q3;        // workspace: fp16 Q planes [Hkv][RB][3][128][DKP]
   int m, H, Hkv, G, dk, R, s, s_tot, keys_per_split, n_splits;
   float scale;
   long kv_row0;  // first pool row of this layer: layer * Hkv * pool_tokens
@@ -85,8 +85,8 @@ struct S1TcArgs {
   float* Mpart;
   float* Lpart;
 };
-int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* k3, const void* v,
-                      long pool_rows_total, int dkp, cudaStream_t st);
+int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
+                      cudaStream_t st);
 int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
                         float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st);
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st);
@@ -95,7 +95,7 @@ int norm_defer_launch(const float* h, int m, long ld, int N, const float* g, voi
 int probe_diag_colsum_launch(const float* q, const float* k, const float* Mfin, const float* Lfin, int m, int H,
                              int Hkv, int dk, int dkp, float scale, float* out, cudaStream_t st);
 int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0, const void* k_pool,
-                          const void* k2_pool, const void* k3_pool, const void* v_pool, long pool_tokens,
+                          const void* k2_pool, const void* v_pool, long pool_tokens,
                           const int32_t* page_table, cudaStream_t st);
 int embed_gather_launch(const void* embed, long lde, const int32_t* ids, const int32_t* sel, int n, int D, float* out,
                         long ldo, cudaStream_t st);

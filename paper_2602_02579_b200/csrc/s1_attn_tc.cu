@@ -1,15 +1,19 @@
 // fp32-faithful narrow-pass attention on tcgen05 (reference model.py:278-308 as
 // called by query_pass model.py:370-402, i.e. score_prophet and finalize_query).
 //
-// The reference computes q.k and p.v in float64 on f32 inputs.  Every fp32
-// operand x is split exactly into three bf16 planes x = xh + xm + xl (24 bits of
-// significand), so on the bf16 tensor cores with fp32 accumulation in TMEM
-//     Q K^T  = Qh Kh + Qh Km + Qm Kh + Qh Kl + Qm Km + Ql Kh   (+ terms < 2^-24 rel.)
-//     P V    = Ph V + Pm V + Pl V                                (V is bf16-exact)
-// The key planes live in the cache: plane 1 is the bf16 K pool itself (RNE of the
-// f32 key), planes 2/3 are written next to it by assembly, Stage II and
-// replace_entries.  Only the context keys [0, s) run here; the m fresh query keys
-// (fp32 K/V) are one extra SIMT split.
+// The reference computes q.k and p.v in float64 on f32 inputs.  On the fp16 tensor
+// cores with fp32 accumulation in TMEM every fp32 operand is split into unscaled fp16
+// planes that share ONE accumulator (split3h_pack / split2h_pack, common.cuh):
+//     Q' = 2^6 q  = Qh + Qm + Ql         (three planes; the 2^6 pre-scale keeps the
+//                                         residual planes out of the fp16 subnormals)
+//     K  = Kh + Kl                        (the fp16 cache key k_pool + its residual plane
+//                                         k2_pool: 2^-22 relative, 2^-25 absolute)
+//     Q' K^T = Qh Kh + Qm Kh + Ql Kh + Qh Kl + Qm Kl    (+ terms < 2^-30 relative)
+//     P' V   = Ph V + Pm V + Pl V,  P' = 2^10 p         (V: fp16 cache values, exact for
+//                                                       the chunk store's bf16 values)
+// so scores and outputs are f32-faithful (~1e-7 relative, far inside the 1e-4 selection
+// tie band).  Only the context keys [0, s) run here; the m fresh query keys (fp32 K/V)
+// are one extra SIMT split.
 //
 // CTA = (KV head g, key split): 128 rows r = j*m + i (query head g*G+j, query i),
 // 64-key tiles (half a cache page), 2-stage TMA ring.
@@ -36,11 +40,11 @@ struct S1TcCfg {
   static constexpr int PLANE = KT * DKP * 2;    // one K plane / the V tile
   static constexpr int ATOM_Q = 128 * 128;      // bytes per 64-col atom of a Q plane
   static constexpr int ATOM_K = KT * 128;       // bytes per 64-col atom of a K/V plane
-  static constexpr int STAGE = 4 * PLANE;       // Kh, Km, Kl, V
+  static constexpr int STAGE = 3 * PLANE;       // Kh, Kl, V
   // The Q planes live in TMEM (A operand of the S MMAs), which frees shared memory for
-  // a third K/V stage: with two, the softmax waited for S ~45 % of the time behind the
+  // the K/V ring: with two stages the softmax waited for S ~45 % of the time behind the
   // TMA (ncu, profiles/r01), the memory pipeline being too shallow.
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = DKP == 128 ? 4 : 6;
   static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
   // TMEM columns: Q planes [0,192) (plane x at 64x, DKP/2 columns each), S [192,256),
   // O [256,256+DKP), P planes [384,480)
@@ -48,9 +52,10 @@ struct S1TcCfg {
   static constexpr int SOFTMAX_WARPS = 8;
 };
 
-// Q planes for the TMA: q3[((g*RB + rb)*3 + plane)*128 + r][DKP] bf16, row r of row
+// Q planes: q3[((g*RB + rb)*3 + plane)*128 + r][DKP] fp16 planes of 2^6 q, row r of row
 // block rb = query head g*G + j, query i with rb*128 + r = j*m + i (zero padded)
-__global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int RB, int dkp, __nv_bfloat16* q3) {
+constexpr float S1_QSCALE = 64.f, S1_PSCALE = 1024.f;
+__global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int RB, int dkp, __half* q3) {
   pdl_entry();
   const int g = blockIdx.y, rr = blockIdx.x;  // rr = rb*128 + r
   const int rb = rr >> 7, r = rr & 127;
@@ -58,9 +63,9 @@ __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int 
   const int jh = valid ? rr / m : 0, qi = valid ? rr - jh * m : 0;
   const float* src = q + ((long)qi * H + g * G + jh) * dkp;
   for (int d2 = threadIdx.x; d2 < dkp / 2; d2 += blockDim.x) {
-    float x0 = valid ? src[2 * d2] : 0.f, x1 = valid ? src[2 * d2 + 1] : 0.f;
+    float x0 = valid ? src[2 * d2] * S1_QSCALE : 0.f, x1 = valid ? src[2 * d2 + 1] * S1_QSCALE : 0.f;
     uint32_t h, mi, l;
-    split3_pack(x0, x1, h, mi, l);
+    split3h_pack(x0, x1, h, mi, l);
     const long base = (((long)g * RB + rb) * 3) * 128 + r;
     reinterpret_cast<uint32_t*>(q3 + base * dkp)[d2] = h;
     reinterpret_cast<uint32_t*>(q3 + (base + 128) * dkp)[d2] = mi;
@@ -71,12 +76,11 @@ __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int 
 template <int DKP>
 __global__ void __launch_bounds__(320, 1)
     s1_attn_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
-                      const __grid_constant__ CUtensorMap tK3, const __grid_constant__ CUtensorMap tV,
-                      const __grid_constant__ CUtensorMap tQ, S1TcArgs a) {
+                      const __grid_constant__ CUtensorMap tV, S1TcArgs a) {
   using C = S1TcCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sKV = smem;  // STAGES x {Kh, Km, Kl, V}
+  uint8_t* sKV = smem;  // STAGES x {Kh, Kl, V}
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::STAGE);
   uint64_t* kv_full = bars;
   uint64_t* kv_empty = bars + C::STAGES;
@@ -120,7 +124,6 @@ __global__ void __launch_bounds__(320, 1)
     if (elect_one()) {
       tma_prefetch(&tK1);
       tma_prefetch(&tK2);
-      tma_prefetch(&tK3);
       tma_prefetch(&tV);
       const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
       for (int j = 0; j < n_tiles; ++j) {
@@ -134,17 +137,17 @@ __global__ void __launch_bounds__(320, 1)
         for (int at = 0; at < C::ATOMS; ++at) {
           tma_load_2d(base + at * C::ATOM_K, &tK1, &kv_full[st], at * 64, row);
           tma_load_2d(base + C::PLANE + at * C::ATOM_K, &tK2, &kv_full[st], at * 64, row);
-          tma_load_2d(base + 2 * C::PLANE + at * C::ATOM_K, &tK3, &kv_full[st], at * 64, row);
-          tma_load_2d(base + 3 * C::PLANE + at * C::ATOM_K, &tV, &kv_full[st], at * 64, row);
+          tma_load_2d(base + 2 * C::PLANE + at * C::ATOM_K, &tV, &kv_full[st], at * 64, row);
         }
       }
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KT);
-    constexpr uint32_t idesc_o = make_idesc_bf16(128, DKP, /*b_mn_major=*/true);
-    constexpr int PA[6] = {0, 0, 1, 0, 1, 2};  // Q plane of each product
-    constexpr int PB[6] = {0, 1, 0, 2, 1, 0};  // K plane of each product
+    constexpr uint32_t idesc_s = make_idesc_f16(128, C::KT);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, DKP, /*b_mn_major=*/true);
+    constexpr int NPROD = 5;
+    constexpr int PA[NPROD] = {0, 1, 2, 0, 1};  // Q plane of each product
+    constexpr int PB[NPROD] = {0, 0, 0, 1, 1};  // K plane of each product
     mbar_wait(q_full, 0);
     tc_fence_after();
     for (int j = 0; j <= n_tiles; ++j) {
@@ -157,11 +160,11 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t k_addr = smem_u32(sKV + st * C::STAGE);
           int n = 0;
 #pragma unroll
-          for (int pr = 0; pr < 6; ++pr)
+          for (int pr = 0; pr < NPROD; ++pr)
 #pragma unroll
             for (int kk = 0; kk < DKP / 16; ++kk, ++n) {
               const uint32_t ko = PB[pr] * C::PLANE + (kk >> 2) * C::ATOM_K + (kk & 3) * 32;
-              umma_bf16_ts(tmem + C::T_S, tmem + C::T_Q + PA[pr] * C::Q_PLANE + kk * 8,
+              umma_ts(tmem + C::T_S, tmem + C::T_Q + PA[pr] * C::Q_PLANE + kk * 8,
                            sdesc_sw128(k_addr + ko, 16, 1024), idesc_s, n > 0 ? 1u : 0u);
             }
           umma_commit(s_full);
@@ -174,13 +177,13 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(p_full, (uint32_t)jp & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t v_addr = smem_u32(sKV + st * C::STAGE + 3 * C::PLANE);
+          const uint32_t v_addr = smem_u32(sKV + st * C::STAGE + 2 * C::PLANE);
           int n = 0;
 #pragma unroll
           for (int x = 0; x < 3; ++x)
 #pragma unroll
             for (int kk = 0; kk < C::KT / 16; ++kk, ++n)
-              umma_bf16_ts(tmem + C::T_O, tmem + C::T_P + x * (C::KT / 2) + kk * 8,
+              umma_ts(tmem + C::T_O, tmem + C::T_P + x * (C::KT / 2) + kk * 8,
                            sdesc_sw128(v_addr + kk * 16 * 128, C::ATOM_K, 1024), idesc_o,
                            (jp > 0 || n > 0) ? 1u : 0u);
           umma_commit(pv_full);
@@ -199,7 +202,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lb = (uint32_t)(quarter * 32) << 16;
     constexpr int HC = C::KT / 2;  // columns per warp
     {  // this warp's half of the row's Q planes -> TMEM (lane = row): A operand of S = Q K^T
-      const __nv_bfloat16* q3 = reinterpret_cast<const __nv_bfloat16*>(a.q3);
+      const __half* q3 = reinterpret_cast<const __half*>(a.q3);
       if (hc * 32 < DKP / 2) {
 #pragma unroll 1
         for (int x = 0; x < 3; ++x) {
@@ -238,9 +241,9 @@ __global__ void __launch_bounds__(320, 1)
         const int okey0 = k_begin + j * C::KT + (hc ^ 1) * HC;
 #pragma unroll
         for (int i = 0; i < HC; ++i) {
-          // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298
-          const float x = (key0 + i < k_end) ? __uint_as_float(u[i]) * a.scale : -INFINITY;
-          const float y = (okey0 + i < k_end) ? __uint_as_float(w[i]) * a.scale : -INFINITY;
+          // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298 (the accumulator holds 2^6 q.k)
+          const float x = (key0 + i < k_end) ? (__uint_as_float(u[i]) * (1.f / S1_QSCALE)) * a.scale : -INFINITY;
+          const float y = (okey0 + i < k_end) ? (__uint_as_float(w[i]) * (1.f / S1_QSCALE)) * a.scale : -INFINITY;
           sv[i] = x;
           tmax = fmaxf(tmax, fmaxf(x, y));
         }
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int i = 0; i < HC / 2; ++i) {
         const float p0 = ex2(fmaf(sv[2 * i], LOG2E, -mb)), p1 = ex2(fmaf(sv[2 * i + 1], LOG2E, -mb));
         psum += p0 + p1;
-        split3_pack(p0, p1, ph[i], pm[i], pl[i]);
+        split3h_pack(p0 * S1_PSCALE, p1 * S1_PSCALE, ph[i], pm[i], pl[i]);
       }
       if (j >= 1) {  // PV(j-1) has read P and accumulated O
         mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
@@ -308,9 +311,10 @@ __global__ void __launch_bounds__(320, 1)
       if (valid) {
         float* od = a.Opart + base * DKP + c * 32;
 #pragma unroll
-        for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4*>(od + i) = make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
-                                                           __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
+        for (int i = 0; i < 32; i += 4)  // the accumulator holds 2^10 p.v
+          *reinterpret_cast<float4*>(od + i) =
+              make_float4(__uint_as_float(u[i]) * (1.f / S1_PSCALE), __uint_as_float(u[i + 1]) * (1.f / S1_PSCALE),
+                          __uint_as_float(u[i + 2]) * (1.f / S1_PSCALE), __uint_as_float(u[i + 3]) * (1.f / S1_PSCALE));
       }
     }
     // row sum = both halves (all MMAs and TMA loads are done: reuse the K/V ring)
@@ -330,33 +334,32 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* k3, const void* v,
-                      long pool_rows_total, int dkp, cudaStream_t st) {
+int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
+                      cudaStream_t st) {
   if (a.n_splits <= 0) return PKV_OK;
   if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
   const int RB = ceil_div(a.R, 128);
   dim3 grid(a.n_splits, a.Hkv, RB);
   launch_k(s1_qprep_kernel, dim3(RB * 128, a.Hkv), 64, 0, st, a.q, a.m, a.H, a.G, a.R, RB, dkp,
-                                                       reinterpret_cast<__nv_bfloat16*>(a.q3));
+                                                       reinterpret_cast<__half*>(a.q3));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_qprep_kernel");
-  CUtensorMap m1, m2, m3, mv, mq;
+  CUtensorMap m1, m2, mv;
   if (!cached_tmap(&m1, k1, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&m2, k2, pool_rows_total, dkp, dkp, 64) ||
-      !cached_tmap(&m3, k3, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&mv, v, pool_rows_total, dkp, dkp, 64) ||
-      !cached_tmap(&mq, a.q3, (long)a.Hkv * RB * 3 * 128, dkp, dkp, 128))
+      !cached_tmap(&mv, v, pool_rows_total, dkp, dkp, 64))
     return set_error(PKV_ERR_CUDA, "narrow pass: TMA encode failed");
   if (dkp == 128) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<128>::SMEM);
     });
-    launch_k(s1_attn_tc_kernel<128>, grid, 320, S1TcCfg<128>::SMEM, st, m1, m2, m3, mv, mq, a);
+    launch_k(s1_attn_tc_kernel<128>, grid, 320, S1TcCfg<128>::SMEM, st, m1, m2, mv, a);
   } else if (dkp == 64) {
     static std::once_flag once;
     std::call_once(once, [] {
       cudaFuncSetAttribute(s1_attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1TcCfg<64>::SMEM);
     });
-    launch_k(s1_attn_tc_kernel<64>, grid, 320, S1TcCfg<64>::SMEM, st, m1, m2, m3, mv, mq, a);
+    launch_k(s1_attn_tc_kernel<64>, grid, 320, S1TcCfg<64>::SMEM, st, m1, m2, mv, a);
   } else {
     return set_error(PKV_ERR_CONFIG, "narrow pass: padded head dim %d unsupported", dkp);
   }

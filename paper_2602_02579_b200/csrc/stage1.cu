@@ -1,9 +1,10 @@
 // Narrow query pass kernels (reference model.py:370-402 query_pass; scoring
 // selection.py:64-86; finalize recompute.py:105-125).  Everything here is
 // fp32-faithful: the m query rows stay fp32, projections run on tcgen05 with a
-// 3-way bf16 split of the activations (x = hi + mid + lo exactly), attention
-// scores / softmax / PV are fp32 SIMT, and the per-token score reductions run in
-// float64 like the reference.
+// scaled 3-way fp16 split of the activations (x = hi + 2^-11 mid + 2^-22 lo exactly,
+// split3s in common.cuh) against the pre-scaled fp16 weights, attention runs on
+// tcgen05 with fp16 planes (s1_attn_tc.cu) or fp32 SIMT, and the per-token score
+// reductions run in float64 like the reference.
 #include <algorithm>
 #include <mutex>
 #include "kernels.cuh"
@@ -12,21 +13,15 @@
 namespace pkv {
 
 // --------------------------------------------------------------- split / norm
-__device__ __forceinline__ void split3(float x, __nv_bfloat16& hi, __nv_bfloat16& mid, __nv_bfloat16& lo) {
-  hi = __float2bfloat16_rn(x);
-  float r1 = x - __bfloat162float(hi);
-  mid = __float2bfloat16_rn(r1);
-  float r2 = r1 - __bfloat162float(mid);
-  lo = __float2bfloat16_rn(r2);
-}
+__device__ __forceinline__ void split3(float x, __half& hi, __half& mid, __half& lo) { split3s(x, hi, mid, lo); }
 
-// x [m][ld] fp32 (first `cols` valid) -> X3 [96][ldx] bf16 rows i, 32+i, 64+i
-__global__ void split3_kernel(const float* x, int m, int cols, long ld, __nv_bfloat16* x3, long ldx) {
+// x [m][ld] fp32 (first `cols` valid) -> X3 [96][ldx] fp16 rows i, 32+i, 64+i
+__global__ void split3_kernel(const float* x, int m, int cols, long ld, __half* x3, long ldx) {
   pdl_entry();
   const int i = blockIdx.y;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ldx; c += gridDim.x * blockDim.x) {
     float v = (i < m && c < cols) ? x[(long)i * ld + c] : 0.f;
-    __nv_bfloat16 a, b, d;
+    __half a, b, d;
     split3(v, a, b, d);
     x3[(long)i * ldx + c] = a;
     x3[(long)(32 + i) * ldx + c] = b;
@@ -36,16 +31,17 @@ __global__ void split3_kernel(const float* x, int m, int cols, long ld, __nv_bfl
 
 int split3_launch(const float* x, int m, int cols, long ld, void* x3, long ldx, cudaStream_t st) {
   dim3 grid(ceil_div(ldx, 256) > 64 ? 64 : ceil_div(ldx, 256), 32);
-  launch_k(split3_kernel, grid, 256, 0, st, x, m, cols, ld, reinterpret_cast<__nv_bfloat16*>(x3), ldx);
+  launch_k(split3_kernel, grid, 256, 0, st, x, m, cols, ld, reinterpret_cast<__half*>(x3), ldx);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("split3_kernel");
   return PKV_OK;
 }
 
 // RMSNorm of each row in float64 (reference tensor.py:78-86), output fp32 and/or
-// the bf16 3-way split (rows >= m of X3 are zero-filled by this kernel).
+// the scaled fp16 3-way split (rows >= m of X3 are zero-filled by this kernel) and/or a
+// 16-bit copy (fp16, or bf16 when y16_bf16).
 __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const float* gain, double eps, float* y,
-                               __nv_bfloat16* x3, long ldx, __nv_bfloat16* ybf) {
+                               __half* x3, long ldx, void* y16, int y16_bf16) {
   pdl_entry();
   const int i = blockIdx.x;
   __shared__ double red[32];
@@ -74,9 +70,12 @@ __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const floa
     float out = 0.f;
     if (i < m && c < D) out = (float)((double)h[(long)i * ld + c] * inv * (double)gain[c]);
     if (y && c < ld) y[(long)i * ld + c] = out;
-    if (ybf && c < ld) ybf[(long)i * ld + c] = __float2bfloat16_rn(out);
+    if (y16 && c < ld) {
+      if (y16_bf16) reinterpret_cast<__nv_bfloat16*>(y16)[(long)i * ld + c] = __float2bfloat16_rn(out);
+      else reinterpret_cast<__half*>(y16)[(long)i * ld + c] = __float2half_rn(out);
+    }
     if (x3) {
-      __nv_bfloat16 a, b, d;
+      __half a, b, d;
       split3(out, a, b, d);
       x3[(long)i * ldx + c] = a;
       x3[(long)(32 + i) * ldx + c] = b;
@@ -85,13 +84,13 @@ __global__ void rmsnorm_kernel(const float* h, int m, int D, long ld, const floa
   }
 }
 
-// narrow-pass rows -> the 3 bf16 planes of the next projection's B operand only: one
+// narrow-pass rows -> the 3 fp16 planes of the next projection's B operand only: one
 // 256-thread CTA per plane row (32 rows; rows >= m zero-filled), the row in registers as
 // float4 vectors, one f64 block reduction, 8-byte plane stores
 template <int NV>
 __global__ void __launch_bounds__(256) rmsnorm_x3_kernel(const float* __restrict__ h, int m, int D, long ld,
                                                          const float* __restrict__ gain, double eps,
-                                                         __nv_bfloat16* __restrict__ x3, long ldx) {
+                                                         __half* __restrict__ x3, long ldx) {
   pdl_entry();
   const int i = blockIdx.x;
   const int nvec = (int)(ld >> 2);
@@ -126,20 +125,21 @@ __global__ void __launch_bounds__(256) rmsnorm_x3_kernel(const float* __restrict
       o[3] = (4 * c + 3 < D) ? (float)((double)v[j].w * inv * (double)g.w) : 0.f;
     }
     uint32_t h0, m0, l0, h1, m1, l1;
-    split3_pack(o[0], o[1], h0, m0, l0);
-    split3_pack(o[2], o[3], h1, m1, l1);
+    split3s_pack(o[0], o[1], h0, m0, l0);
+    split3s_pack(o[2], o[3], h1, m1, l1);
     *reinterpret_cast<uint2*>(x3 + (long)i * ldx + 4 * c) = make_uint2(h0, h1);
     *reinterpret_cast<uint2*>(x3 + (long)(32 + i) * ldx + 4 * c) = make_uint2(m0, m1);
     *reinterpret_cast<uint2*>(x3 + (long)(64 + i) * ldx + 4 * c) = make_uint2(l0, l1);
   }
 }
 
-// Stage-II rows (bf16 GEMM operand only): one 128-thread CTA per row, the row held in
-// registers as float4 vectors (one coalesced read of h), f64 sum of squares as above
-template <int NV>
-__global__ void __launch_bounds__(128) rmsnorm_bf16_kernel(const float* __restrict__ h, int D, long ld,
-                                                           const float* __restrict__ gain, double eps,
-                                                           __nv_bfloat16* __restrict__ ybf) {
+// Stage-II rows (16-bit GEMM operand only: fp16, or bf16 for the full-prefill lm_head):
+// one 128-thread CTA per row, the row held in registers as float4 vectors (one coalesced
+// read of h), f64 sum of squares as above
+template <int NV, bool BF>
+__global__ void __launch_bounds__(128) rmsnorm_y16_kernel(const float* __restrict__ h, int D, long ld,
+                                                          const float* __restrict__ gain, double eps,
+                                                          void* __restrict__ y16) {
   pdl_entry();
   const long i = blockIdx.x;
   const float4* src = reinterpret_cast<const float4*>(h + i * ld);
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(128) rmsnorm_bf16_kernel(const float* __restri
   __syncthreads();
   const double inv = 1.0 / sqrt((red[0] + red[1] + red[2] + red[3]) / (double)D + eps);
   const float4* g4 = reinterpret_cast<const float4*>(gain);
-  uint2* dst = reinterpret_cast<uint2*>(ybf + i * ld);
+  uint2* dst = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(y16) + i * ld);
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int c = j * 128 + threadIdx.x;
@@ -168,30 +168,36 @@ __global__ void __launch_bounds__(128) rmsnorm_bf16_kernel(const float* __restri
       const float o1 = (4 * c + 1 < D) ? (float)((double)v[j].y * inv * (double)g.y) : 0.f;
       const float o2 = (4 * c + 2 < D) ? (float)((double)v[j].z * inv * (double)g.z) : 0.f;
       const float o3 = (4 * c + 3 < D) ? (float)((double)v[j].w * inv * (double)g.w) : 0.f;
-      dst[c] = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+      dst[c] = BF ? make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3)) : make_uint2(pack_f16(o0, o1), pack_f16(o2, o3));
     }
   }
 }
 
 // rows = max(m, 32) blocks when x3 is given so that the padding rows get zeros
+template <bool BF>
+static void launch_rms_y16(int nv, int m, cudaStream_t st, const float* h, int D, long ld, const float* gain,
+                           double eps, void* out) {
+  if (nv <= 2) launch_k(rmsnorm_y16_kernel<2, BF>, m, 128, 0, st, h, D, ld, gain, eps, out);
+  else if (nv <= 4) launch_k(rmsnorm_y16_kernel<4, BF>, m, 128, 0, st, h, D, ld, gain, eps, out);
+  else if (nv <= 8) launch_k(rmsnorm_y16_kernel<8, BF>, m, 128, 0, st, h, D, ld, gain, eps, out);
+  else launch_k(rmsnorm_y16_kernel<16, BF>, m, 128, 0, st, h, D, ld, gain, eps, out);
+}
+
 int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
-                   void* ybf, cudaStream_t st) {
+                   void* ybf, cudaStream_t st, int y16_bf16) {
   if (ybf && !y && !x3 && ld % 4 == 0 && ld <= 128 * 4 * 16) {
     const int nv = ceil_div(ld / 4, 128);
-    auto* out = reinterpret_cast<__nv_bfloat16*>(ybf);
-    if (nv <= 2) launch_k(rmsnorm_bf16_kernel<2>, m, 128, 0, st, h, D, ld, gain, eps, out);
-    else if (nv <= 4) launch_k(rmsnorm_bf16_kernel<4>, m, 128, 0, st, h, D, ld, gain, eps, out);
-    else if (nv <= 8) launch_k(rmsnorm_bf16_kernel<8>, m, 128, 0, st, h, D, ld, gain, eps, out);
-    else launch_k(rmsnorm_bf16_kernel<16>, m, 128, 0, st, h, D, ld, gain, eps, out);
+    if (y16_bf16) launch_rms_y16<true>(nv, m, st, h, D, ld, gain, eps, ybf);
+    else launch_rms_y16<false>(nv, m, st, h, D, ld, gain, eps, ybf);
     PKV_LAUNCHED();
-    PKV_CHECK_LAUNCH("rmsnorm_bf16_kernel");
+    PKV_CHECK_LAUNCH("rmsnorm_y16_kernel");
     return PKV_OK;
   }
   int rows = x3 ? 32 : m;
   if (x3 && ld > ldx) return set_error(PKV_ERR_SHAPE, "rmsnorm: plane width %ld < row width %ld", ldx, ld);
   if (x3 && !y && !ybf && m <= 32 && ld % 4 == 0 && ldx % 4 == 0 && ld <= 256 * 4 * 8) {
     const int nv = ceil_div(ld / 4, 256);
-    auto* o = reinterpret_cast<__nv_bfloat16*>(x3);
+    auto* o = reinterpret_cast<__half*>(x3);
     if (nv <= 1) launch_k(rmsnorm_x3_kernel<1>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
     else if (nv <= 2) launch_k(rmsnorm_x3_kernel<2>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
     else if (nv <= 4) launch_k(rmsnorm_x3_kernel<4>, 32, 256, 0, st, h, m, D, ld, gain, eps, o, ldx);
@@ -202,14 +208,15 @@ int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, dou
   }
   const int chunks = x3 ? std::max(1, std::min(8, (int)(ld / 512))) : 1;
   if (rows <= 0) return PKV_OK;
-  launch_k(rmsnorm_kernel, dim3(rows, chunks), 256, 0, st, h, m, D, ld, gain, eps, y, reinterpret_cast<__nv_bfloat16*>(x3), ldx,
-                                       reinterpret_cast<__nv_bfloat16*>(ybf));
+  launch_k(rmsnorm_kernel, dim3(rows, chunks), 256, 0, st, h, m, D, ld, gain, eps, y, reinterpret_cast<__half*>(x3), ldx,
+           ybf, y16_bf16);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("rmsnorm_kernel");
   return PKV_OK;
 }
 
-// split-K partials P [splits][N][96] -> Y[i][n] (mode 0: store, 1: += residual)
+// split-K partials P [splits][N][96] (the 3 scaled fp16 planes' products, already times the
+// weight scale) -> Y[i][n] (mode 0: store, 1: += residual)
 __global__ void splitk_reduce_kernel(const float* part, int splits, int N, int m, float* y, long ldy, int mode) {
   pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -219,7 +226,7 @@ __global__ void splitk_reduce_kernel(const float* part, int splits, int N, int m
   float acc = 0.f;
   for (int s = 0; s < splits; ++s) {
     const float* p = part + ((long)s * N + n) * 96;
-    acc += (p[i] + p[32 + i]) + p[64 + i];
+    acc += fmaf(p[64 + i], 1.f / X3_LO, fmaf(p[32 + i], 1.f / X3_MID, p[i]));
   }
   float* dst = y + (long)i * ldy + n;
   if (mode == 1) *dst = *dst + acc;
@@ -236,13 +243,12 @@ int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, 
 
 // ------------------------------------------------------------ q/k/v of queries
 // qkv fp32 [m][NQKV] (padded-head layout) -> rotated q [m][H][dkp], k [m][Hkv][dkp],
-// v [m][Hkv][dkp] at positions pos0 + i; optionally append k/v (bf16) to the cache
-// pool and emit the fp32 fresh K/V as the reference returns them ([m][Hkv][dk]).
+// v [m][Hkv][dkp] at positions pos0 + i; optionally append k/v (fp16, key residual plane)
+// to the cache pool and emit the fp32 fresh K/V as the reference returns them ([m][Hkv][dk]).
 __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0,
                                  const double* rcos, const double* rsin, float* q, float* k, float* v,
-                                 __nv_bfloat16* k_pool, __nv_bfloat16* v_pool, long pool_tokens,
-                                 const int32_t* page_table, float* fresh_k, float* fresh_v,
-                                 __nv_bfloat16* k2_pool, __nv_bfloat16* k3_pool) {
+                                 __half* k_pool, __half* v_pool, long pool_tokens,
+                                 const int32_t* page_table, float* fresh_k, float* fresh_v, __half* k2_pool) {
   pdl_entry();
   const int heads = H + 2 * Hkv;
   const long total = (long)m * heads * (dkp / 2);
@@ -278,13 +284,10 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
   if (k_pool != nullptr) {
     const long slot = (long)page_table[pos >> 7] * 128 + (pos & 127);
     const long po = ((long)g * pool_tokens + slot) * dkp + 2 * pi;
-    uint32_t p1, p2, p3;
-    split3_pack(e, o, p1, p2, p3);
+    uint32_t p1, p2;
+    split2h_pack(e, o, p1, p2);
     *reinterpret_cast<uint32_t*>((is_v ? v_pool : k_pool) + po) = p1;
-    if (!is_v && k2_pool != nullptr) {
-      *reinterpret_cast<uint32_t*>(k2_pool + po) = p2;
-      *reinterpret_cast<uint32_t*>(k3_pool + po) = p3;
-    }
+    if (!is_v && k2_pool != nullptr) *reinterpret_cast<uint32_t*>(k2_pool + po) = p2;
   }
   float* fr = is_v ? fresh_v : fresh_k;
   if (fr != nullptr && 2 * pi < dk) {
@@ -296,13 +299,11 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
 
 int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
-                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, void* k3_pool,
-                     cudaStream_t st) {
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, cudaStream_t st) {
   const long total = (long)m * (H + 2 * Hkv) * (dkp / 2);
   launch_k(query_qkv_kernel, ceil_div(total, 256), 256, 0, st, 
-      qkv, m, H, Hkv, dk, dkp, pos0, rcos, rsin, q, k, v, reinterpret_cast<__nv_bfloat16*>(k_pool),
-      reinterpret_cast<__nv_bfloat16*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v,
-      reinterpret_cast<__nv_bfloat16*>(k2_pool), reinterpret_cast<__nv_bfloat16*>(k3_pool));
+      qkv, m, H, Hkv, dk, dkp, pos0, rcos, rsin, q, k, v, reinterpret_cast<__half*>(k_pool),
+      reinterpret_cast<__half*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v, reinterpret_cast<__half*>(k2_pool));
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("query_qkv_kernel");
   return PKV_OK;
@@ -310,12 +311,11 @@ int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, i
 
 // Low-layer probe (selection.py:95-124): the probed context tokens attend to the
 // ASSEMBLED layer-0 entries, their own included -- overwrite the pass's fresh K (rotated)
-// and V of the m rows at positions pos0.. with the cache's exact f32 key (k + k2 + k3
-// planes) and value.
+// and V of the m rows at positions pos0.. with the cache's f32 key (fp16 k + residual
+// plane k2) and value.
 __global__ void probe_cache_kv_kernel(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0,
-                                      const __nv_bfloat16* k_pool, const __nv_bfloat16* k2_pool,
-                                      const __nv_bfloat16* k3_pool, const __nv_bfloat16* v_pool, long pool_tokens,
-                                      const int32_t* page_table) {
+                                      const __half* k_pool, const __half* k2_pool, const __half* v_pool,
+                                      long pool_tokens, const int32_t* page_table) {
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)m * Hkv * dk) return;
   const int d = (int)(gid % dk);
@@ -324,9 +324,8 @@ __global__ void probe_cache_kv_kernel(float* k, float* v, int m, int Hkv, int dk
   const int pos = pos0 + i;
   const long slot = (long)page_table[pos >> 7] * 128 + (pos & 127);
   const long po = ((long)g * pool_tokens + slot) * dkp + d;
-  k[((long)i * Hkv + g) * dkp + d] =
-      (__bfloat162float(k_pool[po]) + __bfloat162float(k2_pool[po])) + __bfloat162float(k3_pool[po]);
-  v[((long)i * Hkv + g) * dkp + d] = __bfloat162float(v_pool[po]);
+  k[((long)i * Hkv + g) * dkp + d] = __half2float(k_pool[po]) + __half2float(k2_pool[po]);
+  v[((long)i * Hkv + g) * dkp + d] = __half2float(v_pool[po]);
 }
 
 // Low-layer probe, kvshare (selection.py:136-142): the block's own keys' share of the
@@ -367,13 +366,12 @@ int probe_diag_colsum_launch(const float* q, const float* k, const float* Mfin, 
 }
 
 int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0, const void* k_pool,
-                          const void* k2_pool, const void* k3_pool, const void* v_pool, long pool_tokens,
-                          const int32_t* page_table, cudaStream_t st) {
+                          const void* k2_pool, const void* v_pool, long pool_tokens, const int32_t* page_table,
+                          cudaStream_t st) {
   const long total = (long)m * Hkv * dk;
   probe_cache_kv_kernel<<<ceil_div(total, 256), 256, 0, st>>>(
-      k, v, m, Hkv, dk, dkp, pos0, reinterpret_cast<const __nv_bfloat16*>(k_pool),
-      reinterpret_cast<const __nv_bfloat16*>(k2_pool), reinterpret_cast<const __nv_bfloat16*>(k3_pool),
-      reinterpret_cast<const __nv_bfloat16*>(v_pool), pool_tokens, page_table);
+      k, v, m, Hkv, dk, dkp, pos0, reinterpret_cast<const __half*>(k_pool), reinterpret_cast<const __half*>(k2_pool),
+      reinterpret_cast<const __half*>(v_pool), pool_tokens, page_table);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("probe_cache_kv_kernel");
   return PKV_OK;
@@ -381,9 +379,9 @@ int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, i
 
 // gate/up interleaved per 256 columns -> act = f32(silu64(gate)) * up
 // (reference model.py:260-262 and 318-321)
-// act (nullable) fp32 [m][Fp]; x3 (nullable): the 3 bf16 planes of act for the next
+// act (nullable) fp32 [m][Fp]; x3 (nullable): the 3 scaled fp16 planes of act for the next
 // projection, rows i / 32+i / 64+i (valid rows only)
-__global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* act, __nv_bfloat16* x3, long ldx) {
+__global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* act, __half* x3, long ldx) {
   pdl_entry();
   const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long)m * Fp) return;
@@ -398,7 +396,7 @@ __global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* ac
   }
   if (act) act[gid] = a;
   if (x3) {
-    __nv_bfloat16 p, q, r;
+    __half p, q, r;
     split3(a, p, q, r);
     x3[(long)i * ldx + f] = p;
     x3[(long)(32 + i) * ldx + f] = q;
@@ -408,7 +406,7 @@ __global__ void silu_act_kernel(const float* gu, int m, int F, int Fp, float* ac
 
 int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st, void* x3, long ldx) {
   const long total = (long)m * Fp;
-  launch_k(silu_act_kernel, ceil_div(total, 256), 256, 0, st, gu, m, F, Fp, act, reinterpret_cast<__nv_bfloat16*>(x3),
+  launch_k(silu_act_kernel, ceil_div(total, 256), 256, 0, st, gu, m, F, Fp, act, reinterpret_cast<__half*>(x3),
                                                         ldx);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("silu_act_kernel");
@@ -483,7 +481,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
       const int t = t0 + kr;
       float kf[8], vf[8];
       if (t < k_end && t < a.s) {
-        uint4 kraw, vraw;
+        uint4 kraw, vraw, k2raw = make_uint4(0, 0, 0, 0);
         const bool from_chunk = a.src_chunks && !(a.recomp != nullptr && a.recomp[t]);
         if (from_chunk) {
           const int ch = a.src_chunk[t], loc = a.src_local[t], tc = a.chunk_len[ch];
@@ -495,23 +493,34 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
           const long off = ((long)g * a.pool_tokens + slot) * DKP + c8 * 8;
           kraw = *reinterpret_cast<const uint4*>(a.k_pool + off);
           vraw = *reinterpret_cast<const uint4*>(a.v_pool + off);
+          k2raw = a.k2_pool != nullptr ? *reinterpret_cast<const uint4*>(a.k2_pool + off) : make_uint4(0, 0, 0, 0);
         }
         const uint32_t kw[4] = {kraw.x, kraw.y, kraw.z, kraw.w};
+        const uint32_t k2w[4] = {k2raw.x, k2raw.y, k2raw.z, k2raw.w};
         const uint32_t vw[4] = {vraw.x, vraw.y, vraw.z, vraw.w};
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          float e0 = bf16_lo(kw[p]), e1 = bf16_hi(kw[p]);
+          float e0, e1;
           const int pi = c8 * 4 + p;
-          if (from_chunk && pi < half) {
-            const double c = a.rcos[(long)t * half + pi], sn = a.rsin[(long)t * half + pi];
-            const double de = e0, dd = e1;
-            e0 = (float)__dsub_rn(__dmul_rn(de, c), __dmul_rn(dd, sn));
-            e1 = (float)__dadd_rn(__dmul_rn(de, sn), __dmul_rn(dd, c));
+          if (from_chunk) {  // bf16 chunk store, rotated here exactly like keys_rebased
+            e0 = bf16_lo(kw[p]);
+            e1 = bf16_hi(kw[p]);
+            if (pi < half) {
+              const double c = a.rcos[(long)t * half + pi], sn = a.rsin[(long)t * half + pi];
+              const double de = e0, dd = e1;
+              e0 = (float)__dsub_rn(__dmul_rn(de, c), __dmul_rn(dd, sn));
+              e1 = (float)__dadd_rn(__dmul_rn(de, sn), __dmul_rn(dd, c));
+            }
+            vf[2 * p] = bf16_lo(vw[p]);
+            vf[2 * p + 1] = bf16_hi(vw[p]);
+          } else {  // fp16 pool key + residual plane, fp16 value
+            e0 = f16_lo(kw[p]) + f16_lo(k2w[p]);
+            e1 = f16_hi(kw[p]) + f16_hi(k2w[p]);
+            vf[2 * p] = f16_lo(vw[p]);
+            vf[2 * p + 1] = f16_hi(vw[p]);
           }
           kf[2 * p] = e0;
           kf[2 * p + 1] = e1;
-          vf[2 * p] = bf16_lo(vw[p]);
-          vf[2 * p + 1] = bf16_hi(vw[p]);
         }
       } else if (t < k_end) {
         const int i = t - a.s;
@@ -635,7 +644,7 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
 // per-row (max, denominator) used by the scoring reduction
 __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const float* Lpart, int splits, int Hkv,
                                 int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin,
-                                __nv_bfloat16* x3, long ldx) {
+                                __half* x3, long ldx) {
   pdl_entry();
   extern __shared__ float wsp[];  // [splits] rescale weight of each split
   __shared__ float sM, sL;
@@ -673,8 +682,8 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
     const float o = acc / L;
     const long col = (long)(g * G + j) * dkp + d;
     out[(long)i * H * dkp + col] = o;
-    if (x3 != nullptr) {  // the o-projection's B operand (3 bf16 planes, rows i/32+i/64+i)
-      __nv_bfloat16 p, q, rr;
+    if (x3 != nullptr) {  // the o-projection's B operand (3 scaled fp16 planes, rows i/32+i/64+i)
+      __half p, q, rr;
       split3(o, p, q, rr);
       x3[(long)i * ldx + col] = p;
       x3[(long)(32 + i) * ldx + col] = q;
@@ -694,7 +703,7 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
 __global__ void s1_attn_combine_fresh(const float* Opart, const float* Mpart, const float* Lpart, int splits,
                                       int Hkv, int R, int m, int G, int H, int dkp, const float* __restrict__ q,
                                       const float* __restrict__ fk, const float* __restrict__ fv, float scale,
-                                      float* out, float* Mfin, float* Lfin, __nv_bfloat16* x3, long ldx) {
+                                      float* out, float* Mfin, float* Lfin, __half* x3, long ldx) {
   pdl_entry();
   extern __shared__ float shc[];  // wsp[splits] | sS[m] (scores, then probabilities) | sV[m][dkp]
   float* wsp = shc;
@@ -766,7 +775,7 @@ __global__ void s1_attn_combine_fresh(const float* Opart, const float* Mpart, co
     const long col = (long)(g * G + j) * dkp + d;
     out[(long)i * H * dkp + col] = o;
     if (x3 != nullptr) {
-      __nv_bfloat16 p, qq, rr;
+      __half p, qq, rr;
       split3(o, p, qq, rr);
       x3[(long)i * ldx + col] = p;
       x3[(long)(32 + i) * ldx + col] = qq;
@@ -924,7 +933,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   const size_t fresh_smem = (a.tc_splits + a.m + (size_t)a.m * a.dkp) * sizeof(float);
   bool combined = false;
   if (a.tc_splits > 0) {
-    // context keys [0, s) on the tensor cores (3-way bf16 split, fp32-faithful)
+    // context keys [0, s) on the tensor cores (fp16 planes, fp32-faithful)
     S1TcArgs t{};
     t.q = a.q;
     t.m = a.m;
@@ -946,7 +955,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.Opart = a.Opart;
     t.Mpart = a.Mpart;
     t.Lpart = a.Lpart;
-    int rc = s1_attn_tc_launch(t, a.k1_all, a.k2_all, a.k3_all, a.v_all, a.pool_rows_total, a.dkp, st);
+    int rc = s1_attn_tc_launch(t, a.k1_all, a.k2_all, a.v_all, a.pool_rows_total, a.dkp, st);
     if (rc) return rc;
     // fused fresh keys + combine: measured neutral (each CTA re-reads the head's fresh V),
     // so opt-in (PKV_FRESH_FUSED=1)
@@ -960,7 +969,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
       });
       launch_k(s1_attn_combine_fresh, dim3(a.R, a.Hkv), 128, fresh_smem, st, a.Opart, a.Mpart, a.Lpart,
                a.tc_splits, a.Hkv, a.R, a.m, a.G, a.H, a.dkp, a.q, a.fk, a.fv, a.scale, attn_out, Mfin, Lfin,
-               reinterpret_cast<__nv_bfloat16*>(a.x3_out), a.x3_ld);
+               reinterpret_cast<__half*>(a.x3_out), a.x3_ld);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_attn_combine_fresh");
       combined = true;
@@ -1001,7 +1010,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_CHECK_LAUNCH("s1_attn_pass1");
   launch_k(s1_attn_combine, dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st, a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin,
-                                                    reinterpret_cast<__nv_bfloat16*>(a.x3_out), a.x3_ld);
+                                                    reinterpret_cast<__half*>(a.x3_out), a.x3_ld);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   }
@@ -1170,11 +1179,11 @@ rows_kernel:
   return PKV_OK;
 }
 
-// Deferred RMSNorm after the tensor-parallel all-reduce of h: the xg = bf16(h * g) and
+// Deferred RMSNorm after the tensor-parallel all-reduce of h: the xg = fp16(h * g) and
 // per-256-column-tile fp32 sums of h^2 that the EPI_RESID epilogue writes on one GPU, in the
 // same (increasing column) order, so head-sharded and unsharded Stage II normalise alike.
 __global__ void norm_defer_kernel(const float* __restrict__ h, long ld, int N, const float* __restrict__ g,
-                                  __nv_bfloat16* __restrict__ xg, long ldxg, float* __restrict__ ssq, int ssq_ld) {
+                                  __half* __restrict__ xg, long ldxg, float* __restrict__ ssq, int ssq_ld) {
   pdl_entry();
   const long row = blockIdx.x;
   const int c0 = threadIdx.x * 256;
@@ -1185,7 +1194,7 @@ __global__ void norm_defer_kernel(const float* __restrict__ h, long ld, int N, c
   for (int c = c0; c < c1; ++c) {
     const float v = hr[c];
     acc = fmaf(v, v, acc);
-    xg[row * ldxg + c] = __float2bfloat16_rn(v * g[c]);
+    xg[row * ldxg + c] = __float2half_rn(v * g[c]);
   }
   ssq[row * ssq_ld + threadIdx.x] = acc;
 }
@@ -1195,7 +1204,7 @@ int norm_defer_launch(const float* h, int m, long ld, int N, const float* g, voi
   if (m <= 0) return PKV_OK;
   const int threads = ceil_div(N, 256);
   if (threads > 1024) return set_error(PKV_ERR_SHAPE, "norm_defer: row too wide");
-  launch_k(norm_defer_kernel, m, threads, 0, st, h, ld, N, g, reinterpret_cast<__nv_bfloat16*>(xg), ldxg, ssq, ssq_ld);
+  launch_k(norm_defer_kernel, m, threads, 0, st, h, ld, N, g, reinterpret_cast<__half*>(xg), ldxg, ssq, ssq_ld);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("norm_defer_kernel");
   return PKV_OK;

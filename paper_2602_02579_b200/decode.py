@@ -4,10 +4,10 @@ model.decode_step / greedy_generate (model.py:405-471).
 A decode step is the fp32-faithful narrow pass with one query row (include/pkv.h
 ``pkv_query_pass``, flags LOGITS | APPEND_KV) over every cache entry so far -- the
 assembled/repaired context, the finalized query and the tokens generated since, all in
-the paged pool with their exact f32 keys (bf16 key + two residual planes) -- appending
+the paged pool with their f32 keys (fp16 key + residual plane) -- appending
 the new token's K/V at position ``cache.length``.  A KVCache from ``finalize_query``
 keeps its device pools; a host KVCache (e.g. ``KVCache.from_prefill``) is uploaded once
-(keys split exactly into the three planes by ``pkv_replace_entries``).
+(keys split into the fp16 key and its residual plane by ``pkv_replace_entries``).
 """
 
 from __future__ import annotations
@@ -32,7 +32,7 @@ class GenerationResult:
 
 
 class DevicePools:
-    """Paged bf16 K/V pools (+ key residual planes) holding `length` entries at positions
+    """Paged fp16 K/V pools (+ key residual plane) holding `length` entries at positions
     0..length-1, with room to append; the device side of a decoding KVCache."""
 
     def __init__(self, config: ModelConfig, device, capacity: int):
@@ -46,10 +46,10 @@ class DevicePools:
         cfg = self.config
         self.pool_tokens = -(-capacity // PAGE) * PAGE
         shape = (cfg.n_layers, cfg.n_kv_heads, self.pool_tokens, cfg.layout().dkp)
-        old = [getattr(self, n, None) for n in ("k_pool", "v_pool", "k2_pool", "k3_pool")]
-        self.k_pool, self.v_pool, self.k2_pool, self.k3_pool = (
-            torch.zeros(shape, dtype=torch.bfloat16, device=self.device) for _ in range(4))
-        for new, o in zip((self.k_pool, self.v_pool, self.k2_pool, self.k3_pool), old):
+        old = [getattr(self, n, None) for n in ("k_pool", "v_pool", "k2_pool")]
+        self.k_pool, self.v_pool, self.k2_pool = (
+            torch.zeros(shape, dtype=torch.float16, device=self.device) for _ in range(3))
+        for new, o in zip((self.k_pool, self.v_pool, self.k2_pool), old):
             if o is not None:
                 new[:, :, : o.shape[2]] = o
         self.pages = torch.arange(self.pool_tokens // PAGE, dtype=torch.int32, device=self.device)
@@ -65,7 +65,7 @@ class DevicePools:
         """pkv_cache view with s = current length (keys read from the pool + planes)."""
         return _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self.pages.data_ptr(),
                           self.length, self._no_tokens.data_ptr(), self.rcos.data_ptr(), self.rsin.data_ptr(),
-                          self.rope_len, None, self.k2_pool.data_ptr(), self.k3_pool.data_ptr(), None,
+                          self.rope_len, None, self.k2_pool.data_ptr(), None,
                           self.rcs32.data_ptr())
 
     @classmethod
@@ -73,7 +73,7 @@ class DevicePools:
         """Adopt a finalized AssembledCache's pools (context + query already appended)."""
         p = cls.__new__(cls)
         p.config, p.device = cache.config, cache.device
-        p.k_pool, p.v_pool, p.k2_pool, p.k3_pool = cache.k_pool, cache.v_pool, cache.k2_pool, cache.k3_pool
+        p.k_pool, p.v_pool, p.k2_pool = cache.k_pool, cache.v_pool, cache.k2_pool
         p.pool_tokens, p.pages = cache.pool_tokens, cache._d_pages
         p.rope_len, p.rcos, p.rsin, p.rcs32 = cache.rope_len, cache._rcos, cache._rsin, cache._rcs32
         p._no_tokens = cache._d_tokens
@@ -99,12 +99,11 @@ class DevicePools:
         return p
 
     def host_layers(self, is_key: bool):
-        """Per-layer f32 [length][Hkv][dk]: keys exactly (k + k2 + k3), values from bf16."""
+        """Per-layer f32 [length][Hkv][dk]: keys k + k2 (f32 to 2^-22), values from fp16."""
         dk = self.config.head_dim
         n = self.length
         if is_key:
-            t = (self.k_pool[:, :, :n, :dk].float() + self.k2_pool[:, :, :n, :dk].float()) + \
-                self.k3_pool[:, :, :n, :dk].float()
+            t = self.k_pool[:, :, :n, :dk].float() + self.k2_pool[:, :, :n, :dk].float()
         else:
             t = self.v_pool[:, :, :n, :dk].float()
         a = t.permute(0, 2, 1, 3).cpu().numpy()

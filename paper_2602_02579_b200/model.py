@@ -3,8 +3,9 @@
 Host-side types keep the reference ``pikv.model`` surface (ModelConfig,
 LayerWeights, ModelWeights, random_weights, FlopTally, KVCache -- reference
 model.py:24-228) so caller code constructs them unchanged.  ``DeviceModel`` is the
-B200 image: bf16 weights transposed to output-major rows, head dims padded to the
-kernel tile (see include/pkv.h "Device layouts"), plus the C-ABI model handle.
+B200 image: fp16 projection weights (pre-scaled by a power of two per matrix)
+transposed to output-major rows, head dims padded to the kernel tile, bf16 embed /
+lm_head (see include/pkv.h "Device layouts"), plus the C-ABI model handle.
 """
 
 from __future__ import annotations
@@ -12,6 +13,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import json
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -146,11 +148,14 @@ class ModelWeights:
         return self._fingerprint
 
     def device(self, config: ModelConfig) -> "DeviceModel":
-        """The cached B200 image of these weights (uploaded once)."""
-        dm = self._device.get("dm")
+        """The cached B200 image of these weights, uploaded once per (config, device): the
+        same weights under another config (rope_theta, norm_eps, ...) get their own image."""
+        import torch
+        key = (config, torch.cuda.current_device())
+        dm = self._device.get(key)
         if dm is None:
             dm = DeviceModel.from_host(self, config)
-            self._device["dm"] = dm
+            self._device[key] = dm
         return dm
 
 
@@ -256,8 +261,19 @@ def _pad2(t, rows, cols):
     return out
 
 
+def fp16_scaled(w):
+    """(fp16 tensor, scale) with w ~= fp16_tensor * scale: the matrix is multiplied by
+    2^e, e chosen so that max|w| * 2^e <= 2^15, before rounding to fp16 -- every
+    bf16-exact weight down to ~2^-24 * 2^-e is represented exactly, larger dynamic
+    ranges keep 11 significant bits.  The kernels multiply accumulators by 2^-e."""
+    import torch
+    mx = float(w.abs().max()) if w.numel() else 0.0
+    e = 0 if not (mx > 0 and math.isfinite(mx)) else max(-60, min(60, math.floor(math.log2(32768.0 / mx))))
+    return (w.float() * (2.0 ** e)).to(torch.float16).contiguous(), 2.0 ** -e
+
+
 class DeviceModel:
-    """bf16 device weights in the kernel layout + the C-ABI model handle."""
+    """fp16 (pre-scaled) device weights in the kernel layout + the C-ABI model handle."""
 
     def __init__(self, config: ModelConfig, tensors: dict, fingerprint: str, tp_rank: int = 0, tp_world: int = 1,
                  comm=None):
@@ -275,7 +291,7 @@ class DeviceModel:
             lt = tensors["layers"][i]
             self._layers[i] = _lib.LayerWeights(lt["attn_norm"].data_ptr(), lt["ffn_norm"].data_ptr(),
                                                 lt["wqkv"].data_ptr(), lt["wo"].data_ptr(), lt["wgu"].data_ptr(),
-                                                lt["wd"].data_ptr())
+                                                lt["wd"].data_ptr(), (ctypes.c_float * 4)(*lt["wscale"]))
         self._w = _lib.Weights(tensors["embed"].data_ptr(), tensors["final_norm"].data_ptr(),
                                tensors["lm_head"].data_ptr(), self._layers)
         self._cfg = config.c_struct()
@@ -300,7 +316,8 @@ class DeviceModel:
     # -- construction ---------------------------------------------------------
     @classmethod
     def from_host(cls, weights: ModelWeights, config: ModelConfig, device=None) -> "DeviceModel":
-        """Upload reference-layout f32 weights, rounding to bf16 (RNE)."""
+        """Upload reference-layout f32 weights: projections as pre-scaled fp16 (exact for
+        bf16-exact weights), embed / lm_head as bf16 (RNE)."""
         torch = _lib.require_cuda()
         weights.validate(config)
         dev = device or torch.device("cuda", torch.cuda.current_device())
@@ -324,17 +341,19 @@ class DeviceModel:
 
         layers = []
         for lw in weights.layers:
-            wqkv = torch.cat([heads_rows(lw.wq, H), heads_rows(lw.wk, Hkv), heads_rows(lw.wv, Hkv)]).to(bf)
+            wqkv, s_qkv = fp16_scaled(torch.cat([heads_rows(lw.wq, H), heads_rows(lw.wk, Hkv), heads_rows(lw.wv, Hkv)]))
             wo = up(lw.wo).t().reshape(config.hidden_dim, H, dk)
             wo_p = torch.zeros((lay.Dp, H, lay.dkp), dtype=torch.float32, device=dev)
             wo_p[: config.hidden_dim, :, :dk] = wo
+            wo16, s_o = fp16_scaled(wo_p.reshape(lay.Dp, lay.HQ))
+            del wo_p
             g = _pad2(up(lw.w_gate).t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
             u = _pad2(up(lw.w_up).t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
-            wgu = torch.stack([g, u], dim=1).reshape(2 * lay.Fp, lay.Dp).to(bf)
-            wd = _pad2(up(lw.w_down).t(), lay.Dp, lay.Fp).to(bf)
-            layers.append({"attn_norm": norm(lw.attn_norm), "ffn_norm": norm(lw.ffn_norm), "wqkv": wqkv.contiguous(),
-                           "wo": wo_p.reshape(lay.Dp, lay.HQ).to(bf).contiguous(), "wgu": wgu.contiguous(),
-                           "wd": wd.contiguous()})
+            wgu, s_gu = fp16_scaled(torch.stack([g, u], dim=1).reshape(2 * lay.Fp, lay.Dp))
+            del g, u
+            wd, s_d = fp16_scaled(_pad2(up(lw.w_down).t(), lay.Dp, lay.Fp))
+            layers.append({"attn_norm": norm(lw.attn_norm), "ffn_norm": norm(lw.ffn_norm), "wqkv": wqkv,
+                           "wo": wo16, "wgu": wgu, "wd": wd, "wscale": (s_qkv, s_o, s_gu, s_d)})
         tensors = {"layers": layers,
                    "embed": _pad2(up(weights.embed), config.vocab_size, lay.Dp).to(bf).contiguous(),
                    "lm_head": _pad2(up(weights.lm_head).t(), config.vocab_size, lay.Dp).to(bf).contiguous(),
@@ -343,8 +362,8 @@ class DeviceModel:
 
     @classmethod
     def random(cls, config: ModelConfig, seed: int = 0, device=None) -> "DeviceModel":
-        """Random-init bf16 weights generated on the device (benchmarks; the layout
-        matches from_host, the values follow the reference's N(0,1)/sqrt(fan_in))."""
+        """Random-init weights generated on the device (benchmarks; the layout matches
+        from_host, the values follow the reference's N(0,1)/sqrt(fan_in), bf16-rounded)."""
         torch = _lib.require_cuda()
         dev = device or torch.device("cuda", torch.cuda.current_device())
         lay = Layout.of(config)
@@ -353,8 +372,8 @@ class DeviceModel:
         bf = torch.bfloat16
         D, F, dk, H, Hkv = config.hidden_dim, config.ffn_dim, config.head_dim, config.n_heads, config.n_kv_heads
 
-        def rnd(rows, cols, fan_in, real_rows, real_cols):
-            t = torch.zeros((rows, cols), dtype=bf, device=dev)
+        def rnd(rows, cols, fan_in, real_rows, real_cols, dtype=bf):
+            t = torch.zeros((rows, cols), dtype=dtype, device=dev)
             t[:real_rows, :real_cols] = (torch.randn((real_rows, real_cols), generator=g, device=dev,
                                                      dtype=torch.float32) / fan_in ** 0.5).to(bf)
             return t
@@ -364,16 +383,20 @@ class DeviceModel:
         layers = []
         for _ in range(config.n_layers):
             if dk == lay.dkp and D == lay.Dp:
-                wqkv = (torch.randn((lay.NQKV, D), generator=g, device=dev) / D ** 0.5).to(bf)
+                wqkv = (torch.randn((lay.NQKV, D), generator=g, device=dev) / D ** 0.5).to(bf).float()
             else:
-                wqkv = torch.zeros((H + 2 * Hkv, lay.dkp, lay.Dp), dtype=bf, device=dev)
+                wqkv = torch.zeros((H + 2 * Hkv, lay.dkp, lay.Dp), dtype=torch.float32, device=dev)
                 wqkv[:, :dk, :D] = (torch.randn((H + 2 * Hkv, dk, D), generator=g, device=dev) / D ** 0.5).to(bf)
                 wqkv = wqkv.reshape(lay.NQKV, lay.Dp)
-            wo = rnd(lay.Dp, lay.HQ, H * dk, D, lay.HQ)
+            wo = rnd(lay.Dp, lay.HQ, H * dk, D, lay.HQ, torch.float32)
             if dk != lay.dkp:
                 wo.view(lay.Dp, H, lay.dkp)[:, :, dk:] = 0
-            layers.append({"attn_norm": ones.clone(), "ffn_norm": ones.clone(), "wqkv": wqkv.contiguous(), "wo": wo,
-                           "wgu": rnd(2 * lay.Fp, lay.Dp, D, 2 * lay.Fp, D), "wd": rnd(lay.Dp, lay.Fp, F, D, F)})
+            wqkv, s_qkv = fp16_scaled(wqkv)
+            wo, s_o = fp16_scaled(wo)
+            wgu, s_gu = fp16_scaled(rnd(2 * lay.Fp, lay.Dp, D, 2 * lay.Fp, D, torch.float32))
+            wd, s_d = fp16_scaled(rnd(lay.Dp, lay.Fp, F, D, F, torch.float32))
+            layers.append({"attn_norm": ones.clone(), "ffn_norm": ones.clone(), "wqkv": wqkv, "wo": wo, "wgu": wgu,
+                           "wd": wd, "wscale": (s_qkv, s_o, s_gu, s_d)})
         embed = torch.zeros((config.vocab_size, lay.Dp), dtype=bf, device=dev)
         embed[:, :D] = torch.randn((config.vocab_size, D), generator=g, device=dev).to(bf)
         tensors = {"layers": layers, "embed": embed, "lm_head": rnd(config.vocab_size, lay.Dp, D, config.vocab_size, D),
@@ -399,7 +422,7 @@ class DeviceModel:
                            "wqkv": torch.cat([q, k, v]).contiguous(),
                            "wo": lt["wo"][:, rank * hl * dkp:(rank + 1) * hl * dkp].contiguous(),
                            "wgu": lt["wgu"][2 * rank * fl:2 * (rank + 1) * fl].contiguous(),
-                           "wd": lt["wd"][:, rank * fl:(rank + 1) * fl].contiguous()})
+                           "wd": lt["wd"][:, rank * fl:(rank + 1) * fl].contiguous(), "wscale": lt["wscale"]})
         tensors = {"layers": layers, "embed": self.t["embed"], "lm_head": self.t["lm_head"],
                    "final_norm": self.t["final_norm"]}
         return DeviceModel(cfg, tensors, self.fingerprint, rank, world, comm)
@@ -436,13 +459,18 @@ def resolve_device_model(weights, config: ModelConfig) -> DeviceModel:
         return weights.device(config)
     # reference pikv.ModelWeights (duck-typed): same field names
     if hasattr(weights, "layers") and hasattr(weights, "embed"):
+        import torch
+        key = (config, torch.cuda.current_device())
         cache = getattr(weights, "__b200_device__", None)
+        if cache is not None and getattr(cache, "_cache_key", None) != key:
+            cache = None  # uploaded under another config / device
         if cache is None:
             mw = ModelWeights(embed=weights.embed, layers=[LayerWeights(**{k: getattr(lw, k) for k in (
                 "attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")})
                 for lw in weights.layers], final_norm=weights.final_norm, lm_head=weights.lm_head)
             cache = DeviceModel.from_host(mw, config)
             cache.fingerprint = weights.fingerprint(config) if hasattr(weights, "fingerprint") else cache.fingerprint
+            cache._cache_key = key
             try:
                 weights.__b200_device__ = cache
             except AttributeError:

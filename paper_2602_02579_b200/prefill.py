@@ -6,7 +6,7 @@
 chunk-store layout (bf16 ``[L][t][Hkv][dkp]``, include/pkv.h), captured inside the QKV
 GEMM epilogue, so a freshly produced chunk is assembled without a host round trip; the
 reference's f32 ``keys_norope``/``values`` are materialised lazily on access.
-Numerics are the Stage-II contract (bf16 operands, fp32 accumulation and residual).
+Numerics are the Stage-II contract (fp16 operands, fp32 accumulation and residual).
 """
 
 from __future__ import annotations
@@ -47,19 +47,23 @@ class _SequenceCache:
         self.n = n
         self.pool_tokens = -(-n // PAGE) * PAGE
         shape = (cfg.n_layers, cfg.n_kv_heads, self.pool_tokens, lay.dkp)
-        self.k_pool = torch.zeros(shape, dtype=torch.bfloat16, device=dev)
+        self.k_pool = torch.zeros(shape, dtype=torch.float16, device=dev)
         self.v_pool = torch.zeros_like(self.k_pool)
+        self.k2_pool = torch.zeros_like(self.k_pool)  # keys' residual plane: k_pool + k2 = f32 key
         self.pages = torch.arange(self.pool_tokens // PAGE, dtype=torch.int32, device=dev)
         self.tokens = torch.from_numpy(ids.astype(np.int32)).to(dev)
         self.rope_len, self.rcos, self.rsin, self.rcs32 = rope_device_tables(cfg.rope_theta, cfg.head_dim,
                                                                             self.pool_tokens)
         self.c = _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self.pages.data_ptr(), n,
                             self.tokens.data_ptr(), self.rcos.data_ptr(), self.rsin.data_ptr(), self.rope_len, None,
-                            None, None, None, self.rcs32.data_ptr())
+                            self.k2_pool.data_ptr(), None, self.rcs32.data_ptr())
 
-    def layer(self, pool, li: int, dk: int) -> np.ndarray:
-        """[n, Hkv, dk] f32 of one layer (pages are in order)."""
-        return pool[li, :, : self.n, :dk].permute(1, 0, 2).float().cpu().numpy()
+    def layer(self, pool, li: int, dk: int, plane=None) -> np.ndarray:
+        """[n, Hkv, dk] f32 of one layer (pages are in order), plus a residual plane."""
+        t = pool[li, :, : self.n, :dk].float()
+        if plane is not None:
+            t = t + plane[li, :, : self.n, :dk].float()
+        return t.permute(1, 0, 2).cpu().numpy()
 
 
 def _run(dm, cfg: ModelConfig, ids: np.ndarray, want_knr: bool, want_logits: bool, stream=None):
@@ -99,7 +103,7 @@ def full_prefill(weights, config: ModelConfig, tokens, capture_attn: bool = Fals
     ids = check_tokens(tokens, config)
     seq, knr, v, logits = _run(dm, config, ids, capture_keys_norope, True)
     dk = config.head_dim
-    keys = [seq.layer(seq.k_pool, li, dk) for li in range(config.n_layers)]
+    keys = [seq.layer(seq.k_pool, li, dk, seq.k2_pool) for li in range(config.n_layers)]
     values = [seq.layer(seq.v_pool, li, dk) for li in range(config.n_layers)]
     keys_nr = None
     if knr is not None:

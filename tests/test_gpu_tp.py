@@ -80,8 +80,8 @@ def test_head_sharded_prefill_matches_oracle(built, case, world):
     assert err <= KV_ABS and cos >= COS_MIN, (err, cos)
 
     # each rank's cache slice == the unsharded cache's heads (Stage-II K/V scattered in place)
-    # (bf16 storage: the fp32 sums differ from the unsharded order by ~1e-7 relative, so
-    # an entry may round to the neighbouring bf16 value -> allow one bf16 ulp)
+    # (fp16 storage: the fp32 sums differ from the unsharded order by ~1e-7 relative, so
+    # an entry may round to a neighbouring fp16 value -> allow two fp16 ulps)
     s = one.s
     kl = cfg.n_kv_heads // world
     kv_err = 0.0
@@ -91,9 +91,9 @@ def test_head_sharded_prefill_matches_oracle(built, case, world):
             for name in ("k_pool", "v_pool"):
                 a = getattr(pipes[r].cache, name)[:, :, :s].float()
                 b = getattr(one.cache, name)[:, r * kl:(r + 1) * kl, :s].float()
-                ulp = torch.clamp(b.abs(), min=1.0) * 2.0 ** -7
+                ulp = torch.clamp(b.abs(), min=1.0) * 2.0 ** -10
                 kv_err = max(kv_err, float(((a - b).abs() / ulp).max()))
-        assert kv_err <= 1.0, f"cache slice differs from the unsharded cache by {kv_err:.2f} bf16 ulp"
+        assert kv_err <= 2.0, f"cache slice differs from the unsharded cache by {kv_err:.2f} fp16 ulp"
     _report(case=f"{case}_tp{world}", s=s, k=k, per_layer_max_rel=rel.max(), sel_symdiff=len(set(sels[0]) ^ set(sel_ref)),
             logits_max_abs=err, logits_cos=cos, kv_vs_unsharded_max_abs=kv_err, same_sel_as_unsharded=same_sel)
     for c in comms:
