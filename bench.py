@@ -6,7 +6,11 @@ score the context with the 32-token query (fp32-faithful narrow pass), fuse +
 top-k at p = 0.2, Stage-II recompute of k = 6554 tokens, finalize -> first-token
 logits.
 
-Multi-GPU (one process per GPU under torchrun), --mode:
+Inputs: SYN1 (paper_2602_02579_b200/synthetic.py) -- random-init weights at the reference's
+init scale, chunk K/V and query generated on the device and reproduced bit for bit by the
+CPU oracle; the run is checked in place against tests/golden/anchor_c3.npz ("parity").
+
+Multi-GPU (one process per GPU; `--gpus N` starts torchrun itself when WORLD_SIZE is unset), --mode:
   heads     (default for N > 1; BASELINE configs[2]) one 32k request head-sharded over
             the N GPUs (tensor parallel, paper_2602_02579_b200.tp): per-layer NCCL sums of
             the per-token score partials before the global top-k and of the o/down
@@ -167,6 +171,120 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def cpu_threads():
+    """Host threading of the CPU baseline: cores in the affinity mask, OMP / BLAS threads."""
+    info = {"affinity_cores": cpu_cores(), "os_cpu_count": os.cpu_count(),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{"api": d.get("internal_api"), "threads": d.get("num_threads")} for d in threadpool_info()]
+    except Exception:  # noqa: BLE001 -- informational
+        pass
+    return info
+
+
+def arm_config(args, cfgd, world, heads):
+    """The `config` dict of a bench line -- identical for our arm and the reference arm."""
+    s = cfgd["n_chunks"] * cfgd["chunk_len"]
+    return {"workload": args.config, "model": "Llama-3-8B shape" if "llama" in args.config else "Mistral-7B shape",
+            "s": s, "chunks": cfgd["n_chunks"], "chunk_len": cfgd["chunk_len"], "m": args.m, "p": args.p,
+            "k": math.ceil(args.p * s),
+            "parallelism": f"tp{world} (KV-head sharded, NCCL)" if heads else f"request-dp{world}",
+            "inputs": f"SYN1 seed 0 (weights, chunk store, query: paper_2602_02579_b200/synthetic.py)"
+            if args.chunks == "synthetic" else "SYN1 weights; chunk K/V precomputed on the GPU",
+            "l2": "inputs larger than L2 (16 GB weights, 4.3 GB KV)"}
+
+
+def ttft_floor_ms(cfgd, p, m, hbm_gbs, tflops):
+    """Algorithmic TTFT floor: assembly + Stage-I weight streaming + final
+    pass (HBM) + Stage-II GEMMs and causal-visible attention (tensor) at the peaks."""
+    L, H, Hkv, dk, D, F, V = (cfgd[k] for k in ("n_layers", "n_heads", "n_kv_heads", "head_dim", "hidden_dim",
+                                                 "ffn_dim", "vocab_size"))
+    s = cfgd["n_chunks"] * cfgd["chunk_len"]
+    k = math.ceil(p * s)
+    params = L * (D * (H * dk + 2 * Hkv * dk) + H * dk * D + 3 * D * F)
+    hbm = (4 * L * s * Hkv * dk * 2 + 2 * params * 2 + D * V * 2 + 2 * L * s * Hkv * dk * 2) / (hbm_gbs * 1e9)
+    flops = 2.0 * k * params + 4.0 * L * H * dk * (k * (s + 1) / 2)
+    return (hbm + flops / (tflops * 1e12)) * 1e3
+
+
+def load_anchor(args, heads):
+    """The oracle fixture of this exact workload (tests/golden/make_anchor.py), if any."""
+    if args.config != "llama3-8b-32k" or args.chunks != "synthetic" or args.m != 32 or abs(args.p - 0.2) > 1e-12:
+        return None
+    path = ROOT / "tests" / "golden" / "anchor_c3.npz"
+    if not path.exists():
+        return None
+    z = np.load(path)
+    return json.loads(str(z["meta"])), {k: z[k] for k in z.files if k != "meta"}
+
+
+def anchor_parity(pipe, anchor, heads):
+    """In-run parity of the benchmarked request against the CPU oracle (north-star
+    tolerances): per-layer scores, selection (tie band 1e-4), first-token logits and, when
+    the selection is the reference's, the recomputed fp16 cache entries at 16 rows x L."""
+    meta, z = anchor
+    per = pipe.per_layer.cpu().numpy()
+    k = int(meta["k"])
+    sel = pipe.idx[:k].cpu().numpy().astype(np.int64)
+    rel = float((np.abs(per - z["per_layer"]) / np.maximum(np.abs(z["per_layer"]), 1e-30)).max())
+    fused = z["fused"]
+    kth = np.sort(fused)[::-1][k - 1]
+    band = np.abs(fused - kth) <= 1e-4 * abs(kth)
+    a, b = set(sel.tolist()), set(z["sel"].tolist())
+    sel_ok = len(a) == k and {i for i in a if not band[i]} == {i for i in b if not band[i]}
+    lg = pipe.logits.cpu().numpy().astype(np.float64)
+    lr = z["first_logits"].astype(np.float64)
+    cos = float(lg @ lr / (np.linalg.norm(lg) * np.linalg.norm(lr)))
+    out = {"fixture": "tests/golden/anchor_c3.npz (oracle on the same SYN1 inputs)", "per_layer_max_rel": rel,
+           "tie_band": int(band.sum()), "sel_symdiff": len(a ^ b), "sel_ok": bool(sel_ok),
+           "logits_max_abs": float(np.abs(lg - lr).max()), "logits_cos": cos}
+    ok = rel <= 1e-4 and sel_ok and out["logits_max_abs"] <= 2e-2 and cos >= 0.999
+    if not heads and a == b:
+        cache, dk = pipe.cache, pipe.cfg.head_dim
+        ix = z["sel"][z["kv_rows"]]
+        err, kcos = 0.0, 1.0
+        for li in range(pipe.cfg.n_layers):
+            for pool, ref in ((cache.k_pool, z["kv_k"][li]), (cache.v_pool, z["kv_v"][li])):
+                got = pool[li, :, ix, :dk].permute(1, 0, 2).float().cpu().numpy().astype(np.float64)
+                err = max(err, float(np.abs(got - ref).max()))
+                kcos = min(kcos, float((got.ravel() @ ref.ravel()) / (np.linalg.norm(got) * np.linalg.norm(ref))))
+        out.update(kv_fp16_cache_max_abs=err, kv_min_cos=kcos, kv_rows=f"{len(ix)} selected rows x every layer")
+        ok = ok and err <= 2e-2 and kcos >= 0.999
+    out["pass"] = bool(ok)
+    return out
+
+
+def nccl_summary(path):
+    """NCCL version / NVLS lines from the NCCL_DEBUG=INFO log of this rank."""
+    try:
+        lines = Path(path).read_text(errors="replace").splitlines()
+    except OSError:
+        return None
+    pick = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if "NCCL INFO" in ln and
+            any(t in ln for t in ("NCCL version", "NVLS", "nvls", "Channel 00", "comm 0x", "Init COMPLETE"))]
+    return {"log": str(path), "nvls": any("NVLS" in ln and "enabled" in ln.lower() for ln in lines),
+            "lines": pick[:12]}
+
+
+def relaunch_under_torchrun(n):
+    """`bench.py --gpus N` without a torchrun environment: start N ranks on this node."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} requested but {have} CUDA device(s) visible"}), flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *sys.argv[1:]]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd))
+
+
 # ----------------------------------------------------------------------------- main
 def run_reference(args, cfgd, rank, world):
     if rank != 0:
@@ -180,12 +298,12 @@ def run_reference(args, cfgd, rank, world):
     ttft = float(np.mean(times))
     value = s / ttft
     cores = cpu_cores()
+    mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
     line = {"impl": "reference", "metric": metric_name(cfgd, args.p), "value": value, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft * 1e3, "ttft_ms": ttft * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
-            "data": "synthetic", "config": {"workload": args.config, "s": s, "m": 32, "p": args.p, "k": k,
-                                            "l2": "inputs larger than L2 (CPU run)"},
-            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
+            "data": "synthetic", "config": arm_config(args, cfgd, world, mode == "heads" and world > 1),
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "threads": cpu_threads(),
                              "sample": f"oracle port of pikv, 1 layer at full width and s={s}, Stage II on {n_s} "
                                        f"of k={k} rows, extrapolated x{cfgd['n_layers']} layers and k/{n_s} rows; "
                                        f"phase seconds {json.dumps({a: round(b, 3) for a, b in tm.items()})}"},
@@ -209,16 +327,30 @@ def main():
     ap.add_argument("--mode", default="auto", choices=["auto", "heads", "requests"])
     ap.add_argument("--p-sweep", default="0.05,0.1,0.2,0.4", help="recompute ratios of the sweep ('' = skip)")
     ap.add_argument("--sweep-steps", type=int, default=3)
-    ap.add_argument("--chunks", default="precompute", choices=["precompute", "random"])
+    ap.add_argument("--chunks", default="synthetic", choices=["synthetic", "precompute"])
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        relaunch_under_torchrun(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-
     if args.impl == "reference":
         run_reference(args, cfgd, rank, world)
         return
+    if world != args.gpus:
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={world}: reporting the {world} launched ranks",
+              file=sys.stderr, flush=True)
+
+    mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
+    heads = mode == "heads" and world > 1
+    nccl_log = None
+    if heads:  # NCCL init / NVLS lines of this rank (summarised in the JSON line)
+        out_dir = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else Path("/tmp")
+        nccl_log = out_dir / f"nccl_rank{rank}.log"
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS,GRAPH")
+        os.environ.setdefault("NCCL_DEBUG_FILE", str(nccl_log))
 
     import torch
     import torch.distributed as dist
@@ -230,51 +362,45 @@ def main():
     __graft_entry__.build()
     import paper_2602_02579_b200 as P
     from paper_2602_02579_b200 import _lib
-    from paper_2602_02579_b200.pipeline import PrefillPipeline, random_device_chunks
+    from paper_2602_02579_b200 import synthetic as S
+    from paper_2602_02579_b200.pipeline import PrefillPipeline
 
     cfg = P.ModelConfig(**{k: cfgd[k] for k in ("n_layers", "n_heads", "n_kv_heads", "head_dim", "hidden_dim",
                                                 "ffn_dim", "vocab_size", "rope_theta")})
     s = cfgd["n_chunks"] * cfgd["chunk_len"]
-    mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
 
     def make_chunks(model, seed):
-        """The request's chunk store: each chunk precomputed on the GPU from uniform random
-        tokens (prefill.precompute_chunk path, realistic K/V), or N(0,1) K/V (--chunks random)."""
-        if args.chunks == "random":
-            return random_device_chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed=seed)
+        """The request's chunk store: SYN1 keys/values (the inputs the oracle fixture was
+        computed on), or precomputed on the GPU from SYN1 token ids (--chunks precompute)."""
+        if args.chunks == "synthetic":
+            return S.chunks(cfg, cfgd["n_chunks"], cfgd["chunk_len"], seed, model.fingerprint)
         from paper_2602_02579_b200.prefill import precompute_chunks_device
-        crng = np.random.default_rng(seed)
-        toks = [crng.integers(0, cfg.vocab_size, cfgd["chunk_len"]) for _ in range(cfgd["n_chunks"])]
+        toks = [S.token_ids(cfgd["chunk_len"], cfg.vocab_size, seed, S.tid_tokens(c)).cpu().numpy()
+                for c in range(cfgd["n_chunks"])]
         out = precompute_chunks_device(model, cfg, toks)
         torch.cuda.synchronize()
         return out
-    heads = mode == "heads" and world > 1
-    comm = None
-    if heads:
-        from paper_2602_02579_b200 import tp
-        try:
-            comm = tp.nccl_comm()
-        except Exception as e:  # noqa: BLE001 -- report and fall back to independent requests
-            print(f"[bench] NCCL communicator failed ({e}); falling back to --mode requests", file=sys.stderr)
-            heads = False
+
     if heads:
         # one request, KV heads (and ffn blocks) sharded over the ranks; every rank builds
-        # the same seeded model / chunk store and keeps its slice
-        full = P.DeviceModel.random(cfg, seed=0)
-        full_chunks = make_chunks(full, 1)
+        # the same SYN1 model / chunk store and keeps its slice.  No fallback: a failing
+        # communicator ends the run.
+        from paper_2602_02579_b200 import tp
+        comm = tp.nccl_comm()
+        full = P.DeviceModel.synthetic(cfg, seed=0)
+        full_chunks = make_chunks(full, 0)
         dm = full.shard(rank, world, comm.handle)
         del full
         chunks = tp.shard_chunks(full_chunks, rank, world)
         del full_chunks
         torch.cuda.empty_cache()
-        qseed = 7
+        qseed = 0
     else:
-        dm = P.DeviceModel.random(cfg, seed=0)
-        chunks = make_chunks(dm, 1 + rank)
-        qseed = 7 + rank
+        dm = P.DeviceModel.synthetic(cfg, seed=0)
+        chunks = make_chunks(dm, rank)  # request r of the batch: chunk store / query seed r
+        qseed = rank
     pipe = PrefillPipeline(dm, chunks, args.m, args.p)
-    rng = np.random.default_rng(qseed)
-    query = rng.integers(0, cfg.vocab_size, args.m)
+    query = S.query(cfg, args.m, qseed)
     pipe.set_query(query)
     stream = torch.cuda.current_stream()
 
@@ -338,6 +464,29 @@ def main():
         dist.barrier()
     value = (1 if heads else world) * s / (ms / 1e3)
 
+    # ---- parity of this very run against the oracle fixture (rank 0's request)
+    anchor = load_anchor(args, heads) if rank == 0 else None
+    parity = anchor_parity(pipe, anchor, heads) if anchor is not None else None
+
+    # ---- graph-timed phase split (each phase captured and replayed alone, serial)
+    graph_phases = {}
+    try:
+        for name, fn in (("assemble_score_select", pipe.score_select), ("stage2", pipe.stage2),
+                         ("final", pipe.final)):
+            g = pipe.capture(fn)
+            g.replay()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(args.steps):
+                g.replay()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            graph_phases[name] = round(a0.elapsed_time(a1) / args.steps, 3)
+            del g
+    except Exception as e:  # noqa: BLE001 -- informational split only
+        graph_phases["error"] = f"{type(e).__name__}: {e}"
+
     # ---- roofline of every kernel group; the dominant one is reported
     hbm, tf_burst, tf_sust, peak_kind = _peaks()
     idx = pipe.idx[: pipe.k].cpu().numpy().astype(np.int64)
@@ -350,6 +499,7 @@ def main():
     work = {  # per launch group: (bound, algorithmic units, unit)
         "assemble": ("hbm", 4.0 * L * s * Hkv * lay.dkp * 2, "GB/s"),
         "qp_proj": ("hbm", dm.weight_bytes(include_head=False) / (4 * L), "GB/s"),
+        "qp_attn": ("hbm", 2.0 * s * Hkv * dk * 2, "GB/s"),  # one layer's context K and V, 2 B each
         "rc_qkv": ("tensor", 2.0 * k * D * (H + 2 * Hkv) * dk, "TFLOP/s"),
         "rc_attn": ("tensor", 4.0 * H * dk * float(np.sum(idx + 1)), "TFLOP/s"),
         "rc_o": ("tensor", 2.0 * k * H * dk * D, "TFLOP/s"),
@@ -364,6 +514,8 @@ def main():
             continue
         if name == "lm_head":  # one GEMV per step, timed together with its final norm (2 timer scopes)
             cnt = args.steps
+        if name == "qp_attn":  # one attention scope per layer per narrow pass (scoring + final)
+            cnt = args.steps * 2 * L
         per_launch_s = tot_ms / cnt / 1e3
         ach = units / per_launch_s / (1e9 if unit == "GB/s" else 1e12)
         peak = hbm if bound == "hbm" else tf_sust
@@ -377,23 +529,28 @@ def main():
         traffic = json.loads(tfile.read_text()).get(args.config, {}).get(dominant) if not heads else None
     roof = dict(rooflines[dominant], kernel=dominant, traffic=traffic,
                 peak_kind=f"{peak_kind} ({'sustained bf16' if rooflines[dominant]['bound'] == 'tensor' else 'HBM copy'})")
+    floor = ttft_floor_ms(cfgd, args.p, args.m, hbm, tf_burst)
 
     line = {"metric": metric_name(cfgd, args.p), "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
-            "vs_baseline": None, "dtype": "bf16 (Stage II) / fp32-faithful (narrow passes)",
-            "data": ("synthetic: random-init weights, uniform random token ids; chunk K/V " +
-                     ("precomputed on the GPU (precompute_chunk)" if args.chunks == "precompute" else "N(0,1)")),
-            "config": {"workload": args.config, "model": "Llama-3-8B shape" if "llama" in args.config else
-                       "Mistral-7B shape", "s": s, "chunks": cfgd["n_chunks"], "m": args.m, "p": args.p, "k": k,
-                       "parallelism": f"tp{world} (KV-head sharded, NCCL)" if heads else f"request-dp{world}",
-                       "l2": "inputs larger than L2 (16 GB weights, 4.3 GB KV)"},
+            "vs_baseline": None, "dtype": "fp16 (Stage II, fp32 accumulate) / fp32-faithful (narrow passes)",
+            "data": ("synthetic: SYN1 random-init weights (reference init scale), token ids and chunk K/V, "
+                     "reproduced bit for bit by the CPU oracle" if args.chunks == "synthetic" else
+                     "synthetic: SYN1 random-init weights and token ids; chunk K/V precomputed on the GPU"),
+            "config": arm_config(args, cfgd, world, heads),
             "gpu_launches": int(n_launch), "launch_mode": launch_mode,
             "clocks": clk, "roofline": roof,
+            "ttft_floor_ms": round(floor, 2), "ttft_floor_frac": round(floor / ms, 4),
+            "graph_phases_ms": graph_phases,
             "eager_phases_ms": {n: round(v[0], 3) for n, v in eager_phases.items()},
             "phases_ms": {n: round(v[0] / args.steps, 3) for n, v in phases.items()},
             "phase_share": {n: round(v[0] / step_total, 4) for n, v in phases.items() if step_total > 0},
             "kernel_rooflines": rooflines}
+    if parity is not None:
+        line["parity"] = parity
+    if nccl_log is not None:
+        line["nccl"] = nccl_summary(nccl_log)
 
     # ---- the north star's comparator: full GPU prefill of the same request, same kernels
     if args.full_steps > 0:
@@ -405,7 +562,7 @@ def main():
             pipe.full_prefill_step()
         f1.record(stream)
         torch.cuda.synchronize()
-        full_ms = f0.elapsed_time(f1) / args.full_steps
+        full_ms = pdist.max_over_ranks(f0.elapsed_time(f1) / args.full_steps, device="cuda")
         H, dk = cfg.n_heads, cfg.head_dim
         full_tf = 2.0 * s * dm.weight_bytes(include_head=False) * dm.tp_world / 2 + 4.0 * L * H * dk * s * (s + 1) / 2
         line["full_prefill"] = {"ttft_ms": full_ms, "tok_per_s": s / (full_ms / 1e3),
@@ -440,7 +597,8 @@ def main():
                 g1.record(stream)
                 torch.cuda.synchronize()
                 t_ms = pdist.max_over_ranks(g0.elapsed_time(g1) / args.sweep_steps, device="cuda")
-                sweep[f"{pp:g}"] = {"k": sp_pipe.k, "ttft_ms": t_ms, "tok_per_s": s / (t_ms / 1e3)}
+                sweep[f"{pp:g}"] = {"k": sp_pipe.k, "ttft_ms": t_ms, "tok_per_s": s / (t_ms / 1e3),
+                                    "ttft_floor_ms": round(ttft_floor_ms(cfgd, pp, args.m, hbm, tf_burst), 2)}
                 del sp_pipe
                 torch.cuda.empty_cache()
             if "full_prefill" in line:
@@ -450,7 +608,7 @@ def main():
 
     # ---- e2e through the public API with host (pinned) inputs
     if args.e2e_steps > 0:
-        host =[(c._k_dev.cpu().pin_memory(), c._v_dev.cpu().pin_memory(), c.token_ids) for c in chunks]
+        host = [(c._k_dev.cpu().pin_memory(), c._v_dev.cpu().pin_memory(), c.token_ids) for c in chunks]
         h2d = sum(a.numel() * 2 + b.numel() * 2 for a, b, _ in host)
         torch.cuda.synchronize()
         mw = dm
@@ -458,7 +616,7 @@ def main():
         def e2e_step():
             # host-tier chunk store: assemble() streams the pinned K/V to HBM layer by
             # layer, overlapped with the scoring pass
-            dch = [P.ChunkKV.from_pinned(i, "device-random", ids, a, b, cfg.head_dim)
+            dch = [P.ChunkKV.from_pinned(i, dm.fingerprint, ids, a, b, cfg.head_dim)
                    for i, (a, b, ids) in enumerate(host)]
             cache = P.assemble(dch, dm.cache_config, fp32_taps=False)
             sc = P.score_prophet(mw, cfg, cache, query)
@@ -468,15 +626,13 @@ def main():
 
         e2e_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = pdist.max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps, device="cuda")
         d2h = L * s * 4 + s * 4 + k * 4 + cfg.vocab_size * 4
         line["e2e"] = {"value": (1 if heads else world) * s / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
                        "h2d_bytes_per_step": int(h2d + args.m * 8), "d2h_bytes_per_step": int(d2h),
@@ -487,7 +643,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ttft, tm, kk, n_s, wall = cpu_sample(cfgd, args.p, n_rows=args.ref_rows)
         line["cpu_baseline"] = {"value": s / ttft, "unit": "tok/s", "cores": cpu_cores(), "kind": "port",
-                                "ttft_ms": ttft * 1e3,
+                                "ttft_ms": ttft * 1e3, "threads": cpu_threads(),
                                 "sample": f"oracle port of pikv: 1 layer, full width, s={s}, Stage II on {n_s}/{kk} "
                                           f"rows; extrapolated x{L} layers (sample wall {wall:.1f}s)"}
     if rank == 0:

@@ -62,13 +62,16 @@ enum {
   PKV_QP_LOGITS = 4,    /* compute last-row logits (finalize_query) */
   PKV_QP_APPEND_KV = 8, /* append query K/V to the cache pool at positions s.. */
   PKV_QP_FROM_CHUNKS = 16, /* read context keys/values from the chunk store (naive cache) */
-  PKV_QP_PROBE = 32       /* low-layer probe (selection.py:95-124): stop after layer 1's QKV
+  PKV_QP_PROBE = 32,      /* low-layer probe (selection.py:95-124): stop after layer 1's QKV
                              projection (fresh_v[1] = the probe's layer-1 values); the m
                              rows are context tokens s.. attending causally to [0, s) and
                              to their own assembled layer-0 entries.  With PKV_QP_SCORES,
                              per_layer[0..s) = layer 0's head/query-mean scores of the rows
                              and per_layer[s..s+m) = sum over rows q >= i of row q's
                              head-mean probability on block key i (kvshare column sums) */
+  PKV_QP_ROWS = 64        /* capture_attn (query_pass model.py:386-398): per_layer receives the
+                             head-averaged attention rows [L][m][s+m] f32 of every query token
+                             over the s context and m query keys (unsharded models) */
 };
 
 /* reference ModelConfig, model.py:24-63 */
@@ -121,6 +124,9 @@ typedef struct pkv_cache {
                                 layer_done[l] once layer l's K/V are final (after its QKV scatter),
                                 so the final query pass can follow Stage II layer by layer on
                                 another stream (pass it these events as layer_ready) */
+  int32_t* nonfinite;        /* nullable device int32: OR-ed with 1 when a Stage-II epilogue writes a
+                                non-finite (or fp16-overflowing) value; the host raises NumericsError
+                                (reference check_finite, tensor.py:31-34) */
 } pkv_cache;
 
 /* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */
@@ -153,7 +159,8 @@ int pkv_assemble_layers(const pkv_config* cfg, const pkv_chunks* chunks, const p
 /* query_pass -- model.py:370-402; with PKV_QP_SCORES it is score_prophet
  * (selection.py:64-86, per_layer [L][s] f32); with PKV_QP_LOGITS|PKV_QP_APPEND_KV
  * it is finalize_query (recompute.py:105-125, last_logits [vocab] f32).
- * query_ids: device int32 [m].  fresh_k/fresh_v (nullable): fp32 [L][m][Hkv][head_dim]. */
+ * query_ids: device int32 [m].  fresh_k/fresh_v (nullable): fp32 [L][m][Hkv][head_dim].
+ * With PKV_QP_ROWS, per_layer is the capture_attn rows buffer [L][m][s+m]. */
 size_t pkv_query_pass_workspace(const pkv_model* m, int32_t s, int32_t n_query, int32_t flags);
 int pkv_query_pass(const pkv_model* m, const pkv_cache* cache, const pkv_chunks* chunks, const int32_t* query_ids,
                    int32_t n_query, int32_t flags, float* per_layer, float* fresh_k, float* fresh_v,

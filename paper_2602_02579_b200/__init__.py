@@ -15,6 +15,7 @@ from .model import (DeviceModel, FlopCounter, FlopTally, KVCache, LayerWeights, 
                     random_weights)
 from .decode import GenerationResult, decode_step, greedy_generate
 from .prefill import PrefillTrace, full_prefill, precompute_chunk
+from .querypass import QueryPassResult, query_pass
 from .recompute import (AnswerRecord, FinalizeResult, RecomputePlan, StrategyRun, finalize_query,
                         recompute_selected, run_strategy, selection_digest)
 from .selection import (STRATEGIES, SelectionResult, ValueScores, fuse_layers, score_cacheblend_l1, score_epic,

@@ -26,6 +26,7 @@ PKV_QP_LOGITS = 4
 PKV_QP_APPEND_KV = 8
 PKV_QP_FROM_CHUNKS = 16
 PKV_QP_PROBE = 32
+PKV_QP_ROWS = 64
 PKV_DT_F32, PKV_DT_F64, PKV_DT_BF16 = 0, 1, 2
 
 
@@ -48,7 +49,7 @@ class Cache(ctypes.Structure):
     _fields_ = [("k_pool", c_vp), ("v_pool", c_vp), ("pool_tokens", c_i64), ("page_table", c_vp), ("s", c_i32),
                 ("token_ids", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("rope_len", c_i32), ("recomputed", c_vp),
                 ("k2_pool", c_vp), ("layer_ready", ctypes.POINTER(c_vp)),
-                ("rope_cs32", c_vp), ("layer_done", ctypes.POINTER(c_vp))]
+                ("rope_cs32", c_vp), ("layer_done", ctypes.POINTER(c_vp)), ("nonfinite", c_vp)]
 
 
 class Chunks(ctypes.Structure):

@@ -204,6 +204,8 @@ class AssembledCache:
         self._d_src_local = torch.from_numpy(self.source_local).to(dev)
         self._d_tokens = torch.from_numpy(self.token_ids.astype(np.int32)).to(dev)
         self._d_recomp = torch.zeros(s, dtype=torch.uint8, device=dev)
+        # device check_finite of the Stage-II epilogues (include/pkv.h pkv_cache.nonfinite)
+        self._d_nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.pool_tokens = -(-(s + QUERY_RESERVE) // PAGE) * PAGE
         n_pages = self.pool_tokens // PAGE
         self._d_pages = torch.arange(n_pages, dtype=torch.int32, device=dev)
@@ -313,7 +315,15 @@ class AssembledCache:
         return _lib.Cache(self.k_pool.data_ptr(), self.v_pool.data_ptr(), self.pool_tokens, self._d_pages.data_ptr(),
                           self.context_length, self._d_tokens.data_ptr(), self._rcos.data_ptr(),
                           self._rsin.data_ptr(), self.rope_len, self._d_recomp.data_ptr(), self.k2_pool.data_ptr(),
-                          ready, self._rcs32.data_ptr())
+                          ready, self._rcs32.data_ptr(), nonfinite=self._d_nonfinite.data_ptr())
+
+    def check_finite(self) -> None:
+        """Raise NumericsError if a Stage-II epilogue wrote a non-finite (or fp16-overflowing)
+        value -- the reference checks every kernel output (tensor.py:31-34); the device flag
+        is read here, after a synchronisation (finalize_query calls it)."""
+        from .errors import NumericsError
+        if int(self._d_nonfinite.item()) != 0:
+            raise NumericsError("non-finite values in the Stage-II repair")
 
     def wait_ready(self, stream=None) -> None:
         """Make `stream` (default: current) wait for a pipelined chunk transfer to finish."""

@@ -427,7 +427,7 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   }
   const int row_blocks = ceil_div(R, 128);
   (void)row_blocks;
-  if (flags & PKV_QP_SCORES) {
+  if (flags & (PKV_QP_SCORES | PKV_QP_ROWS)) {
     w.S = cv.take<float>((size_t)Hkv * R * s_tot);
     w.rows = cv.take<float>((size_t)m * s);
     w.denom = cv.take<double>((size_t)m);
@@ -460,6 +460,8 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
   if (c->rope_len < s + m) return set_error(PKV_ERR_SHAPE, "rope table shorter than context + query");
   if ((flags & PKV_QP_FROM_CHUNKS) && !ch) return set_error(PKV_ERR_ARGUMENT, "chunk view required");
   if ((flags & PKV_QP_APPEND_KV) && c->pool_tokens < s + m) return set_error(PKV_ERR_SHAPE, "pool too small to append");
+  if ((flags & PKV_QP_ROWS) && (flags & (PKV_QP_SCORES | PKV_QP_PROBE)))
+    return set_error(PKV_ERR_ARGUMENT, "PKV_QP_ROWS excludes PKV_QP_SCORES / PKV_QP_PROBE");
   size_t need = 0;
   QpWs w = carve_qp(md, s, m, flags, workspace, &need);
   if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
@@ -550,7 +552,8 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.fk = w.k;
     a.fv = w.v;
     const bool scores = (flags & PKV_QP_SCORES) && per_layer;
-    a.S = scores ? w.S : nullptr;
+    const bool capture = (flags & PKV_QP_ROWS) && per_layer;
+    a.S = (scores || capture) ? w.S : nullptr;
     // pipelined transfer: layer l of the cache may still be in flight
     if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
@@ -560,7 +563,8 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.x3_out = x3;
     a.x3_ld = ldx;
     TTRY(T_QP_ATTN, s1_attention_launch(a, w.attn, w.Mfin, w.Lfin, w.rows, w.denom, scores ? per_layer + (long)l * s : nullptr,
-                            (flags & PKV_QP_RENORM) ? 1 : 0, cf.n_heads, w.rows64, comm, st));
+                            (flags & PKV_QP_RENORM) ? 1 : 0, cf.n_heads, w.rows64, comm, st,
+                            capture ? per_layer + (long)l * m * (s + m) : nullptr));
     if ((flags & PKV_QP_PROBE) && scores && l == 0)  // block keys' column sums after the context's
       TTRY(T_QP_MISC, probe_diag_colsum_launch(w.q, w.k, w.Mfin, w.Lfin, m, H, Hkv, dk, dkp, a.scale, per_layer + s, st));
     // without logits (score_prophet) the last layer's o-projection and MLP only feed a
@@ -690,18 +694,21 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     a.ssq_ld = ntile;
   };
   if (w.sk_cnt) cudaMemsetAsync(w.sk_cnt, 0, w.sk_cnt_n * sizeof(int), st);
-  if (c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
   TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
   for (int l = 0; l < cf.n_layers; ++l) {
     const pkv_layer_weights& lw = md->layers[l];
     // the scatter must land after this layer's (possibly pipelined) assembly
     if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
+    // the repaired-entry flags: after layer 0's assembly, which clears them (a pipelined
+    // host-tier assembly runs on another stream)
+    if (l == 0 && c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
     if (l == 0 || !defer)
       TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
     if (defer && l > 0) consume(g);
     g.f16 = 1;
+    g.nonfinite = c->nonfinite;
     g.acc_scale = lw.wscale[0];
     g.sk_part = w.sk_part;
     g.sk_cnt = w.sk_cnt;
@@ -746,6 +753,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
                        (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
     GemmArgs go{};
     go.f16 = 1;
+    go.nonfinite = c->nonfinite;
     go.acc_scale = lw.wscale[1];
     go.sk_part = w.sk_part;
     go.sk_cnt = w.sk_cnt;
@@ -763,6 +771,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
       TTRY(T_RC_MISC, norm_defer_launch(w.h, k, Dp, Dp, lw.ffn_norm, w.xb, Dp, w.ssq, ntile, st));
     GemmArgs gg{};
     gg.f16 = 1;
+    gg.nonfinite = c->nonfinite;
     gg.acc_scale = lw.wscale[2];
     gg.sk_part = w.sk_part;
     gg.sk_cnt = w.sk_cnt;
@@ -775,6 +784,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
     GemmArgs gd{};
     gd.f16 = 1;
+    gd.nonfinite = c->nonfinite;
     gd.acc_scale = lw.wscale[3];
     gd.sk_part = w.sk_part;
     gd.sk_cnt = w.sk_cnt;

@@ -80,6 +80,8 @@ struct GemmArgs {
   float norm_eps;
   int f16;                    // operands fp16 (Stage II, narrow projections) instead of bf16
   float acc_scale;            // accumulator multiplier (2^-e of the pre-scaled fp16 weights)
+  int* nonfinite;             // nullable: OR-ed with 1 when EPI_QKV / EPI_SILU / EPI_RESID write a
+                              // non-finite value (the reference's check_finite, tensor.py:31-34)
 };
 constexpr int SK_MAXP = 8;    // pieces per tail tile (host plan guarantees)
 
@@ -452,6 +454,7 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
       }
+      bool bad = false;  // a non-finite output in this work item (nonfinite flag)
       if (do_epi) {
       [[maybe_unused]] float rnorm = 1.f;
       if constexpr (EPI == EPI_QKV || EPI == EPI_SILU) {
@@ -578,6 +581,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int j = 0; j < 16; ++j) {
               float a0 = silu_f(__uint_as_float(g[2 * j]) * sc) * (__uint_as_float(u[2 * j]) * sc);
               float a1 = silu_f(__uint_as_float(g[2 * j + 1]) * sc) * (__uint_as_float(u[2 * j + 1]) * sc);
+              bad |= !(fabsf(a0) <= 65504.f) || !(fabsf(a1) <= 65504.f);  // non-finite or fp16 overflow
               packed[j] = pack_f16(a0, a1);
             }
             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(args.C) + (long)row * args.ldc + col);
@@ -613,6 +617,7 @@ __global__ void __launch_bounds__(192, 1)
                                        __uint_as_float(r[4 * j + 2]) * asc, __uint_as_float(r[4 * j + 3]) * asc);
                 if constexpr (EPI == EPI_RESID) {
                   v.x += o[j].x; v.y += o[j].y; v.z += o[j].z; v.w += o[j].w;
+                  bad |= !isfinite(v.x + v.y + v.z + v.w);
                   r[4 * j] = __float_as_uint(v.x);
                   r[4 * j + 1] = __float_as_uint(v.y);
                   r[4 * j + 2] = __float_as_uint(v.z);
@@ -723,7 +728,10 @@ __global__ void __launch_bounds__(192, 1)
             // q -> fp16 operand buffer; k -> fp16 pool + fp16 residual plane; v -> fp16 pool
             uint32_t packed[16], pk2[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) split2h_pack(vals[2 * j], vals[2 * j + 1], packed[j], pk2[j]);
+            for (int j = 0; j < 16; ++j) {
+              bad |= !(fabsf(vals[2 * j]) <= 65504.f) || !(fabsf(vals[2 * j + 1]) <= 65504.f);
+              split2h_pack(vals[2 * j], vals[2 * j + 1], packed[j], pk2[j]);
+            }
             __half* dst;
             if (head_all < H) {
               dst = reinterpret_cast<__half*>(args.C) + (long)row * args.ldc + col0;
@@ -757,6 +765,9 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       }  // do_epi
+      if constexpr (EPI == EPI_QKV || EPI == EPI_SILU || EPI == EPI_RESID) {
+        if (args.nonfinite != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(args.nonfinite, 1);
+      }
       if constexpr (EPI != EPI_PROJ || CG == 2) {  // (EPI_PROJ, CG = 1 released it above)
         tc_fence_before();
         __syncwarp();

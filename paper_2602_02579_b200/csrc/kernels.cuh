@@ -88,7 +88,8 @@ struct S1TcArgs {
 int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
                       cudaStream_t st);
 int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
-                        float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st);
+                        float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st,
+                        float* capture_rows = nullptr);
 int gemv_launch(const float* x, const void* W, int N, int D, long ldw, float* out, cudaStream_t st);
 int norm_defer_launch(const float* h, int m, long ld, int N, const float* g, void* xg, long ldxg, float* ssq,
                       int ssq_ld, cudaStream_t st);

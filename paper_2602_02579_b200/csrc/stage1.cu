@@ -795,7 +795,8 @@ __global__ void s1_attn_combine_fresh(const float* Opart, const float* Mpart, co
 // One warp per context token, lane = query i (S loads of 32 consecutive rows).  p is
 // evaluated as 2^(S*log2e - M*log2e) * (1/L) (rel. error ~3e-7, far inside the 1e-4
 // score tolerance); the query mean is a fixed-order f64 warp reduction.
-//   MODE 0: per_layer directly;  MODE 1: rows [m][s] f32 (renormalised scoring);
+//   MODE 0: per_layer directly;  MODE 1: rows [m][ld] f32 (renormalised scoring: ld = s;
+//           capture_attn: ld = s + m, the fresh-key columns by s1_fresh_rows_kernel);
 //   MODE 2: this rank's head sums rows64 [s][m] f64 (tensor parallel; summed over ranks,
 //           then s1_scores_finish applies the mean over all H heads).
 enum { SC_MEAN = 0, SC_ROWS = 1, SC_PARTIAL = 2 };
@@ -809,7 +810,7 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 template <int MODE>
 __global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict__ S, const float* __restrict__ Mfin,
                                                         const float* __restrict__ Lfin, int Hkv, int G, int R, int m,
-                                                        int s, int H_total, float* out, double* out64) {
+                                                        int s, int H_total, float* out, double* out64, long ld) {
   pdl_entry();
   extern __shared__ float2 shn[];  // [Hkv*R]: (M*log2e, 1/L) per row g*R + r
   constexpr float LOG2E = 1.4426950408889634f;
@@ -860,7 +861,7 @@ __global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict_
       } else {
         const float rv = (float)(acc / (double)H_total);
         if (MODE == SC_ROWS) {
-          if (i < m) out[(long)i * s + t] = rv;
+          if (i < m) out[(long)i * ld + t] = rv;
         } else if (i < m) {
           tok += (double)rv;
         }
@@ -876,7 +877,7 @@ __global__ void __launch_bounds__(256) s1_scores_kernel(const float* __restrict_
 // after the rank sum: rows64 [s][m] -> MODE 0 per_layer / MODE 1 rows [m][s]
 template <int MODE>
 __global__ void __launch_bounds__(256) s1_scores_finish(const double* __restrict__ rows64, int m, int s, int H_total,
-                                                        float* out) {
+                                                        float* out, long ld) {
   pdl_entry();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(256) s1_scores_finish(const double* __restrict
     double tok = 0.0;
     for (int i = lane; i < m; i += 32) {
       const float rv = (float)(rows64[(long)t * m + i] / (double)H_total);
-      if (MODE == SC_ROWS) out[(long)i * s + t] = rv;
+      if (MODE == SC_ROWS) out[(long)i * ld + t] = rv;
       else tok += (double)rv;
     }
     if (MODE == SC_MEAN) {
@@ -892,6 +893,33 @@ __global__ void __launch_bounds__(256) s1_scores_finish(const double* __restrict
       if (lane == 0) out[t] = (float)(tok / (double)m);
     }
   }
+}
+
+// capture_attn rows, the query's own keys (columns s..s+m-1 of rows [m][ld]): the head mean
+// of p = exp(S - M) / L with S recomputed exactly as the fresh-key split forms it
+// (sequential f32 FMAs over the padded head dim, then * scale) and the final row max /
+// sum; causal within the query (j > i: 0)
+__global__ void s1_fresh_rows_kernel(const float* q, const float* k, const float* Mfin, const float* Lfin, int m,
+                                     int H, int Hkv, int dkp, float scale, int s, float* out, long ld) {
+  const int i = blockIdx.x, j = threadIdx.x;
+  if (j >= m) return;
+  constexpr float LOG2E = 1.4426950408889634f;
+  const int G = H / Hkv, R = m * G;
+  float rv = 0.f;
+  if (j <= i) {
+    double acc = 0.0;
+    for (int h = 0; h < H; ++h) {
+      const int g = h / G, jh = h - g * G;
+      const float* qp = q + ((long)i * H + h) * dkp;
+      const float* kp = k + ((long)j * Hkv + g) * dkp;
+      float sc = 0.f;
+      for (int d = 0; d < dkp; ++d) sc = fmaf(qp[d], kp[d], sc);
+      const int r = g * R + jh * m + i;
+      acc += (double)(ex2(fmaf(sc * scale, LOG2E, -Mfin[r] * LOG2E)) * (1.f / Lfin[r]));
+    }
+    rv = (float)(acc / (double)H);
+  }
+  out[(long)i * ld + s + j] = rv;
 }
 
 // optional context-only renormalisation denominators (selection.py:80-84)
@@ -926,7 +954,8 @@ __global__ void s1_query_mean_kernel(const float* rows, const double* denom, int
 }
 
 int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
-                        float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st) {
+                        float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st,
+                        float* capture_rows) {
   S1Attn a = a_in;
   const int row_blocks = ceil_div(a.R, 128);
   int total_splits = a.n_splits;
@@ -1014,7 +1043,27 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   }
-  if (a.S != nullptr && per_layer != nullptr && a.s > 0) {  // (s = 0: no context keys to score)
+  if (a.S != nullptr && capture_rows != nullptr) {  // capture_attn: head-mean rows [m][s + m]
+    const long ld = a.s + a.m;
+    if (comm_world(comm) > 1) return set_error(PKV_ERR_CONFIG, "capture_attn is not supported head-sharded");
+    if (a.s > 0) {
+      const int sgrid = std::min(ceil_div(a.s, 8), 8 * num_sms());
+      const size_t ssmem = (size_t)a.Hkv * a.R * sizeof(float2);
+      static std::once_flag once_c;
+      std::call_once(once_c, [] {
+        cudaFuncSetAttribute(s1_scores_kernel<SC_ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      });
+      launch_k(s1_scores_kernel<SC_ROWS>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
+               capture_rows, (double*)nullptr, ld);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_scores_kernel");
+    }
+    if (a.m > 1024) return set_error(PKV_ERR_SHAPE, "capture_attn: query longer than 1024 tokens");
+    s1_fresh_rows_kernel<<<a.m, ((a.m + 31) / 32) * 32, 0, st>>>(a.q, a.fk, Mfin, Lfin, a.m, a.H, a.Hkv, a.dkp,
+                                                                 a.scale, a.s, capture_rows, ld);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("s1_fresh_rows_kernel");
+  } else if (a.S != nullptr && per_layer != nullptr && a.s > 0) {  // (s = 0: no context keys to score)
     const int sgrid = std::min(ceil_div(a.s, 8), 8 * num_sms());
     const size_t ssmem = (size_t)a.Hkv * a.R * sizeof(float2);
     if (ssmem > 48 * 1024) {
@@ -1028,22 +1077,22 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     if (comm_world(comm) > 1) {
       // per-token score exchange before the global top-k: sum the ranks' head partials
       launch_k(s1_scores_kernel<SC_PARTIAL>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
-                                                              nullptr, rows64);
+               (float*)nullptr, rows64, (long)a.s);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_scores_kernel");
       int rc = comm_allreduce(comm, rows64, (size_t)a.m * a.s, PKV_DT_F64, st);
       if (rc) return rc;
-      if (renorm) launch_k(s1_scores_finish<SC_ROWS>, sgrid, 256, 0, st, rows64, a.m, a.s, H_total, target);
-      else launch_k(s1_scores_finish<SC_MEAN>, sgrid, 256, 0, st, rows64, a.m, a.s, H_total, target);
+      if (renorm) launch_k(s1_scores_finish<SC_ROWS>, sgrid, 256, 0, st, rows64, a.m, a.s, H_total, target, (long)a.s);
+      else launch_k(s1_scores_finish<SC_MEAN>, sgrid, 256, 0, st, rows64, a.m, a.s, H_total, target, (long)a.s);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_scores_finish");
     } else {
       if (renorm)
         launch_k(s1_scores_kernel<SC_ROWS>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
-                                                             target, nullptr);
+                 target, (double*)nullptr, (long)a.s);
       else
         launch_k(s1_scores_kernel<SC_MEAN>, sgrid, 256, ssmem, st, a.S, Mfin, Lfin, a.Hkv, a.G, a.R, a.m, a.s, H_total,
-                                                             target, nullptr);
+                 target, (double*)nullptr, (long)a.s);
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_scores_kernel");
     }

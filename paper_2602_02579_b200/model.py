@@ -321,87 +321,77 @@ class DeviceModel:
         torch = _lib.require_cuda()
         weights.validate(config)
         dev = device or torch.device("cuda", torch.cuda.current_device())
-        lay = Layout.of(config)
-        H, Hkv, dk = config.n_heads, config.n_kv_heads, config.head_dim
-        bf = torch.bfloat16
 
         def up(a):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=F32)).to(dev)
 
+        names = ("attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")
+        layers = ({k: up(getattr(lw, k)) for k in names} for lw in weights.layers)
+        return cls._build(config, layers, up(weights.embed), up(weights.lm_head), up(weights.final_norm),
+                          weights.fingerprint(config), dev)
+
+    @classmethod
+    def _build(cls, config: ModelConfig, layers_ref, embed, lm_head, final_norm, fingerprint: str, dev):
+        """Device layout from reference-layout device tensors (input-major [fan_in, fan_out]
+        projections, one dict per layer; consumed one layer at a time)."""
+        torch = _lib.require_cuda()
+        lay = Layout.of(config)
+        H, Hkv, dk = config.n_heads, config.n_kv_heads, config.head_dim
+        bf = torch.bfloat16
+
         def heads_rows(w, n_h):  # [D, n_h*dk] -> [n_h*dkp, Dp] (transposed, padded per head)
-            t = up(w).t().reshape(n_h, dk, -1)
+            t = w.float().t().reshape(n_h, dk, -1)
             out = torch.zeros((n_h, lay.dkp, lay.Dp), dtype=torch.float32, device=dev)
             out[:, :dk, : config.hidden_dim] = t
             return out.reshape(n_h * lay.dkp, lay.Dp)
 
         def norm(g):
             out = torch.zeros(lay.Dp, dtype=torch.float32, device=dev)
-            out[: config.hidden_dim] = up(g)
+            out[: config.hidden_dim] = g.float()
             return out
 
         layers = []
-        for lw in weights.layers:
-            wqkv, s_qkv = fp16_scaled(torch.cat([heads_rows(lw.wq, H), heads_rows(lw.wk, Hkv), heads_rows(lw.wv, Hkv)]))
-            wo = up(lw.wo).t().reshape(config.hidden_dim, H, dk)
+        for lw in layers_ref:
+            wqkv, s_qkv = fp16_scaled(torch.cat([heads_rows(lw["wq"], H), heads_rows(lw["wk"], Hkv),
+                                                 heads_rows(lw["wv"], Hkv)]))
+            wo = lw["wo"].float().t().reshape(config.hidden_dim, H, dk)
             wo_p = torch.zeros((lay.Dp, H, lay.dkp), dtype=torch.float32, device=dev)
             wo_p[: config.hidden_dim, :, :dk] = wo
             wo16, s_o = fp16_scaled(wo_p.reshape(lay.Dp, lay.HQ))
-            del wo_p
-            g = _pad2(up(lw.w_gate).t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
-            u = _pad2(up(lw.w_up).t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
+            del wo_p, wo
+            g = _pad2(lw["w_gate"].float().t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
+            u = _pad2(lw["w_up"].float().t(), lay.Fp, lay.Dp).reshape(lay.Fp // 128, 128, lay.Dp)
             wgu, s_gu = fp16_scaled(torch.stack([g, u], dim=1).reshape(2 * lay.Fp, lay.Dp))
             del g, u
-            wd, s_d = fp16_scaled(_pad2(up(lw.w_down).t(), lay.Dp, lay.Fp))
-            layers.append({"attn_norm": norm(lw.attn_norm), "ffn_norm": norm(lw.ffn_norm), "wqkv": wqkv,
+            wd, s_d = fp16_scaled(_pad2(lw["w_down"].float().t(), lay.Dp, lay.Fp))
+            layers.append({"attn_norm": norm(lw["attn_norm"]), "ffn_norm": norm(lw["ffn_norm"]), "wqkv": wqkv,
                            "wo": wo16, "wgu": wgu, "wd": wd, "wscale": (s_qkv, s_o, s_gu, s_d)})
+            del lw
         tensors = {"layers": layers,
-                   "embed": _pad2(up(weights.embed), config.vocab_size, lay.Dp).to(bf).contiguous(),
-                   "lm_head": _pad2(up(weights.lm_head).t(), config.vocab_size, lay.Dp).to(bf).contiguous(),
-                   "final_norm": norm(weights.final_norm)}
-        return cls(config, tensors, weights.fingerprint(config))
+                   "embed": _pad2(embed.to(bf), config.vocab_size, lay.Dp).contiguous(),
+                   "lm_head": _pad2(lm_head.to(bf).t(), config.vocab_size, lay.Dp).contiguous(),
+                   "final_norm": norm(final_norm)}
+        return cls(config, tensors, fingerprint)
 
     @classmethod
-    def random(cls, config: ModelConfig, seed: int = 0, device=None) -> "DeviceModel":
-        """Random-init weights generated on the device (benchmarks; the layout matches
-        from_host, the values follow the reference's N(0,1)/sqrt(fan_in), bf16-rounded)."""
+    def synthetic(cls, config: ModelConfig, seed: int = 0, device=None) -> "DeviceModel":
+        """Random-init weights generated on the device by the SYN1 generator
+        (paper_2602_02579_b200/synthetic.py): the reference's initialisation scale, bf16-exact
+        values that the CPU oracle rebuilds bit for bit (oracle/synthetic_inputs.py)."""
+        from . import synthetic as S
         torch = _lib.require_cuda()
         dev = device or torch.device("cuda", torch.cuda.current_device())
-        lay = Layout.of(config)
-        g = torch.Generator(device=dev)
-        g.manual_seed(seed)
-        bf = torch.bfloat16
-        D, F, dk, H, Hkv = config.hidden_dim, config.ffn_dim, config.head_dim, config.n_heads, config.n_kv_heads
+        ones = torch.ones(config.hidden_dim, dtype=torch.float32, device=dev)
 
-        def rnd(rows, cols, fan_in, real_rows, real_cols, dtype=bf):
-            t = torch.zeros((rows, cols), dtype=dtype, device=dev)
-            t[:real_rows, :real_cols] = (torch.randn((real_rows, real_cols), generator=g, device=dev,
-                                                     dtype=torch.float32) / fan_in ** 0.5).to(bf)
-            return t
+        def layers():
+            for li in range(config.n_layers):
+                d = S.layer_weights(config, li, seed, dev)
+                d["attn_norm"], d["ffn_norm"] = ones, ones
+                yield d
+        return cls._build(config, layers(), S.embed(config, seed, dev), S.lm_head(config, seed, dev), ones,
+                          f"syn1-{seed}", dev)
 
-        ones = torch.zeros(lay.Dp, dtype=torch.float32, device=dev)
-        ones[:D] = 1.0
-        layers = []
-        for _ in range(config.n_layers):
-            if dk == lay.dkp and D == lay.Dp:
-                wqkv = (torch.randn((lay.NQKV, D), generator=g, device=dev) / D ** 0.5).to(bf).float()
-            else:
-                wqkv = torch.zeros((H + 2 * Hkv, lay.dkp, lay.Dp), dtype=torch.float32, device=dev)
-                wqkv[:, :dk, :D] = (torch.randn((H + 2 * Hkv, dk, D), generator=g, device=dev) / D ** 0.5).to(bf)
-                wqkv = wqkv.reshape(lay.NQKV, lay.Dp)
-            wo = rnd(lay.Dp, lay.HQ, H * dk, D, lay.HQ, torch.float32)
-            if dk != lay.dkp:
-                wo.view(lay.Dp, H, lay.dkp)[:, :, dk:] = 0
-            wqkv, s_qkv = fp16_scaled(wqkv)
-            wo, s_o = fp16_scaled(wo)
-            wgu, s_gu = fp16_scaled(rnd(2 * lay.Fp, lay.Dp, D, 2 * lay.Fp, D, torch.float32))
-            wd, s_d = fp16_scaled(rnd(lay.Dp, lay.Fp, F, D, F, torch.float32))
-            layers.append({"attn_norm": ones.clone(), "ffn_norm": ones.clone(), "wqkv": wqkv, "wo": wo, "wgu": wgu,
-                           "wd": wd, "wscale": (s_qkv, s_o, s_gu, s_d)})
-        embed = torch.zeros((config.vocab_size, lay.Dp), dtype=bf, device=dev)
-        embed[:, :D] = torch.randn((config.vocab_size, D), generator=g, device=dev).to(bf)
-        tensors = {"layers": layers, "embed": embed, "lm_head": rnd(config.vocab_size, lay.Dp, D, config.vocab_size, D),
-                   "final_norm": ones.clone()}
-        return cls(config, tensors, f"device-random-{seed}")
+    random = synthetic  # benchmark weights (round-1 name)
 
     def shard(self, rank: int, world: int, comm) -> "DeviceModel":
         """Rank `rank`'s tensor-parallel slice of this model (include/pkv.h, "Head-sharded

@@ -106,35 +106,39 @@ class PrefillPipeline:
                                       None, None, self.logits.data_ptr(), self.ws_qp.data_ptr(), self.ws_qp.numel(),
                                       st))
 
-    def capture(self):
-        """Record one step into a CUDA graph (call after a warm-up step so every
-        kernel attribute is set); replay() then launches the ~1.5k kernels of a
-        prefill with one host call."""
+    def capture(self, fn=None):
+        """Record one step (or `fn`, e.g. self.stage2) into a CUDA graph (call after a
+        warm-up step so every kernel attribute is set); replay() then launches the ~1.5k
+        kernels of a prefill with one host call.  Returns the graph."""
         torch = _lib.require_cuda()
-        self.graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            with torch.cuda.graph(self.graph, stream=side):
-                self.step()
+            with torch.cuda.graph(graph, stream=side):
+                (fn or self.step)()
         torch.cuda.current_stream().wait_stream(side)
         # the events' last record was a capture node: waiting on them from eager work
         # (full_prefill_step, an eager step()) is an error until they are recorded again
         for e in self.layer_events + self.done_events:
             e.record()
-        return self.graph
+        if fn is None:
+            self.graph = graph
+        return graph
 
     def replay(self) -> None:
         self.graph.replay()
 
-    def step(self, stream=None) -> None:
-        """One full prefill; results stay on the device (idx, logits, per_layer)."""
+    def score_select(self, stream=None) -> None:
+        """assemble -> scoring pass -> fuse + top-k only (per_layer, fused, idx)."""
         torch = _lib.require_cuda()
-        lib = _lib.load()
-        st = _lib.stream_ptr(torch, stream)
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self._stage1(_lib.load(), _lib.stream_ptr(torch, stream), main)
+        main.wait_stream(self.side)
+
+    def _stage1(self, lib, st, main) -> None:
         c = self.cache
         cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
-        main = stream if stream is not None else torch.cuda.current_stream()
         self.side.wait_stream(main)
         if self.pipelined_assembly:
             for li in range(self.cfg.n_layers):
@@ -147,11 +151,45 @@ class PrefillPipeline:
         _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_score,
                                       self.per_layer.data_ptr(), None, None, None, self.ws_qp.data_ptr(),
                                       self.ws_qp.numel(), st))
-        if self.final_overlap:
-            # after the scoring pass (it shares ws_qp); layer l waits on done[l]
-            self.fin.wait_stream(main)
         _lib.check(lib.pkv_fuse_select(self.per_layer.data_ptr(), self.cfg.n_layers, self.s, self.k,
                                        self.fused.data_ptr(), self.idx.data_ptr(), self.status.data_ptr(), None, 0, st))
+
+    def _plain_cache(self):
+        """The cache view without per-layer readiness events (standalone phases: every layer
+        is assembled before they run, and a graph capture may not wait on eager events)."""
+        cc = _lib.Cache.from_buffer_copy(self.cache.c_cache)
+        cc.layer_ready = None
+        self._c_plain = cc
+        return cc
+
+    def stage2(self, stream=None) -> None:
+        """Stage II alone (recompute of the current selection idx), serial order."""
+        torch = _lib.require_cuda()
+        _lib.check(_lib.load().pkv_recompute(self.dm.handle, ctypes_ref(self._plain_cache()), self.idx.data_ptr(),
+                                             self.k, None, None, self.ws_rc.data_ptr(), self.ws_rc.numel(),
+                                             _lib.stream_ptr(torch, stream)))
+
+    def final(self, stream=None) -> None:
+        """The final query pass alone (first-token logits over the repaired cache)."""
+        torch = _lib.require_cuda()
+        c = self.cache
+        _lib.check(_lib.load().pkv_query_pass(self.dm.handle, ctypes_ref(self._plain_cache()), ctypes_ref(c.c_chunks),
+                                              self.query.data_ptr(), self.m, self.flags_final, None, None, None,
+                                              self.logits.data_ptr(), self.ws_qp.data_ptr(), self.ws_qp.numel(),
+                                              _lib.stream_ptr(torch, stream)))
+
+    def step(self, stream=None) -> None:
+        """One full prefill; results stay on the device (idx, logits, per_layer)."""
+        torch = _lib.require_cuda()
+        lib = _lib.load()
+        st = _lib.stream_ptr(torch, stream)
+        c = self.cache
+        cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self._stage1(lib, st, main)
+        if self.final_overlap:
+            # after the scoring pass (it shares ws_qp) and the selection; layer l waits on done[l]
+            self.fin.wait_stream(main)
         if self.final_overlap:
             self._c_rc.layer_ready = c.c_cache.layer_ready
             _lib.check(lib.pkv_recompute(self.dm.handle, ctypes_ref(self._c_rc), self.idx.data_ptr(), self.k, None,

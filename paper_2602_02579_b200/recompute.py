@@ -19,7 +19,7 @@ import numpy as np
 
 from . import _lib
 from .chunkstore import assemble, mark_finalized
-from .errors import ArgumentError, ConfigError, InputError, StateError
+from .errors import ArgumentError, ConfigError, InputError, NumericsError, StateError
 from .model import FlopTally, KVCache, ModelConfig, bill_query_pass, bill_repair, resolve_device_model
 from .selection import (STRATEGIES, SelectionResult, ValueScores, check_tokens, run_query_pass,
                         score_cacheblend_l1, score_epic, score_kvshare_l1, score_prophet, score_random, select_top_p,
@@ -111,16 +111,25 @@ def _final_overlap(dm) -> bool:
 def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_attn: bool = False,
                    tally: FlopTally | None = None) -> FinalizeResult:
     """Compute the query over the (repaired) cache and append its K/V entries.
-    One-shot per cache (reference recompute.py:105-125)."""
+    One-shot per cache (reference recompute.py:105-125).  With capture_attn the result
+    carries the head-averaged attention rows [m, s+m] of every layer (model.py:386-398).
+    Raises NumericsError for a non-finite value in the Stage-II repair or the logits."""
     torch = _lib.require_cuda()
-    mark_finalized(cache)
     dm = resolve_device_model(weights, config)
     ids = check_tokens(query_tokens, config)
+    if capture_attn and getattr(dm, "tp_world", 1) > 1:
+        raise ConfigError("capture_attn is not supported on a head-sharded model")
+    mark_finalized(cache)
     m = int(ids.shape[0])
     if cache.access_log is not None:
         cache.access_log.extend(("read", li) for li in range(config.n_layers))
     L, Hkv, dk = config.n_layers, cache.config.n_kv_heads, config.head_dim
     flags = _lib.PKV_QP_LOGITS | _lib.PKV_QP_APPEND_KV | _lib.PKV_QP_FROM_CHUNKS
+    s = cache.context_length
+    rows_dev = None
+    if capture_attn:
+        flags |= _lib.PKV_QP_ROWS
+        rows_dev = torch.empty((L, m, s + m), dtype=torch.float32, device=cache.device)
     follow = getattr(cache, "_final_follow", None)
     cache._final_follow = None
     if follow is not None and cache.pool_tokens >= cache.context_length + m:
@@ -134,19 +143,26 @@ def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_at
             fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
             fv = torch.empty_like(fk)
             logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
-            run_query_pass(dm, cache, ids, flags, fresh_k=fk, fresh_v=fv, logits=logits, stream=side, c_cache=c_fin)
+            run_query_pass(dm, cache, ids, flags, per_layer=rows_dev, fresh_k=fk, fresh_v=fv, logits=logits,
+                           stream=side, c_cache=c_fin)
         main.wait_stream(side)
-        for t in (fk, fv, logits):
+        for t in (fk, fv, logits) + ((rows_dev,) if rows_dev is not None else ()):
             t.record_stream(main)
     else:
         fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
         fv = torch.empty_like(fk)
         logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
-        run_query_pass(dm, cache, ids, flags, fresh_k=fk, fresh_v=fv, logits=logits)
+        run_query_pass(dm, cache, ids, flags, per_layer=rows_dev, fresh_k=fk, fresh_v=fv, logits=logits)
     cache.query_kv = (fk, fv)
     bill_query_pass(tally, config, cache.context_length, m)
     first = logits.cpu().numpy()
-    s = cache.context_length
+    cache.check_finite()
+    if not np.isfinite(first).all():
+        raise NumericsError("non-finite values in the first-token logits")
+    rows = None
+    if rows_dev is not None:
+        ra = rows_dev.cpu().numpy()
+        rows = [np.ascontiguousarray(ra[li]) for li in range(L)]
 
     def keys():
         fkh = fk.cpu().numpy()
@@ -159,7 +175,7 @@ def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_at
     kv = KVCache(keys=keys, values=values, positions=np.arange(s + m, dtype=np.int64), last_logits=first)
     from .decode import DevicePools
     kv._device_pools = DevicePools.from_assembled(cache, s + m)  # decoding continues on the device
-    return FinalizeResult(cache=kv, first_logits=first, rows=None)
+    return FinalizeResult(cache=kv, first_logits=first, rows=rows)
 
 
 def selection_digest(indices) -> str:

@@ -163,6 +163,10 @@ def run_query_pass(dm, cache, ids: np.ndarray, flags: int, per_layer=None, fresh
     if c_cache is None:
         cache.ensure_query_room(m)
         c_cache = cache.c_cache
+        # this pass shares the 'qp' workspace with a final pass that would follow Stage II
+        # on its own stream: finalize_query then runs in order
+        if getattr(cache, "_final_follow", None) is not None:
+            cache._final_follow = None
     d_ids = torch.from_numpy(ids.astype(np.int32)).to(cache.device)
     lib = _lib.load()
     nbytes = lib.pkv_query_pass_workspace(dm.handle, cache.context_length, m, flags)
@@ -220,6 +224,7 @@ def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None, 
     torch = _lib.require_cuda()
     dm = resolve_device_model(weights, config)
     s, L = cache.context_length, config.n_layers
+    cache.wait_ready()  # a host-tier chunk transfer may still be filling the chunk buffers / pool
     Hkv, dk = cache.config.n_kv_heads, config.head_dim
     m = 32
     flags = _lib.PKV_QP_PROBE | _lib.PKV_QP_FROM_CHUNKS | (_lib.PKV_QP_SCORES if want_colsum else 0)
