@@ -386,6 +386,8 @@ struct QpWs {
   double* denom;
   double* rows64;  // tensor-parallel: per-(query, token) head-sum partials, all-reduced
   __half* q3;
+  float *sc_w, *sc_c, *sc_part;  // scoring pass 2
+  int sc_splits, sc_keys_per_split;
   ProjWs proj;
   int n_splits, keys_per_split, tc_splits, tc_keys_per_split;
 };
@@ -428,7 +430,18 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
   const int row_blocks = ceil_div(R, 128);
   (void)row_blocks;
   if (flags & (PKV_QP_SCORES | PKV_QP_ROWS)) {
-    w.S = cv.take<float>((size_t)Hkv * R * s_tot);
+    // the [Hkv][s][R] score matrix only for capture_attn rows, the SIMT path and the
+    // head-sharded renormalised scores; otherwise the second pass reduces p per key
+    const bool need_S = (flags & PKV_QP_ROWS) || w.tc_splits == 0 || ((flags & PKV_QP_RENORM) && md->tp_world > 1);
+    if (need_S) w.S = cv.take<float>((size_t)Hkv * R * s_tot);
+    if (w.tc_splits > 0 && s > 0) {
+      const int target = std::max(1, num_sms() / std::max(1, Hkv * row_blocks));
+      w.sc_keys_per_split = std::max(128, ceil_div(ceil_div(s, target), 128) * 128);
+      w.sc_splits = ceil_div(s, w.sc_keys_per_split);
+      w.sc_w = cv.take<float>((size_t)Hkv * R);
+      w.sc_c = cv.take<float>((size_t)Hkv * R);
+      w.sc_part = cv.take<float>((size_t)row_blocks * Hkv * s);
+    }
     w.rows = cv.take<float>((size_t)m * s);
     w.denom = cv.take<double>((size_t)m);
     if (md->tp_world > 1) w.rows64 = cv.take<double>((size_t)m * s);
@@ -554,6 +567,11 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     const bool scores = (flags & PKV_QP_SCORES) && per_layer;
     const bool capture = (flags & PKV_QP_ROWS) && per_layer;
     a.S = (scores || capture) ? w.S : nullptr;
+    a.sc_w = w.sc_w;
+    a.sc_c = w.sc_c;
+    a.sc_part = (scores && tc_splits > 0) ? w.sc_part : nullptr;
+    a.sc_splits = w.sc_splits;
+    a.sc_keys_per_split = w.sc_keys_per_split;
     // pipelined transfer: layer l of the cache may still be in flight
     if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);

@@ -69,6 +69,11 @@ struct S1Attn {
   const void* k2_all;
   const void* v_all;
   long pool_rows_total;
+  // scoring pass 2 (s1_score_tc_kernel) workspace; sc_part == null: score-matrix path
+  float* sc_w;     // [Hkv][R] row weights
+  float* sc_c;     // [Hkv][R] context mass of each row
+  float* sc_part;  // [RB][Hkv][s] column sums
+  int sc_splits, sc_keys_per_split;
 };
 
 // tensor-core narrow-pass attention over the context keys [0, s)
@@ -87,6 +92,22 @@ struct S1TcArgs {
 };
 int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
                       cudaStream_t st);
+
+// second pass of the scoring (K2b): QK^T recomputed exactly as the first pass forms it,
+// p = exp(S - M) * w with the final per-row max M and weight w = 1 / (L * H * m) (or the
+// context-renormalised weight), summed over the CTA's 128 rows per context key
+struct S1ScoreArgs {
+  const void* q3;         // the first pass's fp16 Q planes [Hkv][RB][3][128][DKP]
+  int Hkv, R, s, keys_per_split, n_splits;
+  float scale;
+  long kv_row0, pool_tokens;
+  const int32_t* page_table;
+  const float* Mfin;      // [Hkv][R]
+  const float* W;         // [Hkv][R] row weights
+  float* part;            // [RB][Hkv][s] per-row-block column sums
+};
+int s1_score_tc_launch(const S1ScoreArgs& a, const void* k1, const void* k2, long pool_rows_total, int dkp,
+                       cudaStream_t st);
 int s1_attention_launch(const S1Attn& a, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
                         float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st,
                         float* capture_rows = nullptr);

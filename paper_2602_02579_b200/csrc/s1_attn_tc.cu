@@ -368,4 +368,249 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
   return PKV_OK;
 }
 
+
+// ---------------------------------------------------------------------------------
+// Scoring pass 2 (reference selection.py:76-86 over model.py:294-307):
+// the context keys' scores without the [Hkv][s][R] fp32 score matrix.  Pass 1
+// (s1_attn_tc_kernel with S = null) leaves the final per-row max M and denominator L;
+// this kernel recomputes Q'K^T with the SAME five fp16 plane products (identical
+// accumulator), forms p = 2^(S log2e - M log2e) * w with w = 1 / (L H m) (or the
+// context-renormalised weight, s1_row_weights_kernel) and sums p over the CTA's 128 rows
+// = (G query heads x m queries) for every key of its split: a warp transposes-and-adds
+// its 32 x 32 block with 31 shuffles (lane c ends with column c), the four TMEM lane
+// quarters add through shared memory in a fixed order.  One f32 per (row block, KV
+// head, key) goes to HBM instead of 128.
+//
+// CTA = (key split, KV head g, row block); 128-key tiles = one cache page, 3-stage TMA
+// ring of the two key planes, S double-buffered in TMEM so the MMAs of page j+1 run
+// under the reduction of page j.
+//   warps 0-7  reduction: warp w owns lane quarter w%4 and columns [64*(w/4), +64)
+//   warp 8     TMA producer (Kh, Kl)       warp 9  TMEM owner + MMA issuer
+template <int DKP>
+struct S1ScCfg {
+  static constexpr int ATOMS = DKP / 64;
+  static constexpr int KT = 128;
+  static constexpr int PLANE = KT * DKP * 2;
+  static constexpr int ATOM_K = KT * 128;
+  static constexpr int STAGE = 2 * PLANE;
+  static constexpr int STAGES = DKP == 128 ? 3 : 6;
+  static constexpr int RED = 2 * 4 * KT * 4;  // double-buffered [4 quarters][KT] f32
+  static constexpr int SMEM = STAGES * STAGE + RED + 1024 + 256;
+  static constexpr int T_Q = 0, Q_PLANE = 64, T_S = 256;
+};
+
+// lane c returns sum over the warp's 32 lanes of v[c] (v is clobbered)
+__device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 16; k >= 1; k >>= 1) {
+    const bool up = (lane & k) != 0;
+#pragma unroll
+    for (int i = 0; i < k; ++i) {
+      const float send = up ? v[i] : v[i + k];
+      const float keep = up ? v[i + k] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+    }
+  }
+  return v[0];
+}
+
+template <int DKP>
+__global__ void __launch_bounds__(320, 1)
+    s1_score_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
+                       S1ScoreArgs a) {
+  using C = S1ScCfg<DKP>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  float* red = reinterpret_cast<float*>(sK + C::STAGES * C::STAGE);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red) + C::RED);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + C::STAGES;
+  uint64_t* s_full = bars + 2 * C::STAGES;  // [2]
+  uint64_t* s_free = s_full + 2;            // [2]
+  uint64_t* q_full = s_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.y, split = blockIdx.x, rb = blockIdx.z;
+  const int k_begin = split * a.keys_per_split;
+  const int k_end = min(k_begin + a.keys_per_split, a.s);
+  const int n_tiles = (k_end - k_begin + C::KT - 1) / C::KT;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_free[b], 8);
+    }
+    mbar_init(q_full, 8);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
+
+  if (warp == 8) {
+    if (elect_one()) {
+      tma_prefetch(&tK1);
+      tma_prefetch(&tK2);
+      const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int st = j % C::STAGES;
+        mbar_wait(&kv_empty[st], ((uint32_t)(j / C::STAGES) & 1) ^ 1);
+        const int t0 = k_begin + j * C::KT;  // page-aligned
+        const int row = (int)(head_row + (long)a.page_table[t0 >> 7] * 128);
+        uint8_t* base = sK + st * C::STAGE;
+        mbar_expect_tx(&kv_full[st], C::STAGE);
+#pragma unroll
+        for (int at = 0; at < C::ATOMS; ++at) {
+          tma_load_2d(base + at * C::ATOM_K, &tK1, &kv_full[st], at * 64, row);
+          tma_load_2d(base + C::PLANE + at * C::ATOM_K, &tK2, &kv_full[st], at * 64, row);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idesc = make_idesc_f16(128, C::KT);
+    constexpr int NPROD = 5;  // the first pass's products, same order
+    constexpr int PA[NPROD] = {0, 1, 2, 0, 1};
+    constexpr int PB[NPROD] = {0, 0, 0, 1, 1};
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j % C::STAGES, b = j & 1;
+      mbar_wait(&kv_full[st], (uint32_t)(j / C::STAGES) & 1);
+      if (j >= 2) mbar_wait(&s_free[b], (uint32_t)((j - 2) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t k_addr = smem_u32(sK + st * C::STAGE);
+        int n = 0;
+#pragma unroll
+        for (int pr = 0; pr < NPROD; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < DKP / 16; ++kk, ++n) {
+            const uint32_t ko = PB[pr] * C::PLANE + (kk >> 2) * C::ATOM_K + (kk & 3) * 32;
+            umma_ts(tmem + C::T_S + b * C::KT, tmem + C::T_Q + PA[pr] * C::Q_PLANE + kk * 8,
+                    sdesc_sw128(k_addr + ko, 16, 1024), idesc, n > 0 ? 1u : 0u);
+          }
+        umma_commit(&s_full[b]);
+        umma_commit(&kv_empty[st]);
+      }
+      __syncwarp();
+    }
+  } else {
+    constexpr float LOG2E = 1.4426950408889634f;
+    const int quarter = warp & 3, hc = warp >> 2;
+    const int r = quarter * 32 + lane;
+    const int row = rb * 128 + r;
+    const bool valid = row < a.R;
+    const uint32_t lb = (uint32_t)(quarter * 32) << 16;
+    {  // Q planes -> TMEM, as in the first pass
+      const __half* q3 = reinterpret_cast<const __half*>(a.q3);
+      if (hc * 32 < DKP / 2) {
+#pragma unroll 1
+        for (int x = 0; x < 3; ++x) {
+          const uint4* src = reinterpret_cast<const uint4*>(
+              q3 + ((((long)g * gridDim.z + rb) * 3 + x) * 128 + r) * DKP + hc * 64);
+          uint32_t u[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = src[c];
+            u[4 * c] = v.x; u[4 * c + 1] = v.y; u[4 * c + 2] = v.z; u[4 * c + 3] = v.w;
+          }
+          tmem_st32(tmem + lb + C::T_Q + x * C::Q_PLANE + hc * 32, u);
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+    }
+    const float mb = valid ? a.Mfin[(long)g * a.R + row] * LOG2E : 0.f;
+    const float wr = valid ? a.W[(long)g * a.R + row] : 0.f;
+    const float c1 = (a.scale * (1.f / S1_QSCALE)) * LOG2E;
+    float* out = a.part + ((long)rb * a.Hkv + g) * a.s;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (uint32_t)(j >> 1) & 1);
+      tc_fence_after();
+      uint32_t u0[32], u1[32];
+      tmem_ld32(tmem + lb + C::T_S + b * C::KT + hc * 64, u0);
+      tmem_ld32(tmem + lb + C::T_S + b * C::KT + hc * 64 + 32, u1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[b]);
+      const int key0 = k_begin + j * C::KT + hc * 64;
+      float* rq = red + (b * 4 + quarter) * C::KT + hc * 64;
+      {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          v[i] = (valid && key0 + i < k_end) ? ex2(fmaf(__uint_as_float(u0[i]), c1, -mb)) * wr : 0.f;
+        rq[lane] = warp_colsum32(v);
+      }
+      {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          v[i] = (valid && key0 + 32 + i < k_end) ? ex2(fmaf(__uint_as_float(u1[i]), c1, -mb)) * wr : 0.f;
+        rq[32 + lane] = warp_colsum32(v);
+      }
+      named_bar_sync(1, 256);
+      if (quarter == 0) {
+        const float* rr = red + b * 4 * C::KT + hc * 64;
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = h2 * 32 + lane;
+          const float sum = ((rr[c] + rr[C::KT + c]) + rr[2 * C::KT + c]) + rr[3 * C::KT + c];
+          if (key0 + c < k_end) out[key0 + c] = sum;
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int s1_score_tc_launch(const S1ScoreArgs& a, const void* k1, const void* k2, long pool_rows_total, int dkp,
+                       cudaStream_t st) {
+  if (a.n_splits <= 0) return PKV_OK;
+  if (a.keys_per_split % 128 != 0) return set_error(PKV_ERR_ARGUMENT, "score pass: split not page-aligned");
+  const int RB = ceil_div(a.R, 128);
+  dim3 grid(a.n_splits, a.Hkv, RB);
+  CUtensorMap m1, m2;
+  if (!cached_tmap(&m1, k1, pool_rows_total, dkp, dkp, 128) || !cached_tmap(&m2, k2, pool_rows_total, dkp, dkp, 128))
+    return set_error(PKV_ERR_CUDA, "score pass: TMA encode failed");
+  if (dkp == 128) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(s1_score_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1ScCfg<128>::SMEM);
+    });
+    launch_k(s1_score_tc_kernel<128>, grid, 320, S1ScCfg<128>::SMEM, st, m1, m2, a);
+  } else if (dkp == 64) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(s1_score_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, S1ScCfg<64>::SMEM);
+    });
+    launch_k(s1_score_tc_kernel<64>, grid, 320, S1ScCfg<64>::SMEM, st, m1, m2, a);
+  } else {
+    return set_error(PKV_ERR_CONFIG, "score pass: padded head dim %d unsupported", dkp);
+  }
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("s1_score_tc_kernel");
+  return PKV_OK;
+}
+
 }  // namespace pkv

@@ -642,28 +642,35 @@ __global__ void __launch_bounds__(256) s1_attn_pass1(S1Attn a) {
 
 // combine split partials -> attention output [m][H][dkp] fp32 and the final
 // per-row (max, denominator) used by the scoring reduction
+// Cfin (nullable): the row's probability mass on the context keys (splits [0, n_ctx)),
+// for the context-renormalised scores
 __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const float* Lpart, int splits, int Hkv,
                                 int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin,
-                                __half* x3, long ldx) {
+                                __half* x3, long ldx, int n_ctx, float* Cfin) {
   pdl_entry();
   extern __shared__ float wsp[];  // [splits] rescale weight of each split
-  __shared__ float sM, sL;
+  __shared__ float sM, sL, sC;
   const int r = blockIdx.x, g = blockIdx.y;
   if (threadIdx.x < 32) {
     float M = -INFINITY;
     for (int sp = threadIdx.x; sp < splits; sp += 32) M = fmaxf(M, Mpart[((long)sp * Hkv + g) * R + r]);
     for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float L = 0.f;
+    float L = 0.f, Lc = 0.f;
     for (int sp = threadIdx.x; sp < splits; sp += 32) {
       const long b = ((long)sp * Hkv + g) * R + r;
       const float w = Mpart[b] != -INFINITY ? expf(Mpart[b] - M) : 0.f;
       wsp[sp] = w;
       L += Lpart[b] * w;
+      if (sp < n_ctx) Lc += Lpart[b] * w;
     }
-    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      L += __shfl_xor_sync(0xffffffffu, L, o);
+      Lc += __shfl_xor_sync(0xffffffffu, Lc, o);
+    }
     if (threadIdx.x == 0) {
       sM = M;
       sL = L;
+      sC = Lc / L;
     }
   }
   __syncthreads();
@@ -693,6 +700,7 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
   if (threadIdx.x == 0 && Mfin != nullptr) {
     Mfin[(long)g * R + r] = M;
     Lfin[(long)g * R + r] = L;
+    if (Cfin != nullptr) Cfin[(long)g * R + r] = sC;
   }
 }
 
@@ -953,6 +961,45 @@ __global__ void s1_query_mean_kernel(const float* rows, const double* denom, int
   out[t] = (float)(acc / (double)m);
 }
 
+// row weights of the second scoring pass: w = 1 / (L * H * m), divided by the query's
+// context-only denominator when renormalising (selection.py:80-84: denom_i = sum over the
+// context of the head-mean row = (1/H) sum_h C_{h,i}, C = the row's context mass)
+__global__ void s1_row_weights_kernel(const float* Lfin, const float* Cfin, int Hkv, int G, int R, int m, int H_total,
+                                      float* W) {
+  pdl_entry();
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Hkv * R) return;
+  const int r = idx % R;
+  double w = 1.0 / ((double)Lfin[idx] * (double)H_total * (double)m);
+  if (Cfin != nullptr) {
+    const int i = r % m;
+    double d = 0.0;
+    for (int g = 0; g < Hkv; ++g)
+      for (int j = 0; j < G; ++j) d += (double)Cfin[(long)g * R + j * m + i];
+    d /= (double)H_total;
+    w /= (d > 1e-30 ? d : 1e-30);
+  }
+  W[idx] = (float)w;
+}
+
+// per_layer[t] = f32( sum over (row block, KV head) of the pass-2 column sums ), fixed
+// order in f64;  MODE 1: the f64 sums of this rank's heads (summed over ranks, then
+// rounded by s1_f64_to_f32_kernel)
+template <int MODE>
+__global__ void s1_colsum_finish(const float* __restrict__ part, int nparts, int s, float* out, double* out64) {
+  pdl_entry();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= s) return;
+  double acc = 0.0;
+  for (int p = 0; p < nparts; ++p) acc += (double)__ldg(part + (long)p * s + t);
+  if (MODE == 0) out[t] = (float)acc;
+  else out64[t] = acc;
+}
+__global__ void s1_f64_to_f32_kernel(const double* x, int n, float* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = (float)x[t];
+}
+
 int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float* Lfin, float* rows, double* denom,
                         float* per_layer, int renorm, int H_total, double* rows64, pkv_comm* comm, cudaStream_t st,
                         float* capture_rows) {
@@ -961,6 +1008,10 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   int total_splits = a.n_splits;
   const size_t fresh_smem = (a.tc_splits + a.m + (size_t)a.m * a.dkp) * sizeof(float);
   bool combined = false;
+  // scores by the second pass over the keys (no score matrix) unless the rows themselves
+  // are wanted (capture_attn) or the renormalised scores need other ranks' heads
+  const bool pass2 = a.tc_splits > 0 && per_layer != nullptr && capture_rows == nullptr && a.s > 0 &&
+                     a.sc_part != nullptr && !(renorm && comm_world(comm) > 1);
   if (a.tc_splits > 0) {
     // context keys [0, s) on the tensor cores (fp16 planes, fp32-faithful)
     S1TcArgs t{};
@@ -980,7 +1031,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
     t.pool_tokens = a.pool_tokens;
     t.page_table = a.page_table;
-    t.S = a.S;
+    t.S = pass2 ? nullptr : a.S;
     t.Opart = a.Opart;
     t.Mpart = a.Mpart;
     t.Lpart = a.Lpart;
@@ -989,7 +1040,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     // fused fresh keys + combine: measured neutral (each CTA re-reads the head's fresh V),
     // so opt-in (PKV_FRESH_FUSED=1)
     static const bool fused_fresh = getenv("PKV_FRESH_FUSED") && getenv("PKV_FRESH_FUSED")[0] == '1';
-    if (fused_fresh && fresh_smem <= 160 * 1024) {
+    if (fused_fresh && fresh_smem <= 160 * 1024 && !(pass2 && renorm)) {
       // the m fresh query keys are merged inside the combine (one kernel instead of a
       // SIMT split + combine)
       static std::once_flag once_fresh;
@@ -1039,10 +1090,54 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_CHECK_LAUNCH("s1_attn_pass1");
   launch_k(s1_attn_combine, dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st, a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin,
-                                                    reinterpret_cast<__half*>(a.x3_out), a.x3_ld);
+                                                    reinterpret_cast<__half*>(a.x3_out), a.x3_ld, a.tc_splits,
+                                                    (pass2 && renorm) ? a.sc_c : (float*)nullptr);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_combine");
   }
+  if (pass2) {
+    const int nrw = a.Hkv * a.R;
+    launch_k(s1_row_weights_kernel, ceil_div(nrw, 128), 128, 0, st, (const float*)Lfin,
+             renorm ? (const float*)a.sc_c : (const float*)nullptr, a.Hkv, a.G, a.R, a.m, H_total, a.sc_w);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("s1_row_weights_kernel");
+    S1ScoreArgs sa{};
+    sa.q3 = a.q3;
+    sa.Hkv = a.Hkv;
+    sa.R = a.R;
+    sa.s = a.s;
+    sa.keys_per_split = a.sc_keys_per_split;
+    sa.n_splits = a.sc_splits;
+    sa.scale = a.scale;
+    sa.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
+    sa.pool_tokens = a.pool_tokens;
+    sa.page_table = a.page_table;
+    sa.Mfin = Mfin;
+    sa.W = a.sc_w;
+    sa.part = a.sc_part;
+    int rc = s1_score_tc_launch(sa, a.k1_all, a.k2_all, a.pool_rows_total, a.dkp, st);
+    if (rc) return rc;
+    const int nparts = row_blocks * a.Hkv;
+    if (comm_world(comm) > 1) {
+      launch_k(s1_colsum_finish<1>, ceil_div(a.s, 256), 256, 0, st, (const float*)a.sc_part, nparts, a.s,
+               (float*)nullptr, rows64);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_colsum_finish");
+      rc = comm_allreduce(comm, rows64, (size_t)a.s, PKV_DT_F64, st);
+      if (rc) return rc;
+      launch_k(s1_f64_to_f32_kernel, ceil_div(a.s, 256), 256, 0, st, (const double*)rows64, a.s, per_layer);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_f64_to_f32_kernel");
+    } else {
+      launch_k(s1_colsum_finish<0>, ceil_div(a.s, 256), 256, 0, st, (const float*)a.sc_part, nparts, a.s, per_layer,
+               (double*)nullptr);
+      PKV_LAUNCHED();
+      PKV_CHECK_LAUNCH("s1_colsum_finish");
+    }
+    return PKV_OK;
+  }
+  if (a.S == nullptr && (capture_rows != nullptr || per_layer != nullptr) && a.s > 0)
+    return set_error(PKV_ERR_ARGUMENT, "narrow pass: the score path needs the score workspace");
   if (a.S != nullptr && capture_rows != nullptr) {  // capture_attn: head-mean rows [m][s + m]
     const long ld = a.s + a.m;
     if (comm_world(comm) > 1) return set_error(PKV_ERR_CONFIG, "capture_attn is not supported head-sharded");

@@ -136,6 +136,27 @@ class ModelWeights:
                     (f"{p}.ffn.w_gate", lw.w_gate), (f"{p}.ffn.w_up", lw.w_up), (f"{p}.ffn.w_down", lw.w_down)]
         return out + [("final_norm.gain", self.final_norm), ("lm_head.weight", self.lm_head)]
 
+    @classmethod
+    def from_named(cls, config: ModelConfig, tensors: dict) -> "ModelWeights":
+        """Inverse of named_tensors (reference model.py:124-145): missing name -> ConfigError,
+        tensors taken as contiguous f32, the result validated against the config."""
+        def take(name):
+            if name not in tensors:
+                raise ConfigError(f"missing tensor {name!r}")
+            return np.ascontiguousarray(tensors[name], dtype=F32)
+
+        layers = []
+        for i in range(config.n_layers):
+            p = f"layers.{i}"
+            layers.append(LayerWeights(
+                attn_norm=take(f"{p}.attn_norm.gain"), wq=take(f"{p}.attn.wq"), wk=take(f"{p}.attn.wk"),
+                wv=take(f"{p}.attn.wv"), wo=take(f"{p}.attn.wo"), ffn_norm=take(f"{p}.ffn_norm.gain"),
+                w_gate=take(f"{p}.ffn.w_gate"), w_up=take(f"{p}.ffn.w_up"), w_down=take(f"{p}.ffn.w_down")))
+        w = cls(embed=take("embed.weight"), layers=layers, final_norm=take("final_norm.gain"),
+                lm_head=take("lm_head.weight"))
+        w.validate(config)
+        return w
+
     def fingerprint(self, config: ModelConfig) -> str:
         """blake2b-8 of config JSON + weight bytes (reference model.py:147-160)."""
         if self._fingerprint is None:

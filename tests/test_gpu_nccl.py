@@ -1,0 +1,71 @@
+"""The NCCL back end of the head-sharded prefill, one process per GPU.
+
+Runs only where >= 2 GPUs are visible (this pool's boxes have one; the in-process
+communicator in test_gpu_tp.py covers the sharded math there).  `bench.py --gpus 2`
+starts two ranks itself (torchrun), shards the KV heads over NCCL and checks its own
+request against the CPU oracle fixture in-run; here the line must report two GPUs,
+tensor parallelism, and a selection identical to the oracle's.
+"""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = pytest.mark.gpu
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs (NCCL over NVLink)")
+def test_bench_two_ranks_nccl():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "1",
+                          "--e2e-steps", "0", "--full-steps", "0", "--p-sweep", "", "--no-cpu-baseline"],
+                         capture_output=True, text=True, timeout=1800, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-4000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["config"]["parallelism"].startswith("tp2")
+    assert line["scaling"] == "strong"
+    if "parity" in line:
+        assert line["parity"]["sel_ok"] and line["parity"]["pass"], line["parity"]
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs (NCCL over NVLink)")
+def test_nccl_allreduce_two_processes(tmp_path):
+    """pkv_comm over NCCL: an f64 and an f32 in-place sum across two processes."""
+    script = r'''
+import os, sys, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["PKV_ROOT"])
+import __graft_entry__; __graft_entry__.build()
+from paper_2602_02579_b200 import tp
+r = int(os.environ["RANK"]); torch.cuda.set_device(r)
+dist.init_process_group("nccl", device_id=torch.device("cuda", r))
+c = tp.nccl_comm()
+for dt in (torch.float64, torch.float32):
+    x = torch.arange(1000, dtype=dt, device="cuda") * (r + 1)
+    c.allreduce_(x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, torch.arange(1000, dtype=dt, device="cuda") * 3), dt
+c.close()
+dist.destroy_process_group()
+print("ok", r)
+'''
+    import os
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, PKV_ROOT=str(ROOT))
+    path = tmp_path / "nccl_rank.py"
+    path.write_text(script)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), str(path)],
+                         capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0 and out.stdout.count("ok") == 2, out.stderr[-4000:]

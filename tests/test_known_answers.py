@@ -95,6 +95,14 @@ def test_drop_in_host_types_match_oracle():
     for (na, a), (nb, b) in zip(w.named_tensors(), wo.tensors()):
         assert na == nb and np.array_equal(a, b)
     assert w.fingerprint(cfg) == wo.fingerprint(cfg_o)
+    # from_named round trip (reference model.py:124-145)
+    named = dict(w.named_tensors())
+    w2 = P.ModelWeights.from_named(cfg, named)
+    assert w2.fingerprint(cfg) == w.fingerprint(cfg)
+    with pytest.raises(P.ConfigError):
+        P.ModelWeights.from_named(cfg, {k: v for k, v in named.items() if k != "layers.1.attn.wv"})
+    with pytest.raises(P.ConfigError):
+        P.ModelWeights.from_named(cfg, {**named, "lm_head.weight": named["lm_head.weight"][:, :7]})
     with pytest.raises(P.ConfigError):
         P.ModelConfig(n_layers=1, n_heads=3, n_kv_heads=2, head_dim=4, hidden_dim=12, ffn_dim=8, vocab_size=5)
     with pytest.raises(P.ConfigError):
