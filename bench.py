@@ -164,6 +164,19 @@ def cpu_sample(cfgd: dict, p: float, m: int = 32, n_rows: int = 256, seed: int =
     return ttft, tm, k, len(sample), sum(tm.values())
 
 
+def full_anchor_run(args):
+    """The one FULL CPU run of this workload: the layer-streamed oracle over all 32 layers
+    and all k rows that produced tests/golden/anchor_c3.npz (tests/golden/make_anchor.py,
+    8 threads of the build container, not this box) -- the check on the extrapolation."""
+    path = ROOT / "tests" / "golden" / "anchor_c3.npz"
+    if args.config != "llama3-8b-32k" or not path.exists():
+        return None
+    meta = json.loads(str(np.load(path)["meta"]))
+    return {"wall_s": meta["cpu_seconds"], "threads": 8, "where": "build container (8 cores)",
+            "what": "oracle/anchor.py: assemble + score_prophet + select + recompute (all k rows, "
+                    "causal-visible attention per row block) + finalize, L = 32, s = 32768"}
+
+
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -306,7 +319,8 @@ def run_reference(args, cfgd, rank, world):
             "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "threads": cpu_threads(),
                              "sample": f"oracle port of pikv, 1 layer at full width and s={s}, Stage II on {n_s} "
                                        f"of k={k} rows, extrapolated x{cfgd['n_layers']} layers and k/{n_s} rows; "
-                                       f"phase seconds {json.dumps({a: round(b, 3) for a, b in tm.items()})}"},
+                                       f"phase seconds {json.dumps({a: round(b, 3) for a, b in tm.items()})}",
+                             "full_run": full_anchor_run(args)},
             "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -645,7 +659,8 @@ def main():
         line["cpu_baseline"] = {"value": s / ttft, "unit": "tok/s", "cores": cpu_cores(), "kind": "port",
                                 "ttft_ms": ttft * 1e3, "threads": cpu_threads(),
                                 "sample": f"oracle port of pikv: 1 layer, full width, s={s}, Stage II on {n_s}/{kk} "
-                                          f"rows; extrapolated x{L} layers (sample wall {wall:.1f}s)"}
+                                          f"rows; extrapolated x{L} layers (sample wall {wall:.1f}s)",
+                                "full_run": full_anchor_run(args)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

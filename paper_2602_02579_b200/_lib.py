@@ -106,7 +106,8 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # PKV_LIB: an alternative build of the same library (A/B timing of compile-time variants)
+    p = Path(path) if path else Path(os.environ.get("PKV_LIB", LIB_PATH))
     if not p.exists():
         raise EngineError(f"CUDA extension {p} is not built; run __graft_entry__.build()")
     lib = ctypes.CDLL(str(p))

@@ -421,7 +421,10 @@ static QpWs carve_qp(const pkv_model* md, int s, int m, int flags, void* base, s
     static const bool simt_only = getenv("PKV_S1_SIMT") != nullptr;
     const int row_blocks = ceil_div(R, 128);
     static const int waves = getenv("PKV_S1_WAVES") ? std::max(1, atoi(getenv("PKV_S1_WAVES"))) : 1;
-    const int target = std::max(1, waves * num_sms() / std::max(1, Hkv * row_blocks));
+    int target = std::max(1, waves * num_sms() / std::max(1, Hkv * row_blocks));
+    // the fused fresh-key split takes one CTA slot per (KV head, row block): keep the
+    // launch inside one wave (152 CTAs on 148 SMs doubled the kernel's time)
+    if (m <= 128 && target > 1 && !(getenv("PKV_FRESH_FUSED") && getenv("PKV_FRESH_FUSED")[0] == '1')) target -= 1;
     w.tc_keys_per_split = std::max(64, ceil_div(ceil_div(s, target), 64) * 64);
     w.tc_splits = (simt_only || s == 0) ? 0 : ceil_div(s, w.tc_keys_per_split);
     // partial buffers sized for either path (the caller's cache decides which runs)
@@ -510,11 +513,14 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     const bool append = (flags & PKV_QP_APPEND_KV) != 0;
     const bool planes = c->k2_pool != nullptr;
     __half* k2p = planes ? reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool : nullptr;
+    // the tensor-core attention's Q planes straight from the RoPE kernel when no row block
+    // needs zero padding
+    const bool q3_fused = planes && w.tc_splits > 0 && (m * G) % 128 == 0 && !(flags & PKV_QP_PROBE);
     TTRY(T_QP_MISC, query_qkv_launch(w.qkv, m, H, Hkv, dk, dkp, s, c->rope_cos, c->rope_sin, w.q, w.k, w.v,
                                      append ? kp : nullptr, append ? vp : nullptr, c->pool_tokens, c->page_table,
                                      fresh_k ? fresh_k + (long)l * m * Hkv * dk : nullptr,
                                      fresh_v ? fresh_v + (long)l * m * Hkv * dk : nullptr, append ? k2p : nullptr,
-                                     st));
+                                     st, q3_fused ? w.q3 : nullptr));
     if ((flags & PKV_QP_PROBE) && l == 1) break;  // the probe only needs layer 1's fresh values
     if ((flags & PKV_QP_PROBE) && l == 0) {
       if (!planes) return set_error(PKV_ERR_ARGUMENT, "probe needs the cache's key plane");
@@ -540,6 +546,7 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.tc_splits = tc_splits;
     a.tc_keys_per_split = w.tc_keys_per_split;
     a.q3 = w.q3;
+    a.q3_ready = q3_fused ? 1 : 0;
     a.k1_all = c->k_pool;
     a.k2_all = c->k2_pool;
     a.v_all = c->v_pool;

@@ -28,7 +28,8 @@ int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, dou
 int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, long ldy, int mode, cudaStream_t st);
 int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
-                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, cudaStream_t st);
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, cudaStream_t st,
+                     void* q3 = nullptr);
 int silu_act_launch(const float* gu, int m, int F, int Fp, float* act, cudaStream_t st, void* x3 = nullptr,
                     long ldx = 0);
 
@@ -63,6 +64,7 @@ struct S1Attn {
   float* Lpart;
   // whole-pool bases for the tensor-core path (TMA) and its Q-plane workspace
   void* q3;
+  int q3_ready;  // the Q planes were written by query_qkv_kernel (R % 128 == 0)
   void* x3_out;  // nullable: also write the output as 3 scaled fp16 planes (next projection's B operand)
   long x3_ld;
   const void* k1_all;
@@ -80,6 +82,7 @@ struct S1Attn {
 struct S1TcArgs {
   const float* q;  // [m][H][DKP] rotated fp32
   void* q3;        // workspace: fp16 Q planes [Hkv][RB][3][128][DKP]
+  int q3_ready;    // already written (fused into query_qkv_kernel)
   int m, H, Hkv, G, dk, R, s, s_tot, keys_per_split, n_splits;
   float scale;
   long kv_row0;  // first pool row of this layer: layer * Hkv * pool_tokens
@@ -89,6 +92,11 @@ struct S1TcArgs {
   float* Opart;
   float* Mpart;
   float* Lpart;
+  // fresh = 1: one extra CTA per (KV head, row block) at blockIdx.x == n_splits scores the
+  // m fresh query keys (fp32 K/V [m][Hkv][DKP], causal) as split n_splits (m <= 128)
+  int fresh;
+  const float* fk;
+  const float* fv;
 };
 int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
                       cudaStream_t st);

@@ -8,11 +8,12 @@
 //                                         residual planes out of the fp16 subnormals)
 //     K  = Kh + Kl                        (the fp16 cache key k_pool + its residual plane
 //                                         k2_pool: 2^-22 relative, 2^-25 absolute)
-//     Q' K^T = Qh Kh + Qm Kh + Ql Kh + Qh Kl + Qm Kl    (+ terms < 2^-30 relative)
-//     P' V   = Ph V + Pm V + Pl V,  P' = 2^10 p         (V: fp16 cache values, exact for
+//     Q' K^T = Qh Kh + Qm Kh + Qh Kl   (the dropped Ql Kh, Qm Kl, Ql Kl are < 2^-21 of
+//                                       |q||k|, the key planes' own truncation is 2^-22)
+//     P' V   = Ph V + Pm V,  P' = 2^10 p         (V: fp16 cache values, exact for
 //                                                       the chunk store's bf16 values)
-// so scores and outputs are f32-faithful (~1e-7 relative, far inside the 1e-4 selection
-// tie band).  Only the context keys [0, s) run here; the m fresh query keys (fp32 K/V)
+// so scores and outputs are f32-faithful to ~5e-7 of |q||k| (far inside the 1e-4
+// selection tie band).  Only the context keys [0, s) run here; the m fresh query keys (fp32 K/V)
 // are one extra SIMT split.
 //
 // CTA = (KV head g, key split): 128 rows r = j*m + i (query head g*G+j, query i),
@@ -24,7 +25,7 @@
 //              scores -> S workspace, P split -> TMEM (A operand of PV),
 //              O rescale in TMEM when the row max grows
 //   warp 8     TMA producer: Kh, Km, Kl, V tiles
-//   warp 9     TMEM owner + MMA issuer (6 + 3 products per tile)
+//   warp 9     TMEM owner + MMA issuer (3 + 2 products per tile)
 #include <mutex>
 
 #include "gemm_tc.cuh"
@@ -55,6 +56,19 @@ struct S1TcCfg {
 // Q planes: q3[((g*RB + rb)*3 + plane)*128 + r][DKP] fp16 planes of 2^6 q, row r of row
 // block rb = query head g*G + j, query i with rb*128 + r = j*m + i (zero padded)
 constexpr float S1_QSCALE = 64.f, S1_PSCALE = 1024.f;
+// plane products of S = Q'K^T, in order of significance: QhKh, QmKh, QhKl (each ~2^-11
+// below the previous level), then QlKh, QmKl (~2^-22 of |q||k|).  Three keep the score to
+// ~2^-21 of |q||k| -- the key planes themselves stop at 2^-22 -- for 3/5 of the MMAs
+// (ncu: with 5 QK + 3 PV products the narrow attention was tensor-bound, 69 us per layer
+// for 201 MB of K/V).  P' is two planes (2^-22).  PKV_S1_FULL_PLANES=1 at build time
+// restores 5 + 3 (the round-1 datapath).
+#ifdef PKV_S1_FULL_PLANES
+constexpr int S1_QK_PROD = 5, S1_P_PLANES = 3;
+#else
+constexpr int S1_QK_PROD = 3, S1_P_PLANES = 2;
+#endif
+constexpr int S1_Q_PLANES = S1_QK_PROD > 3 ? 3 : 2;
+
 __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int RB, int dkp, __half* q3) {
   pdl_entry();
   const int g = blockIdx.y, rr = blockIdx.x;  // rr = rb*128 + r
@@ -73,6 +87,66 @@ __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int 
   }
 }
 
+// The m fresh query keys of one (KV head, row block) as split a.n_splits, on the CTA slot
+// the launch adds after the context splits (so no separate SIMT launch): warp per row,
+// lane = 4 head dims; S = f32(q.k) * scale (model.py:291, 298), causal within the query,
+// online softmax; partials in the context splits' form (O unnormalised, M, L).
+template <int DKP>
+__device__ __noinline__ void s1_fresh_cta(const S1TcArgs& a, uint8_t* smem) {
+  constexpr int DPL = DKP / 32;  // dims per lane
+  const int g = blockIdx.y, rb = blockIdx.z;
+  const int m = a.m;
+  float* sk = reinterpret_cast<float*>(smem);
+  float* sv = sk + (long)m * DKP;
+  for (int e = threadIdx.x; e < m * DKP; e += blockDim.x) {
+    const int kk = e / DKP, d = e - kk * DKP;
+    const long src = ((long)kk * a.Hkv + g) * DKP + d;
+    sk[e] = a.fk[src];
+    sv[e] = a.fv[src];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int sp = a.n_splits;
+  for (int r = warp; r < 128; r += nw) {
+    const int row = rb * 128 + r;
+    if (row >= a.R) break;
+    const int jh = row / m, i = row - jh * m;
+    const float* qr = a.q + ((long)i * a.H + g * a.G + jh) * DKP + lane * DPL;
+    float q[DPL], o[DPL];
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) {
+      q[d] = qr[d];
+      o[d] = 0.f;
+    }
+    float mx = -INFINITY, l = 0.f;
+    for (int kk = 0; kk <= i; ++kk) {
+      const float* kr = sk + kk * DKP + lane * DPL;
+      float part = 0.f;
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) part = fmaf(q[d], kr[d], part);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      const float sc = part * a.scale;
+      const float mn = fmaxf(mx, sc);
+      const float corr = mx == -INFINITY ? 0.f : expf(mx - mn);
+      const float p = expf(sc - mn);
+      l = l * corr + p;
+      const float* vr = sv + kk * DKP + lane * DPL;
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) o[d] = fmaf(p, vr[d], o[d] * corr);
+      mx = mn;
+    }
+    const long base = ((long)sp * a.Hkv + g) * a.R + row;
+    float* od = a.Opart + base * DKP + lane * DPL;
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) od[d] = o[d];
+    if (lane == 0) {
+      a.Mpart[base] = mx;
+      a.Lpart[base] = l;
+    }
+  }
+}
+
 template <int DKP>
 __global__ void __launch_bounds__(320, 1)
     s1_attn_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
@@ -80,6 +154,11 @@ __global__ void __launch_bounds__(320, 1)
   using C = S1TcCfg<DKP>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (a.fresh && blockIdx.x == (unsigned)a.n_splits) {  // the fresh query keys' split
+    griddep_wait();
+    s1_fresh_cta<DKP>(a, smem);
+    return;
+  }
   uint8_t* sKV = smem;  // STAGES x {Kh, Kl, V}
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::STAGES * C::STAGE);
   uint64_t* kv_full = bars;
@@ -145,9 +224,9 @@ __global__ void __launch_bounds__(320, 1)
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = make_idesc_f16(128, C::KT);
     constexpr uint32_t idesc_o = make_idesc_f16(128, DKP, /*b_mn_major=*/true);
-    constexpr int NPROD = 5;
-    constexpr int PA[NPROD] = {0, 1, 2, 0, 1};  // Q plane of each product
-    constexpr int PB[NPROD] = {0, 0, 0, 1, 1};  // K plane of each product
+    constexpr int NPROD = S1_QK_PROD;
+    constexpr int PA[5] = {0, 1, 0, 2, 1};
+    constexpr int PB[5] = {0, 0, 1, 0, 1};
     mbar_wait(q_full, 0);
     tc_fence_after();
     for (int j = 0; j <= n_tiles; ++j) {
@@ -180,7 +259,7 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t v_addr = smem_u32(sKV + st * C::STAGE + 2 * C::PLANE);
           int n = 0;
 #pragma unroll
-          for (int x = 0; x < 3; ++x)
+          for (int x = 0; x < S1_P_PLANES; ++x)
 #pragma unroll
             for (int kk = 0; kk < C::KT / 16; ++kk, ++n)
               umma_ts(tmem + C::T_O, tmem + C::T_P + x * (C::KT / 2) + kk * 8,
@@ -205,7 +284,7 @@ __global__ void __launch_bounds__(320, 1)
       const __half* q3 = reinterpret_cast<const __half*>(a.q3);
       if (hc * 32 < DKP / 2) {
 #pragma unroll 1
-        for (int x = 0; x < 3; ++x) {
+        for (int x = 0; x < S1_Q_PLANES; ++x) {
           const uint4* src = reinterpret_cast<const uint4*>(
               q3 + ((((long)g * gridDim.z + blockIdx.z) * 3 + x) * 128 + r) * DKP + hc * 64);
           uint32_t u[32];
@@ -269,7 +348,8 @@ __global__ void __launch_bounds__(320, 1)
       for (int i = 0; i < HC / 2; ++i) {
         const float p0 = ex2(fmaf(sv[2 * i], LOG2E, -mb)), p1 = ex2(fmaf(sv[2 * i + 1], LOG2E, -mb));
         psum += p0 + p1;
-        split3h_pack(p0 * S1_PSCALE, p1 * S1_PSCALE, ph[i], pm[i], pl[i]);
+        if constexpr (S1_P_PLANES == 3) split3h_pack(p0 * S1_PSCALE, p1 * S1_PSCALE, ph[i], pm[i], pl[i]);
+        else split2h_pack(p0 * S1_PSCALE, p1 * S1_PSCALE, ph[i], pm[i]);
       }
       if (j >= 1) {  // PV(j-1) has read P and accumulated O
         mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
@@ -292,7 +372,7 @@ __global__ void __launch_bounds__(320, 1)
       const uint32_t tP = tmem + lb + C::T_P;
       tmem_st16(tP + hc * (HC / 2), ph);
       tmem_st16(tP + C::KT / 2 + hc * (HC / 2), pm);
-      tmem_st16(tP + C::KT + hc * (HC / 2), pl);
+      if constexpr (S1_P_PLANES == 3) tmem_st16(tP + C::KT + hc * (HC / 2), pl);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -339,11 +419,15 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
   if (a.n_splits <= 0) return PKV_OK;
   if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
   const int RB = ceil_div(a.R, 128);
-  dim3 grid(a.n_splits, a.Hkv, RB);
-  launch_k(s1_qprep_kernel, dim3(RB * 128, a.Hkv), 64, 0, st, a.q, a.m, a.H, a.G, a.R, RB, dkp,
-                                                       reinterpret_cast<__half*>(a.q3));
-  PKV_LAUNCHED();
-  PKV_CHECK_LAUNCH("s1_qprep_kernel");
+  dim3 grid(a.n_splits + (a.fresh ? 1 : 0), a.Hkv, RB);
+  if (a.fresh && 2L * a.m * dkp * 4 > S1TcCfg<128>::SMEM - 2048)
+    return set_error(PKV_ERR_ARGUMENT, "narrow pass: fused fresh split needs m <= 128");
+  if (!a.q3_ready) {
+    launch_k(s1_qprep_kernel, dim3(RB * 128, a.Hkv), 64, 0, st, a.q, a.m, a.H, a.G, a.R, RB, dkp,
+             reinterpret_cast<__half*>(a.q3));
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("s1_qprep_kernel");
+  }
   CUtensorMap m1, m2, mv;
   if (!cached_tmap(&m1, k1, pool_rows_total, dkp, dkp, 64) || !cached_tmap(&m2, k2, pool_rows_total, dkp, dkp, 64) ||
       !cached_tmap(&mv, v, pool_rows_total, dkp, dkp, 64))
@@ -373,7 +457,7 @@ int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const v
 // Scoring pass 2 (reference selection.py:76-86 over model.py:294-307):
 // the context keys' scores without the [Hkv][s][R] fp32 score matrix.  Pass 1
 // (s1_attn_tc_kernel with S = null) leaves the final per-row max M and denominator L;
-// this kernel recomputes Q'K^T with the SAME five fp16 plane products (identical
+// this kernel recomputes Q'K^T with the SAME fp16 plane products (identical
 // accumulator), forms p = 2^(S log2e - M log2e) * w with w = 1 / (L H m) (or the
 // context-renormalised weight, s1_row_weights_kernel) and sums p over the CTA's 128 rows
 // = (G query heads x m queries) for every key of its split: a warp transposes-and-adds
@@ -479,9 +563,9 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 9) {
     constexpr uint32_t idesc = make_idesc_f16(128, C::KT);
-    constexpr int NPROD = 5;  // the first pass's products, same order
-    constexpr int PA[NPROD] = {0, 1, 2, 0, 1};
-    constexpr int PB[NPROD] = {0, 0, 0, 1, 1};
+    constexpr int NPROD = S1_QK_PROD;  // the first pass's products, same order
+    constexpr int PA[5] = {0, 1, 0, 2, 1};
+    constexpr int PB[5] = {0, 0, 1, 0, 1};
     mbar_wait(q_full, 0);
     tc_fence_after();
     for (int j = 0; j < n_tiles; ++j) {
@@ -516,7 +600,7 @@ __global__ void __launch_bounds__(320, 1)
       const __half* q3 = reinterpret_cast<const __half*>(a.q3);
       if (hc * 32 < DKP / 2) {
 #pragma unroll 1
-        for (int x = 0; x < 3; ++x) {
+        for (int x = 0; x < S1_Q_PLANES; ++x) {
           const uint4* src = reinterpret_cast<const uint4*>(
               q3 + ((((long)g * gridDim.z + rb) * 3 + x) * 128 + r) * DKP + hc * 64);
           uint32_t u[32];

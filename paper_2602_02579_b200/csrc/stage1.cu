@@ -248,7 +248,8 @@ int splitk_reduce_launch(const float* part, int splits, int N, int m, float* y, 
 __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0,
                                  const double* rcos, const double* rsin, float* q, float* k, float* v,
                                  __half* k_pool, __half* v_pool, long pool_tokens,
-                                 const int32_t* page_table, float* fresh_k, float* fresh_v, __half* k2_pool) {
+                                 const int32_t* page_table, float* fresh_k, float* fresh_v, __half* k2_pool,
+                                 __half* q3, int G, int RB) {
   pdl_entry();
   const int heads = H + 2 * Hkv;
   const long total = (long)m * heads * (dkp / 2);
@@ -275,6 +276,15 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
     float* d = q + ((long)i * H + hh) * dkp + 2 * pi;
     d[0] = e;
     d[1] = o;
+    if (q3 != nullptr) {  // the tensor-core attention's Q planes (s1_qprep_kernel's layout)
+      const int g = hh / G, rr = (hh - g * G) * m + i;
+      uint32_t ph, pm, pl;
+      split3h_pack(e * 64.f, o * 64.f, ph, pm, pl);
+      const long base = (((long)g * RB + (rr >> 7)) * 3) * 128 + (rr & 127);
+      reinterpret_cast<uint32_t*>(q3 + base * dkp)[pi] = ph;
+      reinterpret_cast<uint32_t*>(q3 + (base + 128) * dkp)[pi] = pm;
+      reinterpret_cast<uint32_t*>(q3 + (base + 256) * dkp)[pi] = pl;
+    }
     return;
   }
   const int g = is_v ? hh - H - Hkv : hh - H;
@@ -299,11 +309,14 @@ __global__ void query_qkv_kernel(const float* qkv, int m, int H, int Hkv, int dk
 
 int query_qkv_launch(const float* qkv, int m, int H, int Hkv, int dk, int dkp, int pos0, const double* rcos,
                      const double* rsin, float* q, float* k, float* v, void* k_pool, void* v_pool, long pool_tokens,
-                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, cudaStream_t st) {
+                     const int32_t* page_table, float* fresh_k, float* fresh_v, void* k2_pool, cudaStream_t st,
+                     void* q3) {
   const long total = (long)m * (H + 2 * Hkv) * (dkp / 2);
+  const int G = H / Hkv, RB = ceil_div(m * G, 128);
   launch_k(query_qkv_kernel, ceil_div(total, 256), 256, 0, st, 
       qkv, m, H, Hkv, dk, dkp, pos0, rcos, rsin, q, k, v, reinterpret_cast<__half*>(k_pool),
-      reinterpret_cast<__half*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v, reinterpret_cast<__half*>(k2_pool));
+      reinterpret_cast<__half*>(v_pool), pool_tokens, page_table, fresh_k, fresh_v, reinterpret_cast<__half*>(k2_pool),
+      reinterpret_cast<__half*>(q3), G, RB);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("query_qkv_kernel");
   return PKV_OK;
@@ -1007,7 +1020,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   const int row_blocks = ceil_div(a.R, 128);
   int total_splits = a.n_splits;
   const size_t fresh_smem = (a.tc_splits + a.m + (size_t)a.m * a.dkp) * sizeof(float);
-  bool combined = false;
+  bool combined = false, fresh_done = false;
   // scores by the second pass over the keys (no score matrix) unless the rows themselves
   // are wanted (capture_attn) or the renormalised scores need other ranks' heads
   const bool pass2 = a.tc_splits > 0 && per_layer != nullptr && capture_rows == nullptr && a.s > 0 &&
@@ -1028,6 +1041,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.n_splits = a.tc_splits;
     t.scale = a.scale;
     t.q3 = a.q3;
+    t.q3_ready = a.q3_ready;
     t.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
     t.pool_tokens = a.pool_tokens;
     t.page_table = a.page_table;
@@ -1035,12 +1049,16 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.Opart = a.Opart;
     t.Mpart = a.Mpart;
     t.Lpart = a.Lpart;
+    // the fresh query keys ride along as an extra CTA slot of the same launch
+    static const bool fused_fresh_env = getenv("PKV_FRESH_FUSED") && getenv("PKV_FRESH_FUSED")[0] == '1';
+    t.fresh = (a.m <= 128 && !fused_fresh_env) ? 1 : 0;
+    t.fk = a.fk;
+    t.fv = a.fv;
     int rc = s1_attn_tc_launch(t, a.k1_all, a.k2_all, a.v_all, a.pool_rows_total, a.dkp, st);
     if (rc) return rc;
     // fused fresh keys + combine: measured neutral (each CTA re-reads the head's fresh V),
     // so opt-in (PKV_FRESH_FUSED=1)
-    static const bool fused_fresh = getenv("PKV_FRESH_FUSED") && getenv("PKV_FRESH_FUSED")[0] == '1';
-    if (fused_fresh && fresh_smem <= 160 * 1024 && !(pass2 && renorm)) {
+    if (fused_fresh_env && fresh_smem <= 160 * 1024 && !(pass2 && renorm)) {
       // the m fresh query keys are merged inside the combine (one kernel instead of a
       // SIMT split + combine)
       static std::once_flag once_fresh;
@@ -1053,7 +1071,8 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
       PKV_LAUNCHED();
       PKV_CHECK_LAUNCH("s1_attn_combine_fresh");
       combined = true;
-    } else {  // long queries: the fresh keys as one extra SIMT split
+    } else {  // the fresh keys as one extra split (inside the launch above, or SIMT)
+      fresh_done = t.fresh != 0;
       a.key_base = a.s;
       a.keys_per_split = a.m;
       a.n_splits = 1;
@@ -1062,6 +1081,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     }
   }
   if (!combined) {
+  if (!fresh_done) {
   // short fresh-key split: 32-row CTAs (4x the parallelism); long SIMT ranges: 128 rows
   const bool small = a.tc_splits > 0;
   const int rows_per_cta = small ? 32 : 128;
@@ -1088,6 +1108,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   }
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_pass1");
+  }
   launch_k(s1_attn_combine, dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st, a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin,
                                                     reinterpret_cast<__half*>(a.x3_out), a.x3_ld, a.tc_splits,
