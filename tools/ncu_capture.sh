@@ -16,10 +16,12 @@ cap() {  # name, name-base, regex, skip
 cap rc_attn function '^attn_tc_kernel$' 16
 cap rc_gate_up demangled 'gemm_tc_kernel<\(int\)256, \(int\)3,' 16
 cap rc_down demangled 'gemm_tc_kernel<\(int\)256, \(int\)2,' 33
+cap rc_o demangled 'gemm_tc_kernel<\(int\)256, \(int\)2,' 32
 cap rc_qkv demangled 'gemm_tc_kernel<\(int\)256, \(int\)4,' 16
 cap qp_attn function '^s1_attn_tc_kernel$' 16
+cap qp_score function '^s1_score_tc_kernel$' 16
 cap qp_proj demangled 'gemm_tc_kernel<\(int\)96, \(int\)5,' 40
 cap assemble function '^assemble_kernel$' 0
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $OUT/launches_${TAG}.csv python tools/profile_step.py > $OUT/launches_${TAG}.log 2>&1
 echo "launches rc=$?" >> $OUT/ncu_${TAG}.status
