@@ -244,6 +244,14 @@ int gemm_tc_launch(int epi, int bn, const void* A, long lda, const void* B, long
   static const bool proj_cluster = getenv("PKV_PROJ_CLUSTER") && getenv("PKV_PROJ_CLUSTER")[0] == '1';
   if (cg == 1 && bn == 96 && epi == EPI_PROJ && proj_cluster && args.n_splits >= 2 && args.n_splits <= 8)
     return launch_proj_cluster(ta, tb, args, stream);
+  // grouped raster when the A operand does not stay in L2 (Stage-II down: 188 MB): a wave of
+  // ~P = SMs / cg tiles then covers ~sqrt(P) m-tiles x ~sqrt(P) n-tiles instead of every
+  // m-tile x P / tiles_m n-tiles, so each wave re-reads ~8 A panels instead of all 26.
+  // Opt-in (PKV_GEMM_RASTER=g, group size g): down 608 vs 568 us with g = 8 and 0, within
+  // the run-to-run spread under the power cap (profiles/r02/ab_ttft_r02d.txt), Stage II 125.8
+  // vs 125.6 ms -- the re-read A panels hit L2 often enough (ncu: 69 % hit rate on down).
+  static const int raster_env = getenv("PKV_GEMM_RASTER") ? atoi(getenv("PKV_GEMM_RASTER")) : 0;
+  if (epi != EPI_PROJ && args.raster_gm == 0) args.raster_gm = raster_env;
   args.sk_pairs = 0;
   if (cg == 2 && epi != EPI_PROJ && bn == 256 && args.n_splits == 1 && args.sk_part && args.sk_cnt) {
     int rem, maxp;

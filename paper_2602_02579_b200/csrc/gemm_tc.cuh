@@ -80,6 +80,7 @@ struct GemmArgs {
   float norm_eps;
   int f16;                    // operands fp16 (Stage II, narrow projections) instead of bf16
   float acc_scale;            // accumulator multiplier (2^-e of the pre-scaled fp16 weights)
+  int raster_gm;              // tile-mode order: m-tiles per raster group (0 = all, m fastest)
   int* nonfinite;             // nullable: OR-ed with 1 when EPI_QKV / EPI_SILU / EPI_RESID write a
                               // non-finite value (the reference's check_finite, tensor.py:31-34)
 };
@@ -127,7 +128,11 @@ struct GemmCfg {
   static_assert(MT == 1 || EPI == EPI_PROJ, "sub-tiled A only for the narrow projection epilogue");
   static constexpr int ACC_STRIDE = MT * (BN <= 128 ? 128 : 256);
   static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // fp32 stores (EPI_F32 / EPI_RESID): a 32 x 32 fp32 transpose tile per epilogue warp, so the
+  // residual stream is read and written a whole 128-byte row segment per 8 lanes instead of
+  // one row per lane (32 lines per warp instruction)
+  static constexpr int EPI_STAGE = (EPI == 0 /*EPI_F32*/ || EPI == 2 /*EPI_RESID*/) ? 4 * 32 * 32 * 4 : 0;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE;
 };
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + expf(-x)); }
@@ -205,11 +210,19 @@ __global__ void __launch_bounds__(192, 1)
   griddep_launch();
   if (threadIdx.x == 64) gemm_stamp(args, 1);
 
+  // tile order: m fastest, in groups of raster_gm m-tiles (all n of a group before the next
+  // group) so that a wave of concurrent tiles reads few distinct A panels when A does not
+  // fit in L2 (Stage-II down projection: A = 6554 x 14336 fp16 = 188 MB)
+  const int gm = (args.raster_gm > 0 && args.raster_gm < tiles_m) ? args.raster_gm : tiles_m;
   auto tile_coords = [&](int t, int& mb, int& nb, int& sp) {
-    mb = t % tiles_m;
-    int r = t / tiles_m;
-    nb = r % tiles_n;
-    sp = r / tiles_n;
+    const int mn = tiles_m * tiles_n;
+    sp = t / mn;
+    const int r = t - sp * mn;
+    const int g0 = (r / (gm * tiles_n)) * gm;  // first m-tile of the group
+    const int gsz = min(gm, tiles_m - g0);
+    const int ri = r - g0 * tiles_n;
+    mb = g0 + ri % gsz;
+    nb = ri / gsz;
   };
 
   // Work items.  Tile mode: tile t = (m, n, split) strided over the grid.  Stream-K
@@ -599,6 +612,44 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld32(t_row + c * 32, r);
           tmem_ld_wait();
           const int col0 = nb * BN + c * 32;
+          if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {
+            if (args.xg == nullptr && col0 + 32 <= args.N && (args.ldc & 3) == 0) {
+              // transpose through shared memory: lane = row on the TMEM side, 8 lanes = one
+              // row's 32 columns (128 B) on the global side; float4 slots XOR-swizzled by row
+              float* stg = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256) + quarter * 1024;
+              float* base = reinterpret_cast<float*>(args.C) + (long)(w.slot >= 0 ? 0 : w.idx) * args.M * args.ldc + col0;
+              const int row0 = mb * Cfg::BMT + (int)rank * Cfg::BM + quarter * 32;
+              const int cc = lane & 7;
+              [[maybe_unused]] float4 o[8];
+              if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int gr = row0 + i * 4 + (lane >> 3);
+                  if (gr < args.M) o[i] = __ldcg(reinterpret_cast<const float4*>(base + (long)gr * args.ldc) + cc);
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) * 4)) =
+                    make_float4(__uint_as_float(r[4 * j]) * asc, __uint_as_float(r[4 * j + 1]) * asc,
+                                __uint_as_float(r[4 * j + 2]) * asc, __uint_as_float(r[4 * j + 3]) * asc);
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int rr = i * 4 + (lane >> 3), gr = row0 + rr;
+                float4 v = *reinterpret_cast<const float4*>(stg + rr * 32 + ((cc ^ (rr & 7)) * 4));
+                if (gr < args.M) {
+                  if constexpr (EPI == EPI_RESID) {
+                    v.x += o[i].x; v.y += o[i].y; v.z += o[i].z; v.w += o[i].w;
+                    bad |= !isfinite(v.x + v.y + v.z + v.w);
+                  }
+                  reinterpret_cast<float4*>(base + (long)gr * args.ldc)[cc] = v;
+                }
+              }
+              __syncwarp();
+              continue;
+            }
+          }
           if (!row_ok || col0 >= args.N) continue;
           const bool full = col0 + 32 <= args.N && (args.ldc & 7) == 0;  // vector stores need aligned rows
           if constexpr (EPI == EPI_F32 || EPI == EPI_RESID) {

@@ -125,17 +125,22 @@ def test_sparse_attention_matches_fp32_reference(built, H, Hkv, dk, s, n_q, perm
     assert err < 5e-3 and cos > 0.99999, (err, cos)
 
 
-def test_assembly_is_fp16_of_reference_keys(built):
+@pytest.mark.parametrize("hkv,dk,lens", [(2, 128, [300, 1, 517, 128]),    # 8 tokens per TMA group
+                                          (8, 128, [3, 1, 2, 261, 130]),     # Llama geometry, 4 per group
+                                          (4, 64, [1, 1, 1, 1, 1, 1, 1, 77])])  # one run per token
+def test_assembly_is_fp16_of_reference_keys(built, hkv, dk, lens):
+    """The assembly (ragged chunk boundaries, a context length that is not a multiple of the
+    TMA-staged form's token group) is the reference's stitch + RoPE rebase, rounded to fp16
+    bit for bit.  The TMA-staged form runs in a subprocess (its switch is read once)."""
     torch = _torch()
     P = built
-    cfg_o = O.Cfg(n_layers=3, n_heads=8, n_kv_heads=2, head_dim=128, hidden_dim=1024, ffn_dim=256,
+    cfg_o = O.Cfg(n_layers=3, n_heads=4 * hkv, n_kv_heads=hkv, head_dim=dk, hidden_dim=4 * hkv * dk, ffn_dim=256,
                   vocab_size=64, rope_theta=500000.0)
     rng = np.random.default_rng(5)
-    lens = [300, 1, 517, 128]
     chunks = []
     for ci, t in enumerate(lens):
-        kn = [O.bf16_round(rng.standard_normal((t, 2, 128)).astype(np.float32) * 3) for _ in range(3)]
-        vv = [O.bf16_round(rng.standard_normal((t, 2, 128)).astype(np.float32)) for _ in range(3)]
+        kn = [O.bf16_round(rng.standard_normal((t, hkv, dk)).astype(np.float32) * 3) for _ in range(3)]
+        vv = [O.bf16_round(rng.standard_normal((t, hkv, dk)).astype(np.float32)) for _ in range(3)]
         chunks.append(O.Chunk(chunk_id=ci, fp="fp", token_ids=rng.integers(0, 64, t), k_nr=kn, v=vv))
     ref = O.stitch(chunks, cfg_o)
     cfg = P.ModelConfig(**cfg_o.json())
@@ -143,8 +148,8 @@ def test_assembly_is_fp16_of_reference_keys(built):
     cache = P.assemble(dch, cfg)
     torch.cuda.synchronize()
     s = cache.context_length
-    kp = cache.k_pool[:, :, :s, :128].permute(0, 2, 1, 3)  # [L, s, Hkv, dk]
-    vp = cache.v_pool[:, :, :s, :128].permute(0, 2, 1, 3)
+    kp = cache.k_pool[:, :, :s, :dk].permute(0, 2, 1, 3)  # [L, s, Hkv, dk]
+    vp = cache.v_pool[:, :, :s, :dk].permute(0, 2, 1, 3)
     for li in range(3):
         want_k = torch.from_numpy(ref.keys[li]).cuda().half()
         want_v = torch.from_numpy(ref.values[li]).cuda().half()
@@ -152,7 +157,7 @@ def test_assembly_is_fp16_of_reference_keys(built):
         assert torch.equal(vp[li].view(torch.int16), want_v.view(torch.int16))
         # key + residual plane = the reference's f32 key to 2^-22 relative (2^-25 absolute
         # where the residual is an fp16 subnormal)
-        k2 = cache.k2_pool[li, :, :s, :128].permute(1, 0, 2).float()
+        k2 = cache.k2_pool[li, :, :s, :dk].permute(1, 0, 2).float()
         planes = (kp[li].float() + k2).double().cpu().numpy()
         refk = ref.keys[li].astype(np.float64)
         assert np.all(np.abs(planes - refk) <= np.abs(refk) * 2.0 ** -22 + 2.0 ** -25)
@@ -265,3 +270,20 @@ def test_gemm_stream_k_tail_opt_in(built, tmp_path):
     env = dict(os.environ, PKV_GEMM_SK="1")
     r = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_opt_in_variants():
+    """The opt-in kernel variants whose switches are read once per process -- the TMA-staged
+    assembly (PKV_ASM_TMA=1) and the grouped GEMM raster (PKV_GEMM_RASTER=2: partial groups
+    on every GEMM test shape) -- rerun the kernel tests in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PKV_ASM_TMA="1", PKV_GEMM_RASTER="2")
+    tests = ["tests/test_gpu_kernels.py::test_assembly_is_fp16_of_reference_keys",
+             "tests/test_gpu_kernels.py::test_gemm_matches_fp32_reference",
+             "tests/test_gpu_kernels.py::test_gemm_fp16_operands", "tests/test_gpu_kernels.py::test_gemm_residual_epilogue"]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *tests], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
