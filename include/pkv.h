@@ -204,6 +204,18 @@ int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* cache, int32_t l
 int pkv_cache_view(const pkv_config* cfg, const pkv_cache* cache, const pkv_chunks* chunks, int32_t layer, int32_t is_key,
                    float* out, void* stream);
 
+/* Probe baselines (reference selection.py:95-142, score_cacheblend_l1 / score_kvshare_l1),
+ * the reductions that follow the per-block probe passes (pkv_query_pass with PKV_QP_PROBE):
+ *   pkv_probe_accum   colsum[t] += n * part[t] (t < p0), += part[t] (p0 <= t < p0 + n): the
+ *                     layer-0 head-mean attention column sums of block [p0, p0+n), f64, in
+ *                     block order (reference _low_layer_probe: rows.astype(F64).sum(axis=0));
+ *   pkv_probe_scores  out[t] = f32(colsum[t] * ||dV_t||_1) (kvshare) or f32(||dV_t||_2)
+ *                     (colsum == NULL: cacheblend), dV_t = v1[t] - the assembled layer-1
+ *                     value of token t, norms in f64.  v1: [s][Hkv][head_dim] f32. */
+int pkv_probe_accum(const float* part, int32_t p0, int32_t n, double* colsum, void* stream);
+int pkv_probe_scores(const pkv_config* cfg, const pkv_cache* cache, const float* v1, const double* colsum, float* out,
+                     void* stream);
+
 /* ---------------------------------------------------------------------------
  * Head-sharded (tensor-parallel) prefill -- SURVEY §8(e), config C3 on 2/4/8 GPUs.
  * No reference counterpart: the reference is single-process numpy.

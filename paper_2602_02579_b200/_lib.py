@@ -76,6 +76,8 @@ _SIGS = {
     "pkv_full_prefill": (c_i32, [c_vp, ctypes.POINTER(Cache), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pkv_replace_entries": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "pkv_cache_view": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), ctypes.POINTER(Chunks), c_i32, c_i32, c_vp, c_vp]),
+    "pkv_probe_accum": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "pkv_probe_scores": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), c_vp, c_vp, c_vp, c_vp]),
     "pkv_gemm_bf16": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_i32, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "pkv_proj_narrow": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_vp]),
     "pkv_attention_sparse": (c_i32, [c_vp, ctypes.POINTER(Cache), c_i32, c_vp, c_vp, c_vp, c_i32, c_vp]),
@@ -112,6 +114,8 @@ def load(path: str | os.PathLike | None = None):
         raise EngineError(f"CUDA extension {p} is not built; run __graft_entry__.build()")
     lib = ctypes.CDLL(str(p))
     for name, (res, args) in _SIGS.items():
+        if not hasattr(lib, name) and "PKV_LIB" in os.environ and not path:
+            continue  # an older build under A/B: entry points it lacks stay unbound
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

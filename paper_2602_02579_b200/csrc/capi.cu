@@ -366,6 +366,24 @@ int pkv_cache_view(const pkv_config* cfg, const pkv_cache* c, const pkv_chunks* 
                            out, S(stream));
 }
 
+int pkv_probe_accum(const float* part, int32_t p0, int32_t n, double* colsum, void* stream) {
+  if (!part || !colsum) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (p0 < 0 || n < 0) return set_error(PKV_ERR_ARGUMENT, "bad block");
+  return probe_accum_launch(part, p0, n, colsum, S(stream));
+}
+
+int pkv_probe_scores(const pkv_config* cfg, const pkv_cache* c, const float* v1, const double* colsum, float* out,
+                     void* stream) {
+  if (!cfg || !c || !v1 || !out) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  int lay[5];
+  int rc = layout_of(cfg, lay);
+  if (rc) return rc;
+  if (cfg->n_layers < 2) return set_error(PKV_ERR_ARGUMENT, "the probe scores need layer 1");
+  const long layer_pool = (long)cfg->n_kv_heads * c->pool_tokens * lay[0];
+  return probe_scores_launch(v1, reinterpret_cast<const __half*>(c->v_pool) + layer_pool, c->page_table,
+                             c->pool_tokens, c->s, cfg->n_kv_heads, cfg->head_dim, lay[0], colsum, out, S(stream));
+}
+
 int pkv_replace_entries(const pkv_config* cfg, const pkv_cache* c, int32_t layer, const int32_t* idx, int32_t n,
                         const float* new_k, const float* new_v, void* stream) {
   int lay[5];

@@ -124,6 +124,9 @@ int norm_defer_launch(const float* h, int m, long ld, int N, const float* g, voi
                       int ssq_ld, cudaStream_t st);
 int probe_diag_colsum_launch(const float* q, const float* k, const float* Mfin, const float* Lfin, int m, int H,
                              int Hkv, int dk, int dkp, float scale, float* out, cudaStream_t st);
+int probe_accum_launch(const float* part, int p0, int n, double* colsum, cudaStream_t st);
+int probe_scores_launch(const float* v1, const void* vp1, const int32_t* page_table, long pool_tokens, int s, int Hkv,
+                        int dk, int dkp, const double* colsum, float* out, cudaStream_t st);
 int probe_cache_kv_launch(float* k, float* v, int m, int Hkv, int dk, int dkp, int pos0, const void* k_pool,
                           const void* k2_pool, const void* v_pool, long pool_tokens,
                           const int32_t* page_table, cudaStream_t st);

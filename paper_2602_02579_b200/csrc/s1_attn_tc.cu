@@ -50,6 +50,10 @@ struct S1TcCfg {
   // TMEM columns: Q planes [0,192) (plane x at 64x, DKP/2 columns each), S [192,256),
   // O [256,256+DKP), P planes [384,480)
   static constexpr int T_Q = 0, Q_PLANE = 64, T_S = 192, T_O = 256, T_P = 384;
+  // two P buffers (2 fp16 planes x 32 columns each) when they fit: the softmax writes P(j)
+  // while PV(j-1) still reads P(j-1), and waits for PV(j-1) only to rescale O
+  static constexpr int P_BUFS = 2;  // set below per datapath
+
   static constexpr int SOFTMAX_WARPS = 8;
 };
 
@@ -68,6 +72,7 @@ constexpr int S1_QK_PROD = 5, S1_P_PLANES = 3;
 constexpr int S1_QK_PROD = 3, S1_P_PLANES = 2;
 #endif
 constexpr int S1_Q_PLANES = S1_QK_PROD > 3 ? 3 : 2;
+constexpr int S1_P_BUFS = S1_P_PLANES == 2 ? 2 : 1;  // P buffers in TMEM [384, 512)
 
 __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int RB, int dkp, __half* q3) {
   pdl_entry();
@@ -165,9 +170,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* kv_empty = bars + C::STAGES;
   uint64_t* s_full = bars + 2 * C::STAGES;
   uint64_t* s_free = s_full + 1;
-  uint64_t* p_full = s_free + 1;
-  uint64_t* pv_full = p_full + 1;
-  uint64_t* q_full = pv_full + 1;
+  uint64_t* p_full = s_free + 1;   // [2]: per P buffer
+  uint64_t* pv_full = p_full + 2;  // [2]: PV of the P buffer done
+  uint64_t* q_full = pv_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -185,8 +190,10 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(s_free, C::SOFTMAX_WARPS);
-    mbar_init(p_full, C::SOFTMAX_WARPS);
-    mbar_init(pv_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&p_full[b], C::SOFTMAX_WARPS);
+      mbar_init(&pv_full[b], 1);
+    }
     mbar_init(q_full, C::SOFTMAX_WARPS);
     fence_barrier_init();
   }
@@ -253,7 +260,9 @@ __global__ void __launch_bounds__(320, 1)
       if (j >= 1) {
         const int jp = j - 1;
         const int st = jp % C::STAGES;
-        mbar_wait(p_full, (uint32_t)jp & 1);
+        // P buffer b holds P(b), P(b + B), ...: P(jp) is its (jp / B)-th fill
+        const int pb = jp % S1_P_BUFS;
+        mbar_wait(&p_full[pb], (uint32_t)(jp / S1_P_BUFS) & 1);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t v_addr = smem_u32(sKV + st * C::STAGE + 2 * C::PLANE);
@@ -262,10 +271,10 @@ __global__ void __launch_bounds__(320, 1)
           for (int x = 0; x < S1_P_PLANES; ++x)
 #pragma unroll
             for (int kk = 0; kk < C::KT / 16; ++kk, ++n)
-              umma_ts(tmem + C::T_O, tmem + C::T_P + x * (C::KT / 2) + kk * 8,
+              umma_ts(tmem + C::T_O, tmem + C::T_P + pb * 64 + x * (C::KT / 2) + kk * 8,
                            sdesc_sw128(v_addr + kk * 16 * 128, C::ATOM_K, 1024), idesc_o,
                            (jp > 0 || n > 0) ? 1u : 0u);
-          umma_commit(pv_full);
+          umma_commit(&pv_full[pb]);
           umma_commit(&kv_empty[st]);
         }
         __syncwarp();
@@ -351,10 +360,18 @@ __global__ void __launch_bounds__(320, 1)
         if constexpr (S1_P_PLANES == 3) split3h_pack(p0 * S1_PSCALE, p1 * S1_PSCALE, ph[i], pm[i], pl[i]);
         else split2h_pack(p0 * S1_PSCALE, p1 * S1_PSCALE, ph[i], pm[i]);
       }
-      if (j >= 1) {  // PV(j-1) has read P and accumulated O
-        mbar_wait(pv_full, (uint32_t)(j - 1) & 1);
+      const int pb = j % S1_P_BUFS;
+      if (j >= S1_P_BUFS) {  // PV(j - B) has read this P buffer
+        mbar_wait(&pv_full[pb], (uint32_t)((j - S1_P_BUFS) / S1_P_BUFS) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, grow)) {
+      }
+      if (j >= 1 && __any_sync(0xffffffffu, grow)) {  // rescale O: PV(j-1) must have accumulated
+        {
+          const int jq = j - 1;
+          mbar_wait(&pv_full[jq % S1_P_BUFS], (uint32_t)(jq / S1_P_BUFS) & 1);
+          tc_fence_after();
+        }
+        {
           const float f = grow ? corr : 1.f;
 #pragma unroll 1
           for (int c = hc * DKP / 64; c < (hc + 1) * DKP / 64; ++c) {
@@ -369,17 +386,18 @@ __global__ void __launch_bounds__(320, 1)
       }
       l_run = l_run * (grow ? corr : 1.f) + psum;
       m_run = m_new;
-      const uint32_t tP = tmem + lb + C::T_P;
+      const uint32_t tP = tmem + lb + C::T_P + pb * 64;
       tmem_st16(tP + hc * (HC / 2), ph);
       tmem_st16(tP + C::KT / 2 + hc * (HC / 2), pm);
       if constexpr (S1_P_PLANES == 3) tmem_st16(tP + C::KT + hc * (HC / 2), pl);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[pb]);
     }
     if (n_tiles > 0) {
-      mbar_wait(pv_full, (uint32_t)(n_tiles - 1) & 1);
+      const int jq = n_tiles - 1;  // the last PV completes after all earlier ones
+      mbar_wait(&pv_full[jq % S1_P_BUFS], (uint32_t)(jq / S1_P_BUFS) & 1);
       tc_fence_after();
     }
     const long base = ((long)split * a.Hkv + g) * a.R + row;

@@ -1396,3 +1396,57 @@ int embed_gather_launch(const void* embed, long lde, const int32_t* ids, const i
 }
 
 }  // namespace pkv
+
+namespace pkv {
+
+// ------------------------------------------------------ probe baselines (selection.py:95-142)
+// kvshare column sums: block [p0, p0+n) adds n * (its mean row over keys < p0) and its own
+// diagonal part, in f64, one launch per block in block order (deterministic)
+__global__ void probe_accum_kernel(const float* __restrict__ part, int p0, int n, double* colsum) {
+  pdl_entry();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= p0 + n) return;
+  const double v = (double)part[t];
+  colsum[t] += t < p0 ? v * (double)n : v;
+}
+
+// per context token t (one warp): dV = v1[t] - assembled layer-1 value (fp16 pool = the
+// chunk store's bf16 value exactly), f64 norms; out = f32(colsum[t] * ||dV||_1) (kvshare)
+// or f32(||dV||_2) (cacheblend, colsum == nullptr)
+__global__ void probe_scores_kernel(const float* __restrict__ v1, const __half* __restrict__ vp1,
+                                    const int32_t* page_table, long pool_tokens, int s, int Hkv, int dk, int dkp,
+                                    const double* __restrict__ colsum, float* out) {
+  pdl_entry();
+  const int t = (int)(((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (t >= s) return;
+  const long slot = (long)page_table[t >> 7] * 128 + (t & 127);
+  double acc = 0.0;
+  for (int e = lane; e < Hkv * dk; e += 32) {
+    const int h = e / dk, d = e - h * dk;
+    const double dv = (double)v1[(long)t * Hkv * dk + e] - (double)__half2float(vp1[((long)h * pool_tokens + slot) * dkp + d]);
+    acc += colsum != nullptr ? fabs(dv) : dv * dv;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) out[t] = colsum != nullptr ? (float)(colsum[t] * acc) : (float)sqrt(acc);
+}
+
+int probe_accum_launch(const float* part, int p0, int n, double* colsum, cudaStream_t st) {
+  if (p0 + n <= 0) return PKV_OK;
+  launch_k(probe_accum_kernel, ceil_div(p0 + n, 256), 256, 0, st, part, p0, n, colsum);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("probe_accum_kernel");
+  return PKV_OK;
+}
+
+int probe_scores_launch(const float* v1, const void* vp1, const int32_t* page_table, long pool_tokens, int s, int Hkv,
+                        int dk, int dkp, const double* colsum, float* out, cudaStream_t st) {
+  if (s <= 0) return PKV_OK;
+  launch_k(probe_scores_kernel, ceil_div((long)s * 32, 256), 256, 0, st, v1, reinterpret_cast<const __half*>(vp1),
+           page_table, pool_tokens, s, Hkv, dk, dkp, colsum, out);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("probe_scores_kernel");
+  return PKV_OK;
+}
+
+}  // namespace pkv

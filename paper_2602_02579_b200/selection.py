@@ -212,14 +212,16 @@ def score_epic(cache, n_layers: int) -> ValueScores:
     return ValueScores.from_vector("epic", (-cache.source_local.astype(np.int64)).astype(F32), n_layers)
 
 
-def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None, want_colsum: bool = False):
-    """Layer-1 values of the low-layer probe (reference selection.py:95-124) for every
-    context token, [s, kv_dim] f32 on the device: block 0 over the assembled layer-0 cache,
-    then rmsnorm + the value projection of layer 1.  Context tokens [p, p+32) run as one
-    fp32-faithful narrow pass over the cache truncated to [0, p) -- at positions p.. they
-    attend to it and causally to each other (their fresh layer-0 K/V equal the assembled
-    entries: layer 0 has no context) -- stopped after layer 1's projections
-    (``PKV_QP_PROBE``)."""
+def _probe_scores(weights, config: ModelConfig, cache, tally: FlopTally | None, kvshare: bool) -> np.ndarray:
+    """Scores of the low-layer probe (reference selection.py:95-142) for every context token.
+    Block 0 over the assembled layer-0 cache, then rmsnorm + the value projection of layer 1:
+    context tokens [p, p+32) run as one fp32-faithful narrow pass over the cache truncated to
+    [0, p) -- at positions p.. they attend to it and causally to each other (their fresh
+    layer-0 K/V equal the assembled entries: layer 0 has no context) -- stopped after layer
+    1's projections (``PKV_QP_PROBE``).  Everything stays on the stream: kvshare's layer-0
+    column sums accumulate in f64 on the device in block order (``pkv_probe_accum``), the
+    probe's layer-1 values land in one [s, kv_dim] buffer, and ``pkv_probe_scores`` forms
+    ||dV||_2 (cacheblend) or colsum * ||dV||_1 (kvshare) per token; one [s] read-back."""
     import ctypes
     torch = _lib.require_cuda()
     dm = resolve_device_model(weights, config)
@@ -227,38 +229,41 @@ def _probe_values(weights, config: ModelConfig, cache, tally: FlopTally | None, 
     cache.wait_ready()  # a host-tier chunk transfer may still be filling the chunk buffers / pool
     Hkv, dk = cache.config.n_kv_heads, config.head_dim
     m = 32
-    flags = _lib.PKV_QP_PROBE | _lib.PKV_QP_FROM_CHUNKS | (_lib.PKV_QP_SCORES if want_colsum else 0)
+    flags = _lib.PKV_QP_PROBE | _lib.PKV_QP_FROM_CHUNKS | (_lib.PKV_QP_SCORES if kvshare else 0)
     lib = _lib.load()
-    # kvshare: column sums of layer 0's head-mean attention over every context query;
-    # block [p, p+n) contributes n * (its mean row over keys < p) plus its own diagonal
-    colsum = np.zeros(s, dtype=F64) if want_colsum else None
-    pl = torch.empty(s + m, dtype=torch.float32, device=cache.device) if want_colsum else None
+    st = _lib.stream_ptr(torch)
+    colsum = torch.zeros(s, dtype=torch.float64, device=cache.device) if kvshare else None
+    pl = torch.empty(s + m, dtype=torch.float32, device=cache.device) if kvshare else None
     fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
     fv = torch.empty_like(fk)
     v1 = torch.empty((s, Hkv * dk), dtype=torch.float32, device=cache.device)
-    ids = np.asarray(cache.token_ids, dtype=np.int32)
+    d_ids = torch.from_numpy(np.asarray(cache.token_ids, dtype=np.int32).copy()).to(cache.device)
     chunks = ctypes.byref(cache.c_chunks)
+    # the workspace grows with the truncated context: size it once for the last block
+    # (the split plan of the narrow pass makes the size non-monotone in the context length:
+    # take the largest over the blocks, a host-side computation)
+    ws = workspace(max(lib.pkv_query_pass_workspace(dm.handle, p0, min(m, s - p0), flags) for p0 in range(0, s, m)),
+                   "probe")
+    view = _lib.Cache.from_buffer_copy(cache.c_cache)
+    view.layer_ready = None
     for p0 in range(0, s, m):
         n = min(m, s - p0)
-        view = _lib.Cache.from_buffer_copy(cache.c_cache)
         view.s = p0
-        view.layer_ready = None
-        d_ids = torch.from_numpy(ids[p0:p0 + n].copy()).to(cache.device)
-        ws = workspace(lib.pkv_query_pass_workspace(dm.handle, p0, n, flags), "probe")
-        _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(view), chunks, d_ids.data_ptr(), n, flags,
+        _lib.check(lib.pkv_query_pass(dm.handle, ctypes.byref(view), chunks, d_ids.data_ptr() + 4 * p0, n, flags,
                                       pl.data_ptr() if pl is not None else None, fk.data_ptr(), fv.data_ptr(), None,
-                                      ws.data_ptr(), ws.numel(), _lib.stream_ptr(torch)))
-        if colsum is not None:
-            part = pl[: p0 + n].double().cpu().numpy()
-            colsum[:p0] += part[:p0] * n
-            colsum[p0:p0 + n] += part[p0:p0 + n]
+                                      ws.data_ptr(), ws.numel(), st))
+        if kvshare:
+            _lib.check(lib.pkv_probe_accum(pl.data_ptr(), p0, n, colsum.data_ptr(), st))
         # fresh_v is [L][n][Hkv][dk] for this pass's n rows
         v1[p0:p0 + n] = fv.view(-1)[n * Hkv * dk: 2 * n * Hkv * dk].view(n, Hkv * dk)
+    out = torch.empty(s, dtype=torch.float32, device=cache.device)
+    _lib.check(lib.pkv_probe_scores(ctypes.byref(cache._cfg_c), ctypes.byref(cache.c_cache), v1.data_ptr(),
+                                    colsum.data_ptr() if kvshare else None, out.data_ptr(), st))
     if tally is not None:  # reference books: block 0 with dense s x s attention + layer-1 wv
         H, D, F, KV = config.n_heads, config.hidden_dim, config.ffn_dim, config.kv_dim
         tally.total.add(s * D * (H * dk + 2 * KV) + 2 * H * s * dk * s + s * H * dk * D + 3 * s * D * F + s * D * KV)
         tally.attn_scores.add(H * s * dk * s)
-    return (v1, colsum) if want_colsum else v1
+    return out.cpu().numpy()
 
 
 def score_cacheblend_l1(weights, config: ModelConfig, cache, embeddings=None,
@@ -274,13 +279,7 @@ def score_cacheblend_l1(weights, config: ModelConfig, cache, embeddings=None,
             tally.total.add(s * D * (H * dk + 2 * KV) + 2 * H * s * dk * s + s * H * dk * D + 3 * s * D * F)
             tally.attn_scores.add(H * s * dk * s)
         return ValueScores.from_vector("cacheblend_l1", np.zeros(s, dtype=F32), L)
-    v1 = _probe_values(weights, config, cache, tally)
-    Hkv, dk = cache.config.n_kv_heads, config.head_dim
-    # assembled layer-1 values from the pool (bf16 of the chunk store's f32 values; the
-    # pool slot of context token t is t)
-    cached = cache.v_pool[1, :, :s, :dk].permute(1, 0, 2).reshape(s, Hkv * dk)
-    dv = v1.double().cpu().numpy() - cached.double().cpu().numpy()
-    return ValueScores.from_vector("cacheblend_l1", np.linalg.norm(dv, axis=1), L)
+    return ValueScores.from_vector("cacheblend_l1", _probe_scores(weights, config, cache, tally, kvshare=False), L)
 
 
 def score_kvshare_l1(weights, config: ModelConfig, cache, embeddings=None,
@@ -292,11 +291,7 @@ def score_kvshare_l1(weights, config: ModelConfig, cache, embeddings=None,
     s, L = cache.context_length, config.n_layers
     if L == 1:  # dV = 0, so colsum * ||dV||_1 = 0 (reference selection.py:118-119)
         return score_cacheblend_l1(weights, config, cache, None, tally)._renamed("kvshare_l1")
-    v1, colsum = _probe_values(weights, config, cache, tally, want_colsum=True)
-    Hkv, dk = cache.config.n_kv_heads, config.head_dim
-    cached = cache.v_pool[1, :, :s, :dk].permute(1, 0, 2).reshape(s, Hkv * dk)
-    dv = v1.double().cpu().numpy() - cached.double().cpu().numpy()
-    return ValueScores.from_vector("kvshare_l1", colsum * np.abs(dv).sum(axis=1), L)
+    return ValueScores.from_vector("kvshare_l1", _probe_scores(weights, config, cache, tally, kvshare=True), L)
 
 
 def score_random(s_context: int, seed: int, n_layers: int) -> ValueScores:
