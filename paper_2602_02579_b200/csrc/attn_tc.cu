@@ -747,6 +747,302 @@ __global__ void __launch_bounds__(832, 1)
 }
 
 // ------------------------------------------------------------------ host side
+// One 128-row Q tile per CTA with S double-buffered in TMEM (PKV_ATTN_ONE=1).  The two-tile
+// kernel above keeps one S buffer per tile because two tiles' S and O fill all 512 TMEM
+// columns, so each tile's page loop is the chain softmax(j) -> PV(j) -> S(j+1) ->
+// softmax(j+1) (ncu: the softmax warps wait for S 39 % of the time, tensor pipe 63 %).
+// With one tile the columns hold S(j) and S(j+1) [0,256), O [256,384) and two P buffers
+// [384,512), so S(j+1) is computed while the softmax of page j runs and the softmax runs
+// back to back; the cost is that every CTA streams its own K/V pages (twice the L2 -> SM
+// traffic per flop of the two-tile form).
+//   warps 0-7  softmax: warp w owns TMEM lane quarter w%4 and keys [64h, 64h+64), h = w/4
+//   warp 8     TMA producer (3-stage K/V ring)
+//   warp 9     TMEM owner + MMA issuer: S(0), S(1), then per page j: PV(j), S(j+2)
+constexpr int ATTN1_NST = 3;
+constexpr int ATTN1_NEED = 128 * 128 * 2 /*Q*/ + ATTN1_NST * 2 * 128 * 128 * 2 /*K/V*/ + 2048 /*max exchange*/ +
+                           16 * 8 /*barriers*/ + 16;
+constexpr int ATTN1_SMEM = 232448;  // the per-block maximum; the kernel checks the aligned fit
+
+template <int POLY>
+__global__ void __launch_bounds__(320, 1)
+    attn_tc1_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
+  constexpr int DKP = 128, KVB = 128 * DKP * 2, NST = ATTN1_NST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  if (threadIdx.x == 0 && (smem - smem_raw) + ATTN1_NEED > ATTN1_SMEM) __trap();
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + KVB;  // stage s: K at sKV + 2*s*KVB, V right after
+  float* red = reinterpret_cast<float*>(sKV + NST * 2 * KVB);  // [2 parity][2 halves][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 512);
+  uint64_t* kv_full = bars;         // [NST]
+  uint64_t* kv_empty = bars + NST;  // [NST]
+  uint64_t* s_full = bars + 2 * NST;  // [2] per S buffer
+  uint64_t* s_free = s_full + 2;      // [2]
+  uint64_t* p_full = s_free + 2;      // [2] per P buffer
+  uint64_t* pv_full = p_full + 2;     // [2]
+  uint64_t* q_full = pv_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+  constexpr uint32_t T_O = 256, T_P = 384;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // CTA order: KV-head groups of hg heads, inside a group the heaviest tiles first (LPT)
+  const int per_group = a.hg * a.n_tiles;
+  const int grp = (int)blockIdx.x / per_group, rem_ = (int)blockIdx.x - grp * per_group;
+  const int g = grp * a.hg + rem_ % a.hg;
+  const int b = a.n_tiles - 1 - rem_ / a.hg;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
+      mbar_init(&pv_full[i], 1);
+    }
+    mbar_init(q_full, 8);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // PDL: q / the scattered K/V come from the previous kernel
+  griddep_launch();
+  const int tile_last = min((b + 1) * a.T, a.n_q) - 1;
+  const int n_kv = a.pos[tile_last] / 128 + 1;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % NST;
+        mbar_wait(&kv_empty[st], ((uint32_t)(j / NST) & 1) ^ 1);
+        uint8_t* sk = sKV + st * 2 * KVB;
+        const int row = (int)(head_row + (long)a.page_table[j] * 128);
+        mbar_expect_tx(&kv_full[st], 2 * KVB);
+#pragma unroll
+        for (int at = 0; at < 2; ++at) {
+          tma_load_2d(sk + at * 16384, &tmK, &kv_full[st], at * 64, row);
+          tma_load_2d(sk + KVB + at * 16384, &tmV, &kv_full[st], at * 64, row);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc_s = make_idesc_f16(128, 128);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, DKP, /*b_mn_major=*/true);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint32_t q_addr = smem_u32(sQ);
+    auto issue_s = [&](int j) {  // S(j) = Q K_j^T -> S buffer j % 2
+      mbar_wait(&kv_full[j % NST], (uint32_t)(j / NST) & 1);
+      tc_fence_after();
+      const uint32_t k_addr = smem_u32(sKV + (j % NST) * 2 * KVB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < DKP / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_ss(tmem + (j & 1) * 128, sdesc_sw128(q_addr + off, 16, 1024), sdesc_sw128(k_addr + off, 16, 1024),
+                  idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[j & 1]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    if (n_kv > 1) issue_s(1);
+    for (int j = 0; j < n_kv; ++j) {
+      const int pb = j & 1;
+      mbar_wait(&p_full[pb], (uint32_t)(j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t v_addr = smem_u32(sKV + (j % NST) * 2 * KVB + KVB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ts(tmem + T_O, tmem + T_P + pb * 64 + kk * 8, sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024), idesc_o,
+                  (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&pv_full[pb]);
+        umma_commit(&kv_empty[j % NST]);
+      }
+      __syncwarp();
+      if (j + 2 < n_kv) {
+        mbar_wait(&s_free[pb], (uint32_t)(j >> 1) & 1);  // the softmax has S(j) in registers
+        issue_s(j + 2);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax
+    const int quarter = warp & 3, h = warp >> 2;
+    const int r = quarter * 32 + lane;  // TMEM lane == tile row
+    const int bar_id = 1 + quarter;     // the two key halves of these 32 rows
+    const int hj = r / a.T, ti = r - hj * a.T;
+    const int tok = b * a.T + ti;
+    const bool valid = hj < a.G && tok < a.n_q;
+    const int head = g * a.G + hj;
+    const int min_pos = a.pos[b * a.T];
+    const int my_pos = valid ? a.pos[tok] : a.pos[tile_last];
+    const uint32_t lb = (uint32_t)((quarter * 32) << 16);
+    const float sl2 = a.scale_log2;
+    {  // Q row, this warp's 64-column atom -> smem (128B-swizzled K-major)
+      uint4 v[8];
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) + h * 8;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int ch = c ^ (r & 7);
+        *reinterpret_cast<uint4*>(sQ + h * 16384 + r * 128 + ch * 16) = v[c];
+      }
+      fence_proxy_async_smem();
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_full);
+
+    float m_run = -INFINITY, l_run = 0.f;  // m in log2 units; l: this half's row sum
+    for (int j = 0; j < n_kv; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (uint32_t)(j >> 1) & 1);
+      tc_fence_after();
+      const int key0 = j * 128 + h * 64;
+      float sv[64];
+      {
+        uint32_t u[32], w[32];
+        tmem_ld32(tmem + sb * 128 + lb + h * 64, u);
+        tmem_ld32(tmem + sb * 128 + lb + h * 64 + 32, w);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          sv[i] = __uint_as_float(u[i]);
+          sv[32 + i] = __uint_as_float(w[i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[sb]);  // S(j + 2) may overwrite this buffer
+      if (key0 + 63 > min_pos) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) sv[i] = (key0 + i <= my_pos) ? sv[i] : -INFINITY;
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 64; i += 8)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(sv[i + 2 * q], sv[i + 2 * q + 1]));
+      const float hmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      float* rb = red + sb * 256;
+      rb[h * 128 + r] = hmax;
+      named_bar_sync(bar_id, 64);
+      const float tmax = fmaxf(hmax, rb[(h ^ 1) * 128 + r]);
+      const float m_new = fmaxf(m_run, tmax * sl2);
+      const bool grow = (m_new - m_run) > 8.0f;  // also true on the first page (m_run = -inf)
+      const float m_use = grow ? m_new : m_run;
+      const uint64_t sl2x2 = f32x2(sl2, sl2), negm = f32x2(-m_use, -m_use);
+      uint64_t rsum2 = f32x2(0.f, 0.f), rsum2b = f32x2(0.f, 0.f);
+      uint32_t pk[2][16];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t x = ffma2(f32x2(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]), sl2x2, negm);
+          float x0, x1;
+          f32x2_unpack(x, x0, x1);
+          float p0, p1;
+          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+          if ((kPolyMask >> (i & 7)) & 1u) {
+            p0 = exp2_poly(x0);
+            p1 = exp2_poly(x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
+          else rsum2 = fadd2(rsum2, f32x2(p0, p1));
+          pk[c][i] = pack_f16(p0, p1);
+        }
+      }
+      const int pb = j & 1;
+      if (j >= 2) {  // PV(j-2) has read this P buffer
+        mbar_wait(&pv_full[pb], (uint32_t)((j - 2) >> 1) & 1);
+        tc_fence_after();
+      }
+      tmem_st16(tmem + T_P + pb * 64 + lb + h * 32, pk[0]);
+      tmem_st16(tmem + T_P + pb * 64 + lb + h * 32 + 16, pk[1]);
+      float rs0, rs1;
+      f32x2_unpack(fadd2(rsum2, rsum2b), rs0, rs1);
+      const float rsum = rs0 + rs1;
+      if (__any_sync(0xffffffffu, grow && j > 0)) {  // O rescale: PV(j-1) must have accumulated
+        mbar_wait(&pv_full[(j - 1) & 1], (uint32_t)((j - 1) >> 1) & 1);
+        tc_fence_after();
+        const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
+#pragma unroll 1
+        for (int c = h * DKP / 64; c < (h + 1) * DKP / 64; ++c) {
+          uint32_t u[32];
+          tmem_ld32(tmem + T_O + lb + c * 32, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st32(tmem + T_O + lb + c * 32, u);
+        }
+      }
+      if (grow && j > 0) l_run *= ex2(m_run - m_use);
+      if (grow) m_run = m_use;
+      l_run += rsum;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[pb]);
+    }
+    mbar_wait(&pv_full[(n_kv - 1) & 1], (uint32_t)((n_kv - 1) >> 1) & 1);
+    tc_fence_after();
+    // row sum = both halves; every MMA has completed, so the Q tile is free scratch
+    float* lred = reinterpret_cast<float*>(sQ);
+    lred[h * 128 + r] = l_run;
+    named_bar_sync(bar_id, 64);
+    const float inv_l = 1.f / (lred[r] + lred[128 + r]);
+#pragma unroll 1
+    for (int c = h * DKP / 64; c < (h + 1) * DKP / 64; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tmem + T_O + lb + c * 32, u);
+      tmem_ld_wait();
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_f16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+static int launch_attn1(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(attn_tc1_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ATTN1_SMEM);
+  });
+  if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn1 smem attr: %s", cudaGetErrorString(err));
+  launch_k(attn_tc1_kernel<1>, a.n_tiles * a.Hkv, 320, ATTN1_SMEM, stream, tk, tv, a);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("attn_tc1_kernel");
+  return PKV_OK;
+}
+
 template <int DKP, int POLY>
 static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
   using Cfg = AttnCfg<DKP>;
@@ -858,6 +1154,8 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
       return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
     return launch_attn_pair<1>(tk64, tv, a, stream);
   }
+  static const bool one_env = getenv("PKV_ATTN_ONE") && getenv("PKV_ATTN_ONE")[0] == '1';
+  if (dkp == 128 && one_env && poly == 1) return launch_attn1(tk, tv, a, stream);
   if (dkp == 128) {
     if (poly == 1) return launch_attn<128, 1>(tk, tv, a, stream);
     if (poly < 0) return launch_attn<128, -1>(tk, tv, a, stream);

@@ -274,14 +274,16 @@ def test_gemm_stream_k_tail_opt_in(built, tmp_path):
 
 def test_opt_in_variants():
     """The opt-in kernel variants whose switches are read once per process -- the TMA-staged
-    assembly (PKV_ASM_TMA=1) and the grouped GEMM raster (PKV_GEMM_RASTER=2: partial groups
-    on every GEMM test shape) -- rerun the kernel tests in a subprocess."""
+    assembly (PKV_ASM_TMA=1), the grouped GEMM raster (PKV_GEMM_RASTER=2: partial groups
+    on every GEMM test shape) and the one-tile attention (PKV_ATTN_ONE=1) -- rerun the
+    kernel tests in a subprocess."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PKV_ASM_TMA="1", PKV_GEMM_RASTER="2")
+    env = dict(os.environ, PKV_ASM_TMA="1", PKV_GEMM_RASTER="2", PKV_ATTN_ONE="1")
     tests = ["tests/test_gpu_kernels.py::test_assembly_is_fp16_of_reference_keys",
+             "tests/test_gpu_kernels.py::test_sparse_attention_matches_fp32_reference",
              "tests/test_gpu_kernels.py::test_gemm_matches_fp32_reference",
              "tests/test_gpu_kernels.py::test_gemm_fp16_operands", "tests/test_gpu_kernels.py::test_gemm_residual_epilogue"]
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *tests], cwd=root,
