@@ -97,6 +97,7 @@ struct S1TcArgs {
   int fresh;
   const float* fk;
   const float* fv;
+  unsigned long long* trace;  // debug (PKV_S1_TRACE=1): %globaltimer per tile of CTA (0,0,0), s1_attn_tc.cu
 };
 int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
                       cudaStream_t st);

@@ -152,6 +152,18 @@ __device__ __noinline__ void s1_fresh_cta(const S1TcArgs& a, uint8_t* smem) {
   }
 }
 
+// trace[ev * 64 + j], tile j < 64 of CTA (0,0,0) (tools/s1_trace.py):
+//   ev 0: softmax warp 0 saw S(j)   ev 1: softmax warp 0 arrived P(j)   ev 2: MMA warp saw K/V(j)
+//   ev 3: MMA warp issued PV(j)     ev 4: producer issued tile j        ev 5: j=0 prologue done,
+//   j=1 softmax loop done, j=2 partials written
+__device__ __forceinline__ void s1_stamp(const S1TcArgs& a, int ev, int j) {
+  if (a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[ev * 64 + j] = t;
+  }
+}
+
 template <int DKP>
 __global__ void __launch_bounds__(320, 1)
     s1_attn_tc_kernel(const __grid_constant__ CUtensorMap tK1, const __grid_constant__ CUtensorMap tK2,
@@ -218,6 +230,7 @@ __global__ void __launch_bounds__(320, 1)
         const int t0 = k_begin + j * C::KT;  // 64-aligned: inside one 128-token page
         const int row = (int)(head_row + (long)a.page_table[t0 >> 7] * 128 + (t0 & 127));
         uint8_t* base = sKV + st * C::STAGE;
+        s1_stamp(a, 4, j);
         mbar_expect_tx(&kv_full[st], C::STAGE);
 #pragma unroll
         for (int at = 0; at < C::ATOMS; ++at) {
@@ -240,6 +253,7 @@ __global__ void __launch_bounds__(320, 1)
       if (j < n_tiles) {
         const int st = j % C::STAGES;
         mbar_wait(&kv_full[st], (uint32_t)(j / C::STAGES) & 1);
+        if (lane == 0) s1_stamp(a, 2, j);
         if (j >= 1) mbar_wait(s_free, (uint32_t)(j - 1) & 1);  // S(j-1) is in the softmax's registers
         tc_fence_after();
         if (elect_one()) {
@@ -276,6 +290,7 @@ __global__ void __launch_bounds__(320, 1)
                            (jp > 0 || n > 0) ? 1u : 0u);
           umma_commit(&pv_full[pb]);
           umma_commit(&kv_empty[st]);
+          s1_stamp(a, 3, jp);
         }
         __syncwarp();
       }
@@ -313,9 +328,11 @@ __global__ void __launch_bounds__(320, 1)
     float m_run = -INFINITY, l_run = 0.f;  // l_run: this warp's half of the row sum
     // scores, key-major S[g][t][r] (t < s): one warp store = 32 consecutive rows = 128 B
     float* scol = (a.S != nullptr && valid) ? a.S + (long)g * a.s * a.R + row : nullptr;
+    if (warp == 0 && lane == 0) s1_stamp(a, 5, 0);
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(s_full, (uint32_t)j & 1);
       tc_fence_after();
+      if (warp == 0 && lane == 0) s1_stamp(a, 0, j);
       // both warps of a quarter read the whole 64-key row (cheap TMEM reads) so each
       // has the tile max without an exchange; each then handles its 32 columns
       float sv[HC];
@@ -326,14 +343,27 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld32(tmem + lb + C::T_S + hc * HC, u);
         tmem_ld32(tmem + lb + C::T_S + (hc ^ 1) * HC, w);
         tmem_ld_wait();
-        const int okey0 = k_begin + j * C::KT + (hc ^ 1) * HC;
+        // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298.  The accumulator holds
+        // 2^6 q.k, so acc * (2^-6 scale) rounds exactly like (acc * 2^-6) * scale, and as the
+        // factor is positive the max of the rounded scores is the rounded max accumulator
+        const float c = a.scale * (1.f / S1_QSCALE);
+        if (k_begin + (j + 1) * C::KT <= k_end) {  // whole tile (warp-uniform): no mask
+          float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int i = 0; i < HC; ++i) {
-          // reference: f32(q.k) * F32(1/sqrt(dk)), model.py:291,298 (the accumulator holds 2^6 q.k)
-          const float x = (key0 + i < k_end) ? (__uint_as_float(u[i]) * (1.f / S1_QSCALE)) * a.scale : -INFINITY;
-          const float y = (okey0 + i < k_end) ? (__uint_as_float(w[i]) * (1.f / S1_QSCALE)) * a.scale : -INFINITY;
-          sv[i] = x;
-          tmax = fmaxf(tmax, fmaxf(x, y));
+          for (int i = 0; i < HC; ++i) {
+            sv[i] = __uint_as_float(u[i]) * c;
+            mx[i & 3] = fmaxf(mx[i & 3], fmaxf(__uint_as_float(u[i]), __uint_as_float(w[i])));
+          }
+          tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * c;
+        } else {
+          const int okey0 = k_begin + j * C::KT + (hc ^ 1) * HC;
+#pragma unroll
+          for (int i = 0; i < HC; ++i) {
+            const float x = (key0 + i < k_end) ? __uint_as_float(u[i]) * c : -INFINITY;
+            const float y = (okey0 + i < k_end) ? __uint_as_float(w[i]) * c : -INFINITY;
+            sv[i] = x;
+            tmax = fmaxf(tmax, fmaxf(x, y));
+          }
         }
       }
       tc_fence_before();
@@ -347,10 +377,14 @@ __global__ void __launch_bounds__(320, 1)
           for (int i = 0; i < HC && key0 + i < k_end; ++i) scol[(long)(key0 + i) * a.R] = sv[i];
         }
       }
+      // lazy rescale: the running max moves (and O / l are rescaled) only when a row's max
+      // grows by more than 2^5 in p; P' = 2^10 p then stays below 2^15 (fp16), and the
+      // pass's (M, L) stay a consistent pair for the split combine and scoring pass 2
       const float m_new = fmaxf(m_run, tmax);
-      const bool grow = m_new > m_run;
-      const float corr = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_new) * LOG2E);
-      const float mb = m_new * LOG2E;
+      const bool grow = (m_new - m_run) * LOG2E > 5.f;  // also true on the first tile (m_run = -inf)
+      const float m_use = grow ? m_new : m_run;
+      const float corr = (m_run == -INFINITY) ? 0.f : ex2((m_run - m_use) * LOG2E);
+      const float mb = m_use * LOG2E;
       float psum = 0.f;
       uint32_t ph[HC / 2], pm[HC / 2], pl[HC / 2];
 #pragma unroll
@@ -385,7 +419,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
       l_run = l_run * (grow ? corr : 1.f) + psum;
-      m_run = m_new;
+      m_run = m_use;
       const uint32_t tP = tmem + lb + C::T_P + pb * 64;
       tmem_st16(tP + hc * (HC / 2), ph);
       tmem_st16(tP + C::KT / 2 + hc * (HC / 2), pm);
@@ -394,7 +428,9 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[pb]);
+      if (warp == 0 && lane == 0) s1_stamp(a, 1, j);
     }
+    if (warp == 0 && lane == 0) s1_stamp(a, 5, 1);
     if (n_tiles > 0) {
       const int jq = n_tiles - 1;  // the last PV completes after all earlier ones
       mbar_wait(&pv_full[jq % S1_P_BUFS], (uint32_t)(jq / S1_P_BUFS) & 1);
@@ -423,6 +459,7 @@ __global__ void __launch_bounds__(320, 1)
       a.Mpart[base] = n_tiles > 0 ? m_run : -INFINITY;
       a.Lpart[base] = l_run + red[128 + r];
     }
+    if (warp == 0 && lane == 0) s1_stamp(a, 5, 2);
     tc_fence_before();
   }
   __syncthreads();
@@ -432,9 +469,18 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-int s1_attn_tc_launch(const S1TcArgs& a, const void* k1, const void* k2, const void* v, long pool_rows_total, int dkp,
-                      cudaStream_t st) {
+static unsigned long long* g_s1_trace = nullptr;
+
+int s1_attn_tc_launch(const S1TcArgs& a_in, const void* k1, const void* k2, const void* v, long pool_rows_total,
+                      int dkp, cudaStream_t st) {
+  S1TcArgs a = a_in;
   if (a.n_splits <= 0) return PKV_OK;
+  {
+    static const bool tr = getenv("PKV_S1_TRACE") && getenv("PKV_S1_TRACE")[0] == '1';
+    if (tr && g_s1_trace == nullptr && cudaMalloc(&g_s1_trace, 6 * 64 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(g_s1_trace, 0, 6 * 64 * sizeof(unsigned long long));
+    a.trace = tr ? g_s1_trace : nullptr;
+  }
   if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
   const int RB = ceil_div(a.R, 128);
   dim3 grid(a.n_splits + (a.fresh ? 1 : 0), a.Hkv, RB);
@@ -716,3 +762,10 @@ int s1_score_tc_launch(const S1ScoreArgs& a, const void* k1, const void* k2, lon
 }
 
 }  // namespace pkv
+
+extern "C" int pkv_debug_s1_trace(unsigned long long* host) {
+  if (pkv::g_s1_trace == nullptr) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, pkv::g_s1_trace, 6 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
