@@ -485,8 +485,10 @@ def main():
     # ---- graph-timed phase split (each phase captured and replayed alone, serial)
     graph_phases = {}
     try:
-        for name, fn in (("assemble_score_select", pipe.score_select), ("stage2", pipe.stage2),
-                         ("final", pipe.final)):
+        phase_fns = [("assemble_score_select", pipe.score_select), ("stage2", pipe.stage2)]
+        if not pipe.fused_final:  # else the query rows ride along Stage II (pkv_recompute_query)
+            phase_fns.append(("final", pipe.final))
+        for name, fn in phase_fns:
             g = pipe.capture(fn)
             g.replay()
             torch.cuda.synchronize()
@@ -528,8 +530,8 @@ def main():
             continue
         if name == "lm_head":  # one GEMV per step, timed together with its final norm (2 timer scopes)
             cnt = args.steps
-        if name == "qp_attn":  # one attention scope per layer per narrow pass (scoring + final)
-            cnt = args.steps * 2 * L
+        if name == "qp_attn":  # one attention scope per layer per narrow pass (scoring [+ final])
+            cnt = args.steps * L * (1 if pipe.fused_final else 2)
         per_launch_s = tot_ms / cnt / 1e3
         ach = units / per_launch_s / (1e9 if unit == "GB/s" else 1e12)
         peak = hbm if bound == "hbm" else tf_sust

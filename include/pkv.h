@@ -185,6 +185,21 @@ size_t pkv_recompute_workspace(const pkv_model* m, int32_t k);
 int pkv_recompute(const pkv_model* m, const pkv_cache* cache, const int32_t* sel, int32_t k, float* tap_k,
                   float* tap_v, void* workspace, size_t workspace_bytes, void* stream);
 
+/* recompute_selected (recompute.py:43-82) followed by finalize_query (recompute.py:105-125)
+ * in one pass: the m query tokens (device int32 ids) ride along the repair as rows
+ * k..k+m-1 at positions s..s+m-1 -- per layer they attend over the repaired layer plus their
+ * own causal entries, exactly what the separate query pass (model.py:370-402) reads --
+ * their K/V are appended to the pool (as PKV_QP_APPEND_KV), and last_logits receives the
+ * first-token logits of the last query row.  Stage-II precision (fp16 operands, fp32
+ * accumulation and residual stream) instead of the fp32-faithful narrow pass; the north-star
+ * logits tolerance (2e-2 / 0.999) applies.  query_k/query_v (nullable): fp32 [L][m][Hkv][dk]
+ * fresh query K/V (the reference's appended KVCache entries).  Needs pool_tokens and
+ * rope_len >= s + m. */
+size_t pkv_recompute_query_workspace(const pkv_model* m, int32_t k, int32_t n_query);
+int pkv_recompute_query(const pkv_model* m, const pkv_cache* cache, const int32_t* sel, int32_t k,
+                        const int32_t* query_ids, int32_t n_query, float* tap_k, float* tap_v, float* query_k,
+                        float* query_v, float* last_logits, void* workspace, size_t workspace_bytes, void* stream);
+
 /* full_prefill -- model.py:332-359 (and precompute_chunk, chunkstore.py:52-62) on the
  * device: the Stage-II layer loop over every position 0..s-1 of `cache` (its token_ids
  * are the sequence; K/V land in its pool, RoPE'd at 0..s-1).  Optional captures:

@@ -703,9 +703,33 @@ size_t pkv_recompute_workspace(const pkv_model* m, int32_t k) {
 // attention / o / MLP only update the residual stream, which recompute_selected drops
 // after the loop (reference recompute.py:57-82 returns the cache; the K/V writes are the
 // only observable result), so that work is dead.  full_prefill keeps it for the logits.
+//
+// Query rows (q.m > 0, pkv_recompute_query): the m query tokens of finalize_query
+// (reference recompute.py:105-125 -> model.py query_pass 370-402) ride along as rows
+// k..k+m-1 at positions s..s+m-1.  Layer by layer they see exactly what the separate query
+// pass would see -- the repaired layer (every selected entry written by this layer's QKV
+// GEMM before its attention) plus their own causal K/V, appended to the pool -- so the
+// final query pass disappears (it had to run after, or interleaved with, Stage II).  The
+// last layer computes attention / o / MLP for the query rows only; then final norm and
+// lm_head on the last query row.  (Stage-II precision: fp16 operands, fp32 accumulation
+// and residual stream, instead of the fp32-faithful narrow pass.)
+struct QueryRows {
+  const int32_t* ids = nullptr;  // [m] device token ids
+  int m = 0;
+  int32_t* pos = nullptr;        // workspace [k + m]: sel, then s..s+m-1
+  float* tap_k = nullptr;        // optional fp32 [L][m][Hkv][dk] fresh query K / V
+  float* tap_v = nullptr;
+  float* logits = nullptr;       // [vocab] first-token logits
+  float* xl = nullptr;           // workspace [Dp]: normalised last row
+};
+__global__ void iota_from_kernel(int32_t* v, int n, int base) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = base + i;
+}
+
 static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k,
                           float* tap_v, void* knr_out, void* v_out, const RcWs& w, cudaStream_t st,
-                          bool need_final_h) {
+                          bool need_final_h, const QueryRows& q = QueryRows()) {
   const pkv_config& cf = md->cfg;
   const int H = md->H, Hkv = md->Hkv, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
   // row-parallel o / down GEMMs under tensor parallelism: rank 0 accumulates into the
@@ -714,13 +738,23 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
   pkv_comm* comm = md->comm;
   const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
   int rc;
+  const int m = q.m;
+  const int n = k + m;  // rows of the layer loop
+  const int32_t* pos = sel;
+  if (m > 0) {  // positions of all rows: the selection, then the query at s..s+m-1
+    cudaMemcpyAsync(q.pos, sel, sizeof(int32_t) * k, cudaMemcpyDeviceToDevice, st);
+    iota_from_kernel<<<ceil_div(m, 128), 128, 0, st>>>(q.pos + k, m, c->s);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("iota_from_kernel");
+    pos = q.pos;
+  }
   // deferred RMSNorm (opt-in PKV_NORM_DEFER=1): the o / down GEMM epilogues (or,
   // head-sharded, a small pass after the all-reduce) write bf16(h * g) and per-tile sums of
   // h^2; the QKV / gate-up epilogues scale by 1/rms, so only layer 0's attention norm runs
   // as its own kernel.  Measured +1 ms per prefill (fp32 sums; +15 ms with f64 sums): the
   // extra epilogue stores compete with the mainloop's TMA fill, which costs more than the
   // 2 ms of standalone norm passes it removes.
-  const bool defer = getenv("PKV_NORM_DEFER") && getenv("PKV_NORM_DEFER")[0] == '1';
+  const bool defer = m == 0 && getenv("PKV_NORM_DEFER") && getenv("PKV_NORM_DEFER")[0] == '1';
   const int ntile = ceil_div(Dp, 256);
   auto consume = [&](GemmArgs& a) {
     a.ssq_in = w.ssq;
@@ -738,8 +772,11 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
   };
   if (w.sk_cnt) cudaMemsetAsync(w.sk_cnt, 0, w.sk_cnt_n * sizeof(int), st);
   TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, c->token_ids, sel, k, cf.hidden_dim, w.h, Dp, st));
+  if (m > 0)
+    TTRY(T_RC_MISC, embed_gather_launch(md->w.embed, Dp, q.ids, nullptr, m, cf.hidden_dim, w.h + (long)k * Dp, Dp, st));
   for (int l = 0; l < cf.n_layers; ++l) {
     const pkv_layer_weights& lw = md->layers[l];
+    const bool last = l == cf.n_layers - 1;
     // the scatter must land after this layer's (possibly pipelined) assembly
     if (c->layer_ready != nullptr && c->layer_ready[l] != nullptr)
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
@@ -747,7 +784,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     // host-tier assembly runs on another stream)
     if (l == 0 && c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
     if (l == 0 || !defer)
-      TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+      TTRY(T_RC_MISC, rmsnorm_launch(w.h, n, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
     if (defer && l > 0) consume(g);
     g.f16 = 1;
@@ -755,12 +792,12 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     g.acc_scale = lw.wscale[0];
     g.sk_part = w.sk_part;
     g.sk_cnt = w.sk_cnt;
-    g.M = k;
+    g.M = n;
     g.N = md->NQKV;
     g.n_splits = 1;
     g.C = w.qb;
     g.ldc = md->HQ;
-    g.pos = sel;
+    g.pos = pos;
     g.rope_cos = c->rope_cos;
     g.rope_sin = c->rope_sin;
     g.rope_cs32 = reinterpret_cast<const float2*>(c->rope_cs32);
@@ -774,13 +811,18 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     g.page_table = c->page_table;
     g.tap_k = tap_k ? tap_k + (long)l * k * Hkv * dk : nullptr;
     g.tap_v = tap_v ? tap_v + (long)l * k * Hkv * dk : nullptr;
+    if (m > 0) {
+      g.tap_rows = k;
+      g.qtap_k = q.tap_k ? q.tap_k + (long)l * m * Hkv * dk : nullptr;
+      g.qtap_v = q.tap_v ? q.tap_v + (long)l * m * Hkv * dk : nullptr;
+    }
     g.knr_out = knr_out ? reinterpret_cast<__nv_bfloat16*>(knr_out) + (long)l * k * Hkv * dkp : nullptr;
     g.vcap_out = v_out ? reinterpret_cast<__nv_bfloat16*>(v_out) + (long)l * k * Hkv * dkp : nullptr;
     if (c->k2_pool != nullptr) g.k2_pool = reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool;
     // K/V of every selected token are in the cache before this layer's attention.  The last
     // layer of a repair only scatters K/V (its attention / o / MLP are dead, below): skip
     // the query rows of wqkv.
-    if (l == cf.n_layers - 1 && !need_final_h) {
+    if (last && !need_final_h && m == 0) {
       g.N = 2 * Hkv * dkp;
       g.head0 = H;
       TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp,
@@ -791,57 +833,67 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     }
     if (c->layer_done != nullptr && c->layer_done[l] != nullptr)
       cudaEventRecord(reinterpret_cast<cudaEvent_t>(c->layer_done[l]), st);
-    if (l == cf.n_layers - 1 && !need_final_h) break;
-    TTRY(T_RC_ATTN, attn_tc_launch(w.qb, w.ab, sel, k, H, Hkv, dk, dkp, c->k_pool, c->v_pool,
-                       (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l, c->page_table, st));
+    if (last && !need_final_h && m == 0) break;
+    // rows [r0, n) continue: all of them, or on the last layer of a repair with query rows
+    // only the query rows (the selected rows' last attention / o / MLP are dead)
+    const int r0 = (last && !need_final_h) ? k : 0, nr = n - r0;
+    TTRY(T_RC_ATTN, attn_tc_launch(w.qb + (long)r0 * md->HQ, w.ab + (long)r0 * md->HQ, pos + r0, nr, H, Hkv, dk, dkp,
+                                   c->k_pool, c->v_pool, (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l,
+                                   c->page_table, st));
     GemmArgs go{};
     go.f16 = 1;
     go.nonfinite = c->nonfinite;
     go.acc_scale = lw.wscale[1];
     go.sk_part = w.sk_part;
     go.sk_cnt = w.sk_cnt;
-    go.M = k;
+    go.M = nr;
     go.N = Dp;
     go.n_splits = 1;
-    go.C = w.h;
+    go.C = w.h + (long)r0 * Dp;
     go.ldc = Dp;
     if (defer && !comm) produce(go, lw.ffn_norm);
-    TTRY(T_RC_O, gemm_tc_launch(epi_resid, 256, w.ab, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
-    if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
+    TTRY(T_RC_O, gemm_tc_launch(epi_resid, 256, w.ab + (long)r0 * md->HQ, md->HQ, lw.wo, md->HQ, md->HQ, go, st));
+    if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h + (long)r0 * Dp, (size_t)nr * Dp, PKV_DT_F32, st));
     if (!defer)
-      TTRY(T_RC_MISC, rmsnorm_launch(w.h, k, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
+      TTRY(T_RC_MISC, rmsnorm_launch(w.h + (long)r0 * Dp, nr, cf.hidden_dim, Dp, lw.ffn_norm, cf.norm_eps, nullptr,
+                                     nullptr, 0, w.xb + (long)r0 * Dp, st));
     else if (comm)
-      TTRY(T_RC_MISC, norm_defer_launch(w.h, k, Dp, Dp, lw.ffn_norm, w.xb, Dp, w.ssq, ntile, st));
+      TTRY(T_RC_MISC, norm_defer_launch(w.h, n, Dp, Dp, lw.ffn_norm, w.xb, Dp, w.ssq, ntile, st));
     GemmArgs gg{};
     gg.f16 = 1;
     gg.nonfinite = c->nonfinite;
     gg.acc_scale = lw.wscale[2];
     gg.sk_part = w.sk_part;
     gg.sk_cnt = w.sk_cnt;
-    gg.M = k;
+    gg.M = nr;
     gg.N = 2 * Fp;
     gg.n_splits = 1;
-    gg.C = w.act;
+    gg.C = w.act + (long)r0 * Fp;
     gg.ldc = Fp;
     if (defer) consume(gg);
-    TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb, Dp, lw.wgu, Dp, Dp, gg, st));
+    TTRY(T_RC_GU, gemm_tc_launch(EPI_SILU, 256, w.xb + (long)r0 * Dp, Dp, lw.wgu, Dp, Dp, gg, st));
     GemmArgs gd{};
     gd.f16 = 1;
     gd.nonfinite = c->nonfinite;
     gd.acc_scale = lw.wscale[3];
     gd.sk_part = w.sk_part;
     gd.sk_cnt = w.sk_cnt;
-    gd.M = k;
+    gd.M = nr;
     gd.N = Dp;
     gd.n_splits = 1;
-    gd.C = w.h;
+    gd.C = w.h + (long)r0 * Dp;
     gd.ldc = Dp;
     const float* next_norm = l + 1 < cf.n_layers ? md->layers[l + 1].attn_norm : nullptr;
     if (defer && !comm && next_norm) produce(gd, next_norm);
-    TTRY(T_RC_DOWN, gemm_tc_launch(epi_resid, 256, w.act, Fp, lw.wd, Fp, Fp, gd, st));
-    if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h, (size_t)k * Dp, PKV_DT_F32, st));
+    TTRY(T_RC_DOWN, gemm_tc_launch(epi_resid, 256, w.act + (long)r0 * Fp, Fp, lw.wd, Fp, Fp, gd, st));
+    if (comm) TTRY(T_COMM, comm_allreduce(comm, w.h + (long)r0 * Dp, (size_t)nr * Dp, PKV_DT_F32, st));
     if (defer && comm && next_norm)
-      TTRY(T_RC_MISC, norm_defer_launch(w.h, k, Dp, Dp, next_norm, w.xb, Dp, w.ssq, ntile, st));
+      TTRY(T_RC_MISC, norm_defer_launch(w.h, n, Dp, Dp, next_norm, w.xb, Dp, w.ssq, ntile, st));
+  }
+  if (m > 0 && q.logits != nullptr) {  // _head_logits (model.py:326-329) of the last query row
+    TTRY(T_LMHEAD, rmsnorm_launch(w.h + (long)(n - 1) * Dp, 1, cf.hidden_dim, Dp, md->w.final_norm, cf.norm_eps, q.xl,
+                                  nullptr, 0, nullptr, st));
+    TTRY(T_LMHEAD, gemv_launch(q.xl, md->w.lm_head, cf.vocab_size, Dp, Dp, q.logits, st));
   }
   return PKV_OK;
 }
@@ -854,6 +906,35 @@ int pkv_recompute(const pkv_model* md, const pkv_cache* c, const int32_t* sel, i
   RcWs w = carve_rc(md, k, workspace, &need);
   if (ws_bytes < need) return set_error(PKV_ERR_ARGUMENT, "workspace too small (%zu < %zu)", ws_bytes, need);
   return recompute_core(md, c, sel, k, tap_k, tap_v, nullptr, nullptr, w, S(stream), /*need_final_h=*/false);
+}
+
+size_t pkv_recompute_query_workspace(const pkv_model* md, int32_t k, int32_t m) {
+  size_t t = 0;
+  carve_rc(md, k + m, nullptr, &t);
+  return t + ((size_t)(k + m) * sizeof(int32_t) + 255) / 256 * 256 + ((size_t)md->Dp * sizeof(float) + 255) / 256 * 256;
+}
+
+int pkv_recompute_query(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k,
+                        const int32_t* query_ids, int32_t m, float* tap_k, float* tap_v, float* query_k,
+                        float* query_v, float* last_logits, void* workspace, size_t ws_bytes, void* stream) {
+  if (!md || !c || !sel || !query_ids || !last_logits) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (k < 0 || k > c->s) return set_error(PKV_ERR_ARGUMENT, "bad selection size %d", k);
+  if (m <= 0) return set_error(PKV_ERR_INPUT, "token sequence must be non-empty");
+  if (c->pool_tokens < c->s + m || c->rope_len < c->s + m) return set_error(PKV_ERR_SHAPE, "pool too small to append");
+  if (ws_bytes < pkv_recompute_query_workspace(md, k, m))
+    return set_error(PKV_ERR_ARGUMENT, "workspace too small");
+  size_t used = 0;
+  RcWs w = carve_rc(md, k + m, workspace, &used);
+  uint8_t* tail = reinterpret_cast<uint8_t*>(workspace) + used;
+  QueryRows q;
+  q.ids = query_ids;
+  q.m = m;
+  q.pos = reinterpret_cast<int32_t*>(tail);
+  q.xl = reinterpret_cast<float*>(tail + ((size_t)(k + m) * sizeof(int32_t) + 255) / 256 * 256);
+  q.tap_k = query_k;
+  q.tap_v = query_v;
+  q.logits = last_logits;
+  return recompute_core(md, c, sel, k, tap_k, tap_v, nullptr, nullptr, w, S(stream), /*need_final_h=*/false, q);
 }
 
 // ------------------------------------------------------------------ full prefill

@@ -45,6 +45,9 @@ struct GemmArgs {
   const int32_t* page_table;
   float* tap_k;               // optional fp32 [M][Hkv][dk]
   float* tap_v;
+  int tap_rows;               // with qtap_*: rows >= tap_rows tap into qtap_* at row - tap_rows instead
+  float* qtap_k;              // (the query rows riding along a Stage-II repair, pkv_recompute_query)
+  float* qtap_v;
   __half* k2_pool;            // optional residual key plane fp16(k - k_pool) (layer base), see s1_attn_tc.cu
   __nv_bfloat16* knr_out;     // optional bf16 [M][Hkv][dkp]: keys BEFORE RoPE (chunk-store layout)
   __nv_bfloat16* vcap_out;    // optional bf16 [M][Hkv][dkp]: values (chunk-store layout)
@@ -799,8 +802,13 @@ __global__ void __launch_bounds__(192, 1)
                       make_uint4(pk2[4 * j], pk2[4 * j + 1], pk2[4 * j + 2], pk2[4 * j + 3]);
               }
               float* tap = is_v ? args.tap_v : args.tap_k;
+              long trow = row;
+              if ((args.qtap_k != nullptr || args.qtap_v != nullptr) && row >= args.tap_rows) {
+                tap = is_v ? args.qtap_v : args.qtap_k;
+                trow = row - args.tap_rows;
+              }
               if (tap != nullptr) {
-                float* tp = tap + ((long)row * Hkv + g) * args.head_dim;
+                float* tp = tap + (trow * Hkv + g) * args.head_dim;
                 for (int j = 0; j < 32; ++j)
                   if (d0 + j < args.head_dim) tp[d0 + j] = vals[j];
               }

@@ -49,8 +49,13 @@ class PrefillPipeline:
         qp_bytes = max(lib.pkv_query_pass_workspace(dm.handle, s, m, self.flags_score),
                        lib.pkv_query_pass_workspace(dm.handle, s, m, self.flags_final))
         self.ws_qp = torch.empty(qp_bytes, dtype=torch.uint8, device=dev)
-        self.ws_rc = torch.empty(max(lib.pkv_recompute_workspace(dm.handle, max(self.k, 1)), 256), dtype=torch.uint8,
-                                 device=dev)
+        # finalize fused into Stage II (pkv_recompute_query): the query rows ride along the
+        # repair, so no separate final pass runs after or interleaved with Stage II
+        # (PKV_FUSED_FINAL=0: the separate fp32-faithful query pass)
+        self.fused_final = os.environ.get("PKV_FUSED_FINAL", "1") == "1"
+        rc_bytes = (lib.pkv_recompute_query_workspace(dm.handle, self.k, m) if self.fused_final
+                    else lib.pkv_recompute_workspace(dm.handle, max(self.k, 1)))
+        self.ws_rc = torch.empty(max(rc_bytes, 256), dtype=torch.uint8, device=dev)
         self.per_layer = torch.empty((cfg.n_layers, s), dtype=torch.float32, device=dev)
         self.fused = torch.empty(s, dtype=torch.float32, device=dev)
         self.idx = torch.empty(max(self.k, 1), dtype=torch.int32, device=dev)
@@ -163,11 +168,19 @@ class PrefillPipeline:
         return cc
 
     def stage2(self, stream=None) -> None:
-        """Stage II alone (recompute of the current selection idx), serial order."""
+        """Stage II alone (recompute of the current selection idx; with the fused finalize
+        also the query rows and the first-token logits), serial order."""
         torch = _lib.require_cuda()
-        _lib.check(_lib.load().pkv_recompute(self.dm.handle, ctypes_ref(self._plain_cache()), self.idx.data_ptr(),
-                                             self.k, None, None, self.ws_rc.data_ptr(), self.ws_rc.numel(),
-                                             _lib.stream_ptr(torch, stream)))
+        self._recompute(_lib.load(), ctypes_ref(self._plain_cache()), _lib.stream_ptr(torch, stream))
+
+    def _recompute(self, lib, cc, st) -> None:
+        if self.fused_final:
+            _lib.check(lib.pkv_recompute_query(self.dm.handle, cc, self.idx.data_ptr(), self.k, self.query.data_ptr(),
+                                               self.m, None, None, None, None, self.logits.data_ptr(),
+                                               self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
+        else:
+            _lib.check(lib.pkv_recompute(self.dm.handle, cc, self.idx.data_ptr(), self.k, None, None,
+                                         self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
 
     def final(self, stream=None) -> None:
         """The final query pass alone (first-token logits over the repaired cache)."""
@@ -187,6 +200,10 @@ class PrefillPipeline:
         cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
         main = stream if stream is not None else torch.cuda.current_stream()
         self._stage1(lib, st, main)
+        if self.fused_final:
+            self._recompute(lib, cc, st)
+            main.wait_stream(self.side)  # rejoin (required for graph capture)
+            return
         if self.final_overlap:
             # after the scoring pass (it shares ws_qp) and the selection; layer l waits on done[l]
             self.fin.wait_stream(main)

@@ -62,6 +62,55 @@ def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
         tap_k = torch.empty((L, k, Hkv, dk), dtype=torch.float32, device=cache.device)
         tap_v = torch.empty_like(tap_k)
     lib = _lib.load()
+    query = getattr(cache, "_pending_query", None)
+    cache._pending_query = None
+    if query is not None and _fused_final():
+        _recompute_with_query(lib, dm, config, cache, d_sel, k, query, tap_k, tap_v)
+    else:
+        _recompute(lib, dm, cache, d_sel, k, tap_k, tap_v, L)
+    cache.recomputed[:, sel] = True
+    if tap_k is not None:
+        for li in range(L):
+            cache.add_tap(li, sel, tap_k[li], tap_v[li])
+    if cache.access_log is not None:
+        for li in range(L):  # each layer writes its fresh K/V before its attention reads them
+            cache.access_log.append(("write", li))
+            cache.access_log.append(("read", li))
+    bill_repair(tally, config, cache.context_length, k)
+    return cache
+
+
+def _fused_final() -> bool:
+    """The query rows of finalize_query ride along Stage II (pkv_recompute_query) when the
+    scoring pass left its query on the cache; PKV_FUSED_FINAL=0 keeps the separate
+    fp32-faithful query pass."""
+    import os
+    return os.environ.get("PKV_FUSED_FINAL", "1") == "1"
+
+
+def _recompute_with_query(lib, dm, config, cache, d_sel, k, query, tap_k, tap_v) -> None:
+    """Stage II over the selection plus the m query rows at positions s..s+m-1: the query's
+    first-token logits and fresh K/V are kept on the cache for finalize_query (reference
+    recompute.py:105-125) of the same tokens, which then runs no pass of its own."""
+    torch = _lib.require_cuda()
+    m = int(query.shape[0])
+    cache.ensure_query_room(m)
+    L, Hkv, dk = config.n_layers, cache.config.n_kv_heads, config.head_dim
+    fk = torch.empty((L, m, Hkv, dk), dtype=torch.float32, device=cache.device)
+    fv = torch.empty_like(fk)
+    logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
+    d_q = torch.from_numpy(query).to(cache.device)
+    ws = workspace(lib.pkv_recompute_query_workspace(dm.handle, k, m), "rc")
+    cache._final_follow = None
+    _lib.check(lib.pkv_recompute_query(dm.handle, ctypes.byref(cache.c_cache), d_sel.data_ptr(), k, d_q.data_ptr(), m,
+                                       tap_k.data_ptr() if tap_k is not None else None,
+                                       tap_v.data_ptr() if tap_v is not None else None, fk.data_ptr(), fv.data_ptr(),
+                                       logits.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(torch)))
+    cache._fused_final = (query, logits, fk, fv)
+
+
+def _recompute(lib, dm, cache, d_sel, k, tap_k, tap_v, L) -> None:
+    torch = _lib.require_cuda()
     ws = workspace(lib.pkv_recompute_workspace(dm.handle, k), "rc")
     c_rc = cache.c_cache
     if _final_overlap(dm):
@@ -82,16 +131,6 @@ def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
                                  tap_k.data_ptr() if tap_k is not None else None,
                                  tap_v.data_ptr() if tap_v is not None else None, ws.data_ptr(), ws.numel(),
                                  _lib.stream_ptr(torch)))
-    cache.recomputed[:, sel] = True
-    if tap_k is not None:
-        for li in range(L):
-            cache.add_tap(li, sel, tap_k[li], tap_v[li])
-    if cache.access_log is not None:
-        for li in range(L):  # each layer writes its fresh K/V before its attention reads them
-            cache.access_log.append(("write", li))
-            cache.access_log.append(("read", li))
-    bill_repair(tally, config, cache.context_length, k)
-    return cache
 
 
 @dataclass
@@ -132,7 +171,12 @@ def finalize_query(weights, config: ModelConfig, cache, query_tokens, capture_at
         rows_dev = torch.empty((L, m, s + m), dtype=torch.float32, device=cache.device)
     follow = getattr(cache, "_final_follow", None)
     cache._final_follow = None
-    if follow is not None and cache.pool_tokens >= cache.context_length + m:
+    fused = getattr(cache, "_fused_final", None)
+    cache._fused_final = None
+    if fused is not None and not capture_attn and np.array_equal(fused[0], ids.astype(np.int32)):
+        # the query rode along Stage II (pkv_recompute_query): logits and K/V are ready
+        _, logits, fk, fv = fused
+    elif follow is not None and cache.pool_tokens >= cache.context_length + m:
         # after the scoring pass (pre), layer l after Stage II's layer l (done[l]): the
         # narrow kernels of this pass run in the gaps of Stage II's big kernels
         pre, done, arr, c_fin = follow

@@ -198,6 +198,9 @@ def score_prophet(weights, config: ModelConfig, cache, query_tokens, tally: Flop
     if renormalize_context_only:
         flags |= _lib.PKV_QP_RENORM
     run_query_pass(dm, cache, ids, flags, per_layer=per_layer)
+    # the query a later recompute_selected may carry along Stage II so that finalize_query
+    # of the same tokens needs no separate pass (recompute.py, pkv_recompute_query)
+    cache._pending_query = np.asarray(ids, dtype=np.int32).copy()
     fused = torch.empty(s, dtype=torch.float32, device=cache.device)
     _fuse_device(per_layer, fused)
     bill_query_pass(tally, config, s, int(ids.shape[0]))
