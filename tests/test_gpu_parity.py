@@ -219,6 +219,7 @@ def test_final_pass_following_stage2_is_identical(built, monkeypatch):
     cfg_o, seed, units, query, p = _materialise("llama_width")
     w, chunks = _setup(cfg_o, seed, units, query)
     cfg, mw, dch = _device_inputs(P, cfg_o, w, chunks)
+    monkeypatch.setenv("PKV_FUSED_FINAL", "0")  # the separate final pass (the fused one has none)
     runs = []
     for ov in ("0", "1"):
         monkeypatch.setenv("PKV_FINAL_OVERLAP", ov)
@@ -245,6 +246,59 @@ def test_final_pass_following_stage2_is_identical(built, monkeypatch):
         torch.cuda.synchronize()
         outs.append((pipe.idx.clone(), pipe.logits.clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("case", ["c1", "llama_width"])
+def test_fused_finalize_matches_separate_pass(built, monkeypatch, case):
+    """The query rows riding along Stage II (pkv_recompute_query, default) against the
+    separate fp32-faithful final pass (PKV_FUSED_FINAL=0): the repaired context entries are
+    bit-identical (each row of a GEMM / attention tile is computed independently of the rows
+    added after it), the first-token logits and the appended query K/V agree within the
+    contract, and both agree with the oracle -- through the public API and the pipeline."""
+    import torch
+
+    from paper_2602_02579_b200.pipeline import PrefillPipeline
+    P = built
+    cfg_o, seed, units, query, p = _materialise(case)
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg, mw, dch = _device_inputs(P, cfg_o, w, chunks)
+    ref = O.prophet_ttft_slice(w, cfg_o, chunks, query, p)
+    runs = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("PKV_FUSED_FINAL", fused)
+        cache = P.assemble(dch, cfg, fp32_taps=False)
+        sc = P.score_prophet(mw, cfg, cache, query)
+        sel = P.select_top_p(sc, p)
+        P.recompute_selected(mw, cfg, cache, P.RecomputePlan(sel))
+        fin = P.finalize_query(mw, cfg, cache, query)
+        torch.cuda.synchronize()
+        s, m = cache.context_length, len(query)
+        runs.append((sel.indices, fin.first_logits, cache.k_pool[:, :, :s].clone(), cache.v_pool[:, :, :s].clone(),
+                     cache.k_pool[:, :, s:s + m].float().clone(), fin.cache.keys, fin.cache.values))
+    assert runs[0][0] == runs[1][0]
+    assert torch.equal(runs[0][2], runs[1][2]) and torch.equal(runs[0][3], runs[1][3])
+    for lg in (runs[0][1], runs[1][1]):
+        assert np.abs(lg - ref["first_logits"]).max() <= KV_ABS and _cos(lg, ref["first_logits"]) >= COS_MIN
+    assert float((runs[0][4] - runs[1][4]).abs().max()) <= KV_ABS
+    for li in range(cfg.n_layers):  # the reference KVCache view: context + query rows
+        assert np.abs(runs[0][5][li] - runs[1][5][li]).max() <= KV_ABS
+        assert np.abs(runs[0][6][li] - runs[1][6][li]).max() <= KV_ABS
+    _report(case=f"{case}_fused_final", logits_fused_max_abs=float(np.abs(runs[1][1] - ref["first_logits"]).max()),
+            logits_separate_max_abs=float(np.abs(runs[0][1] - ref["first_logits"]).max()))
+
+    dm = P.DeviceModel.from_host(mw, cfg)
+    outs = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("PKV_FUSED_FINAL", fused)
+        pipe = PrefillPipeline(dm, dch, len(query), p)
+        pipe.set_query(query)
+        pipe.step()
+        pipe.capture()
+        pipe.replay()
+        torch.cuda.synchronize()
+        outs.append((pipe.idx.clone(), pipe.logits.cpu().numpy()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert np.abs(outs[1][1] - ref["first_logits"]).max() <= KV_ABS
 
 
 def test_deferred_norm_matches_standalone_norm(built, monkeypatch):
