@@ -15,10 +15,14 @@ Multi-GPU (one process per GPU; `--gpus N` starts torchrun itself when WORLD_SIZ
             the N GPUs (tensor parallel, paper_2602_02579_b200.tp): per-layer NCCL sums of
             the per-token score partials before the global top-k and of the o/down
             projection outputs; value = s / TTFT (strong scaling)
+  tokens    one 32k request: every GPU holds the full model and cache and scores the whole
+            request (replicated), Stage II repairs each GPU's share of the selected rows
+            and all-gathers the fresh cache entries per layer (DeviceModel.rows); value =
+            s / TTFT (strong scaling)
   requests  (configs[4]-style) one independent request per GPU, no data-path
             collective; value = N * s / TTFT (weak scaling)
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode heads|requests]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode heads|tokens|requests]
 """
 
 from __future__ import annotations
@@ -197,13 +201,15 @@ def cpu_threads():
     return info
 
 
-def arm_config(args, cfgd, world, heads):
+def arm_config(args, cfgd, world, heads, tokens=False):
     """The `config` dict of a bench line -- identical for our arm and the reference arm."""
     s = cfgd["n_chunks"] * cfgd["chunk_len"]
     return {"workload": args.config, "model": "Llama-3-8B shape" if "llama" in args.config else "Mistral-7B shape",
             "s": s, "chunks": cfgd["n_chunks"], "chunk_len": cfgd["chunk_len"], "m": args.m, "p": args.p,
             "k": math.ceil(args.p * s),
-            "parallelism": f"tp{world} (KV-head sharded, NCCL)" if heads else f"request-dp{world}",
+            "parallelism": (f"tp{world} (KV-head sharded, NCCL)" if heads else
+                            f"tokens{world} (scoring replicated, Stage II token-parallel, NCCL all-gather)"
+                            if tokens else f"request-dp{world}"),
             "inputs": f"SYN1 seed 0 (weights, chunk store, query: paper_2602_02579_b200/synthetic.py)"
             if args.chunks == "synthetic" else "SYN1 weights; chunk K/V precomputed on the GPU",
             "l2": "inputs larger than L2 (16 GB weights, 4.3 GB KV)"}
@@ -315,7 +321,8 @@ def run_reference(args, cfgd, rank, world):
     line = {"impl": "reference", "metric": metric_name(cfgd, args.p), "value": value, "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft * 1e3, "ttft_ms": ttft * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 accumulate)",
-            "data": "synthetic", "config": arm_config(args, cfgd, world, mode == "heads" and world > 1),
+            "data": "synthetic", "config": arm_config(args, cfgd, world, mode == "heads" and world > 1,
+                                                      mode == "tokens" and world > 1),
             "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port", "threads": cpu_threads(),
                              "sample": f"oracle port of pikv, 1 layer at full width and s={s}, Stage II on {n_s} "
                                        f"of k={k} rows, extrapolated x{cfgd['n_layers']} layers and k/{n_s} rows; "
@@ -338,7 +345,7 @@ def main():
     ap.add_argument("--full-steps", type=int, default=1, help="full-prefill comparator runs (0: skip)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=128)
-    ap.add_argument("--mode", default="auto", choices=["auto", "heads", "requests"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "heads", "tokens", "requests"])
     ap.add_argument("--p-sweep", default="0.05,0.1,0.2,0.4", help="recompute ratios of the sweep ('' = skip)")
     ap.add_argument("--sweep-steps", type=int, default=3)
     ap.add_argument("--chunks", default="synthetic", choices=["synthetic", "precompute"])
@@ -358,8 +365,10 @@ def main():
 
     mode = args.mode if args.mode != "auto" else ("heads" if world > 1 else "requests")
     heads = mode == "heads" and world > 1
+    tokens = mode == "tokens" and world > 1
+    shared = heads or tokens  # one request over all ranks (strong scaling)
     nccl_log = None
-    if heads:  # NCCL init / NVLS lines of this rank (summarised in the JSON line)
+    if shared:  # NCCL init / NVLS lines of this rank (summarised in the JSON line)
         out_dir = ROOT / "gpurun_out" if (ROOT / "gpurun_out").is_dir() else Path("/tmp")
         nccl_log = out_dir / f"nccl_rank{rank}.log"
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -408,6 +417,16 @@ def main():
         chunks = tp.shard_chunks(full_chunks, rank, world)
         del full_chunks
         torch.cuda.empty_cache()
+        qseed = 0
+    elif tokens:
+        # one request: every rank holds the full SYN1 model and chunk store, scores the whole
+        # request (replicated, deterministic -> identical selections) and repairs its share of
+        # the selected rows (DeviceModel.rows, pkv_recompute_rows)
+        from paper_2602_02579_b200 import tp
+        comm = tp.nccl_comm()
+        full = P.DeviceModel.synthetic(cfg, seed=0)
+        chunks = make_chunks(full, 0)
+        dm = full.rows(comm)
         qseed = 0
     else:
         dm = P.DeviceModel.synthetic(cfg, seed=0)
@@ -476,7 +495,7 @@ def main():
     ms = pdist.max_over_ranks(ms, device="cuda")
     if world > 1:
         dist.barrier()
-    value = (1 if heads else world) * s / (ms / 1e3)
+    value = (1 if shared else world) * s / (ms / 1e3)
 
     # ---- parity of this very run against the oracle fixture (rank 0's request)
     anchor = load_anchor(args, heads) if rank == 0 else None
@@ -508,6 +527,10 @@ def main():
     idx = pipe.idx[: pipe.k].cpu().numpy().astype(np.int64)
     k = pipe.k
     # per-rank work: this rank's heads / ffn slice when head-sharded
+    if tokens:  # this rank's share of the selected rows (pkv_recompute_rows' unit assignment)
+        from paper_2602_02579_b200 import tp as _tp
+        idx = idx[_tp.rows_share(k, cfg.n_heads // cfg.n_kv_heads, world, rank)]
+        k = int(idx.size)
     lcfg = dm.cache_config
     L, H, Hkv, dk, D = cfg.n_layers, lcfg.n_heads, lcfg.n_kv_heads, cfg.head_dim, cfg.hidden_dim
     F = cfg.ffn_dim // dm.tp_world
@@ -549,12 +572,12 @@ def main():
 
     line = {"metric": metric_name(cfgd, args.p), "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "ttft_ms": ms, "higher_is_better": True,
-            "scaling": "strong" if heads else "weak",
+            "scaling": "strong" if shared else "weak",
             "vs_baseline": None, "dtype": "fp16 (Stage II, fp32 accumulate) / fp32-faithful (narrow passes)",
             "data": ("synthetic: SYN1 random-init weights (reference init scale), token ids and chunk K/V, "
                      "reproduced bit for bit by the CPU oracle" if args.chunks == "synthetic" else
                      "synthetic: SYN1 random-init weights and token ids; chunk K/V precomputed on the GPU"),
-            "config": arm_config(args, cfgd, world, heads),
+            "config": arm_config(args, cfgd, world, heads, tokens),
             "gpu_launches": int(n_launch), "launch_mode": launch_mode,
             "clocks": clk, "roofline": roof,
             "ttft_floor_ms": round(floor, 2), "ttft_floor_frac": round(floor / ms, 4),
@@ -650,7 +673,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = pdist.max_over_ranks((time.perf_counter() - t0) * 1e3 / args.e2e_steps, device="cuda")
         d2h = L * s * 4 + s * 4 + k * 4 + cfg.vocab_size * 4
-        line["e2e"] = {"value": (1 if heads else world) * s / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
+        line["e2e"] = {"value": (1 if shared else world) * s / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
                        "h2d_bytes_per_step": int(h2d + args.m * 8), "d2h_bytes_per_step": int(d2h),
                        "path": "assemble -> score_prophet -> select_top_p -> recompute_selected -> finalize_query, "
                                "chunk K/V copied from pinned host memory each step (layer-pipelined with "

@@ -261,6 +261,22 @@ int pkv_comm_rank(const pkv_comm* c);
 int pkv_comm_world(const pkv_comm* c);
 void pkv_comm_destroy(pkv_comm* c);
 
+/* Token-parallel Stage II over the W ranks of `comm` (one process per GPU, every rank holding
+ * the UNSHARDED model and a full assembled cache; multi-GPU alternative to head sharding,
+ * SURVEY §8(e)).  No reference counterpart (single-process numpy).  sel: the global selection
+ * (identical on every rank: the scoring pass is replicated and deterministic).  Rank r
+ * repairs the attention units (128/G consecutive selected rows) r, r+W, r+2W, ...; after
+ * each layer's QKV GEMM the ranks all-gather the fresh cache entries of their rows (fp16 K,
+ * K residual, V: 6 KB per row at Llama width) and scatter the peers' into their own pools,
+ * so the attention of every rank reads the whole repaired layer and all ranks end with the
+ * identical cache -- one all-gather of ~40 MB per layer instead of two [k][D] fp32
+ * all-reduces.  m > 0: the query rows ride along on every rank (as pkv_recompute_query)
+ * and last_logits gets the first-token logits. */
+size_t pkv_recompute_rows_workspace(const pkv_model* m, int32_t k, int32_t n_query, int32_t world);
+int pkv_recompute_rows(const pkv_model* m, const pkv_cache* cache, const int32_t* sel, int32_t k,
+                       const int32_t* query_ids, int32_t n_query, pkv_comm* comm, float* last_logits,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
 /* cfg is the FULL model config; w holds rank tp_rank's weight shard (layouts
  * above with the local head / ffn counts).  comm may be NULL iff tp_world == 1. */
 int pkv_model_create_sharded(const pkv_config* cfg, const pkv_weights* w, int32_t tp_rank, int32_t tp_world,

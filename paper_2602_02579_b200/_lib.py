@@ -75,6 +75,9 @@ _SIGS = {
     "pkv_recompute_query_workspace": (c_sz, [c_vp, c_i32, c_i32]),
     "pkv_recompute_query": (c_i32, [c_vp, ctypes.POINTER(Cache), c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                     c_vp, c_sz, c_vp]),
+    "pkv_recompute_rows_workspace": (c_sz, [c_vp, c_i32, c_i32, c_i32]),
+    "pkv_recompute_rows": (c_i32, [c_vp, ctypes.POINTER(Cache), c_vp, c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_sz,
+                                   c_vp]),
     "pkv_full_prefill_workspace": (c_sz, [c_vp, c_i32]),
     "pkv_full_prefill": (c_i32, [c_vp, ctypes.POINTER(Cache), c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "pkv_replace_entries": (c_i32, [ctypes.POINTER(Config), ctypes.POINTER(Cache), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp]),

@@ -722,6 +722,47 @@ struct QueryRows {
   float* logits = nullptr;       // [vocab] first-token logits
   float* xl = nullptr;           // workspace [Dp]: normalised last row
 };
+// Token-parallel Stage II (pkv_recompute_rows): rank r of W repairs the 128/G-row attention
+// units r, r+W, r+2W, ... of the selection with the full model; after each layer's QKV GEMM
+// the ranks all-gather the fresh cache entries of their rows (fp16 K, K residual, V) and
+// scatter the others' into their own pools, so every rank's attention reads the whole
+// repaired layer and every rank ends with the identical repaired cache.
+struct RowsMode {
+  pkv_comm* comm = nullptr;           // null: off
+  const int32_t* sel_global = nullptr;
+  int k_global = 0, T = 32, kmax = 0;
+  __half* kvc = nullptr;              // [kmax + m][3][Hkv][dkp] this rank's rows
+  __half* recv = nullptr;             // [W][kmax][3][Hkv][dkp]
+};
+__host__ __device__ inline int rows_global(int j, int i, int W, int T) { return (j + W * (i / T)) * T + i % T; }
+__global__ void rows_local_kernel(const int32_t* sel, int T, int W, int r, int kr, int32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < kr) out[i] = sel[rows_global(r, i, W, T)];
+}
+__global__ void rows_scatter_kernel(const uint4* __restrict__ recv, int W, int kmax, int me, const int32_t* sel, int k,
+                                    int T, int Hkv, int dkp, const int32_t* page_table, long pool_tokens, __half* kp,
+                                    __half* k2p, __half* vp) {
+  const int vpr = 3 * Hkv * dkp / 8;  // 16-byte vectors per row
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)W * kmax * vpr) return;
+  const int j = (int)(gid / ((long)kmax * vpr));
+  const long rem = gid - (long)j * kmax * vpr;
+  const int i = (int)(rem / vpr), v = (int)(rem - (long)i * vpr);
+  if (j == me) return;
+  const int g = rows_global(j, i, W, T);
+  if (g >= k) return;
+  const int plane = v / (Hkv * dkp / 8), h = (v / (dkp / 8)) % Hkv, c = v % (dkp / 8);
+  __half* base = plane == 0 ? kp : plane == 1 ? k2p : vp;
+  if (base == nullptr) return;
+  const int pos = sel[g];
+  const long slot = (long)page_table[pos >> 7] * 128 + (pos & 127);
+  reinterpret_cast<uint4*>(base + ((long)h * pool_tokens + slot) * dkp)[c] = recv[gid];
+}
+static void rows_counts(int k, int T, int W, int* kr) {  // rows per rank
+  for (int j = 0; j < W; ++j) kr[j] = 0;
+  for (int u = 0; u * T < k; ++u) kr[u % W] += std::min(T, k - u * T);
+}
+
 __global__ void iota_from_kernel(int32_t* v, int n, int base) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = base + i;
@@ -729,7 +770,7 @@ __global__ void iota_from_kernel(int32_t* v, int n, int base) {
 
 static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k, float* tap_k,
                           float* tap_v, void* knr_out, void* v_out, const RcWs& w, cudaStream_t st,
-                          bool need_final_h, const QueryRows& q = QueryRows()) {
+                          bool need_final_h, const QueryRows& q = QueryRows(), const RowsMode& rows = RowsMode()) {
   const pkv_config& cf = md->cfg;
   const int H = md->H, Hkv = md->Hkv, dk = cf.head_dim, dkp = md->dkp, Dp = md->Dp, Fp = md->Fp;
   // row-parallel o / down GEMMs under tensor parallelism: rank 0 accumulates into the
@@ -782,7 +823,9 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
       cudaStreamWaitEvent(st, reinterpret_cast<cudaEvent_t>(c->layer_ready[l]), 0);
     // the repaired-entry flags: after layer 0's assembly, which clears them (a pipelined
     // host-tier assembly runs on another stream)
-    if (l == 0 && c->recomputed) TTRY(T_RC_MISC, mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
+    if (l == 0 && c->recomputed)
+      TTRY(T_RC_MISC, rows.comm ? mark_launch(rows.sel_global, rows.k_global, const_cast<uint8_t*>(c->recomputed), st)
+                                : mark_launch(sel, k, const_cast<uint8_t*>(c->recomputed), st));
     if (l == 0 || !defer)
       TTRY(T_RC_MISC, rmsnorm_launch(w.h, n, cf.hidden_dim, Dp, lw.attn_norm, cf.norm_eps, nullptr, nullptr, 0, w.xb, st));
     GemmArgs g{};
@@ -819,6 +862,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     g.knr_out = knr_out ? reinterpret_cast<__nv_bfloat16*>(knr_out) + (long)l * k * Hkv * dkp : nullptr;
     g.vcap_out = v_out ? reinterpret_cast<__nv_bfloat16*>(v_out) + (long)l * k * Hkv * dkp : nullptr;
     if (c->k2_pool != nullptr) g.k2_pool = reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool;
+    g.kvc = rows.kvc;
     // K/V of every selected token are in the cache before this layer's attention.  The last
     // layer of a repair only scatters K/V (its attention / o / MLP are dead, below): skip
     // the query rows of wqkv.
@@ -830,6 +874,19 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
                                     st));
     } else {
       TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
+    }
+    if (rows.comm) {  // every rank's fresh entries of this layer into every pool
+      const size_t bytes = (size_t)rows.kmax * 3 * Hkv * dkp * sizeof(__half);
+      TTRY(T_COMM, comm_allgather(rows.comm, rows.kvc, rows.recv, bytes, st));
+      const int W = comm_world(rows.comm);
+      const long nvec = (long)W * rows.kmax * 3 * Hkv * dkp / 8;
+      if (nvec > 0) {
+        rows_scatter_kernel<<<ceil_div(nvec, 256), 256, 0, st>>>(
+            reinterpret_cast<const uint4*>(rows.recv), W, rows.kmax, comm_rank(rows.comm), rows.sel_global,
+            rows.k_global, rows.T, Hkv, dkp, c->page_table, c->pool_tokens, g.k_pool, g.k2_pool, g.v_pool);
+        PKV_LAUNCHED();
+        PKV_CHECK_LAUNCH("rows_scatter_kernel");
+      }
     }
     if (c->layer_done != nullptr && c->layer_done[l] != nullptr)
       cudaEventRecord(reinterpret_cast<cudaEvent_t>(c->layer_done[l]), st);
@@ -935,6 +992,75 @@ int pkv_recompute_query(const pkv_model* md, const pkv_cache* c, const int32_t* 
   q.tap_v = query_v;
   q.logits = last_logits;
   return recompute_core(md, c, sel, k, tap_k, tap_v, nullptr, nullptr, w, S(stream), /*need_final_h=*/false, q);
+}
+
+// token-parallel workspace: Stage-II buffers for kmax + m rows, positions, the normalised
+// last row, the local selection, this rank's compact entries and the gathered ones
+static size_t rows_ws(const pkv_model* md, int k, int m, int world, RcWs* w, QueryRows* q, RowsMode* rm,
+                      int32_t** local, void* base) {
+  const int G = md->H / md->Hkv, T = std::max(1, 128 / std::max(1, G));
+  std::vector<int> kr(std::max(1, world));
+  rows_counts(k, T, std::max(1, world), kr.data());
+  const int kmax = *std::max_element(kr.begin(), kr.end());
+  size_t used = 0;
+  RcWs ww = carve_rc(md, kmax + m, base, &used);
+  Carver cv{reinterpret_cast<uint8_t*>(base), used, 0};
+  int32_t* pos = cv.take<int32_t>((size_t)kmax + m);
+  float* xl = cv.take<float>((size_t)md->Dp);
+  int32_t* loc = cv.take<int32_t>((size_t)std::max(kmax, 1));
+  const size_t row_elems = (size_t)3 * md->Hkv * md->dkp;
+  __half* kvc = cv.take<__half>((size_t)(kmax + m) * row_elems);
+  __half* recv = cv.take<__half>((size_t)std::max(1, world) * kmax * row_elems);
+  if (w) *w = ww;
+  if (q) {
+    q->pos = pos;
+    q->xl = xl;
+  }
+  if (rm) {
+    rm->T = T;
+    rm->kmax = kmax;
+    rm->kvc = kvc;
+    rm->recv = recv;
+  }
+  if (local) *local = loc;
+  return cv.off + 256;
+}
+
+size_t pkv_recompute_rows_workspace(const pkv_model* md, int32_t k, int32_t m, int32_t world) {
+  return rows_ws(md, k, m, world, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+int pkv_recompute_rows(const pkv_model* md, const pkv_cache* c, const int32_t* sel, int32_t k,
+                       const int32_t* query_ids, int32_t m, pkv_comm* comm, float* last_logits, void* workspace,
+                       size_t ws_bytes, void* stream) {
+  if (!md || !c || !sel) return set_error(PKV_ERR_ARGUMENT, "null argument");
+  if (md->tp_world != 1) return set_error(PKV_ERR_ARGUMENT, "token-parallel Stage II needs the unsharded model");
+  if (k < 0 || k > c->s) return set_error(PKV_ERR_ARGUMENT, "bad selection size %d", k);
+  if (m < 0 || (m > 0 && (!query_ids || !last_logits))) return set_error(PKV_ERR_ARGUMENT, "query rows");
+  if (m > 0 && (c->pool_tokens < c->s + m || c->rope_len < c->s + m))
+    return set_error(PKV_ERR_SHAPE, "pool too small to append");
+  const int W = comm_world(comm), r = comm_rank(comm);
+  if (ws_bytes < pkv_recompute_rows_workspace(md, k, m, W)) return set_error(PKV_ERR_ARGUMENT, "workspace too small");
+  RcWs w;
+  QueryRows q;
+  RowsMode rm;
+  int32_t* local = nullptr;
+  rows_ws(md, k, m, W, &w, &q, &rm, &local, workspace);
+  std::vector<int> kr(W);
+  rows_counts(k, rm.T, W, kr.data());
+  cudaStream_t st = S(stream);
+  if (kr[r] > 0) {
+    rows_local_kernel<<<ceil_div(kr[r], 128), 128, 0, st>>>(sel, rm.T, W, r, kr[r], local);
+    PKV_LAUNCHED();
+    PKV_CHECK_LAUNCH("rows_local_kernel");
+  }
+  rm.comm = comm;
+  rm.sel_global = sel;
+  rm.k_global = k;
+  q.ids = query_ids;
+  q.m = m;
+  q.logits = last_logits;
+  return recompute_core(md, c, local, kr[r], nullptr, nullptr, nullptr, nullptr, w, st, /*need_final_h=*/false, q, rm);
 }
 
 // ------------------------------------------------------------------ full prefill

@@ -43,6 +43,7 @@ struct NcclApi {
   int (*get_id)(NcclId*) = nullptr;
   int (*init_rank)(void**, int, NcclId, int) = nullptr;
   int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   int (*destroy)(void*) = nullptr;
   const char* (*err_str)(int) = nullptr;
 };
@@ -63,9 +64,11 @@ static int nccl_load(const char* path) {
   a.init_rank = reinterpret_cast<int (*)(void**, int, NcclId, int)>(dlsym(so, "ncclCommInitRank"));
   a.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
       dlsym(so, "ncclAllReduce"));
+  a.all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(
+      dlsym(so, "ncclAllGather"));
   a.destroy = reinterpret_cast<int (*)(void*)>(dlsym(so, "ncclCommDestroy"));
   a.err_str = reinterpret_cast<const char* (*)(int)>(dlsym(so, "ncclGetErrorString"));
-  if (!a.get_id || !a.init_rank || !a.all_reduce || !a.destroy || !a.err_str)
+  if (!a.get_id || !a.init_rank || !a.all_reduce || !a.all_gather || !a.destroy || !a.err_str)
     return set_error(PKV_ERR_CUDA, "libnccl is missing an entry point");
   g_nccl = a;
   return PKV_OK;
@@ -181,6 +184,37 @@ int comm_allreduce(pkv_comm* c, void* buf, size_t count, int dt, cudaStream_t st
   if (c->kind == 1) return local_allreduce(c, buf, count, dt, st);
   const int r = g_nccl.all_reduce(buf, buf, count, nccl_dtype(dt), /*ncclSum*/ 0, c->nccl, st);
   if (r != 0) return set_error(PKV_ERR_CUDA, "ncclAllReduce: %s", g_nccl.err_str(r));
+  return PKV_OK;
+}
+
+// local all-gather: every rank copies the W published send buffers into its recv buffer
+// (rank order), then waits until every peer has finished reading its own send buffer
+static int local_allgather(pkv_comm* c, const void* send, void* recv, size_t bytes, cudaStream_t st) {
+  LocalGroup& g = *c->grp;
+  const int r = c->rank;
+  g.bufs[r] = const_cast<void*>(send);
+  cudaEventRecord(g.ready[r], st);
+  if (!g.barrier()) return set_error(PKV_ERR_CUDA, "local comm: a rank did not reach the collective");
+  for (int j = 0; j < g.world; ++j) {
+    cudaStreamWaitEvent(st, g.ready[j], 0);
+    cudaMemcpyAsync(reinterpret_cast<uint8_t*>(recv) + (size_t)j * bytes, g.bufs[j], bytes, cudaMemcpyDeviceToDevice,
+                    st);
+  }
+  cudaEventRecord(g.done[r], st);
+  if (!g.barrier()) return set_error(PKV_ERR_CUDA, "local comm: a rank did not reach the collective");
+  for (int j = 0; j < g.world; ++j) cudaStreamWaitEvent(st, g.done[j], 0);  // peers finished reading send
+  return PKV_OK;
+}
+
+int comm_allgather(pkv_comm* c, const void* send, void* recv, size_t bytes, cudaStream_t st) {
+  if (c == nullptr || bytes == 0) return PKV_OK;
+  if (c->world <= 1) {
+    if (recv != send) cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st);
+    return PKV_OK;
+  }
+  if (c->kind == 1) return local_allgather(c, send, recv, bytes, st);
+  const int r = g_nccl.all_gather(send, recv, bytes, /*ncclUint8*/ 1, c->nccl, st);
+  if (r != 0) return set_error(PKV_ERR_CUDA, "ncclAllGather: %s", g_nccl.err_str(r));
   return PKV_OK;
 }
 

@@ -48,6 +48,8 @@ struct GemmArgs {
   int tap_rows;               // with qtap_*: rows >= tap_rows tap into qtap_* at row - tap_rows instead
   float* qtap_k;              // (the query rows riding along a Stage-II repair, pkv_recompute_query)
   float* qtap_v;
+  __half* kvc;                // optional compact copy of the cache entries [M][3][Hkv][dkp] fp16 (K, K
+                              // residual, V) for the token-parallel exchange (pkv_recompute_rows)
   __half* k2_pool;            // optional residual key plane fp16(k - k_pool) (layer base), see s1_attn_tc.cu
   __nv_bfloat16* knr_out;     // optional bf16 [M][Hkv][dkp]: keys BEFORE RoPE (chunk-store layout)
   __nv_bfloat16* vcap_out;    // optional bf16 [M][Hkv][dkp]: values (chunk-store layout)
@@ -795,6 +797,16 @@ __global__ void __launch_bounds__(192, 1)
               __half* pool = is_v ? args.v_pool : args.k_pool;
               const long po = ((long)g * args.pool_tokens + slot) * dkp + d0;
               dst = pool + po;
+              if (args.kvc != nullptr) {  // compact copy for the token-parallel exchange
+                uint4* kc = reinterpret_cast<uint4*>(args.kvc + (((long)row * 3 + (is_v ? 2 : 0)) * Hkv + g) * dkp + d0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) kc[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+                if (!is_v) {
+                  uint4* k2c = reinterpret_cast<uint4*>(args.kvc + (((long)row * 3 + 1) * Hkv + g) * dkp + d0);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) k2c[j] = make_uint4(pk2[4 * j], pk2[4 * j + 1], pk2[4 * j + 2], pk2[4 * j + 3]);
+                }
+              }
               if (!is_v && args.k2_pool != nullptr) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j)

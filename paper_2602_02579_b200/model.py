@@ -325,7 +325,7 @@ class DeviceModel:
 
     def __del__(self):
         try:
-            if getattr(self, "handle", None):
+            if getattr(self, "handle", None) and not getattr(self, "_view_of", None):
                 _lib.load().pkv_model_destroy(self.handle)
         except Exception:
             pass
@@ -437,6 +437,20 @@ class DeviceModel:
         tensors = {"layers": layers, "embed": self.t["embed"], "lm_head": self.t["lm_head"],
                    "final_norm": self.t["final_norm"]}
         return DeviceModel(cfg, tensors, self.fingerprint, rank, world, comm)
+
+    def rows(self, comm) -> "DeviceModel":
+        """This (unsharded) model with a token-parallel Stage II over comm's ranks
+        (pkv_recompute_rows): every rank holds the full weights and a full cache, the
+        scoring pass is replicated, and the repair of the selected rows is split by
+        attention unit with one all-gather of fresh cache entries per layer.  Shares the
+        device tensors and the C model handle."""
+        if self.tp_world != 1:
+            raise ConfigError("token-parallel Stage II needs the unsharded model")
+        view = object.__new__(DeviceModel)
+        view.__dict__.update(self.__dict__)
+        view._view_of = self  # keeps the owner (and its C handle) alive; the view never frees it
+        view.rows_comm = comm
+        return view
 
     def weight_bytes(self, include_head: bool = True) -> int:
         n = 0

@@ -53,8 +53,13 @@ class PrefillPipeline:
         # repair, so no separate final pass runs after or interleaved with Stage II
         # (PKV_FUSED_FINAL=0: the separate fp32-faithful query pass)
         self.fused_final = os.environ.get("PKV_FUSED_FINAL", "1") == "1"
-        rc_bytes = (lib.pkv_recompute_query_workspace(dm.handle, self.k, m) if self.fused_final
-                    else lib.pkv_recompute_workspace(dm.handle, max(self.k, 1)))
+        self.rows_comm = getattr(dm, "rows_comm", None)  # token-parallel Stage II (DeviceModel.rows)
+        if self.rows_comm is not None:
+            rc_bytes = lib.pkv_recompute_rows_workspace(dm.handle, self.k, m if self.fused_final else 0,
+                                                        self.rows_comm.world)
+        else:
+            rc_bytes = (lib.pkv_recompute_query_workspace(dm.handle, self.k, m) if self.fused_final
+                        else lib.pkv_recompute_workspace(dm.handle, max(self.k, 1)))
         self.ws_rc = torch.empty(max(rc_bytes, 256), dtype=torch.uint8, device=dev)
         self.per_layer = torch.empty((cfg.n_layers, s), dtype=torch.float32, device=dev)
         self.fused = torch.empty(s, dtype=torch.float32, device=dev)
@@ -174,7 +179,17 @@ class PrefillPipeline:
         self._recompute(_lib.load(), ctypes_ref(self._plain_cache()), _lib.stream_ptr(torch, stream))
 
     def _recompute(self, lib, cc, st) -> None:
-        if self.fused_final:
+        if self.rows_comm is not None:
+            m = self.m if self.fused_final else 0
+            _lib.check(lib.pkv_recompute_rows(self.dm.handle, cc, self.idx.data_ptr(), self.k,
+                                              self.query.data_ptr() if m else None, m, self.rows_comm.handle,
+                                              self.logits.data_ptr() if m else None, self.ws_rc.data_ptr(),
+                                              self.ws_rc.numel(), st))
+            if not m:
+                _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ctypes_ref(self.cache.c_chunks), self.query.data_ptr(),
+                                              self.m, self.flags_final, None, None, None, self.logits.data_ptr(),
+                                              self.ws_qp.data_ptr(), self.ws_qp.numel(), st))
+        elif self.fused_final:
             _lib.check(lib.pkv_recompute_query(self.dm.handle, cc, self.idx.data_ptr(), self.k, self.query.data_ptr(),
                                                self.m, None, None, None, None, self.logits.data_ptr(),
                                                self.ws_rc.data_ptr(), self.ws_rc.numel(), st))
@@ -200,7 +215,7 @@ class PrefillPipeline:
         cc, ch = ctypes_ref(c.c_cache), ctypes_ref(c.c_chunks)
         main = stream if stream is not None else torch.cuda.current_stream()
         self._stage1(lib, st, main)
-        if self.fused_final:
+        if self.fused_final or self.rows_comm is not None:
             self._recompute(lib, cc, st)
             main.wait_stream(self.side)  # rejoin (required for graph capture)
             return

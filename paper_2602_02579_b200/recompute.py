@@ -64,7 +64,11 @@ def recompute_selected(weights, config: ModelConfig, cache, plan: RecomputePlan,
     lib = _lib.load()
     query = getattr(cache, "_pending_query", None)
     cache._pending_query = None
-    if query is not None and _fused_final():
+    if getattr(dm, "rows_comm", None) is not None:
+        if tap_k is not None:
+            raise ConfigError("fp32 taps are not available with the token-parallel Stage II")
+        _recompute_rows(lib, dm, config, cache, d_sel, k, query if _fused_final() else None)
+    elif query is not None and _fused_final():
         _recompute_with_query(lib, dm, config, cache, d_sel, k, query, tap_k, tap_v)
     else:
         _recompute(lib, dm, cache, d_sel, k, tap_k, tap_v, L)
@@ -107,6 +111,31 @@ def _recompute_with_query(lib, dm, config, cache, d_sel, k, query, tap_k, tap_v)
                                        tap_v.data_ptr() if tap_v is not None else None, fk.data_ptr(), fv.data_ptr(),
                                        logits.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(torch)))
     cache._fused_final = (query, logits, fk, fv)
+
+
+def _recompute_rows(lib, dm, config, cache, d_sel, k, query) -> None:
+    """Token-parallel Stage II (pkv_recompute_rows) on this rank's share of the selection,
+    with the query rows riding along when finalize_query will follow (every rank)."""
+    torch = _lib.require_cuda()
+    comm = dm.rows_comm
+    m = int(query.shape[0]) if query is not None else 0
+    logits = d_q = None
+    if m:
+        cache.ensure_query_room(m)
+        logits = torch.empty(config.vocab_size, dtype=torch.float32, device=cache.device)
+        d_q = torch.from_numpy(query).to(cache.device)
+    ws = workspace(lib.pkv_recompute_rows_workspace(dm.handle, k, m, comm.world), "rc")
+    cache._final_follow = None
+    _lib.check(lib.pkv_recompute_rows(dm.handle, ctypes.byref(cache.c_cache), d_sel.data_ptr(), k,
+                                      d_q.data_ptr() if m else None, m, comm.handle,
+                                      logits.data_ptr() if m else None, ws.data_ptr(), ws.numel(),
+                                      _lib.stream_ptr(torch)))
+    if m:
+        # the query's fresh K/V for the KVCache views: read back from the pool (fp16 entries)
+        s, L, Hkv, dk = cache.context_length, config.n_layers, cache.config.n_kv_heads, config.head_dim
+        fk = (cache.k_pool[:, :, s:s + m, :dk].float() + cache.k2_pool[:, :, s:s + m, :dk].float()).permute(0, 2, 1, 3)
+        fv = cache.v_pool[:, :, s:s + m, :dk].float().permute(0, 2, 1, 3)
+        cache._fused_final = (query, logits, fk.contiguous(), fv.contiguous())
 
 
 def _recompute(lib, dm, cache, d_sel, k, tap_k, tap_v, L) -> None:

@@ -95,9 +95,11 @@ _WS: dict = {}
 
 
 def workspace(nbytes: int, tag: str = "ws"):
-    """Grow-only device scratch per (device, tag)."""
+    """Grow-only device scratch per (device, tag, host thread): the ranks of an in-process
+    group (tp.run_ranks) are threads sharing one device and must not share scratch."""
+    import threading
     torch = _lib.require_cuda()
-    key = (torch.cuda.current_device(), tag)
+    key = (torch.cuda.current_device(), tag, threading.get_ident())
     buf = _WS.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")

@@ -12,6 +12,11 @@ stage loops, include/pkv.h "Head-sharded prefill"):
 * the row-parallel o / down projection outputs of the narrow passes ([m][D] fp32)
   and of Stage II ([k][D] fp32).
 
+Alternative (``DeviceModel.rows``, include/pkv.h pkv_recompute_rows): token-parallel
+Stage II -- every rank holds the full model and cache, the scoring pass is replicated,
+and each rank repairs its attention units of the selected rows with one all-gather of
+fresh cache entries per layer instead of the two [k][D] fp32 all-reduces.
+
 Two communicator back ends: NCCL (one process per GPU, NVLink / NVSwitch; the
 unique id travels over the torch.distributed process group) and an in-process
 group of W threads sharing one GPU, which runs the sharded math end to end on a
@@ -29,7 +34,7 @@ from . import _lib
 from .chunkstore import ChunkKV
 from .model import DeviceModel, shard_config
 
-__all__ = ["Comm", "local_group", "nccl_comm", "shard_chunks", "shard_config", "run_ranks"]
+__all__ = ["Comm", "local_group", "nccl_comm", "shard_chunks", "shard_config", "run_ranks", "rows_share"]
 
 
 class Comm:
@@ -122,6 +127,17 @@ def shard_chunks(chunks, rank: int, world: int) -> list:
                                        k[:, :, rank * kl:(rank + 1) * kl].contiguous(),
                                        v[:, :, rank * kl:(rank + 1) * kl].contiguous(), c._dk))
     return out
+
+
+def rows_share(k: int, group: int, world: int, rank: int):
+    """Global selection rows the rank repairs under token-parallel Stage II (include/pkv.h
+    pkv_recompute_rows): attention units of T = 128 / group consecutive rows, unit u on rank
+    u mod world."""
+    import numpy as np
+    T = max(1, 128 // max(1, group))
+    units = range(rank, -(-k // T), world)
+    return np.concatenate([np.arange(u * T, min(k, (u + 1) * T)) for u in units]) if len(units) else \
+        np.zeros(0, dtype=np.int64)
 
 
 def shard_model(dm: DeviceModel, comms: list) -> list:

@@ -115,3 +115,64 @@ def test_local_allreduce_sums_bit_identically(built):
         assert torch.equal(b, want)
     for c in comms:
         c.close()
+
+
+@pytest.mark.parametrize("case,world", [("c1", 2), ("llama_width", 2), ("llama_width", 4), ("tiny_ref", 3)])
+def test_token_parallel_stage2_is_bit_identical(built, case, world):
+    """Token-parallel Stage II (DeviceModel.rows, pkv_recompute_rows): every rank holds the
+    full model and cache, repairs its attention units of the selection and all-gathers the
+    fresh entries per layer.  Each row is computed exactly as in the single-GPU run (a GEMM
+    row and an attention tile do not depend on the other rows), so every rank's repaired
+    cache and first-token logits equal the unsharded run's bit for bit -- through the
+    graph-capturable pipeline and through the public API."""
+    import torch
+
+    import paper_2602_02579_b200 as P
+    from paper_2602_02579_b200 import tp
+    cfg_o, seed, units, query, p = _materialise(case)
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg = P.ModelConfig(**cfg_o.json())
+    mw = P.ModelWeights(embed=w.embed, layers=[P.LayerWeights(**{n: getattr(lw, n) for n in (
+        "attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")}) for lw in w.layers],
+        final_norm=w.final_norm, lm_head=w.lm_head)
+    dm = P.DeviceModel.from_host(mw, cfg)
+    fp = mw.fingerprint(cfg)
+    dch = [P.ChunkKV(c.chunk_id, fp, c.token_ids, c.k_nr, c.v) for c in chunks]
+    for c in dch:
+        c.device_buffers(cfg)
+    one = _run(P, dm, dch, query, p)
+    one.step()
+    torch.cuda.synchronize()
+
+    comms = tp.local_group(world)
+    pipes = [_run(P, dm.rows(c), dch, query, p) for c in comms]
+    torch.cuda.synchronize()
+    tp.run_ranks([pipe.step for pipe in pipes])
+    torch.cuda.synchronize()
+    s, k = one.s, one.k
+    for r, pipe in enumerate(pipes):
+        assert torch.equal(pipe.idx[:k], one.idx[:k]), r
+        for name in ("k_pool", "v_pool", "k2_pool"):
+            assert torch.equal(getattr(pipe.cache, name)[:, :, :s], getattr(one.cache, name)[:, :, :s]), (r, name)
+        assert torch.equal(pipe.logits, one.logits), r
+        assert torch.equal(pipe.cache.k_pool[:, :, s:s + len(query)], one.cache.k_pool[:, :, s:s + len(query)]), r
+
+    # the public API on the same ranks: score -> select -> recompute -> finalize
+    def api(c):
+        def run():
+            cache = P.assemble(dch, cfg, fp32_taps=False)
+            sc = P.score_prophet(dm.rows(c), cfg, cache, query)
+            sel = P.select_top_p(sc, p)
+            P.recompute_selected(dm.rows(c), cfg, cache, P.RecomputePlan(sel))
+            fin = P.finalize_query(dm.rows(c), cfg, cache, query)
+            torch.cuda.current_stream().synchronize()
+            return sel.indices, fin.first_logits, cache.k_pool[:, :, :s].clone()
+        return run
+    outs = tp.run_ranks([api(c) for c in comms])
+    for sel_r, lg_r, kp_r in outs:
+        assert sel_r == one.idx[:k].cpu().numpy().tolist()
+        assert np.array_equal(lg_r, one.logits.cpu().numpy())
+        assert torch.equal(kp_r, one.cache.k_pool[:, :, :s])
+    _report(case=f"{case}_rows{world}", s=s, k=k, bit_identical=True)
+    for c in comms:
+        c.close()

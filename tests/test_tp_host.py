@@ -109,3 +109,20 @@ def test_exchange_algebra_on_the_oracle():
     for r in range(W):
         for j in range(hl):
             assert (r * hl + j) // G in range(r * (Hkv // W), (r + 1) * (Hkv // W))
+
+
+def test_token_parallel_row_partition():
+    """pkv_recompute_rows' unit assignment (tp.rows_share): 128/G-row attention units,
+    unit u on rank u mod W -- every selected row on exactly one rank, in ascending order
+    per rank, balanced to one unit."""
+    import numpy as np
+
+    from paper_2602_02579_b200 import tp
+    for k, group, world in [(6554, 4, 8), (6554, 4, 2), (410, 2, 4), (5, 2, 3), (0, 4, 2), (128, 1, 2)]:
+        parts = [tp.rows_share(k, group, world, r) for r in range(world)]
+        allr = np.sort(np.concatenate(parts)) if k else np.zeros(0)
+        assert np.array_equal(allr, np.arange(k))
+        for p in parts:
+            assert np.all(np.diff(p) > 0)
+        T = max(1, 128 // group)
+        assert max(len(p) for p in parts) - min(len(p) for p in parts) <= T
