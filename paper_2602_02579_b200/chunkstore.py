@@ -422,6 +422,8 @@ def replace_entries(cache: AssembledCache, layer: int, indices, new_keys, new_va
     # a later finalize_query must see this write: no overlap with the preceding repair
     # (recompute.finalize_query only follows Stage II's per-layer events)
     cache._final_follow = None
+    # ... nor reuse the query rows a fused repair computed before this write
+    cache._fused_final = None
     idx = np.asarray(indices, dtype=np.int64)
     if idx.ndim != 1:
         raise ShapeError("indices must be 1-D")

@@ -1043,6 +1043,273 @@ static int launch_attn1(const CUtensorMap& tk, const CUtensorMap& tv, const Attn
   return PKV_OK;
 }
 
+// One thread per Q-tile row (PKV_ATTN_ROW=1): the two-tile kernel above with 4 softmax
+// warps per tile instead of 8 -- each thread reads its row's 128 scores, takes the max
+// in registers (no half-row exchange through shared memory and no named barrier per
+// page) and exponentiates all 128 keys; warps 0-3 tile A, 4-7 tile B, 8 TMA, 9 MMA.
+template <int POLY>
+__global__ void __launch_bounds__(320, 1)
+    attn_row_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
+  constexpr int DKP = 128;
+  using Cfg = AttnCfg<DKP>;
+  constexpr int NST = Cfg::STAGES, KVB = Cfg::KV_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + 2 * Cfg::Q_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NST * 2 * KVB);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + NST;
+  uint64_t* s_full = bars + 2 * NST;  // [2] per tile
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* pv_full = p_full + 2;     // [2]
+  uint64_t* q_full = pv_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cid = (int)blockIdx.x;
+  const int per_group = a.hg * a.n_pairs;
+  const int grp = cid / per_group, rem_ = cid - grp * per_group;
+  const int g = grp * a.hg + rem_ % a.hg;
+  const int pair = a.n_pairs - 1 - rem_ / a.hg;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_full[i], 1);
+    }
+    mbar_init(q_full, 8);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
+  const int last_tok = min((2 * pair + 2) * a.T, a.n_q) - 1;
+  const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
+
+  if (warp == 8) {
+    if (elect_one()) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
+      for (int j = 0; j < n_kv_tiles; ++j) {
+        const int st = j % NST;
+        mbar_wait(&kv_empty[st], ((uint32_t)(j / NST) & 1) ^ 1);
+        uint8_t* sk = sKV + st * 2 * KVB;
+        uint8_t* sv = sk + KVB;
+        const int row = (int)(head_row + (long)a.page_table[j] * 128);
+        mbar_expect_tx(&kv_full[st], 2 * KVB);
+#pragma unroll
+        for (int at = 0; at < Cfg::ATOMS; ++at) {
+          tma_load_2d(sk + at * 16384, &tmK, &kv_full[st], at * 64, row);
+          tma_load_2d(sv + at * 16384, &tmV, &kv_full[st], at * 64, row);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idesc_s = make_idesc_f16(128, 128);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, DKP, /*b_mn_major=*/true);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint32_t q_addr = smem_u32(sQ);
+    auto issue_s = [&](int t, int j) {
+      const uint32_t k_addr = smem_u32(sKV + (j % NST) * 2 * KVB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < DKP / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_ss(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                  sdesc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j) {
+      const uint32_t v_addr = smem_u32(sKV + (j % NST) * 2 * KVB + KVB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024),
+                  idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&pv_full[t]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(&kv_full[0], 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int j = 0; j < n_kv_tiles; ++j) {
+      const bool more = j + 1 < n_kv_tiles;
+      mbar_wait(&p_full[0], (uint32_t)j & 1);
+      tc_fence_after();
+      issue_pv(0, j);
+      if (more) {
+        mbar_wait(&kv_full[(j + 1) % NST], (uint32_t)((j + 1) / NST) & 1);
+        tc_fence_after();
+        issue_s(0, j + 1);
+      }
+      mbar_wait(&p_full[1], (uint32_t)j & 1);
+      tc_fence_after();
+      issue_pv(1, j);
+      if (elect_one()) umma_commit(&kv_empty[j % NST]);
+      __syncwarp();
+      if (more) issue_s(1, j + 1);
+    }
+  } else {
+    const int t = warp >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int b = 2 * pair + t;
+    const bool has_tile = pair >= 0 && b < a.n_tiles;
+    const int hj = r / a.T, ti = r - hj * a.T;
+    const int tok = b * a.T + ti;
+    const bool valid = has_tile && hj < a.G && tok < a.n_q;
+    const int head = g * a.G + hj;
+    const int tile_last = min((b + 1) * a.T, a.n_q) - 1;
+    const int min_pos = has_tile ? a.pos[b * a.T] : 0x7fffffff;
+    const int my_pos = valid ? a.pos[tok] : (has_tile ? a.pos[tile_last] : 0x7fffffff);
+    const uint32_t lb = (uint32_t)((quarter * 32) << 16);
+    const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
+    const float sl2 = a.scale_log2;
+#pragma unroll 1
+    for (int h = 0; h < Cfg::ATOMS; ++h) {  // this row's Q -> smem (both 64-column atoms)
+      uint4 v[8];
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) + h * 8;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(sQ + t * Cfg::Q_BYTES + h * 16384 + r * 128 + ((c ^ (r & 7)) * 16)) = v[c];
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(q_full);
+
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_kv_tiles; ++j) {
+      mbar_wait(&s_full[t], (uint32_t)j & 1);  // also implies PV_t(j-1) is complete
+      tc_fence_after();
+      const int key0 = j * 128;
+      float sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tS + lb + c * 32, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(u[i]);
+      }
+      if (key0 + 127 > min_pos) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i) sv[i] = (key0 + i <= my_pos) ? sv[i] : -INFINITY;
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int i = 0; i < 128; i += 8)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(sv[i + 2 * q], sv[i + 2 * q + 1]));
+      const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      const float m_new = fmaxf(m_run, tmax * sl2);
+      const bool grow = (m_new - m_run) > 8.0f;
+      const float m_use = grow ? m_new : m_run;
+      const uint64_t sl2x2 = f32x2(sl2, sl2), negm = f32x2(-m_use, -m_use);
+      uint64_t rsum2 = f32x2(0.f, 0.f), rsum2b = f32x2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint64_t x = ffma2(f32x2(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]), sl2x2, negm);
+          float x0, x1;
+          f32x2_unpack(x, x0, x1);
+          float p0, p1;
+          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+          if ((kPolyMask >> (i & 7)) & 1u) {
+            p0 = exp2_poly(x0);
+            p1 = exp2_poly(x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
+          else rsum2 = fadd2(rsum2, f32x2(p0, p1));
+          pk[i] = pack_f16(p0, p1);
+        }
+        tmem_st16(tS + lb + c * 16, pk);  // P of keys [32c, 32c+32): the S columns are in registers
+      }
+      float rs0, rs1;
+      f32x2_unpack(fadd2(rsum2, rsum2b), rs0, rs1);
+      if (__any_sync(0xffffffffu, grow && j > 0)) {
+        const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < DKP / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld32(tO + lb + c * 32, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+          tmem_st32(tO + lb + c * 32, u);
+        }
+      }
+      if (grow && j > 0) l_run *= ex2(m_run - m_use);
+      if (grow) m_run = m_use;
+      l_run += rs0 + rs1;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&pv_full[t], (uint32_t)(n_kv_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l_run;
+#pragma unroll 1
+    for (int c = 0; c < DKP / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tO + lb + c * 32, u);
+      tmem_ld_wait();
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + c * 32);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_f16(__uint_as_float(u[8 * i]) * inv_l, __uint_as_float(u[8 * i + 1]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 2]) * inv_l, __uint_as_float(u[8 * i + 3]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 4]) * inv_l, __uint_as_float(u[8 * i + 5]) * inv_l),
+                              pack_f16(__uint_as_float(u[8 * i + 6]) * inv_l, __uint_as_float(u[8 * i + 7]) * inv_l));
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+static int launch_attn_row(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
+  using Cfg = AttnCfg<128>;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(attn_row_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  });
+  if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn_row smem attr: %s", cudaGetErrorString(err));
+  launch_k(attn_row_kernel<1>, a.n_pairs * a.Hkv, 320, Cfg::SMEM, stream, tk, tv, a);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("attn_row_kernel");
+  return PKV_OK;
+}
+
 template <int DKP, int POLY>
 static int launch_attn(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
   using Cfg = AttnCfg<DKP>;
@@ -1154,6 +1421,8 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
       return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
     return launch_attn_pair<1>(tk64, tv, a, stream);
   }
+  static const bool row_env = getenv("PKV_ATTN_ROW") && getenv("PKV_ATTN_ROW")[0] == '1';
+  if (dkp == 128 && row_env && poly == 1) return launch_attn_row(tk, tv, a, stream);
   static const bool one_env = getenv("PKV_ATTN_ONE") && getenv("PKV_ATTN_ONE")[0] == '1';
   if (dkp == 128 && one_env && poly == 1) return launch_attn1(tk, tv, a, stream);
   if (dkp == 128) {

@@ -275,8 +275,8 @@ def test_gemm_stream_k_tail_opt_in(built, tmp_path):
 def test_opt_in_variants():
     """The opt-in kernel variants whose switches are read once per process -- the TMA-staged
     assembly (PKV_ASM_TMA=1), the grouped GEMM raster (PKV_GEMM_RASTER=2: partial groups
-    on every GEMM test shape) and the one-tile attention (PKV_ATTN_ONE=1) -- rerun the
-    kernel tests in a subprocess."""
+    on every GEMM test shape), the one-tile attention (PKV_ATTN_ONE=1) and the
+    one-thread-per-row attention (PKV_ATTN_ROW=1) -- rerun the kernel tests in a subprocess."""
     import os
     import subprocess
     import sys
@@ -287,5 +287,11 @@ def test_opt_in_variants():
              "tests/test_gpu_kernels.py::test_gemm_matches_fp32_reference",
              "tests/test_gpu_kernels.py::test_gemm_fp16_operands", "tests/test_gpu_kernels.py::test_gemm_residual_epilogue"]
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *tests], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    # one thread per Q-tile row (PKV_ATTN_ROW=1)
+    env = dict(os.environ, PKV_ATTN_ROW="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_kernels.py::test_sparse_attention_matches_fp32_reference"], cwd=root,
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
