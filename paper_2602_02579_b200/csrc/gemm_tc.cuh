@@ -700,7 +700,11 @@ __global__ void __launch_bounds__(192, 1)
                 }
               }
             } else {
-              for (int j = 0; j < 32 && col0 + j < args.N; ++j) {
+              // (fully unrolled with a predicate: a data-dependent trip count would index r[]
+              // dynamically and put every accumulator chunk of the kernel in local memory)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (col0 + j >= args.N) continue;
                 float v = __uint_as_float(r[j]) * asc;
                 if constexpr (EPI == EPI_RESID) {
                   v += dst[j];
@@ -723,7 +727,9 @@ __global__ void __launch_bounds__(192, 1)
                                pack_bf16(__uint_as_float(r[8 * j + 4]) * asc, __uint_as_float(r[8 * j + 5]) * asc),
                                pack_bf16(__uint_as_float(r[8 * j + 6]) * asc, __uint_as_float(r[8 * j + 7]) * asc));
             } else {
-              for (int j = 0; j < 32 && col0 + j < args.N; ++j) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * asc);
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j < args.N) dst[j] = __float2bfloat16_rn(__uint_as_float(r[j]) * asc);
             }
           } else if constexpr (EPI == EPI_QKV) {
             // a 32-column chunk never straddles a head (dkp is 64 or 128)

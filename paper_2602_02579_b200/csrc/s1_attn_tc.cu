@@ -374,7 +374,9 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int i = 0; i < HC; ++i) scol[(long)(key0 + i) * a.R] = sv[i];
         } else {
-          for (int i = 0; i < HC && key0 + i < k_end; ++i) scol[(long)(key0 + i) * a.R] = sv[i];
+#pragma unroll
+          for (int i = 0; i < HC; ++i)  // (predicated, not a data-dependent trip count: sv stays in registers)
+            if (key0 + i < k_end) scol[(long)(key0 + i) * a.R] = sv[i];
         }
       }
       // lazy rescale: the running max moves (and O / l are rescaled) only when a row's max
