@@ -346,33 +346,52 @@ __global__ void probe_cache_kv_kernel(float* k, float* v, int m, int Hkv, int dk
 // (rows = f32 head mean of the probabilities, reference model.py:296-305).  Scores are
 // recomputed exactly as s1_attn_pass1 forms the fresh-key scores (sequential f32 FMAs over
 // the padded head dim, then * scale) and normalised with the pass's final row max / sum.
-__global__ void probe_diag_colsum_kernel(const float* q, const float* k, const float* Mfin, const float* Lfin,
-                                         int m, int H, int Hkv, int dk, int dkp, float scale, float* out) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= m) return;
+// kvshare: the block keys' own column sums (reference _low_layer_probe: rows of the
+// block's queries over its own keys, causal).  One CTA per block key t: the (query, head)
+// terms exp(s - M) / L are formed in parallel into shared memory, then summed in the
+// round-1 kernel's order -- per query the heads in order in f64, rounded to f32 after the
+// head mean; the queries in order in f64 -- so the result is unchanged bit for bit.
+__global__ void __launch_bounds__(256) probe_diag_colsum_kernel(const float* q, const float* k, const float* Mfin,
+                                                                const float* Lfin, int m, int H, int Hkv, int dk,
+                                                                int dkp, float scale, float* out) {
+  extern __shared__ float term[];  // [m][H]
+  __shared__ float rowv[128];
+  const int t = blockIdx.x;
   constexpr float LOG2E = 1.4426950408889634f;
   const int G = H / Hkv, R = m * G;
-  double col = 0.0;
-  for (int qi = t; qi < m; ++qi) {
-    double acc = 0.0;
-    for (int h = 0; h < H; ++h) {
-      const int g = h / G, j = h - g * G;
-      const float* qp = q + ((long)qi * H + h) * dkp;
-      const float* kp = k + ((long)t * Hkv + g) * dkp;
-      float sc = 0.f;
-      for (int d = 0; d < dkp; ++d) sc = fmaf(qp[d], kp[d], sc);
-      const float sv = sc * scale;
-      const int r = g * R + j * m + qi;
-      acc += (double)(ex2(fmaf(sv, LOG2E, -Mfin[r] * LOG2E)) * (1.f / Lfin[r]));
-    }
-    col += (double)(float)(acc / (double)H);
+  for (int pidx = threadIdx.x; pidx < m * H; pidx += blockDim.x) {
+    const int qi = pidx / H, h = pidx - qi * H;
+    if (qi < t) continue;
+    const int g = h / G, j = h - g * G;
+    const float* qp = q + ((long)qi * H + h) * dkp;
+    const float* kp = k + ((long)t * Hkv + g) * dkp;
+    float sc = 0.f;
+    for (int d = 0; d < dkp; ++d) sc = fmaf(qp[d], kp[d], sc);
+    const float sv = sc * scale;
+    const int r = g * R + j * m + qi;
+    term[pidx] = ex2(fmaf(sv, LOG2E, -Mfin[r] * LOG2E)) * (1.f / Lfin[r]);
   }
-  out[t] = (float)col;
+  __syncthreads();
+  for (int qi = t + (int)threadIdx.x; qi < m; qi += blockDim.x) {
+    double acc = 0.0;
+    for (int h = 0; h < H; ++h) acc += (double)term[qi * H + h];
+    rowv[qi] = (float)(acc / (double)H);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double col = 0.0;
+    for (int qi = t; qi < m; ++qi) col += (double)rowv[qi];
+    out[t] = (float)col;
+  }
 }
 
 int probe_diag_colsum_launch(const float* q, const float* k, const float* Mfin, const float* Lfin, int m, int H,
                              int Hkv, int dk, int dkp, float scale, float* out, cudaStream_t st) {
-  probe_diag_colsum_kernel<<<ceil_div(m, 32), 32, 0, st>>>(q, k, Mfin, Lfin, m, H, Hkv, dk, dkp, scale, out);
+  if (m <= 0) return PKV_OK;
+  if (m > 128 || (size_t)m * H * sizeof(float) > 48 * 1024)
+    return set_error(PKV_ERR_ARGUMENT, "probe block of %d rows x %d heads", m, H);
+  probe_diag_colsum_kernel<<<m, 256, (size_t)m * H * sizeof(float), st>>>(q, k, Mfin, Lfin, m, H, Hkv, dk, dkp, scale,
+                                                                          out);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("probe_diag_colsum_kernel");
   return PKV_OK;
