@@ -185,6 +185,7 @@ static void launch_rms_y16(int nv, int m, cudaStream_t st, const float* h, int D
 
 int rmsnorm_launch(const float* h, int m, int D, long ld, const float* gain, double eps, float* y, void* x3, long ldx,
                    void* ybf, cudaStream_t st, int y16_bf16) {
+  if (m <= 0 && !x3) return PKV_OK;  // e.g. a token-parallel rank without rows
   if (ybf && !y && !x3 && ld % 4 == 0 && ld <= 128 * 4 * 16) {
     const int nv = ceil_div(ld / 4, 128);
     if (y16_bf16) launch_rms_y16<true>(nv, m, st, h, D, ld, gain, eps, ybf);

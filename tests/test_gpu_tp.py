@@ -176,3 +176,37 @@ def test_token_parallel_stage2_is_bit_identical(built, case, world):
     _report(case=f"{case}_rows{world}", s=s, k=k, bit_identical=True)
     for c in comms:
         c.close()
+
+
+def test_token_parallel_without_query_rows(built, monkeypatch):
+    """Token-parallel Stage II with the separate final pass (PKV_FUSED_FINAL=0: no query rows
+    ride along) and a rank that owns no selected rows: it still joins every per-layer
+    all-gather and ends with the full repaired cache."""
+    import torch
+
+    import paper_2602_02579_b200 as P
+    from paper_2602_02579_b200 import tp
+    monkeypatch.setenv("PKV_FUSED_FINAL", "0")
+    cfg_o, seed, units, query, p = _materialise("tiny_ref")
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg = P.ModelConfig(**cfg_o.json())
+    mw = P.ModelWeights(embed=w.embed, layers=[P.LayerWeights(**{n: getattr(lw, n) for n in (
+        "attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")}) for lw in w.layers],
+        final_norm=w.final_norm, lm_head=w.lm_head)
+    dm = P.DeviceModel.from_host(mw, cfg)
+    fp = mw.fingerprint(cfg)
+    dch = [P.ChunkKV(c.chunk_id, fp, c.token_ids, c.k_nr, c.v) for c in chunks]
+    one = _run(P, dm, dch, query, p)
+    one.step()
+    torch.cuda.synchronize()
+    comms = tp.local_group(3)
+    pipes = [_run(P, dm.rows(c), dch, query, p) for c in comms]
+    tp.run_ranks([pipe.step for pipe in pipes])
+    torch.cuda.synchronize()
+    s = one.s
+    for pipe in pipes:
+        for name in ("k_pool", "v_pool", "k2_pool"):
+            assert torch.equal(getattr(pipe.cache, name)[:, :, :s], getattr(one.cache, name)[:, :, :s])
+        assert torch.equal(pipe.logits, one.logits)
+    for c in comms:
+        c.close()
