@@ -560,6 +560,17 @@ def main():
         peak = hbm if bound == "hbm" else tf_sust
         rooflines[name] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
                            "ms_per_launch": per_launch_s * 1e3, "launches": cnt}
+    if "qp_attn" in rooflines:
+        # the narrow attention implements fp32 math with fp16 plane products on the tensor
+        # cores (s1_attn_tc.cu: 3 QK + 2 PV products, scoring pass 2 another 3 QK): its
+        # executed tensor work against the bf16 peak, next to the algorithmic K/V bytes
+        # above.  The scope holds both passes' kernels, combine and finish.
+        r = rooflines["qp_attn"]
+        R = args.m * (cfg.n_heads // cfg.n_kv_heads)
+        prod = 2.0 * R * s * dk * Hkv * (5 + 3)  # pass 1 (3 QK + 2 PV) + pass 2 (3 QK)
+        tf = prod / (r["ms_per_launch"] / 1e3) / 1e12
+        r["executed_tensor"] = {"tflop_per_launch": prod / 1e12, "achieved": tf, "peak": tf_sust, "frac": tf / tf_sust,
+                                "note": "latency-bound: one wave of 144 CTAs x 28 64-key tiles (DESIGN.md section 3)"}
     step_total = sum(v[0] for v in phases.values())
     dominant = max((n for n in rooflines), key=lambda n: phases[n][0])
     traffic = None
