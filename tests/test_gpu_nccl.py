@@ -69,3 +69,67 @@ print("ok", r)
                           "--master-addr", "127.0.0.1", "--master-port", str(port), str(path)],
                          capture_output=True, text=True, timeout=600, env=env)
     assert out.returncode == 0 and out.stdout.count("ok") == 2, out.stderr[-4000:]
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs (NCCL over NVLink)")
+def test_bench_two_ranks_token_parallel():
+    """`bench.py --gpus 2 --mode tokens`: replicated scoring, token-parallel Stage II over
+    NCCL all-gathers; rank 0's request is checked against the oracle fixture in-run."""
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--mode", "tokens", "--steps", "2",
+                          "--warmup", "1", "--e2e-steps", "0", "--full-steps", "0", "--p-sweep", "",
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=1800, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-4000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["parallelism"].startswith("tokens2")
+    if "parity" in line:
+        assert line["parity"]["sel_ok"] and line["parity"]["pass"], line["parity"]
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs (NCCL over NVLink)")
+def test_nccl_allgather_two_processes(tmp_path):
+    """The all-gather the token-parallel Stage II uses (comm_allgather -> ncclAllGather),
+    driven through a two-rank token-parallel repair on tiny inputs: both ranks end with the
+    unsharded run's cache bit for bit."""
+    script = r'''
+import os, sys, numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, os.environ["PKV_ROOT"]); sys.path.insert(0, os.path.join(os.environ["PKV_ROOT"], "tests"))
+import __graft_entry__; __graft_entry__.build()
+import paper_2602_02579_b200 as P
+from paper_2602_02579_b200 import tp
+from paper_2602_02579_b200.pipeline import PrefillPipeline
+from test_gpu_parity import _materialise, _setup
+r = int(os.environ["RANK"]); torch.cuda.set_device(r)
+dist.init_process_group("nccl", device_id=torch.device("cuda", r))
+cfg_o, seed, units, query, p = _materialise("c1")
+w, chunks = _setup(cfg_o, seed, units, query)
+cfg = P.ModelConfig(**cfg_o.json())
+mw = P.ModelWeights(embed=w.embed, layers=[P.LayerWeights(**{n: getattr(lw, n) for n in (
+    "attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")}) for lw in w.layers],
+    final_norm=w.final_norm, lm_head=w.lm_head)
+dm = P.DeviceModel.from_host(mw, cfg)
+dch = [P.ChunkKV(c.chunk_id, mw.fingerprint(cfg), c.token_ids, c.k_nr, c.v) for c in chunks]
+one = PrefillPipeline(dm, dch, len(query), p); one.set_query(query); one.step()
+c = tp.nccl_comm()
+pipe = PrefillPipeline(dm.rows(c), dch, len(query), p); pipe.set_query(query); pipe.step()
+torch.cuda.synchronize()
+s = one.s
+for name in ("k_pool", "v_pool", "k2_pool"):
+    assert torch.equal(getattr(pipe.cache, name)[:, :, :s], getattr(one.cache, name)[:, :, :s]), name
+assert torch.equal(pipe.logits, one.logits)
+c.close()
+dist.destroy_process_group()
+print("ok", r)
+'''
+    import os
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, PKV_ROOT=str(ROOT))
+    path = tmp_path / "nccl_rows.py"
+    path.write_text(script)
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), str(path)],
+                         capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0 and out.stdout.count("ok") == 2, out.stderr[-4000:]
