@@ -93,55 +93,141 @@ __global__ void s1_qprep_kernel(const float* q, int m, int H, int G, int R, int 
 }
 
 // The m fresh query keys of one (KV head, row block) as split a.n_splits, on the CTA slot
-// the launch adds after the context splits (so no separate SIMT launch): warp per row,
-// lane = 4 head dims; S = f32(q.k) * scale (model.py:291, 298), causal within the query,
-// online softmax; partials in the context splits' form (O unnormalised, M, L).
+// the launch adds after the context splits (so no separate SIMT launch).  S = f32(q.k) *
+// scale (model.py:291, 298), causal within the query; partials in the context splits' form
+// (O unnormalised, M, L).  Warp per row with lane = KEY (keys lane, lane + 32, ...): every
+// lane forms whole dot products from shared memory (key rows padded to DKP + 4 floats, so
+// the lanes' 16-byte reads of 32 different keys hit distinct banks), one max / sum
+// reduction per row, then lane = 4 output dims.  (Round 1's lane = 4 dims with a
+// shuffle-reduced dot product per key made this CTA the launch's critical path: 60 us
+// against ~43 us for the context splits, tools/s1_trace.py.)
 template <int DKP>
 __device__ __noinline__ void s1_fresh_cta(const S1TcArgs& a, uint8_t* smem) {
-  constexpr int DPL = DKP / 32;  // dims per lane
+  constexpr int KS = DKP + 4, DPL = DKP / 32;
   const int g = blockIdx.y, rb = blockIdx.z;
   const int m = a.m;
+  const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* sk = reinterpret_cast<float*>(smem);
-  float* sv = sk + (long)m * DKP;
-  for (int e = threadIdx.x; e < m * DKP; e += blockDim.x) {
-    const int kk = e / DKP, d = e - kk * DKP;
-    const long src = ((long)kk * a.Hkv + g) * DKP + d;
-    sk[e] = a.fk[src];
-    sv[e] = a.fv[src];
+  float* sv = sk + (long)m * KS;
+  float* qs = sv + (long)m * KS;  // [128][DKP] the CTA's query rows, then [nw][32] probabilities
+  // float4 copies, 4 in flight per thread (a load per element had taken 9 us, latency-bound)
+  const int nv4 = m * (DKP / 4);
+  for (int e0 = threadIdx.x; e0 < nv4; e0 += 4 * blockDim.x) {
+    float4 kv[4], vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < nv4) {
+        const int kk = e / (DKP / 4), d4 = e - kk * (DKP / 4);
+        const long src = ((long)kk * a.Hkv + g) * DKP + 4 * d4;
+        kv[u] = *reinterpret_cast<const float4*>(a.fk + src);
+        vv[u] = *reinterpret_cast<const float4*>(a.fv + src);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < nv4) {
+        const int kk = e / (DKP / 4), d4 = e - kk * (DKP / 4);
+        *reinterpret_cast<float4*>(sk + kk * KS + 4 * d4) = kv[u];
+        *reinterpret_cast<float4*>(sv + kk * KS + 4 * d4) = vv[u];
+      }
+    }
+  }
+  for (int e0 = threadIdx.x; e0 < 128 * (DKP / 4); e0 += 4 * blockDim.x) {  // the 128 query rows
+    float4 qv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x, r = e / (DKP / 4), d4 = e - r * (DKP / 4), row = rb * 128 + r;
+      qv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < 128 * (DKP / 4) && row < a.R) {
+        const int jh = row / m, i = row - jh * m;
+        qv[u] = *reinterpret_cast<const float4*>(a.q + ((long)i * a.H + g * a.G + jh) * DKP + 4 * d4);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < 128 * (DKP / 4)) reinterpret_cast<float4*>(qs)[e] = qv[u];
+    }
   }
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int sp = a.n_splits;
+  if (a.trace != nullptr && g == 0 && rb == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[5 * 64 + 6] = t;  // fresh-key CTA: K/V staged
+  }
+  float* pw = qs + 128 * DKP + warp * 32;  // this warp's probabilities of one key block
   for (int r = warp; r < 128; r += nw) {
     const int row = rb * 128 + r;
     if (row >= a.R) break;
-    const int jh = row / m, i = row - jh * m;
-    const float* qr = a.q + ((long)i * a.H + g * a.G + jh) * DKP + lane * DPL;
-    float q[DPL], o[DPL];
+    const int i = row % m;
+    const float* qw = qs + r * DKP;
+    float sc[4];
+    float mx = -INFINITY;
 #pragma unroll
-    for (int d = 0; d < DPL; ++d) {
-      q[d] = qr[d];
-      o[d] = 0.f;
+    for (int t = 0; t < 4; ++t) {
+      const int kk = lane + 32 * t;
+      sc[t] = -INFINITY;
+      if (kk < m && kk <= i) {
+        const float4* kr = reinterpret_cast<const float4*>(sk + kk * KS);
+        const float4* q4 = reinterpret_cast<const float4*>(qw);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};  // four independent chains, summed in a fixed order
+#pragma unroll 8
+        for (int d = 0; d < DKP / 4; ++d) {
+          const float4 x = q4[d], y = kr[d];
+          acc[0] = fmaf(x.x, y.x, acc[0]);
+          acc[1] = fmaf(x.y, y.y, acc[1]);
+          acc[2] = fmaf(x.z, y.z, acc[2]);
+          acc[3] = fmaf(x.w, y.w, acc[3]);
+        }
+        sc[t] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * a.scale;
+      }
+      mx = fmaxf(mx, sc[t]);
     }
-    float mx = -INFINITY, l = 0.f;
-    for (int kk = 0; kk <= i; ++kk) {
-      const float* kr = sk + kk * DKP + lane * DPL;
-      float part = 0.f;
 #pragma unroll
-      for (int d = 0; d < DPL; ++d) part = fmaf(q[d], kr[d], part);
+    for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    float pk[4], l = 0.f;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
-      const float sc = part * a.scale;
-      const float mn = fmaxf(mx, sc);
-      const float corr = mx == -INFINITY ? 0.f : expf(mx - mn);
-      const float p = expf(sc - mn);
-      l = l * corr + p;
-      const float* vr = sv + kk * DKP + lane * DPL;
-#pragma unroll
-      for (int d = 0; d < DPL; ++d) o[d] = fmaf(p, vr[d], o[d] * corr);
-      mx = mn;
+    for (int t = 0; t < 4; ++t) {
+      pk[t] = sc[t] == -INFINITY ? 0.f : expf(sc[t] - mx);
+      l += pk[t];
     }
-    const long base = ((long)sp * a.Hkv + g) * a.R + row;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    float o[DPL];
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) o[d] = 0.f;
+    const int nk = min(i + 1, m);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (32 * t >= m) break;  // (m is uniform: no dynamic indexing of pk)
+      // all 32 lanes' probabilities of this key block to shared memory (reuses the query
+      // row slot, read by this warp only), then 4 keys per step: independent loads in flight
+      __syncwarp();
+      pw[lane] = pk[t];
+      __syncwarp();
+      const int k1 = min(nk, 32 * t + 32);
+      int kk = 32 * t;
+      for (; kk + 4 <= k1; kk += 4) {
+        const float4 pv = *reinterpret_cast<const float4*>(pw + (kk - 32 * t));
+        const float* vr = sv + kk * KS + lane * DPL;
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) {
+          o[d] = fmaf(pv.x, vr[d], o[d]);
+          o[d] = fmaf(pv.y, vr[KS + d], o[d]);
+          o[d] = fmaf(pv.z, vr[2 * KS + d], o[d]);
+          o[d] = fmaf(pv.w, vr[3 * KS + d], o[d]);
+        }
+      }
+      for (; kk < k1; ++kk) {
+        const float pv = pw[kk - 32 * t];
+        const float* vr = sv + kk * KS + lane * DPL;
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) o[d] = fmaf(pv, vr[d], o[d]);
+      }
+    }
+    const long base = ((long)a.n_splits * a.Hkv + g) * a.R + row;
     float* od = a.Opart + base * DKP + lane * DPL;
 #pragma unroll
     for (int d = 0; d < DPL; ++d) od[d] = o[d];
@@ -149,13 +235,14 @@ __device__ __noinline__ void s1_fresh_cta(const S1TcArgs& a, uint8_t* smem) {
       a.Mpart[base] = mx;
       a.Lpart[base] = l;
     }
+    __syncwarp();
   }
 }
 
 // trace[ev * 64 + j], tile j < 64 of CTA (0,0,0) (tools/s1_trace.py):
 //   ev 0: softmax warp 0 saw S(j)   ev 1: softmax warp 0 arrived P(j)   ev 2: MMA warp saw K/V(j)
 //   ev 3: MMA warp issued PV(j)     ev 4: producer issued tile j        ev 5: j=0 prologue done,
-//   j=1 softmax loop done, j=2 partials written
+//   j=1 softmax loop done, j=2 partials written, j=4/5 fresh-key CTA of KV head 0 start/end
 __device__ __forceinline__ void s1_stamp(const S1TcArgs& a, int ev, int j) {
   if (a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < 64) {
     unsigned long long t;
@@ -173,7 +260,15 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   if (a.fresh && blockIdx.x == (unsigned)a.n_splits) {  // the fresh query keys' split
     griddep_wait();
+    const bool tr = a.trace != nullptr && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0;
+    unsigned long long t0 = 0, t1 = 0;
+    if (tr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     s1_fresh_cta<DKP>(a, smem);
+    if (tr) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      a.trace[5 * 64 + 4] = t0;  // fresh-key CTA of KV head 0: start / end
+      a.trace[5 * 64 + 5] = t1;
+    }
     return;
   }
   uint8_t* sKV = smem;  // STAGES x {Kh, Kl, V}
@@ -486,7 +581,7 @@ int s1_attn_tc_launch(const S1TcArgs& a_in, const void* k1, const void* k2, cons
   if (a.keys_per_split % 64 != 0) return set_error(PKV_ERR_ARGUMENT, "narrow pass: split not 64-aligned");
   const int RB = ceil_div(a.R, 128);
   dim3 grid(a.n_splits + (a.fresh ? 1 : 0), a.Hkv, RB);
-  if (a.fresh && 2L * a.m * dkp * 4 > S1TcCfg<128>::SMEM - 2048)
+  if (a.fresh && (a.m > 128 || (2L * a.m * (dkp + 4) + 128L * dkp + 10L * 32) * 4 > S1TcCfg<128>::SMEM - 2048))
     return set_error(PKV_ERR_ARGUMENT, "narrow pass: fused fresh split needs m <= 128");
   if (!a.q3_ready) {
     launch_k(s1_qprep_kernel, dim3(RB * 128, a.Hkv), 64, 0, st, a.q, a.m, a.H, a.G, a.R, RB, dkp,

@@ -33,7 +33,8 @@ t0 = t[t > 0].min()
 rel = np.where(t > 0, (t - t0) / 1e3, np.nan)
 names = ["softmax saw S", "softmax P done", "mma saw K/V", "mma issued PV", "tma issued", "markers"]
 n = int(np.sum(t[0] > 0))
-print(f"tiles traced: {n}; markers (prologue done, softmax loop done, partials written): {rel[5, :3].round(2)}")
+print(f"tiles traced: {n}; markers (prologue done, softmax loop done, partials written): {rel[5, :3].round(2)}; "
+      f"fresh-key CTA start / staged / end: {rel[5, [4, 6, 5]].round(2)}")
 for j in range(n):
     print(f"j={j:2d} " + "  ".join(f"{names[e][:14]:>14s} {rel[e, j]:7.2f}" for e in range(5)))
 d = np.diff(rel[0, :n])
