@@ -38,6 +38,8 @@ struct AttnArgs {
   long pool_tokens;
   float scale_log2;          // log2(e) / sqrt(head_dim)
   unsigned long long* trace; // debug (PKV_ATTN_TRACE=1): %globaltimer per page of CTA 0, see below
+  unsigned long long* cta_trace;  // debug (PKV_ATTN_CTA_TRACE=1): per CTA {start, end, smid, pages}
+  int* ticket;                    // attn_ps_kernel: next work unit (zeroed before the launch)
 };
 
 // trace[ev * 64 + j] for page j < 64 of blockIdx.x == 0 (tools/attn_trace.py):
@@ -184,6 +186,15 @@ __global__ void __launch_bounds__(576, 1)
   // last valid token of the pair decides how many KV pages the CTA walks
   const int last_tok = min((2 * lead_pair + 2) * a.T, a.n_q) - 1;
   const int n_kv_tiles = a.pos[last_tok] / 128 + 1;
+  if (a.cta_trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    uint32_t sm;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.cta_trace[blockIdx.x * 4 + 0] = t;
+    a.cta_trace[blockIdx.x * 4 + 2] = sm;
+    a.cta_trace[blockIdx.x * 4 + 3] = (unsigned long long)n_kv_tiles;
+  }
 
   if (warp == 16) {
     // ------------------------------------------------------------ TMA producer
@@ -456,6 +467,11 @@ __global__ void __launch_bounds__(576, 1)
     tc_fence_before();
   }
   __syncthreads();
+  if (a.cta_trace != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.cta_trace[blockIdx.x * 4 + 1] = t;
+  }
   if constexpr (PAIR) cluster_sync();  // no TMEM use or remote arrive left in either CTA
   if (warp == 17) {
     tc_fence_after();
@@ -1296,6 +1312,338 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// Persistent form of attn_row_kernel (PKV_ATTN_PERSIST=1): one CTA per SM walks its share of
+// the work units (KV head, pair of 32-token blocks) -- zigzag over the LPT-ordered list --
+// instead of one CTA per unit.  The per-CTA timeline (tools/attn_cta_trace.py) had put
+// ~11.5 us of fixed cost on every unit (barrier init, TMEM alloc, Q tiles, the first K/V
+// pages, the output) plus ~3.7 us between consecutive CTAs of an SM; persistent, the K/V
+// ring keeps streaming across units (the next unit's first pages arrive while this one
+// drains) and only the Q load and the output remain per unit.  Barrier phases run on
+// the CTA-global page count (every tile walks every page of its unit).
+// Units are handed out dynamically in LPT order (a global ticket, as the hardware scheduler
+// does for one CTA per unit): the producer warp takes the next ticket when it reaches the
+// unit and publishes it through a 4-slot ring in shared memory to the MMA and softmax warps.
+constexpr int ATTN_PS_RING = 4;
+
+template <int POLY>
+__global__ void __launch_bounds__(320, 1)
+    attn_ps_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
+  constexpr int DKP = 128;
+  using Cfg = AttnCfg<DKP>;
+  constexpr int NST = Cfg::STAGES, KVB = Cfg::KV_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + 2 * Cfg::Q_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + NST * 2 * KVB);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = bars + NST;
+  uint64_t* s_full = bars + 2 * NST;  // [2] per tile
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* pv_full = p_full + 2;     // [2]
+  uint64_t* q_full = pv_full + 2;
+  uint64_t* u_full = q_full + 1;              // [RING] unit ticket published
+  uint64_t* u_empty = u_full + ATTN_PS_RING;  // [RING] read by the MMA warp and the 8 softmax warps
+  int* u_ids = reinterpret_cast<int*>(u_empty + ATTN_PS_RING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u_ids + ATTN_PS_RING);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_units = a.n_pairs * a.Hkv;
+  // the k-th unit of this CTA (consumers: wait for the producer's ticket, release the slot)
+  auto take_unit = [&](int k) -> int {
+    const int slot = k % ATTN_PS_RING;
+    mbar_wait(&u_full[slot], (uint32_t)(k / ATTN_PS_RING) & 1);
+    const int u = *reinterpret_cast<volatile int*>(&u_ids[slot]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&u_empty[slot]);
+    return u;
+  };
+  const int per_group = a.hg * a.n_pairs;
+  auto unit_of = [&](int u, int& g, int& pair, int& n_kv) {
+    const int grp = u / per_group, rem_ = u - grp * per_group;
+    g = grp * a.hg + rem_ % a.hg;
+    pair = a.n_pairs - 1 - rem_ / a.hg;
+    n_kv = a.pos[min((2 * pair + 2) * a.T, a.n_q) - 1] / 128 + 1;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_full[i], 1);
+    }
+    mbar_init(q_full, 8);
+    for (int i = 0; i < ATTN_PS_RING; ++i) {
+      mbar_init(&u_full[i], 1);
+      mbar_init(&u_empty[i], 9);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();
+  griddep_launch();
+
+  if (warp == 8) {
+    if (elect_one()) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      int jg = 0;  // pages loaded by this CTA so far
+      for (int k = 0;; ++k) {
+        const int slot = k % ATTN_PS_RING;
+        mbar_wait(&u_empty[slot], ((uint32_t)(k / ATTN_PS_RING) & 1) ^ 1);
+        const int u = atomicAdd(a.ticket, 1);
+        *reinterpret_cast<volatile int*>(&u_ids[slot]) = u;
+        mbar_arrive(&u_full[slot]);  // (release: the ticket is visible to the waiting warps)
+        if (u >= n_units) break;
+        int g, pair, n_kv;
+        unit_of(u, g, pair, n_kv);
+        const long head_row = a.kv_row0 + (long)g * a.pool_tokens;
+        for (int j = 0; j < n_kv; ++j, ++jg) {
+          const int st = jg % NST;
+          mbar_wait(&kv_empty[st], ((uint32_t)(jg / NST) & 1) ^ 1);
+          uint8_t* sk = sKV + st * 2 * KVB;
+          const int row = (int)(head_row + (long)a.page_table[j] * 128);
+          mbar_expect_tx(&kv_full[st], 2 * KVB);
+#pragma unroll
+          for (int at = 0; at < Cfg::ATOMS; ++at) {
+            tma_load_2d(sk + at * 16384, &tmK, &kv_full[st], at * 64, row);
+            tma_load_2d(sk + KVB + at * 16384, &tmV, &kv_full[st], at * 64, row);
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idesc_s = make_idesc_f16(128, 128);
+    constexpr uint32_t idesc_o = make_idesc_f16(128, DKP, /*b_mn_major=*/true);
+    const uint32_t q_addr = smem_u32(sQ);
+    auto issue_s = [&](int t, int jg) {
+      const uint32_t k_addr = smem_u32(sKV + (jg % NST) * 2 * KVB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < DKP / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_ss(tmem + t * 128, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                  sdesc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j, int jg) {
+      const uint32_t v_addr = smem_u32(sKV + (jg % NST) * 2 * KVB + KVB);
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_sw128(v_addr + kk * 16 * 128, 16384, 1024),
+                  idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&pv_full[t]);
+      }
+      __syncwarp();
+    };
+    int jg = 0;
+    for (int k = 0;; ++k) {
+      const int u = take_unit(k);
+      if (u >= n_units) break;
+      int g, pair, n_kv;
+      unit_of(u, g, pair, n_kv);
+      mbar_wait(q_full, (uint32_t)k & 1);  // both tiles' Q of this unit are in shared memory
+      tc_fence_after();
+      mbar_wait(&kv_full[jg % NST], (uint32_t)(jg / NST) & 1);
+      tc_fence_after();
+      issue_s(0, jg);
+      issue_s(1, jg);
+      for (int j = 0; j < n_kv; ++j, ++jg) {
+        const bool more = j + 1 < n_kv;
+        mbar_wait(&p_full[0], (uint32_t)jg & 1);
+        tc_fence_after();
+        issue_pv(0, j, jg);
+        if (more) {
+          mbar_wait(&kv_full[(jg + 1) % NST], (uint32_t)((jg + 1) / NST) & 1);
+          tc_fence_after();
+          issue_s(0, jg + 1);
+        }
+        mbar_wait(&p_full[1], (uint32_t)jg & 1);
+        tc_fence_after();
+        issue_pv(1, j, jg);
+        if (elect_one()) umma_commit(&kv_empty[jg % NST]);
+        __syncwarp();
+        if (more) issue_s(1, jg + 1);
+      }
+    }
+  } else {
+    const int t = warp >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lb = (uint32_t)((quarter * 32) << 16);
+    const uint32_t tS = tmem + t * 128, tO = tmem + 256 + t * 128;
+    const float sl2 = a.scale_log2;
+    const int hj = r / a.T, ti = r - hj * a.T;
+    int jg = 0;
+    for (int k = 0;; ++k) {
+      const int u = take_unit(k);
+      if (u >= n_units) break;
+      int g, pair, n_kv;
+      unit_of(u, g, pair, n_kv);
+      const int b = 2 * pair + t;
+      const bool has_tile = b < a.n_tiles;
+      const int tok = b * a.T + ti;
+      const bool valid = has_tile && hj < a.G && tok < a.n_q;
+      const int head = g * a.G + hj;
+      const int tile_last = min((b + 1) * a.T, a.n_q) - 1;
+      const int min_pos = has_tile ? a.pos[b * a.T] : 0x7fffffff;
+      const int my_pos = valid ? a.pos[tok] : (has_tile ? a.pos[tile_last] : 0x7fffffff);
+#pragma unroll 1
+      for (int h = 0; h < Cfg::ATOMS; ++h) {  // this row's Q -> smem (both 64-column atoms)
+        uint4 v[8];
+        const uint4* src = reinterpret_cast<const uint4*>(a.q + ((long)tok * a.H + head) * DKP) + h * 8;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = valid ? src[c] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(sQ + t * Cfg::Q_BYTES + h * 16384 + r * 128 + ((c ^ (r & 7)) * 16)) = v[c];
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(q_full);
+
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < n_kv; ++j, ++jg) {
+        mbar_wait(&s_full[t], (uint32_t)jg & 1);  // also implies PV_t(j-1) is complete
+        tc_fence_after();
+        const int key0 = j * 128;
+        float sv[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t w[32];
+          tmem_ld32(tS + lb + c * 32, w);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(w[i]);
+        }
+        if (key0 + 127 > min_pos) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) sv[i] = (key0 + i <= my_pos) ? sv[i] : -INFINITY;
+        }
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int i = 0; i < 128; i += 8)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) mx[q] = fmaxf(mx[q], fmaxf(sv[i + 2 * q], sv[i + 2 * q + 1]));
+        const float tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        const float m_new = fmaxf(m_run, tmax * sl2);
+        const bool grow = (m_new - m_run) > 8.0f;
+        const float m_use = grow ? m_new : m_run;
+        const uint64_t sl2x2 = f32x2(sl2, sl2), negm = f32x2(-m_use, -m_use);
+        uint64_t rsum2 = f32x2(0.f, 0.f), rsum2b = f32x2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint64_t x = ffma2(f32x2(sv[c * 32 + 2 * i], sv[c * 32 + 2 * i + 1]), sl2x2, negm);
+            float x0, x1;
+            f32x2_unpack(x, x0, x1);
+            float p0, p1;
+            constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+            if ((kPolyMask >> (i & 7)) & 1u) {
+              p0 = exp2_poly(x0);
+              p1 = exp2_poly(x1);
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            if (i & 1) rsum2b = fadd2(rsum2b, f32x2(p0, p1));
+            else rsum2 = fadd2(rsum2, f32x2(p0, p1));
+            pk[i] = pack_f16(p0, p1);
+          }
+          tmem_st16(tS + lb + c * 16, pk);
+        }
+        float rs0, rs1;
+        f32x2_unpack(fadd2(rsum2, rsum2b), rs0, rs1);
+        if (__any_sync(0xffffffffu, grow && j > 0)) {
+          const float alpha = (grow && j > 0) ? ex2(m_run - m_use) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < DKP / 32; ++c) {
+            uint32_t w[32];
+            tmem_ld32(tO + lb + c * 32, w);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(__uint_as_float(w[i]) * alpha);
+            tmem_st32(tO + lb + c * 32, w);
+          }
+        }
+        if (grow && j > 0) l_run *= ex2(m_run - m_use);
+        if (grow) m_run = m_use;
+        l_run += rs0 + rs1;
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+      }
+      mbar_wait(&pv_full[t], (uint32_t)(jg - 1) & 1);  // the unit's last PV of this tile
+      tc_fence_after();
+      const float inv_l = 1.f / l_run;
+#pragma unroll 1
+      for (int c = 0; c < DKP / 32; ++c) {
+        uint32_t w[32];
+        tmem_ld32(tO + lb + c * 32, w);
+        tmem_ld_wait();
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(a.out + ((long)tok * a.H + head) * DKP + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_f16(__uint_as_float(w[8 * i]) * inv_l, __uint_as_float(w[8 * i + 1]) * inv_l),
+                                pack_f16(__uint_as_float(w[8 * i + 2]) * inv_l, __uint_as_float(w[8 * i + 3]) * inv_l),
+                                pack_f16(__uint_as_float(w[8 * i + 4]) * inv_l, __uint_as_float(w[8 * i + 5]) * inv_l),
+                                pack_f16(__uint_as_float(w[8 * i + 6]) * inv_l, __uint_as_float(w[8 * i + 7]) * inv_l));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+static int launch_attn_ps(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream,
+                          int* ticket_ws) {
+  using Cfg = AttnCfg<128>;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(attn_ps_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+  });
+  if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn_ps smem attr: %s", cudaGetErrorString(err));
+  const int units = a.n_pairs * a.Hkv;
+  // the caller's workspace ticket (Stage II: one per repair, so concurrent in-process ranks do
+  // not share it); else one per process for the standalone entry point
+  static int* own = nullptr;
+  int* ticket = ticket_ws;
+  if (ticket == nullptr) {
+    if (own == nullptr && cudaMalloc(&own, sizeof(int)) != cudaSuccess)
+      return set_error(PKV_ERR_CUDA, "attn_ps: ticket allocation");
+    ticket = own;
+  }
+  cudaMemsetAsync(ticket, 0, sizeof(int), stream);
+  AttnArgs b = a;
+  b.ticket = ticket;
+  launch_k(attn_ps_kernel<1>, std::min(units, num_sms()), 320, Cfg::SMEM, stream, tk, tv, b);
+  PKV_LAUNCHED();
+  PKV_CHECK_LAUNCH("attn_ps_kernel");
+  return PKV_OK;
+}
+
 static int launch_attn_row(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream) {
   using Cfg = AttnCfg<128>;
   static std::once_flag once;
@@ -1355,11 +1703,12 @@ static int launch_attn_pair(const CUtensorMap& tk64, const CUtensorMap& tv, cons
 }
 
 static unsigned long long* g_attn_trace = nullptr;
+static unsigned long long* g_attn_cta_trace = nullptr;
 
 // q/out: [n_q][H][dkp] fp16; k_pool/v_pool: [L][Hkv][pool_tokens][dkp] fp16 (whole pool)
 int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H, int Hkv, int head_dim, int dkp,
                    const void* k_pool, const void* v_pool, long pool_rows_total, long pool_tokens, int layer,
-                   const int32_t* page_table, cudaStream_t stream) {
+                   const int32_t* page_table, cudaStream_t stream, int* ticket) {
   if (n_q <= 0) return PKV_OK;
   const int G = H / Hkv;
   if (G > 128) return set_error(PKV_ERR_CONFIG, "attention: group size %d > 128", G);
@@ -1385,6 +1734,14 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   a.pool_tokens = pool_tokens;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)head_dim));
   a.trace = nullptr;
+  a.cta_trace = nullptr;
+  {
+    static const bool ct = getenv("PKV_ATTN_CTA_TRACE") && getenv("PKV_ATTN_CTA_TRACE")[0] == '1';
+    if (ct && g_attn_cta_trace == nullptr &&
+        cudaMalloc(&g_attn_cta_trace, 16384 * 4 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(g_attn_cta_trace, 0, 16384 * 4 * sizeof(unsigned long long));
+    if (ct && (long)a.n_pairs * Hkv <= 16384) a.cta_trace = g_attn_cta_trace;
+  }
   {
     static const bool tr = getenv("PKV_ATTN_TRACE") && getenv("PKV_ATTN_TRACE")[0] == '1';
     static unsigned long long* buf = nullptr;
@@ -1421,6 +1778,10 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
       return set_error(PKV_ERR_CUDA, "attention: TMA encode failed");
     return launch_attn_pair<1>(tk64, tv, a, stream);
   }
+  // persistent, dynamically scheduled form by default (1.393 vs 1.410 ms per C3 layer,
+  // tools/bench_attn.py); PKV_ATTN_PERSIST=0 launches one CTA per unit
+  static const bool ps_env = !(getenv("PKV_ATTN_PERSIST") && getenv("PKV_ATTN_PERSIST")[0] == '0');
+  if (dkp == 128 && ps_env && poly == 1) return launch_attn_ps(tk, tv, a, stream, ticket);
   static const bool row_env = getenv("PKV_ATTN_ROW") && getenv("PKV_ATTN_ROW")[0] == '1';
   if (dkp == 128 && row_env && poly == 1) return launch_attn_row(tk, tv, a, stream);
   static const bool one_env = getenv("PKV_ATTN_ONE") && getenv("PKV_ATTN_ONE")[0] == '1';
@@ -1440,5 +1801,13 @@ extern "C" int pkv_debug_attn_trace(unsigned long long* host) {
   if (pkv::g_attn_trace == nullptr) return -1;
   cudaDeviceSynchronize();
   cudaMemcpy(host, pkv::g_attn_trace, 8 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
+
+extern "C" int pkv_debug_attn_cta_trace(unsigned long long* host, int n_ctas) {
+  if (pkv::g_attn_cta_trace == nullptr) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, pkv::g_attn_cta_trace, (size_t)std::min(n_ctas, 16384) * 4 * sizeof(unsigned long long),
+             cudaMemcpyDeviceToHost);
   return 0;
 }

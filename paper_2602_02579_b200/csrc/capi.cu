@@ -670,6 +670,7 @@ struct RcWs {
   int* sk_cnt;
   size_t sk_cnt_n;
   float* ssq;      // deferred RMSNorm: [k][ceil(Dp/256)] per-tile sums of h^2
+  int* ticket;     // work ticket of the persistent attention (attn_ps_kernel)
 };
 static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   Carver cv{reinterpret_cast<uint8_t*>(base), 0, 0};
@@ -680,6 +681,7 @@ static RcWs carve_rc(const pkv_model* md, int k, void* base, size_t* total) {
   w.ab = cv.take<__half>((size_t)k * md->HQ);
   w.act = cv.take<__half>((size_t)k * md->Fp);
   w.ssq = cv.take<float>((size_t)k * ceil_div(md->Dp, 256));
+  w.ticket = cv.take<int>(1);
   const size_t skf = std::max(std::max(gemm_sk_ws_floats(k, md->NQKV, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->HQ)),
                               std::max(gemm_sk_ws_floats(k, 2 * md->Fp, md->Dp), gemm_sk_ws_floats(k, md->Dp, md->Fp)));
   if (skf > 0) {
@@ -896,7 +898,7 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     const int r0 = (last && !need_final_h) ? k : 0, nr = n - r0;
     TTRY(T_RC_ATTN, attn_tc_launch(w.qb + (long)r0 * md->HQ, w.ab + (long)r0 * md->HQ, pos + r0, nr, H, Hkv, dk, dkp,
                                    c->k_pool, c->v_pool, (long)cf.n_layers * Hkv * c->pool_tokens, c->pool_tokens, l,
-                                   c->page_table, st));
+                                   c->page_table, st, w.ticket));
     GemmArgs go{};
     go.f16 = 1;
     go.nonfinite = c->nonfinite;

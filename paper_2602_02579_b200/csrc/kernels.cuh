@@ -137,6 +137,6 @@ int fuse_layers_launch(const float* per_layer, int L, int s, float* fused, cudaS
 int topk_launch(const float* v, int n, int k, int32_t* out, int32_t* status, cudaStream_t st);
 int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H, int Hkv, int head_dim, int dkp,
                    const void* k_pool, const void* v_pool, long pool_rows_total, long pool_tokens, int layer,
-                   const int32_t* page_table, cudaStream_t stream);
+                   const int32_t* page_table, cudaStream_t stream, int* ticket = nullptr);
 
 }  // namespace pkv

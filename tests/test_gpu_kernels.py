@@ -281,7 +281,7 @@ def test_opt_in_variants():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PKV_ASM_TMA="1", PKV_GEMM_RASTER="2", PKV_ATTN_ONE="1")
+    env = dict(os.environ, PKV_ASM_TMA="1", PKV_GEMM_RASTER="2", PKV_ATTN_ONE="1", PKV_ATTN_PERSIST="0")
     tests = ["tests/test_gpu_kernels.py::test_assembly_is_fp16_of_reference_keys",
              "tests/test_gpu_kernels.py::test_sparse_attention_matches_fp32_reference",
              "tests/test_gpu_kernels.py::test_gemm_matches_fp32_reference",
@@ -289,7 +289,14 @@ def test_opt_in_variants():
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider", *tests], cwd=root,
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    # one thread per Q-tile row (PKV_ATTN_ROW=1)
+    # one thread per Q-tile row, one CTA per unit (PKV_ATTN_PERSIST=0 PKV_ATTN_ROW=1), and the
+    # round-1 two-tile kernel with 8 softmax warps per tile (PKV_ATTN_PERSIST=0)
+    for extra in ({"PKV_ATTN_PERSIST": "0", "PKV_ATTN_ROW": "1"}, {"PKV_ATTN_PERSIST": "0"}):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                            "tests/test_gpu_kernels.py::test_sparse_attention_matches_fp32_reference"], cwd=root,
+                           env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     env = dict(os.environ, PKV_ATTN_ROW="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         "tests/test_gpu_kernels.py::test_sparse_attention_matches_fp32_reference"], cwd=root,
