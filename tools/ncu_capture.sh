@@ -13,7 +13,7 @@ cap() {  # name, name-base, regex, skip
     python tools/profile_step.py > $OUT/ncu_${TAG}_$1.log 2>&1
   echo "$1 rc=$?" >> $OUT/ncu_${TAG}.status
 }
-cap rc_attn function '^attn_tc_kernel$' 16
+cap rc_attn function '^attn_ps_kernel$' 16
 cap rc_gate_up demangled 'gemm_tc_kernel<\(int\)256, \(int\)3,' 16
 cap rc_down demangled 'gemm_tc_kernel<\(int\)256, \(int\)2,' 33
 cap rc_o demangled 'gemm_tc_kernel<\(int\)256, \(int\)2,' 32
