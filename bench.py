@@ -15,10 +15,10 @@ Multi-GPU (one process per GPU; `--gpus N` starts torchrun itself when WORLD_SIZ
             the N GPUs (tensor parallel, paper_2602_02579_b200.tp): per-layer NCCL sums of
             the per-token score partials before the global top-k and of the o/down
             projection outputs; value = s / TTFT (strong scaling)
-  tokens    one 32k request: every GPU holds the full model and cache and scores the whole
-            request (replicated), Stage II repairs each GPU's share of the selected rows
-            and all-gathers the fresh cache entries per layer (DeviceModel.rows); value =
-            s / TTFT (strong scaling)
+  tokens    one 32k request: every GPU holds the full model and cache; the scoring pass is
+            head-sharded over each GPU's head slice (per-layer score all-reduce), Stage II
+            repairs each GPU's share of the selected rows and all-gathers the fresh cache
+            entries per layer (DeviceModel.rows); value = s / TTFT (strong scaling)
   requests  (configs[4]-style) one independent request per GPU, no data-path
             collective; value = N * s / TTFT (weak scaling)
 
@@ -208,7 +208,7 @@ def arm_config(args, cfgd, world, heads, tokens=False):
             "s": s, "chunks": cfgd["n_chunks"], "chunk_len": cfgd["chunk_len"], "m": args.m, "p": args.p,
             "k": math.ceil(args.p * s),
             "parallelism": (f"tp{world} (KV-head sharded, NCCL)" if heads else
-                            f"tokens{world} (scoring replicated, Stage II token-parallel, NCCL all-gather)"
+                            f"tokens{world} (scoring KV-head sharded, Stage II token-parallel, NCCL)"
                             if tokens else f"request-dp{world}"),
             "inputs": f"SYN1 seed 0 (weights, chunk store, query: paper_2602_02579_b200/synthetic.py)"
             if args.chunks == "synthetic" else "SYN1 weights; chunk K/V precomputed on the GPU",
@@ -427,12 +427,14 @@ def main():
         full = P.DeviceModel.synthetic(cfg, seed=0)
         chunks = make_chunks(full, 0)
         dm = full.rows(comm)
+        # the scoring pass head-sharded over this rank's head slice of the full cache
+        stage1_dm = full.shard(rank, world, comm.handle)
         qseed = 0
     else:
         dm = P.DeviceModel.synthetic(cfg, seed=0)
         chunks = make_chunks(dm, rank)  # request r of the batch: chunk store / query seed r
         qseed = rank
-    pipe = PrefillPipeline(dm, chunks, args.m, args.p)
+    pipe = PrefillPipeline(dm, chunks, args.m, args.p, stage1_dm=stage1_dm if tokens else None)
     query = S.query(cfg, args.m, qseed)
     pipe.set_query(query)
     stream = torch.cuda.current_stream()

@@ -127,6 +127,11 @@ typedef struct pkv_cache {
   int32_t* nonfinite;        /* nullable device int32: OR-ed with 1 when a Stage-II epilogue writes a
                                 non-finite (or fp16-overflowing) value; the host raises NumericsError
                                 (reference check_finite, tensor.py:31-34) */
+  int32_t pool_heads;        /* 0, or the KV heads of the pools' layout when this cache is a head slice
+                                of a larger cache (narrow passes only): layer stride pool_heads, this
+                                view's heads start at head0 (token-parallel Stage II with a head-sharded
+                                scoring pass, DeviceModel.rows + shard) */
+  int32_t head0;
 } pkv_cache;
 
 /* reference list[ChunkKV] in prompt order, chunkstore.py:37-49 */

@@ -49,7 +49,8 @@ class Cache(ctypes.Structure):
     _fields_ = [("k_pool", c_vp), ("v_pool", c_vp), ("pool_tokens", c_i64), ("page_table", c_vp), ("s", c_i32),
                 ("token_ids", c_vp), ("rope_cos", c_vp), ("rope_sin", c_vp), ("rope_len", c_i32), ("recomputed", c_vp),
                 ("k2_pool", c_vp), ("layer_ready", ctypes.POINTER(c_vp)),
-                ("rope_cs32", c_vp), ("layer_done", ctypes.POINTER(c_vp)), ("nonfinite", c_vp)]
+                ("rope_cs32", c_vp), ("layer_done", ctypes.POINTER(c_vp)), ("nonfinite", c_vp),
+                ("pool_heads", c_i32), ("head0", c_i32)]
 
 
 class Chunks(ctypes.Structure):

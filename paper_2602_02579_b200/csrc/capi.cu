@@ -513,7 +513,13 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     if ((rc = (x)) != 0) return rc; \
   } while (0)
   TTRY(T_QP_MISC, embed_gather_launch(md->w.embed, Dp, query_ids, nullptr, m, cf.hidden_dim, w.h, Dp, st));
-  const long layer_pool = (long)Hkv * c->pool_tokens * dkp;
+  // a head-slice view of a larger cache (pool_heads > 0): layer stride over all its heads,
+  // this view's heads from head0
+  const int HP = c->pool_heads > 0 ? c->pool_heads : Hkv, h0 = c->pool_heads > 0 ? c->head0 : 0;
+  if (h0 < 0 || h0 + Hkv > HP) return set_error(PKV_ERR_ARGUMENT, "head slice [%d, %d) of %d heads", h0, h0 + Hkv, HP);
+  if (c->pool_heads > 0 && (flags & (PKV_QP_PROBE | PKV_QP_ROWS)))
+    return set_error(PKV_ERR_ARGUMENT, "probe / row capture passes need the whole cache");
+  const long layer_pool = (long)HP * c->pool_tokens * dkp, head_off = (long)h0 * c->pool_tokens * dkp;
   // m <= 32: producers write the bf16 planes of the next GEMM input directly and the
   // projection epilogue reduces planes + split-K partials itself (one launch each)
   const bool fused = m <= 32;
@@ -526,11 +532,11 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
                                    ldx, nullptr, st));
     if (fused) TTRY(T_QP_PROJ, proj_fused(lw.wqkv, lw.wscale[0], md->NQKV, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
     else TTRY(T_QP_PROJ, proj_f32(lw.wqkv, lw.wscale[0], md->NQKV, Dp, w.x, Dp, m, w.qkv, md->NQKV, 0, w.proj, st));
-    __half* kp = reinterpret_cast<__half*>(c->k_pool) + l * layer_pool;
-    __half* vp = reinterpret_cast<__half*>(c->v_pool) + l * layer_pool;
+    __half* kp = reinterpret_cast<__half*>(c->k_pool) + l * layer_pool + head_off;
+    __half* vp = reinterpret_cast<__half*>(c->v_pool) + l * layer_pool + head_off;
     const bool append = (flags & PKV_QP_APPEND_KV) != 0;
     const bool planes = c->k2_pool != nullptr;
-    __half* k2p = planes ? reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool : nullptr;
+    __half* k2p = planes ? reinterpret_cast<__half*>(c->k2_pool) + l * layer_pool + head_off : nullptr;
     // the tensor-core attention's Q planes straight from the RoPE kernel when no row block
     // needs zero padding
     const bool q3_fused = planes && w.tc_splits > 0 && (m * G) % 128 == 0 && !(flags & PKV_QP_PROBE);
@@ -568,7 +574,9 @@ int pkv_query_pass(const pkv_model* md, const pkv_cache* c, const pkv_chunks* ch
     a.k1_all = c->k_pool;
     a.k2_all = c->k2_pool;
     a.v_all = c->v_pool;
-    a.pool_rows_total = (long)cf.n_layers * Hkv * c->pool_tokens;
+    a.pool_rows_total = (long)cf.n_layers * HP * c->pool_tokens;
+    a.pool_heads = HP;
+    a.head0 = h0;
     a.scale = (float)(1.0 / std::sqrt((double)dk));
     a.src_chunks = (flags & PKV_QP_FROM_CHUNKS) ? 1 : 0;
     a.recomp = c->recomputed;

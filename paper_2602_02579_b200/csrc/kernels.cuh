@@ -56,6 +56,7 @@ struct S1Attn {
   long pool_tokens;
   const int32_t* page_table;
   int layer;
+  int pool_heads, head0;  // the pools' head layout (a head-slice view of a larger cache)
   const float* fk;
   const float* fv;
   float* S;

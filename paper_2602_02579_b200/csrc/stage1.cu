@@ -1062,7 +1062,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     t.scale = a.scale;
     t.q3 = a.q3;
     t.q3_ready = a.q3_ready;
-    t.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
+    t.kv_row0 = ((long)a.layer * a.pool_heads + a.head0) * a.pool_tokens;
     t.pool_tokens = a.pool_tokens;
     t.page_table = a.page_table;
     t.S = pass2 ? nullptr : a.S;
@@ -1150,7 +1150,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
     sa.keys_per_split = a.sc_keys_per_split;
     sa.n_splits = a.sc_splits;
     sa.scale = a.scale;
-    sa.kv_row0 = (long)a.layer * a.Hkv * a.pool_tokens;
+    sa.kv_row0 = ((long)a.layer * a.pool_heads + a.head0) * a.pool_tokens;
     sa.pool_tokens = a.pool_tokens;
     sa.page_table = a.page_table;
     sa.Mfin = Mfin;

@@ -32,9 +32,13 @@ def _created_events(n: int) -> list:
 
 
 class PrefillPipeline:
-    def __init__(self, dm: DeviceModel, chunks: list, m: int, p: float):
+    def __init__(self, dm: DeviceModel, chunks: list, m: int, p: float, stage1_dm: DeviceModel | None = None):
+        """stage1_dm: the scoring pass on a head-sharded model (DeviceModel.shard) over its
+        head slice of this pipeline's full cache, with Stage II token-parallel on dm
+        (DeviceModel.rows) -- both multi-GPU splits at once (include/pkv.h pool_heads)."""
         torch = _lib.require_cuda()
         self.dm = dm
+        self.s1_dm = stage1_dm if stage1_dm is not None else dm
         cfg = dm.config
         self.cfg = cfg
         self.cache = AssembledCache(dm.cache_config, chunks, track_access=False, fp32_taps=False)
@@ -46,7 +50,7 @@ class PrefillPipeline:
         lib = _lib.load()
         self.flags_score = _lib.PKV_QP_SCORES | _lib.PKV_QP_FROM_CHUNKS
         self.flags_final = _lib.PKV_QP_LOGITS | _lib.PKV_QP_APPEND_KV | _lib.PKV_QP_FROM_CHUNKS
-        qp_bytes = max(lib.pkv_query_pass_workspace(dm.handle, s, m, self.flags_score),
+        qp_bytes = max(lib.pkv_query_pass_workspace(self.s1_dm.handle, s, m, self.flags_score),
                        lib.pkv_query_pass_workspace(dm.handle, s, m, self.flags_final))
         self.ws_qp = torch.empty(qp_bytes, dtype=torch.uint8, device=dev)
         # finalize fused into Stage II (pkv_recompute_query): the query rows ride along the
@@ -158,7 +162,14 @@ class PrefillPipeline:
             _lib.check(lib.pkv_assemble(ctypes_ref(c._cfg_c), ch, cc, self.side.cuda_stream))
             for ev in self.layer_events:
                 ev.record(self.side)
-        _lib.check(lib.pkv_query_pass(self.dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_score,
+        if self.s1_dm is not self.dm:  # this rank's head slice of the full cache
+            w = self.s1_dm.tp_world
+            hl = self.cfg.n_kv_heads // w
+            sc = _lib.Cache.from_buffer_copy(c.c_cache)
+            sc.pool_heads, sc.head0 = self.cfg.n_kv_heads, self.s1_dm.tp_rank * hl
+            self._c_slice = sc
+            cc = ctypes_ref(sc)
+        _lib.check(lib.pkv_query_pass(self.s1_dm.handle, cc, ch, self.query.data_ptr(), self.m, self.flags_score,
                                       self.per_layer.data_ptr(), None, None, None, self.ws_qp.data_ptr(),
                                       self.ws_qp.numel(), st))
         _lib.check(lib.pkv_fuse_select(self.per_layer.data_ptr(), self.cfg.n_layers, self.s, self.k,

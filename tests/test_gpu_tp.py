@@ -210,3 +210,49 @@ def test_token_parallel_without_query_rows(built, monkeypatch):
         assert torch.equal(pipe.logits, one.logits)
     for c in comms:
         c.close()
+
+
+@pytest.mark.parametrize("case,world", [("llama_width", 2), ("llama_width", 4)])
+def test_sharded_scoring_with_token_parallel_stage2(built, case, world):
+    """Both multi-GPU splits at once (bench --mode tokens): the scoring pass head-sharded over
+    each rank's head slice of its full cache (pkv_cache.pool_heads / head0, per-layer score
+    all-reduce), Stage II token-parallel on the full model.  Every rank selects what the
+    unsharded run selects and ends with its repaired cache and logits bit for bit."""
+    import torch
+
+    import paper_2602_02579_b200 as P
+    from paper_2602_02579_b200 import tp
+    cfg_o, seed, units, query, p = _materialise(case)
+    w, chunks = _setup(cfg_o, seed, units, query)
+    cfg = P.ModelConfig(**cfg_o.json())
+    mw = P.ModelWeights(embed=w.embed, layers=[P.LayerWeights(**{n: getattr(lw, n) for n in (
+        "attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")}) for lw in w.layers],
+        final_norm=w.final_norm, lm_head=w.lm_head)
+    dm = P.DeviceModel.from_host(mw, cfg)
+    fp = mw.fingerprint(cfg)
+    dch = [P.ChunkKV(c.chunk_id, fp, c.token_ids, c.k_nr, c.v) for c in chunks]
+    one = _run(P, dm, dch, query, p)
+    one.step()
+    torch.cuda.synchronize()
+    comms = tp.local_group(world)
+    from paper_2602_02579_b200.pipeline import PrefillPipeline
+    pipes = []
+    for c in comms:
+        pipe = PrefillPipeline(dm.rows(c), dch, len(query), p, stage1_dm=dm.shard(c.rank, world, c.handle))
+        pipe.set_query(query)
+        pipes.append(pipe)
+    torch.cuda.synchronize()
+    tp.run_ranks([pipe.step for pipe in pipes])
+    torch.cuda.synchronize()
+    s, k = one.s, one.k
+    rel = float(((pipes[0].per_layer - one.per_layer).abs() / one.per_layer.abs().clamp_min(1e-30)).max())
+    assert rel <= REL_TOL, rel
+    for r, pipe in enumerate(pipes):
+        assert torch.equal(pipe.per_layer, pipes[0].per_layer), r
+        assert torch.equal(pipe.idx[:k], one.idx[:k]), r
+        for name in ("k_pool", "v_pool", "k2_pool"):
+            assert torch.equal(getattr(pipe.cache, name)[:, :, :s], getattr(one.cache, name)[:, :, :s]), (r, name)
+        assert torch.equal(pipe.logits, one.logits), r
+    _report(case=f"{case}_hybrid{world}", s=s, k=k, per_layer_rel_vs_unsharded=rel, bit_identical_stage2=True)
+    for c in comms:
+        c.close()
