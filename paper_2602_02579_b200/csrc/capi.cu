@@ -876,12 +876,23 @@ static int recompute_core(const pkv_model* md, const pkv_cache* c, const int32_t
     // K/V of every selected token are in the cache before this layer's attention.  The last
     // layer of a repair only scatters K/V (its attention / o / MLP are dead, below): skip
     // the query rows of wqkv.
-    if (last && !need_final_h && m == 0) {
+    if (last && !need_final_h) {
+      GemmArgs gq = g;  // (the query rows' own QKV, below)
+      g.M = k;
       g.N = 2 * Hkv * dkp;
       g.head0 = H;
       TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp,
                                     reinterpret_cast<const __half*>(lw.wqkv) + (long)H * dkp * Dp, Dp, Dp, g,
                                     st));
+      if (m > 0) {  // the query rows need their q as well: the full wqkv for those m rows only
+        gq.M = m;
+        gq.pos = pos + k;
+        gq.C = w.qb + (long)k * md->HQ;
+        gq.tap_k = gq.tap_v = nullptr;
+        gq.tap_rows = 0;
+        gq.kvc = nullptr;  // (replicated on every rank: not exchanged)
+        TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb + (long)k * Dp, Dp, lw.wqkv, Dp, Dp, gq, st));
+      }
     } else {
       TTRY(T_RC_QKV, gemm_tc_launch(EPI_QKV, 256, w.xb, Dp, lw.wqkv, Dp, Dp, g, st));
     }
