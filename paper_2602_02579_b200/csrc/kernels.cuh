@@ -115,6 +115,7 @@ struct S1ScoreArgs {
   const float* Mfin;      // [Hkv][R]
   const float* W;         // [Hkv][R] row weights
   float* part;            // [RB][Hkv][s] per-row-block column sums
+  unsigned long long* trace;  // debug (PKV_S1_TRACE=1): CTA (0,0,0) start, Q in TMEM, S(j) seen, end
 };
 int s1_score_tc_launch(const S1ScoreArgs& a, const void* k1, const void* k2, long pool_rows_total, int dkp,
                        cudaStream_t st);

@@ -679,6 +679,11 @@ __global__ void __launch_bounds__(320, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.y, split = blockIdx.x, rb = blockIdx.z;
+  if (a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[0] = t;
+  }
   const int k_begin = split * a.keys_per_split;
   const int k_end = min(k_begin + a.keys_per_split, a.s);
   const int n_tiles = (k_end - k_begin + C::KT - 1) / C::KT;
@@ -782,10 +787,21 @@ __global__ void __launch_bounds__(320, 1)
     const float wr = valid ? a.W[(long)g * a.R + row] : 0.f;
     const float c1 = (a.scale * (1.f / S1_QSCALE)) * LOG2E;
     float* out = a.part + ((long)rb * a.Hkv + g) * a.s;
+    const bool tr = a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && warp == 0 &&
+                    lane == 0;
+    auto stamp = [&](int i) {
+      if (tr && i < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[i] = t;
+      }
+    };
+    stamp(1);
     for (int j = 0; j < n_tiles; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (uint32_t)(j >> 1) & 1);
       tc_fence_after();
+      stamp(4 + j);
       uint32_t u0[32], u1[32];
       tmem_ld32(tmem + lb + C::T_S + b * C::KT + hc * 64, u0);
       tmem_ld32(tmem + lb + C::T_S + b * C::KT + hc * 64 + 32, u1);
@@ -820,6 +836,7 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
+    stamp(2);
     tc_fence_before();
   }
   __syncthreads();
@@ -829,9 +846,18 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-int s1_score_tc_launch(const S1ScoreArgs& a, const void* k1, const void* k2, long pool_rows_total, int dkp,
+static unsigned long long* g_s1s_trace = nullptr;
+
+int s1_score_tc_launch(const S1ScoreArgs& a_in, const void* k1, const void* k2, long pool_rows_total, int dkp,
                        cudaStream_t st) {
+  S1ScoreArgs a = a_in;
   if (a.n_splits <= 0) return PKV_OK;
+  {
+    static const bool tr = getenv("PKV_S1_TRACE") && getenv("PKV_S1_TRACE")[0] == '1';
+    if (tr && g_s1s_trace == nullptr && cudaMalloc(&g_s1s_trace, 64 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(g_s1s_trace, 0, 64 * sizeof(unsigned long long));
+    a.trace = tr ? g_s1s_trace : nullptr;
+  }
   if (a.keys_per_split % 128 != 0) return set_error(PKV_ERR_ARGUMENT, "score pass: split not page-aligned");
   const int RB = ceil_div(a.R, 128);
   dim3 grid(a.n_splits, a.Hkv, RB);
@@ -864,5 +890,12 @@ extern "C" int pkv_debug_s1_trace(unsigned long long* host) {
   if (pkv::g_s1_trace == nullptr) return -1;
   cudaDeviceSynchronize();
   cudaMemcpy(host, pkv::g_s1_trace, 6 * 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return 0;
+}
+
+extern "C" int pkv_debug_s1_score_trace(unsigned long long* host) {
+  if (pkv::g_s1s_trace == nullptr) return -1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, pkv::g_s1s_trace, 64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return 0;
 }

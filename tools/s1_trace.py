@@ -40,3 +40,14 @@ for j in range(n):
 d = np.diff(rel[0, :n])
 print(f"softmax period median {np.nanmedian(d):.3f} us; P(j) - S(j) median {np.nanmedian(rel[1, :n] - rel[0, :n]):.3f} us; "
       f"S(j+1) - P(j) median {np.nanmedian(rel[0, 1:n] - rel[1, :n - 1]):.3f} us")
+
+# scoring pass 2 (s1_score_tc_kernel), CTA (0,0,0): start, Q planes in TMEM, S(j) seen, done
+sb = np.zeros(64, dtype=np.uint64)
+lib.pkv_debug_s1_score_trace.argtypes = [ctypes.c_void_p]
+if lib.pkv_debug_s1_score_trace(sb.ctypes.data_as(ctypes.c_void_p)) == 0 and sb[0] > 0:
+    t = sb.astype(np.int64)
+    rel2 = np.where(t > 0, (t - t[0]) / 1e3, np.nan)
+    nt = int(np.sum(t[4:] > 0))
+    d2 = np.diff(rel2[4:4 + nt])
+    print(f"score pass 2: Q in TMEM {rel2[1]:.2f} us, tiles {nt}, first S {rel2[4]:.2f}, done {rel2[2]:.2f}, "
+          f"tile period median {np.nanmedian(d2):.3f} us")
