@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(576, 1)
           float x0, x1;
           f32x2_unpack(x, x0, x1);
           float p0, p1;
-          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : POLY == 1 ? 0x80u : 0u;
           if constexpr (POLY < 0) {
             // two exponentials per MUFU op (ex2.approx.f16x2): the argument is rounded to
             // f16 (|x| < 1: 2^-11 relative; larger |x| only for P < 2^-4) and P is rounded
@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(832, 1)
         float x0, x1;
         f32x2_unpack(x, x0, x1);
         float p0, p1;
-        constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+        constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : POLY == 1 ? 0x80u : 0u;
         if ((kPolyMask >> (i & 7)) & 1u) {
           p0 = exp2_poly(x0);
           p1 = exp2_poly(x1);
@@ -970,7 +970,7 @@ __global__ void __launch_bounds__(320, 1)
           float x0, x1;
           f32x2_unpack(x, x0, x1);
           float p0, p1;
-          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : POLY == 1 ? 0x80u : 0u;
           if ((kPolyMask >> (i & 7)) & 1u) {
             p0 = exp2_poly(x0);
             p1 = exp2_poly(x1);
@@ -1249,7 +1249,7 @@ __global__ void __launch_bounds__(320, 1)
           float x0, x1;
           f32x2_unpack(x, x0, x1);
           float p0, p1;
-          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+          constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : POLY == 1 ? 0x80u : 0u;
           if ((kPolyMask >> (i & 7)) & 1u) {
             p0 = exp2_poly(x0);
             p1 = exp2_poly(x1);
@@ -1551,7 +1551,7 @@ __global__ void __launch_bounds__(320, 1)
             float x0, x1;
             f32x2_unpack(x, x0, x1);
             float p0, p1;
-            constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : 0x80u;
+            constexpr uint32_t kPolyMask = POLY >= 4 ? 0xAAu : POLY == 3 ? 0x94u : POLY == 2 ? 0x88u : POLY == 1 ? 0x80u : 0u;
             if ((kPolyMask >> (i & 7)) & 1u) {
               p0 = exp2_poly(x0);
               p1 = exp2_poly(x1);
@@ -1616,13 +1616,14 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+template <int POLY>
 static int launch_attn_ps(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream,
                           int* ticket_ws) {
   using Cfg = AttnCfg<128>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(attn_ps_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    err = cudaFuncSetAttribute(attn_ps_kernel<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn_ps smem attr: %s", cudaGetErrorString(err));
   const int units = a.n_pairs * a.Hkv;
@@ -1638,7 +1639,7 @@ static int launch_attn_ps(const CUtensorMap& tk, const CUtensorMap& tv, const At
   cudaMemsetAsync(ticket, 0, sizeof(int), stream);
   AttnArgs b = a;
   b.ticket = ticket;
-  launch_k(attn_ps_kernel<1>, std::min(units, num_sms()), 320, Cfg::SMEM, stream, tk, tv, b);
+  launch_k(attn_ps_kernel<POLY>, std::min(units, num_sms()), 320, Cfg::SMEM, stream, tk, tv, b);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_ps_kernel");
   return PKV_OK;
@@ -1781,7 +1782,10 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   // persistent, dynamically scheduled form by default (1.393 vs 1.410 ms per C3 layer,
   // tools/bench_attn.py); PKV_ATTN_PERSIST=0 launches one CTA per unit
   static const bool ps_env = !(getenv("PKV_ATTN_PERSIST") && getenv("PKV_ATTN_PERSIST")[0] == '0');
-  if (dkp == 128 && ps_env && poly == 1) return launch_attn_ps(tk, tv, a, stream, ticket);
+  if (dkp == 128 && ps_env && poly == 0) return launch_attn_ps<0>(tk, tv, a, stream, ticket);
+  if (dkp == 128 && ps_env && poly == 1) return launch_attn_ps<1>(tk, tv, a, stream, ticket);
+  if (dkp == 128 && ps_env && poly == 2) return launch_attn_ps<2>(tk, tv, a, stream, ticket);
+  if (dkp == 128 && ps_env && poly == 3) return launch_attn_ps<3>(tk, tv, a, stream, ticket);
   static const bool row_env = getenv("PKV_ATTN_ROW") && getenv("PKV_ATTN_ROW")[0] == '1';
   if (dkp == 128 && row_env && poly == 1) return launch_attn_row(tk, tv, a, stream);
   static const bool one_env = getenv("PKV_ATTN_ONE") && getenv("PKV_ATTN_ONE")[0] == '1';
