@@ -9,6 +9,7 @@ as fp32-faithful narrow passes.
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -91,19 +92,22 @@ class SelectionResult:
     _dev_idx: object = field(default=None, repr=False, compare=False)
 
 
-_WS: dict = {}
+_WS = threading.local()
 
 
 def workspace(nbytes: int, tag: str = "ws"):
-    """Grow-only device scratch per (device, tag, host thread): the ranks of an in-process
-    group (tp.run_ranks) are threads sharing one device and must not share scratch."""
-    import threading
+    """Grow-only device scratch per (host thread, device, tag): the ranks of an in-process
+    group (tp.run_ranks) are threads sharing one device and must not share scratch. Kept in
+    thread-local storage so a rank thread's buffers are released when the thread ends."""
     torch = _lib.require_cuda()
-    key = (torch.cuda.current_device(), tag, threading.get_ident())
-    buf = _WS.get(key)
+    bufs = getattr(_WS, "bufs", None)
+    if bufs is None:
+        bufs = _WS.bufs = {}
+    key = (torch.cuda.current_device(), tag)
+    buf = bufs.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device="cuda")
-        _WS[key] = buf
+        bufs[key] = buf
     return buf
 
 
