@@ -1325,7 +1325,7 @@ __global__ void __launch_bounds__(320, 1)
 // unit and publishes it through a 4-slot ring in shared memory to the MMA and softmax warps.
 constexpr int ATTN_PS_RING = 4;
 
-template <int POLY>
+template <int POLY, int SPLIT>
 __global__ void __launch_bounds__(320, 1)
     attn_ps_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, AttnArgs a) {
   constexpr int DKP = 128;
@@ -1344,7 +1344,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* q_full = pv_full + 2;
   uint64_t* u_full = q_full + 1;              // [RING] unit ticket published
   uint64_t* u_empty = u_full + ATTN_PS_RING;  // [RING] read by the MMA warp and the 8 softmax warps
-  int* u_ids = reinterpret_cast<int*>(u_empty + ATTN_PS_RING);
+  uint64_t* s_free = u_empty + ATTN_PS_RING;  // [2] SPLIT: the tile's S(j) is in the softmax's registers
+  int* u_ids = reinterpret_cast<int*>(s_free + 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u_ids + ATTN_PS_RING);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1375,6 +1376,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_full[i], 1);
+      mbar_init(&s_free[i], 4);
     }
     mbar_init(q_full, 8);
     for (int i = 0; i < ATTN_PS_RING; ++i) {
@@ -1437,6 +1439,21 @@ __global__ void __launch_bounds__(320, 1)
       }
       __syncwarp();
     };
+    // keys [64 half, +64) of page jg -> S columns [64 half, +64); commits s_full when last
+    auto issue_s_half = [&](int t, int jg, int half, bool last) {
+      constexpr uint32_t idesc_h = make_idesc_f16(128, 64);
+      const uint32_t k_addr = smem_u32(sKV + (jg % NST) * 2 * KVB) + half * 8192;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < DKP / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_ss(tmem + t * 128 + half * 64, sdesc_sw128(q_addr + t * Cfg::Q_BYTES + off, 16, 1024),
+                  sdesc_sw128(k_addr + off, 16, 1024), idesc_h, kk > 0 ? 1u : 0u);
+        }
+        if (last) umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
     auto issue_pv = [&](int t, int j, int jg) {
       const uint32_t v_addr = smem_u32(sKV + (jg % NST) * 2 * KVB + KVB);
       if (elect_one()) {
@@ -1460,6 +1477,31 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_after();
       issue_s(0, jg);
       issue_s(1, jg);
+      if constexpr (SPLIT) {
+        // P(j) occupies S columns [0, 64) only: keys [64, 128) of S(j+1) go into columns
+        // [64, 128) as soon as the softmax holds S(j) in registers, so after P(j) only PV(j)
+        // and the other half of S(j+1) stand between two softmax passes of a tile
+        for (int j = 0; j < n_kv; ++j, ++jg) {
+          const bool more = j + 1 < n_kv;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(&s_free[t], (uint32_t)jg & 1);
+            if (more) {
+              if (t == 0) mbar_wait(&kv_full[(jg + 1) % NST], (uint32_t)((jg + 1) / NST) & 1);
+              tc_fence_after();
+              issue_s_half(t, jg + 1, 1, false);
+            }
+            mbar_wait(&p_full[t], (uint32_t)jg & 1);
+            tc_fence_after();
+            issue_pv(t, j, jg);
+            if (t == 1) {
+              if (elect_one()) umma_commit(&kv_empty[jg % NST]);
+              __syncwarp();
+            }
+            if (more) issue_s_half(t, jg + 1, 0, true);
+          }
+        }
+      } else {
       for (int j = 0; j < n_kv; ++j, ++jg) {
         const bool more = j + 1 < n_kv;
         mbar_wait(&p_full[0], (uint32_t)jg & 1);
@@ -1476,6 +1518,7 @@ __global__ void __launch_bounds__(320, 1)
         if (elect_one()) umma_commit(&kv_empty[jg % NST]);
         __syncwarp();
         if (more) issue_s(1, jg + 1);
+      }
       }
     }
   } else {
@@ -1526,6 +1569,11 @@ __global__ void __launch_bounds__(320, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(w[i]);
+        }
+        if constexpr (SPLIT) {  // S(j) is in registers: columns [64, 128) may take S(j+1)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[t]);
         }
         if (key0 + 127 > min_pos) {
 #pragma unroll
@@ -1616,14 +1664,14 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-template <int POLY>
+template <int POLY, int SPLIT = 0>
 static int launch_attn_ps(const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a, cudaStream_t stream,
                           int* ticket_ws) {
   using Cfg = AttnCfg<128>;
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(attn_ps_kernel<POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    err = cudaFuncSetAttribute(attn_ps_kernel<POLY, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
   });
   if (err != cudaSuccess) return set_error(PKV_ERR_CUDA, "attn_ps smem attr: %s", cudaGetErrorString(err));
   const int units = a.n_pairs * a.Hkv;
@@ -1639,7 +1687,7 @@ static int launch_attn_ps(const CUtensorMap& tk, const CUtensorMap& tv, const At
   cudaMemsetAsync(ticket, 0, sizeof(int), stream);
   AttnArgs b = a;
   b.ticket = ticket;
-  launch_k(attn_ps_kernel<POLY>, std::min(units, num_sms()), 320, Cfg::SMEM, stream, tk, tv, b);
+  launch_k(attn_ps_kernel<POLY, SPLIT>, std::min(units, num_sms()), 320, Cfg::SMEM, stream, tk, tv, b);
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("attn_ps_kernel");
   return PKV_OK;
@@ -1782,6 +1830,9 @@ int attn_tc_launch(const void* q, void* out, const int32_t* pos, int n_q, int H,
   // persistent, dynamically scheduled form by default (1.393 vs 1.410 ms per C3 layer,
   // tools/bench_attn.py); PKV_ATTN_PERSIST=0 launches one CTA per unit
   static const bool ps_env = !(getenv("PKV_ATTN_PERSIST") && getenv("PKV_ATTN_PERSIST")[0] == '0');
+  // S(j+1) issued in two key halves, one of them during the softmax of page j
+  static const bool split_env = getenv("PKV_ATTN_SPLIT_S") && getenv("PKV_ATTN_SPLIT_S")[0] == '1';
+  if (dkp == 128 && ps_env && split_env && poly == 1) return launch_attn_ps<1, 1>(tk, tv, a, stream, ticket);
   if (dkp == 128 && ps_env && poly == 0) return launch_attn_ps<0>(tk, tv, a, stream, ticket);
   if (dkp == 128 && ps_env && poly == 1) return launch_attn_ps<1>(tk, tv, a, stream, ticket);
   if (dkp == 128 && ps_env && poly == 2) return launch_attn_ps<2>(tk, tv, a, stream, ticket);

@@ -291,7 +291,9 @@ def test_opt_in_variants():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     # one thread per Q-tile row, one CTA per unit (PKV_ATTN_PERSIST=0 PKV_ATTN_ROW=1), and the
     # round-1 two-tile kernel with 8 softmax warps per tile (PKV_ATTN_PERSIST=0)
-    for extra in ({"PKV_ATTN_PERSIST": "0", "PKV_ATTN_ROW": "1"}, {"PKV_ATTN_PERSIST": "0"}):
+    # and the persistent kernel with S(j+1) in two key halves (PKV_ATTN_SPLIT_S=1)
+    for extra in ({"PKV_ATTN_PERSIST": "0", "PKV_ATTN_ROW": "1"}, {"PKV_ATTN_PERSIST": "0"},
+                  {"PKV_ATTN_SPLIT_S": "1"}):
         env = dict(os.environ, **extra)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                             "tests/test_gpu_kernels.py::test_sparse_attention_matches_fp32_reference"], cwd=root,
