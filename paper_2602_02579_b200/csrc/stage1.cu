@@ -681,7 +681,8 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
                                 int R, int m, int G, int H, int dkp, float* out, float* Mfin, float* Lfin,
                                 __half* x3, long ldx, int n_ctx, float* Cfin) {
   pdl_entry();
-  extern __shared__ float wsp[];  // [splits] rescale weight of each split
+  extern __shared__ float wsp[];  // [splits rounded up to 8] rescale weight of each split (0 past splits:
+                                  // the unrolled loop below reads it in 16-byte vectors)
   __shared__ float sM, sL, sC;
   const int r = blockIdx.x, g = blockIdx.y;
   if (threadIdx.x < 32) {
@@ -696,6 +697,7 @@ __global__ void s1_attn_combine(const float* Opart, const float* Mpart, const fl
       L += Lpart[b] * w;
       if (sp < n_ctx) Lc += Lpart[b] * w;
     }
+    for (int sp = splits + threadIdx.x; sp < ((splits + 7) & ~7); sp += 32) wsp[sp] = 0.f;
     for (int o = 16; o > 0; o >>= 1) {
       L += __shfl_xor_sync(0xffffffffu, L, o);
       Lc += __shfl_xor_sync(0xffffffffu, Lc, o);
@@ -1129,7 +1131,7 @@ int s1_attention_launch(const S1Attn& a_in, float* attn_out, float* Mfin, float*
   PKV_LAUNCHED();
   PKV_CHECK_LAUNCH("s1_attn_pass1");
   }
-  launch_k(s1_attn_combine, dim3(a.R, a.Hkv), 128, total_splits * sizeof(float), st, a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
+  launch_k(s1_attn_combine, dim3(a.R, a.Hkv), 128, ((total_splits + 7) & ~7) * sizeof(float), st, a.Opart, a.Mpart, a.Lpart, total_splits, a.Hkv, a.R, a.m, a.G, a.H,
                                                     a.dkp, attn_out, Mfin, Lfin,
                                                     reinterpret_cast<__half*>(a.x3_out), a.x3_ld, a.tc_splits,
                                                     (pass2 && renorm) ? a.sc_c : (float*)nullptr);

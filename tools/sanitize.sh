@@ -1,0 +1,9 @@
+# compute-sanitizer over smoke() (one small prefill through every default kernel) and the
+# kernel unit tests.  synccheck is not run: it flags mbarrier phases that complete without a
+# waiter (pv_full / kv_empty by design: the consumers wait on later phases, ordered by s_full).
+mkdir -p gpurun_out
+CS="/usr/local/cuda/bin/compute-sanitizer --print-limit 20"
+SMOKE='import __graft_entry__ as g; g.smoke(); print("smoke ok")'
+timeout 1200 $CS --tool memcheck python -c "$SMOKE" > gpurun_out/sanitize_memcheck.txt 2>&1; echo "memcheck rc=$?" >> gpurun_out/sanitize_memcheck.txt
+timeout 1200 $CS --tool racecheck python -c "$SMOKE" > gpurun_out/sanitize_racecheck.txt 2>&1; echo "racecheck rc=$?" >> gpurun_out/sanitize_racecheck.txt
+timeout 1800 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_kernels.py -k "not opt_in" > gpurun_out/sanitize_kernels.txt 2>&1; echo "kernels memcheck rc=$?" >> gpurun_out/sanitize_kernels.txt
