@@ -7,3 +7,7 @@ SMOKE='import __graft_entry__ as g; g.smoke(); print("smoke ok")'
 timeout 1200 $CS --tool memcheck python -c "$SMOKE" > gpurun_out/sanitize_memcheck.txt 2>&1; echo "memcheck rc=$?" >> gpurun_out/sanitize_memcheck.txt
 timeout 1200 $CS --tool racecheck python -c "$SMOKE" > gpurun_out/sanitize_racecheck.txt 2>&1; echo "racecheck rc=$?" >> gpurun_out/sanitize_racecheck.txt
 timeout 1800 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_kernels.py -k "not opt_in" > gpurun_out/sanitize_kernels.txt 2>&1; echo "kernels memcheck rc=$?" >> gpurun_out/sanitize_kernels.txt
+# head dim 128 (the default persistent attention, the tcgen05 narrow pass, CTA-pair GEMMs) at
+# Llama width, the fused finalize, and the sharded / token-parallel paths
+timeout 2400 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "llama_width or mistral_width" > gpurun_out/sanitize_parity128.txt 2>&1; echo "parity128 memcheck rc=$?" >> gpurun_out/sanitize_parity128.txt
+timeout 2400 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_tp.py > gpurun_out/sanitize_tp.txt 2>&1; echo "tp memcheck rc=$?" >> gpurun_out/sanitize_tp.txt
