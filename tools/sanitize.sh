@@ -11,3 +11,5 @@ timeout 1800 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/t
 # Llama width, the fused finalize, and the sharded / token-parallel paths
 timeout 2400 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "llama_width or mistral_width" > gpurun_out/sanitize_parity128.txt 2>&1; echo "parity128 memcheck rc=$?" >> gpurun_out/sanitize_parity128.txt
 timeout 2400 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_tp.py > gpurun_out/sanitize_tp.txt 2>&1; echo "tp memcheck rc=$?" >> gpurun_out/sanitize_tp.txt
+timeout 2400 $CS --tool racecheck python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "prophet_slice and llama_width" > gpurun_out/sanitize_race128.txt 2>&1; echo "race128 rc=$?" >> gpurun_out/sanitize_race128.txt
+timeout 1200 $CS --tool initcheck python -c "$SMOKE" > gpurun_out/sanitize_initcheck.txt 2>&1; echo "initcheck rc=$?" >> gpurun_out/sanitize_initcheck.txt
