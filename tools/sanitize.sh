@@ -13,3 +13,6 @@ timeout 2400 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/t
 timeout 2400 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/test_gpu_tp.py > gpurun_out/sanitize_tp.txt 2>&1; echo "tp memcheck rc=$?" >> gpurun_out/sanitize_tp.txt
 timeout 2400 $CS --tool racecheck python -m pytest -q -p no:cacheprovider tests/test_gpu_parity.py -k "prophet_slice and llama_width" > gpurun_out/sanitize_race128.txt 2>&1; echo "race128 rc=$?" >> gpurun_out/sanitize_race128.txt
 timeout 1200 $CS --tool initcheck python -c "$SMOKE" > gpurun_out/sanitize_initcheck.txt 2>&1; echo "initcheck rc=$?" >> gpurun_out/sanitize_initcheck.txt
+for t in test_gpu_api test_gpu_decode test_gpu_prefill test_gpu_chunkfile test_gpu_acceptance; do
+  timeout 1500 $CS --tool memcheck python -m pytest -q -p no:cacheprovider tests/$t.py > gpurun_out/sanitize_$t.txt 2>&1; echo "$t rc=$?" >> gpurun_out/sanitize_$t.txt
+done
